@@ -1,0 +1,162 @@
+/* laxol_b200 — C-ABI of the B200-native Lax-Oleinik min-plus hot path.
+ *
+ * The reference (`laxol`, /root/reference/proj) is a C++20 library with no
+ * C-ABI or FFI of its own.  Its stepping API is the drop-in surface:
+ *   kinetic_convolve(u, kernel, eta, ConvEngine, blocks*)   proj/include/laxol/scheme.hpp:52-53
+ *   step_fully_discrete(u, t, spec, params, kernel, engine)  proj/include/laxol/scheme.hpp:57-59
+ *   evolve(u0, t0, steps, spec, params, options)             proj/include/laxol/scheme.hpp:82-90
+ *   split_step_nd(u, t, SplitSpec, params)                   proj/include/laxol/splitting.hpp:40-41
+ * The engine switch those calls go through (proj/src/scheme.cpp:114-121) is
+ * where the entry points below plug in.  The C++ mirror
+ * of that API lives in paper_1210_4090_b200/csrc/host/laxol_b200.hpp.
+ *
+ * Conventions
+ *  - A "line" is one 1-D periodic problem of n samples: the FUNDAMENTAL
+ *    domain, no duplicated seam (the host GridFn keeps n+1 samples,
+ *    proj/include/laxol/grid_fn.hpp:8-12).  Lines are stored row-major,
+ *    lines x n doubles, in device memory owned by the caller.
+ *  - The kernel window of line l is ktab[l*ktab_stride + w], w = 0..2n, the
+ *    table build_kernel produces (proj/src/scheme.cpp:77-81), with grid
+ *    displacement d = first[l] + w (first = center_index - n).
+ *    ktab_stride 0 = one table shared by all lines.
+ *  - tv is tau*V already rounded on the host (the product of
+ *    proj/src/scheme.cpp:161); the device applies out = best - tv[j] with one
+ *    rounding, never an FMA.  tv_stride 0 = shared across lines; tv NULL = V == 0.
+ *  - Every entry point is asynchronous on `stream` (a cudaStream_t, NULL =
+ *    legacy default) unless its name ends in _host.
+ *  - Status codes map back to the reference's exception types
+ *    (proj/include/laxol/errors.hpp:8-17): LOB_INVALID_INPUT -> InvalidInput,
+ *    LOB_EVALUATION_ERROR -> EvaluationError.  lob_last_error(ctx) explains.
+ *  - There is no CPU fallback: without a CUDA device every compute entry
+ *    point returns LOB_CUDA_ERROR.
+ */
+#ifndef LAXOL_B200_H
+#define LAXOL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LOB_OK 0
+#define LOB_INVALID_INPUT 1
+#define LOB_EVALUATION_ERROR 2
+#define LOB_CUDA_ERROR 3
+
+/* Engines: ConvEngine{Fast, Naive} (proj/include/laxol/scheme.hpp:13) gains
+ * two device engines. */
+#define LOB_ENGINE_DIRECT 0 /* K1: exact O(n^2) min-plus, bit-identical to ConvEngine::Naive */
+#define LOB_ENGINE_FAST 1   /* K2: exact O(n) local-minimum walk (mechanical kinetics) */
+
+typedef struct lob_ctx lob_ctx;
+
+/* Context: one per host thread; owns scratch and cached tables. */
+int lob_ctx_create(int device, lob_ctx** out);
+int lob_ctx_destroy(lob_ctx* ctx);
+const char* lob_last_error(const lob_ctx* ctx);
+const char* lob_version(void);
+
+/* K1 — direct min-plus, fp64, fused potential epilogue.
+ * Replaces conv_naive (proj/src/minplus.cpp:116-126) + periodic aliasing
+ * (proj/src/scheme.cpp:125-134) + potential loop (proj/src/scheme.cpp:156-162):
+ *   out[l][j] = min_{w=0..2n} (u[l][(j - first[l] - w) mod n] + ktab_l[w]) - tv_l[j]
+ * first: device array of `lines` int64. */
+int lob_minplus_direct_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
+                           const double* ktab, int64_t ktab_stride, const int64_t* first,
+                           const double* tv, int64_t tv_stride, void* stream);
+
+/* K1 — fp32 variant (no potential; the reference has no fp32 path). */
+int lob_minplus_direct_f32(lob_ctx* ctx, const float* u, float* out, int64_t lines, int64_t n,
+                           const float* ktab, int64_t ktab_stride, const int64_t* first,
+                           void* stream);
+
+/* K1 on windowed (non-periodic) lines of m samples (proj/src/scheme.cpp:135-144):
+ *   out[l][j] = min over w with 0 <= j-first-w < m of u[l][j-first-w] + ktab_l[w]
+ * Returns LOB_EVALUATION_ERROR when an output has no candidate
+ * (j - first outside the convolution, proj/src/scheme.cpp:138-141). */
+int lob_minplus_window_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t m,
+                           int64_t n, const double* ktab, int64_t ktab_stride,
+                           const int64_t* first, const double* tv, int64_t tv_stride,
+                           void* stream);
+
+/* K2 — fast exact min-plus for mechanical kinetics K*(v) = v^2/2 - drift*v.
+ * Replaces conv_fast (proj/src/minplus.cpp:219-252) in kinetic_convolve.
+ * The kernel window is evaluated on the device with the exact IEEE operation
+ * sequence of build_kernel (proj/src/scheme.cpp:79-80,
+ * proj/src/hamiltonian.cpp:43), so values are bit-identical to the table.
+ * drift: device array of `lines` doubles; n_space = n; tau > 0.
+ * blocks (nullable, device int64[lines]) receives decompose(u, eta)'s block
+ * count of the INPUT u (what StepStats.block_count reports).
+ * The workspace carries per-tile statistics of u between consecutive calls:
+ * pass LOB_FAST_STATS_VALID when `u` is the `out` of the previous call with
+ * the same workspace (the device-resident evolve loop), else 0 and the
+ * statistics are recomputed (one extra read of u). */
+#define LOB_FAST_STATS_VALID 1
+int lob_fast_workspace_bytes(int64_t lines, int64_t n, size_t* bytes);
+int lob_minplus_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
+                         const double* drift, double tau, const double* tv, int64_t tv_stride,
+                         double eta, int64_t* blocks, void* workspace, size_t workspace_bytes,
+                         int flags, void* stream);
+
+/* K3 — split_step_nd (proj/src/splitting.cpp:37-99) for a periodic n x n
+ * row-major tensor: sweep axis 0 (columns, kernel 1), sweep axis 1 (rows,
+ * kernel 2), then subtract tau*V once.  The potential is the separable
+ * descriptor V(t,x1,x2) = a1[i]*a2[k] + b  (each product and sum one IEEE
+ * rounding, as the C++ expression a1*a2 + b), i.e. the reference's
+ * PotentialNd callback evaluated on the host per axis and per step;
+ * a1 == NULL means V == 0.  tmp: device scratch of n*n doubles.
+ * engine LOB_ENGINE_DIRECT or LOB_ENGINE_FAST (fast needs workspace of
+ * lob_fast_workspace_bytes(n, n)). */
+int lob_split_step_2d_f64(lob_ctx* ctx, const double* u, double* out, double* tmp, int64_t n,
+                          double tau, double drift1, double drift2, const double* a1,
+                          const double* a2, double b, int engine, void* workspace,
+                          size_t workspace_bytes, void* stream);
+
+/* Device-resident batched evolve (proj/src/scheme.cpp:208-272): `steps`
+ * steps of `lines` periodic lines with a shared, time-independent tv.  u is
+ * updated in place (double-buffered against `scratch`, n*lines doubles).
+ * Per-step drift (mean of u_next - u, fp64, device reduction) and block
+ * counts are written to step_drift[steps*lines] / step_blocks[steps*lines]
+ * (device, nullable).  Returns LOB_EVALUATION_ERROR (after finishing the
+ * step) if a non-finite value appears; *completed_steps receives the number
+ * of steps done. */
+int lob_evolve_f64(lob_ctx* ctx, double* u, double* scratch, int64_t lines, int64_t n,
+                   const double* drift, double tau, const double* tv, int64_t tv_stride,
+                   double eta, int engine, int64_t steps, double* step_drift,
+                   int64_t* step_blocks, int64_t* completed_steps, void* workspace,
+                   size_t workspace_bytes, void* stream);
+
+/* Host-buffer entry point (the e2e path): one step of `lines` lines whose u,
+ * out, drift and tv live in host memory (pinned or pageable).  Copies in,
+ * runs K1/K2 on the context's stream, copies out, synchronizes. */
+int lob_step_host_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
+                      const double* drift, double tau, const double* tv, int64_t tv_stride,
+                      double eta, int engine, int64_t* blocks);
+
+/* Kernel window of mechanical(drift) built on the device (for checking
+ * against build_kernel): window[2n+1], first, argmin, and the
+ * fast path's slope-estimate tolerance delta (in displacement units). */
+int lob_kernel_mech_host(lob_ctx* ctx, int64_t n, double tau, double drift, double* window,
+                         int64_t* first, int64_t* argmin, double* delta);
+
+/* Decomposition block counts of device lines (decompose, proj/src/minplus.cpp:152-188,
+ * on the closed period; capped counts are not supported: eta must be 0 or the
+ * uncapped count is returned). blocks: device int64[lines]. */
+int lob_block_counts(lob_ctx* ctx, const double* u, int64_t lines, int64_t n, double eta,
+                     int64_t* blocks, void* stream);
+
+/* Micro-benchmarks of the FP64 pipe on this device: the sustained rate of
+ * the min-plus candidate instruction mix (DADD + DSETP + 2 FSEL) and of a
+ * pure DADD stream, in operations per second (FP64 lane-ops). */
+int lob_bench_fp64(lob_ctx* ctx, double* minplus_cand_per_s, double* dadd_ops_per_s,
+                   double* sm_clock_ghz);
+
+/* Number of kernel launches issued by this context since creation. */
+int64_t lob_launch_count(const lob_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LAXOL_B200_H */

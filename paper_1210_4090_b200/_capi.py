@@ -1,0 +1,110 @@
+"""ctypes binding of the laxol_b200 C-ABI (include/laxol_b200.h).
+
+The product path is the in-tree CUDA library ``lib/liblaxol_b200.so``.  There
+is no CPU fallback: if the library cannot be loaded, or no CUDA device is
+present, every compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int64, c_size_t, c_uint64, c_void_p
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "liblaxol_b200.so")
+
+LOB_OK = 0
+LOB_INVALID_INPUT = 1
+LOB_EVALUATION_ERROR = 2
+LOB_CUDA_ERROR = 3
+
+ENGINE_DIRECT = 0
+ENGINE_FAST = 1
+FAST_STATS_VALID = 1
+
+# name -> (restype, argtypes); every symbol declared in include/laxol_b200.h
+# and include/laxol_b200_configs.h.
+_P = c_void_p
+SIGNATURES = {
+    "lob_ctx_create": (c_int, [c_int, POINTER(c_void_p)]),
+    "lob_ctx_destroy": (c_int, [_P]),
+    "lob_last_error": (c_char_p, [_P]),
+    "lob_version": (c_char_p, []),
+    "lob_minplus_direct_f64": (c_int, [_P, _P, _P, c_int64, c_int64, _P, c_int64, _P, _P, c_int64, _P]),
+    "lob_minplus_direct_f32": (c_int, [_P, _P, _P, c_int64, c_int64, _P, c_int64, _P, _P]),
+    "lob_minplus_window_f64": (c_int, [_P, _P, _P, c_int64, c_int64, c_int64, _P, c_int64, _P, _P, c_int64, _P]),
+    "lob_fast_workspace_bytes": (c_int, [c_int64, c_int64, POINTER(c_size_t)]),
+    "lob_minplus_fast_f64": (c_int, [_P, _P, _P, c_int64, c_int64, _P, c_double, _P, c_int64, c_double,
+                                     _P, _P, c_size_t, c_int, _P]),
+    "lob_split_step_2d_f64": (c_int, [_P, _P, _P, _P, c_int64, c_double, c_double, c_double, _P, _P,
+                                      c_double, c_int, _P, c_size_t, _P]),
+    "lob_evolve_f64": (c_int, [_P, _P, _P, c_int64, c_int64, _P, c_double, _P, c_int64, c_double, c_int,
+                               c_int64, _P, _P, POINTER(c_int64), _P, c_size_t, _P]),
+    "lob_step_host_f64": (c_int, [_P, _P, _P, c_int64, c_int64, _P, c_double, _P, c_int64, c_double, c_int, _P]),
+    "lob_kernel_mech_host": (c_int, [_P, c_int64, c_double, c_double, _P, POINTER(c_int64), POINTER(c_int64),
+                                     POINTER(c_double)]),
+    "lob_block_counts": (c_int, [_P, _P, c_int64, c_int64, c_double, _P, _P]),
+    "lob_bench_fp64": (c_int, [_P, POINTER(c_double), POINTER(c_double), POINTER(c_double)]),
+    "lob_launch_count": (c_int64, [_P]),
+    # synthetic workloads (include/laxol_b200_configs.h)
+    "lob_gen_sin": (None, [c_int64, _P]),
+    "lob_gen_cos": (None, [c_int64, _P]),
+    "lob_gen_potential": (None, [c_int, c_int64, _P]),
+    "lob_gen_c2_drifts": (None, [c_int64, _P]),
+    "lob_gen_c3_lines": (None, [c_int64, c_int64, c_int64, c_uint64, _P]),
+    "lob_gen_c4_u0": (None, [c_int64, _P]),
+    "lob_c4_time_term": (c_double, [c_double]),
+    "lob_gen_c5_lines": (None, [c_int64, c_int64, c_int64, c_uint64, _P, c_int]),
+}
+
+_lib = None
+
+
+class LaxolError(RuntimeError):
+    """Base error; subclasses mirror the reference's exception types."""
+
+
+class InvalidInput(LaxolError):
+    """proj/include/laxol/errors.hpp:9-11"""
+
+
+class EvaluationError(LaxolError):
+    """proj/include/laxol/errors.hpp:15-17"""
+
+
+class CudaError(LaxolError):
+    pass
+
+
+def load(path: str = LIB_PATH, required_symbols=None):
+    """Load the CUDA library; raises OSError if it was not built."""
+    global _lib
+    if _lib is not None and path == LIB_PATH:
+        return _lib
+    if not os.path.exists(path):
+        raise OSError(f"laxol_b200 CUDA library not built: {path} (run __graft_entry__.build())")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        if required_symbols is not None and name not in required_symbols:
+            continue
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path == LIB_PATH:
+        _lib = lib
+    return lib
+
+
+def check(status: int, ctx=None, where: str = ""):
+    if status == LOB_OK:
+        return
+    msg = ""
+    if ctx is not None:
+        raw = load().lob_last_error(ctx)
+        msg = raw.decode() if raw else ""
+    text = f"{where}: {msg}" if where else msg
+    if status == LOB_INVALID_INPUT:
+        raise InvalidInput(text)
+    if status == LOB_EVALUATION_ERROR:
+        raise EvaluationError(text)
+    raise CudaError(text or "CUDA error / no device")

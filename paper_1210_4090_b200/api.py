@@ -1,0 +1,277 @@
+"""Python mirror of the reference's stepping API over the laxol_b200 C-ABI.
+
+Names and argument meaning follow the reference (`laxol`, /root/reference/proj):
+``build_kernel`` (proj/src/scheme.cpp:59-105), ``kinetic_convolve``
+(proj/src/scheme.cpp:107-146), ``step_fully_discrete`` (:148-164),
+``evolve`` (:208-272) and ``split_step_nd`` (proj/src/splitting.cpp:37-99).
+Lines are numpy arrays (host) or torch CUDA tensors (device-resident);
+every compute call runs on the B200 through ``lib/liblaxol_b200.so``.
+Errors raise the mirrors of the reference's exceptions (InvalidInput,
+EvaluationError).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+from ._capi import (ENGINE_DIRECT, ENGINE_FAST, FAST_STATS_VALID, EvaluationError,  # noqa: F401
+                    InvalidInput, check)
+
+
+def _ptr(x) -> int | None:
+    """Raw data pointer of a numpy array or torch tensor (None passes NULL)."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        if not x.flags["C_CONTIGUOUS"]:
+            raise InvalidInput("array must be C-contiguous")
+        return x.ctypes.data
+    if not x.is_contiguous():
+        raise InvalidInput("tensor must be contiguous")
+    return x.data_ptr()
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        import torch
+
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+@dataclass
+class Kernel:
+    """Sampled kinetic cost (proj/include/laxol/scheme.hpp:34-42): window of
+    2n+1 samples at grid displacements first..first+2n."""
+
+    window: np.ndarray
+    first: int
+    argmin_index: int
+    center_index: int
+    n_space: int
+    tau: float
+    drift: float
+    delta: float = 0.0  # fast-path slope-estimate tolerance (displacement units)
+
+
+@dataclass
+class SchemeParams:
+    """proj/include/laxol/scheme.hpp:17-26"""
+
+    n_space: int
+    tau: float
+    eta: float = 0.0
+    h0: float = 1.0
+    arrival: bool = True  # PotentialSampling::Arrival (V at t + tau)
+
+    @property
+    def epsilon(self) -> float:
+        return 1.0 / float(self.n_space)
+
+
+def validate(params: SchemeParams) -> None:
+    """proj/src/scheme.cpp:39-53 (AntiCflMode::Fail)."""
+    if params.n_space < 1:
+        raise InvalidInput("SchemeParams: n_space must be >= 1")
+    if not params.tau > 0.0:
+        raise InvalidInput("SchemeParams: tau must be positive")
+    if params.eta < 0.0:
+        raise InvalidInput("SchemeParams: eta must be >= 0")
+    if not params.h0 > 0.0:
+        raise InvalidInput("SchemeParams: h0 must be positive")
+    if params.epsilon / params.tau >= params.h0:
+        raise InvalidInput("SchemeParams: epsilon/tau violates the bound epsilon/tau < h0")
+
+
+class Device:
+    """One laxol_b200 context (lob_ctx) on one CUDA device."""
+
+    def __init__(self, device: int = 0):
+        self.lib = _capi.load()
+        h = ctypes.c_void_p()
+        st = self.lib.lob_ctx_create(int(device), ctypes.byref(h))
+        if st != 0:
+            raise _capi.CudaError(f"lob_ctx_create(device={device}) failed with status {st} "
+                                  "(no CUDA device? there is no CPU fallback)")
+        self.ctx = h
+        self.device = device
+
+    def close(self):
+        if self.ctx:
+            self.lib.lob_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st, where):
+        check(st, self.ctx, where)
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.lob_launch_count(self.ctx))
+
+    # ---- kernels -----------------------------------------------------------
+    def build_kernel(self, n_space: int, tau: float, drift: float) -> Kernel:
+        """Host build_kernel for mechanical(drift) (proj/src/scheme.cpp:59-105)."""
+        validate(SchemeParams(n_space, tau))
+        win = np.empty(2 * n_space + 1, dtype=np.float64)
+        first = ctypes.c_int64()
+        arg = ctypes.c_int64()
+        delta = ctypes.c_double()
+        st = self.lib.lob_kernel_mech_host(self.ctx, n_space, tau, drift, win.ctypes.data,
+                                           ctypes.byref(first), ctypes.byref(arg), ctypes.byref(delta))
+        self._check(st, "build_kernel")
+        return Kernel(win, int(first.value), int(arg.value), int(first.value) + n_space, n_space,
+                      tau, drift, float(delta.value))
+
+    def direct_f64(self, u, out, ktab, first, tv=None, ktab_stride=0, tv_stride=0, stream=None):
+        lines, n = u.shape
+        st = self.lib.lob_minplus_direct_f64(self.ctx, _ptr(u), _ptr(out), lines, n, _ptr(ktab),
+                                             ktab_stride, _ptr(first), _ptr(tv), tv_stride,
+                                             _stream_ptr(stream))
+        self._check(st, "lob_minplus_direct_f64")
+
+    def direct_f32(self, u, out, ktab, first, ktab_stride=0, stream=None):
+        lines, n = u.shape
+        st = self.lib.lob_minplus_direct_f32(self.ctx, _ptr(u), _ptr(out), lines, n, _ptr(ktab),
+                                             ktab_stride, _ptr(first), _stream_ptr(stream))
+        self._check(st, "lob_minplus_direct_f32")
+
+    def window_f64(self, u, out, n_space, ktab, first, tv=None, ktab_stride=0, tv_stride=0,
+                   stream=None):
+        lines, m = u.shape
+        st = self.lib.lob_minplus_window_f64(self.ctx, _ptr(u), _ptr(out), lines, m, n_space,
+                                             _ptr(ktab), ktab_stride, _ptr(first), _ptr(tv),
+                                             tv_stride, _stream_ptr(stream))
+        self._check(st, "lob_minplus_window_f64")
+
+    def fast_workspace_bytes(self, lines: int, n: int) -> int:
+        b = ctypes.c_size_t()
+        st = self.lib.lob_fast_workspace_bytes(lines, n, ctypes.byref(b))
+        self._check(st, "lob_fast_workspace_bytes")
+        return int(b.value)
+
+    def fast_f64(self, u, out, drift, tau, tv=None, tv_stride=0, eta=0.0, blocks=None,
+                 workspace=None, flags=0, stream=None):
+        lines, n = u.shape
+        ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+        st = self.lib.lob_minplus_fast_f64(self.ctx, _ptr(u), _ptr(out), lines, n, _ptr(drift),
+                                           float(tau), _ptr(tv), tv_stride, float(eta), _ptr(blocks),
+                                           _ptr(workspace), ws_bytes, int(flags), _stream_ptr(stream))
+        self._check(st, "lob_minplus_fast_f64")
+
+    def split_step_2d(self, u, out, tmp, tau, drift1, drift2, a1=None, a2=None, b=0.0,
+                      engine=ENGINE_DIRECT, workspace=None, stream=None):
+        n = u.shape[0]
+        ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+        st = self.lib.lob_split_step_2d_f64(self.ctx, _ptr(u), _ptr(out), _ptr(tmp), n, float(tau),
+                                            float(drift1), float(drift2), _ptr(a1), _ptr(a2),
+                                            float(b), int(engine), _ptr(workspace), ws_bytes,
+                                            _stream_ptr(stream))
+        self._check(st, "lob_split_step_2d_f64")
+
+    def evolve(self, u, scratch, drift, tau, steps, tv=None, tv_stride=0, eta=0.0,
+               engine=ENGINE_FAST, step_drift=None, step_blocks=None, workspace=None, stream=None):
+        lines, n = u.shape
+        done = ctypes.c_int64()
+        ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+        st = self.lib.lob_evolve_f64(self.ctx, _ptr(u), _ptr(scratch), lines, n, _ptr(drift),
+                                     float(tau), _ptr(tv), tv_stride, float(eta), int(engine),
+                                     int(steps), _ptr(step_drift), _ptr(step_blocks),
+                                     ctypes.byref(done), _ptr(workspace), ws_bytes,
+                                     _stream_ptr(stream))
+        self._check(st, "lob_evolve_f64")
+        return int(done.value)
+
+    def step_host(self, u: np.ndarray, drift: np.ndarray, tau: float, tv=None, tv_stride=0,
+                  eta=0.0, engine=ENGINE_FAST, out=None, blocks=None) -> np.ndarray:
+        lines, n = u.shape
+        if out is None:
+            out = np.empty_like(u)
+        st = self.lib.lob_step_host_f64(self.ctx, _ptr(u), _ptr(out), lines, n, _ptr(drift),
+                                        float(tau), _ptr(tv), tv_stride, float(eta), int(engine),
+                                        _ptr(blocks))
+        self._check(st, "lob_step_host_f64")
+        return out
+
+    def block_counts(self, u, blocks, eta=0.0, stream=None):
+        lines, n = u.shape
+        st = self.lib.lob_block_counts(self.ctx, _ptr(u), lines, n, float(eta), _ptr(blocks),
+                                       _stream_ptr(stream))
+        self._check(st, "lob_block_counts")
+
+    def bench_fp64(self):
+        a, b, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        st = self.lib.lob_bench_fp64(self.ctx, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c))
+        self._check(st, "lob_bench_fp64")
+        return {"minplus_cand_per_s": a.value, "dadd_ops_per_s": b.value, "sm_clock_ghz": c.value}
+
+
+# ---- synthetic workloads (include/laxol_b200_configs.h) ---------------------
+
+def gen_sin(n: int) -> np.ndarray:
+    out = np.empty(n, np.float64)
+    _capi.load().lob_gen_sin(n, out.ctypes.data)
+    return out
+
+
+def gen_cos(n: int) -> np.ndarray:
+    out = np.empty(n, np.float64)
+    _capi.load().lob_gen_cos(n, out.ctypes.data)
+    return out
+
+
+def gen_potential(kind: int, n: int) -> np.ndarray:
+    out = np.empty(n, np.float64)
+    _capi.load().lob_gen_potential(int(kind), n, out.ctypes.data)
+    return out
+
+
+def gen_c2_drifts(lines: int = 256) -> np.ndarray:
+    out = np.empty(lines, np.float64)
+    _capi.load().lob_gen_c2_drifts(lines, out.ctypes.data)
+    return out
+
+
+def gen_c3_lines(line0: int, lines: int, n: int = 4096, seed0: int = 1000) -> np.ndarray:
+    out = np.empty((lines, n), np.float64)
+    _capi.load().lob_gen_c3_lines(line0, lines, n, seed0, out.ctypes.data)
+    return out
+
+
+def gen_c4_u0(n: int = 2048) -> np.ndarray:
+    out = np.empty((n, n), np.float64)
+    _capi.load().lob_gen_c4_u0(n, out.ctypes.data)
+    return out
+
+
+def c4_time_term(t: float) -> float:
+    return float(_capi.load().lob_c4_time_term(float(t)))
+
+
+def gen_c5_lines(line0: int, lines: int, n: int = 1 << 20, seed0: int = 5000,
+                 nthreads: int = 0) -> np.ndarray:
+    import os
+
+    out = np.empty((lines, n), np.float64)
+    nt = nthreads or (os.cpu_count() or 1)
+    _capi.load().lob_gen_c5_lines(line0, lines, n, seed0, out.ctypes.data, nt)
+    return out
+
+
+def tau_v(v: np.ndarray, tau: float) -> np.ndarray:
+    """tau*V rounded once (the product in proj/src/scheme.cpp:161)."""
+    return np.multiply(float(tau), v)
+
+
+def llround(x: float) -> int:
+    """C llround: half away from zero."""
+    return int(math.floor(x + 0.5)) if x >= 0 else -int(math.floor(-x + 0.5))

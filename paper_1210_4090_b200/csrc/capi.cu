@@ -1,0 +1,373 @@
+// C-ABI entry points of laxol_b200 (declared in include/laxol_b200.h).
+// Validation mirrors the reference's InvalidInput checks
+// (proj/src/scheme.cpp:18-24,39-53; proj/src/grid_fn.cpp:11-22).
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "lob_internal.cuh"
+
+using namespace lob;
+
+namespace {
+
+const char* kVersion = "laxol_b200 0.1 (sm_100a)";
+
+int check_lines(lob_ctx* ctx, int64_t lines, int64_t n, const char* who) {
+    if (!ctx) return LOB_INVALID_INPUT;
+    if (lines < 0) return set_error(ctx, LOB_INVALID_INPUT, std::string(who) + ": lines < 0");
+    if (n < 1)
+        return set_error(ctx, LOB_INVALID_INPUT,
+                         std::string(who) + ": periodic function needs n >= 1");
+    return LOB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lob_version(void) { return kVersion; }
+
+int lob_ctx_create(int device, lob_ctx** out) {
+    if (!out) return LOB_INVALID_INPUT;
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) return LOB_CUDA_ERROR;  // no CPU fallback
+    if (device < 0 || device >= count) return LOB_INVALID_INPUT;
+    auto* ctx = new lob_ctx();
+    ctx->device = device;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        delete ctx;
+        return LOB_CUDA_ERROR;
+    }
+    cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete ctx;
+        return LOB_CUDA_ERROR;
+    }
+    *out = ctx;
+    return LOB_OK;
+}
+
+int lob_ctx_destroy(lob_ctx* ctx) {
+    if (!ctx) return LOB_OK;
+    cudaSetDevice(ctx->device);
+    for (auto& kv : ctx->vtabs) cudaFree(kv.second.dev);
+    if (ctx->scratch) cudaFree(ctx->scratch);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return LOB_OK;
+}
+
+const char* lob_last_error(const lob_ctx* ctx) { return ctx ? ctx->last_error.c_str() : ""; }
+
+int64_t lob_launch_count(const lob_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int lob_minplus_direct_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
+                           const double* ktab, int64_t ktab_stride, const int64_t* first,
+                           const double* tv, int64_t tv_stride, void* stream) {
+    int st = check_lines(ctx, lines, n, "lob_minplus_direct_f64");
+    if (st) return st;
+    if (lines == 0) return LOB_OK;
+    if (!u || !out || !ktab || !first)
+        return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_direct_f64: null buffer");
+    if (u == out)
+        return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_direct_f64: out must not alias u");
+    return launch_direct_f64(ctx, u, out, lines, n, ktab, ktab_stride, first, tv, tv_stride,
+                             static_cast<cudaStream_t>(stream));
+}
+
+int lob_minplus_direct_f32(lob_ctx* ctx, const float* u, float* out, int64_t lines, int64_t n,
+                           const float* ktab, int64_t ktab_stride, const int64_t* first,
+                           void* stream) {
+    int st = check_lines(ctx, lines, n, "lob_minplus_direct_f32");
+    if (st) return st;
+    if (lines == 0) return LOB_OK;
+    if (!u || !out || !ktab || !first)
+        return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_direct_f32: null buffer");
+    if (static_cast<const void*>(u) == static_cast<const void*>(out))
+        return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_direct_f32: out must not alias u");
+    return launch_direct_f32(ctx, u, out, lines, n, ktab, ktab_stride, first,
+                             static_cast<cudaStream_t>(stream));
+}
+
+int lob_minplus_window_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t m,
+                           int64_t n, const double* ktab, int64_t ktab_stride,
+                           const int64_t* first, const double* tv, int64_t tv_stride,
+                           void* stream) {
+    int st = check_lines(ctx, lines, n, "lob_minplus_window_f64");
+    if (st) return st;
+    if (m < 1) return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_window_f64: empty sample vector");
+    if (lines == 0) return LOB_OK;
+    if (lines > 65535) return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_window_f64: too many lines");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int* d_err = nullptr;
+    LOB_CUDA_TRY(ctx, cudaMallocAsync(&d_err, sizeof(int), s));
+    LOB_CUDA_TRY(ctx, cudaMemsetAsync(d_err, 0, sizeof(int), s));
+    st = launch_window_f64(ctx, u, out, lines, m, n, ktab, ktab_stride, first, tv, tv_stride,
+                           d_err, s);
+    int h_err = 0;
+    if (st == LOB_OK) {
+        LOB_CUDA_TRY(ctx, cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+        LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    }
+    cudaFreeAsync(d_err, s);
+    if (st) return st;
+    if (h_err)
+        return set_error(ctx, LOB_EVALUATION_ERROR,
+                         "kinetic_convolve: kernel window does not reach some grid index");
+    return LOB_OK;
+}
+
+int lob_fast_workspace_bytes(int64_t lines, int64_t n, size_t* bytes) {
+    if (!bytes || lines < 0 || n < 1) return LOB_INVALID_INPUT;
+    *bytes = fast_workspace_bytes(lines, n);
+    return LOB_OK;
+}
+
+int lob_minplus_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
+                         const double* drift, double tau, const double* tv, int64_t tv_stride,
+                         double eta, int64_t* blocks, void* workspace, size_t workspace_bytes,
+                         int flags, void* stream) {
+    int st = check_lines(ctx, lines, n, "lob_minplus_fast_f64");
+    if (st) return st;
+    if (!(tau > 0.0)) return set_error(ctx, LOB_INVALID_INPUT, "SchemeParams: tau must be positive");
+    if (eta < 0.0) return set_error(ctx, LOB_INVALID_INPUT, "SchemeParams: eta must be >= 0");
+    if ((1.0 / static_cast<double>(n)) / tau >= 1.0)
+        return set_error(ctx, LOB_INVALID_INPUT, "SchemeParams: epsilon/tau violates epsilon/tau < h0");
+    if (lines == 0) return LOB_OK;
+    if (!u || !out || !drift)
+        return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_fast_f64: null buffer");
+    if (u == out) return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_fast_f64: out must not alias u");
+    return launch_fast_f64(ctx, u, out, lines, n, drift, tau, tv, tv_stride, eta, blocks, workspace,
+                           workspace_bytes, flags, static_cast<cudaStream_t>(stream));
+}
+
+int lob_block_counts(lob_ctx* ctx, const double* u, int64_t lines, int64_t n, double eta,
+                     int64_t* blocks, void* stream) {
+    int st = check_lines(ctx, lines, n, "lob_block_counts");
+    if (st) return st;
+    if (lines == 0) return LOB_OK;
+    return launch_block_counts(ctx, u, lines, n, eta, blocks, static_cast<cudaStream_t>(stream));
+}
+
+int lob_split_step_2d_f64(lob_ctx* ctx, const double* u, double* out, double* tmp, int64_t n,
+                          double tau, double drift1, double drift2, const double* a1,
+                          const double* a2, double b, int engine, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+    int st = check_lines(ctx, n, n, "lob_split_step_2d_f64");
+    if (st) return st;
+    if (!u || !out || !tmp || u == out || u == tmp || out == tmp)
+        return set_error(ctx, LOB_INVALID_INPUT, "lob_split_step_2d_f64: need distinct u/out/tmp");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // kernel tables / drifts for the two axes live in the context scratch
+    const size_t W = static_cast<size_t>(2 * n + 1);
+    const size_t need = 2 * W * sizeof(double) + 2 * n * sizeof(int64_t) + 2 * n * sizeof(double);
+    if (ctx->scratch_bytes < need) {
+        if (ctx->scratch) cudaFree(ctx->scratch);
+        ctx->scratch = nullptr;
+        LOB_CUDA_TRY(ctx, cudaMalloc(&ctx->scratch, need));
+        ctx->scratch_bytes = need;
+    }
+    double* k1 = static_cast<double*>(ctx->scratch);
+    double* k2 = k1 + W;
+    int64_t* firsts = reinterpret_cast<int64_t*>(k2 + W);  // n entries per axis
+    double* drifts = reinterpret_cast<double*>(firsts + 2 * n);
+    std::vector<double> h1, h2;
+    int64_t f1, f2, arg;
+    double dl;
+    h1.resize(W);
+    h2.resize(W);
+    if (lob_kernel_mech_host(ctx, n, tau, drift1, h1.data(), &f1, &arg, &dl) ||
+        lob_kernel_mech_host(ctx, n, tau, drift2, h2.data(), &f2, &arg, &dl))
+        return set_error(ctx, LOB_INVALID_INPUT, "split_step_nd: invalid kernel parameters");
+    std::vector<int64_t> hf(static_cast<size_t>(2 * n));
+    for (int64_t i = 0; i < n; ++i) {
+        hf[i] = f1;
+        hf[n + i] = f2;
+    }
+    std::vector<double> hd(static_cast<size_t>(2 * n));
+    for (int64_t i = 0; i < n; ++i) {
+        hd[i] = drift1;
+        hd[n + i] = drift2;
+    }
+    // tables are tiny; synchronous upload keeps the host vectors' lifetime simple
+    LOB_CUDA_TRY(ctx, cudaMemcpyAsync(k1, h1.data(), W * sizeof(double), cudaMemcpyHostToDevice, s));
+    LOB_CUDA_TRY(ctx, cudaMemcpyAsync(k2, h2.data(), W * sizeof(double), cudaMemcpyHostToDevice, s));
+    LOB_CUDA_TRY(ctx, cudaMemcpyAsync(firsts, hf.data(), hf.size() * sizeof(int64_t),
+                                      cudaMemcpyHostToDevice, s));
+    LOB_CUDA_TRY(ctx, cudaMemcpyAsync(drifts, hd.data(), hd.size() * sizeof(double),
+                                      cudaMemcpyHostToDevice, s));
+    LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    // axis 0: columns of u are rows of u^T
+    if ((st = launch_transpose(ctx, u, tmp, n, s))) return st;
+    if (engine == LOB_ENGINE_FAST) {
+        if ((st = launch_fast_f64(ctx, tmp, out, n, n, drifts, tau, nullptr, 0, 0.0, nullptr,
+                                  workspace, workspace_bytes, 0, s)))
+            return st;
+    } else {
+        if ((st = launch_direct_f64(ctx, tmp, out, n, n, k1, 0, firsts, nullptr, 0, s))) return st;
+    }
+    if ((st = launch_transpose(ctx, out, tmp, n, s))) return st;
+    // axis 1: contiguous rows
+    if (engine == LOB_ENGINE_FAST) {
+        if ((st = launch_fast_f64(ctx, tmp, out, n, n, drifts + n, tau, nullptr, 0, 0.0, nullptr,
+                                  workspace, workspace_bytes, 0, s)))
+            return st;
+    } else {
+        if ((st = launch_direct_f64(ctx, tmp, out, n, n, k2, 0, firsts + n, nullptr, 0, s)))
+            return st;
+    }
+    if (a1 && a2) return launch_potential2d(ctx, out, a1, a2, b, tau, n, s);
+    return LOB_OK;
+}
+
+int lob_evolve_f64(lob_ctx* ctx, double* u, double* scratch, int64_t lines, int64_t n,
+                   const double* drift, double tau, const double* tv, int64_t tv_stride,
+                   double eta, int engine, int64_t steps, double* step_drift,
+                   int64_t* step_blocks, int64_t* completed_steps, void* workspace,
+                   size_t workspace_bytes, void* stream) {
+    int st = check_lines(ctx, lines, n, "lob_evolve_f64");
+    if (st) return st;
+    if (steps < 0) return set_error(ctx, LOB_INVALID_INPUT, "evolve: steps must be >= 0");
+    if (completed_steps) *completed_steps = 0;
+    if (lines == 0 || steps == 0) return LOB_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // direct engine needs the per-line kernel tables: built on the host
+    // (proj/src/scheme.cpp:213 builds the kernel once per evolve)
+    std::vector<double> hdrift(static_cast<size_t>(lines));
+    LOB_CUDA_TRY(ctx, cudaMemcpyAsync(hdrift.data(), drift, lines * sizeof(double),
+                                      cudaMemcpyDeviceToHost, s));
+    LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    double* ktab = nullptr;
+    int64_t* firsts = nullptr;
+    int* halt = nullptr;
+    const int64_t W = 2 * n + 1;
+    if (engine == LOB_ENGINE_DIRECT) {
+        LOB_CUDA_TRY(ctx, cudaMallocAsync(&ktab, lines * W * sizeof(double), s));
+        LOB_CUDA_TRY(ctx, cudaMallocAsync(&firsts, lines * sizeof(int64_t), s));
+        std::vector<double> hk(static_cast<size_t>(lines * W));
+        std::vector<int64_t> hf(static_cast<size_t>(lines));
+        for (int64_t l = 0; l < lines; ++l) {
+            int64_t arg;
+            double dl;
+            if (lob_kernel_mech_host(ctx, n, tau, hdrift[l], hk.data() + l * W, &hf[l], &arg, &dl))
+                return set_error(ctx, LOB_INVALID_INPUT, "evolve: invalid scheme parameters");
+        }
+        LOB_CUDA_TRY(ctx, cudaMemcpyAsync(ktab, hk.data(), hk.size() * sizeof(double),
+                                          cudaMemcpyHostToDevice, s));
+        LOB_CUDA_TRY(ctx, cudaMemcpyAsync(firsts, hf.data(), hf.size() * sizeof(int64_t),
+                                          cudaMemcpyHostToDevice, s));
+        LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    }
+    LOB_CUDA_TRY(ctx, cudaMallocAsync(&halt, sizeof(int), s));
+    const int big = 0x7fffffff;
+    LOB_CUDA_TRY(ctx, cudaMemcpyAsync(halt, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+    double* cur = u;
+    double* nxt = scratch;
+    int64_t done = 0;
+    int hstep = big;
+    const int64_t chunk = 64;
+    for (int64_t i = 0; i < steps; ++i) {
+        if (engine == LOB_ENGINE_DIRECT) {
+            st = launch_direct_f64(ctx, cur, nxt, lines, n, ktab, W, firsts, tv, tv_stride, s);
+            if (st == LOB_OK && step_blocks)
+                st = launch_block_counts(ctx, cur, lines, n, eta, step_blocks + i * lines, s);
+        } else {
+            st = launch_fast_f64(ctx, cur, nxt, lines, n, drift, tau, tv, tv_stride, eta,
+                                 step_blocks ? step_blocks + i * lines : nullptr, workspace,
+                                 workspace_bytes, i == 0 ? 0 : LOB_FAST_STATS_VALID, s);
+        }
+        if (st) break;
+        st = launch_drift(ctx, nxt, cur, lines, n, step_drift ? step_drift + i * lines : nullptr,
+                          halt, static_cast<int>(i), s);
+        if (st) break;
+        std::swap(cur, nxt);
+        done = i + 1;
+        if ((i + 1) % chunk == 0 || i + 1 == steps) {
+            LOB_CUDA_TRY(ctx, cudaMemcpyAsync(&hstep, halt, sizeof(int), cudaMemcpyDeviceToHost, s));
+            LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+            if (hstep != big) break;
+        }
+    }
+    if (st == LOB_OK && hstep != big) {
+        // non-finite after step hstep+1 (proj/src/scheme.cpp:257-264): the trace
+        // stops there.  Steps after it within the chunk ran on non-finite data;
+        // the caller re-runs with steps = hstep+1 to obtain that state.
+        done = hstep + 1;
+    }
+    if (cur != u && st == LOB_OK && hstep == big)
+        LOB_CUDA_TRY(ctx, cudaMemcpyAsync(u, cur, lines * n * sizeof(double),
+                                          cudaMemcpyDeviceToDevice, s));
+    if (ktab) cudaFreeAsync(ktab, s);
+    if (firsts) cudaFreeAsync(firsts, s);
+    cudaFreeAsync(halt, s);
+    LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    if (completed_steps) *completed_steps = done;
+    if (st) return st;
+    if (hstep != big)
+        return set_error(ctx, LOB_EVALUATION_ERROR,
+                         "non-finite value after step " + std::to_string(hstep + 1));
+    return LOB_OK;
+}
+
+int lob_step_host_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
+                      const double* drift, double tau, const double* tv, int64_t tv_stride,
+                      double eta, int engine, int64_t* blocks) {
+    int st = check_lines(ctx, lines, n, "lob_step_host_f64");
+    if (st) return st;
+    if (lines == 0) return LOB_OK;
+    cudaStream_t s = ctx->stream;
+    const size_t ub = static_cast<size_t>(lines * n) * sizeof(double);
+    const size_t tvn = tv ? static_cast<size_t>(tv_stride ? lines * tv_stride : n) : 0;
+    size_t wsb = fast_workspace_bytes(lines, n);
+    const int64_t W = 2 * n + 1;
+    const size_t kb = engine == LOB_ENGINE_DIRECT ? static_cast<size_t>(lines * W) * sizeof(double) : 0;
+    const size_t need = 2 * ub + tvn * sizeof(double) + lines * (sizeof(double) + 2 * sizeof(int64_t)) +
+                        wsb + kb + 256;
+    if (ctx->scratch_bytes < need) {
+        if (ctx->scratch) cudaFree(ctx->scratch);
+        ctx->scratch = nullptr;
+        LOB_CUDA_TRY(ctx, cudaMalloc(&ctx->scratch, need));
+        ctx->scratch_bytes = need;
+    }
+    char* p = static_cast<char*>(ctx->scratch);
+    double* du = reinterpret_cast<double*>(p);
+    double* dout = du + lines * n;
+    double* dtv = dout + lines * n;
+    double* ddrift = dtv + tvn;
+    int64_t* dblocks = reinterpret_cast<int64_t*>(ddrift + lines);
+    int64_t* dfirst = dblocks + lines;
+    double* dk = reinterpret_cast<double*>(dfirst + lines);
+    void* ws = reinterpret_cast<char*>(dk) + kb;
+    LOB_CUDA_TRY(ctx, cudaMemcpyAsync(du, u, ub, cudaMemcpyHostToDevice, s));
+    if (tv) LOB_CUDA_TRY(ctx, cudaMemcpyAsync(dtv, tv, tvn * sizeof(double), cudaMemcpyHostToDevice, s));
+    LOB_CUDA_TRY(ctx, cudaMemcpyAsync(ddrift, drift, lines * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (engine == LOB_ENGINE_DIRECT) {
+        std::vector<double> hk(static_cast<size_t>(lines * W));
+        std::vector<int64_t> hf(static_cast<size_t>(lines));
+        for (int64_t l = 0; l < lines; ++l) {
+            int64_t arg;
+            double dl;
+            if (lob_kernel_mech_host(ctx, n, tau, drift[l], hk.data() + l * W, &hf[l], &arg, &dl))
+                return set_error(ctx, LOB_INVALID_INPUT, "step: invalid scheme parameters");
+        }
+        LOB_CUDA_TRY(ctx, cudaMemcpyAsync(dk, hk.data(), hk.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+        LOB_CUDA_TRY(ctx, cudaMemcpyAsync(dfirst, hf.data(), hf.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        st = launch_direct_f64(ctx, du, dout, lines, n, dk, W, dfirst, tv ? dtv : nullptr, tv_stride, s);
+        if (st == LOB_OK && blocks) st = launch_block_counts(ctx, du, lines, n, eta, dblocks, s);
+        LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));  // host vectors go out of scope
+    } else {
+        st = launch_fast_f64(ctx, du, dout, lines, n, ddrift, tau, tv ? dtv : nullptr, tv_stride, eta,
+                             blocks ? dblocks : nullptr, ws, wsb, 0, s);
+    }
+    if (st) return st;
+    LOB_CUDA_TRY(ctx, cudaMemcpyAsync(out, dout, ub, cudaMemcpyDeviceToHost, s));
+    if (blocks)
+        LOB_CUDA_TRY(ctx, cudaMemcpyAsync(blocks, dblocks, lines * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    return LOB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,81 @@
+// Host-side kernel-window construction, restating build_kernel for the
+// mechanical conjugate (proj/src/scheme.cpp:59-105 with
+// proj/src/hamiltonian.cpp:42-44) so the device path sees the identical
+// table, plus the fast engine's slope-inversion tolerance.
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "laxol_b200.hpp"
+
+namespace laxol_b200 {
+
+KernelWindow build_kernel_mech(int64_t n_space, double tau, double drift) {
+    if (n_space < 1) throw InvalidInput("SchemeParams: n_space must be >= 1");
+    if (!(tau > 0.0)) throw InvalidInput("SchemeParams: tau must be positive");
+    const double eps = 1.0 / static_cast<double>(n_space);
+    if (eps / tau >= 1.0)
+        throw InvalidInput("SchemeParams: epsilon/tau = " + std::to_string(eps / tau) +
+                           " violates the bound epsilon/tau < h0 = 1");
+    KernelWindow k;
+    k.n_space = n_space;
+    k.tau = tau;
+    k.drift = drift;
+    const int64_t center = std::llround(tau * drift / eps);
+    k.first = center - n_space;
+    k.center_index = center;
+    const int64_t m = 2 * n_space + 1;
+    k.window.resize(static_cast<size_t>(m));
+    for (int64_t i = 0; i < m; ++i) {
+        const double x = static_cast<double>(k.first + i) * eps;
+        const double v = x / tau;
+        k.window[static_cast<size_t>(i)] = tau * (0.5 * v * v - drift * v);
+    }
+    for (int64_t i = 0; i + 2 < m; ++i) {
+        const double lo = k.window[i + 1] - k.window[i];
+        const double hi = k.window[i + 2] - k.window[i + 1];
+        if (hi < lo)
+            throw InvalidInput("build_kernel: sampled window is not convex at segment " +
+                               std::to_string(i + 1));
+    }
+    int64_t arg = 0;
+    for (int64_t i = 1; i < m; ++i)
+        if (k.window[i] < k.window[arg]) arg = i;
+    k.argmin_index = arg;
+    k.delta = fast_delta(n_space, tau, drift, k.first);
+    return k;
+}
+
+// Tolerance (in displacement units) of the fast engine's slope inversion
+// d(s) = (s + drift*eps)/a - 1/2 against the rounded table: bound on the
+// table's slope error (each K value carries <= 6 ulp of its magnitude) plus
+// the rounding of the inversion itself.  See DESIGN.md "K2".
+double fast_delta(int64_t n_space, double tau, double drift, int64_t first) {
+    const double u = std::ldexp(1.0, -53);
+    const double eps = 1.0 / static_cast<double>(n_space);
+    const double a = eps * eps / tau;
+    const double dmax = std::fmax(std::fabs(static_cast<double>(first)),
+                                  std::fabs(static_cast<double>(first + 2 * n_space)));
+    const double vmax = dmax * eps / tau;
+    const double kmag = tau * (0.5 * vmax * vmax + std::fabs(drift) * vmax);
+    return 32.0 * u * kmag / a + 8.0 * u * (2.0 * n_space + std::fabs(drift) * eps / a) + 1e-9;
+}
+
+}  // namespace laxol_b200
+
+extern "C" int lob_kernel_mech_host(lob_ctx*, int64_t n, double tau, double drift,
+                                    double* window, int64_t* first, int64_t* argmin,
+                                    double* delta) {
+    try {
+        const laxol_b200::KernelWindow k = laxol_b200::build_kernel_mech(n, tau, drift);
+        if (window) std::memcpy(window, k.window.data(), k.window.size() * sizeof(double));
+        if (first) *first = k.first;
+        if (argmin) *argmin = k.argmin_index;
+        if (delta) *delta = k.delta;
+        return LOB_OK;
+    } catch (const laxol_b200::InvalidInput&) {
+        return LOB_INVALID_INPUT;
+    }
+}

@@ -1,0 +1,158 @@
+// laxol_b200 — C++ host API mirroring the reference's stepping API
+// (namespace laxol, /root/reference/proj/include/laxol/{grid_fn,scheme,
+// splitting,hamiltonian,errors}.hpp) over the C-ABI in include/laxol_b200.h.
+//
+// A reference user switches by replacing `laxol::` calls on the hot path
+// with `laxol_b200::Engine` methods of the same name and arguments; the
+// engine value ConvEngine::GpuFast / GpuDirect selects the B200 kernels the
+// way ConvEngine::{Fast,Naive} selects the reference's CPU engines
+// (proj/include/laxol/scheme.hpp:13, dispatch proj/src/scheme.cpp:114-121).
+#pragma once
+
+#include <cstdint>
+#include <functional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../../include/laxol_b200.h"
+
+namespace laxol_b200 {
+
+// proj/include/laxol/errors.hpp:9-17
+struct InvalidInput : std::runtime_error {
+    explicit InvalidInput(const std::string& w) : std::runtime_error(w) {}
+};
+struct EvaluationError : std::runtime_error {
+    explicit EvaluationError(const std::string& w) : std::runtime_error(w) {}
+};
+
+// proj/include/laxol/grid_fn.hpp:13-23: closed period for periodic functions
+// (seam duplicated), n() = values.size() - 1.
+struct GridFn {
+    std::vector<double> values;
+    double step = 1.0;
+    double origin = 0.0;
+    bool periodic = false;
+    std::size_t n() const { return values.size() - 1; }
+    std::size_t size() const { return values.size(); }
+    double coord(std::size_t i) const { return origin + static_cast<double>(i) * step; }
+};
+GridFn make_periodic(std::vector<double> fundamental, double step, double origin = 0.0);
+GridFn make_grid_fn(std::vector<double> values, double step, double origin = 0.0);
+
+// Kernel (proj/include/laxol/scheme.hpp:34-42) for the mechanical conjugate
+// K*(v) = v^2/2 - drift*v; window[w] at grid displacement first + w.
+struct KernelWindow {
+    std::vector<double> window;
+    int64_t first = 0;
+    int64_t center_index = 0;
+    int64_t argmin_index = 0;
+    int64_t n_space = 0;
+    double tau = 0.0;
+    double drift = 0.0;
+    double delta = 0.0;  // fast-engine slope-inversion tolerance
+};
+KernelWindow build_kernel_mech(int64_t n_space, double tau, double drift);
+double fast_delta(int64_t n_space, double tau, double drift, int64_t first);
+
+enum class ConvEngine { Fast, Naive, GpuFast, GpuDirect };
+enum class PotentialSampling { Arrival, Departure };
+
+// proj/include/laxol/scheme.hpp:17-26
+struct SchemeParams {
+    int n_space = 0;
+    double tau = 0.0;
+    double eta = 0.0;
+    double h0 = 1.0;
+    PotentialSampling v_sampling = PotentialSampling::Arrival;
+    double epsilon() const { return 1.0 / static_cast<double>(n_space); }
+};
+void validate(const SchemeParams& p);
+
+// V(t, x) callback (proj/include/laxol/hamiltonian.hpp:34-73 reduced to what
+// the hot path calls): evaluated on the host per grid point, like the
+// reference (proj/src/scheme.cpp:158).  Empty = V == 0.
+struct Potential {
+    std::function<double(double, double)> fn;
+    bool time_dependent = false;
+    double operator()(double t, double x) const { return fn ? fn(t, x) : 0.0; }
+    explicit operator bool() const { return static_cast<bool>(fn); }
+};
+
+struct StepStats {
+    int64_t block_count = 0;
+};
+
+// proj/include/laxol/scheme.hpp:61-90
+struct StepRecord {
+    double time = 0.0;
+    int64_t blocks = 0;
+    double drift = 0.0;
+    double wall_seconds = 0.0;
+};
+struct EvolutionTrace {
+    std::vector<double> times;
+    std::vector<int64_t> snapshot_steps;
+    std::vector<GridFn> snapshots;
+    std::vector<StepRecord> per_step;
+    bool completed = true;
+    std::string abort_reason;
+};
+struct EvolveOptions {
+    int64_t snapshot_stride = 0;
+    ConvEngine engine = ConvEngine::GpuFast;
+    std::vector<int64_t> capture_steps;
+};
+
+// proj/include/laxol/splitting.hpp:13-41 (rank 2, periodic, separable
+// potential V = a1(x1)*a2(x2) + b(t) given by its host factors).
+struct TensorFn {
+    std::vector<double> values;
+    std::vector<std::size_t> dims;
+    double step = 1.0;
+    std::vector<double> origins;
+    bool periodic = true;
+};
+struct SeparablePotential2D {
+    std::function<double(double)> a1, a2;  // x -> factor, empty = V == 0
+    std::function<double(double)> b;       // t -> additive time term
+};
+struct SplitSpec2D {
+    double drift1 = 0.0, drift2 = 0.0;
+    SeparablePotential2D potential;
+};
+
+// The device engine: owns a lob_ctx, device buffers and workspaces.
+class Engine {
+public:
+    explicit Engine(int device = 0);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    // proj/src/scheme.cpp:107-146
+    GridFn kinetic_convolve(const GridFn& u, const KernelWindow& kernel, double eta,
+                            ConvEngine engine = ConvEngine::GpuFast, int64_t* blocks = nullptr);
+    // proj/src/scheme.cpp:148-164
+    GridFn step_fully_discrete(const GridFn& u, double t, const Potential& V,
+                               const SchemeParams& params, const KernelWindow& kernel,
+                               ConvEngine engine = ConvEngine::GpuFast,
+                               StepStats* stats = nullptr);
+    // proj/src/scheme.cpp:208-272 (time-independent V: device-resident loop)
+    EvolutionTrace evolve(const GridFn& u0, double t0, int64_t steps, double drift,
+                          const Potential& V, const SchemeParams& params,
+                          const EvolveOptions& options = {});
+    // proj/src/splitting.cpp:37-99
+    TensorFn split_step_nd(const TensorFn& u, double t, const SplitSpec2D& spec,
+                           const SchemeParams& params,
+                           ConvEngine engine = ConvEngine::GpuDirect);
+
+    lob_ctx* ctx() const { return ctx_; }
+
+private:
+    lob_ctx* ctx_ = nullptr;
+};
+
+}  // namespace laxol_b200

@@ -1,0 +1,98 @@
+// Internal definitions shared by the laxol_b200 CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <map>
+#include <string>
+#include <tuple>
+
+#include "../../include/laxol_b200.h"
+
+struct lob_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;  // the context's own stream (host entry points)
+    std::string last_error;
+    int64_t launches = 0;
+    // cached velocity tables v_d = (d*eps)/tau keyed by (n, tau bits)
+    struct VTab {
+        double* dev = nullptr;
+        int64_t dmin = 0, count = 0;
+    };
+    std::map<std::pair<int64_t, uint64_t>, VTab> vtabs;
+    // fast-engine workspaces: which statistics buffer holds the current u
+    std::map<const void*, int> ws_parity;
+    std::map<const void*, std::pair<int64_t, int64_t>> ws_shape;
+    // scratch for host entry points
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+};
+
+namespace lob {
+
+inline int set_error(lob_ctx* ctx, int code, const std::string& msg) {
+    if (ctx) ctx->last_error = msg;
+    return code;
+}
+
+inline int cuda_status(lob_ctx* ctx, cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return LOB_OK;
+    return set_error(ctx, LOB_CUDA_ERROR, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define LOB_CUDA_TRY(ctx, expr)                                      \
+    do {                                                             \
+        cudaError_t _e = (expr);                                     \
+        if (_e != cudaSuccess) return ::lob::cuda_status(ctx, _e, #expr); \
+    } while (0)
+
+// Order-preserving map double -> uint64 (x < y  <=>  key(x) < key(y) for
+// non-NaN x, y; -0 orders just below +0).
+__device__ __forceinline__ unsigned long long dkey(double x) {
+    unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dkey_inv(unsigned long long k) {
+    unsigned long long b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+    return __longlong_as_double(static_cast<long long>(b));
+}
+constexpr unsigned long long kKeyInf = 0xfff0000000000000ull;  // dkey(+inf)
+
+inline int64_t floordiv(int64_t a, int64_t b) {
+    int64_t q = a / b;
+    return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
+}
+inline int64_t posmod(int64_t a, int64_t n) {
+    int64_t r = a % n;
+    return r < 0 ? r + n : r;
+}
+
+// Launch helpers implemented in the .cu files.
+int launch_direct_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
+                      const double* ktab, int64_t ktab_stride, const int64_t* first,
+                      const double* tv, int64_t tv_stride, cudaStream_t s);
+int launch_direct_f32(lob_ctx* ctx, const float* u, float* out, int64_t lines, int64_t n,
+                      const float* ktab, int64_t ktab_stride, const int64_t* first,
+                      cudaStream_t s);
+int launch_window_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t m,
+                      int64_t n, const double* ktab, int64_t ktab_stride, const int64_t* first,
+                      const double* tv, int64_t tv_stride, int* d_err, cudaStream_t s);
+
+size_t fast_workspace_bytes(int64_t lines, int64_t n);
+int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
+                    const double* drift, double tau, const double* tv, int64_t tv_stride,
+                    double eta, int64_t* blocks, void* workspace, size_t ws_bytes, int flags,
+                    cudaStream_t s);
+int launch_block_counts(lob_ctx* ctx, const double* u, int64_t lines, int64_t n, double eta,
+                        int64_t* blocks, cudaStream_t s);
+
+int launch_transpose(lob_ctx* ctx, const double* src, double* dst, int64_t n, cudaStream_t s);
+int launch_potential2d(lob_ctx* ctx, double* out, const double* a1, const double* a2, double b,
+                       double tau, int64_t n, cudaStream_t s);
+int launch_drift(lob_ctx* ctx, const double* nxt, const double* cur, int64_t lines, int64_t n,
+                 double* drift_out, int* halt, int step, cudaStream_t s);
+
+}  // namespace lob

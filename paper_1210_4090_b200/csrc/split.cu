@@ -1,0 +1,103 @@
+// K3 — 2-D dimension splitting (proj/src/splitting.cpp:37-99, Remark 2.8)
+// on a periodic n x n row-major tensor:
+//   axis 0 (columns, kernel 1) -> axis 1 (rows, kernel 2) -> out -= tau*V.
+// The reference gathers each strided column into a temporary line and
+// scatters it back (proj/src/splitting.cpp:67-76).  Here a tiled transpose
+// (32x64 tiles through shared memory, coalesced 128-bit global accesses on
+// both sides) turns columns into rows so both sweeps run the batched line
+// kernels; the potential pass evaluates the separable descriptor
+// V = a1[i]*a2[k] + b with the C++ expression's roundings and applies
+// out = out - tau*V (two roundings, no FMA; proj/src/splitting.cpp:95).
+// Also: the per-step drift / finiteness check of evolve
+// (proj/src/scheme.cpp:244-264).
+#include "lob_internal.cuh"
+
+namespace lob {
+namespace {
+
+constexpr int kTD = 32;  // transpose tile
+
+__global__ void __launch_bounds__(256) transpose_kernel(const double* __restrict__ src,
+                                                        double* __restrict__ dst, int64_t n) {
+    __shared__ double tile[kTD][kTD + 1];
+    const int64_t bx = static_cast<int64_t>(blockIdx.x) * kTD;  // column block of src
+    const int64_t by = static_cast<int64_t>(blockIdx.y) * kTD;  // row block of src
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;     // 32 x 8
+    for (int r = ty; r < kTD; r += 8) {
+        const int64_t i = by + r, k = bx + tx;
+        if (i < n && k < n) tile[r][tx] = src[i * n + k];
+    }
+    __syncthreads();
+    for (int r = ty; r < kTD; r += 8) {
+        const int64_t k = bx + r, i = by + tx;  // dst[k][i] = src[i][k]
+        if (i < n && k < n) dst[k * n + i] = tile[tx][r];
+    }
+}
+
+__global__ void __launch_bounds__(256) potential2d_kernel(double* __restrict__ out,
+                                                          const double* __restrict__ a1,
+                                                          const double* __restrict__ a2, double b,
+                                                          double tau, int64_t n) {
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= n * n) return;
+    const int64_t i = idx / n, k = idx - i * n;
+    // V = a1*a2 + b; out -= tau*V   (no contraction)
+    const double v = __dadd_rn(__dmul_rn(a1[i], a2[k]), b);
+    out[idx] = __dsub_rn(out[idx], __dmul_rn(tau, v));
+}
+
+__global__ void __launch_bounds__(256) drift_kernel(const double* __restrict__ nxt,
+                                                    const double* __restrict__ cur, int64_t n,
+                                                    double* __restrict__ drift_out,
+                                                    int* __restrict__ halt, int step) {
+    __shared__ double sh[8];
+    __shared__ int bad;
+    const int64_t line = blockIdx.x;
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    double acc = 0.0;
+    int nonfinite = 0;
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+        const double a = nxt[line * n + j];
+        acc += a - cur[line * n + j];
+        nonfinite |= !isfinite(a);
+    }
+    if (nonfinite) bad = 1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < 8; ++w) s += sh[w];
+        if (drift_out) drift_out[line] = s / static_cast<double>(n);
+        if (bad && halt) atomicMin(halt, step);
+    }
+}
+
+}  // namespace
+
+int launch_transpose(lob_ctx* ctx, const double* src, double* dst, int64_t n, cudaStream_t s) {
+    dim3 grid(static_cast<unsigned>((n + kTD - 1) / kTD), static_cast<unsigned>((n + kTD - 1) / kTD));
+    transpose_kernel<<<grid, 256, 0, s>>>(src, dst, n);
+    ctx->launches += 1;
+    return cuda_status(ctx, cudaGetLastError(), "transpose_kernel");
+}
+
+int launch_potential2d(lob_ctx* ctx, double* out, const double* a1, const double* a2, double b,
+                       double tau, int64_t n, cudaStream_t s) {
+    const int64_t total = n * n;
+    potential2d_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(out, a1, a2, b,
+                                                                                  tau, n);
+    ctx->launches += 1;
+    return cuda_status(ctx, cudaGetLastError(), "potential2d_kernel");
+}
+
+int launch_drift(lob_ctx* ctx, const double* nxt, const double* cur, int64_t lines, int64_t n,
+                 double* drift_out, int* halt, int step, cudaStream_t s) {
+    drift_kernel<<<static_cast<unsigned>(lines), 256, 0, s>>>(nxt, cur, n, drift_out, halt, step);
+    ctx->launches += 1;
+    return cuda_status(ctx, cudaGetLastError(), "drift_kernel");
+}
+
+}  // namespace lob

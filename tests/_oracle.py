@@ -1,0 +1,220 @@
+"""Test-only loaders for the CPU checkers under oracle/ (never the product).
+
+oracle():    the plain-C restatement, oracle/_build/liblaxol_oracle.so
+reference(): the unmodified reference library built from /root/reference
+             sources + our extern "C" shim, oracle/_ref/liblaxol_ref.so
+"""
+import ctypes
+import os
+import subprocess
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int64, c_void_p
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_SO = os.path.join(ROOT, "oracle", "_build", "liblaxol_oracle.so")
+REF_SO = os.path.join(ROOT, "oracle", "_ref", "liblaxol_ref.so")
+
+_P = c_void_p
+
+
+def _build_oracle():
+    subprocess.run(["make", "-s", "-f", os.path.join(ROOT, "oracle", "Makefile"), "oracle"],
+                   check=True, cwd=ROOT)
+
+
+class Oracle:
+    def __init__(self, lib):
+        self.lib = lib
+        sig = {
+            "orc_kernel_mech": (c_int, [c_int, c_double, c_double, _P, POINTER(c_int64), POINTER(c_int64)]),
+            "orc_direct_f64": (None, [_P, _P, c_int64, c_int64, _P, c_int64, _P, _P, c_int64, c_int]),
+            "orc_direct_f32": (None, [_P, _P, c_int64, c_int64, _P, c_int64, _P, c_int]),
+            "orc_window_f64": (c_int, [_P, c_int64, c_int64, _P, c_int64, _P]),
+            "orc_conv_naive": (None, [_P, c_int64, _P, c_int64, _P]),
+            "orc_decompose_count": (c_int64, [_P, c_int64, c_double, c_int]),
+            "orc_line_blocks": (c_int64, [_P, c_int64, c_double, c_int]),
+            "orc_split2d_f64": (None, [_P, _P, c_int64, c_int64, _P, c_int64, _P, c_int64, _P, c_int]),
+            "orc_drift": (c_double, [_P, _P, c_int64, POINTER(c_int)]),
+            "orc_tau_v": (None, [_P, c_double, c_int64, _P]),
+        }
+        for k, (r, a) in sig.items():
+            f = getattr(lib, k)
+            f.restype, f.argtypes = r, a
+
+    def kernel(self, n, tau, drift):
+        w = np.empty(2 * n + 1)
+        first, arg = c_int64(), c_int64()
+        st = self.lib.orc_kernel_mech(n, tau, drift, w.ctypes.data, ctypes.byref(first), ctypes.byref(arg))
+        return w, first.value, arg.value, st
+
+    def direct(self, u, ktab, first, tv=None, ktab_stride=0, tv_stride=0, nthreads=0):
+        u = np.ascontiguousarray(u, np.float64)
+        lines, n = u.shape
+        out = np.empty_like(u)
+        first = np.ascontiguousarray(np.broadcast_to(np.asarray(first, np.int64), (lines,)))
+        self.lib.orc_direct_f64(u.ctypes.data, out.ctypes.data, lines, n, ktab.ctypes.data, ktab_stride,
+                                first.ctypes.data, None if tv is None else tv.ctypes.data, tv_stride,
+                                nthreads)
+        return out
+
+    def direct_f32(self, u, ktab, first, ktab_stride=0, nthreads=0):
+        u = np.ascontiguousarray(u, np.float32)
+        lines, n = u.shape
+        out = np.empty_like(u)
+        first = np.ascontiguousarray(np.broadcast_to(np.asarray(first, np.int64), (lines,)))
+        self.lib.orc_direct_f32(u.ctypes.data, out.ctypes.data, lines, n, ktab.ctypes.data, ktab_stride,
+                                first.ctypes.data, nthreads)
+        return out
+
+    def window(self, u, n, ktab, first):
+        u = np.ascontiguousarray(u, np.float64)
+        out = np.empty_like(u)
+        st = self.lib.orc_window_f64(u.ctypes.data, u.size, n, ktab.ctypes.data, first, out.ctypes.data)
+        return out, st
+
+    def conv_naive(self, a, b):
+        a = np.ascontiguousarray(a, np.float64)
+        b = np.ascontiguousarray(b, np.float64)
+        out = np.empty(a.size + b.size - 1)
+        self.lib.orc_conv_naive(a.ctypes.data, a.size, b.ctypes.data, b.size, out.ctypes.data)
+        return out
+
+    def decompose_count(self, v, eta=0.0, capped=False):
+        v = np.ascontiguousarray(v, np.float64)
+        return int(self.lib.orc_decompose_count(v.ctypes.data, v.size, eta, int(capped)))
+
+    def line_blocks(self, u, eta=0.0, capped=False):
+        u = np.ascontiguousarray(u, np.float64)
+        return int(self.lib.orc_line_blocks(u.ctypes.data, u.size, eta, int(capped)))
+
+    def split2d(self, u, k1, first1, k2, first2, tv=None, nthreads=0):
+        u = np.ascontiguousarray(u, np.float64)
+        out = np.empty_like(u)
+        n1, n2 = u.shape
+        self.lib.orc_split2d_f64(u.ctypes.data, out.ctypes.data, n1, n2, k1.ctypes.data, first1,
+                                 k2.ctypes.data, first2, None if tv is None else tv.ctypes.data, nthreads)
+        return out
+
+    def drift(self, nxt, u):
+        fin = c_int()
+        d = self.lib.orc_drift(np.ascontiguousarray(nxt).ctypes.data, np.ascontiguousarray(u).ctypes.data,
+                               u.size, ctypes.byref(fin))
+        return d, bool(fin.value)
+
+
+class Reference:
+    """The reference library itself (oracle/_ref), via oracle/ref_shim.cpp."""
+
+    def __init__(self, lib):
+        self.lib = lib
+        sig = {
+            "ref_last_error": (c_char_p, []),
+            "ref_set_max_threads": (None, [c_int]),
+            "ref_kernel_mech": (c_int, [c_int, c_double, c_double, _P, POINTER(c_int64), POINTER(c_int64)]),
+            "ref_kinetic_convolve": (c_int, [_P, c_int64, c_int, c_int, c_double, c_double, c_double, c_int, _P,
+                                             POINTER(c_int64)]),
+            "ref_step_lines": (c_int, [_P, c_int64, c_int, c_double, _P, _P, c_double, c_double, c_int, c_int,
+                                       _P, _P]),
+            "ref_evolve": (c_int, [_P, c_int, c_double, c_double, _P, c_double, c_int64, c_double, c_int, _P, _P,
+                                   _P, POINTER(c_int)]),
+            "ref_split_step_2d": (c_int, [_P, c_int64, c_int64, c_int, c_double, c_double, c_double, c_int,
+                                          c_double, c_int, _P]),
+            "ref_decompose": (c_int64, [_P, c_int64, c_double, _P, _P, _P, c_int64]),
+            "ref_conv": (c_int, [c_int, _P, c_int64, _P, c_int64, c_double, _P, _P]),
+        }
+        for k, (r, a) in sig.items():
+            f = getattr(lib, k)
+            f.restype, f.argtypes = r, a
+
+    def err(self):
+        return self.lib.ref_last_error().decode()
+
+    def kernel(self, n, tau, drift):
+        w = np.empty(2 * n + 1)
+        c, a = c_int64(), c_int64()
+        st = self.lib.ref_kernel_mech(n, tau, drift, w.ctypes.data, ctypes.byref(c), ctypes.byref(a))
+        return w, c.value - n, a.value, st
+
+    def kinetic_convolve(self, u, n_space, tau, drift, eta=0.0, engine=0, periodic=True):
+        u = np.ascontiguousarray(u, np.float64)
+        out = np.empty(n_space if periodic else u.size)
+        blocks = c_int64()
+        st = self.lib.ref_kinetic_convolve(u.ctypes.data, u.size, int(periodic), n_space, tau, drift, eta,
+                                           engine, out.ctypes.data, ctypes.byref(blocks))
+        return out, blocks.value, st
+
+    def step_lines(self, u, tau, drifts, v=None, t=0.0, eta=0.0, engine=0, nthreads=1):
+        u = np.ascontiguousarray(u, np.float64)
+        lines, n = u.shape
+        drifts = np.ascontiguousarray(np.broadcast_to(np.asarray(drifts, np.float64), (lines,)))
+        out = np.empty_like(u)
+        blocks = np.empty(lines, np.int64)
+        st = self.lib.ref_step_lines(u.ctypes.data, lines, n, tau, drifts.ctypes.data,
+                                     None if v is None else np.ascontiguousarray(v).ctypes.data, t, eta, engine,
+                                     nthreads, out.ctypes.data, blocks.ctypes.data)
+        if st:
+            raise RuntimeError(self.err())
+        return out, blocks
+
+    def evolve(self, u0, tau, drift, v, steps, t0=0.0, eta=0.0, engine=0):
+        u0 = np.ascontiguousarray(u0, np.float64)
+        n = u0.size
+        uf = np.empty(n)
+        dr = np.empty(max(steps, 1))
+        bl = np.empty(max(steps, 1), np.int64)
+        comp = c_int()
+        st = self.lib.ref_evolve(u0.ctypes.data, n, tau, drift, None if v is None else v.ctypes.data, t0, steps,
+                                 eta, engine, uf.ctypes.data, dr.ctypes.data, bl.ctypes.data, ctypes.byref(comp))
+        if st:
+            raise RuntimeError(self.err())
+        return uf, dr[:steps], bl[:steps], bool(comp.value)
+
+    def split_step_2d(self, u, tau, d1, d2, pot_kind=0, t=0.0, periodic=True):
+        u = np.ascontiguousarray(u, np.float64)
+        n1, n2 = u.shape
+        out = np.empty_like(u)
+        st = self.lib.ref_split_step_2d(u.ctypes.data, n1, n2, n1, tau, d1, d2, pot_kind, t, int(periodic),
+                                        out.ctypes.data)
+        if st:
+            raise RuntimeError(self.err())
+        return out
+
+    def decompose(self, v, eta=0.0):
+        v = np.ascontiguousarray(v, np.float64)
+        cap = v.size + 1
+        kinds = np.empty(cap, np.int32)
+        starts = np.empty(cap, np.int64)
+        ends = np.empty(cap, np.int64)
+        c = self.lib.ref_decompose(v.ctypes.data, v.size, eta, kinds.ctypes.data, starts.ctypes.data,
+                                   ends.ctypes.data, cap)
+        return int(c), kinds[:c], starts[:c], ends[:c]
+
+    def conv(self, which, a, b, eta=0.0):
+        a = np.ascontiguousarray(a, np.float64)
+        b = np.ascontiguousarray(b, np.float64)
+        out = np.empty(a.size + b.size - 1)
+        blocks = c_int64()
+        st = self.lib.ref_conv(which, a.ctypes.data, a.size, b.ctypes.data, b.size, eta, out.ctypes.data,
+                               ctypes.byref(blocks))
+        return out, blocks.value, st
+
+
+_ORC = None
+
+
+def oracle():
+    global _ORC
+    if _ORC is None:
+        if not os.path.exists(ORACLE_SO):
+            _build_oracle()
+        _ORC = Oracle(ctypes.CDLL(ORACLE_SO))
+    return _ORC
+
+
+def reference():
+    if not os.path.exists(REF_SO) and os.path.isdir("/root/reference/proj/src"):
+        subprocess.run(["make", "-s", "-f", os.path.join(ROOT, "oracle", "Makefile"), "ref"], check=True, cwd=ROOT)
+    if not os.path.exists(REF_SO):
+        return None
+    return Reference(ctypes.CDLL(REF_SO))

@@ -1,0 +1,151 @@
+"""K2 (fast exact min-plus) parity on the B200.
+
+Gate: |fast - oracle| <= 1e-12 * max(1, max|u_ref|) per
+element; in practice the walk finds the exact-real minimiser, so results
+are expected bit-identical, which is asserted where the oracle can run."""
+import numpy as np
+import pytest
+
+from paper_1210_4090_b200 import api
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def to_dev(x):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def fast_step(dev, u, drifts, tau, tv=None, blocks=False, ws=None, flags=0):
+    import torch
+    lines, n = u.shape
+    du = to_dev(u) if isinstance(u, np.ndarray) else u
+    out = torch.empty_like(du)
+    if ws is None:
+        ws = torch.empty(dev.fast_workspace_bytes(lines, n), dtype=torch.uint8, device="cuda")
+    db = torch.empty(lines, dtype=torch.int64, device="cuda") if blocks else None
+    dev.fast_f64(du, out, to_dev(np.broadcast_to(np.asarray(drifts, np.float64), (lines,)).copy()), tau,
+                 tv=None if tv is None else to_dev(tv), blocks=db, workspace=ws, flags=flags)
+    torch.cuda.synchronize()
+    return out, (db.cpu().numpy() if blocks else None)
+
+
+def oracle_step(orc, u, drifts, tau, tv=None):
+    lines, n = u.shape
+    outs = []
+    for l in range(lines):
+        d = float(np.broadcast_to(drifts, (lines,))[l])
+        K, first, _, _ = orc.kernel(n, tau, d)
+        outs.append(orc.direct(u[l:l + 1], K, first, tv=tv)[0])
+    return np.stack(outs)
+
+
+def assert_close(got, want):
+    scale = max(1.0, float(np.max(np.abs(want))))
+    err = float(np.max(np.abs(got - want)))
+    assert err <= TOL * scale, err
+    return err
+
+
+@pytest.mark.parametrize("drift", [0.0, 0.4, -0.7, 1.0])
+@pytest.mark.parametrize("n,tau", [(24, 0.25), (48, 0.125), (600, 0.04), (1024, 0.05), (4096, 0.01)])
+def test_fast_random_vs_oracle(dev, orc, n, tau, drift):
+    rng = np.random.default_rng(n + int(drift * 10))
+    u = rng.uniform(-1, 1, (4, n))
+    got, blocks = fast_step(dev, u, drift, tau, blocks=True)
+    want = oracle_step(orc, u, drift, tau)
+    assert np.array_equal(got.cpu().numpy(), want)
+    assert [orc.line_blocks(u[l]) for l in range(4)] == list(blocks)
+
+
+def test_fast_c3_lines_bit_exact(dev, orc):
+    n = 4096
+    u = api.gen_c3_lines(0, 32, n)
+    got, blocks = fast_step(dev, u, 0.0, 0.01, blocks=True)
+    want = oracle_step(orc, u, 0.0, 0.01)
+    assert np.array_equal(got.cpu().numpy(), want)
+    assert list(blocks) == [orc.line_blocks(u[l]) for l in range(32)]
+
+
+def test_fast_c1_full_evolve_matches_reference(dev, orc, ref):
+    """C1 in full: N=1024, tau=0.05, P=0.5, V=cos(2 pi x), u0=sin(2 pi x),
+    2000 steps; final state and H-bar against the reference itself."""
+    import torch
+    n, tau, steps = 1024, 0.05, 2000
+    u0 = api.gen_sin(n)
+    v = api.gen_potential(1, n)
+    tv = api.tau_v(v, tau)
+    uf_ref, drift_ref, blocks_ref, comp = ref.evolve(u0, tau, 0.5, v, steps, engine=0)
+    assert comp
+    for engine in (api.ENGINE_FAST, api.ENGINE_DIRECT):
+        u = to_dev(u0[None, :])
+        scratch = torch.empty_like(u)
+        sd = torch.empty(steps, dtype=torch.float64, device="cuda")
+        sb = torch.empty(steps, dtype=torch.int64, device="cuda")
+        ws = torch.empty(dev.fast_workspace_bytes(1, n), dtype=torch.uint8, device="cuda")
+        done = dev.evolve(u, scratch, to_dev(np.array([0.5])), tau, steps, tv=to_dev(tv), engine=engine,
+                          step_drift=sd, step_blocks=sb, workspace=ws)
+        assert done == steps
+        uf = u.cpu().numpy()[0]
+        assert np.array_equal(uf, uf_ref)
+        assert np.array_equal(sb.cpu().numpy(), blocks_ref)
+        assert np.max(np.abs(sd.cpu().numpy() - drift_ref)) <= 1e-12
+        hbar = np.sum(uf - u0) / n / (steps * tau)  # mean(u_T - u_0)/T
+        hbar_ref = np.sum(uf_ref - u0) / n / (steps * tau)
+        assert abs(hbar - hbar_ref) <= 1e-12 * abs(hbar_ref)
+
+
+def test_fast_c2_slice_vs_oracle(dev, orc):
+    """C2 shape: N=65536, tau=0.02, per-line P, V = cos(2 pi x)+0.5 cos(4 pi x+1),
+    u0 = 0.  Run 30 fast steps on 8 lines spanning P in [-2, 2]; the oracle
+    checks step 30 from the GPU's step-29 state (per-step parity)."""
+    import torch
+    n, tau = 65536, 0.02
+    drifts = api.gen_c2_drifts(256)[[0, 40, 90, 127, 128, 170, 220, 255]]
+    tv = api.tau_v(api.gen_potential(2, n), tau)
+    u = torch.zeros((8, n), dtype=torch.float64, device="cuda")
+    ws = torch.empty(dev.fast_workspace_bytes(8, n), dtype=torch.uint8, device="cuda")
+    dd, dtv = to_dev(drifts), to_dev(tv)
+    prev = None
+    for i in range(30):
+        out = torch.empty_like(u)
+        dev.fast_f64(u, out, dd, tau, tv=dtv, workspace=ws, flags=api.FAST_STATS_VALID if i else 0)
+        prev, u = u, out
+    torch.cuda.synchronize()
+    want = oracle_step(orc, prev.cpu().numpy(), drifts, tau, tv=tv)
+    assert np.array_equal(u.cpu().numpy(), want)
+
+
+def test_fast_equals_direct_c5_shape(dev, orc):
+    """C5 shape (N=2^20, tau=0.005, P=0.25, V=0.5 sin(2 pi x)) on 2 seeded lines:
+    one fast step vs the oracle (exact)."""
+    n, tau = 1 << 20, 0.005
+    u = api.gen_c5_lines(0, 2, n)
+    tv = api.tau_v(api.gen_potential(3, n), tau)
+    got, blocks = fast_step(dev, u, 0.25, tau, tv=tv, blocks=True)
+    K, first, _, _ = orc.kernel(n, tau, 0.25)
+    # the oracle's O(N^2) is too slow at 2^20 for all outputs: check a strided subset
+    want = oracle_step_subset(orc, u, K, first, tv, stride=4093)
+    g = got.cpu().numpy()
+    for l in range(2):
+        idx, vals = want[l]
+        assert np.array_equal(g[l, idx], vals)
+    assert list(blocks) == [orc.line_blocks(u[l]) for l in range(2)]
+
+
+def oracle_step_subset(orc, u, K, first, tv, stride):
+    """Definition-level outputs at j = 0, stride, 2 stride, ... (exact)."""
+    res = []
+    n = u.shape[1]
+    W = 2 * n + 1
+    for l in range(u.shape[0]):
+        idx = np.arange(0, n, stride)
+        vals = []
+        for j in idx:
+            ys = (j - first - np.arange(W)) % n
+            c = u[l, ys] + K
+            vals.append(np.min(c) - tv[j])
+        res.append((idx, np.array(vals)))
+    return res
