@@ -2,6 +2,8 @@
 // Validation mirrors the reference's InvalidInput checks
 // (proj/src/scheme.cpp:18-24,39-53; proj/src/grid_fn.cpp:11-22).
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 

@@ -21,6 +21,8 @@
 // DADD + DSETP + 2x FSEL and nothing else (R^2 candidates per R LDS.64 of u
 // and R broadcast LDS of K).  u is padded one double per R in shared memory
 // so the stride-R per-thread reads are bank-conflict free.
+#include <cstdlib>
+
 #include "lob_internal.cuh"
 
 namespace lob {
@@ -58,7 +60,7 @@ __device__ __forceinline__ float pos_inf<float>() {
 }
 
 template <int R>
-__device__ __forceinline__ int padded(int i) {
+__host__ __device__ __forceinline__ constexpr int padded(int i) {
     return i + i / R;
 }
 
