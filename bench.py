@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""Benchmark: Lax-Oleinik grid-point updates/s (fp64) on B200.
+
+Workload (BASELINE.json configs[1], "C2"): 256 independent periodic lines of
+N = 65536, per-line drift P_l = -2 + 4 l/255, tau = 0.02,
+V = cos(2 pi x) + 0.5 cos(4 pi x + 1), u0 = 0.  One bench step = one fully
+discrete Lax-Oleinik step of all 256 lines (min-plus with the kinetic kernel
++ potential + the block-count statistics step_fully_discrete reports), run by
+the K2 fast exact engine, device-resident (u^{n+1} feeds the next step).
+The state is first evolved `--presteps` steps (untimed) so the timed steps
+see a developed, kinked solution like the bulk of C2's 5000 steps.
+Working set 2 x 134 MB > 126 MB L2, so no L2 flush is needed.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref,
+the laxol library built from its sources) on the box's host cores.
+
+Prints ONE JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Lax-Oleinik grid-point updates/s (fp64) at 1 GPU; % of FP64/HBM roofline"
+N_SPACE, LINES, TAU = 65536, 256, 0.02
+WORKLOAD = "C2: 256 lines x N=65536, P in [-2,2], tau=0.02, V=cos(2pi x)+0.5cos(4pi x+1), u0=0"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--presteps", type=int, default=1000)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-extras", action="store_true", help="skip the per-kernel extra measurements")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q, "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 7:
+                for k, nm in enumerate(names):
+                    if r[3 + k].lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        backend = "nccl" if args.impl == "b200" else "gloo"
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend, rank=rank, world_size=world,
+                                device_id=None if backend == "gloo" else None)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def allreduce_max(x: float, world: int, device=None) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- reference arm
+def cpu_reference_rate(lines_sample: int, nthreads: int, engine: int = 1):
+    """One step of `lines_sample` C2 lines through the reference library
+    (oracle/_ref; step_fully_discrete per line on a std::thread pool).
+    Returns (updates/s, seconds, sample description)."""
+    from tests import _oracle
+
+    ref = _oracle.reference()
+    if ref is None:
+        return None
+    from paper_1210_4090_b200 import api
+
+    drifts = api.gen_c2_drifts(LINES)
+    idx = np.linspace(0, LINES - 1, lines_sample).round().astype(int)
+    v = api.gen_potential(2, N_SPACE)
+    rng = np.random.default_rng(0)
+    # the Naive engine's cost is data independent; a rough state stands in
+    u = np.cumsum(rng.uniform(-1.0 / N_SPACE, 1.0 / N_SPACE, (lines_sample, N_SPACE)), axis=1)
+    u -= np.linspace(0, 1, N_SPACE)[None, :] * u[:, -1:]
+    t0 = time.perf_counter()
+    ref.step_lines(u, TAU, drifts[idx], v=v, engine=engine, nthreads=nthreads)
+    dt = time.perf_counter() - t0
+    return lines_sample * N_SPACE / dt, dt, f"{lines_sample} C2 lines x 1 step, ConvEngine::Naive, {nthreads} threads"
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    nthreads = os.cpu_count() or 1
+    lines_sample = max(1, min(nthreads, 64))
+    rates, times = [], []
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference_rate(lines_sample, nthreads)
+        if r is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref (reference build) missing"}))
+            return
+        if i >= args.warmup:
+            rates.append(r[0])
+            times.append(r[1])
+    value = float(np.median(rates))
+    line = {"metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": float(np.median(times)) * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": WORKLOAD, "engine": "reference laxol ConvEngine::Naive (CPU)"},
+            "cpu_baseline": {"value": value, "unit": "updates/s", "cores": nthreads, "kind": "reference",
+                             "sample": r[2]},
+            "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------------------- b200 arm
+def run_b200(args, world, rank, local):
+    import torch
+
+    from paper_1210_4090_b200 import api
+
+    torch.cuda.set_device(local)
+    dev = api.Device(local)
+    stream = torch.cuda.current_stream()
+    drifts = torch.from_numpy(api.gen_c2_drifts(LINES)).cuda()
+    tv_h = api.tau_v(api.gen_potential(2, N_SPACE), TAU)
+    tv = torch.from_numpy(tv_h).cuda()
+    a = torch.zeros((LINES, N_SPACE), dtype=torch.float64, device="cuda")
+    b = torch.empty_like(a)
+    blocks = torch.empty(LINES, dtype=torch.int64, device="cuda")
+    ws = torch.empty(dev.fast_workspace_bytes(LINES, N_SPACE), dtype=torch.uint8, device="cuda")
+    st = {"cur": a, "nxt": b, "i": 0}
+
+    def step():
+        dev.fast_f64(st["cur"], st["nxt"], drifts, TAU, tv=tv, blocks=blocks, workspace=ws,
+                     flags=api.FAST_STATS_VALID if st["i"] else 0, stream=stream)
+        st["cur"], st["nxt"] = st["nxt"], st["cur"]
+        st["i"] += 1
+
+    for _ in range(args.presteps + args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = dev.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    launches = dev.launches - launches0
+    clk = clocks.stop()
+    barrier(world)
+    ms_max = allreduce_max(ms, world, device="cuda")
+    updates = LINES * N_SPACE * args.steps * world
+    value = updates / (ms_max * 1e-3)
+    hbm_peak, peak_kind = measured_peaks()
+    per_launch_s = (ms / 1e3) / args.steps  # one fast_kernel launch per step
+    achieved = LINES * N_SPACE * 16 / per_launch_s / 1e9
+    finite = bool(torch.isfinite(st["cur"]).all().item())
+    blocks_mean = float(blocks.double().mean().item())
+
+    # ---- e2e: the host-buffer C-ABI entry (H2D + step + D2H every step) ----
+    e2e = None
+    if rank == 0 or world > 1:
+        uh = torch.empty((LINES, N_SPACE), dtype=torch.float64, pin_memory=True)
+        uh.copy_(st["cur"])
+        oh = torch.empty_like(uh, pin_memory=True)
+        bh = np.empty(LINES, np.int64)
+        dh = api.gen_c2_drifts(LINES)
+        un, on = uh.numpy(), oh.numpy()
+        e2e_steps = max(1, min(args.steps, 10))
+        dev.step_host(un, dh, TAU, tv=tv_h, out=on, blocks=bh)  # warm
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            dev.step_host(un, dh, TAU, tv=tv_h, out=on, blocks=bh)
+            un, on = on, un
+        dt = time.perf_counter() - t0
+        dt = allreduce_max(dt, world, device="cuda")
+        e2e = {"value": LINES * N_SPACE * e2e_steps * world / dt, "unit": "updates/s",
+               "h2d_bytes_per_step": int(LINES * N_SPACE * 8 + LINES * 8 + N_SPACE * 8),
+               "d2h_bytes_per_step": int(LINES * N_SPACE * 8 + LINES * 8),
+               "steps": e2e_steps, "api": "lob_step_host_f64 (pinned host buffers)"}
+
+    if rank != 0:
+        return
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "k2_c2_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded C2 generators, include/laxol_b200_configs.h)",
+        "config": {"workload": WORKLOAD, "engine": "K2 fast exact min-plus (LOB_ENGINE_FAST)",
+                   "presteps": args.presteps, "lines_per_gpu": LINES, "n": N_SPACE,
+                   "l2": "working set 268 MB > 126 MB L2 (no flush needed)",
+                   "parallelism": f"line-sharded replicas x{world}", "state_finite": finite,
+                   "mean_blocks_per_line": blocks_mean},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_update": 16},
+        "clocks": clk, "gpu_launches": int(launches), "e2e": e2e,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        nthreads = os.cpu_count() or 1
+        r = cpu_reference_rate(max(1, min(nthreads, 64)), nthreads)
+        if r is not None:
+            line["cpu_baseline"] = {"value": r[0], "unit": "updates/s", "cores": nthreads, "kind": "reference",
+                                    "sample": r[2], "seconds": r[1]}
+    if not args.no_extras and world == 1:
+        line["kernels"] = extras(dev)
+    print(json.dumps(line))
+
+
+def extras(dev):
+    """Secondary measurements: K1 direct (C3) against the FP64 pipe, K2 on C3/C5."""
+    import torch
+
+    from paper_1210_4090_b200 import api
+
+    out = {}
+    fp = dev.bench_fp64()
+    out["fp64_pipe_measured"] = fp
+    ev = lambda: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))  # noqa: E731
+
+    def timeit(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        s, e = ev()
+        s.record()
+        for _ in range(reps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / reps * 1e-3
+
+    n = 4096
+    K = dev.build_kernel(n, 0.01, 0.0)
+    u = torch.from_numpy(api.gen_c3_lines(0, 4096, n)).cuda()
+    o = torch.empty_like(u)
+    dk = torch.from_numpy(K.window).cuda()
+    df = torch.full((4096,), K.first, dtype=torch.int64, device="cuda")
+    t = timeit(lambda: dev.direct_f64(u, o, dk, df), 5)
+    cand = 4096 * 4096 * (2 * n + 1)
+    out["k1_direct_c3_f64"] = {
+        "ms": t * 1e3, "updates_per_s": 4096 * 4096 / t, "cand_per_s": cand / t,
+        "roofline": {"bound": "fp64 pipe", "ops_per_candidate": 2, "achieved_ops": 2 * cand / t,
+                     "peak_ops": fp["dadd_ops_per_s"], "frac": 2 * cand / t / fp["dadd_ops_per_s"],
+                     "frac_of_minplus_mix_peak": cand / t / fp["minplus_cand_per_s"]}}
+    u32, o32, dk32 = u.float(), torch.empty_like(u.float()), dk.float()
+    t = timeit(lambda: dev.direct_f32(u32, o32, dk32, df), 5)
+    out["k1_direct_c3_f32"] = {"ms": t * 1e3, "updates_per_s": 4096 * 4096 / t, "cand_per_s": cand / t}
+    ws = torch.empty(dev.fast_workspace_bytes(4096, n), dtype=torch.uint8, device="cuda")
+    z = torch.zeros(4096, dtype=torch.float64, device="cuda")
+    t = timeit(lambda: dev.fast_f64(u, o, z, 0.01, workspace=ws), 10)
+    out["k2_fast_c3"] = {"ms": t * 1e3, "updates_per_s": 4096 * 4096 / t,
+                         "hbm_frac": 4096 * 4096 * 16 / t / 1e9 / measured_peaks()[0]}
+    return out
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_b200(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
