@@ -100,6 +100,12 @@ int lob_minplus_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lin
                          double eta, int64_t* blocks, void* workspace, size_t workspace_bytes,
                          int flags, void* stream);
 
+/* Number of fast-engine outputs (cumulative over calls with this workspace)
+ * for which the local-minimum walk produced no candidate and the exact
+ * direct scan was used instead; 0 in correct operation (tests assert it). */
+int lob_fast_diagnostics(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n,
+                         uint64_t* missed_outputs);
+
 /* K3 — split_step_nd (proj/src/splitting.cpp:37-99) for a periodic n x n
  * row-major tensor: sweep axis 0 (columns, kernel 1), sweep axis 1 (rows,
  * kernel 2), then subtract tau*V once.  The potential is the separable
@@ -135,9 +141,10 @@ int lob_step_host_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines,
                       const double* drift, double tau, const double* tv, int64_t tv_stride,
                       double eta, int engine, int64_t* blocks);
 
-/* Kernel window of mechanical(drift) built on the device (for checking
- * against build_kernel): window[2n+1], first, argmin, and the
- * fast path's slope-estimate tolerance delta (in displacement units). */
+/* Kernel window of mechanical(drift) built on the host exactly as
+ * build_kernel does (proj/src/scheme.cpp:59-105): window[2n+1], first,
+ * argmin, and the fast path's slope-inversion tolerance delta (in
+ * displacement units).  ctx may be NULL. */
 int lob_kernel_mech_host(lob_ctx* ctx, int64_t n, double tau, double drift, double* window,
                          int64_t* first, int64_t* argmin, double* delta);
 

@@ -168,6 +168,12 @@ class Device:
                                            _ptr(workspace), ws_bytes, int(flags), _stream_ptr(stream))
         self._check(st, "lob_minplus_fast_f64")
 
+    def fast_diagnostics(self, workspace, lines: int, n: int) -> int:
+        v = ctypes.c_uint64()
+        st = self.lib.lob_fast_diagnostics(self.ctx, _ptr(workspace), lines, n, ctypes.byref(v))
+        self._check(st, "lob_fast_diagnostics")
+        return int(v.value)
+
     def split_step_2d(self, u, out, tmp, tau, drift1, drift2, a1=None, a2=None, b=0.0,
                       engine=ENGINE_DIRECT, workspace=None, stream=None):
         n = u.shape[0]

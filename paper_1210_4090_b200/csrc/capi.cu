@@ -146,6 +146,12 @@ int lob_minplus_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lin
                            workspace_bytes, flags, static_cast<cudaStream_t>(stream));
 }
 
+int lob_fast_diagnostics(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n,
+                         uint64_t* missed_outputs) {
+    if (!ctx || !workspace || !missed_outputs) return LOB_INVALID_INPUT;
+    return fast_diag_count(ctx, workspace, lines, n, missed_outputs, ctx->stream);
+}
+
 int lob_block_counts(lob_ctx* ctx, const double* u, int64_t lines, int64_t n, double eta,
                      int64_t* blocks, void* stream) {
     int st = check_lines(ctx, lines, n, "lob_block_counts");

@@ -18,21 +18,27 @@
 //     z(s) = (s + P eps)/a,
 // where delta bounds the table's rounding (csrc/host/kernel_build.cpp).
 // Window-edge minima are excluded by checking osc(u) < K(edge) - K(min)
-// (else the tile falls back to the direct scan).  The intervals of a
-// locally convex run tile the outputs contiguously (the paper's convex
-// merge, Lemma 4.1 / Algorithm 1); concave kinks leave empty intervals and
-// fold the walk back (Algorithm 2's envelope), and the overlaps are resolved
-// by an exact min.  Total candidates ~ n + TV+(s)/a per line.
+// (else the tile falls back to the direct scan).  Inside a locally convex
+// run the intervals tile the outputs contiguously (the slope merge of the
+// paper's Algorithm 1 / Lemma 4.1); concave kinks leave empty intervals and
+// fold the walk back (Algorithm 2's envelope); overlaps resolve by an exact
+// min.  Total candidates ~ n + TV+(s)/a per line.
 //
-// Layout: a CTA owns a tile of T outputs of one line.  Per-tile statistics
-// of u (min/max of u and of its slopes, and the decomposition FSM summary)
-// are produced by the previous step's epilogue (or by stats_kernel) and
-// tell each CTA which source tiles can reach its outputs.  Candidates are
-// combined with shared-memory atomicMin on order-preserving 64-bit keys.
-// The epilogue applies out = best - tv (one rounding), writes u^{n+1}
-// coalesced, and computes the statistics of u^{n+1} for the next step,
-// including the block count of decompose() (proj/src/minplus.cpp:152-188)
-// as a 3-state transition function per tile.
+// Layout and data flow (one launch per step, device resident):
+//  * a CTA (256 threads) owns T = 2048 consecutive outputs of one line;
+//  * statistics of u from the previous step's epilogue: per 256-sample
+//    sub-tile slope bounds, per-tile decompose() FSM summary, and per-line
+//    min/max of u and of its slopes (global 64-bit atomics on
+//    order-preserving keys, three rotating buffers);
+//  * the CTA bounds its source range with the line stats, keeps only the
+//    sub-tiles whose slope-implied displacements reach its outputs, stages
+//    U (chunks of 2048 + halo) and the K values it needs in shared memory,
+//    and emits candidates into shared 64-bit keys (exact min);
+//  * the epilogue writes u^{n+1} = best - tv coalesced and produces the
+//    statistics of u^{n+1} for the next step, including decompose()'s block
+//    count (proj/src/minplus.cpp:152-188) as a composable 3-state
+//    transition summary per tile.
+#include <climits>
 #include <cmath>
 #include <cstring>
 
@@ -40,110 +46,97 @@
 
 namespace lob {
 
-constexpr int kTile = 2048;  // outputs (and sources) per tile
-constexpr int kThreads = 512;
-constexpr int kMaxSrcList = 2048;
-
-// decompose() FSM: states U=0, Cx=1, Cc=2; summary for each entry state.
-struct TileStats {
-    double umin, umax, smin, smax;
-    unsigned short cnt[3];
-    unsigned char exit[3];
-    unsigned char pad;
-};
-static_assert(sizeof(TileStats) == 48, "TileStats layout");
+constexpr int kT = 2048;       // outputs per CTA tile
+constexpr int kNT = 256;       // threads per CTA
+constexpr int kG = 256;        // sub-tile (slope statistics granularity)
+constexpr int kSub = kT / kG;  // sub-tiles per tile (= warps per CTA)
+constexpr int kPer = kT / kNT; // outputs / sources per thread
+constexpr int kKCap = 4096;    // K values staged in shared memory
+static_assert(kSub == kNT / 32, "one warp per sub-tile in the epilogue");
 
 struct FastParams {
     int64_t n;
-    int64_t tiles;
-    int64_t T;
+    int64_t tiles;  // ceil(n / kT)
+    int64_t subs;   // ceil(n / kG)
     double tau;
     double eta;
     const double* vtab;  // v_d for d in [-vofs, vofs]
     int64_t vofs;
 };
 
+struct FastBuffers {
+    const double2* sub_in;  // [lines][subs] (min, max) of s over the sub-tile + left halo
+    const unsigned long long* fsm_in;   // [lines][tiles]
+    const unsigned long long* line_in;  // [lines][4] keys: umin, umax, smin, smax
+    double2* sub_out;
+    unsigned long long* fsm_out;
+    unsigned long long* line_out;
+    unsigned long long* line_reset;
+};
+
 namespace {
 
-__device__ __forceinline__ double kval(const double* vtab, int64_t vofs, int64_t d, double drift,
-                                       double tau) {
-    const double v = vtab[d + vofs];
+__device__ __forceinline__ double kval_v(double v, double drift, double tau) {
     // tau * ((0.5*v)*v - drift*v): proj/src/scheme.cpp:80 + hamiltonian.cpp:43
     return __dmul_rn(tau, __dsub_rn(__dmul_rn(__dmul_rn(0.5, v), v), __dmul_rn(drift, v)));
 }
+__device__ __forceinline__ double kval(const double* vtab, int64_t vofs, int64_t d, double drift,
+                                       double tau) {
+    return kval_v(vtab[d + vofs], drift, tau);
+}
 
-// FSM step for one increment (proj/src/minplus.cpp:161-187).
+// ---- decompose() FSM (proj/src/minplus.cpp:161-187) ------------------------
+// Classes: 0 pos (inc > eta), 1 neg (inc < -eta), 2 zero band, 3 NaN.
+// States: 0 undetermined, 1 convex, 2 concave.  A "vector" packs the current
+// state of the three runs started in U, Cx, Cc (2 bits each); the LUT maps
+// (vector, class) -> next vector | emits<<6 (one bit per run).
 __device__ __forceinline__ int fsm_class(double inc, double eta) {
-    if (inc > eta) return 0;     // pos
-    if (inc < -eta) return 1;    // neg
-    if (inc == inc) return 2;    // zero band
-    return 3;                    // NaN
+    return inc > eta ? 0 : (inc < -eta ? 1 : (inc == inc ? 2 : 3));
 }
-__device__ __forceinline__ void fsm_step(int& q, int& emits, int c) {
+__host__ __device__ inline int fsm_next(int q, int c, int* emit) {
     if (q == 0) {
-        q = c == 0 ? 1 : (c == 1 ? 2 : 0);
-    } else if (q == 1) {
-        if (c == 1 || c == 3) {
-            q = 0;
-            ++emits;
-        }
-    } else {
-        if (c == 0 || c == 3) {
-            q = 0;
-            ++emits;
-        }
+        *emit = 0;
+        return c == 0 ? 1 : (c == 1 ? 2 : 0);
     }
+    if (q == 1) {
+        *emit = (c == 1 || c == 3) ? 1 : 0;
+        return *emit ? 0 : 1;
+    }
+    *emit = (c == 0 || c == 3) ? 1 : 0;
+    return *emit ? 0 : 2;
 }
 
-struct Fsm3 {
-    int exit[3];
+// packed summary: bits 0..5 exit states of the 3 runs, bits 16.. counts (3 x 16 bits)
+__device__ __forceinline__ unsigned long long fsm_pack(int v, const int* cnt) {
+    return static_cast<unsigned long long>(v) | (static_cast<unsigned long long>(cnt[0]) << 16) |
+           (static_cast<unsigned long long>(cnt[1]) << 32) |
+           (static_cast<unsigned long long>(cnt[2]) << 48);
+}
+__device__ __forceinline__ unsigned long long fsm_identity() { return 0u | (1u << 2) | (2u << 4); }
+// compose summaries: a then b
+__device__ __forceinline__ unsigned long long fsm_compose(unsigned long long a, unsigned long long b) {
+    int v = 0;
     int cnt[3];
-};
-__device__ __forceinline__ Fsm3 fsm_compose(const Fsm3& a, const Fsm3& b) {
-    Fsm3 r;
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-        const int m = a.exit[q];
-        r.exit[q] = b.exit[m];
-        r.cnt[q] = a.cnt[q] + b.cnt[m];
+        const int m = static_cast<int>((a >> (2 * q)) & 3);
+        v |= static_cast<int>((b >> (2 * m)) & 3) << (2 * q);
+        cnt[q] = static_cast<int>((a >> (16 + 16 * q)) & 0xffff) +
+                 static_cast<int>((b >> (16 + 16 * m)) & 0xffff);
     }
-    return r;
-}
-__device__ __forceinline__ Fsm3 fsm_identity() {
-    Fsm3 r;
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-        r.exit[q] = q;
-        r.cnt[q] = 0;
-    }
-    return r;
+    return fsm_pack(v, cnt);
 }
 
-// Block-wide ordered composition of per-thread FSM summaries.
-__device__ Fsm3 block_fsm(Fsm3 f, Fsm3* sh) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // inclusive ordered reduction within the warp (lane order preserved)
+__constant__ unsigned short c_fsm_lut[64 * 4];
+
+__device__ __forceinline__ unsigned long long warp_fsm(unsigned long long f) {
+    const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-        Fsm3 o;
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            o.exit[q] = __shfl_down_sync(0xffffffffu, f.exit[q], off);
-            o.cnt[q] = __shfl_down_sync(0xffffffffu, f.cnt[q], off);
-        }
+        const unsigned long long o = __shfl_down_sync(0xffffffffu, f, off);
         if ((lane & (2 * off - 1)) == 0 && lane + off < 32) f = fsm_compose(f, o);
     }
-    if (lane == 0) sh[warp] = f;
-    __syncthreads();
-    Fsm3 r = fsm_identity();
-    if (threadIdx.x == 0) {
-        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) r = fsm_compose(r, sh[w]);
-        sh[0] = r;
-    }
-    __syncthreads();
-    r = sh[0];
-    __syncthreads();
-    return r;
+    return f;  // valid in lane 0
 }
 
 __device__ __forceinline__ double warp_min(double x) {
@@ -156,101 +149,142 @@ __device__ __forceinline__ double warp_max(double x) {
     for (int o = 16; o; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
     return x;
 }
+__device__ __forceinline__ long long warp_min_ll(long long x) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x = min(x, __shfl_xor_sync(0xffffffffu, x, o));
+    return x;
+}
+__device__ __forceinline__ long long warp_max_ll(long long x) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
+    return x;
+}
 
-// Block reduce of (min, max, min, max) into sh4[0..3].
-__device__ void block_minmax4(double a, double b, double c, double d, double* sh) {
-    a = warp_min(a);
-    b = warp_max(b);
-    c = warp_min(c);
-    d = warp_max(d);
+struct EpiShared {
+    double red[4][kNT / 32];
+    unsigned long long fsm[kNT / 32];
+};
+
+// Statistics of u^{n+1} (or of an input u) for the tile whose values are
+// vals[i] = u(j0 - 1 + i), i = 0 .. Tl + 2 (periodic), Tl = tile length.
+// Warp w owns sub-tile w; thread t owns increments e = j0 + 1 + t*kPer ...
+__device__ void tile_epilogue_stats(const double* vals, int Tl, int64_t j0, int64_t line,
+                                    int64_t tile, const FastParams& p, const FastBuffers& b,
+                                    EpiShared& sh) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    __syncthreads();
-    if (lane == 0) {
-        sh[4 * warp + 0] = a;
-        sh[4 * warp + 1] = b;
-        sh[4 * warp + 2] = c;
-        sh[4 * warp + 3] = d;
+    {
+        // sub-tile q covers sources [qG, qG+len); its slopes s(qG-1 .. qG+len-1)
+        // are vals[i+1]-vals[i] for i = start .. start+len (start = r*G)
+        const int start = warp * kG;
+        double smn = INFINITY, smx = -INFINITY;
+        if (start < Tl) {
+            const int len = min(kG, Tl - start);
+            for (int i = start + lane; i <= start + len; i += 32) {
+                const double s = __dsub_rn(vals[i + 1], vals[i]);
+                if (s == s) {
+                    smn = fmin(smn, s);
+                    smx = fmax(smx, s);
+                } else {
+                    smn = -INFINITY;
+                    smx = INFINITY;
+                }
+            }
+            smn = warp_min(smn);
+            smx = warp_max(smx);
+            if (lane == 0) {
+                const int64_t q = (j0 + start) / kG;
+                b.sub_out[line * p.subs + q] = make_double2(smn, smx);
+            }
+        }
+        double umn = INFINITY, umx = -INFINITY;
+        for (int i = 1 + threadIdx.x; i <= Tl; i += kNT) {
+            const double v = vals[i];
+            if (isfinite(v)) {
+                umn = fmin(umn, v);
+                umx = fmax(umx, v);
+            } else {
+                umn = -INFINITY;
+                umx = INFINITY;
+            }
+        }
+        umn = warp_min(umn);
+        umx = warp_max(umx);
+        if (lane == 0) {
+            sh.red[0][warp] = umn;
+            sh.red[1][warp] = umx;
+            sh.red[2][warp] = smn;
+            sh.red[3][warp] = smx;
+        }
+    }
+    {
+        // decompose() FSM over increments e = j0+1 .. j0+Tl (e <= n-1);
+        // inc(e) = s(e) - s(e-1) with s(e) = vals[e-j0+2] - vals[e-j0+1]
+        int v = 0 | (1 << 2) | (2 << 4);
+        int cnt[3] = {0, 0, 0};
+        const int i_lo = 1 + threadIdx.x * kPer;
+#pragma unroll
+        for (int m = 0; m < kPer; ++m) {
+            const int i = i_lo + m;  // e = j0 + i
+            if (i <= Tl && j0 + i <= p.n - 1) {
+                const double inc = __dsub_rn(__dsub_rn(vals[i + 2], vals[i + 1]),
+                                             __dsub_rn(vals[i + 1], vals[i]));
+                const int x = c_fsm_lut[v * 4 + fsm_class(inc, p.eta)];
+                v = x & 63;
+                cnt[0] += (x >> 6) & 1;
+                cnt[1] += (x >> 7) & 1;
+                cnt[2] += (x >> 8) & 1;
+            }
+        }
+        const unsigned long long f = warp_fsm(fsm_pack(v, cnt));
+        if (lane == 0) sh.fsm[warp] = f;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
-            sh[0] = fmin(sh[0], sh[4 * w + 0]);
-            sh[1] = fmax(sh[1], sh[4 * w + 1]);
-            sh[2] = fmin(sh[2], sh[4 * w + 2]);
-            sh[3] = fmax(sh[3], sh[4 * w + 3]);
+        double umn = INFINITY, umx = -INFINITY, smn = INFINITY, smx = -INFINITY;
+        unsigned long long f = fsm_identity();
+        for (int w = 0; w < kNT / 32; ++w) {
+            umn = fmin(umn, sh.red[0][w]);
+            umx = fmax(umx, sh.red[1][w]);
+            smn = fmin(smn, sh.red[2][w]);
+            smx = fmax(smx, sh.red[3][w]);
+            f = fsm_compose(f, sh.fsm[w]);
         }
-    }
-    __syncthreads();
-}
-
-// Statistics of a tile whose values are vals[0 .. Tl+1] (vals[i] = u(j0+i),
-// periodic), shared by the stats kernel and the K2 epilogue.
-__device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t n, double eta,
-                           TileStats* dst, double* shred, Fsm3* shfsm) {
-    double umin = INFINITY, umax = -INFINITY, smin = INFINITY, smax = -INFINITY;
-    for (int i = threadIdx.x; i < Tl; i += blockDim.x) {
-        const double v = vals[i];
-        const double s = __dsub_rn(vals[i + 1], v);
-        umin = fmin(umin, v);
-        umax = fmax(umax, v);
-        smin = fmin(smin, s);
-        smax = fmax(smax, s);
-        if (!isfinite(v) || !isfinite(s)) {  // non-finite: the next step falls back
-            umin = -INFINITY;
-            umax = INFINITY;
-        }
-    }
-    // increments e = j0+i, i in [1, Tl], e <= n-1, each thread a contiguous chunk
-    const int per = (Tl + blockDim.x - 1) / blockDim.x;
-    const int i_lo = 1 + threadIdx.x * per;
-    const int i_hi = min(Tl, i_lo + per - 1);
-    Fsm3 f;
-    for (int q = 0; q < 3; ++q) {
-        int st = q, em = 0;
-        for (int i = i_lo; i <= i_hi; ++i) {
-            if (j0 + i > n - 1) break;
-            const double inc = __dsub_rn(__dsub_rn(vals[i + 1], vals[i]), __dsub_rn(vals[i], vals[i - 1]));
-            fsm_step(st, em, fsm_class(inc, eta));
-        }
-        f.exit[q] = st;
-        f.cnt[q] = em;
-    }
-    f = block_fsm(f, shfsm);
-    block_minmax4(umin, umax, smin, smax, shred);
-    if (threadIdx.x == 0) {
-        TileStats ts;
-        ts.umin = shred[0];
-        ts.umax = shred[1];
-        ts.smin = shred[2];
-        ts.smax = shred[3];
-        for (int q = 0; q < 3; ++q) {
-            ts.cnt[q] = static_cast<unsigned short>(f.cnt[q]);
-            ts.exit[q] = static_cast<unsigned char>(f.exit[q]);
-        }
-        ts.pad = 0;
-        *dst = ts;
+        b.fsm_out[line * p.tiles + tile] = f;
+        unsigned long long* L = b.line_out + line * 4;
+        atomicMin(L + 0, dkey(umn));
+        atomicMax(L + 1, dkey(umx));
+        atomicMin(L + 2, dkey(smn));
+        atomicMax(L + 3, dkey(smx));
     }
 }
 
-__global__ void __launch_bounds__(kThreads) stats_kernel(const double* __restrict__ u,
-                                                         TileStats* __restrict__ stats,
-                                                         FastParams p) {
-    __shared__ double vals[kTile + 2];
-    __shared__ double shred[4 * (kThreads / 32)];
-    __shared__ Fsm3 shfsm[kThreads / 32];
+__global__ void __launch_bounds__(kNT) stats_kernel(const double* __restrict__ u, FastParams p,
+                                                    FastBuffers b) {
+    __shared__ double vals[kT + 3];
+    __shared__ EpiShared sh;
     const int64_t line = blockIdx.x / p.tiles;
     const int64_t tile = blockIdx.x - line * p.tiles;
-    const int64_t j0 = tile * p.T;
-    const int Tl = static_cast<int>(min(p.T, p.n - j0));
+    const int64_t j0 = tile * kT;
+    const int Tl = static_cast<int>(min(static_cast<int64_t>(kT), p.n - j0));
     const double* ul = u + line * p.n;
-    for (int i = threadIdx.x; i < Tl + 2; i += blockDim.x) {
-        int64_t j = j0 + i;
+    for (int i = threadIdx.x; i < Tl + 3; i += kNT) {
+        int64_t j = j0 - 1 + i;
+        if (j < 0) j += p.n;
         if (j >= p.n) j -= p.n;
         if (j >= p.n) j -= p.n;
         vals[i] = ul[j];
     }
     __syncthreads();
-    tile_stats(vals, Tl, j0, p.n, p.eta, stats + blockIdx.x, shred, shfsm);
+    tile_epilogue_stats(vals, Tl, j0, line, tile, p, b, sh);
+}
+
+__global__ void line_init_kernel(unsigned long long* L, int64_t lines) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= lines) return;
+    L[4 * i + 0] = ~0ull;
+    L[4 * i + 1] = 0ull;
+    L[4 * i + 2] = ~0ull;
+    L[4 * i + 3] = 0ull;
 }
 
 __global__ void build_vtab_kernel(double* vtab, int64_t vofs, double eps, double tau) {
@@ -261,77 +295,97 @@ __global__ void build_vtab_kernel(double* vtab, int64_t vofs, double eps, double
     vtab[i] = __ddiv_rn(__dmul_rn(static_cast<double>(d), eps), tau);
 }
 
-__global__ void combine_blocks_kernel(const TileStats* __restrict__ st, int64_t lines,
+__global__ void combine_blocks_kernel(const unsigned long long* __restrict__ fsm, int64_t lines,
                                       int64_t tiles, int64_t* __restrict__ blocks) {
     const int64_t line = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (line >= lines) return;
     int q = 0;
     int64_t em = 0;
     for (int64_t t = 0; t < tiles; ++t) {
-        em += st[line * tiles + t].cnt[q];
-        q = st[line * tiles + t].exit[q];
+        const unsigned long long f = fsm[line * tiles + t];
+        em += (f >> (16 + 16 * q)) & 0xffff;
+        q = static_cast<int>((f >> (2 * q)) & 3);
     }
     blocks[line] = 1 + em;
 }
 
-// Main K2 kernel.
-__global__ void __launch_bounds__(kThreads) fast_kernel(
-    const double* __restrict__ u, double* __restrict__ out, const TileStats* __restrict__ st_in,
-    TileStats* __restrict__ st_out, const double* __restrict__ drift_arr,
+struct MainShared {
+    unsigned long long keys[kT + 3];
+    double ubuf[kT + 3];
+    double Ks[kKCap];
+    EpiShared epi;
+    long long ya, yb, dlo, dhi;
+};
+
+__device__ __forceinline__ void smem_atomic_min(unsigned long long* addr, unsigned long long key) {
+    unsigned long long old = *addr;
+    while (key < old) {
+        const unsigned long long prev = atomicCAS(addr, old, key);
+        if (prev == old) break;
+        old = prev;
+    }
+}
+
+// Main K2 kernel: one CTA = (line, tile of kT outputs).
+__global__ void __launch_bounds__(kNT, 3) fast_kernel(
+    const double* __restrict__ u, double* __restrict__ out, const double* __restrict__ drift_arr,
     const double* __restrict__ tv, int64_t tv_stride, int64_t* __restrict__ blocks_out,
-    unsigned long long* __restrict__ diag, FastParams p) {
-    __shared__ unsigned long long keys[kTile + 2];
-    __shared__ double ubuf[kTile + 2];
-    __shared__ int srclist[kMaxSrcList];
-    __shared__ int nsrc;
-    __shared__ int fallback;
-    __shared__ double shred[4 * (kThreads / 32)];
-    __shared__ Fsm3 shfsm[kThreads / 32];
+    unsigned long long* __restrict__ diag, FastParams p, FastBuffers b) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    MainShared& S = *reinterpret_cast<MainShared*>(smem_raw);
 
     const int64_t n = p.n;
     const int64_t line = blockIdx.x / p.tiles;
     const int64_t tile = blockIdx.x - line * p.tiles;
-    const int64_t j0 = tile * p.T;
-    const int Tl = static_cast<int>(min(p.T, n - j0));
-    const int64_t j1 = j0 + Tl + 1;  // last (unrolled) output this CTA evaluates
+    const int64_t j0 = tile * kT;
+    const int Tl = static_cast<int>(min(static_cast<int64_t>(kT), n - j0));
+    const long long jlo = j0 - 1;  // outputs evaluated: jlo .. jhi (unrolled)
+    const long long jhi = j0 + Tl + 1;
     const double* ul = u + line * n;
-    const TileStats* sl = st_in + line * p.tiles;
     const double drift = drift_arr[line];
     const double tau = p.tau;
+    const int tid = threadIdx.x, lane = tid & 31;
 
-    // ---- per-line kernel constants (identical arithmetic to the host) ----
+    // ---- per-line kernel constants (same IEEE operations as the host) ----
     const double eps = __ddiv_rn(1.0, static_cast<double>(n));
     const int64_t center = llround(__ddiv_rn(__dmul_rn(tau, drift), eps));
     const int64_t first = center - n;
-    const int64_t dmin_w = first + 1, dmax_w = first + 2 * n - 1;  // interior of the window
+    const int64_t dmin_w = first + 1, dmax_w = first + 2 * n - 1;  // window interior
     const double a = __ddiv_rn(__dmul_rn(eps, eps), tau);
     const double ia = __ddiv_rn(1.0, a);
     const double pe = __dmul_rn(drift, eps);
-    double delta;
+    double hl, hr;  // dL = ceil(z + hl), dR = floor(z + hr)
     {
-        const double uu = 1.1102230246251565e-16;  // 2^-53
+        const double uu = 1.1102230246251565e-16;
         const double dm = fmax(fabs(static_cast<double>(first)), fabs(static_cast<double>(first + 2 * n)));
         const double vmax = dm * eps / tau;
         const double kmag = tau * (0.5 * vmax * vmax + fabs(drift) * vmax);
-        delta = 32.0 * uu * kmag / a + 8.0 * uu * (2.0 * n + fabs(drift) * eps / a) + 1e-9;
-        delta = delta * 2.0;  // device-side margin on top of the host bound
+        double delta = 32.0 * uu * kmag / a + 8.0 * uu * (2.0 * n + fabs(drift) * eps / a) + 1e-9;
+        delta *= 2.0;
+        hl = -0.5 - delta;
+        hr = 0.5 + delta;
     }
 
-    if (threadIdx.x == 0) {
-        nsrc = 0;
-        fallback = 0;
+    for (int i = tid; i < Tl + 3; i += kNT) S.keys[i] = kKeyInf;
+    // reset the line statistics buffer two steps ahead
+    if (tile == 0 && tid < 4) b.line_reset[line * 4 + tid] = (tid & 1) ? 0ull : ~0ull;
+    if (blocks_out && tile == 0 && tid == 0) {
+        int q = 0;
+        int64_t em = 0;
+        for (int64_t t = 0; t < p.tiles; ++t) {
+            const unsigned long long f = b.fsm_in[line * p.tiles + t];
+            em += (f >> (16 + 16 * q)) & 0xffff;
+            q = static_cast<int>((f >> (2 * q)) & 3);
+        }
+        blocks_out[line] = 1 + em;
     }
-    for (int i = threadIdx.x; i < Tl + 2; i += blockDim.x) keys[i] = kKeyInf;
 
-    // ---- line-wide oscillation, window-edge gap ----
-    double lo = INFINITY, hi = -INFINITY;
-    for (int64_t t = threadIdx.x; t < p.tiles; t += blockDim.x) {
-        lo = fmin(lo, sl[t].umin);
-        hi = fmax(hi, sl[t].umax);
-    }
-    block_minmax4(lo, hi, 0.0, 0.0, shred);
-    const double umin = shred[0], umax = shred[1];
-    __syncthreads();
+    // ---- line statistics: oscillation gate and global displacement bounds ----
+    const unsigned long long* L = b.line_in + line * 4;
+    const double umin = dkey_inv(L[0]), umax = dkey_inv(L[1]);
+    const double smin = dkey_inv(L[2]), smax = dkey_inv(L[3]);
+    bool ok;
+    long long DLg = dmin_w, DRg = dmax_w;
     {
         const double kfirst = kval(p.vtab, p.vofs, first, drift, tau);
         const double klast = kval(p.vtab, p.vofs, first + 2 * n, drift, tau);
@@ -340,102 +394,126 @@ __global__ void __launch_bounds__(kThreads) fast_kernel(
             if (d >= first && d <= first + 2 * n) kmin = fmin(kmin, kval(p.vtab, p.vofs, d, drift, tau));
         const double gap = fmin(kfirst, klast) - kmin;
         const double osc = umax - umin;
-        const bool ok = (osc * (1.0 + 1e-12) < gap * (1.0 - 1e-12)) && n >= 3;
-        if (!ok && threadIdx.x == 0) fallback = 1;
-    }
-
-    // ---- block count of the INPUT u (decompose on the closed period) ----
-    if (blocks_out && tile == 0 && threadIdx.x == 0) {
-        int q = 0;
-        int64_t em = 0;
-        for (int64_t t = 0; t < p.tiles; ++t) {
-            em += sl[t].cnt[q];
-            q = sl[t].exit[q];
+        ok = (osc * (1.0 + 1e-12) < gap * (1.0 - 1e-12)) && n >= 3 && isfinite(smin) && isfinite(smax);
+        if (ok) {
+            const double zl = ceil(__dmul_rn(__dadd_rn(smin, pe), ia) + hl);
+            const double zr = floor(__dmul_rn(__dadd_rn(smax, pe), ia) + hr);
+            DLg = static_cast<long long>(fmax(zl, static_cast<double>(dmin_w)));
+            DRg = static_cast<long long>(fmin(zr, static_cast<double>(dmax_w)));
+            ok = DLg <= DRg;
         }
-        blocks_out[line] = 1 + em;
     }
-    __syncthreads();
 
-    // unrolled source range that can reach outputs [j0, j1]
-    const int64_t ylo = j0 - dmax_w, yhi = j1 - dmin_w;
-    const int64_t k_lo = (ylo >= 0) ? ylo / n : -((-ylo + n - 1) / n);
-    const int64_t k_hi = (yhi >= 0) ? yhi / n : -((-yhi + n - 1) / n);
-    if (!fallback) {
-        // ---- which (unrolled) source tiles can reach outputs [j0, j1]? ----
-        const int64_t ncand = (k_hi - k_lo + 1) * p.tiles;
-        for (int64_t c = threadIdx.x; c < ncand; c += blockDim.x) {
-            const int64_t k = k_lo + c / p.tiles;
-            const int64_t sg = c - (c / p.tiles) * p.tiles;
-            const int64_t sgp = sg == 0 ? p.tiles - 1 : sg - 1;
-            const double smn = fmin(sl[sg].smin, sl[sgp].smin);
-            const double smx = sl[sg].smax;
-            double zl = ceil(__dmul_rn(__dadd_rn(smn, pe), ia) - 0.5 - delta);
-            double zr = floor(__dmul_rn(__dadd_rn(smx, pe), ia) + 0.5 + delta);
-            zl = fmax(zl, static_cast<double>(dmin_w));
-            zr = fmin(zr, static_cast<double>(dmax_w));
-            if (!(zl <= zr)) continue;
-            const int64_t ys = k * n + sg * p.T;
-            const int64_t ye = ys + min(p.T, n - sg * p.T) - 1;
-            if (ys + static_cast<int64_t>(zl) <= j1 && ye + static_cast<int64_t>(zr) >= j0) {
-                const int slot = atomicAdd(&nsrc, 1);
-                if (slot < kMaxSrcList)
-                    srclist[slot] = static_cast<int>(c);
-                else
-                    fallback = 1;
+    if (ok) {
+        // ---- candidate sub-tiles: unrolled sources y in [jlo - DRg, jhi - DLg] ----
+        const long long y0 = jlo - DRg, y1 = jhi - DLg;
+        const long long k0 = y0 >= 0 ? y0 / n : -((-y0 + n - 1) / n);
+        const long long Q0 = k0 * p.subs + (y0 - k0 * n) / kG;
+        const long long k1 = y1 >= 0 ? y1 / n : -((-y1 + n - 1) / n);
+        const long long Q1 = k1 * p.subs + (y1 - k1 * n) / kG;
+        long long ya = LLONG_MAX, yb = LLONG_MIN, dlo = LLONG_MAX, dhi = LLONG_MIN;
+        for (long long Q = Q0 + tid; Q <= Q1; Q += kNT) {
+            const long long k = Q >= 0 ? Q / p.subs : -((-Q + p.subs - 1) / p.subs);
+            const long long q = Q - k * p.subs;
+            const double2 sb = b.sub_in[line * p.subs + q];
+            const long long ys = k * n + q * kG;
+            const long long ye = ys + min(static_cast<long long>(kG), static_cast<long long>(n - q * kG)) - 1;
+            const double zl = ceil(__dmul_rn(__dadd_rn(sb.x, pe), ia) + hl);
+            const double zr = floor(__dmul_rn(__dadd_rn(sb.y, pe), ia) + hr);
+            const long long dl = static_cast<long long>(fmax(zl, static_cast<double>(DLg)));
+            const long long dr = static_cast<long long>(fmin(zr, static_cast<double>(DRg)));
+            if (dl <= dr && ys + dl <= jhi && ye + dr >= jlo) {
+                ya = min(ya, ys);
+                yb = max(yb, ye);
+                dlo = min(dlo, dl);
+                dhi = max(dhi, dr);
             }
+        }
+        ya = warp_min_ll(ya);
+        yb = warp_max_ll(yb);
+        dlo = warp_min_ll(dlo);
+        dhi = warp_max_ll(dhi);
+        if (tid == 0) {
+            S.ya = LLONG_MAX;
+            S.yb = LLONG_MIN;
+            S.dlo = LLONG_MAX;
+            S.dhi = LLONG_MIN;
         }
         __syncthreads();
-    }
-
-    if (!fallback) {
-        const int ns = nsrc;
-        for (int li = 0; li < ns; ++li) {
-            const int64_t c = srclist[li];
-            const int64_t k = k_lo + c / p.tiles;
-            const int64_t sg = c - (c / p.tiles) * p.tiles;
-            const int64_t ys = k * n + sg * p.T;
-            const int Ts = static_cast<int>(min(p.T, n - sg * p.T));
-            __syncthreads();
-            // U(ys-1 .. ys+Ts) -> ubuf[0 .. Ts+1]
-            const int64_t base = ys - 1;
-            int64_t bm = base % n;
-            if (bm < 0) bm += n;
-            for (int i = threadIdx.x; i < Ts + 2; i += blockDim.x) {
-                int64_t yy = bm + i;
-                if (yy >= n) yy -= n;
-                if (yy >= n) yy -= n;
-                ubuf[i] = ul[yy];
-            }
-            __syncthreads();
-            for (int i = threadIdx.x; i < Ts; i += blockDim.x) {
-                const double uy = ubuf[i + 1];
-                const double sp = __dsub_rn(uy, ubuf[i]);      // s(y-1)
-                const double sn = __dsub_rn(ubuf[i + 2], uy);  // s(y)
-                double zl = ceil(__dmul_rn(__dadd_rn(sp, pe), ia) - 0.5 - delta);
-                double zr = floor(__dmul_rn(__dadd_rn(sn, pe), ia) + 0.5 + delta);
-                const int64_t y = ys + i;
-                zl = fmax(zl, fmax(static_cast<double>(dmin_w), static_cast<double>(j0 - y)));
-                zr = fmin(zr, fmin(static_cast<double>(dmax_w), static_cast<double>(j1 - y)));
-                if (!(zl <= zr)) continue;
-                const int64_t dl = static_cast<int64_t>(zl), dr = static_cast<int64_t>(zr);
-                for (int64_t d = dl; d <= dr; ++d) {
-                    const double c2 = __dadd_rn(uy, kval(p.vtab, p.vofs, d, drift, tau));
-                    atomicMin(&keys[y + d - j0], dkey(c2));
+        if (lane == 0) {
+            atomicMin(&S.ya, ya);
+            atomicMax(&S.yb, yb);
+            atomicMin(&S.dlo, dlo);
+            atomicMax(&S.dhi, dhi);
+        }
+        __syncthreads();
+        ya = S.ya;
+        yb = S.yb;
+        if (ya <= yb) {
+            dlo = max(S.dlo, jlo - yb);
+            dhi = min(S.dhi, jhi - ya);
+            const bool kglob = dhi - dlo + 1 > kKCap;
+            // ---- stage K(d), d in [dlo, dhi] (exact build_kernel arithmetic) ----
+            if (!kglob)
+                for (long long d = dlo + tid; d <= dhi; d += kNT)
+                    S.Ks[d - dlo] = kval(p.vtab, p.vofs, d, drift, tau);
+            // ---- sources in chunks of kT ----
+            for (long long yc = ya; yc <= yb; yc += kT) {
+                const int clen = static_cast<int>(min(static_cast<long long>(kT), yb - yc + 1));
+                __syncthreads();
+                // U(yc-1 .. yc+clen) -> ubuf[0 .. clen+1]
+                const long long base = yc - 1;
+                int bm = static_cast<int>(base % n);
+                if (bm < 0) bm += static_cast<int>(n);
+                for (int i = tid; i < clen + 2; i += kNT) {
+                    int yy = bm + i;
+                    if (yy >= n) yy -= static_cast<int>(n);
+                    if (yy >= n) yy -= static_cast<int>(n);
+                    S.ubuf[i] = ul[yy];
+                }
+                __syncthreads();
+                const int i0 = tid * kPer;
+                if (i0 < clen) {
+                    double uv[kPer + 2];
+#pragma unroll
+                    for (int m = 0; m < kPer + 2; ++m) uv[m] = S.ubuf[min(i0 + m, clen + 1)];
+                    double z[kPer + 1];
+#pragma unroll
+                    for (int m = 0; m < kPer + 1; ++m)
+                        z[m] = __dmul_rn(__dadd_rn(__dsub_rn(uv[m + 1], uv[m]), pe), ia);
+#pragma unroll
+                    for (int m = 0; m < kPer; ++m) {
+                        if (i0 + m < clen) {
+                            const long long y = yc + i0 + m;
+                            const double uy = uv[m + 1];
+                            long long dl = static_cast<long long>(fmax(ceil(z[m] + hl), static_cast<double>(DLg)));
+                            long long dr = static_cast<long long>(fmin(floor(z[m + 1] + hr), static_cast<double>(DRg)));
+                            dl = max(dl, jlo - y);
+                            dr = min(dr, jhi - y);
+                            for (long long d = dl; d <= dr; ++d) {
+                                const double kd = kglob ? kval(p.vtab, p.vofs, d, drift, tau) : S.Ks[d - dlo];
+                                smem_atomic_min(&S.keys[y + d - jlo], dkey(__dadd_rn(uy, kd)));
+                            }
+                        }
+                    }
                 }
             }
         }
     }
     __syncthreads();
 
-    // ---- epilogue: exact min -> out, with direct fallback where needed ----
+    // ---- epilogue: exact min -> u^{n+1}; direct scan where nothing landed ----
     const double* tvl = tv ? tv + line * tv_stride : nullptr;
-    for (int i = threadIdx.x; i < Tl + 2; i += blockDim.x) {
-        int64_t j = j0 + i;
+    double* vals = S.ubuf;  // reuse: vals[i] = u^{n+1}(jlo + i), i = 0 .. Tl+2
+    for (int i = tid; i < Tl + 3; i += kNT) {
+        int64_t j = jlo + i;
+        if (j < 0) j += n;
         if (j >= n) j -= n;
         if (j >= n) j -= n;
         double best;
-        if (fallback || keys[i] == kKeyInf) {
-            if (!fallback && diag) atomicAdd(diag, 1ull);
+        const unsigned long long kk = S.keys[i];
+        if (kk == kKeyInf) {
+            if (ok && diag) atomicAdd(diag, 1ull);
             // direct scan of the full window (proj/tests/unit_scheme.cpp:184-190)
             best = INFINITY;
             int64_t y = (j - first) % n;
@@ -446,22 +524,57 @@ __global__ void __launch_bounds__(kThreads) fast_kernel(
                 y = y == 0 ? n - 1 : y - 1;
             }
         } else {
-            best = dkey_inv(keys[i]);
+            best = dkey_inv(kk);
         }
         const double o = tvl ? __dsub_rn(best, tvl[j]) : best;
-        ubuf[i] = o;
-        if (i < Tl) out[line * n + j] = o;
+        vals[i] = o;
+        if (i >= 1 && i <= Tl) out[line * n + j] = o;
     }
     __syncthreads();
-    if (st_out) tile_stats(ubuf, Tl, j0, n, p.eta, st_out + blockIdx.x, shred, shfsm);
+    tile_epilogue_stats(vals, Tl, j0, line, tile, p, b, S.epi);
 }
 
 }  // namespace
 
-size_t fast_workspace_bytes(int64_t lines, int64_t n) {
-    const int64_t T = n < kTile ? n : kTile;
-    const int64_t tiles = (n + T - 1) / T;
-    return 2 * static_cast<size_t>(lines * tiles) * sizeof(TileStats) + 64;
+// ---------------------------------------------------------------------------
+// workspace: sub[2][lines][subs] double2 | fsm[2][lines][tiles] u64 |
+//            line[3][lines][4] u64 | diag u64
+struct WsLayout {
+    size_t sub, fsm, line, diag, total;
+};
+static WsLayout ws_layout(int64_t lines, int64_t n) {
+    const int64_t tiles = (n + kT - 1) / kT, subs = (n + kG - 1) / kG;
+    WsLayout w;
+    w.sub = 0;
+    w.fsm = w.sub + 2 * static_cast<size_t>(lines * subs) * sizeof(double2);
+    w.line = w.fsm + 2 * static_cast<size_t>(lines * tiles) * sizeof(unsigned long long);
+    w.diag = w.line + 3 * static_cast<size_t>(lines) * 4 * sizeof(unsigned long long);
+    w.total = w.diag + 64;
+    return w;
+}
+
+size_t fast_workspace_bytes(int64_t lines, int64_t n) { return ws_layout(lines, n).total; }
+
+static bool g_lut_ready = false;
+
+static int ensure_lut(lob_ctx* ctx) {
+    if (g_lut_ready) return LOB_OK;
+    unsigned short lut[64 * 4];
+    for (int v = 0; v < 64; ++v)
+        for (int c = 0; c < 4; ++c) {
+            int nv = 0, em = 0;
+            for (int q = 0; q < 3; ++q) {
+                const int st = (v >> (2 * q)) & 3;
+                int e = 0;
+                const int ns = st > 2 ? 0 : fsm_next(st, c, &e);
+                nv |= ns << (2 * q);
+                em |= e << q;
+            }
+            lut[v * 4 + c] = static_cast<unsigned short>(nv | (em << 6));
+        }
+    LOB_CUDA_TRY(ctx, cudaMemcpyToSymbol(c_fsm_lut, lut, sizeof(lut)));
+    g_lut_ready = true;
+    return LOB_OK;
 }
 
 static int ensure_vtab(lob_ctx* ctx, int64_t n, double tau, const double** out, int64_t* vofs,
@@ -487,60 +600,116 @@ static int ensure_vtab(lob_ctx* ctx, int64_t n, double tau, const double** out, 
     return LOB_OK;
 }
 
+static FastParams make_params(int64_t n, double tau, double eta) {
+    FastParams p{};
+    p.n = n;
+    p.tiles = (n + kT - 1) / kT;
+    p.subs = (n + kG - 1) / kG;
+    p.tau = tau;
+    p.eta = eta;
+    return p;
+}
+
+static FastBuffers make_buffers(void* ws, int64_t lines, int64_t n, int64_t counter) {
+    const WsLayout w = ws_layout(lines, n);
+    char* base = static_cast<char*>(ws);
+    const int64_t subs = (n + kG - 1) / kG, tiles = (n + kT - 1) / kT;
+    double2* sub = reinterpret_cast<double2*>(base + w.sub);
+    unsigned long long* fsm = reinterpret_cast<unsigned long long*>(base + w.fsm);
+    unsigned long long* line = reinterpret_cast<unsigned long long*>(base + w.line);
+    const int64_t c2 = counter % 2, c3 = counter % 3;
+    FastBuffers b;
+    b.sub_in = sub + c2 * lines * subs;
+    b.sub_out = sub + (1 - c2) * lines * subs;
+    b.fsm_in = fsm + c2 * lines * tiles;
+    b.fsm_out = fsm + (1 - c2) * lines * tiles;
+    b.line_in = line + c3 * lines * 4;
+    b.line_out = line + ((c3 + 1) % 3) * lines * 4;
+    b.line_reset = line + ((c3 + 2) % 3) * lines * 4;
+    return b;
+}
+
 int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
                     const double* drift, double tau, const double* tv, int64_t tv_stride,
                     double eta, int64_t* blocks, void* workspace, size_t ws_bytes, int flags,
                     cudaStream_t s) {
     if (ws_bytes < fast_workspace_bytes(lines, n) || !workspace)
         return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_fast_f64: workspace too small");
-    FastParams p;
-    p.n = n;
-    p.T = n < kTile ? n : kTile;
-    p.tiles = (n + p.T - 1) / p.T;
-    p.tau = tau;
-    p.eta = eta;
-    int st = ensure_vtab(ctx, n, tau, &p.vtab, &p.vofs, s);
+    if (n > (1ll << 30)) return set_error(ctx, LOB_INVALID_INPUT, "fast: n too large");
+    int st = ensure_lut(ctx);
+    if (st) return st;
+    FastParams p = make_params(n, tau, eta);
+    st = ensure_vtab(ctx, n, tau, &p.vtab, &p.vofs, s);
     if (st) return st;
     const int64_t nblk = lines * p.tiles;
     if (nblk > 0x7fffffffll) return set_error(ctx, LOB_INVALID_INPUT, "fast: grid too large");
-    TileStats* base = static_cast<TileStats*>(workspace);
-    int& parity = ctx->ws_parity[workspace];
     if (ctx->ws_shape[workspace] != std::make_pair(lines, n)) {
         ctx->ws_shape[workspace] = std::make_pair(lines, n);
         flags &= ~LOB_FAST_STATS_VALID;
     }
-    TileStats* sin = base + parity * nblk;
-    TileStats* sout = base + (1 - parity) * nblk;
+    int64_t& counter = ctx->ws_counter[workspace];
+    FastBuffers b = make_buffers(workspace, lines, n, counter);
+    const WsLayout w = ws_layout(lines, n);
     unsigned long long* diag =
-        reinterpret_cast<unsigned long long*>(base + 2 * nblk);
+        reinterpret_cast<unsigned long long*>(static_cast<char*>(workspace) + w.diag);
     if (!(flags & LOB_FAST_STATS_VALID)) {
-        stats_kernel<<<static_cast<unsigned>(nblk), kThreads, 0, s>>>(u, sin, p);
-        ctx->launches += 1;
+        // statistics of the given u into the "in" buffers; "out" line stats reset
+        FastBuffers sb = b;
+        sb.sub_out = const_cast<double2*>(b.sub_in);
+        sb.fsm_out = const_cast<unsigned long long*>(b.fsm_in);
+        sb.line_out = const_cast<unsigned long long*>(b.line_in);
+        const unsigned lb = static_cast<unsigned>((lines + 127) / 128);
+        line_init_kernel<<<lb, 128, 0, s>>>(const_cast<unsigned long long*>(b.line_in), lines);
+        line_init_kernel<<<lb, 128, 0, s>>>(b.line_out, lines);
+        stats_kernel<<<static_cast<unsigned>(nblk), kNT, 0, s>>>(u, p, sb);
+        ctx->launches += 3;
         LOB_CUDA_TRY(ctx, cudaGetLastError());
     }
-    fast_kernel<<<static_cast<unsigned>(nblk), kThreads, 0, s>>>(u, out, sin, sout, drift, tv,
-                                                                  tv_stride, blocks, diag, p);
+    static bool attr = false;
+    if (!attr) {
+        LOB_CUDA_TRY(ctx, cudaFuncSetAttribute(fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(sizeof(MainShared))));
+        attr = true;
+    }
+    fast_kernel<<<static_cast<unsigned>(nblk), kNT, sizeof(MainShared), s>>>(u, out, drift, tv, tv_stride,
+                                                                             blocks, diag, p, b);
     ctx->launches += 1;
     LOB_CUDA_TRY(ctx, cudaGetLastError());
-    parity = 1 - parity;
+    counter += 1;
+    return LOB_OK;
+}
+
+int fast_diag_count(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n, uint64_t* count,
+                    cudaStream_t s) {
+    const WsLayout w = ws_layout(lines, n);
+    unsigned long long v = 0;
+    LOB_CUDA_TRY(ctx, cudaMemcpyAsync(&v, static_cast<char*>(workspace) + w.diag, sizeof(v),
+                                      cudaMemcpyDeviceToHost, s));
+    LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    *count = v;
     return LOB_OK;
 }
 
 int launch_block_counts(lob_ctx* ctx, const double* u, int64_t lines, int64_t n, double eta,
                         int64_t* blocks, cudaStream_t s) {
-    FastParams p{};
-    p.n = n;
-    p.T = n < kTile ? n : kTile;
-    p.tiles = (n + p.T - 1) / p.T;
-    p.eta = eta;
+    int st = ensure_lut(ctx);
+    if (st) return st;
+    FastParams p = make_params(n, 1.0, eta);
     const int64_t nblk = lines * p.tiles;
-    TileStats* st = nullptr;
-    LOB_CUDA_TRY(ctx, cudaMallocAsync(&st, nblk * sizeof(TileStats), s));
-    stats_kernel<<<static_cast<unsigned>(nblk), kThreads, 0, s>>>(u, st, p);
-    combine_blocks_kernel<<<static_cast<unsigned>((lines + 127) / 128), 128, 0, s>>>(st, lines,
+    void* ws = nullptr;
+    const size_t bytes = fast_workspace_bytes(lines, n);
+    LOB_CUDA_TRY(ctx, cudaMallocAsync(&ws, bytes, s));
+    FastBuffers b = make_buffers(ws, lines, n, 0);
+    FastBuffers sb = b;
+    sb.sub_out = const_cast<double2*>(b.sub_in);
+    sb.fsm_out = const_cast<unsigned long long*>(b.fsm_in);
+    sb.line_out = const_cast<unsigned long long*>(b.line_in);
+    line_init_kernel<<<static_cast<unsigned>((lines + 127) / 128), 128, 0, s>>>(sb.line_out, lines);
+    stats_kernel<<<static_cast<unsigned>(nblk), kNT, 0, s>>>(u, p, sb);
+    combine_blocks_kernel<<<static_cast<unsigned>((lines + 127) / 128), 128, 0, s>>>(b.fsm_in, lines,
                                                                                      p.tiles, blocks);
-    ctx->launches += 2;
-    cudaFreeAsync(st, s);
+    ctx->launches += 3;
+    cudaFreeAsync(ws, s);
     return cuda_status(ctx, cudaGetLastError(), "block counts");
 }
 

@@ -24,7 +24,7 @@ struct lob_ctx {
     };
     std::map<std::pair<int64_t, uint64_t>, VTab> vtabs;
     // fast-engine workspaces: which statistics buffer holds the current u
-    std::map<const void*, int> ws_parity;
+    std::map<const void*, int64_t> ws_counter;
     std::map<const void*, std::pair<int64_t, int64_t>> ws_shape;
     // scratch for host entry points
     void* scratch = nullptr;
@@ -85,6 +85,8 @@ size_t fast_workspace_bytes(int64_t lines, int64_t n);
 int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
                     const double* drift, double tau, const double* tv, int64_t tv_stride,
                     double eta, int64_t* blocks, void* workspace, size_t ws_bytes, int flags,
+                    cudaStream_t s);
+int fast_diag_count(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n, uint64_t* count,
                     cudaStream_t s);
 int launch_block_counts(lob_ctx* ctx, const double* u, int64_t lines, int64_t n, double eta,
                         int64_t* blocks, cudaStream_t s);

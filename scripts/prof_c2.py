@@ -1,0 +1,26 @@
+"""C2 fast-path driver for ncu: evolve --pre steps, then --steps more."""
+import argparse
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_1210_4090_b200 import api  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--pre", type=int, default=300)
+ap.add_argument("--steps", type=int, default=2)
+ap.add_argument("--lines", type=int, default=256)
+a = ap.parse_args()
+n, tau, L = 65536, 0.02, a.lines
+dev = api.Device(0)
+dr = torch.from_numpy(api.gen_c2_drifts(256)[:L]).cuda()
+tv = torch.from_numpy(api.tau_v(api.gen_potential(2, n), tau)).cuda()
+x = torch.zeros((L, n), dtype=torch.float64, device="cuda")
+y = torch.empty_like(x)
+ws = torch.empty(dev.fast_workspace_bytes(L, n), dtype=torch.uint8, device="cuda")
+for i in range(a.pre + a.steps):
+    dev.fast_f64(x, y, dr, tau, tv=tv, workspace=ws, flags=api.FAST_STATS_VALID if i else 0)
+    x, y = y, x
+torch.cuda.synchronize()
+print("done", float(x.mean()))

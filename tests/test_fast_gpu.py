@@ -116,6 +116,7 @@ def test_fast_c2_slice_vs_oracle(dev, orc):
     torch.cuda.synchronize()
     want = oracle_step(orc, prev.cpu().numpy(), drifts, tau, tv=tv)
     assert np.array_equal(u.cpu().numpy(), want)
+    assert dev.fast_diagnostics(ws, 8, n) == 0  # every output found by the local-minimum walk
 
 
 def test_fast_equals_direct_c5_shape(dev, orc):
