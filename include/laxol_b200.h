@@ -91,8 +91,8 @@ int lob_minplus_window_f64(lob_ctx* ctx, const double* u, double* out, int64_t l
  * count of the INPUT u (what StepStats.block_count reports).
  * The workspace carries per-tile statistics of u between consecutive calls:
  * pass LOB_FAST_STATS_VALID when `u` is the `out` of the previous call with
- * the same workspace (the device-resident evolve loop), else 0 and the
- * statistics are recomputed (one extra read of u). */
+ * the same workspace, drift, tau and n (the device-resident evolve loop),
+ * else 0 and the statistics are recomputed (one extra read of u). */
 #define LOB_FAST_STATS_VALID 1
 int lob_fast_workspace_bytes(int64_t lines, int64_t n, size_t* bytes);
 int lob_minplus_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,

@@ -51,7 +51,16 @@ constexpr int kNT = 256;       // threads per CTA
 constexpr int kG = 256;        // sub-tile (slope statistics granularity)
 constexpr int kSub = kT / kG;  // sub-tiles per tile (= warps per CTA)
 constexpr int kPer = kT / kNT; // outputs / sources per thread
-constexpr int kKCap = 4096;    // K values staged in shared memory
+constexpr int kKCap = 2048;    // K values staged in shared memory
+constexpr int kQCap = 1024;    // queued long source intervals per chunk
+
+struct LineConst {
+    long long first;  // window displacement of w = 0
+    double pe;        // drift * eps
+    double hl, hr;    // dL = ceil(z + hl), dR = floor(z + hr), z = (s + pe)/a
+    double gap;       // min(K(first), K(first+2n)) - min K: the oscillation gate
+    double drift;
+};
 static_assert(kSub == kNT / 32, "one warp per sub-tile in the epilogue");
 
 struct FastParams {
@@ -60,6 +69,7 @@ struct FastParams {
     int64_t subs;   // ceil(n / kG)
     double tau;
     double eta;
+    double eps, a, ia;  // 1/n, eps^2/tau, 1/a (host IEEE, same as the device's)
     const double* vtab;  // v_d for d in [-vofs, vofs]
     int64_t vofs;
 };
@@ -162,7 +172,7 @@ __device__ __forceinline__ long long warp_max_ll(long long x) {
 
 struct EpiShared {
     double red[4][kNT / 32];
-    unsigned long long fsm[kNT / 32];
+    unsigned long long fsm[kNT];
 };
 
 // Statistics of u^{n+1} (or of an input u) for the tile whose values are
@@ -235,19 +245,26 @@ __device__ void tile_epilogue_stats(const double* vals, int Tl, int64_t j0, int6
                 cnt[2] += (x >> 8) & 1;
             }
         }
-        const unsigned long long f = warp_fsm(fsm_pack(v, cnt));
-        if (lane == 0) sh.fsm[warp] = f;
+        sh.fsm[threadIdx.x] = fsm_pack(v, cnt);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        // lane l composes summaries 8l .. 8l+7, then an ordered warp reduction
+        unsigned long long f = sh.fsm[lane * (kNT / 32)];
+#pragma unroll
+        for (int k = 1; k < kNT / 32; ++k) f = fsm_compose(f, sh.fsm[lane * (kNT / 32) + k]);
+        f = warp_fsm(f);
+        if (lane == 0) sh.fsm[0] = f;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         double umn = INFINITY, umx = -INFINITY, smn = INFINITY, smx = -INFINITY;
-        unsigned long long f = fsm_identity();
+        const unsigned long long f = sh.fsm[0];
         for (int w = 0; w < kNT / 32; ++w) {
             umn = fmin(umn, sh.red[0][w]);
             umx = fmax(umx, sh.red[1][w]);
             smn = fmin(smn, sh.red[2][w]);
             smx = fmax(smx, sh.red[3][w]);
-            f = fsm_compose(f, sh.fsm[w]);
         }
         b.fsm_out[line * p.tiles + tile] = f;
         unsigned long long* L = b.line_out + line * 4;
@@ -270,8 +287,7 @@ __global__ void __launch_bounds__(kNT) stats_kernel(const double* __restrict__ u
     for (int i = threadIdx.x; i < Tl + 3; i += kNT) {
         int64_t j = j0 - 1 + i;
         if (j < 0) j += p.n;
-        if (j >= p.n) j -= p.n;
-        if (j >= p.n) j -= p.n;
+        if (j >= p.n) j %= p.n;
         vals[i] = ul[j];
     }
     __syncthreads();
@@ -313,8 +329,10 @@ struct MainShared {
     unsigned long long keys[kT + 3];
     double ubuf[kT + 3];
     double Ks[kKCap];
+    int3 queue[kQCap];
     EpiShared epi;
-    long long ya, yb, dlo, dhi;
+    long long ya, yb;
+    int dlo, dhi, nq;
 };
 
 __device__ __forceinline__ void smem_atomic_min(unsigned long long* addr, unsigned long long key) {
@@ -326,9 +344,39 @@ __device__ __forceinline__ void smem_atomic_min(unsigned long long* addr, unsign
     }
 }
 
+// Per-line constants of the step (identical IEEE operations to the host's
+// build_kernel for first/center; the tolerance only needs to be a bound).
+__global__ void line_setup_kernel(const double* __restrict__ drift_arr, int64_t lines, FastParams p,
+                                  LineConst* __restrict__ lc) {
+    const int64_t line = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (line >= lines) return;
+    const int64_t n = p.n;
+    const double drift = drift_arr[line], tau = p.tau, eps = p.eps, a = p.a;
+    const int64_t center = llround(__ddiv_rn(__dmul_rn(tau, drift), eps));
+    const int64_t first = center - n;
+    const double uu = 1.1102230246251565e-16;
+    const double dm = fmax(fabs(static_cast<double>(first)), fabs(static_cast<double>(first + 2 * n)));
+    const double vmax = dm * eps / tau;
+    const double kmag = tau * (0.5 * vmax * vmax + fabs(drift) * vmax);
+    const double delta = 2.0 * (32.0 * uu * kmag / a + 8.0 * uu * (2.0 * n + fabs(drift) * eps / a) + 1e-9);
+    const double kfirst = kval(p.vtab, p.vofs, first, drift, tau);
+    const double klast = kval(p.vtab, p.vofs, first + 2 * n, drift, tau);
+    double kmin = INFINITY;
+    for (int64_t d = center - 2; d <= center + 2; ++d)
+        if (d >= first && d <= first + 2 * n) kmin = fmin(kmin, kval(p.vtab, p.vofs, d, drift, tau));
+    LineConst c;
+    c.first = first;
+    c.pe = __dmul_rn(drift, eps);
+    c.hl = -0.5 - delta;
+    c.hr = 0.5 + delta;
+    c.gap = fmin(kfirst, klast) - kmin;
+    c.drift = drift;
+    lc[line] = c;
+}
+
 // Main K2 kernel: one CTA = (line, tile of kT outputs).
 __global__ void __launch_bounds__(kNT, 3) fast_kernel(
-    const double* __restrict__ u, double* __restrict__ out, const double* __restrict__ drift_arr,
+    const double* __restrict__ u, double* __restrict__ out, const LineConst* __restrict__ lcs,
     const double* __restrict__ tv, int64_t tv_stride, int64_t* __restrict__ blocks_out,
     unsigned long long* __restrict__ diag, FastParams p, FastBuffers b) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -339,34 +387,18 @@ __global__ void __launch_bounds__(kNT, 3) fast_kernel(
     const int64_t tile = blockIdx.x - line * p.tiles;
     const int64_t j0 = tile * kT;
     const int Tl = static_cast<int>(min(static_cast<int64_t>(kT), n - j0));
-    const long long jlo = j0 - 1;  // outputs evaluated: jlo .. jhi (unrolled)
-    const long long jhi = j0 + Tl + 1;
+    const long long jlo = j0 - 1;  // outputs evaluated: jlo .. jlo + Tl + 2 (unrolled)
+    const int jspan = Tl + 2;      // relative output index range [0, jspan]
+    const long long jhi = jlo + jspan;
     const double* ul = u + line * n;
-    const double drift = drift_arr[line];
-    const double tau = p.tau;
-    const int tid = threadIdx.x, lane = tid & 31;
+    const LineConst lc = lcs[line];
+    const double tau = p.tau, ia = p.ia, pe = lc.pe, hl = lc.hl, hr = lc.hr;
+    const int64_t first = lc.first;
+    const int dmin_w = static_cast<int>(first + 1), dmax_w = static_cast<int>(first + 2 * n - 1);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-    // ---- per-line kernel constants (same IEEE operations as the host) ----
-    const double eps = __ddiv_rn(1.0, static_cast<double>(n));
-    const int64_t center = llround(__ddiv_rn(__dmul_rn(tau, drift), eps));
-    const int64_t first = center - n;
-    const int64_t dmin_w = first + 1, dmax_w = first + 2 * n - 1;  // window interior
-    const double a = __ddiv_rn(__dmul_rn(eps, eps), tau);
-    const double ia = __ddiv_rn(1.0, a);
-    const double pe = __dmul_rn(drift, eps);
-    double hl, hr;  // dL = ceil(z + hl), dR = floor(z + hr)
-    {
-        const double uu = 1.1102230246251565e-16;
-        const double dm = fmax(fabs(static_cast<double>(first)), fabs(static_cast<double>(first + 2 * n)));
-        const double vmax = dm * eps / tau;
-        const double kmag = tau * (0.5 * vmax * vmax + fabs(drift) * vmax);
-        double delta = 32.0 * uu * kmag / a + 8.0 * uu * (2.0 * n + fabs(drift) * eps / a) + 1e-9;
-        delta *= 2.0;
-        hl = -0.5 - delta;
-        hr = 0.5 + delta;
-    }
-
-    for (int i = tid; i < Tl + 3; i += kNT) S.keys[i] = kKeyInf;
+    for (int i = tid; i <= jspan; i += kNT) S.keys[i] = kKeyInf;
+    if (tid == 0) S.nq = 0;
     // reset the line statistics buffer two steps ahead
     if (tile == 0 && tid < 4) b.line_reset[line * 4 + tid] = (tid & 1) ? 0ull : ~0ull;
     if (blocks_out && tile == 0 && tid == 0) {
@@ -384,24 +416,13 @@ __global__ void __launch_bounds__(kNT, 3) fast_kernel(
     const unsigned long long* L = b.line_in + line * 4;
     const double umin = dkey_inv(L[0]), umax = dkey_inv(L[1]);
     const double smin = dkey_inv(L[2]), smax = dkey_inv(L[3]);
-    bool ok;
-    long long DLg = dmin_w, DRg = dmax_w;
-    {
-        const double kfirst = kval(p.vtab, p.vofs, first, drift, tau);
-        const double klast = kval(p.vtab, p.vofs, first + 2 * n, drift, tau);
-        double kmin = INFINITY;
-        for (int64_t d = center - 2; d <= center + 2; ++d)
-            if (d >= first && d <= first + 2 * n) kmin = fmin(kmin, kval(p.vtab, p.vofs, d, drift, tau));
-        const double gap = fmin(kfirst, klast) - kmin;
-        const double osc = umax - umin;
-        ok = (osc * (1.0 + 1e-12) < gap * (1.0 - 1e-12)) && n >= 3 && isfinite(smin) && isfinite(smax);
-        if (ok) {
-            const double zl = ceil(__dmul_rn(__dadd_rn(smin, pe), ia) + hl);
-            const double zr = floor(__dmul_rn(__dadd_rn(smax, pe), ia) + hr);
-            DLg = static_cast<long long>(fmax(zl, static_cast<double>(dmin_w)));
-            DRg = static_cast<long long>(fmin(zr, static_cast<double>(dmax_w)));
-            ok = DLg <= DRg;
-        }
+    int DLg = dmin_w, DRg = dmax_w;
+    const double osc = umax - umin;
+    bool ok = (osc * (1.0 + 1e-12) < lc.gap * (1.0 - 1e-12)) && n >= 3 && isfinite(smin) && isfinite(smax);
+    if (ok) {
+        DLg = max(__double2int_ru(__dmul_rn(__dadd_rn(smin, pe), ia) + hl), dmin_w);
+        DRg = min(__double2int_rd(__dmul_rn(__dadd_rn(smax, pe), ia) + hr), dmax_w);
+        ok = DLg <= DRg;
     }
 
     if (ok) {
@@ -411,17 +432,16 @@ __global__ void __launch_bounds__(kNT, 3) fast_kernel(
         const long long Q0 = k0 * p.subs + (y0 - k0 * n) / kG;
         const long long k1 = y1 >= 0 ? y1 / n : -((-y1 + n - 1) / n);
         const long long Q1 = k1 * p.subs + (y1 - k1 * n) / kG;
-        long long ya = LLONG_MAX, yb = LLONG_MIN, dlo = LLONG_MAX, dhi = LLONG_MIN;
+        long long ya = LLONG_MAX, yb = LLONG_MIN;
+        int dlo = INT_MAX, dhi = INT_MIN;
         for (long long Q = Q0 + tid; Q <= Q1; Q += kNT) {
             const long long k = Q >= 0 ? Q / p.subs : -((-Q + p.subs - 1) / p.subs);
             const long long q = Q - k * p.subs;
             const double2 sb = b.sub_in[line * p.subs + q];
             const long long ys = k * n + q * kG;
             const long long ye = ys + min(static_cast<long long>(kG), static_cast<long long>(n - q * kG)) - 1;
-            const double zl = ceil(__dmul_rn(__dadd_rn(sb.x, pe), ia) + hl);
-            const double zr = floor(__dmul_rn(__dadd_rn(sb.y, pe), ia) + hr);
-            const long long dl = static_cast<long long>(fmax(zl, static_cast<double>(DLg)));
-            const long long dr = static_cast<long long>(fmin(zr, static_cast<double>(DRg)));
+            const int dl = max(__double2int_ru(__dmul_rn(__dadd_rn(sb.x, pe), ia) + hl), DLg);
+            const int dr = min(__double2int_rd(__dmul_rn(__dadd_rn(sb.y, pe), ia) + hr), DRg);
             if (dl <= dr && ys + dl <= jhi && ye + dr >= jlo) {
                 ya = min(ya, ys);
                 yb = max(yb, ye);
@@ -431,13 +451,13 @@ __global__ void __launch_bounds__(kNT, 3) fast_kernel(
         }
         ya = warp_min_ll(ya);
         yb = warp_max_ll(yb);
-        dlo = warp_min_ll(dlo);
-        dhi = warp_max_ll(dhi);
+        dlo = static_cast<int>(warp_min_ll(dlo));
+        dhi = static_cast<int>(warp_max_ll(dhi));
         if (tid == 0) {
             S.ya = LLONG_MAX;
             S.yb = LLONG_MIN;
-            S.dlo = LLONG_MAX;
-            S.dhi = LLONG_MIN;
+            S.dlo = INT_MAX;
+            S.dhi = INT_MIN;
         }
         __syncthreads();
         if (lane == 0) {
@@ -450,25 +470,23 @@ __global__ void __launch_bounds__(kNT, 3) fast_kernel(
         ya = S.ya;
         yb = S.yb;
         if (ya <= yb) {
-            dlo = max(S.dlo, jlo - yb);
-            dhi = min(S.dhi, jhi - ya);
+            dlo = static_cast<int>(max(static_cast<long long>(S.dlo), jlo - yb));
+            dhi = static_cast<int>(min(static_cast<long long>(S.dhi), jhi - ya));
             const bool kglob = dhi - dlo + 1 > kKCap;
             // ---- stage K(d), d in [dlo, dhi] (exact build_kernel arithmetic) ----
             if (!kglob)
-                for (long long d = dlo + tid; d <= dhi; d += kNT)
-                    S.Ks[d - dlo] = kval(p.vtab, p.vofs, d, drift, tau);
+                for (int d = dlo + tid; d <= dhi; d += kNT) S.Ks[d - dlo] = kval(p.vtab, p.vofs, d, lc.drift, tau);
             // ---- sources in chunks of kT ----
             for (long long yc = ya; yc <= yb; yc += kT) {
                 const int clen = static_cast<int>(min(static_cast<long long>(kT), yb - yc + 1));
+                const int base = static_cast<int>(yc - jlo);  // jj = base + i + d
                 __syncthreads();
                 // U(yc-1 .. yc+clen) -> ubuf[0 .. clen+1]
-                const long long base = yc - 1;
-                int bm = static_cast<int>(base % n);
+                int bm = static_cast<int>((yc - 1) % n);
                 if (bm < 0) bm += static_cast<int>(n);
                 for (int i = tid; i < clen + 2; i += kNT) {
                     int yy = bm + i;
-                    if (yy >= n) yy -= static_cast<int>(n);
-                    if (yy >= n) yy -= static_cast<int>(n);
+                    if (yy >= n) yy = yy - static_cast<int>(n) < n ? yy - static_cast<int>(n) : yy % static_cast<int>(n);
                     S.ubuf[i] = ul[yy];
                 }
                 __syncthreads();
@@ -483,20 +501,47 @@ __global__ void __launch_bounds__(kNT, 3) fast_kernel(
                         z[m] = __dmul_rn(__dadd_rn(__dsub_rn(uv[m + 1], uv[m]), pe), ia);
 #pragma unroll
                     for (int m = 0; m < kPer; ++m) {
-                        if (i0 + m < clen) {
-                            const long long y = yc + i0 + m;
-                            const double uy = uv[m + 1];
-                            long long dl = static_cast<long long>(fmax(ceil(z[m] + hl), static_cast<double>(DLg)));
-                            long long dr = static_cast<long long>(fmin(floor(z[m + 1] + hr), static_cast<double>(DRg)));
-                            dl = max(dl, jlo - y);
-                            dr = min(dr, jhi - y);
-                            for (long long d = dl; d <= dr; ++d) {
-                                const double kd = kglob ? kval(p.vtab, p.vofs, d, drift, tau) : S.Ks[d - dlo];
-                                smem_atomic_min(&S.keys[y + d - jlo], dkey(__dadd_rn(uy, kd)));
+                        const int off = base + i0 + m;  // jj of d = 0
+                        int dl = max(max(__double2int_ru(z[m] + hl), DLg), -off);
+                        int dr = min(min(__double2int_rd(z[m + 1] + hr), DRg), jspan - off);
+                        if (i0 + m >= clen) dr = dl - 1;
+                        const double uy = uv[m + 1];
+                        // inline: the first two candidates; longer intervals are queued
+                        if (dl <= dr) {
+                            const double kd = kglob ? kval(p.vtab, p.vofs, dl, lc.drift, tau) : S.Ks[dl - dlo];
+                            smem_atomic_min(&S.keys[off + dl], dkey(__dadd_rn(uy, kd)));
+                        }
+                        if (dl + 1 <= dr) {
+                            const double kd = kglob ? kval(p.vtab, p.vofs, dl + 1, lc.drift, tau) : S.Ks[dl + 1 - dlo];
+                            smem_atomic_min(&S.keys[off + dl + 1], dkey(__dadd_rn(uy, kd)));
+                        }
+                        if (dl + 2 <= dr) {
+                            const int slot = atomicAdd(&S.nq, 1);
+                            if (slot < kQCap) {
+                                S.queue[slot] = make_int3(i0 + m, dl + 2, dr);
+                            } else {
+                                for (int d = dl + 2; d <= dr; ++d) {
+                                    const double kd = kglob ? kval(p.vtab, p.vofs, d, lc.drift, tau) : S.Ks[d - dlo];
+                                    smem_atomic_min(&S.keys[off + d], dkey(__dadd_rn(uy, kd)));
+                                }
                             }
                         }
                     }
                 }
+                __syncthreads();
+                // ---- long intervals: one warp per queued source, lanes over d ----
+                const int nq = min(S.nq, kQCap);
+                for (int e = warp; e < nq; e += kNT / 32) {
+                    const int3 qe = S.queue[e];
+                    const double uy = S.ubuf[qe.x + 1];
+                    const int off = base + qe.x;
+                    for (int d = qe.y + lane; d <= qe.z; d += 32) {
+                        const double kd = kglob ? kval(p.vtab, p.vofs, d, lc.drift, tau) : S.Ks[d - dlo];
+                        smem_atomic_min(&S.keys[off + d], dkey(__dadd_rn(uy, kd)));
+                    }
+                }
+                __syncthreads();
+                if (tid == 0) S.nq = 0;
             }
         }
     }
@@ -505,11 +550,10 @@ __global__ void __launch_bounds__(kNT, 3) fast_kernel(
     // ---- epilogue: exact min -> u^{n+1}; direct scan where nothing landed ----
     const double* tvl = tv ? tv + line * tv_stride : nullptr;
     double* vals = S.ubuf;  // reuse: vals[i] = u^{n+1}(jlo + i), i = 0 .. Tl+2
-    for (int i = tid; i < Tl + 3; i += kNT) {
+    for (int i = tid; i <= jspan; i += kNT) {
         int64_t j = jlo + i;
         if (j < 0) j += n;
-        if (j >= n) j -= n;
-        if (j >= n) j -= n;
+        if (j >= n) j %= n;
         double best;
         const unsigned long long kk = S.keys[i];
         if (kk == kKeyInf) {
@@ -519,7 +563,7 @@ __global__ void __launch_bounds__(kNT, 3) fast_kernel(
             int64_t y = (j - first) % n;
             if (y < 0) y += n;
             for (int64_t w = 0; w <= 2 * n; ++w) {
-                const double c2 = __dadd_rn(ul[y], kval(p.vtab, p.vofs, first + w, drift, tau));
+                const double c2 = __dadd_rn(ul[y], kval(p.vtab, p.vofs, first + w, lc.drift, tau));
                 best = c2 < best ? c2 : best;
                 y = y == 0 ? n - 1 : y - 1;
             }
@@ -538,9 +582,9 @@ __global__ void __launch_bounds__(kNT, 3) fast_kernel(
 
 // ---------------------------------------------------------------------------
 // workspace: sub[2][lines][subs] double2 | fsm[2][lines][tiles] u64 |
-//            line[3][lines][4] u64 | diag u64
+//            line[3][lines][4] u64 | LineConst[lines] | diag u64
 struct WsLayout {
-    size_t sub, fsm, line, diag, total;
+    size_t sub, fsm, line, lc, diag, total;
 };
 static WsLayout ws_layout(int64_t lines, int64_t n) {
     const int64_t tiles = (n + kT - 1) / kT, subs = (n + kG - 1) / kG;
@@ -548,7 +592,8 @@ static WsLayout ws_layout(int64_t lines, int64_t n) {
     w.sub = 0;
     w.fsm = w.sub + 2 * static_cast<size_t>(lines * subs) * sizeof(double2);
     w.line = w.fsm + 2 * static_cast<size_t>(lines * tiles) * sizeof(unsigned long long);
-    w.diag = w.line + 3 * static_cast<size_t>(lines) * 4 * sizeof(unsigned long long);
+    w.lc = w.line + 3 * static_cast<size_t>(lines) * 4 * sizeof(unsigned long long);
+    w.diag = w.lc + static_cast<size_t>(lines) * sizeof(LineConst);
     w.total = w.diag + 64;
     return w;
 }
@@ -607,6 +652,9 @@ static FastParams make_params(int64_t n, double tau, double eta) {
     p.subs = (n + kG - 1) / kG;
     p.tau = tau;
     p.eta = eta;
+    p.eps = 1.0 / static_cast<double>(n);  // SchemeParams::epsilon(), proj/include/laxol/scheme.hpp:25
+    p.a = p.eps * p.eps / tau;
+    p.ia = 1.0 / p.a;
     return p;
 }
 
@@ -652,7 +700,12 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     const WsLayout w = ws_layout(lines, n);
     unsigned long long* diag =
         reinterpret_cast<unsigned long long*>(static_cast<char*>(workspace) + w.diag);
+    LineConst* lcs = reinterpret_cast<LineConst*>(static_cast<char*>(workspace) + w.lc);
     if (!(flags & LOB_FAST_STATS_VALID)) {
+        // per-line constants (valid while drift/tau/n and the workspace are unchanged)
+        line_setup_kernel<<<static_cast<unsigned>((lines + 127) / 128), 128, 0, s>>>(drift, lines, p, lcs);
+        LOB_CUDA_TRY(ctx, cudaMemsetAsync(diag, 0, sizeof(unsigned long long), s));
+        ctx->launches += 1;
         // statistics of the given u into the "in" buffers; "out" line stats reset
         FastBuffers sb = b;
         sb.sub_out = const_cast<double2*>(b.sub_in);
@@ -671,7 +724,7 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
                                                static_cast<int>(sizeof(MainShared))));
         attr = true;
     }
-    fast_kernel<<<static_cast<unsigned>(nblk), kNT, sizeof(MainShared), s>>>(u, out, drift, tv, tv_stride,
+    fast_kernel<<<static_cast<unsigned>(nblk), kNT, sizeof(MainShared), s>>>(u, out, lcs, tv, tv_stride,
                                                                              blocks, diag, p, b);
     ctx->launches += 1;
     LOB_CUDA_TRY(ctx, cudaGetLastError());
