@@ -100,11 +100,14 @@ int lob_minplus_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lin
                          double eta, int64_t* blocks, void* workspace, size_t workspace_bytes,
                          int flags, void* stream);
 
-/* Number of fast-engine outputs (cumulative over calls with this workspace)
- * for which the local-minimum walk produced no candidate and the exact
- * direct scan was used instead; 0 in correct operation (tests assert it). */
+/* Fast-engine counters, cumulative since the last call without
+ * LOB_FAST_STATS_VALID on this workspace (counters[8]):
+ *  [0] outputs for which the local-minimum walk produced no candidate and the
+ *      exact direct scan was used instead (0 in correct operation),
+ *  [1] sources scanned, [2] candidates emitted inline, [3] candidates from
+ *  queued long intervals, [4] queued intervals, [5] tiles processed. */
 int lob_fast_diagnostics(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n,
-                         uint64_t* missed_outputs);
+                         uint64_t* counters);
 
 /* K3 — split_step_nd (proj/src/splitting.cpp:37-99) for a periodic n x n
  * row-major tensor: sweep axis 0 (columns, kernel 1), sweep axis 1 (rows,

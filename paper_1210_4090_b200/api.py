@@ -168,11 +168,16 @@ class Device:
                                            _ptr(workspace), ws_bytes, int(flags), _stream_ptr(stream))
         self._check(st, "lob_minplus_fast_f64")
 
-    def fast_diagnostics(self, workspace, lines: int, n: int) -> int:
-        v = ctypes.c_uint64()
-        st = self.lib.lob_fast_diagnostics(self.ctx, _ptr(workspace), lines, n, ctypes.byref(v))
+    def fast_counters(self, workspace, lines: int, n: int) -> dict:
+        v = (ctypes.c_uint64 * 8)()
+        st = self.lib.lob_fast_diagnostics(self.ctx, _ptr(workspace), lines, n, v)
         self._check(st, "lob_fast_diagnostics")
-        return int(v.value)
+        keys = ["missed_outputs", "sources", "inline_candidates", "queued_candidates", "queued_intervals",
+                "tiles"]
+        return {k: int(v[i]) for i, k in enumerate(keys)}
+
+    def fast_diagnostics(self, workspace, lines: int, n: int) -> int:
+        return self.fast_counters(workspace, lines, n)["missed_outputs"]
 
     def split_step_2d(self, u, out, tmp, tau, drift1, drift2, a1=None, a2=None, b=0.0,
                       engine=ENGINE_DIRECT, workspace=None, stream=None):

@@ -147,9 +147,10 @@ int lob_minplus_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lin
 }
 
 int lob_fast_diagnostics(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n,
-                         uint64_t* missed_outputs) {
-    if (!ctx || !workspace || !missed_outputs) return LOB_INVALID_INPUT;
-    return fast_diag_count(ctx, workspace, lines, n, missed_outputs, ctx->stream);
+                         uint64_t* counters) {
+    if (!ctx || !workspace || !counters) return LOB_INVALID_INPUT;
+    cudaDeviceSynchronize();
+    return fast_diag_count(ctx, workspace, lines, n, counters, ctx->stream);
 }
 
 int lob_block_counts(lob_ctx* ctx, const double* u, int64_t lines, int64_t n, double eta,

@@ -52,7 +52,7 @@ constexpr int kG = 256;        // sub-tile (slope statistics granularity)
 constexpr int kSub = kT / kG;  // sub-tiles per tile (= warps per CTA)
 constexpr int kPer = kT / kNT; // outputs / sources per thread
 constexpr int kKCap = 2048;    // K values staged in shared memory
-constexpr int kQCap = 1024;    // queued long source intervals per chunk
+constexpr int kQCap = 512;     // queued long source intervals per chunk
 
 struct LineConst {
     long long first;  // window displacement of w = 0
@@ -175,77 +175,85 @@ struct EpiShared {
     unsigned long long fsm[kNT];
 };
 
+// Shared-memory padding: one slot per 8 doubles, so the per-thread
+// contiguous (stride-8) access patterns are bank-conflict free.
+__host__ __device__ __forceinline__ constexpr int P8(int i) { return i + (i >> 3); }
+
+__device__ __forceinline__ double dmin2(double a, double b) { return b < a ? b : a; }
+__device__ __forceinline__ double dmax2(double a, double b) { return b > a ? b : a; }
+
 // Statistics of u^{n+1} (or of an input u) for the tile whose values are
-// vals[i] = u(j0 - 1 + i), i = 0 .. Tl + 2 (periodic), Tl = tile length.
-// Warp w owns sub-tile w; thread t owns increments e = j0 + 1 + t*kPer ...
-__device__ void tile_epilogue_stats(const double* vals, int Tl, int64_t j0, int64_t line,
-                                    int64_t tile, const FastParams& p, const FastBuffers& b,
-                                    EpiShared& sh) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    {
-        // sub-tile q covers sources [qG, qG+len); its slopes s(qG-1 .. qG+len-1)
-        // are vals[i+1]-vals[i] for i = start .. start+len (start = r*G)
-        const int start = warp * kG;
-        double smn = INFINITY, smx = -INFINITY;
-        if (start < Tl) {
-            const int len = min(kG, Tl - start);
-            for (int i = start + lane; i <= start + len; i += 32) {
-                const double s = __dsub_rn(vals[i + 1], vals[i]);
-                if (s == s) {
-                    smn = fmin(smn, s);
-                    smx = fmax(smx, s);
-                } else {
-                    smn = -INFINITY;
-                    smx = INFINITY;
-                }
-            }
-            smn = warp_min(smn);
-            smx = warp_max(smx);
-            if (lane == 0) {
-                const int64_t q = (j0 + start) / kG;
-                b.sub_out[line * p.subs + q] = make_double2(smn, smx);
-            }
-        }
-        double umn = INFINITY, umx = -INFINITY;
-        for (int i = 1 + threadIdx.x; i <= Tl; i += kNT) {
-            const double v = vals[i];
-            if (isfinite(v)) {
-                umn = fmin(umn, v);
-                umx = fmax(umx, v);
-            } else {
-                umn = -INFINITY;
-                umx = INFINITY;
-            }
-        }
-        umn = warp_min(umn);
-        umx = warp_max(umx);
-        if (lane == 0) {
-            sh.red[0][warp] = umn;
-            sh.red[1][warp] = umx;
-            sh.red[2][warp] = smn;
-            sh.red[3][warp] = smx;
+// vals[i] = u(j0 - 1 + i), i = 0 .. Tl + 2 (periodic), Tl = tile length,
+// all in shared memory.  Thread t owns outputs j0 + 8t .. j0 + 8t + 7, the
+// slopes s(j0 + 8t - 1 .. j0 + 8t + 7) and the increments e = j0 + 8t + 1
+// .. j0 + 8t + 8; warp w owns sub-tile w (256 sources).  lut: the FSM
+// transition table in shared memory.
+__device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line, int64_t tile,
+                           const FastParams& p, const FastBuffers& b, EpiShared& sh,
+                           const unsigned short* lut) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int i0 = kPer * tid;  // vals index of u(j0 + 8t - 1)
+    double w[kPer + 3];
+#pragma unroll
+    for (int m = 0; m < kPer + 3; ++m) w[m] = (i0 + m <= Tl + 2) ? vals[P8(i0 + m)] : 0.0;
+    double umn = INFINITY, umx = -INFINITY, smn = INFINITY, smx = -INFINITY;
+    bool bad_u = false, bad_s = false;
+    double sl[kPer + 2];
+#pragma unroll
+    for (int m = 0; m < kPer + 2; ++m) sl[m] = __dsub_rn(w[m + 1], w[m]);
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        if (i0 + k < Tl) {  // own output j0 + 8t + k = vals[i0 + k + 1]
+            const double v = w[k + 1];
+            umn = dmin2(umn, v);
+            umx = dmax2(umx, v);
+            bad_u |= !isfinite(v);
         }
     }
-    {
-        // decompose() FSM over increments e = j0+1 .. j0+Tl (e <= n-1);
-        // inc(e) = s(e) - s(e-1) with s(e) = vals[e-j0+2] - vals[e-j0+1]
-        int v = 0 | (1 << 2) | (2 << 4);
-        int cnt[3] = {0, 0, 0};
-        const int i_lo = 1 + threadIdx.x * kPer;
 #pragma unroll
-        for (int m = 0; m < kPer; ++m) {
-            const int i = i_lo + m;  // e = j0 + i
-            if (i <= Tl && j0 + i <= p.n - 1) {
-                const double inc = __dsub_rn(__dsub_rn(vals[i + 2], vals[i + 1]),
-                                             __dsub_rn(vals[i + 1], vals[i]));
-                const int x = c_fsm_lut[v * 4 + fsm_class(inc, p.eta)];
-                v = x & 63;
-                cnt[0] += (x >> 6) & 1;
-                cnt[1] += (x >> 7) & 1;
-                cnt[2] += (x >> 8) & 1;
-            }
+    for (int m = 0; m <= kPer; ++m) {
+        if (m <= Tl - i0) {  // s(j0 - 1 + 8t + m), up to s(j0 + Tl - 1)
+            smn = dmin2(smn, sl[m]);
+            smx = dmax2(smx, sl[m]);
+            bad_s |= !(sl[m] == sl[m]);
         }
-        sh.fsm[threadIdx.x] = fsm_pack(v, cnt);
+    }
+    if (bad_u) {
+        umn = -INFINITY;
+        umx = INFINITY;
+    }
+    if (bad_s) {
+        smn = -INFINITY;
+        smx = INFINITY;
+    }
+    // decompose() FSM: increments e = j0 + 8t + 1 + k, inc = s(e) - s(e-1)
+    int v = 0 | (1 << 2) | (2 << 4);
+    int cnt[3] = {0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const int i = i0 + 1 + k;  // e = j0 + i
+        if (i <= Tl && j0 + i <= p.n - 1) {
+            const int x = lut[v * 4 + fsm_class(__dsub_rn(sl[k + 2], sl[k + 1]), p.eta)];
+            v = x & 63;
+            cnt[0] += (x >> 6) & 1;
+            cnt[1] += (x >> 7) & 1;
+            cnt[2] += (x >> 8) & 1;
+        }
+    }
+    sh.fsm[tid] = fsm_pack(v, cnt);
+    smn = warp_min(smn);
+    smx = warp_max(smx);
+    umn = warp_min(umn);
+    umx = warp_max(umx);
+    if (lane == 0) {
+        if (warp * kG < Tl) {
+            const int64_t q = (j0 + warp * kG) / kG;
+            b.sub_out[line * p.subs + q] = make_double2(smn, smx);
+        }
+        sh.red[0][warp] = umn;
+        sh.red[1][warp] = umx;
+        sh.red[2][warp] = smn;
+        sh.red[3][warp] = smx;
     }
     __syncthreads();
     if (warp == 0) {
@@ -254,31 +262,30 @@ __device__ void tile_epilogue_stats(const double* vals, int Tl, int64_t j0, int6
 #pragma unroll
         for (int k = 1; k < kNT / 32; ++k) f = fsm_compose(f, sh.fsm[lane * (kNT / 32) + k]);
         f = warp_fsm(f);
-        if (lane == 0) sh.fsm[0] = f;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double umn = INFINITY, umx = -INFINITY, smn = INFINITY, smx = -INFINITY;
-        const unsigned long long f = sh.fsm[0];
-        for (int w = 0; w < kNT / 32; ++w) {
-            umn = fmin(umn, sh.red[0][w]);
-            umx = fmax(umx, sh.red[1][w]);
-            smn = fmin(smn, sh.red[2][w]);
-            smx = fmax(smx, sh.red[3][w]);
+        if (lane == 0) {
+            double a0 = INFINITY, a1 = -INFINITY, a2 = INFINITY, a3 = -INFINITY;
+            for (int q = 0; q < kNT / 32; ++q) {
+                a0 = fmin(a0, sh.red[0][q]);
+                a1 = fmax(a1, sh.red[1][q]);
+                a2 = fmin(a2, sh.red[2][q]);
+                a3 = fmax(a3, sh.red[3][q]);
+            }
+            b.fsm_out[line * p.tiles + tile] = f;
+            unsigned long long* L = b.line_out + line * 4;
+            atomicMin(L + 0, dkey(a0));
+            atomicMax(L + 1, dkey(a1));
+            atomicMin(L + 2, dkey(a2));
+            atomicMax(L + 3, dkey(a3));
         }
-        b.fsm_out[line * p.tiles + tile] = f;
-        unsigned long long* L = b.line_out + line * 4;
-        atomicMin(L + 0, dkey(umn));
-        atomicMax(L + 1, dkey(umx));
-        atomicMin(L + 2, dkey(smn));
-        atomicMax(L + 3, dkey(smx));
     }
 }
 
 __global__ void __launch_bounds__(kNT) stats_kernel(const double* __restrict__ u, FastParams p,
                                                     FastBuffers b) {
-    __shared__ double vals[kT + 3];
+    __shared__ __align__(16) double vals[P8(kT + 3) + 1];
     __shared__ EpiShared sh;
+    __shared__ unsigned short lut[64 * 4];
+    if (threadIdx.x < 64 * 4) lut[threadIdx.x] = c_fsm_lut[threadIdx.x];
     const int64_t line = blockIdx.x / p.tiles;
     const int64_t tile = blockIdx.x - line * p.tiles;
     const int64_t j0 = tile * kT;
@@ -288,10 +295,10 @@ __global__ void __launch_bounds__(kNT) stats_kernel(const double* __restrict__ u
         int64_t j = j0 - 1 + i;
         if (j < 0) j += p.n;
         if (j >= p.n) j %= p.n;
-        vals[i] = ul[j];
+        vals[P8(i)] = ul[j];
     }
     __syncthreads();
-    tile_epilogue_stats(vals, Tl, j0, line, tile, p, b, sh);
+    tile_stats(vals, Tl, j0, line, tile, p, b, sh, lut);
 }
 
 __global__ void line_init_kernel(unsigned long long* L, int64_t lines) {
@@ -326,13 +333,13 @@ __global__ void combine_blocks_kernel(const unsigned long long* __restrict__ fsm
 }
 
 struct MainShared {
-    unsigned long long keys[kT + 3];
-    double ubuf[kT + 3];
-    double Ks[kKCap];
+    unsigned long long keys[P8(kT + 3) + 1];
+    double ubuf[P8(kT + 3) + 1];
     int3 queue[kQCap];
     EpiShared epi;
-    long long ya, yb;
-    int dlo, dhi, nq;
+    unsigned short lut[64 * 4];
+    int ya, yb, nq;
+    unsigned int c_inline, c_queued, c_src, c_qent;
 };
 
 __device__ __forceinline__ void smem_atomic_min(unsigned long long* addr, unsigned long long key) {
@@ -374,195 +381,194 @@ __global__ void line_setup_kernel(const double* __restrict__ drift_arr, int64_t 
     lc[line] = c;
 }
 
-// Main K2 kernel: one CTA = (line, tile of kT outputs).
-__global__ void __launch_bounds__(kNT, 3) fast_kernel(
+// Main K2 kernel: one CTA = (tile of kT outputs, line); grid (tiles, lines).
+// All index arithmetic is 32-bit (n <= 2^29); "unrolled" source/output
+// indices y, j may lie in (-3n, 3n) and are reduced mod n only on access.
+__global__ void __launch_bounds__(kNT, 4) fast_kernel(
     const double* __restrict__ u, double* __restrict__ out, const LineConst* __restrict__ lcs,
     const double* __restrict__ tv, int64_t tv_stride, int64_t* __restrict__ blocks_out,
     unsigned long long* __restrict__ diag, FastParams p, FastBuffers b) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     MainShared& S = *reinterpret_cast<MainShared*>(smem_raw);
 
-    const int64_t n = p.n;
-    const int64_t line = blockIdx.x / p.tiles;
-    const int64_t tile = blockIdx.x - line * p.tiles;
-    const int64_t j0 = tile * kT;
-    const int Tl = static_cast<int>(min(static_cast<int64_t>(kT), n - j0));
-    const long long jlo = j0 - 1;  // outputs evaluated: jlo .. jlo + Tl + 2 (unrolled)
-    const int jspan = Tl + 2;      // relative output index range [0, jspan]
-    const long long jhi = jlo + jspan;
-    const double* ul = u + line * n;
+    const int n = static_cast<int>(p.n);
+    const int tiles = static_cast<int>(p.tiles), subs = static_cast<int>(p.subs);
+    const int tile = blockIdx.x;
+    const int64_t line = blockIdx.y;
+    const int j0 = tile * kT;
+    const int Tl = min(kT, n - j0);
+    const int jlo = j0 - 1;     // outputs evaluated: jlo .. jlo + jspan (unrolled)
+    const int jspan = Tl + 2;
+    const int jhi = jlo + jspan;
+    const bool big = n >= 2 * kT + 4;  // one conditional wrap suffices
+    const double* ul = u + line * p.n;
     const LineConst lc = lcs[line];
     const double tau = p.tau, ia = p.ia, pe = lc.pe, hl = lc.hl, hr = lc.hr;
-    const int64_t first = lc.first;
-    const int dmin_w = static_cast<int>(first + 1), dmax_w = static_cast<int>(first + 2 * n - 1);
+    const int first = static_cast<int>(lc.first);
+    const int dmin_w = first + 1, dmax_w = first + 2 * n - 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-    for (int i = tid; i <= jspan; i += kNT) S.keys[i] = kKeyInf;
-    if (tid == 0) S.nq = 0;
+    for (int i = tid; i <= jspan; i += kNT) S.keys[P8(i)] = kKeyInf;
+    if (tid < 64 * 4) S.lut[tid] = c_fsm_lut[tid];
+    if (tid == 0) {
+        S.nq = 0;
+        S.ya = INT_MAX;
+        S.yb = INT_MIN;
+        S.c_inline = S.c_queued = S.c_src = S.c_qent = 0;
+    }
     // reset the line statistics buffer two steps ahead
     if (tile == 0 && tid < 4) b.line_reset[line * 4 + tid] = (tid & 1) ? 0ull : ~0ull;
-    if (blocks_out && tile == 0 && tid == 0) {
-        int q = 0;
-        int64_t em = 0;
-        for (int64_t t = 0; t < p.tiles; ++t) {
-            const unsigned long long f = b.fsm_in[line * p.tiles + t];
-            em += (f >> (16 + 16 * q)) & 0xffff;
-            q = static_cast<int>((f >> (2 * q)) & 3);
-        }
-        blocks_out[line] = 1 + em;
-    }
 
     // ---- line statistics: oscillation gate and global displacement bounds ----
     const unsigned long long* L = b.line_in + line * 4;
     const double umin = dkey_inv(L[0]), umax = dkey_inv(L[1]);
     const double smin = dkey_inv(L[2]), smax = dkey_inv(L[3]);
     int DLg = dmin_w, DRg = dmax_w;
-    const double osc = umax - umin;
-    bool ok = (osc * (1.0 + 1e-12) < lc.gap * (1.0 - 1e-12)) && n >= 3 && isfinite(smin) && isfinite(smax);
+    bool ok = ((umax - umin) * (1.0 + 1e-12) < lc.gap * (1.0 - 1e-12)) && n >= 3 && isfinite(smin) &&
+              isfinite(smax);
     if (ok) {
         DLg = max(__double2int_ru(__dmul_rn(__dadd_rn(smin, pe), ia) + hl), dmin_w);
         DRg = min(__double2int_rd(__dmul_rn(__dadd_rn(smax, pe), ia) + hr), dmax_w);
         ok = DLg <= DRg;
     }
+    __syncthreads();  // keys / counters initialised
 
     if (ok) {
         // ---- candidate sub-tiles: unrolled sources y in [jlo - DRg, jhi - DLg] ----
-        const long long y0 = jlo - DRg, y1 = jhi - DLg;
-        const long long k0 = y0 >= 0 ? y0 / n : -((-y0 + n - 1) / n);
-        const long long Q0 = k0 * p.subs + (y0 - k0 * n) / kG;
-        const long long k1 = y1 >= 0 ? y1 / n : -((-y1 + n - 1) / n);
-        const long long Q1 = k1 * p.subs + (y1 - k1 * n) / kG;
-        long long ya = LLONG_MAX, yb = LLONG_MIN;
-        int dlo = INT_MAX, dhi = INT_MIN;
-        for (long long Q = Q0 + tid; Q <= Q1; Q += kNT) {
-            const long long k = Q >= 0 ? Q / p.subs : -((-Q + p.subs - 1) / p.subs);
-            const long long q = Q - k * p.subs;
+        const int y0 = jlo - DRg, y1 = jhi - DLg;
+        const int k0 = y0 >= 0 ? y0 / n : -((n - 1 - y0) / n);
+        const int Q0 = k0 * subs + (y0 - k0 * n) / kG;
+        const int k1 = y1 >= 0 ? y1 / n : -((n - 1 - y1) / n);
+        const int Q1 = k1 * subs + (y1 - k1 * n) / kG;
+        int ya = INT_MAX, yb = INT_MIN;
+        for (int Q = Q0 + tid; Q <= Q1; Q += kNT) {
+            const int k = Q >= 0 ? Q / subs : -((subs - 1 - Q) / subs);
+            const int q = Q - k * subs;
             const double2 sb = b.sub_in[line * p.subs + q];
-            const long long ys = k * n + q * kG;
-            const long long ye = ys + min(static_cast<long long>(kG), static_cast<long long>(n - q * kG)) - 1;
+            const int ys = k * n + q * kG;
+            const int ye = ys + min(kG, n - q * kG) - 1;
             const int dl = max(__double2int_ru(__dmul_rn(__dadd_rn(sb.x, pe), ia) + hl), DLg);
             const int dr = min(__double2int_rd(__dmul_rn(__dadd_rn(sb.y, pe), ia) + hr), DRg);
             if (dl <= dr && ys + dl <= jhi && ye + dr >= jlo) {
                 ya = min(ya, ys);
                 yb = max(yb, ye);
-                dlo = min(dlo, dl);
-                dhi = max(dhi, dr);
             }
         }
-        ya = warp_min_ll(ya);
-        yb = warp_max_ll(yb);
-        dlo = static_cast<int>(warp_min_ll(dlo));
-        dhi = static_cast<int>(warp_max_ll(dhi));
-        if (tid == 0) {
-            S.ya = LLONG_MAX;
-            S.yb = LLONG_MIN;
-            S.dlo = INT_MAX;
-            S.dhi = INT_MIN;
-        }
-        __syncthreads();
+        ya = __reduce_min_sync(0xffffffffu, ya);
+        yb = __reduce_max_sync(0xffffffffu, yb);
         if (lane == 0) {
             atomicMin(&S.ya, ya);
             atomicMax(&S.yb, yb);
-            atomicMin(&S.dlo, dlo);
-            atomicMax(&S.dhi, dhi);
         }
         __syncthreads();
         ya = S.ya;
         yb = S.yb;
-        if (ya <= yb) {
-            dlo = static_cast<int>(max(static_cast<long long>(S.dlo), jlo - yb));
-            dhi = static_cast<int>(min(static_cast<long long>(S.dhi), jhi - ya));
-            const bool kglob = dhi - dlo + 1 > kKCap;
-            // ---- stage K(d), d in [dlo, dhi] (exact build_kernel arithmetic) ----
-            if (!kglob)
-                for (int d = dlo + tid; d <= dhi; d += kNT) S.Ks[d - dlo] = kval(p.vtab, p.vofs, d, lc.drift, tau);
-            // ---- sources in chunks of kT ----
-            for (long long yc = ya; yc <= yb; yc += kT) {
-                const int clen = static_cast<int>(min(static_cast<long long>(kT), yb - yc + 1));
-                const int base = static_cast<int>(yc - jlo);  // jj = base + i + d
-                __syncthreads();
-                // U(yc-1 .. yc+clen) -> ubuf[0 .. clen+1]
-                int bm = static_cast<int>((yc - 1) % n);
-                if (bm < 0) bm += static_cast<int>(n);
-                for (int i = tid; i < clen + 2; i += kNT) {
+        // K(d) = tau*((0.5 v)v - P v) from the shared v_d table (L1/L2 resident)
+        const double* vt = p.vtab + p.vofs;
+        const double kdrift = lc.drift;
+        // ---- sources in chunks of kT ----
+        for (int yc = ya; yc <= yb; yc += kT) {
+            const int clen = min(kT, yb - yc + 1);
+            const int base = yc - jlo;  // output index of source i at d: base + i + d
+            // U(yc-1 .. yc+clen) -> ubuf[0 .. clen+1]
+            int bm = (yc - 1) % n;
+            if (bm < 0) bm += n;
+            {
+                constexpr int kL = (kT + 2 + kNT - 1) / kNT;
+                double v[kL];
+#pragma unroll
+                for (int k = 0; k < kL; ++k) {  // all loads in flight before the stores
+                    const int i = tid + k * kNT;
                     int yy = bm + i;
-                    if (yy >= n) yy = yy - static_cast<int>(n) < n ? yy - static_cast<int>(n) : yy % static_cast<int>(n);
-                    S.ubuf[i] = ul[yy];
+                    if (big) {
+                        yy = yy >= n ? yy - n : yy;
+                    } else {
+                        yy %= n;
+                    }
+                    v[k] = i < clen + 2 ? __ldg(ul + yy) : 0.0;
                 }
-                __syncthreads();
-                const int i0 = tid * kPer;
-                if (i0 < clen) {
-                    double uv[kPer + 2];
 #pragma unroll
-                    for (int m = 0; m < kPer + 2; ++m) uv[m] = S.ubuf[min(i0 + m, clen + 1)];
-                    double z[kPer + 1];
+                for (int k = 0; k < kL; ++k) {
+                    const int i = tid + k * kNT;
+                    if (i < clen + 2) S.ubuf[P8(i)] = v[k];
+                }
+            }
+            __syncthreads();
+            const int i0 = tid * kPer;
+            if (tid == 0) atomicAdd(&S.c_src, static_cast<unsigned>(clen));
+            if (i0 < clen) {
+                unsigned ninl = 0;
+                double uv[kPer + 2];
 #pragma unroll
-                    for (int m = 0; m < kPer + 1; ++m)
-                        z[m] = __dmul_rn(__dadd_rn(__dsub_rn(uv[m + 1], uv[m]), pe), ia);
+                for (int m = 0; m < kPer + 2; ++m) uv[m] = S.ubuf[P8(min(i0 + m, clen + 1))];
+                double z[kPer + 1];
 #pragma unroll
-                    for (int m = 0; m < kPer; ++m) {
-                        const int off = base + i0 + m;  // jj of d = 0
-                        int dl = max(max(__double2int_ru(z[m] + hl), DLg), -off);
-                        int dr = min(min(__double2int_rd(z[m + 1] + hr), DRg), jspan - off);
-                        if (i0 + m >= clen) dr = dl - 1;
-                        const double uy = uv[m + 1];
-                        // inline: the first two candidates; longer intervals are queued
-                        if (dl <= dr) {
-                            const double kd = kglob ? kval(p.vtab, p.vofs, dl, lc.drift, tau) : S.Ks[dl - dlo];
-                            smem_atomic_min(&S.keys[off + dl], dkey(__dadd_rn(uy, kd)));
-                        }
-                        if (dl + 1 <= dr) {
-                            const double kd = kglob ? kval(p.vtab, p.vofs, dl + 1, lc.drift, tau) : S.Ks[dl + 1 - dlo];
-                            smem_atomic_min(&S.keys[off + dl + 1], dkey(__dadd_rn(uy, kd)));
-                        }
+                for (int m = 0; m < kPer + 1; ++m) z[m] = __dmul_rn(__dadd_rn(__dsub_rn(uv[m + 1], uv[m]), pe), ia);
+#pragma unroll
+                for (int m = 0; m < kPer; ++m) {
+                    const int off = base + i0 + m;  // output index of this source at d = 0
+                    const int dl = max(max(__double2int_ru(z[m] + hl), DLg), -off);
+                    int dr = min(min(__double2int_rd(z[m + 1] + hr), DRg), jspan - off);
+                    if (i0 + m >= clen) dr = dl - 1;
+                    const double uy = uv[m + 1];
+                    // inline: the first two candidates; longer intervals are queued
+                    if (dl <= dr) {
+                        const double v0 = __ldg(vt + dl);
+                        const double v1 = dl + 1 <= dr ? __ldg(vt + dl + 1) : 0.0;
+                        smem_atomic_min(&S.keys[P8(off + dl)], dkey(__dadd_rn(uy, kval_v(v0, kdrift, tau))));
+                        if (dl + 1 <= dr)
+                            smem_atomic_min(&S.keys[P8(off + dl + 1)], dkey(__dadd_rn(uy, kval_v(v1, kdrift, tau))));
+                        ninl += min(dr - dl + 1, 2);
                         if (dl + 2 <= dr) {
                             const int slot = atomicAdd(&S.nq, 1);
                             if (slot < kQCap) {
                                 S.queue[slot] = make_int3(i0 + m, dl + 2, dr);
                             } else {
-                                for (int d = dl + 2; d <= dr; ++d) {
-                                    const double kd = kglob ? kval(p.vtab, p.vofs, d, lc.drift, tau) : S.Ks[d - dlo];
-                                    smem_atomic_min(&S.keys[off + d], dkey(__dadd_rn(uy, kd)));
-                                }
+                                for (int d = dl + 2; d <= dr; ++d)
+                                    smem_atomic_min(&S.keys[P8(off + d)], dkey(__dadd_rn(uy, kval_v(__ldg(vt + d), kdrift, tau))));
                             }
                         }
                     }
                 }
-                __syncthreads();
-                // ---- long intervals: one warp per queued source, lanes over d ----
-                const int nq = min(S.nq, kQCap);
+                if (ninl) atomicAdd(&S.c_inline, ninl);
+            }
+            __syncthreads();
+            // ---- long intervals: one warp per queued source, lanes over d ----
+            const int nq = min(S.nq, kQCap);
+            if (nq) {
                 for (int e = warp; e < nq; e += kNT / 32) {
                     const int3 qe = S.queue[e];
-                    const double uy = S.ubuf[qe.x + 1];
+                    const double uy = S.ubuf[P8(qe.x + 1)];
                     const int off = base + qe.x;
-                    for (int d = qe.y + lane; d <= qe.z; d += 32) {
-                        const double kd = kglob ? kval(p.vtab, p.vofs, d, lc.drift, tau) : S.Ks[d - dlo];
-                        smem_atomic_min(&S.keys[off + d], dkey(__dadd_rn(uy, kd)));
-                    }
+                    if (lane == 0) atomicAdd(&S.c_queued, static_cast<unsigned>(qe.z - qe.y + 1));
+                    for (int d = qe.y + lane; d <= qe.z; d += 32)
+                        smem_atomic_min(&S.keys[P8(off + d)], dkey(__dadd_rn(uy, kval_v(__ldg(vt + d), kdrift, tau))));
                 }
                 __syncthreads();
-                if (tid == 0) S.nq = 0;
+                if (tid == 0) {
+                    S.c_qent += nq;
+                    S.nq = 0;
+                }
             }
+            __syncthreads();
         }
     }
-    __syncthreads();
 
     // ---- epilogue: exact min -> u^{n+1}; direct scan where nothing landed ----
+    // Thread t owns outputs j0 + 8t .. j0 + 8t + 7 (vals index 8t+1 ..);
+    // threads 0..2 also evaluate the halo outputs jlo, j0+Tl, j0+Tl+1.
     const double* tvl = tv ? tv + line * tv_stride : nullptr;
     double* vals = S.ubuf;  // reuse: vals[i] = u^{n+1}(jlo + i), i = 0 .. Tl+2
-    for (int i = tid; i <= jspan; i += kNT) {
-        int64_t j = jlo + i;
-        if (j < 0) j += n;
-        if (j >= n) j %= n;
+    auto finish = [&](int i, int j, double tvj) -> double {
+        const unsigned long long kk = S.keys[P8(i)];
         double best;
-        const unsigned long long kk = S.keys[i];
         if (kk == kKeyInf) {
             if (ok && diag) atomicAdd(diag, 1ull);
             // direct scan of the full window (proj/tests/unit_scheme.cpp:184-190)
             best = INFINITY;
-            int64_t y = (j - first) % n;
+            int y = (j - first) % n;
             if (y < 0) y += n;
-            for (int64_t w = 0; w <= 2 * n; ++w) {
+            for (int w = 0; w <= 2 * n; ++w) {
                 const double c2 = __dadd_rn(ul[y], kval(p.vtab, p.vofs, first + w, lc.drift, tau));
                 best = c2 < best ? c2 : best;
                 y = y == 0 ? n - 1 : y - 1;
@@ -570,12 +576,64 @@ __global__ void __launch_bounds__(kNT, 3) fast_kernel(
         } else {
             best = dkey_inv(kk);
         }
-        const double o = tvl ? __dsub_rn(best, tvl[j]) : best;
-        vals[i] = o;
-        if (i >= 1 && i <= Tl) out[line * n + j] = o;
+        return tvl ? __dsub_rn(best, tvj) : best;
+    };
+    {
+        const int i0 = kPer * tid + 1;
+        if (i0 <= Tl) {
+            const int jb = j0 + kPer * tid;  // never wraps: jb + k < j0 + Tl <= n
+            double tvv[kPer];
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) tvv[k] = (tvl && i0 + k <= Tl) ? __ldg(tvl + jb + k) : 0.0;
+            double o[kPer];
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) o[k] = i0 + k <= Tl ? finish(i0 + k, jb + k, tvv[k]) : 0.0;
+#pragma unroll
+            for (int k = 0; k < kPer; ++k)
+                if (i0 + k <= Tl) vals[P8(i0 + k)] = o[k];
+            double* dst = out + line * p.n + jb;
+            if (i0 + kPer - 1 <= Tl && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+                for (int k = 0; k < kPer; k += 2) reinterpret_cast<double2*>(dst)[k / 2] = make_double2(o[k], o[k + 1]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < kPer; ++k)
+                    if (i0 + k <= Tl) dst[k] = o[k];
+            }
+        }
+        if (tid < 3) {
+            const int i = tid == 0 ? 0 : Tl + tid;
+            int j = jlo + i;
+            if (j < 0) j += n;
+            j %= n;
+            vals[P8(i)] = finish(i, j, tvl ? __ldg(tvl + j) : 0.0);
+        }
     }
     __syncthreads();
-    tile_epilogue_stats(vals, Tl, j0, line, tile, p, b, S.epi);
+    if (tid == 0 && diag) {
+        atomicAdd(diag + 1, static_cast<unsigned long long>(S.c_src));
+        atomicAdd(diag + 2, static_cast<unsigned long long>(S.c_inline));
+        atomicAdd(diag + 3, static_cast<unsigned long long>(S.c_queued));
+        atomicAdd(diag + 4, static_cast<unsigned long long>(S.c_qent));
+        atomicAdd(diag + 5, 1ull);
+    }
+    tile_stats(vals, Tl, j0, line, tile, p, b, S.epi, S.lut);
+    // block count of the INPUT u (decompose on the closed period): warp 0 of
+    // the line's first tile composes the tile summaries
+    if (blocks_out && tile == 0 && warp == 0) {
+        int q = 0;
+        int64_t em = 0;
+        for (int t0 = 0; t0 < tiles; t0 += 32) {
+            const unsigned long long mine = t0 + lane < tiles ? b.fsm_in[line * p.tiles + t0 + lane] : fsm_identity();
+            const int cnt = min(32, tiles - t0);
+            for (int k = 0; k < cnt; ++k) {
+                const unsigned long long f = __shfl_sync(0xffffffffu, mine, k);
+                em += (f >> (16 + 16 * q)) & 0xffff;
+                q = static_cast<int>((f >> (2 * q)) & 3);
+            }
+        }
+        if (lane == 0) blocks_out[line] = 1 + em;
+    }
 }
 
 }  // namespace
@@ -683,7 +741,8 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
                     cudaStream_t s) {
     if (ws_bytes < fast_workspace_bytes(lines, n) || !workspace)
         return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_fast_f64: workspace too small");
-    if (n > (1ll << 30)) return set_error(ctx, LOB_INVALID_INPUT, "fast: n too large");
+    if (n > (1ll << 29)) return set_error(ctx, LOB_INVALID_INPUT, "fast: n too large");
+    if (lines > 65535) return set_error(ctx, LOB_INVALID_INPUT, "fast: at most 65535 lines per call");
     int st = ensure_lut(ctx);
     if (st) return st;
     FastParams p = make_params(n, tau, eta);
@@ -704,7 +763,7 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     if (!(flags & LOB_FAST_STATS_VALID)) {
         // per-line constants (valid while drift/tau/n and the workspace are unchanged)
         line_setup_kernel<<<static_cast<unsigned>((lines + 127) / 128), 128, 0, s>>>(drift, lines, p, lcs);
-        LOB_CUDA_TRY(ctx, cudaMemsetAsync(diag, 0, sizeof(unsigned long long), s));
+        LOB_CUDA_TRY(ctx, cudaMemsetAsync(diag, 0, 8 * sizeof(unsigned long long), s));
         ctx->launches += 1;
         // statistics of the given u into the "in" buffers; "out" line stats reset
         FastBuffers sb = b;
@@ -724,8 +783,8 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
                                                static_cast<int>(sizeof(MainShared))));
         attr = true;
     }
-    fast_kernel<<<static_cast<unsigned>(nblk), kNT, sizeof(MainShared), s>>>(u, out, lcs, tv, tv_stride,
-                                                                             blocks, diag, p, b);
+    dim3 grid(static_cast<unsigned>(p.tiles), static_cast<unsigned>(lines));
+    fast_kernel<<<grid, kNT, sizeof(MainShared), s>>>(u, out, lcs, tv, tv_stride, blocks, diag, p, b);
     ctx->launches += 1;
     LOB_CUDA_TRY(ctx, cudaGetLastError());
     counter += 1;
@@ -735,11 +794,9 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
 int fast_diag_count(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n, uint64_t* count,
                     cudaStream_t s) {
     const WsLayout w = ws_layout(lines, n);
-    unsigned long long v = 0;
-    LOB_CUDA_TRY(ctx, cudaMemcpyAsync(&v, static_cast<char*>(workspace) + w.diag, sizeof(v),
-                                      cudaMemcpyDeviceToHost, s));
+    LOB_CUDA_TRY(ctx, cudaMemcpyAsync(count, static_cast<char*>(workspace) + w.diag,
+                                      8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
-    *count = v;
     return LOB_OK;
 }
 

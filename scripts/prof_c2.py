@@ -24,3 +24,11 @@ for i in range(a.pre + a.steps):
     x, y = y, x
 torch.cuda.synchronize()
 print("done", float(x.mean()))
+ws2 = torch.empty_like(ws)
+dev.fast_f64(x, y, dr, tau, tv=tv, workspace=ws2, flags=0)
+for i in range(5):
+    x, y = y, x
+    dev.fast_f64(x, y, dr, tau, tv=tv, workspace=ws2, flags=api.FAST_STATS_VALID)
+c = dev.fast_counters(ws2, L, n)
+upd = 6 * L * n
+print({k: v / upd for k, v in c.items()}, c)
