@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-extras", action="store_true", help="skip the per-kernel extra measurements")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-lines", type=int, default=0,
+                    help="C2 lines per reference-arm step (default: one per host thread, <= 64)")
     return ap.parse_args()
 
 
@@ -115,8 +117,7 @@ def dist_setup(args):
 
         backend = "nccl" if args.impl == "b200" else "gloo"
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group(backend, rank=rank, world_size=world,
-                                device_id=None if backend == "gloo" else None)
+        dist.init_process_group(backend, rank=rank, world_size=world)
     return world, rank, local
 
 
@@ -167,7 +168,7 @@ def run_reference(args, world, rank):
     if rank != 0:
         return
     nthreads = os.cpu_count() or 1
-    lines_sample = max(1, min(nthreads, 64))
+    lines_sample = args.ref_lines or max(1, min(nthreads, 64))
     rates, times = [], []
     for i in range(args.warmup + args.steps):
         r = cpu_reference_rate(lines_sample, nthreads)

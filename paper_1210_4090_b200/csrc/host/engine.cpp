@@ -1,0 +1,373 @@
+// C++ host API over the laxol_b200 C-ABI: the reference's stepping calls
+// (proj/src/scheme.cpp, proj/src/splitting.cpp) with the B200 engines.
+// Semantics follow the reference line by line where it matters for parity:
+//  * periodic GridFn = closed period, seam duplicated (proj/src/grid_fn.cpp:30-36);
+//  * V is sampled on the host through the user's callback at t+tau (Arrival)
+//    or t (Departure), per fundamental grid index (proj/src/scheme.cpp:26-35,156-162),
+//    and tau*V is rounded once on the host;
+//  * evolve keeps snapshots 0, every stride-th, captures and the last
+//    (proj/src/scheme.cpp:215-225), records per-step drift and block counts,
+//    and stops after the first step producing a non-finite value
+//    (proj/src/scheme.cpp:257-264).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "laxol_b200.hpp"
+
+namespace laxol_b200 {
+
+namespace {
+
+void check_status(int st, lob_ctx* ctx, const char* where) {
+    if (st == LOB_OK) return;
+    const std::string msg = std::string(where) + ": " + (ctx ? lob_last_error(ctx) : "");
+    if (st == LOB_INVALID_INPUT) throw InvalidInput(msg);
+    if (st == LOB_EVALUATION_ERROR) throw EvaluationError(msg);
+    throw std::runtime_error(msg + " (CUDA error; there is no CPU fallback)");
+}
+
+void check_cuda(cudaError_t e, const char* where) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// RAII device buffer
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    explicit DevBuf(size_t count) : n(count) {
+        if (count) check_cuda(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    void upload(const T* h, size_t count) {
+        check_cuda(cudaMemcpy(p, h, count * sizeof(T), cudaMemcpyHostToDevice), "H2D");
+    }
+    void download(T* h, size_t count) const {
+        check_cuda(cudaMemcpy(h, p, count * sizeof(T), cudaMemcpyDeviceToHost), "D2H");
+    }
+};
+
+void check_u_grid(const GridFn& u, const SchemeParams& params, const char* who) {
+    // proj/src/scheme.cpp:18-24 + proj/src/grid_fn.cpp:11-22
+    if (u.values.empty()) throw InvalidInput(std::string(who) + ": empty sample vector");
+    if (!(u.step > 0.0)) throw InvalidInput(std::string(who) + ": step must be positive");
+    for (double v : u.values)
+        if (!std::isfinite(v)) throw InvalidInput(std::string(who) + ": non-finite sample");
+    if (u.periodic) {
+        if (u.n() < 1) throw InvalidInput(std::string(who) + ": periodic function needs n >= 1");
+        if (u.values.front() != u.values.back())
+            throw InvalidInput(std::string(who) + ": periodic seam samples differ");
+    }
+    if (u.step != params.epsilon())
+        throw InvalidInput(std::string(who) + ": u.step does not match params.epsilon()");
+    if (u.periodic && u.n() != static_cast<std::size_t>(params.n_space))
+        throw InvalidInput(std::string(who) + ": periodic u must hold one unit period");
+}
+
+double potential_time(double t, const SchemeParams& params) {
+    return params.v_sampling == PotentialSampling::Arrival ? t + params.tau : t;
+}
+
+// tau*V(tv_time, x_j) for j < count (fundamental indices), host callback
+std::vector<double> tabulate_tv(const GridFn& u, const Potential& V, double tt, double tau,
+                                std::size_t count) {
+    std::vector<double> tv(count);
+    for (std::size_t j = 0; j < count; ++j) {
+        const double vx = V(tt, u.coord(j));
+        if (!std::isfinite(vx))
+            throw EvaluationError("step_fully_discrete: potential sample is not finite");
+        tv[j] = tau * vx;
+    }
+    return tv;
+}
+
+int engine_code(ConvEngine e) {
+    if (e == ConvEngine::GpuFast) return LOB_ENGINE_FAST;
+    if (e == ConvEngine::GpuDirect) return LOB_ENGINE_DIRECT;
+    throw InvalidInput(
+        "laxol_b200: ConvEngine::Fast/Naive are the reference's CPU engines; use GpuFast or GpuDirect");
+}
+
+}  // namespace
+
+GridFn make_periodic(std::vector<double> fundamental, double step, double origin) {
+    if (fundamental.empty()) throw InvalidInput("make_periodic: empty sample vector");
+    fundamental.push_back(fundamental.front());
+    GridFn f{std::move(fundamental), step, origin, true};
+    return f;
+}
+
+GridFn make_grid_fn(std::vector<double> values, double step, double origin) {
+    if (values.empty()) throw InvalidInput("make_grid_fn: empty sample vector");
+    return GridFn{std::move(values), step, origin, false};
+}
+
+void validate(const SchemeParams& p) {
+    if (p.n_space < 1) throw InvalidInput("SchemeParams: n_space must be >= 1");
+    if (!(p.tau > 0.0)) throw InvalidInput("SchemeParams: tau must be positive");
+    if (p.eta < 0.0) throw InvalidInput("SchemeParams: eta must be >= 0");
+    if (!(p.h0 > 0.0)) throw InvalidInput("SchemeParams: h0 must be positive");
+    if (p.epsilon() / p.tau >= p.h0)
+        throw InvalidInput("SchemeParams: epsilon/tau = " + std::to_string(p.epsilon() / p.tau) +
+                           " violates the bound epsilon/tau < h0 = " + std::to_string(p.h0));
+}
+
+Engine::Engine(int device) {
+    const int st = lob_ctx_create(device, &ctx_);
+    if (st != LOB_OK)
+        throw std::runtime_error("laxol_b200: no usable CUDA device (status " + std::to_string(st) +
+                                 "); there is no CPU fallback");
+}
+
+Engine::~Engine() { lob_ctx_destroy(ctx_); }
+
+GridFn Engine::kinetic_convolve(const GridFn& u, const KernelWindow& kernel, double eta,
+                                ConvEngine engine, int64_t* blocks) {
+    const int64_t n = kernel.n_space;
+    const int code = engine_code(engine);
+    if (u.periodic) {
+        if (static_cast<int64_t>(u.n()) != n)
+            throw InvalidInput("kinetic_convolve: periodic u must hold one unit period");
+        DevBuf<double> du(n), dout(n);
+        du.upload(u.values.data(), n);
+        int64_t b = 0;
+        if (code == LOB_ENGINE_FAST) {
+            size_t wsb = 0;
+            lob_fast_workspace_bytes(1, n, &wsb);
+            DevBuf<unsigned char> ws(wsb);
+            DevBuf<double> dd(1);
+            dd.upload(&kernel.drift, 1);
+            DevBuf<int64_t> db(1);
+            check_status(lob_minplus_fast_f64(ctx_, du.p, dout.p, 1, n, dd.p, kernel.tau, nullptr, 0, eta,
+                                              db.p, ws.p, wsb, 0, nullptr),
+                         ctx_, "kinetic_convolve");
+            db.download(&b, 1);
+        } else {
+            DevBuf<double> dk(kernel.window.size());
+            dk.upload(kernel.window.data(), kernel.window.size());
+            DevBuf<int64_t> df(1);
+            df.upload(&kernel.first, 1);
+            check_status(lob_minplus_direct_f64(ctx_, du.p, dout.p, 1, n, dk.p, 0, df.p, nullptr, 0, nullptr),
+                         ctx_, "kinetic_convolve");
+            if (blocks) {
+                DevBuf<int64_t> db(1);
+                check_status(lob_block_counts(ctx_, du.p, 1, n, eta, db.p, nullptr), ctx_, "block counts");
+                db.download(&b, 1);
+            }
+        }
+        check_cuda(cudaDeviceSynchronize(), "kinetic_convolve");
+        std::vector<double> out(static_cast<size_t>(n) + 1);
+        dout.download(out.data(), n);
+        out[n] = out[0];
+        if (blocks) *blocks = b;
+        return GridFn{std::move(out), u.step, u.origin, true};
+    }
+    // windowed domain: direct engine (proj/src/scheme.cpp:135-144)
+    const int64_t m = static_cast<int64_t>(u.size());
+    DevBuf<double> du(m), dout(m), dk(kernel.window.size());
+    DevBuf<int64_t> df(1);
+    du.upload(u.values.data(), m);
+    dk.upload(kernel.window.data(), kernel.window.size());
+    df.upload(&kernel.first, 1);
+    check_status(lob_minplus_window_f64(ctx_, du.p, dout.p, 1, m, n, dk.p, 0, df.p, nullptr, 0, nullptr),
+                 ctx_, "kinetic_convolve");
+    std::vector<double> out(m);
+    dout.download(out.data(), m);
+    if (blocks) {
+        // decompose() of the windowed samples (plain vector): host scan like the reference
+        int64_t count = 0;
+        std::size_t b = 0;
+        const std::size_t nn = u.n();
+        std::vector<double> s(nn);
+        for (std::size_t i = 0; i < nn; ++i) s[i] = u.values[i + 1] - u.values[i];
+        if (nn == 0) count = 1;
+        while (b < nn) {
+            bool det = false, convex = true;
+            std::size_t e = b + 1;
+            while (e < nn) {
+                const double inc = s[e] - s[e - 1];
+                if (!det) {
+                    if (inc > eta) det = true, convex = true;
+                    else if (inc < -eta) det = true, convex = false;
+                } else if (convex ? !(inc >= -eta) : !(inc <= eta)) {
+                    break;
+                }
+                ++e;
+            }
+            ++count;
+            b = e;
+        }
+        *blocks = count;
+    }
+    return GridFn{std::move(out), u.step, u.origin, false};
+}
+
+GridFn Engine::step_fully_discrete(const GridFn& u, double t, const Potential& V,
+                                   const SchemeParams& params, const KernelWindow& kernel,
+                                   ConvEngine engine, StepStats* stats) {
+    check_u_grid(u, params, "step_fully_discrete");
+    int64_t blocks = 0;
+    GridFn out = kinetic_convolve(u, kernel, params.eta, engine, &blocks);
+    if (stats) stats->block_count = blocks;
+    const double tt = potential_time(t, params);
+    // out[j] -= tau*V(t', x_{j mod n}) (proj/src/scheme.cpp:156-162)
+    const std::size_t fund = u.periodic ? u.n() : u.size();
+    const std::vector<double> tv = tabulate_tv(u, V, tt, params.tau, fund);
+    for (std::size_t j = 0; j < out.size(); ++j) out.values[j] -= tv[u.periodic ? j % fund : j];
+    return out;
+}
+
+EvolutionTrace Engine::evolve(const GridFn& u0, double t0, int64_t steps, double drift,
+                              const Potential& V, const SchemeParams& params,
+                              const EvolveOptions& options) {
+    if (steps < 0) throw InvalidInput("evolve: steps must be >= 0");
+    check_u_grid(u0, params, "evolve");
+    validate(params);
+    if (!u0.periodic) throw InvalidInput("laxol_b200 evolve: periodic domains only");
+    const int code = engine_code(options.engine);
+    const int64_t n = params.n_space;
+
+    int64_t stride = options.snapshot_stride;
+    if (stride <= 0) stride = steps <= 1024 ? 1 : (steps + 1023) / 1024;
+    std::vector<int64_t> capture = options.capture_steps;
+    std::sort(capture.begin(), capture.end());
+    auto keep = [&](int64_t i) {
+        if (i == 0 || i == steps) return true;
+        if (i % stride == 0) return true;
+        return std::binary_search(capture.begin(), capture.end(), i);
+    };
+
+    EvolutionTrace trace;
+    trace.times.push_back(t0);
+    trace.snapshot_steps.push_back(0);
+    trace.snapshots.push_back(u0);
+    if (steps == 0) return trace;
+
+    DevBuf<double> du(n), dscr(n), dd(1), dtv(n);
+    du.upload(u0.values.data(), n);
+    dd.upload(&drift, 1);
+    size_t wsb = 0;
+    lob_fast_workspace_bytes(1, n, &wsb);
+    DevBuf<unsigned char> ws(wsb);
+    DevBuf<double> dstep_drift(static_cast<size_t>(steps));
+    DevBuf<int64_t> dstep_blocks(static_cast<size_t>(steps));
+    const bool tdep = V && V.time_dependent;
+    std::vector<double> tv;
+    if (V && !tdep) {
+        tv = tabulate_tv(u0, V, potential_time(t0, params), params.tau, n);
+        dtv.upload(tv.data(), n);
+    }
+    std::vector<double> host(static_cast<size_t>(n) + 1);
+    int64_t done = 0;
+    bool aborted = false;
+    while (done < steps && !aborted) {
+        // run up to the next snapshot step (one step at a time for time-dependent V)
+        int64_t next = done + 1;
+        if (!tdep)
+            while (next < steps && !keep(next)) ++next;
+        const int64_t chunk = next - done;
+        if (tdep) {
+            tv = tabulate_tv(u0, V, potential_time(t0 + static_cast<double>(done) * params.tau, params),
+                             params.tau, n);
+            dtv.upload(tv.data(), n);
+        }
+        int64_t completed = 0;
+        const auto started = std::chrono::steady_clock::now();
+        const int st = lob_evolve_f64(ctx_, du.p, dscr.p, 1, n, dd.p, params.tau, V ? dtv.p : nullptr, 0,
+                                      params.eta, code, chunk, dstep_drift.p + done,
+                                      dstep_blocks.p + done, &completed, ws.p, wsb, nullptr);
+        const std::chrono::duration<double> el = std::chrono::steady_clock::now() - started;
+        if (st == LOB_EVALUATION_ERROR) {
+            aborted = true;
+        } else {
+            check_status(st, ctx_, "evolve");
+        }
+        std::vector<double> sd(static_cast<size_t>(completed));
+        std::vector<int64_t> sb(static_cast<size_t>(completed));
+        if (completed) {
+            dstep_drift.download(sd.data(), completed);
+            check_cuda(cudaMemcpy(sb.data(), dstep_blocks.p + done, completed * sizeof(int64_t),
+                                  cudaMemcpyDeviceToHost),
+                       "D2H");
+            check_cuda(cudaMemcpy(sd.data(), dstep_drift.p + done, completed * sizeof(double),
+                                  cudaMemcpyDeviceToHost),
+                       "D2H");
+        }
+        for (int64_t k = 0; k < completed; ++k)
+            trace.per_step.push_back({t0 + static_cast<double>(done + k + 1) * params.tau, sb[k], sd[k],
+                                      el.count() / static_cast<double>(completed)});
+        done += completed;
+        if (aborted) {
+            // lob_evolve_f64 may have advanced past the offending step inside its
+            // check interval: replay exactly `completed` steps from the chunk start
+            trace.completed = false;
+            trace.abort_reason = "non-finite value after step " + std::to_string(done);
+            du.upload(trace.snapshots.back().values.data(), n);
+            int64_t again = 0;
+            lob_evolve_f64(ctx_, du.p, dscr.p, 1, n, dd.p, params.tau, V ? dtv.p : nullptr, 0, params.eta,
+                           code, completed, nullptr, nullptr, &again, ws.p, wsb, nullptr);
+        }
+        du.download(host.data(), n);
+        host[n] = host[0];
+        if (aborted || keep(done)) {
+            trace.times.push_back(t0 + static_cast<double>(done) * params.tau);
+            trace.snapshot_steps.push_back(done);
+            trace.snapshots.push_back(GridFn{host, u0.step, u0.origin, true});
+        }
+        if (st == LOB_EVALUATION_ERROR) break;
+    }
+    return trace;
+}
+
+TensorFn Engine::split_step_nd(const TensorFn& u, double t, const SplitSpec2D& spec,
+                               const SchemeParams& params, ConvEngine engine) {
+    // proj/src/splitting.cpp:37-49 validation
+    if (u.dims.size() != 2)
+        throw InvalidInput("split_step_nd: kinetic part is not separable over the tensor axes");
+    if (u.step != params.epsilon())
+        throw InvalidInput("split_step_nd: tensor step does not match params.epsilon()");
+    if (!u.periodic) throw InvalidInput("laxol_b200 split_step_nd: periodic tensors only");
+    for (std::size_t d : u.dims)
+        if (d != static_cast<std::size_t>(params.n_space))
+            throw InvalidInput("split_step_nd: periodic axes must hold one unit period");
+    const int64_t n = params.n_space;
+    const int code = engine_code(engine);
+    DevBuf<double> du(n * n), dout(n * n), dtmp(n * n), da1(n), da2(n);
+    du.upload(u.values.data(), n * n);
+    double b = 0.0;
+    const bool hasv = static_cast<bool>(spec.potential.a1);
+    if (hasv) {
+        const double tt = potential_time(t, params);
+        std::vector<double> a1(n), a2(n);
+        for (int64_t i = 0; i < n; ++i) {
+            a1[i] = spec.potential.a1(u.origins[0] + static_cast<double>(i) * u.step);
+            a2[i] = spec.potential.a2(u.origins[1] + static_cast<double>(i) * u.step);
+        }
+        b = spec.potential.b ? spec.potential.b(tt) : 0.0;
+        da1.upload(a1.data(), n);
+        da2.upload(a2.data(), n);
+    }
+    size_t wsb = 0;
+    lob_fast_workspace_bytes(n, n, &wsb);
+    DevBuf<unsigned char> ws(code == LOB_ENGINE_FAST ? wsb : 0);
+    check_status(lob_split_step_2d_f64(ctx_, du.p, dout.p, dtmp.p, n, params.tau, spec.drift1, spec.drift2,
+                                       hasv ? da1.p : nullptr, hasv ? da2.p : nullptr, b, code, ws.p, wsb,
+                                       nullptr),
+                 ctx_, "split_step_nd");
+    check_cuda(cudaDeviceSynchronize(), "split_step_nd");
+    TensorFn out = u;
+    dout.download(out.values.data(), n * n);
+    return out;
+}
+
+}  // namespace laxol_b200

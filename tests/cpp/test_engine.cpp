@@ -1,0 +1,174 @@
+// C++ parity tests of the laxol_b200 host API (csrc/host/laxol_b200.hpp),
+// written the way the reference's own unit tests exercise its stepping API
+// (proj/tests/unit_scheme.cpp, proj/tests/unit_splitting.cpp), with
+// independent brute-force oracles.  Needs a CUDA device; prints one
+// PASS/FAIL line per check and exits non-zero on any failure.
+#include <cmath>
+#include <cstdio>
+#include <limits>
+#include <random>
+#include <vector>
+
+#include "laxol_b200.hpp"
+
+using namespace laxol_b200;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond, ...)                           \
+    do {                                           \
+        if (cond) {                                \
+            ++g_pass;                              \
+        } else {                                   \
+            ++g_fail;                              \
+            std::printf("[FAIL] " __VA_ARGS__);    \
+            std::printf("  (%s:%d)\n", __FILE__, __LINE__); \
+        }                                          \
+    } while (0)
+
+static SchemeParams params_of(int n, double tau) {
+    SchemeParams p;
+    p.n_space = n;
+    p.tau = tau;
+    return p;
+}
+
+static GridFn random_periodic(std::mt19937_64& rng, int n, double amp, double step) {
+    std::uniform_real_distribution<double> d(-amp, amp);
+    std::vector<double> v(n);
+    for (double& x : v) x = d(rng);
+    return make_periodic(std::move(v), step);
+}
+
+// definition-level periodic minimum (proj/tests/unit_scheme.cpp:184-190)
+static double def_min(const GridFn& u, const KernelWindow& k, int64_t j) {
+    const int64_t n = static_cast<int64_t>(u.n());
+    double want = std::numeric_limits<double>::infinity();
+    for (std::size_t w = 0; w < k.window.size(); ++w) {
+        const int64_t d = k.first + static_cast<int64_t>(w);
+        const int64_t y = (((j - d) % n) + n) % n;
+        want = std::min(want, u.values[y] + k.window[w]);
+    }
+    return want;
+}
+
+int main() {
+    Engine eng(0);
+    std::mt19937_64 rng(39);
+    // 1. kinetic_convolve == definition-level minimum, both device engines
+    for (double drift : {0.0, 0.4, -0.7, 1.0}) {
+        const SchemeParams p = params_of(24, 0.25);
+        const KernelWindow k = build_kernel_mech(24, 0.25, drift);
+        const GridFn u = random_periodic(rng, 24, 1.0, p.epsilon());
+        for (ConvEngine e : {ConvEngine::GpuDirect, ConvEngine::GpuFast}) {
+            const GridFn got = eng.kinetic_convolve(u, k, 0.0, e);
+            bool ok = got.values.size() == 25 && got.values[24] == got.values[0];
+            for (std::size_t j = 0; j < 24; ++j) ok = ok && got.values[j] == def_min(u, k, j);
+            CHECK(ok, "kinetic_convolve drift %g engine %d", drift, static_cast<int>(e));
+        }
+    }
+    // 2. constants are fixed points of the kinetic-only flow (unit_scheme.cpp:87-94)
+    {
+        const SchemeParams p = params_of(32, 0.125);
+        const KernelWindow k = build_kernel_mech(32, 0.125, 0.0);
+        const GridFn u = make_periodic(std::vector<double>(32, 1.25), p.epsilon());
+        for (ConvEngine e : {ConvEngine::GpuDirect, ConvEngine::GpuFast}) {
+            const GridFn v = eng.step_fully_discrete(u, 0.0, Potential{}, p, k, e);
+            bool ok = true;
+            for (double x : v.values) ok = ok && x == 1.25;
+            CHECK(ok, "constant fixed point engine %d", static_cast<int>(e));
+        }
+    }
+    // 3. representable drift lands exactly: -tau P^2/2 = -0.1 (unit_scheme.cpp:96-106)
+    {
+        const SchemeParams p = params_of(10, 0.2);
+        const KernelWindow k = build_kernel_mech(10, 0.2, 1.0);
+        const GridFn u = make_periodic(std::vector<double>(10, 0.0), p.epsilon());
+        for (ConvEngine e : {ConvEngine::GpuDirect, ConvEngine::GpuFast}) {
+            const GridFn v = eng.step_fully_discrete(u, 0.0, Potential{}, p, k, e);
+            bool ok = true;
+            for (double x : v.values) ok = ok && x == -0.1;
+            CHECK(ok, "representable drift engine %d", static_cast<int>(e));
+        }
+    }
+    // 4. evolve: single step trace matches a direct call; engines agree; thinning
+    {
+        const SchemeParams p = params_of(48, 0.125);
+        Potential V;
+        V.fn = [](double, double x) { return 0.5 + 0.5 * std::cos(2.0 * 2.0 * M_PI * x); };
+        const GridFn u = random_periodic(rng, 48, 1.0, p.epsilon());
+        const KernelWindow k = build_kernel_mech(48, 0.125, 0.7);
+        EvolveOptions fast, direct;
+        fast.engine = ConvEngine::GpuFast;
+        direct.engine = ConvEngine::GpuDirect;
+        const EvolutionTrace one = eng.evolve(u, 0.0, 1, 0.7, V, p, fast);
+        const GridFn step1 = eng.step_fully_discrete(u, 0.0, V, p, k, ConvEngine::GpuDirect);
+        CHECK(one.snapshots.size() == 2 && one.snapshots[1].values == step1.values && one.completed,
+              "evolve single step == step_fully_discrete");
+        const EvolutionTrace a = eng.evolve(u, 0.0, 12, 0.7, V, p, fast);
+        const EvolutionTrace b = eng.evolve(u, 0.0, 12, 0.7, V, p, direct);
+        bool ok = a.snapshots.size() == b.snapshots.size() && a.snapshots.size() == 13;
+        for (std::size_t s = 0; ok && s < a.snapshots.size(); ++s)
+            for (std::size_t j = 0; j < a.snapshots[s].values.size(); ++j)
+                ok = ok && std::fabs(a.snapshots[s].values[j] - b.snapshots[s].values[j]) <= 1e-13;
+        CHECK(ok, "evolve fast vs direct engines agree step by step");
+        ok = a.per_step.size() == 12;
+        for (std::size_t i = 0; ok && i < 12; ++i)
+            ok = a.per_step[i].blocks == b.per_step[i].blocks &&
+                 std::fabs(a.per_step[i].time - 0.125 * (i + 1)) < 1e-15;
+        CHECK(ok, "evolve per-step block counts and times");
+        EvolveOptions thin;
+        thin.snapshot_stride = 1000;
+        thin.capture_steps = {3};
+        const EvolutionTrace t = eng.evolve(make_periodic(std::vector<double>(8, 0.0), 1.0 / 8), 0.0, 7, 0.0,
+                                            Potential{}, params_of(8, 0.5), thin);
+        CHECK(t.snapshot_steps.size() == 3 && t.snapshot_steps[1] == 3 && t.snapshot_steps[2] == 7,
+              "evolve snapshot thinning keeps endpoints and captures");
+    }
+    // 5. evolve aborts with a partial trace when values blow up (unit_scheme.cpp:323-333)
+    {
+        const SchemeParams p = params_of(16, 0.25);
+        Potential V;
+        V.fn = [](double tt, double) { return tt < 0.9 ? 0.0 : 1e308; };
+        V.time_dependent = true;
+        EvolveOptions o;
+        o.engine = ConvEngine::GpuFast;
+        const EvolutionTrace tr = eng.evolve(make_periodic(std::vector<double>(16, 0.0), 1.0 / 16), 0.0, 12,
+                                             0.0, V, p, o);
+        CHECK(!tr.completed && !tr.abort_reason.empty() && tr.snapshots.size() >= 2,
+              "evolve aborts on non-finite values");
+    }
+    // 6. split_step_nd == direct 2-D minimum, associating (u + k1) + k2 (unit_splitting.cpp:25-65,103-121)
+    {
+        const int n = 16;
+        const SchemeParams p = params_of(n, 0.25);
+        const KernelWindow k1 = build_kernel_mech(n, 0.25, 0.0), k2 = build_kernel_mech(n, 0.25, 0.5);
+        std::uniform_real_distribution<double> d(-1.0, 1.0);
+        for (ConvEngine e : {ConvEngine::GpuDirect, ConvEngine::GpuFast}) {
+            TensorFn u;
+            u.values.resize(n * n);
+            for (double& x : u.values) x = d(rng);
+            u.dims = {n, n};
+            u.step = p.epsilon();
+            u.origins = {0.0, 0.0};
+            SplitSpec2D spec;
+            spec.drift1 = 0.0;
+            spec.drift2 = 0.5;
+            const TensorFn out = eng.split_step_nd(u, 0.0, spec, p, e);
+            bool ok = true;
+            for (int x1 = 0; x1 < n; ++x1)
+                for (int x2 = 0; x2 < n; ++x2) {
+                    double best = std::numeric_limits<double>::infinity();
+                    for (std::size_t w1 = 0; w1 < k1.window.size(); ++w1)
+                        for (std::size_t w2 = 0; w2 < k2.window.size(); ++w2) {
+                            const int64_t y1 = (((x1 - (k1.first + (int64_t)w1)) % n) + n) % n;
+                            const int64_t y2 = (((x2 - (k2.first + (int64_t)w2)) % n) + n) % n;
+                            best = std::min(best, (u.values[y1 * n + y2] + k1.window[w1]) + k2.window[w2]);
+                        }
+                    ok = ok && out.values[x1 * n + x2] == best;
+                }
+            CHECK(ok, "split_step_nd == 2-D brute force, engine %d", static_cast<int>(e));
+        }
+    }
+    std::printf("%s: %d passed, %d failed\n", g_fail ? "FAIL" : "ALL PASS", g_pass, g_fail);
+    return g_fail ? 1 : 0;
+}

@@ -1,0 +1,74 @@
+"""K3 (2-D dimension splitting: transposes + sweeps + separable potential)
+parity on the B200 against the oracle and the reference itself."""
+import numpy as np
+import pytest
+
+from paper_1210_4090_b200 import api
+
+pytestmark = pytest.mark.gpu
+
+
+def run_split(dev, u, tau, d1, d2, a1=None, a2=None, b=0.0, engine=api.ENGINE_DIRECT):
+    import torch
+    n = u.shape[0]
+    du = torch.from_numpy(np.ascontiguousarray(u)).cuda()
+    out = torch.empty_like(du)
+    tmp = torch.empty_like(du)
+    ws = torch.empty(dev.fast_workspace_bytes(n, n), dtype=torch.uint8, device="cuda")
+    ta1 = None if a1 is None else torch.from_numpy(a1).cuda()
+    ta2 = None if a2 is None else torch.from_numpy(a2).cuda()
+    dev.split_step_2d(du, out, tmp, tau, d1, d2, a1=ta1, a2=ta2, b=b, engine=engine, workspace=ws)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("engine", [api.ENGINE_DIRECT, api.ENGINE_FAST])
+def test_split_16_vs_reference(dev, orc, ref, engine):
+    # proj/tests/unit_splitting.cpp:103-121 / acceptance criterion 5
+    rng = np.random.default_rng(42)
+    n, tau = 16, 0.25
+    for _ in range(5):
+        u = rng.uniform(-1, 1, (n, n))
+        got = run_split(dev, u, tau, 0.0, 0.5, engine=engine)
+        assert np.array_equal(got, ref.split_step_2d(u, tau, 0.0, 0.5))
+
+
+@pytest.mark.parametrize("engine", [api.ENGINE_DIRECT, api.ENGINE_FAST])
+def test_split_c4_potential_vs_reference(dev, ref, engine):
+    """C4's kinetics and potential V = cos(2 pi x1) cos(2 pi x2) + 0.2 sin(2 pi t) at t+tau."""
+    n, tau, t = 64, 0.05, 0.35
+    u = api.gen_c4_u0(n)
+    a = api.gen_cos(n)
+    b = api.c4_time_term(t + tau)
+    got = run_split(dev, u, tau, 0.3, -0.7, a1=a, a2=a, b=b, engine=engine)
+    want = ref.split_step_2d(u, tau, 0.3, -0.7, pot_kind=1, t=t)
+    assert np.array_equal(got, want)
+
+
+def test_split_c4_full_size_vs_oracle(dev, orc):
+    """C4 at full size (2048^2, tau=0.01, P=(0.3,-0.7)), one step, both engines
+    bit-identical to the oracle's split step."""
+    n, tau, t = 2048, 0.01, 0.0
+    u = api.gen_c4_u0(n)
+    a = api.gen_cos(n)
+    b = api.c4_time_term(t + tau)
+    k1, f1, _, _ = orc.kernel(n, tau, 0.3)
+    k2, f2, _, _ = orc.kernel(n, tau, -0.7)
+    tv = api.tau_v(np.add(np.multiply(a[:, None], a[None, :]), b), tau)
+    want = orc.split2d(u, k1, f1, k2, f2, tv=tv)
+    for engine in (api.ENGINE_DIRECT, api.ENGINE_FAST):
+        got = run_split(dev, u, tau, 0.3, -0.7, a1=a, a2=a, b=b, engine=engine)
+        assert np.array_equal(got, want), engine
+
+
+def test_split_separable_data_stays_separable(dev, orc):
+    # proj/tests/unit_splitting.cpp:76-101: f(x1)+g(x2) -> (f conv K)(x1)+(g conv K)(x2), 1e-13
+    rng = np.random.default_rng(41)
+    n, tau = 16, 0.25
+    f, g = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    u = f[:, None] + g[None, :]
+    got = run_split(dev, u, tau, 0.0, 0.0)
+    K, first, _, _ = orc.kernel(n, tau, 0.0)
+    f1 = orc.direct(f[None, :], K, first)[0]
+    g1 = orc.direct(g[None, :], K, first)[0]
+    assert np.max(np.abs(got - (f1[:, None] + g1[None, :]))) <= 1e-13 * np.max(np.abs(got))
