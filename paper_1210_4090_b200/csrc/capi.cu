@@ -334,22 +334,28 @@ int lob_step_host_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines,
     const int64_t W = 2 * n + 1;
     const size_t kb = engine == LOB_ENGINE_DIRECT ? static_cast<size_t>(lines * W) * sizeof(double) : 0;
     const size_t need = 2 * ub + tvn * sizeof(double) + lines * (sizeof(double) + 2 * sizeof(int64_t)) +
-                        wsb + kb + 256;
+                        wsb + kb + 8 * 256;
     if (ctx->scratch_bytes < need) {
         if (ctx->scratch) cudaFree(ctx->scratch);
         ctx->scratch = nullptr;
         LOB_CUDA_TRY(ctx, cudaMalloc(&ctx->scratch, need));
         ctx->scratch_bytes = need;
     }
+    // sub-buffers aligned to 256 bytes (the fast workspace holds double2 arrays)
     char* p = static_cast<char*>(ctx->scratch);
-    double* du = reinterpret_cast<double*>(p);
-    double* dout = du + lines * n;
-    double* dtv = dout + lines * n;
-    double* ddrift = dtv + tvn;
-    int64_t* dblocks = reinterpret_cast<int64_t*>(ddrift + lines);
-    int64_t* dfirst = dblocks + lines;
-    double* dk = reinterpret_cast<double*>(dfirst + lines);
-    void* ws = reinterpret_cast<char*>(dk) + kb;
+    auto take = [&p](size_t bytes) {
+        char* r = p;
+        p += (bytes + 255) & ~static_cast<size_t>(255);
+        return r;
+    };
+    double* du = reinterpret_cast<double*>(take(ub));
+    double* dout = reinterpret_cast<double*>(take(ub));
+    double* dtv = reinterpret_cast<double*>(take(tvn * sizeof(double)));
+    double* ddrift = reinterpret_cast<double*>(take(lines * sizeof(double)));
+    int64_t* dblocks = reinterpret_cast<int64_t*>(take(lines * sizeof(int64_t)));
+    int64_t* dfirst = reinterpret_cast<int64_t*>(take(lines * sizeof(int64_t)));
+    double* dk = reinterpret_cast<double*>(take(kb));
+    void* ws = take(wsb);
     LOB_CUDA_TRY(ctx, cudaMemcpyAsync(du, u, ub, cudaMemcpyHostToDevice, s));
     if (tv) LOB_CUDA_TRY(ctx, cudaMemcpyAsync(dtv, tv, tvn * sizeof(double), cudaMemcpyHostToDevice, s));
     LOB_CUDA_TRY(ctx, cudaMemcpyAsync(ddrift, drift, lines * sizeof(double), cudaMemcpyHostToDevice, s));
