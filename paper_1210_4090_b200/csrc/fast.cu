@@ -171,7 +171,7 @@ __device__ __forceinline__ long long warp_max_ll(long long x) {
 }
 
 struct EpiShared {
-    double red[4][kNT / 32];
+    unsigned kred[2][kNT / 32];
     unsigned long long fsm[kNT];
 };
 
@@ -182,12 +182,32 @@ __host__ __device__ __forceinline__ constexpr int P8(int i) { return i + (i >> 3
 __device__ __forceinline__ double dmin2(double a, double b) { return b < a ? b : a; }
 __device__ __forceinline__ double dmax2(double a, double b) { return b > a ? b : a; }
 
+// High 32 bits of the order-preserving key: a monotone coarse key.  The
+// smallest (largest) double with a given coarse key is a lower (upper) bound
+// of every double with that key, within 2^-20 relative.
+__device__ __forceinline__ unsigned hkey(double x) {
+    const unsigned hi = static_cast<unsigned>(__double2hiint(x));
+    return hi ^ (static_cast<unsigned>(static_cast<int>(hi) >> 31) | 0x80000000u);
+}
+__device__ __forceinline__ double hkey_lower(unsigned k) {
+    return dkey_inv(static_cast<unsigned long long>(k) << 32);
+}
+__device__ __forceinline__ double hkey_upper(unsigned k) {
+    return dkey_inv((static_cast<unsigned long long>(k) << 32) | 0xffffffffull);
+}
+
 // Statistics of u^{n+1} (or of an input u) for the tile whose values are
 // vals[i] = u(j0 - 1 + i), i = 0 .. Tl + 2 (periodic), Tl = tile length,
-// all in shared memory.  Thread t owns outputs j0 + 8t .. j0 + 8t + 7, the
-// slopes s(j0 + 8t - 1 .. j0 + 8t + 7) and the increments e = j0 + 8t + 1
-// .. j0 + 8t + 8; warp w owns sub-tile w (256 sources).  lut: the FSM
-// transition table in shared memory.
+// all in shared memory.  Thread t owns the slopes s(j0 + 8t - 1 .. j0 + 8t + 7)
+// and the increments e = j0 + 8t + 1 .. j0 + 8t + 8; warp w owns sub-tile w
+// (256 sources).  Produced:
+//  * per sub-tile: conservative bounds [smin, smax] of its slopes s(qG-1 .. qG+len-1)
+//    (coarse keys reduced with REDUX; exactness is not needed, only enclosure);
+//  * per line: the same bounds over the whole line (global atomics);
+//  * per tile: decompose()'s 3-state transition summary (FSM of
+//    proj/src/minplus.cpp:161-187).  For eta == 0 the increment class is the
+//    exact comparison of consecutive slopes (fl(a-b) > 0 <=> a > b), made on
+//    order-preserving keys of s + 0.0 (so -0 == +0 like the reference's inc == 0).
 __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line, int64_t tile,
                            const FastParams& p, const FastBuffers& b, EpiShared& sh,
                            const unsigned short* lut) {
@@ -196,64 +216,54 @@ __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line,
     double w[kPer + 3];
 #pragma unroll
     for (int m = 0; m < kPer + 3; ++m) w[m] = (i0 + m <= Tl + 2) ? vals[P8(i0 + m)] : 0.0;
-    double umn = INFINITY, umx = -INFINITY, smn = INFINITY, smx = -INFINITY;
-    bool bad_u = false, bad_s = false;
     double sl[kPer + 2];
 #pragma unroll
-    for (int m = 0; m < kPer + 2; ++m) sl[m] = __dsub_rn(w[m + 1], w[m]);
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-        if (i0 + k < Tl) {  // own output j0 + 8t + k = vals[i0 + k + 1]
-            const double v = w[k + 1];
-            umn = dmin2(umn, v);
-            umx = dmax2(umx, v);
-            bad_u |= !isfinite(v);
-        }
-    }
+    for (int m = 0; m < kPer + 2; ++m) sl[m] = __dadd_rn(__dsub_rn(w[m + 1], w[m]), 0.0);
+    unsigned kmin = 0xffffffffu, kmax = 0u;
 #pragma unroll
     for (int m = 0; m <= kPer; ++m) {
         if (m <= Tl - i0) {  // s(j0 - 1 + 8t + m), up to s(j0 + Tl - 1)
-            smn = dmin2(smn, sl[m]);
-            smx = dmax2(smx, sl[m]);
-            bad_s |= !(sl[m] == sl[m]);
+            const unsigned k = hkey(sl[m]);
+            kmin = min(kmin, k);
+            kmax = max(kmax, k);
         }
     }
-    if (bad_u) {
-        umn = -INFINITY;
-        umx = INFINITY;
-    }
-    if (bad_s) {
-        smn = -INFINITY;
-        smx = INFINITY;
-    }
-    // decompose() FSM: increments e = j0 + 8t + 1 + k, inc = s(e) - s(e-1)
+    // decompose() FSM over increments e = j0 + 8t + 1 + k: inc = s(e) - s(e-1)
     int v = 0 | (1 << 2) | (2 << 4);
     int cnt[3] = {0, 0, 0};
+    const bool exact_cmp = p.eta == 0.0;
+    unsigned long long kprev = dkey(sl[0 + 1]);
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
         const int i = i0 + 1 + k;  // e = j0 + i
+        const unsigned long long kc = dkey(sl[k + 2]);
         if (i <= Tl && j0 + i <= p.n - 1) {
-            const int x = lut[v * 4 + fsm_class(__dsub_rn(sl[k + 2], sl[k + 1]), p.eta)];
+            int c;
+            if (exact_cmp) {
+                c = kc > kprev ? 0 : (kc < kprev ? 1 : 2);
+                if (!(sl[k + 2] == sl[k + 2]) || !(sl[k + 1] == sl[k + 1])) c = 3;
+            } else {
+                c = fsm_class(__dsub_rn(sl[k + 2], sl[k + 1]), p.eta);
+            }
+            const int x = lut[v * 4 + c];
             v = x & 63;
             cnt[0] += (x >> 6) & 1;
             cnt[1] += (x >> 7) & 1;
             cnt[2] += (x >> 8) & 1;
         }
+        kprev = kc;
     }
     sh.fsm[tid] = fsm_pack(v, cnt);
-    smn = warp_min(smn);
-    smx = warp_max(smx);
-    umn = warp_min(umn);
-    umx = warp_max(umx);
+    kmin = __reduce_min_sync(0xffffffffu, kmin);
+    kmax = __reduce_max_sync(0xffffffffu, kmax);
     if (lane == 0) {
+        const double smn = hkey_lower(kmin), smx = hkey_upper(kmax);
         if (warp * kG < Tl) {
             const int64_t q = (j0 + warp * kG) / kG;
             b.sub_out[line * p.subs + q] = make_double2(smn, smx);
         }
-        sh.red[0][warp] = umn;
-        sh.red[1][warp] = umx;
-        sh.red[2][warp] = smn;
-        sh.red[3][warp] = smx;
+        sh.kred[0][warp] = kmin;
+        sh.kred[1][warp] = kmax;
     }
     __syncthreads();
     if (warp == 0) {
@@ -262,20 +272,15 @@ __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line,
 #pragma unroll
         for (int k = 1; k < kNT / 32; ++k) f = fsm_compose(f, sh.fsm[lane * (kNT / 32) + k]);
         f = warp_fsm(f);
+        unsigned a0 = lane < kNT / 32 ? sh.kred[0][lane] : 0xffffffffu;
+        unsigned a1 = lane < kNT / 32 ? sh.kred[1][lane] : 0u;
+        a0 = __reduce_min_sync(0xffffffffu, a0);
+        a1 = __reduce_max_sync(0xffffffffu, a1);
         if (lane == 0) {
-            double a0 = INFINITY, a1 = -INFINITY, a2 = INFINITY, a3 = -INFINITY;
-            for (int q = 0; q < kNT / 32; ++q) {
-                a0 = fmin(a0, sh.red[0][q]);
-                a1 = fmax(a1, sh.red[1][q]);
-                a2 = fmin(a2, sh.red[2][q]);
-                a3 = fmax(a3, sh.red[3][q]);
-            }
             b.fsm_out[line * p.tiles + tile] = f;
             unsigned long long* L = b.line_out + line * 4;
-            atomicMin(L + 0, dkey(a0));
-            atomicMax(L + 1, dkey(a1));
-            atomicMin(L + 2, dkey(a2));
-            atomicMax(L + 3, dkey(a3));
+            atomicMin(L + 2, dkey(hkey_lower(a0)));
+            atomicMax(L + 3, dkey(hkey_upper(a1)));
         }
     }
 }
@@ -421,10 +426,11 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
 
     // ---- line statistics: oscillation gate and global displacement bounds ----
     const unsigned long long* L = b.line_in + line * 4;
-    const double umin = dkey_inv(L[0]), umax = dkey_inv(L[1]);
     const double smin = dkey_inv(L[2]), smax = dkey_inv(L[3]);
     int DLg = dmin_w, DRg = dmax_w;
-    bool ok = ((umax - umin) * (1.0 + 1e-12) < lc.gap * (1.0 - 1e-12)) && n >= 3 && isfinite(smin) &&
+    // oscillation of a periodic line <= (n/2) max|slope| (shorter arc)
+    const double osc_bound = 0.5 * static_cast<double>(n) * fmax(fabs(smin), fabs(smax));
+    bool ok = (osc_bound * (1.0 + 1e-12) < lc.gap * (1.0 - 1e-12)) && n >= 3 && isfinite(smin) &&
               isfinite(smax);
     if (ok) {
         DLg = max(__double2int_ru(__dmul_rn(__dadd_rn(smin, pe), ia) + hl), dmin_w);
