@@ -510,28 +510,45 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
                 double z[kPer + 1];
 #pragma unroll
                 for (int m = 0; m < kPer + 1; ++m) z[m] = __dmul_rn(__dadd_rn(__dsub_rn(uv[m + 1], uv[m]), pe), ia);
+                // groups of 4 sources: all arithmetic first (independent, overlaps
+                // latencies), then the shared-memory min updates
+                constexpr int kGrp = 4;
 #pragma unroll
-                for (int m = 0; m < kPer; ++m) {
-                    const int off = base + i0 + m;  // output index of this source at d = 0
-                    const int dl = max(max(__double2int_ru(z[m] + hl), DLg), -off);
-                    int dr = min(min(__double2int_rd(z[m + 1] + hr), DRg), jspan - off);
-                    if (i0 + m >= clen) dr = dl - 1;
-                    const double uy = uv[m + 1];
-                    // inline: the first two candidates; longer intervals are queued
-                    if (dl <= dr) {
-                        const double v0 = __ldg(vt + dl);
-                        const double v1 = dl + 1 <= dr ? __ldg(vt + dl + 1) : 0.0;
-                        smem_atomic_min(&S.keys[P8(off + dl)], dkey(__dadd_rn(uy, kval_v(v0, kdrift, tau))));
-                        if (dl + 1 <= dr)
-                            smem_atomic_min(&S.keys[P8(off + dl + 1)], dkey(__dadd_rn(uy, kval_v(v1, kdrift, tau))));
-                        ninl += min(dr - dl + 1, 2);
-                        if (dl + 2 <= dr) {
-                            const int slot = atomicAdd(&S.nq, 1);
-                            if (slot < kQCap) {
-                                S.queue[slot] = make_int3(i0 + m, dl + 2, dr);
-                            } else {
-                                for (int d = dl + 2; d <= dr; ++d)
-                                    smem_atomic_min(&S.keys[P8(off + d)], dkey(__dadd_rn(uy, kval_v(__ldg(vt + d), kdrift, tau))));
+                for (int g = 0; g < kPer; g += kGrp) {
+                    int dls[kGrp], drs[kGrp];
+                    unsigned long long k0s[kGrp], k1s[kGrp];
+#pragma unroll
+                    for (int q = 0; q < kGrp; ++q) {
+                        const int m = g + q;
+                        const int off = base + i0 + m;  // output index of this source at d = 0
+                        const int dl = max(max(__double2int_ru(z[m] + hl), DLg), -off);
+                        int dr = min(min(__double2int_rd(z[m + 1] + hr), DRg), jspan - off);
+                        if (i0 + m >= clen) dr = dl - 1;
+                        const int dd = dl <= dr ? dl : first + n;  // a valid index either way
+                        const double uy = uv[m + 1];
+                        k0s[q] = dkey(__dadd_rn(uy, kval_v(__ldg(vt + dd), kdrift, tau)));
+                        k1s[q] = dkey(__dadd_rn(uy, kval_v(__ldg(vt + dd + 1), kdrift, tau)));
+                        dls[q] = dl;
+                        drs[q] = dr;
+                    }
+#pragma unroll
+                    for (int q = 0; q < kGrp; ++q) {
+                        const int m = g + q;
+                        const int off = base + i0 + m;
+                        const int dl = dls[q], dr = drs[q];
+                        if (dl <= dr) {
+                            smem_atomic_min(&S.keys[P8(off + dl)], k0s[q]);
+                            if (dl + 1 <= dr) smem_atomic_min(&S.keys[P8(off + dl + 1)], k1s[q]);
+                            ninl += min(dr - dl + 1, 2);
+                            if (dl + 2 <= dr) {
+                                const int slot = atomicAdd(&S.nq, 1);
+                                if (slot < kQCap) {
+                                    S.queue[slot] = make_int3(i0 + m, dl + 2, dr);
+                                } else {
+                                    const double uy = uv[m + 1];
+                                    for (int d = dl + 2; d <= dr; ++d)
+                                        smem_atomic_min(&S.keys[P8(off + d)], dkey(__dadd_rn(uy, kval_v(__ldg(vt + d), kdrift, tau))));
+                                }
                             }
                         }
                     }
