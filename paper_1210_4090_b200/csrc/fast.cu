@@ -338,8 +338,8 @@ __global__ void combine_blocks_kernel(const unsigned long long* __restrict__ fsm
 }
 
 struct MainShared {
-    unsigned long long keys[P8(kT + 3) + 1];
-    double ubuf[P8(kT + 3) + 1];
+    unsigned long long keys[kT + 4];   // candidates, lane-interleaved access (no padding)
+    double ubuf[P8(kT + 3) + 1];      // sources (unpadded) / then u^{n+1} values (padded, for stats)
     int3 queue[kQCap];
     EpiShared epi;
     unsigned short lut[64 * 4];
@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
     const int dmin_w = first + 1, dmax_w = first + 2 * n - 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-    for (int i = tid; i <= jspan; i += kNT) S.keys[P8(i)] = kKeyInf;
+    for (int i = tid; i <= jspan; i += kNT) S.keys[i] = kKeyInf;
     if (tid < 64 * 4) S.lut[tid] = c_fsm_lut[tid];
     if (tid == 0) {
         S.nq = 0;
@@ -496,59 +496,38 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
 #pragma unroll
                 for (int k = 0; k < kL; ++k) {
                     const int i = tid + k * kNT;
-                    if (i < clen + 2) S.ubuf[P8(i)] = v[k];
+                    if (i < clen + 2) S.ubuf[i] = v[k];
                 }
             }
             __syncthreads();
-            const int i0 = tid * kPer;
             if (tid == 0) atomicAdd(&S.c_src, static_cast<unsigned>(clen));
-            if (i0 < clen) {
+            {
+                // warp w takes chunk sources 256w + lane + 32m (consecutive lanes,
+                // consecutive sources: conflict-free shared accesses)
                 unsigned ninl = 0;
-                double uv[kPer + 2];
-#pragma unroll
-                for (int m = 0; m < kPer + 2; ++m) uv[m] = S.ubuf[P8(min(i0 + m, clen + 1))];
-                double z[kPer + 1];
-#pragma unroll
-                for (int m = 0; m < kPer + 1; ++m) z[m] = __dmul_rn(__dadd_rn(__dsub_rn(uv[m + 1], uv[m]), pe), ia);
-                // groups of 4 sources: all arithmetic first (independent, overlaps
-                // latencies), then the shared-memory min updates
-                constexpr int kGrp = 4;
-#pragma unroll
-                for (int g = 0; g < kPer; g += kGrp) {
-                    int dls[kGrp], drs[kGrp];
-                    unsigned long long k0s[kGrp], k1s[kGrp];
-#pragma unroll
-                    for (int q = 0; q < kGrp; ++q) {
-                        const int m = g + q;
-                        const int off = base + i0 + m;  // output index of this source at d = 0
-                        const int dl = max(max(__double2int_ru(z[m] + hl), DLg), -off);
-                        int dr = min(min(__double2int_rd(z[m + 1] + hr), DRg), jspan - off);
-                        if (i0 + m >= clen) dr = dl - 1;
-                        const int dd = dl <= dr ? dl : first + n;  // a valid index either way
-                        const double uy = uv[m + 1];
-                        k0s[q] = dkey(__dadd_rn(uy, kval_v(__ldg(vt + dd), kdrift, tau)));
-                        k1s[q] = dkey(__dadd_rn(uy, kval_v(__ldg(vt + dd + 1), kdrift, tau)));
-                        dls[q] = dl;
-                        drs[q] = dr;
-                    }
-#pragma unroll
-                    for (int q = 0; q < kGrp; ++q) {
-                        const int m = g + q;
-                        const int off = base + i0 + m;
-                        const int dl = dls[q], dr = drs[q];
-                        if (dl <= dr) {
-                            smem_atomic_min(&S.keys[P8(off + dl)], k0s[q]);
-                            if (dl + 1 <= dr) smem_atomic_min(&S.keys[P8(off + dl + 1)], k1s[q]);
-                            ninl += min(dr - dl + 1, 2);
-                            if (dl + 2 <= dr) {
-                                const int slot = atomicAdd(&S.nq, 1);
-                                if (slot < kQCap) {
-                                    S.queue[slot] = make_int3(i0 + m, dl + 2, dr);
-                                } else {
-                                    const double uy = uv[m + 1];
-                                    for (int d = dl + 2; d <= dr; ++d)
-                                        smem_atomic_min(&S.keys[P8(off + d)], dkey(__dadd_rn(uy, kval_v(__ldg(vt + d), kdrift, tau))));
-                                }
+#pragma unroll 2
+                for (int m = 0; m < kPer; ++m) {
+                    const int i = warp * (32 * kPer) + lane + 32 * m;  // source index in the chunk
+                    if (i >= clen) break;
+                    const double ul0 = S.ubuf[i], u0 = S.ubuf[i + 1], ur0 = S.ubuf[i + 2];
+                    const double zl = __dmul_rn(__dadd_rn(__dsub_rn(u0, ul0), pe), ia);
+                    const double zr = __dmul_rn(__dadd_rn(__dsub_rn(ur0, u0), pe), ia);
+                    const int off = base + i;  // output index of this source at d = 0
+                    const int dl = max(max(__double2int_ru(zl + hl), DLg), -off);
+                    const int dr = min(min(__double2int_rd(zr + hr), DRg), jspan - off);
+                    if (dl <= dr) {
+                        const double v0 = __ldg(vt + dl);
+                        const double v1 = dl + 1 <= dr ? __ldg(vt + dl + 1) : 0.0;
+                        smem_atomic_min(&S.keys[off + dl], dkey(__dadd_rn(u0, kval_v(v0, kdrift, tau))));
+                        if (dl + 1 <= dr) smem_atomic_min(&S.keys[off + dl + 1], dkey(__dadd_rn(u0, kval_v(v1, kdrift, tau))));
+                        ninl += min(dr - dl + 1, 2);
+                        if (dl + 2 <= dr) {
+                            const int slot = atomicAdd(&S.nq, 1);
+                            if (slot < kQCap) {
+                                S.queue[slot] = make_int3(i, dl + 2, dr);
+                            } else {
+                                for (int d = dl + 2; d <= dr; ++d)
+                                    smem_atomic_min(&S.keys[off + d], dkey(__dadd_rn(u0, kval_v(__ldg(vt + d), kdrift, tau))));
                             }
                         }
                     }
@@ -561,11 +540,11 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
             if (nq) {
                 for (int e = warp; e < nq; e += kNT / 32) {
                     const int3 qe = S.queue[e];
-                    const double uy = S.ubuf[P8(qe.x + 1)];
+                    const double uy = S.ubuf[qe.x + 1];
                     const int off = base + qe.x;
                     if (lane == 0) atomicAdd(&S.c_queued, static_cast<unsigned>(qe.z - qe.y + 1));
                     for (int d = qe.y + lane; d <= qe.z; d += 32)
-                        smem_atomic_min(&S.keys[P8(off + d)], dkey(__dadd_rn(uy, kval_v(__ldg(vt + d), kdrift, tau))));
+                        smem_atomic_min(&S.keys[off + d], dkey(__dadd_rn(uy, kval_v(__ldg(vt + d), kdrift, tau))));
                 }
                 __syncthreads();
                 if (tid == 0) {
@@ -583,7 +562,7 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
     const double* tvl = tv ? tv + line * tv_stride : nullptr;
     double* vals = S.ubuf;  // reuse: vals[i] = u^{n+1}(jlo + i), i = 0 .. Tl+2
     auto finish = [&](int i, int j, double tvj) -> double {
-        const unsigned long long kk = S.keys[P8(i)];
+        const unsigned long long kk = S.keys[i];
         double best;
         if (kk == kKeyInf) {
             if (ok && diag) atomicAdd(diag, 1ull);
@@ -602,26 +581,21 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
         return tvl ? __dsub_rn(best, tvj) : best;
     };
     {
-        const int i0 = kPer * tid + 1;
-        if (i0 <= Tl) {
-            const int jb = j0 + kPer * tid;  // never wraps: jb + k < j0 + Tl <= n
-            double tvv[kPer];
+        // outputs j0 + t + kNT*m (vals index 1 + t + kNT*m): coalesced, conflict-free
+        double tvv[kPer];
 #pragma unroll
-            for (int k = 0; k < kPer; ++k) tvv[k] = (tvl && i0 + k <= Tl) ? __ldg(tvl + jb + k) : 0.0;
-            double o[kPer];
+        for (int m = 0; m < kPer; ++m) {
+            const int i = 1 + tid + kNT * m;
+            tvv[m] = (tvl && i <= Tl) ? __ldg(tvl + j0 + i - 1) : 0.0;
+        }
+        double* ol = out + line * p.n + j0;
 #pragma unroll
-            for (int k = 0; k < kPer; ++k) o[k] = i0 + k <= Tl ? finish(i0 + k, jb + k, tvv[k]) : 0.0;
-#pragma unroll
-            for (int k = 0; k < kPer; ++k)
-                if (i0 + k <= Tl) vals[P8(i0 + k)] = o[k];
-            double* dst = out + line * p.n + jb;
-            if (i0 + kPer - 1 <= Tl && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-#pragma unroll
-                for (int k = 0; k < kPer; k += 2) reinterpret_cast<double2*>(dst)[k / 2] = make_double2(o[k], o[k + 1]);
-            } else {
-#pragma unroll
-                for (int k = 0; k < kPer; ++k)
-                    if (i0 + k <= Tl) dst[k] = o[k];
+        for (int m = 0; m < kPer; ++m) {
+            const int i = 1 + tid + kNT * m;
+            if (i <= Tl) {
+                const double o = finish(i, j0 + i - 1, tvv[m]);
+                vals[P8(i)] = o;
+                ol[i - 1] = o;
             }
         }
         if (tid < 3) {

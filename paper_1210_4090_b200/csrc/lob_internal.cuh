@@ -52,12 +52,19 @@ inline int cuda_status(lob_ctx* ctx, cudaError_t e, const char* where) {
 // Order-preserving map double -> uint64 (x < y  <=>  key(x) < key(y) for
 // non-NaN x, y; -0 orders just below +0).
 __device__ __forceinline__ unsigned long long dkey(double x) {
-    unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
-    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+    unsigned hi = static_cast<unsigned>(__double2hiint(x));
+    unsigned lo = static_cast<unsigned>(__double2loint(x));
+    const unsigned m = static_cast<unsigned>(static_cast<int>(hi) >> 31);  // 0 or ~0
+    hi ^= m | 0x80000000u;
+    lo ^= m;
+    return (static_cast<unsigned long long>(hi) << 32) | lo;
 }
 __device__ __forceinline__ double dkey_inv(unsigned long long k) {
-    unsigned long long b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
-    return __longlong_as_double(static_cast<long long>(b));
+    unsigned hi = static_cast<unsigned>(k >> 32), lo = static_cast<unsigned>(k);
+    const unsigned m = (hi & 0x80000000u) ? 0x80000000u : 0xffffffffu;
+    hi ^= m;
+    lo ^= (m == 0xffffffffu) ? 0xffffffffu : 0u;
+    return __hiloint2double(static_cast<int>(hi), static_cast<int>(lo));
 }
 constexpr unsigned long long kKeyInf = 0xfff0000000000000ull;  // dkey(+inf)
 
