@@ -339,13 +339,42 @@ __global__ void combine_blocks_kernel(const unsigned long long* __restrict__ fsm
 
 struct MainShared {
     unsigned long long keys[kT + 4];   // candidates, lane-interleaved access (no padding)
-    double ubuf[P8(kT + 3) + 1];      // sources (unpadded) / then u^{n+1} values (padded, for stats)
+    unsigned long long mbar;           // TMA completion barrier for the source chunk
+    __align__(16) double ubuf[P8(kT + 3) + 1];  // sources (unpadded) / then u^{n+1} (padded, stats)
     int3 queue[kQCap];
     EpiShared epi;
     unsigned short lut[64 * 4];
     int ya, yb, nq;
     unsigned int c_inline, c_queued, c_src, c_qent;
 };
+
+// ---- TMA bulk copies (cp.async.bulk) completed on an mbarrier ------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n LAB_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra LAB_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ void smem_atomic_min(unsigned long long* addr, unsigned long long key) {
     unsigned long long old = *addr;
@@ -416,6 +445,8 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
     for (int i = tid; i <= jspan; i += kNT) S.keys[i] = kKeyInf;
     if (tid < 64 * 4) S.lut[tid] = c_fsm_lut[tid];
     if (tid == 0) {
+        mbar_init(&S.mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         S.nq = 0;
         S.ya = INT_MAX;
         S.yb = INT_MIN;
@@ -473,33 +504,33 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
         const double* vt = p.vtab + p.vofs;
         const double kdrift = lc.drift;
         // ---- sources in chunks of kT ----
+        unsigned mphase = 0;
         for (int yc = ya; yc <= yb; yc += kT) {
             const int clen = min(kT, yb - yc + 1);
             const int base = yc - jlo;  // output index of source i at d: base + i + d
-            // U(yc-1 .. yc+clen) -> ubuf[0 .. clen+1]
+            // U(yc-1 .. yc+clen) -> ubuf[sh .. sh+clen+1]
             int bm = (yc - 1) % n;
             if (bm < 0) bm += n;
-            {
-                constexpr int kL = (kT + 2 + kNT - 1) / kNT;
-                double v[kL];
-#pragma unroll
-                for (int k = 0; k < kL; ++k) {  // all loads in flight before the stores
-                    const int i = tid + k * kNT;
-                    int yy = bm + i;
-                    if (big) {
-                        yy = yy >= n ? yy - n : yy;
-                    } else {
-                        yy %= n;
-                    }
-                    v[k] = i < clen + 2 ? __ldg(ul + yy) : 0.0;
+            int sh = 0;
+            if (big) {
+                // TMA bulk copies: 16-byte aligned even start, wrapped at the period
+                sh = bm & 1;
+                if (tid == 0) {
+                    const int s0 = bm - sh;                      // even, in [0, n)
+                    const int cnt = (clen + 2 + sh + 1) & ~1;    // even count
+                    const int c1 = min(cnt, n - s0);             // first segment (n even)
+                    fence_proxy_async();
+                    mbar_expect_tx(&S.mbar, static_cast<unsigned>(cnt) * 8u);
+                    tma_load_1d(S.ubuf, ul + s0, static_cast<unsigned>(c1) * 8u, &S.mbar);
+                    if (cnt > c1) tma_load_1d(S.ubuf + c1, ul, static_cast<unsigned>(cnt - c1) * 8u, &S.mbar);
                 }
-#pragma unroll
-                for (int k = 0; k < kL; ++k) {
-                    const int i = tid + k * kNT;
-                    if (i < clen + 2) S.ubuf[i] = v[k];
-                }
+                mbar_wait(&S.mbar, mphase);
+                mphase ^= 1u;
+            } else {
+                for (int i = tid; i < clen + 2; i += kNT) S.ubuf[i] = __ldg(ul + (bm + i) % n);
+                __syncthreads();
             }
-            __syncthreads();
+            const double* ub = S.ubuf + sh;
             if (tid == 0) atomicAdd(&S.c_src, static_cast<unsigned>(clen));
             {
                 // warp w takes chunk sources 256w + lane + 32m (consecutive lanes,
@@ -509,7 +540,7 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
                 for (int m = 0; m < kPer; ++m) {
                     const int i = warp * (32 * kPer) + lane + 32 * m;  // source index in the chunk
                     if (i >= clen) break;
-                    const double ul0 = S.ubuf[i], u0 = S.ubuf[i + 1], ur0 = S.ubuf[i + 2];
+                    const double ul0 = ub[i], u0 = ub[i + 1], ur0 = ub[i + 2];
                     const double zl = __dmul_rn(__dadd_rn(__dsub_rn(u0, ul0), pe), ia);
                     const double zr = __dmul_rn(__dadd_rn(__dsub_rn(ur0, u0), pe), ia);
                     const int off = base + i;  // output index of this source at d = 0
@@ -540,7 +571,7 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
             if (nq) {
                 for (int e = warp; e < nq; e += kNT / 32) {
                     const int3 qe = S.queue[e];
-                    const double uy = S.ubuf[qe.x + 1];
+                    const double uy = ub[qe.x + 1];
                     const int off = base + qe.x;
                     if (lane == 0) atomicAdd(&S.c_queued, static_cast<unsigned>(qe.z - qe.y + 1));
                     for (int d = qe.y + lane; d <= qe.z; d += 32)
