@@ -377,8 +377,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ void smem_atomic_min(unsigned long long* addr, unsigned long long key) {
-    unsigned long long old = *addr;
-    while (key < old) {
+    // fast path: the first candidate of an output replaces the +inf sentinel
+    unsigned long long old = atomicCAS(addr, kKeyInf, key);
+    while (old != kKeyInf && key < old) {
         const unsigned long long prev = atomicCAS(addr, old, key);
         if (prev == old) break;
         old = prev;
@@ -473,9 +474,12 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
     if (ok) {
         // ---- candidate sub-tiles: unrolled sources y in [jlo - DRg, jhi - DLg] ----
         const int y0 = jlo - DRg, y1 = jhi - DLg;
-        const int k0 = y0 >= 0 ? y0 / n : -((n - 1 - y0) / n);
+        int k0 = 0;
+        while (y0 - k0 * n < 0) --k0;
+        while (y0 - k0 * n >= n) ++k0;
         const int Q0 = k0 * subs + (y0 - k0 * n) / kG;
-        const int k1 = y1 >= 0 ? y1 / n : -((n - 1 - y1) / n);
+        int k1 = k0;
+        while (y1 - k1 * n >= n) ++k1;
         const int Q1 = k1 * subs + (y1 - k1 * n) / kG;
         int ya = INT_MAX, yb = INT_MIN;
         for (int Q = Q0 + tid; Q <= Q1; Q += kNT) {
@@ -509,8 +513,9 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
             const int clen = min(kT, yb - yc + 1);
             const int base = yc - jlo;  // output index of source i at d: base + i + d
             // U(yc-1 .. yc+clen) -> ubuf[sh .. sh+clen+1]
-            int bm = (yc - 1) % n;
-            if (bm < 0) bm += n;
+            int bm = yc - 1;  // yc in (-3n, 3n)
+            while (bm < 0) bm += n;
+            while (bm >= n) bm -= n;
             int sh = 0;
             if (big) {
                 // TMA bulk copies: 16-byte aligned even start, wrapped at the period
