@@ -419,7 +419,7 @@ __global__ void line_setup_kernel(const double* __restrict__ drift_arr, int64_t 
 // Main K2 kernel: one CTA = (tile of kT outputs, line); grid (tiles, lines).
 // All index arithmetic is 32-bit (n <= 2^29); "unrolled" source/output
 // indices y, j may lie in (-3n, 3n) and are reduced mod n only on access.
-__global__ void __launch_bounds__(kNT, 4) fast_kernel(
+__global__ void __launch_bounds__(kNT, 5) fast_kernel(
     const double* __restrict__ u, double* __restrict__ out, const LineConst* __restrict__ lcs,
     const double* __restrict__ tv, int64_t tv_stride, int64_t* __restrict__ blocks_out,
     unsigned long long* __restrict__ diag, FastParams p, FastBuffers b) {
