@@ -77,9 +77,11 @@ class CudaError(LaxolError):
     pass
 
 
-def load(path: str = LIB_PATH, required_symbols=None):
+def load(path: str | None = None, required_symbols=None):
     """Load the CUDA library; raises OSError if it was not built."""
     global _lib
+    if path is None:
+        path = LIB_PATH
     if _lib is not None and path == LIB_PATH:
         return _lib
     if not os.path.exists(path):
