@@ -52,7 +52,8 @@ constexpr int kG = 256;        // sub-tile (slope statistics granularity)
 constexpr int kSub = kT / kG;  // sub-tiles per tile (= warps per CTA)
 constexpr int kPer = kT / kNT; // outputs / sources per thread
 constexpr int kKCap = 2048;    // K values staged in shared memory
-constexpr int kQCap = 512;     // queued long source intervals per chunk
+constexpr int kQCap = 128;     // queued long source intervals per chunk
+constexpr int kC = 4096;       // sources staged per chunk (a typical tile + halo in one pass)
 
 struct LineConst {
     long long first;  // window displacement of w = 0
@@ -340,7 +341,7 @@ __global__ void combine_blocks_kernel(const unsigned long long* __restrict__ fsm
 struct MainShared {
     unsigned long long keys[kT + 4];   // candidates, lane-interleaved access (no padding)
     unsigned long long mbar;           // TMA completion barrier for the source chunk
-    __align__(16) double ubuf[P8(kT + 3) + 1];  // sources (unpadded) / then u^{n+1} (padded, stats)
+    __align__(16) double ubuf[kC + 8];  // sources (unpadded) / then u^{n+1} (padded, stats)
     int3 queue[kQCap];
     EpiShared epi;
     unsigned short lut[64 * 4];
@@ -419,7 +420,7 @@ __global__ void line_setup_kernel(const double* __restrict__ drift_arr, int64_t 
 // Main K2 kernel: one CTA = (tile of kT outputs, line); grid (tiles, lines).
 // All index arithmetic is 32-bit (n <= 2^29); "unrolled" source/output
 // indices y, j may lie in (-3n, 3n) and are reduced mod n only on access.
-__global__ void __launch_bounds__(kNT, 5) fast_kernel(
+__global__ void __launch_bounds__(kNT, 4) fast_kernel(
     const double* __restrict__ u, double* __restrict__ out, const LineConst* __restrict__ lcs,
     const double* __restrict__ tv, int64_t tv_stride, int64_t* __restrict__ blocks_out,
     unsigned long long* __restrict__ diag, FastParams p, FastBuffers b) {
@@ -435,7 +436,7 @@ __global__ void __launch_bounds__(kNT, 5) fast_kernel(
     const int jlo = j0 - 1;     // outputs evaluated: jlo .. jlo + jspan (unrolled)
     const int jspan = Tl + 2;
     const int jhi = jlo + jspan;
-    const bool big = n >= 2 * kT + 4;  // one conditional wrap suffices
+    const bool big = n >= kC + 8;  // one conditional wrap suffices for source loads
     const double* ul = u + line * p.n;
     const LineConst lc = lcs[line];
     const double tau = p.tau, ia = p.ia, pe = lc.pe, hl = lc.hl, hr = lc.hr;
@@ -509,8 +510,8 @@ __global__ void __launch_bounds__(kNT, 5) fast_kernel(
         const double kdrift = lc.drift;
         // ---- sources in chunks of kT ----
         unsigned mphase = 0;
-        for (int yc = ya; yc <= yb; yc += kT) {
-            const int clen = min(kT, yb - yc + 1);
+        for (int yc = ya; yc <= yb; yc += kC) {
+            const int clen = min(kC, yb - yc + 1);
             const int base = yc - jlo;  // output index of source i at d: base + i + d
             // U(yc-1 .. yc+clen) -> ubuf[sh .. sh+clen+1]
             int bm = yc - 1;  // yc in (-3n, 3n)
@@ -541,9 +542,11 @@ __global__ void __launch_bounds__(kNT, 5) fast_kernel(
                 // warp w takes chunk sources 256w + lane + 32m (consecutive lanes,
                 // consecutive sources: conflict-free shared accesses)
                 unsigned ninl = 0;
+                // the chunk's sources split evenly over the warps (multiples of 32)
+                const int per = ((clen + kNT - 1) / kNT) * 32;
 #pragma unroll 2
-                for (int m = 0; m < kPer; ++m) {
-                    const int i = warp * (32 * kPer) + lane + 32 * m;  // source index in the chunk
+                for (int m = 0; m < per / 32; ++m) {
+                    const int i = warp * per + lane + 32 * m;  // source index in the chunk
                     if (i >= clen) break;
                     const double ul0 = ub[i], u0 = ub[i + 1], ur0 = ub[i + 2];
                     const double zl = __dmul_rn(__dadd_rn(__dsub_rn(u0, ul0), pe), ia);
