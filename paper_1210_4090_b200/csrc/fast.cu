@@ -53,7 +53,8 @@ constexpr int kSub = kT / kG;  // sub-tiles per tile (= warps per CTA)
 constexpr int kPer = kT / kNT; // outputs / sources per thread
 constexpr int kKCap = 2048;    // K values staged in shared memory
 constexpr int kQCap = 128;     // queued long source intervals per chunk
-constexpr int kC = 4096;       // sources staged per chunk (a typical tile + halo in one pass)
+constexpr int kC = 3584;       // sources staged per chunk (a typical tile + halo in one pass)
+constexpr int kVCap = 640;     // v_d values staged per tile (TMA, with the first chunk)
 
 struct LineConst {
     long long first;  // window displacement of w = 0
@@ -343,9 +344,10 @@ struct MainShared {
     unsigned long long mbar;           // TMA completion barrier for the source chunk
     __align__(16) double ubuf[kC + 8];  // sources (unpadded) / then u^{n+1} (padded, stats)
     int3 queue[kQCap];
+    __align__(16) double vbuf[kVCap];
     EpiShared epi;
     unsigned short lut[64 * 4];
-    int ya, yb, nq;
+    int ya, yb, nq, dlo, dhi;
     unsigned int c_inline, c_queued, c_src, c_qent;
 };
 
@@ -452,6 +454,8 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
         S.nq = 0;
         S.ya = INT_MAX;
         S.yb = INT_MIN;
+        S.dlo = INT_MAX;
+        S.dhi = INT_MIN;
         S.c_inline = S.c_queued = S.c_src = S.c_qent = 0;
     }
     // reset the line statistics buffer two steps ahead
@@ -482,7 +486,7 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
         int k1 = k0;
         while (y1 - k1 * n >= n) ++k1;
         const int Q1 = k1 * subs + (y1 - k1 * n) / kG;
-        int ya = INT_MAX, yb = INT_MIN;
+        int ya = INT_MAX, yb = INT_MIN, dlo = INT_MAX, dhi = INT_MIN;
         for (int Q = Q0 + tid; Q <= Q1; Q += kNT) {
             const int k = Q >= 0 ? Q / subs : -((subs - 1 - Q) / subs);
             const int q = Q - k * subs;
@@ -494,19 +498,30 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
             if (dl <= dr && ys + dl <= jhi && ye + dr >= jlo) {
                 ya = min(ya, ys);
                 yb = max(yb, ye);
+                dlo = min(dlo, max(dl, jlo - ye));
+                dhi = max(dhi, min(dr, jhi - ys));
             }
         }
         ya = __reduce_min_sync(0xffffffffu, ya);
         yb = __reduce_max_sync(0xffffffffu, yb);
+        dlo = __reduce_min_sync(0xffffffffu, dlo);
+        dhi = __reduce_max_sync(0xffffffffu, dhi);
         if (lane == 0) {
             atomicMin(&S.ya, ya);
             atomicMax(&S.yb, yb);
+            atomicMin(&S.dlo, dlo);
+            atomicMax(&S.dhi, dhi);
         }
         __syncthreads();
         ya = S.ya;
         yb = S.yb;
-        // K(d) = tau*((0.5 v)v - P v) from the shared v_d table (L1/L2 resident)
-        const double* vt = p.vtab + p.vofs;
+        // K(d) = tau*((0.5 v)v - P v) from v_d: staged in shared memory with the
+        // first source chunk when the tile's displacement range fits, else L1/L2
+        const int vd0 = S.dlo - ((S.dlo + static_cast<int>(p.vofs)) & 1);  // 16-byte aligned start
+        const int vcnt = (S.dhi - vd0 + 2) & ~1;
+        const bool vstage = big && S.dhi >= S.dlo && vcnt <= kVCap;
+        const double* gvt = p.vtab + p.vofs;
+        const double* svt = S.vbuf - vd0;
         const double kdrift = lc.drift;
         // ---- sources in chunks of kT ----
         unsigned mphase = 0;
@@ -525,10 +540,12 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
                     const int s0 = bm - sh;                      // even, in [0, n)
                     const int cnt = (clen + 2 + sh + 1) & ~1;    // even count
                     const int c1 = min(cnt, n - s0);             // first segment (n even)
+                    const bool vfirst = vstage && yc == ya;
                     fence_proxy_async();
-                    mbar_expect_tx(&S.mbar, static_cast<unsigned>(cnt) * 8u);
+                    mbar_expect_tx(&S.mbar, static_cast<unsigned>(cnt + (vfirst ? vcnt : 0)) * 8u);
                     tma_load_1d(S.ubuf, ul + s0, static_cast<unsigned>(c1) * 8u, &S.mbar);
                     if (cnt > c1) tma_load_1d(S.ubuf + c1, ul, static_cast<unsigned>(cnt - c1) * 8u, &S.mbar);
+                    if (vfirst) tma_load_1d(S.vbuf, gvt + vd0, static_cast<unsigned>(vcnt) * 8u, &S.mbar);
                 }
                 mbar_wait(&S.mbar, mphase);
                 mphase ^= 1u;
@@ -555,8 +572,8 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
                     const int dl = max(max(__double2int_ru(zl + hl), DLg), -off);
                     const int dr = min(min(__double2int_rd(zr + hr), DRg), jspan - off);
                     if (dl <= dr) {
-                        const double v0 = __ldg(vt + dl);
-                        const double v1 = dl + 1 <= dr ? __ldg(vt + dl + 1) : 0.0;
+                        const double v0 = vstage ? svt[dl] : __ldg(gvt + dl);
+                        const double v1 = dl + 1 <= dr ? (vstage ? svt[dl + 1] : __ldg(gvt + dl + 1)) : 0.0;
                         smem_atomic_min(&S.keys[off + dl], dkey(__dadd_rn(u0, kval_v(v0, kdrift, tau))));
                         if (dl + 1 <= dr) smem_atomic_min(&S.keys[off + dl + 1], dkey(__dadd_rn(u0, kval_v(v1, kdrift, tau))));
                         ninl += min(dr - dl + 1, 2);
@@ -566,7 +583,7 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
                                 S.queue[slot] = make_int3(i, dl + 2, dr);
                             } else {
                                 for (int d = dl + 2; d <= dr; ++d)
-                                    smem_atomic_min(&S.keys[off + d], dkey(__dadd_rn(u0, kval_v(__ldg(vt + d), kdrift, tau))));
+                                    smem_atomic_min(&S.keys[off + d], dkey(__dadd_rn(u0, kval_v(vstage ? svt[d] : __ldg(gvt + d), kdrift, tau))));
                             }
                         }
                     }
@@ -583,7 +600,7 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
                     const int off = base + qe.x;
                     if (lane == 0) atomicAdd(&S.c_queued, static_cast<unsigned>(qe.z - qe.y + 1));
                     for (int d = qe.y + lane; d <= qe.z; d += 32)
-                        smem_atomic_min(&S.keys[off + d], dkey(__dadd_rn(uy, kval_v(__ldg(vt + d), kdrift, tau))));
+                        smem_atomic_min(&S.keys[off + d], dkey(__dadd_rn(uy, kval_v(vstage ? svt[d] : __ldg(gvt + d), kdrift, tau))));
                 }
                 __syncthreads();
                 if (tid == 0) {
