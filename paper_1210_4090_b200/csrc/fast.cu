@@ -523,6 +523,9 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
         const double* gvt = p.vtab + p.vofs;
         const double* svt = S.vbuf - vd0;
         const double kdrift = lc.drift;
+        // every candidate lies in [S.dlo, S.dhi] when the statistics describe u;
+        // clamping to it keeps stale statistics memory-safe (wrong, never out of bounds)
+        const int dlo_t = S.dlo, dhi_t = S.dhi;
         // ---- sources in chunks of kT ----
         unsigned mphase = 0;
         for (int yc = ya; yc <= yb; yc += kC) {
@@ -569,8 +572,8 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
                     const double zl = __dmul_rn(__dadd_rn(__dsub_rn(u0, ul0), pe), ia);
                     const double zr = __dmul_rn(__dadd_rn(__dsub_rn(ur0, u0), pe), ia);
                     const int off = base + i;  // output index of this source at d = 0
-                    const int dl = max(max(__double2int_ru(zl + hl), DLg), -off);
-                    const int dr = min(min(__double2int_rd(zr + hr), DRg), jspan - off);
+                    const int dl = max(max(__double2int_ru(zl + hl), dlo_t), -off);
+                    const int dr = min(min(__double2int_rd(zr + hr), dhi_t), jspan - off);
                     if (dl <= dr) {
                         const double v0 = vstage ? svt[dl] : __ldg(gvt + dl);
                         const double v1 = dl + 1 <= dr ? (vstage ? svt[dl + 1] : __ldg(gvt + dl + 1)) : 0.0;
@@ -807,6 +810,9 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
         ctx->ws_shape[workspace] = std::make_pair(lines, n);
         flags &= ~LOB_FAST_STATS_VALID;
     }
+    // the statistics describe the previous call's output: any other input recomputes them
+    if (ctx->ws_last_out[workspace] != static_cast<const void*>(u)) flags &= ~LOB_FAST_STATS_VALID;
+    ctx->ws_last_out[workspace] = out;
     int64_t& counter = ctx->ws_counter[workspace];
     FastBuffers b = make_buffers(workspace, lines, n, counter);
     const WsLayout w = ws_layout(lines, n);

@@ -26,6 +26,7 @@ struct lob_ctx {
     // fast-engine workspaces: which statistics buffer holds the current u
     std::map<const void*, int64_t> ws_counter;
     std::map<const void*, std::pair<int64_t, int64_t>> ws_shape;
+    std::map<const void*, const void*> ws_last_out;  // workspace -> out of its last K2 call
     // scratch for host entry points
     void* scratch = nullptr;
     size_t scratch_bytes = 0;

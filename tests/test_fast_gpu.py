@@ -150,3 +150,16 @@ def oracle_step_subset(orc, u, K, first, tv, stride):
             vals.append(np.min(c) - tv[j])
         res.append((idx, np.array(vals)))
     return res
+
+
+def test_stats_valid_with_foreign_input_is_recomputed(dev, orc):
+    """LOB_FAST_STATS_VALID promises u is the previous call's out; when the
+    pointer differs the statistics are recomputed instead of trusted."""
+    import torch
+    n, tau, lines = 4096, 0.01, 4
+    u1 = api.gen_c3_lines(0, lines, n)
+    u2 = np.sin(np.linspace(0, 6 * np.pi, n, endpoint=False))[None, :].repeat(lines, 0) * 0.3
+    ws = torch.empty(dev.fast_workspace_bytes(lines, n), dtype=torch.uint8, device="cuda")
+    fast_step(dev, u1, 0.2, tau, ws=ws)
+    got, _ = fast_step(dev, u2, 0.2, tau, ws=ws, flags=api.FAST_STATS_VALID)
+    assert np.array_equal(got.cpu().numpy(), oracle_step(orc, u2, 0.2, tau))

@@ -164,3 +164,96 @@ def test_gpu_c3_c2_split_golden(dev):
                           b=api.c4_time_term(0.35 + 0.05), engine=engine, workspace=wsp)
         torch.cuda.synchronize()
         assert np.array_equal(o.cpu().numpy(), g["out32"])
+
+
+# ---------------------------------------------------------------- long-run fixtures (make_golden_long.py)
+
+def test_oracle_c2_hbar_sweep_n1024_golden(orc):
+    """One line of the N=1024 C2 sweep in full (5000 steps) with the oracle."""
+    g = load("c2_hbar_n1024.npz")
+    n, tau, k = 1024, 0.02, 1  # keep[1] = line 37
+    line = int(g["keep"][k])
+    w, first, _, _ = orc.kernel(n, tau, float(g["drifts"][line]))
+    tv = api.tau_v(g["v"], tau)
+    u = np.zeros(n)
+    for i in range(5000):
+        nxt = orc.direct(u[None, :], w, first, tv=tv)[0]
+        if i % 499 == 0:
+            assert orc.drift(nxt, u)[0] == g["step_drift"][k][i]
+        u = nxt
+    assert np.array_equal(u, g["u_final"][k])
+    assert np.sum(u) / n / (5000 * tau) == g["hbar"][line]
+
+
+def test_oracle_c4_n128_golden(orc):
+    g = load("c4_n128.npz")
+    n, tau = 128, 0.01
+    k1, f1, _, _ = orc.kernel(n, tau, 0.3)
+    k2, f2, _, _ = orc.kernel(n, tau, -0.7)
+    a = api.gen_cos(n)
+    u, k = g["u0"], 0
+    for i in range(int(g["at"][-1]) + 1):
+        tv = api.tau_v(np.add.outer(a, np.zeros(n)) * a[None, :] + api.c4_time_term(i * tau + tau), tau)
+        u = orc.split2d(u, k1, f1, k2, f2, tv=tv)
+        if i == g["at"][k]:
+            assert np.array_equal(u, g["states"][k]), i
+            k += 1
+
+
+@pytest.mark.gpu
+def test_gpu_c2_hbar_sweep_n1024_golden(dev):
+    """All 256 C2 drifts, 5000 steps at N=1024 (K2 via lob_evolve_f64): H-bar(P)
+    within 1e-12 relative of the reference's, kept lines bit-exact."""
+    import torch
+    g = load("c2_hbar_n1024.npz")
+    n, tau, steps, lines = 1024, 0.02, 5000, 256
+    u = torch.zeros((lines, n), dtype=torch.float64, device="cuda")
+    sc = torch.empty_like(u)
+    ws = torch.empty(dev.fast_workspace_bytes(lines, n), dtype=torch.uint8, device="cuda")
+    sb = torch.empty((steps, lines), dtype=torch.int64, device="cuda")
+    sd = torch.empty((steps, lines), dtype=torch.float64, device="cuda")
+    assert dev.evolve(u, sc, to_dev(g["drifts"]), tau, steps, tv=to_dev(api.tau_v(g["v"], tau)),
+                      step_drift=sd, step_blocks=sb, workspace=ws) == steps
+    uf = u.cpu().numpy()
+    hb = uf.sum(axis=1) / n / (steps * tau)
+    assert np.max(np.abs(hb - g["hbar"]) / np.abs(g["hbar"])) <= 1e-12
+    assert np.array_equal(uf[g["keep"]], g["u_final"])
+    assert np.array_equal(sb.cpu().numpy()[:, g["keep"]].T, g["step_blocks"])
+    assert np.max(np.abs(sd.cpu().numpy()[:, g["keep"]].T - g["step_drift"])) <= 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("engine", [api.ENGINE_FAST, api.ENGINE_DIRECT])
+def test_gpu_c5_spectrum_n16384_golden(dev, engine):
+    import torch
+    g = load("c5_n16384.npz")
+    n, tau, steps = 1 << 14, 0.005, 40
+    u = to_dev(g["u0"])
+    sc = torch.empty_like(u)
+    ws = torch.empty(dev.fast_workspace_bytes(2, n), dtype=torch.uint8, device="cuda")
+    sb = torch.empty((steps, 2), dtype=torch.int64, device="cuda")
+    assert dev.evolve(u, sc, to_dev(np.full(2, 0.25)), tau, steps, tv=to_dev(api.tau_v(g["v"], tau)),
+                      engine=engine, step_blocks=sb, workspace=ws) == steps
+    assert np.array_equal(u.cpu().numpy(), g["u_final"])
+    assert np.array_equal(sb.cpu().numpy().T, g["step_blocks"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("engine", [api.ENGINE_FAST, api.ENGINE_DIRECT])
+def test_gpu_c4_n128_golden(dev, engine):
+    import torch
+    g = load("c4_n128.npz")
+    n, tau = 128, 0.01
+    a = to_dev(api.gen_cos(n))
+    u = to_dev(g["u0"])
+    o, t = torch.empty_like(u), torch.empty_like(u)
+    ws = torch.empty(dev.fast_workspace_bytes(n, n), dtype=torch.uint8, device="cuda")
+    k = 0
+    for i in range(int(g["at"][-1]) + 1):
+        dev.split_step_2d(u, o, t, tau, 0.3, -0.7, a1=a, a2=a, b=api.c4_time_term(i * tau + tau),
+                          engine=engine, workspace=ws)
+        u, o = o, u
+        if i == g["at"][k]:
+            torch.cuda.synchronize()
+            assert np.array_equal(u.cpu().numpy(), g["states"][k]), i
+            k += 1
