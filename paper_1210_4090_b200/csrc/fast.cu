@@ -64,6 +64,7 @@ struct LineConst {
     double drift;
 };
 static_assert(kSub == kNT / 32, "one warp per sub-tile in the epilogue");
+static_assert(kPer % 2 == 0, "FSM pairs");
 
 struct FastParams {
     int64_t n;
@@ -139,7 +140,12 @@ __device__ __forceinline__ unsigned long long fsm_compose(unsigned long long a, 
     return fsm_pack(v, cnt);
 }
 
-__constant__ unsigned short c_fsm_lut[64 * 4];
+// Pair table: entry (v, c0, c1) = v' | emit_run0 << 6 | emit_run1 << 9 | emit_run2 << 12
+// after classes c0 then c1 (class 3 = no increment).  A run emits at most once
+// per pair (an emission leaves it undetermined), so 4 pairs accumulate into
+// 3-bit fields.  1024 x 2 B, copied to shared memory by each CTA.
+__device__ unsigned short g_fsm_lut2[64 * 16];
+constexpr int kLut2 = 64 * 16;
 
 __device__ __forceinline__ unsigned long long warp_fsm(unsigned long long f) {
     const int lane = threadIdx.x & 31;
@@ -208,8 +214,8 @@ __device__ __forceinline__ double hkey_upper(unsigned k) {
 //  * per line: the same bounds over the whole line (global atomics);
 //  * per tile: decompose()'s 3-state transition summary (FSM of
 //    proj/src/minplus.cpp:161-187).  For eta == 0 the increment class is the
-//    exact comparison of consecutive slopes (fl(a-b) > 0 <=> a > b), made on
-//    order-preserving keys of s + 0.0 (so -0 == +0 like the reference's inc == 0).
+//    exact comparison of consecutive slopes (fl(a-b) > 0 <=> a > b for finite
+//    doubles; -0 == +0 like the reference's inc == 0).
 __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line, int64_t tile,
                            const FastParams& p, const FastBuffers& b, EpiShared& sh,
                            const unsigned short* lut) {
@@ -220,7 +226,7 @@ __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line,
     for (int m = 0; m < kPer + 3; ++m) w[m] = (i0 + m <= Tl + 2) ? vals[P8(i0 + m)] : 0.0;
     double sl[kPer + 2];
 #pragma unroll
-    for (int m = 0; m < kPer + 2; ++m) sl[m] = __dadd_rn(__dsub_rn(w[m + 1], w[m]), 0.0);
+    for (int m = 0; m < kPer + 2; ++m) sl[m] = __dsub_rn(w[m + 1], w[m]);
     unsigned kmin = 0xffffffffu, kmax = 0u;
 #pragma unroll
     for (int m = 0; m <= kPer; ++m) {
@@ -230,31 +236,27 @@ __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line,
             kmax = max(kmax, k);
         }
     }
-    // decompose() FSM over increments e = j0 + 8t + 1 + k: inc = s(e) - s(e-1)
+    // decompose() FSM over increments e = j0 + 8t + 1 + k: inc = s(e) - s(e-1),
+    // two increments per table lookup.  Non-finite u (which the reference
+    // rejects before decompose, proj/src/scheme.cpp:18-24) is not classified.
     int v = 0 | (1 << 2) | (2 << 4);
-    int cnt[3] = {0, 0, 0};
+    unsigned acc = 0;
     const bool exact_cmp = p.eta == 0.0;
-    unsigned long long kprev = dkey(sl[0 + 1]);
+    auto cls = [&](int k) -> int {  // class of increment e = j0 + i0 + 1 + k
+        const int i = i0 + 1 + k;
+        if (!(i <= Tl && j0 + i <= p.n - 1)) return 3;
+        if (exact_cmp) return sl[k + 2] > sl[k + 1] ? 0 : (sl[k + 2] < sl[k + 1] ? 1 : 2);
+        const double inc = __dsub_rn(sl[k + 2], sl[k + 1]);
+        return inc > p.eta ? 0 : (inc < -p.eta ? 1 : 2);
+    };
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-        const int i = i0 + 1 + k;  // e = j0 + i
-        const unsigned long long kc = dkey(sl[k + 2]);
-        if (i <= Tl && j0 + i <= p.n - 1) {
-            int c;
-            if (exact_cmp) {
-                c = kc > kprev ? 0 : (kc < kprev ? 1 : 2);
-                if (!(sl[k + 2] == sl[k + 2]) || !(sl[k + 1] == sl[k + 1])) c = 3;
-            } else {
-                c = fsm_class(__dsub_rn(sl[k + 2], sl[k + 1]), p.eta);
-            }
-            const int x = lut[v * 4 + c];
-            v = x & 63;
-            cnt[0] += (x >> 6) & 1;
-            cnt[1] += (x >> 7) & 1;
-            cnt[2] += (x >> 8) & 1;
-        }
-        kprev = kc;
+    for (int k = 0; k < kPer; k += 2) {
+        const unsigned x = lut[v * 16 + cls(k) * 4 + cls(k + 1)];
+        v = static_cast<int>(x & 63u);
+        acc += x >> 6;
     }
+    const int cnt[3] = {static_cast<int>(acc & 7u), static_cast<int>((acc >> 3) & 7u),
+                        static_cast<int>(acc >> 6)};
     sh.fsm[tid] = fsm_pack(v, cnt);
     kmin = __reduce_min_sync(0xffffffffu, kmin);
     kmax = __reduce_max_sync(0xffffffffu, kmax);
@@ -291,8 +293,8 @@ __global__ void __launch_bounds__(kNT) stats_kernel(const double* __restrict__ u
                                                     FastBuffers b) {
     __shared__ __align__(16) double vals[P8(kT + 3) + 1];
     __shared__ EpiShared sh;
-    __shared__ unsigned short lut[64 * 4];
-    if (threadIdx.x < 64 * 4) lut[threadIdx.x] = c_fsm_lut[threadIdx.x];
+    __shared__ unsigned short lut[kLut2];
+    for (int i = threadIdx.x; i < kLut2; i += kNT) lut[i] = __ldg(g_fsm_lut2 + i);
     const int64_t line = blockIdx.x / p.tiles;
     const int64_t tile = blockIdx.x - line * p.tiles;
     const int64_t j0 = tile * kT;
@@ -346,8 +348,8 @@ struct MainShared {
     int3 queue[kQCap];
     __align__(16) double vbuf[kVCap];
     EpiShared epi;
-    unsigned short lut[64 * 4];
-    int ya, yb, nq, dlo, dhi;
+    unsigned short lut[kLut2];
+    int ya, yb, nq, dlo, dhi, DLg, DRg, ok;
     unsigned int c_inline, c_queued, c_src, c_qent;
 };
 
@@ -379,14 +381,36 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-__device__ __forceinline__ void smem_atomic_min(unsigned long long* addr, unsigned long long key) {
-    // fast path: the first candidate of an output replaces the +inf sentinel
-    unsigned long long old = atomicCAS(addr, kKeyInf, key);
-    while (old != kKeyInf && key < old) {
-        const unsigned long long prev = atomicCAS(addr, old, key);
+constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;  // +inf
+
+// exact min of doubles in shared memory (CAS on the bit pattern; the first
+// candidate of an output replaces the +inf sentinel)
+__device__ __forceinline__ void smem_fmin(unsigned long long* addr, double c) {
+    const unsigned long long cb = static_cast<unsigned long long>(__double_as_longlong(c));
+    unsigned long long old = atomicCAS(addr, kInfBits, cb);
+    while (old != kInfBits && c < __longlong_as_double(static_cast<long long>(old))) {
+        const unsigned long long prev = atomicCAS(addr, old, cb);
         if (prev == old) break;
         old = prev;
     }
+}
+
+// One thread: TMA bulk copies of U(yc-1 .. yc+clen) (wrapped at the period,
+// 16-byte aligned even start) into ubuf, plus optionally vcnt v_d values.
+__device__ __forceinline__ void issue_chunk(MainShared& S, const double* ul, int n, int yc, int clen,
+                                            const double* vsrc, int vcnt) {
+    int bm = yc - 1;
+    while (bm < 0) bm += n;
+    while (bm >= n) bm -= n;
+    const int sh = bm & 1;
+    const int s0 = bm - sh;                    // even, in [0, n)
+    const int cnt = (clen + 2 + sh + 1) & ~1;  // even count
+    const int c1 = min(cnt, n - s0);           // first segment (n even)
+    fence_proxy_async();
+    mbar_expect_tx(&S.mbar, static_cast<unsigned>(cnt + (vsrc ? vcnt : 0)) * 8u);
+    tma_load_1d(S.ubuf, ul + s0, static_cast<unsigned>(c1) * 8u, &S.mbar);
+    if (cnt > c1) tma_load_1d(S.ubuf + c1, ul, static_cast<unsigned>(cnt - c1) * 8u, &S.mbar);
+    if (vsrc) tma_load_1d(S.vbuf, vsrc, static_cast<unsigned>(vcnt) * 8u, &S.mbar);
 }
 
 // Per-line constants of the step (identical IEEE operations to the host's
@@ -446,123 +470,124 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
     const int dmin_w = first + 1, dmax_w = first + 2 * n - 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-    for (int i = tid; i <= jspan; i += kNT) S.keys[i] = kKeyInf;
-    if (tid < 64 * 4) S.lut[tid] = c_fsm_lut[tid];
-    if (tid == 0) {
-        mbar_init(&S.mbar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        S.nq = 0;
-        S.ya = INT_MAX;
-        S.yb = INT_MIN;
-        S.dlo = INT_MAX;
-        S.dhi = INT_MIN;
-        S.c_inline = S.c_queued = S.c_src = S.c_qent = 0;
-    }
+    for (int i = tid; i <= jspan; i += kNT) S.keys[i] = kInfBits;
+    for (int i = tid; i < kLut2; i += kNT) S.lut[i] = __ldg(g_fsm_lut2 + i);
     // reset the line statistics buffer two steps ahead
     if (tile == 0 && tid < 4) b.line_reset[line * 4 + tid] = (tid & 1) ? 0ull : ~0ull;
 
-    // ---- line statistics: oscillation gate and global displacement bounds ----
-    const unsigned long long* L = b.line_in + line * 4;
-    const double smin = dkey_inv(L[2]), smax = dkey_inv(L[3]);
-    int DLg = dmin_w, DRg = dmax_w;
-    // oscillation of a periodic line <= (n/2) max|slope| (shorter arc)
-    const double osc_bound = 0.5 * static_cast<double>(n) * fmax(fabs(smin), fabs(smax));
-    bool ok = (osc_bound * (1.0 + 1e-12) < lc.gap * (1.0 - 1e-12)) && n >= 3 && isfinite(smin) &&
-              isfinite(smax);
-    if (ok) {
-        DLg = max(__double2int_ru(__dmul_rn(__dadd_rn(smin, pe), ia) + hl), dmin_w);
-        DRg = min(__double2int_rd(__dmul_rn(__dadd_rn(smax, pe), ia) + hr), dmax_w);
-        ok = DLg <= DRg;
-    }
-    __syncthreads();  // keys / counters initialised
-
-    if (ok) {
-        // ---- candidate sub-tiles: unrolled sources y in [jlo - DRg, jhi - DLg] ----
-        const int y0 = jlo - DRg, y1 = jhi - DLg;
-        int k0 = 0;
-        while (y0 - k0 * n < 0) --k0;
-        while (y0 - k0 * n >= n) ++k0;
-        const int Q0 = k0 * subs + (y0 - k0 * n) / kG;
-        int k1 = k0;
-        while (y1 - k1 * n >= n) ++k1;
-        const int Q1 = k1 * subs + (y1 - k1 * n) / kG;
+    // ---- warp 0: line gate, candidate sub-tiles, first TMA issue ----
+    if (warp == 0) {
+        // line statistics: oscillation gate and global displacement bounds
+        const unsigned long long* L = b.line_in + line * 4;
+        const double smin = dkey_inv(L[2]), smax = dkey_inv(L[3]);
+        int DLg = dmin_w, DRg = dmax_w;
+        // oscillation of a periodic line <= (n/2) max|slope| (shorter arc)
+        const double osc_bound = 0.5 * static_cast<double>(n) * fmax(fabs(smin), fabs(smax));
+        bool okl = (osc_bound * (1.0 + 1e-12) < lc.gap * (1.0 - 1e-12)) && n >= 3 && isfinite(smin) &&
+                   isfinite(smax);
+        if (okl) {
+            DLg = max(__double2int_ru(__dmul_rn(__dadd_rn(smin, pe), ia) + hl), dmin_w);
+            DRg = min(__double2int_rd(__dmul_rn(__dadd_rn(smax, pe), ia) + hr), dmax_w);
+            okl = DLg <= DRg;
+        }
         int ya = INT_MAX, yb = INT_MIN, dlo = INT_MAX, dhi = INT_MIN;
-        for (int Q = Q0 + tid; Q <= Q1; Q += kNT) {
-            const int k = Q >= 0 ? Q / subs : -((subs - 1 - Q) / subs);
-            const int q = Q - k * subs;
-            const double2 sb = b.sub_in[line * p.subs + q];
-            const int ys = k * n + q * kG;
-            const int ye = ys + min(kG, n - q * kG) - 1;
-            const int dl = max(__double2int_ru(__dmul_rn(__dadd_rn(sb.x, pe), ia) + hl), DLg);
-            const int dr = min(__double2int_rd(__dmul_rn(__dadd_rn(sb.y, pe), ia) + hr), DRg);
-            if (dl <= dr && ys + dl <= jhi && ye + dr >= jlo) {
-                ya = min(ya, ys);
-                yb = max(yb, ye);
-                dlo = min(dlo, max(dl, jlo - ye));
-                dhi = max(dhi, min(dr, jhi - ys));
+        if (okl) {
+            // candidate sub-tiles: unrolled sources y in [jlo - DRg, jhi - DLg]
+            const int y0 = jlo - DRg, y1 = jhi - DLg;
+            int k0 = 0;
+            while (y0 - k0 * n < 0) --k0;
+            while (y0 - k0 * n >= n) ++k0;
+            const int Q0 = k0 * subs + (y0 - k0 * n) / kG;
+            int k1 = k0;
+            while (y1 - k1 * n >= n) ++k1;
+            const int Q1 = k1 * subs + (y1 - k1 * n) / kG;
+            for (int Q = Q0 + lane; Q <= Q1; Q += 32) {
+                const int k = Q >= 0 ? Q / subs : -((subs - 1 - Q) / subs);
+                const int q = Q - k * subs;
+                const double2 sb = b.sub_in[line * p.subs + q];
+                const int ys = k * n + q * kG;
+                const int ye = ys + min(kG, n - q * kG) - 1;
+                const int dl = max(__double2int_ru(__dmul_rn(__dadd_rn(sb.x, pe), ia) + hl), DLg);
+                const int dr = min(__double2int_rd(__dmul_rn(__dadd_rn(sb.y, pe), ia) + hr), DRg);
+                if (dl <= dr && ys + dl <= jhi && ye + dr >= jlo) {
+                    ya = min(ya, ys);
+                    yb = max(yb, ye);
+                    dlo = min(dlo, max(dl, jlo - ye));
+                    dhi = max(dhi, min(dr, jhi - ys));
+                }
+            }
+            ya = __reduce_min_sync(0xffffffffu, ya);
+            yb = __reduce_max_sync(0xffffffffu, yb);
+            dlo = __reduce_min_sync(0xffffffffu, dlo);
+            dhi = __reduce_max_sync(0xffffffffu, dhi);
+        }
+        if (lane == 0) {
+            S.ok = okl;
+            S.DLg = DLg;
+            S.DRg = DRg;
+            S.ya = ya;
+            S.yb = yb;
+            S.dlo = dlo;
+            S.dhi = dhi;
+            S.nq = 0;
+            S.c_inline = S.c_queued = S.c_src = S.c_qent = 0;
+            mbar_init(&S.mbar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            if (okl && big && ya <= yb) {
+                // first source chunk + the tile's v_d range, in flight across the barrier
+                const int vd0 = dlo - ((dlo + static_cast<int>(p.vofs)) & 1);
+                const int vcnt = (dhi - vd0 + 2) & ~1;
+                issue_chunk(S, ul, n, ya, min(kC, yb - ya + 1), vcnt <= kVCap ? p.vtab + p.vofs + vd0 : nullptr,
+                            vcnt);
             }
         }
-        ya = __reduce_min_sync(0xffffffffu, ya);
-        yb = __reduce_max_sync(0xffffffffu, yb);
-        dlo = __reduce_min_sync(0xffffffffu, dlo);
-        dhi = __reduce_max_sync(0xffffffffu, dhi);
-        if (lane == 0) {
-            atomicMin(&S.ya, ya);
-            atomicMax(&S.yb, yb);
-            atomicMin(&S.dlo, dlo);
-            atomicMax(&S.dhi, dhi);
-        }
-        __syncthreads();
-        ya = S.ya;
-        yb = S.yb;
-        // K(d) = tau*((0.5 v)v - P v) from v_d: staged in shared memory with the
-        // first source chunk when the tile's displacement range fits, else L1/L2
-        const int vd0 = S.dlo - ((S.dlo + static_cast<int>(p.vofs)) & 1);  // 16-byte aligned start
-        const int vcnt = (S.dhi - vd0 + 2) & ~1;
-        const bool vstage = big && S.dhi >= S.dlo && vcnt <= kVCap;
-        const double* gvt = p.vtab + p.vofs;
-        const double* svt = S.vbuf - vd0;
-        const double kdrift = lc.drift;
-        // every candidate lies in [S.dlo, S.dhi] when the statistics describe u;
-        // clamping to it keeps stale statistics memory-safe (wrong, never out of bounds)
+    }
+    __syncthreads();  // keys, LUT, gate, ranges, mbarrier initialised
+    const bool ok = S.ok;
+
+    if (ok) {
+        const int ya = S.ya, yb = S.yb;
         const int dlo_t = S.dlo, dhi_t = S.dhi;
-        // ---- sources in chunks of kT ----
+        // K(d) = tau*((0.5 v)v - P v): staged in shared memory (TMA'd v_d, converted
+        // in place) when the tile's displacement range fits, else from the global v_d table
+        const int vd0 = dlo_t - ((dlo_t + static_cast<int>(p.vofs)) & 1);
+        const int vcnt = (dhi_t - vd0 + 2) & ~1;
+        const bool kstage = big && dhi_t >= dlo_t && vcnt <= kVCap;
+        const double* gvt = p.vtab + p.vofs;
+        const double* skt = S.vbuf - vd0;
+        const double kdrift = lc.drift;
+        auto kd = [&](int d) -> double { return kstage ? skt[d] : kval_v(__ldg(gvt + d), kdrift, tau); };
+        // ---- sources in chunks of kC ----
         unsigned mphase = 0;
         for (int yc = ya; yc <= yb; yc += kC) {
             const int clen = min(kC, yb - yc + 1);
             const int base = yc - jlo;  // output index of source i at d: base + i + d
-            // U(yc-1 .. yc+clen) -> ubuf[sh .. sh+clen+1]
-            int bm = yc - 1;  // yc in (-3n, 3n)
-            while (bm < 0) bm += n;
-            while (bm >= n) bm -= n;
             int sh = 0;
             if (big) {
-                // TMA bulk copies: 16-byte aligned even start, wrapped at the period
+                int bm = yc - 1;
+                while (bm < 0) bm += n;
+                while (bm >= n) bm -= n;
                 sh = bm & 1;
-                if (tid == 0) {
-                    const int s0 = bm - sh;                      // even, in [0, n)
-                    const int cnt = (clen + 2 + sh + 1) & ~1;    // even count
-                    const int c1 = min(cnt, n - s0);             // first segment (n even)
-                    const bool vfirst = vstage && yc == ya;
-                    fence_proxy_async();
-                    mbar_expect_tx(&S.mbar, static_cast<unsigned>(cnt + (vfirst ? vcnt : 0)) * 8u);
-                    tma_load_1d(S.ubuf, ul + s0, static_cast<unsigned>(c1) * 8u, &S.mbar);
-                    if (cnt > c1) tma_load_1d(S.ubuf + c1, ul, static_cast<unsigned>(cnt - c1) * 8u, &S.mbar);
-                    if (vfirst) tma_load_1d(S.vbuf, gvt + vd0, static_cast<unsigned>(vcnt) * 8u, &S.mbar);
-                }
-                mbar_wait(&S.mbar, mphase);
+                if (yc != ya && tid == 0) issue_chunk(S, ul, n, yc, clen, nullptr, 0);
+                if (warp == 0) mbar_wait(&S.mbar, mphase);
                 mphase ^= 1u;
+                __syncthreads();
+                if (yc == ya && kstage) {
+                    for (int i = tid; i < vcnt; i += kNT) S.vbuf[i] = kval_v(S.vbuf[i], kdrift, tau);
+                    __syncthreads();
+                }
             } else {
+                int bm = yc - 1;
+                while (bm < 0) bm += n;
                 for (int i = tid; i < clen + 2; i += kNT) S.ubuf[i] = __ldg(ul + (bm + i) % n);
                 __syncthreads();
             }
             const double* ub = S.ubuf + sh;
-            if (tid == 0) atomicAdd(&S.c_src, static_cast<unsigned>(clen));
+            if (tid == 0) S.c_src += static_cast<unsigned>(clen);
             {
-                // warp w takes chunk sources 256w + lane + 32m (consecutive lanes,
+                // warp w takes chunk sources w*per + lane + 32m (consecutive lanes,
                 // consecutive sources: conflict-free shared accesses)
                 unsigned ninl = 0;
-                // the chunk's sources split evenly over the warps (multiples of 32)
                 const int per = ((clen + kNT - 1) / kNT) * 32;
 #pragma unroll 2
                 for (int m = 0; m < per / 32; ++m) {
@@ -572,21 +597,22 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
                     const double zl = __dmul_rn(__dadd_rn(__dsub_rn(u0, ul0), pe), ia);
                     const double zr = __dmul_rn(__dadd_rn(__dsub_rn(ur0, u0), pe), ia);
                     const int off = base + i;  // output index of this source at d = 0
+                    // every candidate lies in [dlo_t, dhi_t] when the statistics describe u;
+                    // the clamp keeps stale statistics memory-safe (wrong, never out of bounds)
                     const int dl = max(max(__double2int_ru(zl + hl), dlo_t), -off);
                     const int dr = min(min(__double2int_rd(zr + hr), dhi_t), jspan - off);
                     if (dl <= dr) {
-                        const double v0 = vstage ? svt[dl] : __ldg(gvt + dl);
-                        const double v1 = dl + 1 <= dr ? (vstage ? svt[dl + 1] : __ldg(gvt + dl + 1)) : 0.0;
-                        smem_atomic_min(&S.keys[off + dl], dkey(__dadd_rn(u0, kval_v(v0, kdrift, tau))));
-                        if (dl + 1 <= dr) smem_atomic_min(&S.keys[off + dl + 1], dkey(__dadd_rn(u0, kval_v(v1, kdrift, tau))));
+                        const double k0v = kd(dl);
+                        const double k1v = dl + 1 <= dr ? kd(dl + 1) : 0.0;
+                        smem_fmin(&S.keys[off + dl], __dadd_rn(u0, k0v));
+                        if (dl + 1 <= dr) smem_fmin(&S.keys[off + dl + 1], __dadd_rn(u0, k1v));
                         ninl += min(dr - dl + 1, 2);
                         if (dl + 2 <= dr) {
                             const int slot = atomicAdd(&S.nq, 1);
                             if (slot < kQCap) {
                                 S.queue[slot] = make_int3(i, dl + 2, dr);
                             } else {
-                                for (int d = dl + 2; d <= dr; ++d)
-                                    smem_atomic_min(&S.keys[off + d], dkey(__dadd_rn(u0, kval_v(vstage ? svt[d] : __ldg(gvt + d), kdrift, tau))));
+                                for (int d = dl + 2; d <= dr; ++d) smem_fmin(&S.keys[off + d], __dadd_rn(u0, kd(d)));
                             }
                         }
                     }
@@ -602,16 +628,15 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
                     const double uy = ub[qe.x + 1];
                     const int off = base + qe.x;
                     if (lane == 0) atomicAdd(&S.c_queued, static_cast<unsigned>(qe.z - qe.y + 1));
-                    for (int d = qe.y + lane; d <= qe.z; d += 32)
-                        smem_atomic_min(&S.keys[off + d], dkey(__dadd_rn(uy, kval_v(vstage ? svt[d] : __ldg(gvt + d), kdrift, tau))));
+                    for (int d = qe.y + lane; d <= qe.z; d += 32) smem_fmin(&S.keys[off + d], __dadd_rn(uy, kd(d)));
                 }
                 __syncthreads();
                 if (tid == 0) {
                     S.c_qent += nq;
                     S.nq = 0;
                 }
+                __syncthreads();
             }
-            __syncthreads();
         }
     }
 
@@ -623,7 +648,7 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
     auto finish = [&](int i, int j, double tvj) -> double {
         const unsigned long long kk = S.keys[i];
         double best;
-        if (kk == kKeyInf) {
+        if (kk == kInfBits) {
             if (ok && diag) atomicAdd(diag, 1ull);
             // direct scan of the full window (proj/tests/unit_scheme.cpp:184-190)
             best = INFINITY;
@@ -635,7 +660,7 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
                 y = y == 0 ? n - 1 : y - 1;
             }
         } else {
-            best = dkey_inv(kk);
+            best = __longlong_as_double(static_cast<long long>(kk));
         }
         return tvl ? __dsub_rn(best, tvj) : best;
     };
@@ -718,20 +743,25 @@ static bool g_lut_ready = false;
 
 static int ensure_lut(lob_ctx* ctx) {
     if (g_lut_ready) return LOB_OK;
-    unsigned short lut[64 * 4];
+    unsigned short lut[kLut2];
     for (int v = 0; v < 64; ++v)
-        for (int c = 0; c < 4; ++c) {
-            int nv = 0, em = 0;
-            for (int q = 0; q < 3; ++q) {
-                const int st = (v >> (2 * q)) & 3;
-                int e = 0;
-                const int ns = st > 2 ? 0 : fsm_next(st, c, &e);
-                nv |= ns << (2 * q);
-                em |= e << q;
+        for (int c0 = 0; c0 < 4; ++c0)
+            for (int c1 = 0; c1 < 4; ++c1) {
+                int nv = 0;
+                unsigned em = 0;
+                for (int q = 0; q < 3; ++q) {
+                    int st = (v >> (2 * q)) & 3;
+                    if (st > 2) st = 0;
+                    int e = 0, e2 = 0;
+                    if (c0 < 3) st = fsm_next(st, c0, &e);
+                    if (c1 < 3) st = fsm_next(st, c1, &e2);
+                    nv |= st << (2 * q);
+                    if (e + e2 > 1) return set_error(ctx, LOB_CUDA_ERROR, "fsm table: two emits per pair");
+                    em |= static_cast<unsigned>(e + e2) << (3 * q);
+                }
+                lut[v * 16 + c0 * 4 + c1] = static_cast<unsigned short>(static_cast<unsigned>(nv) | (em << 6));
             }
-            lut[v * 4 + c] = static_cast<unsigned short>(nv | (em << 6));
-        }
-    LOB_CUDA_TRY(ctx, cudaMemcpyToSymbol(c_fsm_lut, lut, sizeof(lut)));
+    LOB_CUDA_TRY(ctx, cudaMemcpyToSymbol(g_fsm_lut2, lut, sizeof(lut)));
     g_lut_ready = true;
     return LOB_OK;
 }
