@@ -21,6 +21,8 @@ LOB_CUDA_ERROR = 3
 ENGINE_DIRECT = 0
 ENGINE_FAST = 1
 FAST_STATS_VALID = 1
+DIRECT_SCREENED = 0
+DIRECT_PLAIN = 1
 
 # name -> (restype, argtypes); every symbol declared in include/laxol_b200.h
 # and include/laxol_b200_configs.h.
@@ -47,6 +49,8 @@ SIGNATURES = {
     "lob_block_counts": (c_int, [_P, _P, c_int64, c_int64, c_double, _P, _P]),
     "lob_bench_fp64": (c_int, [_P, POINTER(c_double), POINTER(c_double), POINTER(c_double)]),
     "lob_launch_count": (c_int64, [_P]),
+    "lob_ctx_set_direct_mode": (c_int, [_P, c_int]),
+    "lob_direct_fallbacks": (c_int, [_P, POINTER(c_uint64), c_int]),
     # synthetic workloads (include/laxol_b200_configs.h)
     "lob_gen_sin": (None, [c_int64, _P]),
     "lob_gen_cos": (None, [c_int64, _P]),

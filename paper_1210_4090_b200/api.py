@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _capi
-from ._capi import (ENGINE_DIRECT, ENGINE_FAST, FAST_STATS_VALID, EvaluationError,  # noqa: F401
+from ._capi import (DIRECT_PLAIN, DIRECT_SCREENED, ENGINE_DIRECT, ENGINE_FAST, FAST_STATS_VALID, EvaluationError,  # noqa: F401
                     InvalidInput, check)
 
 
@@ -118,6 +118,16 @@ class Device:
     def launches(self) -> int:
         return int(self.lib.lob_launch_count(self.ctx))
 
+    def set_direct_mode(self, mode: int) -> None:
+        """DIRECT_SCREENED (default: fp32 screen + fp64 re-evaluation) or DIRECT_PLAIN."""
+        self._check(self.lib.lob_ctx_set_direct_mode(self.ctx, int(mode)), "lob_ctx_set_direct_mode")
+
+    def direct_fallbacks(self, reset: bool = True) -> int:
+        """Outputs the screened K1 swept in full fp64 since the last reset."""
+        v = ctypes.c_uint64()
+        self._check(self.lib.lob_direct_fallbacks(self.ctx, ctypes.byref(v), int(reset)), "lob_direct_fallbacks")
+        return int(v.value)
+
     # ---- kernels -----------------------------------------------------------
     def build_kernel(self, n_space: int, tau: float, drift: float) -> Kernel:
         """Host build_kernel for mechanical(drift) (proj/src/scheme.cpp:59-105)."""
@@ -173,7 +183,7 @@ class Device:
         st = self.lib.lob_fast_diagnostics(self.ctx, _ptr(workspace), lines, n, v)
         self._check(st, "lob_fast_diagnostics")
         keys = ["missed_outputs", "sources", "inline_candidates", "queued_candidates", "queued_intervals",
-                "tiles", "r6", "r7", "cyc_init", "cyc_scan", "cyc_load", "cyc_emit", "cyc_epilogue", "cyc_stats"]
+                "tiles", "tiles_k_unstaged", "k_range_sum", "cyc_init", "cyc_scan", "cyc_load", "cyc_emit", "cyc_epilogue", "cyc_stats"]
         return {k: int(v[i]) for i, k in enumerate(keys)}
 
     def fast_diagnostics(self, workspace, lines: int, n: int) -> int:

@@ -57,12 +57,34 @@ int lob_ctx_destroy(lob_ctx* ctx) {
     cudaSetDevice(ctx->device);
     for (auto& kv : ctx->vtabs) cudaFree(kv.second.dev);
     if (ctx->scratch) cudaFree(ctx->scratch);
+    if (ctx->direct_full) cudaFree(ctx->direct_full);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return LOB_OK;
 }
 
 const char* lob_last_error(const lob_ctx* ctx) { return ctx ? ctx->last_error.c_str() : ""; }
+
+int lob_ctx_set_direct_mode(lob_ctx* ctx, int mode) {
+    if (!ctx) return LOB_INVALID_INPUT;
+    if (mode != LOB_DIRECT_SCREENED && mode != LOB_DIRECT_PLAIN)
+        return set_error(ctx, LOB_INVALID_INPUT, "lob_ctx_set_direct_mode: unknown mode");
+    ctx->direct_mode = mode;
+    return LOB_OK;
+}
+
+int lob_direct_fallbacks(lob_ctx* ctx, uint64_t* count, int reset) {
+    if (!ctx || !count) return LOB_INVALID_INPUT;
+    cudaSetDevice(ctx->device);
+    *count = 0;
+    if (!ctx->direct_full) return LOB_OK;
+    LOB_CUDA_TRY(ctx, cudaDeviceSynchronize());
+    unsigned long long v = 0;
+    LOB_CUDA_TRY(ctx, cudaMemcpy(&v, ctx->direct_full, sizeof(v), cudaMemcpyDeviceToHost));
+    *count = v;
+    if (reset) LOB_CUDA_TRY(ctx, cudaMemset(ctx->direct_full, 0, sizeof(v)));
+    return LOB_OK;
+}
 
 int64_t lob_launch_count(const lob_ctx* ctx) { return ctx ? ctx->launches : 0; }
 

@@ -109,15 +109,19 @@ __global__ void __launch_bounds__(NT) direct_kernel(const T* __restrict__ u, T* 
         }
         __syncthreads();
 
-        int i0 = t * R + TW;  // logical index of U(jt - first - wc)
+        // logical index of U(jt - first - wc) is i0 = t*R + TW (a multiple of R):
+        // padded(i0 + k) = pa + k and padded(i0 - 1 - k) = pa - 2 - k, pa = padded(i0)
+        const T* pa = Us + padded<R>(t * R + TW);
         T A[R];
 #pragma unroll
-        for (int k = 0; k < R; ++k) A[k] = Us[padded<R>(i0 + k)];
+        for (int k = 0; k < R; ++k) A[k] = pa[k];
+        // the last chunk stops at the window's end (rounded up to R)
+        const int send = static_cast<int>(min(static_cast<int64_t>(TW), (W - wc + R - 1) / R * R));
 #pragma unroll 1
-        for (int s0 = 0; s0 < TW; s0 += R) {
+        for (int s0 = 0; s0 < send; s0 += R) {
             T B[R];
 #pragma unroll
-            for (int k = 0; k < R; ++k) B[k] = Us[padded<R>(i0 - 1 - k)];
+            for (int k = 0; k < R; ++k) B[k] = pa[-2 - k];
 #pragma unroll
             for (int s = 0; s < R; ++s) {
                 const T kw = Ks[s0 + s];
@@ -130,7 +134,7 @@ __global__ void __launch_bounds__(NT) direct_kernel(const T* __restrict__ u, T* 
             }
 #pragma unroll
             for (int k = 0; k < R; ++k) A[k] = B[R - 1 - k];
-            i0 -= R;
+            pa -= R + 1;
         }
     }
 
@@ -201,9 +205,9 @@ __global__ void window_kernel(const double* __restrict__ u, double* __restrict__
 
 }  // namespace
 
-int launch_direct_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
-                      const double* ktab, int64_t ktab_stride, const int64_t* first,
-                      const double* tv, int64_t tv_stride, cudaStream_t s) {
+int launch_direct_plain_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
+                            const double* ktab, int64_t ktab_stride, const int64_t* first,
+                            const double* tv, int64_t tv_stride, cudaStream_t s) {
     if (n >= 2048)
         return launch_cfg<double, 16, 128, 1024>(ctx, u, out, lines, n, ktab, ktab_stride, first,
                                                  tv, tv_stride, s);

@@ -52,9 +52,13 @@ constexpr int kG = 256;        // sub-tile (slope statistics granularity)
 constexpr int kSub = kT / kG;  // sub-tiles per tile (= warps per CTA)
 constexpr int kPer = kT / kNT; // outputs / sources per thread
 constexpr int kKCap = 2048;    // K values staged in shared memory
-constexpr int kQCap = 128;     // queued long source intervals per chunk
+constexpr int kQCap = 256;     // queued source intervals (long / contended) per chunk
 constexpr int kC = 3584;       // sources staged per chunk (a typical tile + halo in one pass)
-constexpr int kVCap = 640;     // v_d values staged per tile (TMA, with the first chunk)
+#ifndef LOB_VCAP
+#define LOB_VCAP 1120
+#endif
+constexpr int kVCap = LOB_VCAP;  // v_d values staged per tile (TMA, with the first chunk)
+constexpr int kPfMargin = 256; // L2 prefetch margin around the central source range
 
 struct LineConst {
     long long first;  // window displacement of w = 0
@@ -341,17 +345,25 @@ __global__ void combine_blocks_kernel(const unsigned long long* __restrict__ fsm
     blocks[line] = 1 + em;
 }
 
-struct MainShared {
-    unsigned long long keys[kT + 4];   // candidates, lane-interleaved access (no padding)
-    unsigned long long mbar;           // TMA completion barrier for the source chunk
-    __align__(16) double ubuf[kC + 8];  // sources (unpadded) / then u^{n+1} (padded, stats)
-    int3 queue[kQCap];
-    __align__(16) double vbuf[kVCap];
+// After the emission phase the tail of ubuf holds the epilogue's reduction
+// scratch and the FSM table (u^{n+1} occupies the first P8(kT + 3) + 1 doubles).
+constexpr int kValsLen = P8(kT + 3) + 2;
+struct PostShared {
     EpiShared epi;
     unsigned short lut[kLut2];
+};
+struct MainShared {
+    unsigned long long keys[kT + 4];   // exact-min slots (+inf bits = empty), lane-interleaved access
+    unsigned long long mbar;           // TMA completion barrier for the source chunk
+    __align__(16) double ubuf[kC + 8];  // sources (unpadded) / then u^{n+1} (padded, stats) + PostShared
+    int3 queue[kQCap];
+    __align__(16) double vbuf[kVCap];  // v_d of the tile's displacement range, converted to K(d)
     int ya, yb, nq, dlo, dhi, DLg, DRg, ok;
     unsigned int c_inline, c_queued, c_src, c_qent;
+    __device__ PostShared& post() { return *reinterpret_cast<PostShared*>(ubuf + kValsLen); }
 };
+static_assert(kValsLen * 8 + sizeof(PostShared) <= (kC + 8) * 8, "post-emission scratch fits in ubuf");
+static_assert(4 * (sizeof(MainShared) + 1024) <= 233472, "four CTAs per SM");
 
 // ---- TMA bulk copies (cp.async.bulk) completed on an mbarrier ------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -379,9 +391,22 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
         "r"(phase)
         : "memory");
 }
+__device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;  // +inf
+
+// x in (-3n, 3n) -> x mod n in [0, n)
+__device__ __forceinline__ int wrap_idx(int x, int n) {
+    x += x < 0 ? n : 0;
+    x += x < 0 ? n : 0;
+    x += x < 0 ? n : 0;
+    x -= x >= n ? n : 0;
+    x -= x >= n ? n : 0;
+    return x - (x >= n ? n : 0);
+}
 
 // exact min of doubles in shared memory (CAS on the bit pattern; the first
 // candidate of an output replaces the +inf sentinel)
@@ -399,9 +424,7 @@ __device__ __forceinline__ void smem_fmin(unsigned long long* addr, double c) {
 // 16-byte aligned even start) into ubuf, plus optionally vcnt v_d values.
 __device__ __forceinline__ void issue_chunk(MainShared& S, const double* ul, int n, int yc, int clen,
                                             const double* vsrc, int vcnt) {
-    int bm = yc - 1;
-    while (bm < 0) bm += n;
-    while (bm >= n) bm -= n;
+    const int bm = wrap_idx(yc - 1, n);
     const int sh = bm & 1;
     const int s0 = bm - sh;                    // even, in [0, n)
     const int cnt = (clen + 2 + sh + 1) & ~1;  // even count
@@ -411,6 +434,90 @@ __device__ __forceinline__ void issue_chunk(MainShared& S, const double* ul, int
     tma_load_1d(S.ubuf, ul + s0, static_cast<unsigned>(c1) * 8u, &S.mbar);
     if (cnt > c1) tma_load_1d(S.ubuf + c1, ul, static_cast<unsigned>(cnt - c1) * 8u, &S.mbar);
     if (vsrc) tma_load_1d(S.vbuf, vsrc, static_cast<unsigned>(vcnt) * 8u, &S.mbar);
+}
+
+struct ChunkArgs {
+    const double* ub;  // ub[i + 1] = U(yc + i), i in [-1, clen]
+    int clen, base, jspan;
+    double pe, ia, hl, hr;
+    int dlo, dhi;       // the tile's displacement range (clamp)
+    const double* skt;  // K(d) staged in shared memory (KS) ...
+    const double* gvt;  // ... or v_d in global memory
+    double drift, tau;
+};
+
+template <bool KS>
+__device__ __forceinline__ double kvalue(const ChunkArgs& a, int d) {
+    if constexpr (KS) return a.skt[d];
+    else return kval_v(__ldg(a.gvt + d), a.drift, a.tau);
+}
+
+// Candidates of one staged source chunk.  Warp w takes sources w*per + lane +
+// 32m (consecutive lanes, consecutive sources: conflict-free shared loads).
+// Each source's first two displacements go straight to the output slots
+// with one CAS against the empty sentinel; slots already holding a larger
+// value, and intervals longer than two, are queued and finished after the
+// barrier with exact CAS-min loops, one warp per queued source.
+template <bool KS>
+__device__ __forceinline__ void process_chunk(MainShared& S, const ChunkArgs& a) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int per = ((a.clen + kNT - 1) / kNT) * 32;
+    const int iend = min(a.clen, (warp + 1) * per);
+    unsigned ninl = 0;
+#pragma unroll 2
+    for (int i = warp * per + lane; i < iend; i += 32) {
+        const double ul0 = a.ub[i], u0 = a.ub[i + 1], ur0 = a.ub[i + 2];
+        const double zl = __dmul_rn(__dadd_rn(__dsub_rn(u0, ul0), a.pe), a.ia);
+        const double zr = __dmul_rn(__dadd_rn(__dsub_rn(ur0, u0), a.pe), a.ia);
+        const int off = a.base + i;  // output index of this source at d = 0
+        // every candidate lies in [dlo, dhi] when the statistics describe u;
+        // the clamp keeps stale statistics memory-safe (wrong, never out of bounds)
+        const int dl = max(max(__double2int_ru(zl + a.hl), a.dlo), -off);
+        const int dr = min(min(__double2int_rd(zr + a.hr), a.dhi), a.jspan - off);
+        if (dl <= dr) {
+            unsigned long long* slot = &S.keys[off + dl];
+            const double c0 = __dadd_rn(u0, kvalue<KS>(a, dl));
+            const unsigned long long o0 = atomicCAS(slot, kInfBits, static_cast<unsigned long long>(__double_as_longlong(c0)));
+            const bool r0 = o0 != kInfBits && c0 < __longlong_as_double(static_cast<long long>(o0));
+            bool r1 = false;
+            if (dl < dr) {
+                const double c1 = __dadd_rn(u0, kvalue<KS>(a, dl + 1));
+                const unsigned long long o1 =
+                    atomicCAS(slot + 1, kInfBits, static_cast<unsigned long long>(__double_as_longlong(c1)));
+                r1 = o1 != kInfBits && c1 < __longlong_as_double(static_cast<long long>(o1));
+            }
+            ninl += min(dr - dl + 1, 2);
+            const bool longer = dl + 2 <= dr;
+            if (r0 | r1 | longer) {
+                const int qlo = r0 ? dl : (r1 ? dl + 1 : dl + 2);
+                const int qhi = longer ? dr : (r1 ? dl + 1 : dl);
+                const int q = atomicAdd(&S.nq, 1);
+                if (q < kQCap) {
+                    S.queue[q] = make_int3(i, qlo, qhi);
+                } else {
+                    for (int d = qlo; d <= qhi; ++d) smem_fmin(&S.keys[off + d], __dadd_rn(u0, kvalue<KS>(a, d)));
+                }
+            }
+        }
+    }
+    if (ninl) atomicAdd(&S.c_inline, ninl);
+    __syncthreads();
+    const int nq = min(S.nq, kQCap);
+    if (nq) {
+        for (int e = warp; e < nq; e += kNT / 32) {
+            const int3 qe = S.queue[e];
+            const double uy = a.ub[qe.x + 1];
+            const int off = a.base + qe.x;
+            if (lane == 0) atomicAdd(&S.c_queued, static_cast<unsigned>(qe.z - qe.y + 1));
+            for (int d = qe.y + lane; d <= qe.z; d += 32) smem_fmin(&S.keys[off + d], __dadd_rn(uy, kvalue<KS>(a, d)));
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            S.c_qent += nq;
+            S.nq = 0;
+        }
+        __syncthreads();
+    }
 }
 
 // Per-line constants of the step (identical IEEE operations to the host's
@@ -471,11 +578,25 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
     for (int i = tid; i <= jspan; i += kNT) S.keys[i] = kInfBits;
-    for (int i = tid; i < kLut2; i += kNT) S.lut[i] = __ldg(g_fsm_lut2 + i);
     // reset the line statistics buffer two steps ahead
     if (tile == 0 && tid < 4) b.line_reset[line * 4 + tid] = (tid & 1) ? 0ull : ~0ull;
 
     // ---- warp 0: line gate, candidate sub-tiles, first TMA issue ----
+#ifndef LOB_NO_PF
+    if (tid == 0 && big) {
+#else
+    if (false) {
+#endif
+        // the sources near the line's central displacement start moving to L2
+        // while the statistics round trips below are in flight
+        const int center = first + n;
+        int y0 = (jlo - center - kPfMargin) % n;
+        y0 = (y0 < 0 ? y0 + n : y0) & ~1;
+        const int cnt = min((jspan + 2 * kPfMargin + 4) & ~1, n);
+        const int c1 = min(cnt, n - y0);
+        prefetch_l2(ul + y0, static_cast<unsigned>(c1) * 8u);
+        if (cnt > c1) prefetch_l2(ul, static_cast<unsigned>(cnt - c1) * 8u);
+    }
     if (warp == 0) {
         // line statistics: oscillation gate and global displacement bounds
         const unsigned long long* L = b.line_in + line * 4;
@@ -556,7 +677,10 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
         const double* gvt = p.vtab + p.vofs;
         const double* skt = S.vbuf - vd0;
         const double kdrift = lc.drift;
-        auto kd = [&](int d) -> double { return kstage ? skt[d] : kval_v(__ldg(gvt + d), kdrift, tau); };
+        if (tid == 0 && diag) {
+            atomicAdd(diag + 6, kstage ? 0ull : 1ull);
+            atomicAdd(diag + 7, static_cast<unsigned long long>(vcnt));
+        }
         // ---- sources in chunks of kC ----
         unsigned mphase = 0;
         for (int yc = ya; yc <= yb; yc += kC) {
@@ -564,10 +688,7 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
             const int base = yc - jlo;  // output index of source i at d: base + i + d
             int sh = 0;
             if (big) {
-                int bm = yc - 1;
-                while (bm < 0) bm += n;
-                while (bm >= n) bm -= n;
-                sh = bm & 1;
+                sh = wrap_idx(yc - 1, n) & 1;
                 if (yc != ya && tid == 0) issue_chunk(S, ul, n, yc, clen, nullptr, 0);
                 if (warp == 0) mbar_wait(&S.mbar, mphase);
                 mphase ^= 1u;
@@ -577,66 +698,17 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
                     __syncthreads();
                 }
             } else {
-                int bm = yc - 1;
-                while (bm < 0) bm += n;
+                const int bm = wrap_idx(yc - 1, n);
                 for (int i = tid; i < clen + 2; i += kNT) S.ubuf[i] = __ldg(ul + (bm + i) % n);
                 __syncthreads();
             }
             const double* ub = S.ubuf + sh;
             if (tid == 0) S.c_src += static_cast<unsigned>(clen);
-            {
-                // warp w takes chunk sources w*per + lane + 32m (consecutive lanes,
-                // consecutive sources: conflict-free shared accesses)
-                unsigned ninl = 0;
-                const int per = ((clen + kNT - 1) / kNT) * 32;
-#pragma unroll 2
-                for (int m = 0; m < per / 32; ++m) {
-                    const int i = warp * per + lane + 32 * m;  // source index in the chunk
-                    if (i >= clen) break;
-                    const double ul0 = ub[i], u0 = ub[i + 1], ur0 = ub[i + 2];
-                    const double zl = __dmul_rn(__dadd_rn(__dsub_rn(u0, ul0), pe), ia);
-                    const double zr = __dmul_rn(__dadd_rn(__dsub_rn(ur0, u0), pe), ia);
-                    const int off = base + i;  // output index of this source at d = 0
-                    // every candidate lies in [dlo_t, dhi_t] when the statistics describe u;
-                    // the clamp keeps stale statistics memory-safe (wrong, never out of bounds)
-                    const int dl = max(max(__double2int_ru(zl + hl), dlo_t), -off);
-                    const int dr = min(min(__double2int_rd(zr + hr), dhi_t), jspan - off);
-                    if (dl <= dr) {
-                        const double k0v = kd(dl);
-                        const double k1v = dl + 1 <= dr ? kd(dl + 1) : 0.0;
-                        smem_fmin(&S.keys[off + dl], __dadd_rn(u0, k0v));
-                        if (dl + 1 <= dr) smem_fmin(&S.keys[off + dl + 1], __dadd_rn(u0, k1v));
-                        ninl += min(dr - dl + 1, 2);
-                        if (dl + 2 <= dr) {
-                            const int slot = atomicAdd(&S.nq, 1);
-                            if (slot < kQCap) {
-                                S.queue[slot] = make_int3(i, dl + 2, dr);
-                            } else {
-                                for (int d = dl + 2; d <= dr; ++d) smem_fmin(&S.keys[off + d], __dadd_rn(u0, kd(d)));
-                            }
-                        }
-                    }
-                }
-                if (ninl) atomicAdd(&S.c_inline, ninl);
-            }
-            __syncthreads();
-            // ---- long intervals: one warp per queued source, lanes over d ----
-            const int nq = min(S.nq, kQCap);
-            if (nq) {
-                for (int e = warp; e < nq; e += kNT / 32) {
-                    const int3 qe = S.queue[e];
-                    const double uy = ub[qe.x + 1];
-                    const int off = base + qe.x;
-                    if (lane == 0) atomicAdd(&S.c_queued, static_cast<unsigned>(qe.z - qe.y + 1));
-                    for (int d = qe.y + lane; d <= qe.z; d += 32) smem_fmin(&S.keys[off + d], __dadd_rn(uy, kd(d)));
-                }
-                __syncthreads();
-                if (tid == 0) {
-                    S.c_qent += nq;
-                    S.nq = 0;
-                }
-                __syncthreads();
-            }
+            const ChunkArgs ca{ub, clen, base, jspan, pe, ia, hl, hr, dlo_t, dhi_t, skt, gvt, kdrift, tau};
+            if (kstage)
+                process_chunk<true>(S, ca);
+            else
+                process_chunk<false>(S, ca);
         }
     }
 
@@ -689,6 +761,9 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
             j %= n;
             vals[P8(i)] = finish(i, j, tvl ? __ldg(tvl + j) : 0.0);
         }
+        // FSM table for tile_stats (ubuf's tail is free once emission is done)
+        unsigned* lut = reinterpret_cast<unsigned*>(S.post().lut);
+        for (int i = tid; i < kLut2 / 2; i += kNT) lut[i] = __ldg(reinterpret_cast<const unsigned*>(g_fsm_lut2) + i);
     }
     __syncthreads();
     if (tid == 0 && diag) {
@@ -698,7 +773,7 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
         atomicAdd(diag + 4, static_cast<unsigned long long>(S.c_qent));
         atomicAdd(diag + 5, 1ull);
     }
-    tile_stats(vals, Tl, j0, line, tile, p, b, S.epi, S.lut);
+    tile_stats(vals, Tl, j0, line, tile, p, b, S.post().epi, S.post().lut);
     // block count of the INPUT u (decompose on the closed period): warp 0 of
     // the line's first tile composes the tile summaries
     if (blocks_out && tile == 0 && warp == 0) {

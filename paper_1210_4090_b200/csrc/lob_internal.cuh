@@ -27,6 +27,10 @@ struct lob_ctx {
     std::map<const void*, int64_t> ws_counter;
     std::map<const void*, std::pair<int64_t, int64_t>> ws_shape;
     std::map<const void*, const void*> ws_last_out;  // workspace -> out of its last K2 call
+    // K1 mode (LOB_DIRECT_SCREENED / LOB_DIRECT_PLAIN) and the screened kernel's
+    // count of outputs swept in full fp64 (device counter, lazily allocated)
+    int direct_mode = 0;
+    unsigned long long* direct_full = nullptr;
     // scratch for host entry points
     void* scratch = nullptr;
     size_t scratch_bytes = 0;
@@ -79,6 +83,14 @@ inline int64_t posmod(int64_t a, int64_t n) {
 }
 
 // Launch helpers implemented in the .cu files.
+int launch_direct_plain_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
+                            const double* ktab, int64_t ktab_stride, const int64_t* first,
+                            const double* tv, int64_t tv_stride, cudaStream_t s);
+int launch_direct_screen_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
+                             const double* ktab, int64_t ktab_stride, const int64_t* first,
+                             const double* tv, int64_t tv_stride, unsigned long long* counters,
+                             cudaStream_t s);
+// dispatch on ctx->direct_mode
 int launch_direct_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
                       const double* ktab, int64_t ktab_stride, const int64_t* first,
                       const double* tv, int64_t tv_stride, cudaStream_t s);

@@ -8,6 +8,14 @@ from paper_1210_4090_b200 import api
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True, params=[api.DIRECT_SCREENED, api.DIRECT_PLAIN], ids=["screened", "plain"])
+def direct_mode(request, dev):
+    """Every K1 test runs with the fp32-screened sweep (default) and the plain fp64 sweep."""
+    dev.set_direct_mode(request.param)
+    yield request.param
+    dev.set_direct_mode(api.DIRECT_SCREENED)
+
+
 def torch_dev(x):
     import torch
     return torch.from_numpy(np.ascontiguousarray(x)).cuda()
@@ -112,3 +120,41 @@ def test_direct_properties_full_c3(dev, orc):
     # spot-check 8 random lines against the oracle bit-exactly
     idx = np.random.default_rng(2).choice(4096, 8, replace=False)
     assert np.array_equal(a[idx], orc.direct(u[idx], K, first))
+
+
+def test_direct_screen_ties_fall_back_exactly(dev, orc, direct_mode):
+    """Two equal wells half a period apart and a symmetric kernel: outputs a
+    quarter period away see an exact tie between two sub-chunks, which the
+    fp32 bound cannot separate; those outputs are swept in full fp64."""
+    n = 4096
+    K, first, _, _ = orc.kernel(n, 0.01, 0.0)
+    u = np.zeros((2, n))
+    u[:, 100] = u[:, 100 + n // 2] = -10.0  # deeper than K(+-n/4) = 3.125
+    u[1] += np.linspace(0, 1e-9, n)  # breaks some ties below fp32 resolution
+    dev.direct_fallbacks(reset=True)
+    assert np.array_equal(run_direct(dev, u, K, first), orc.direct(u, K, first))
+    if direct_mode == api.DIRECT_SCREENED:
+        assert dev.direct_fallbacks() > 0
+
+
+@pytest.mark.parametrize("scale", [1e300, 1e-40, 1e-310])
+def test_direct_screen_extreme_magnitudes(dev, orc, scale):
+    """fp32 overflow (1e300: the CTA sweeps in fp64) and fp32/fp64 subnormal
+    ranges (the bound's absolute slack) still give the reference's doubles."""
+    n = 2048
+    rng = np.random.default_rng(7)
+    K, first, _, _ = orc.kernel(n, 0.02, 0.3)
+    u = rng.uniform(-1, 1, (3, n)) * scale
+    assert np.array_equal(run_direct(dev, u, K, first), orc.direct(u, K, first))
+    Ks = K * scale
+    assert np.array_equal(run_direct(dev, u, Ks, first), orc.direct(u, Ks, first))
+
+
+def test_direct_screen_nan_inputs_match_reference_min(dev, orc):
+    """NaN candidates never win std::min(best, c) (proj/src/minplus.cpp:121-123)."""
+    n = 1024
+    K, first, _, _ = orc.kernel(n, 0.05, 0.5)
+    u = np.sin(np.linspace(0, 2 * np.pi, n, endpoint=False))[None, :].repeat(2, 0)
+    u[0, 17] = np.nan
+    got, want = run_direct(dev, u, K, first), orc.direct(u, K, first)
+    assert np.array_equal(got, want, equal_nan=True)
