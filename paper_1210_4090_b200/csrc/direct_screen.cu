@@ -57,7 +57,10 @@ __device__ __noinline__ double exact_sweep(const double* __restrict__ ul, const 
 }
 
 template <int R, int NT, int TW, int SUB>
-__global__ void __launch_bounds__(NT) screen_kernel(const double* __restrict__ u, double* __restrict__ out,
+#ifndef LOB_SCREEN_MINB
+#define LOB_SCREEN_MINB 1
+#endif
+__global__ void __launch_bounds__(NT, LOB_SCREEN_MINB) screen_kernel(const double* __restrict__ u, double* __restrict__ out,
                                                     int64_t n, int64_t tiles, const double* __restrict__ ktab,
                                                     int64_t ktab_stride, const int64_t* __restrict__ first_arr,
                                                     const double* __restrict__ tv, int64_t tv_stride,
@@ -126,7 +129,11 @@ __global__ void __launch_bounds__(NT) screen_kernel(const double* __restrict__ u
         for (int k = 0; k < R; ++k) A[k] = pa[k];
         // the last chunk stops at the window's end (rounded up to R)
         const int send = static_cast<int>(min(static_cast<int64_t>(TW), (W - wc + R - 1) / R * R));
+#ifdef LOB_S0_UNROLL
+#pragma unroll 2
+#else
 #pragma unroll 1
+#endif
         for (int s0 = 0; s0 < send; s0 += R) {
             float B[R];
 #pragma unroll
