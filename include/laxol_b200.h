@@ -70,15 +70,16 @@ int lob_minplus_direct_f64(lob_ctx* ctx, const double* u, double* out, int64_t l
 /* K1 implementation (per context; every K1 sweep — lob_minplus_direct_f64,
  * evolve and split steps with LOB_ENGINE_DIRECT — uses it):
  *  LOB_DIRECT_SCREENED (default): the O(n^2) sweep runs in fp32 with a
- *    rigorous error bound; per output the best sub-chunk of 64 displacements
- *    is re-evaluated in fp64 (or the whole window when the bound cannot
- *    separate sub-chunks).  Results are the same doubles as the plain sweep.
+ *    rigorous error bound; per output only the span of 64-displacement
+ *    sub-chunks that can hold the minimiser is re-evaluated in fp64.
+ *    Results are the same doubles as the plain sweep.
  *  LOB_DIRECT_PLAIN: every candidate in fp64 (DADD + DSETP per candidate). */
 #define LOB_DIRECT_SCREENED 0
 #define LOB_DIRECT_PLAIN 1
 int lob_ctx_set_direct_mode(lob_ctx* ctx, int mode);
-/* Outputs the screened K1 swept in full fp64 since the last reset (synchronizes). */
-int lob_direct_fallbacks(lob_ctx* ctx, uint64_t* count, int reset);
+/* Screened-K1 counters since the last reset (synchronizes): outputs swept in
+ * full fp64 (non-finite screen) and fp64 candidates re-evaluated in total. */
+int lob_direct_stats(lob_ctx* ctx, uint64_t* full_outputs, uint64_t* fp64_candidates, int reset);
 
 /* K1 — fp32 variant (no potential; the reference has no fp32 path). */
 int lob_minplus_direct_f32(lob_ctx* ctx, const float* u, float* out, int64_t lines, int64_t n,

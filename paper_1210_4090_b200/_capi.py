@@ -50,7 +50,7 @@ SIGNATURES = {
     "lob_bench_fp64": (c_int, [_P, POINTER(c_double), POINTER(c_double), POINTER(c_double)]),
     "lob_launch_count": (c_int64, [_P]),
     "lob_ctx_set_direct_mode": (c_int, [_P, c_int]),
-    "lob_direct_fallbacks": (c_int, [_P, POINTER(c_uint64), c_int]),
+    "lob_direct_stats": (c_int, [_P, POINTER(c_uint64), POINTER(c_uint64), c_int]),
     # synthetic workloads (include/laxol_b200_configs.h)
     "lob_gen_sin": (None, [c_int64, _P]),
     "lob_gen_cos": (None, [c_int64, _P]),

@@ -122,11 +122,17 @@ class Device:
         """DIRECT_SCREENED (default: fp32 screen + fp64 re-evaluation) or DIRECT_PLAIN."""
         self._check(self.lib.lob_ctx_set_direct_mode(self.ctx, int(mode)), "lob_ctx_set_direct_mode")
 
+    def direct_stats(self, reset: bool = True) -> dict:
+        """Screened-K1 counters since the last reset: outputs swept in full fp64
+        and fp64 candidates re-evaluated."""
+        f, c = ctypes.c_uint64(), ctypes.c_uint64()
+        self._check(self.lib.lob_direct_stats(self.ctx, ctypes.byref(f), ctypes.byref(c), int(reset)),
+                    "lob_direct_stats")
+        return {"full_outputs": int(f.value), "fp64_candidates": int(c.value)}
+
     def direct_fallbacks(self, reset: bool = True) -> int:
         """Outputs the screened K1 swept in full fp64 since the last reset."""
-        v = ctypes.c_uint64()
-        self._check(self.lib.lob_direct_fallbacks(self.ctx, ctypes.byref(v), int(reset)), "lob_direct_fallbacks")
-        return int(v.value)
+        return self.direct_stats(reset)["full_outputs"]
 
     # ---- kernels -----------------------------------------------------------
     def build_kernel(self, n_space: int, tau: float, drift: float) -> Kernel:

@@ -58,6 +58,7 @@ int lob_ctx_destroy(lob_ctx* ctx) {
     for (auto& kv : ctx->vtabs) cudaFree(kv.second.dev);
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->direct_full) cudaFree(ctx->direct_full);
+    if (ctx->direct_umax) cudaFree(ctx->direct_umax);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return LOB_OK;
@@ -73,16 +74,17 @@ int lob_ctx_set_direct_mode(lob_ctx* ctx, int mode) {
     return LOB_OK;
 }
 
-int lob_direct_fallbacks(lob_ctx* ctx, uint64_t* count, int reset) {
-    if (!ctx || !count) return LOB_INVALID_INPUT;
+int lob_direct_stats(lob_ctx* ctx, uint64_t* full_outputs, uint64_t* fp64_candidates, int reset) {
+    if (!ctx) return LOB_INVALID_INPUT;
     cudaSetDevice(ctx->device);
-    *count = 0;
-    if (!ctx->direct_full) return LOB_OK;
-    LOB_CUDA_TRY(ctx, cudaDeviceSynchronize());
-    unsigned long long v = 0;
-    LOB_CUDA_TRY(ctx, cudaMemcpy(&v, ctx->direct_full, sizeof(v), cudaMemcpyDeviceToHost));
-    *count = v;
-    if (reset) LOB_CUDA_TRY(ctx, cudaMemset(ctx->direct_full, 0, sizeof(v)));
+    unsigned long long v[2] = {0, 0};
+    if (ctx->direct_full) {
+        LOB_CUDA_TRY(ctx, cudaDeviceSynchronize());
+        LOB_CUDA_TRY(ctx, cudaMemcpy(v, ctx->direct_full, sizeof(v), cudaMemcpyDeviceToHost));
+        if (reset) LOB_CUDA_TRY(ctx, cudaMemset(ctx->direct_full, 0, sizeof(v)));
+    }
+    if (full_outputs) *full_outputs = v[0];
+    if (fp64_candidates) *fp64_candidates = v[1];
     return LOB_OK;
 }
 

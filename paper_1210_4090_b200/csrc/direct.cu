@@ -23,46 +23,11 @@
 // so the stride-R per-thread reads are bank-conflict free.
 #include <cstdlib>
 
-#include "lob_internal.cuh"
+#include "direct_common.cuh"
 
 namespace lob {
 namespace {
-
-template <typename T>
-__device__ __forceinline__ T add_rn(T a, T b);
-template <>
-__device__ __forceinline__ double add_rn<double>(double a, double b) {
-    return __dadd_rn(a, b);
-}
-template <>
-__device__ __forceinline__ float add_rn<float>(float a, float b) {
-    return __fadd_rn(a, b);
-}
-
-template <typename T>
-__device__ __forceinline__ T min_exact(T best, T c) {
-    return c < best ? c : best;  // std::min(best, c)
-}
-template <>
-__device__ __forceinline__ float min_exact<float>(float best, float c) {
-    return fminf(best, c);  // FMNMX; equal to the ternary for non-NaN c
-}
-
-template <typename T>
-__device__ __forceinline__ T pos_inf();
-template <>
-__device__ __forceinline__ double pos_inf<double>() {
-    return __longlong_as_double(0x7ff0000000000000ll);
-}
-template <>
-__device__ __forceinline__ float pos_inf<float>() {
-    return __int_as_float(0x7f800000);
-}
-
-template <int R>
-__host__ __device__ __forceinline__ constexpr int padded(int i) {
-    return i + i / R;
-}
+using namespace k1;
 
 template <typename T, int R, int NT, int TW>
 __global__ void __launch_bounds__(NT) direct_kernel(const T* __restrict__ u, T* __restrict__ out,
@@ -90,53 +55,7 @@ __global__ void __launch_bounds__(NT) direct_kernel(const T* __restrict__ u, T* 
     T best[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) best[r] = pos_inf<T>();
-
-    for (int64_t wc = 0; wc < W; wc += TW) {
-        __syncthreads();
-        // sources y = j - first - w for j in [j0, j0+TJ), w in [wc, wc+TW):
-        // y in [ylo, ylo + L) with ylo = j0 - first - wc - TW
-        const int64_t ylo = j0 - first - wc - TW;
-        int64_t ym = ylo % n;
-        if (ym < 0) ym += n;
-        for (int i = t; i < L; i += NT) {
-            int64_t y = ym + i;
-            y -= (y / n) * n;
-            Us[padded<R>(i)] = ul[y];
-        }
-        for (int s = t; s < TW; s += NT) {
-            const int64_t w = wc + s;
-            Ks[s] = w < W ? Kl[w] : pos_inf<T>();
-        }
-        __syncthreads();
-
-        // logical index of U(jt - first - wc) is i0 = t*R + TW (a multiple of R):
-        // padded(i0 + k) = pa + k and padded(i0 - 1 - k) = pa - 2 - k, pa = padded(i0)
-        const T* pa = Us + padded<R>(t * R + TW);
-        T A[R];
-#pragma unroll
-        for (int k = 0; k < R; ++k) A[k] = pa[k];
-        // the last chunk stops at the window's end (rounded up to R)
-        const int send = static_cast<int>(min(static_cast<int64_t>(TW), (W - wc + R - 1) / R * R));
-#pragma unroll 1
-        for (int s0 = 0; s0 < send; s0 += R) {
-            T B[R];
-#pragma unroll
-            for (int k = 0; k < R; ++k) B[k] = pa[-2 - k];
-#pragma unroll
-            for (int s = 0; s < R; ++s) {
-                const T kw = Ks[s0 + s];
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const int idx = r - s;
-                    const T val = idx >= 0 ? A[idx >= 0 ? idx : 0] : B[idx < 0 ? -idx - 1 : 0];
-                    best[r] = min_exact<T>(best[r], add_rn<T>(val, kw));
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < R; ++k) A[k] = B[R - 1 - k];
-            pa -= R + 1;
-        }
-    }
+    k1::sweep_range<T, R, NT, TW>(Us, Ks, ul, Kl, n, j0, first, 0, W, best);
 
     const int64_t jt = j0 + static_cast<int64_t>(t) * R;
     T* ol = out + line * n;

@@ -30,7 +30,9 @@ struct lob_ctx {
     // K1 mode (LOB_DIRECT_SCREENED / LOB_DIRECT_PLAIN) and the screened kernel's
     // count of outputs swept in full fp64 (device counter, lazily allocated)
     int direct_mode = 0;
-    unsigned long long* direct_full = nullptr;
+    unsigned long long* direct_full = nullptr;  // [0] outputs swept in full, [1] fp64 candidates
+    double* direct_umax = nullptr;              // per-line max |u| (screen bound)
+    int64_t direct_umax_cap = 0;
     // scratch for host entry points
     void* scratch = nullptr;
     size_t scratch_bytes = 0;

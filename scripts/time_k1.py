@@ -39,9 +39,9 @@ def med(fn, reps=int(sys.argv[1]) if len(sys.argv) > 1 else 10):
 res = {}
 for name, mode in (("screened", api.DIRECT_SCREENED), ("plain", api.DIRECT_PLAIN)):
     dev.set_direct_mode(mode)
-    dev.direct_fallbacks(reset=True)
+    dev.direct_stats(reset=True)
     t = med(lambda: dev.direct_f64(u, o, dk, df))
-    res[name] = {"ms": t, "cand_per_s": cand / t * 1e3, "fallback_outputs": dev.direct_fallbacks()}
+    res[name] = {"ms": t, "cand_per_s": cand / t * 1e3, **dev.direct_stats()}
     res[name]["out_sum"] = float(o.sum())
 dev.set_direct_mode(api.DIRECT_SCREENED)
 u32, o32, dk32 = u.float(), torch.empty_like(u, dtype=torch.float32), dk.float()
