@@ -1,6 +1,7 @@
 // C-ABI entry points of laxol_b200 (declared in include/laxol_b200.h).
 // Validation mirrors the reference's InvalidInput checks
 // (proj/src/scheme.cpp:18-24,39-53; proj/src/grid_fn.cpp:11-22).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -60,6 +61,10 @@ int lob_ctx_destroy(lob_ctx* ctx) {
     if (ctx->direct_full) cudaFree(ctx->direct_full);
     if (ctx->direct_umax) cudaFree(ctx->direct_umax);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    for (auto& a : ctx->aux)
+        if (a) cudaStreamDestroy(a);
+    for (auto& e : ctx->aux_ev)
+        if (e) cudaEventDestroy(e);
     delete ctx;
     return LOB_OK;
 }
@@ -345,6 +350,9 @@ int lob_evolve_f64(lob_ctx* ctx, double* u, double* scratch, int64_t lines, int6
     return LOB_OK;
 }
 
+// line chunks of the pipelined host step (fast engine)
+constexpr int64_t kHostChunks = 8;  // <= 16 (two events per chunk in lob_ctx::aux_ev)
+
 int lob_step_host_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
                       const double* drift, double tau, const double* tv, int64_t tv_stride,
                       double eta, int engine, int64_t* blocks) {
@@ -355,10 +363,12 @@ int lob_step_host_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines,
     const size_t ub = static_cast<size_t>(lines * n) * sizeof(double);
     const size_t tvn = tv ? static_cast<size_t>(tv_stride ? lines * tv_stride : n) : 0;
     size_t wsb = fast_workspace_bytes(lines, n);
+    const int64_t per_chunk = (lines + kHostChunks - 1) / kHostChunks;
+    const size_t wsb_chunk = fast_workspace_bytes(per_chunk, n);
     const int64_t W = 2 * n + 1;
     const size_t kb = engine == LOB_ENGINE_DIRECT ? static_cast<size_t>(lines * W) * sizeof(double) : 0;
     const size_t need = 2 * ub + tvn * sizeof(double) + lines * (sizeof(double) + 2 * sizeof(int64_t)) +
-                        wsb + kb + 8 * 256;
+                        wsb + 2 * wsb_chunk + kb + 10 * 256;
     if (ctx->scratch_bytes < need) {
         if (ctx->scratch) cudaFree(ctx->scratch);
         ctx->scratch = nullptr;
@@ -380,7 +390,9 @@ int lob_step_host_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines,
     int64_t* dfirst = reinterpret_cast<int64_t*>(take(lines * sizeof(int64_t)));
     double* dk = reinterpret_cast<double*>(take(kb));
     void* ws = take(wsb);
-    LOB_CUDA_TRY(ctx, cudaMemcpyAsync(du, u, ub, cudaMemcpyHostToDevice, s));
+    void* ws_chunk[2] = {take(wsb_chunk), take(wsb_chunk)};
+    const bool piped = engine != LOB_ENGINE_DIRECT && lines >= 2 * kHostChunks;
+    if (!piped) LOB_CUDA_TRY(ctx, cudaMemcpyAsync(du, u, ub, cudaMemcpyHostToDevice, s));
     if (tv) LOB_CUDA_TRY(ctx, cudaMemcpyAsync(dtv, tv, tvn * sizeof(double), cudaMemcpyHostToDevice, s));
     LOB_CUDA_TRY(ctx, cudaMemcpyAsync(ddrift, drift, lines * sizeof(double), cudaMemcpyHostToDevice, s));
     if (engine == LOB_ENGINE_DIRECT) {
@@ -397,6 +409,39 @@ int lob_step_host_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines,
         st = launch_direct_f64(ctx, du, dout, lines, n, dk, W, dfirst, tv ? dtv : nullptr, tv_stride, s);
         if (st == LOB_OK && blocks) st = launch_block_counts(ctx, du, lines, n, eta, dblocks, s);
         LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));  // host vectors go out of scope
+    } else if (lines >= 2 * kHostChunks) {
+        // pipelined over line chunks: uploads, steps and downloads run on three
+        // streams linked by per-chunk events, so the host->device and
+        // device->host copy engines stay busy concurrently
+        if (!ctx->aux[0]) {
+            for (auto& a : ctx->aux) LOB_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+            for (auto& e : ctx->aux_ev) LOB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        cudaStream_t up = ctx->aux[0], cs = ctx->aux[1], dn = ctx->aux[2];
+        LOB_CUDA_TRY(ctx, cudaEventRecord(ctx->aux_ev[32], s));  // tv, drift uploaded on s
+        LOB_CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ctx->aux_ev[32], 0));
+        const int64_t per = (lines + kHostChunks - 1) / kHostChunks;
+        for (int64_t l0 = 0, k = 0; l0 < lines; l0 += per, ++k) {
+            const int64_t cl = std::min(per, lines - l0);
+            const size_t cb = static_cast<size_t>(cl * n) * sizeof(double);
+            cudaEvent_t in_ready = ctx->aux_ev[2 * k], done = ctx->aux_ev[2 * k + 1];
+            LOB_CUDA_TRY(ctx, cudaMemcpyAsync(du + l0 * n, u + l0 * n, cb, cudaMemcpyHostToDevice, up));
+            LOB_CUDA_TRY(ctx, cudaEventRecord(in_ready, up));
+            LOB_CUDA_TRY(ctx, cudaStreamWaitEvent(cs, in_ready, 0));
+            st = launch_fast_f64(ctx, du + l0 * n, dout + l0 * n, cl, n, ddrift + l0, tau,
+                                 tv ? dtv + (tv_stride ? l0 * tv_stride : 0) : nullptr, tv_stride, eta,
+                                 blocks ? dblocks + l0 : nullptr, ws_chunk[k % 2], wsb_chunk, 0, cs);
+            if (st) return st;
+            LOB_CUDA_TRY(ctx, cudaEventRecord(done, cs));
+            LOB_CUDA_TRY(ctx, cudaStreamWaitEvent(dn, done, 0));
+            LOB_CUDA_TRY(ctx, cudaMemcpyAsync(out + l0 * n, dout + l0 * n, cb, cudaMemcpyDeviceToHost, dn));
+        }
+        // block counts last, in one copy: a pageable destination would make a
+        // per-chunk copy synchronous and serialise the pipeline
+        if (blocks)
+            LOB_CUDA_TRY(ctx, cudaMemcpyAsync(blocks, dblocks, lines * sizeof(int64_t), cudaMemcpyDeviceToHost, dn));
+        LOB_CUDA_TRY(ctx, cudaStreamSynchronize(dn));
+        return LOB_OK;
     } else {
         st = launch_fast_f64(ctx, du, dout, lines, n, ddrift, tau, tv ? dtv : nullptr, tv_stride, eta,
                              blocks ? dblocks : nullptr, ws, wsb, 0, s);
@@ -410,3 +455,4 @@ int lob_step_host_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines,
 }
 
 }  // extern "C"
+

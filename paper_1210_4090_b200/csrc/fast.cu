@@ -857,6 +857,8 @@ static int ensure_vtab(lob_ctx* ctx, int64_t n, double tau, const double** out, 
                                                                                          eps, tau);
         ctx->launches += 1;
         LOB_CUDA_TRY(ctx, cudaGetLastError());
+        // cached for later calls on any stream: complete it now
+        LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
         it = ctx->vtabs.emplace(key, vt).first;
     }
     *out = it->second.dev;

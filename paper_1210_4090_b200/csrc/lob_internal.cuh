@@ -33,6 +33,10 @@ struct lob_ctx {
     unsigned long long* direct_full = nullptr;  // [0] outputs swept in full, [1] fp64 candidates
     double* direct_umax = nullptr;              // per-line max |u| (screen bound)
     int64_t direct_umax_cap = 0;
+    // host entry point pipeline: upload / compute / download streams and
+    // per-chunk events (inputs ready, step done) + one for the shared inputs
+    cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t aux_ev[33] = {};
     // scratch for host entry points
     void* scratch = nullptr;
     size_t scratch_bytes = 0;

@@ -68,3 +68,27 @@ def test_step_host_e2e_matches_device(dev, orc):
             K, first, _, _ = orc.kernel(n, tau, d)
             assert np.array_equal(out[l], orc.direct(u[l:l + 1], K, first, tv=tv)[0])
             assert blocks[l] == orc.line_blocks(u[l])
+
+
+@pytest.mark.parametrize("per_line_tv", [False, True])
+def test_step_host_pipelined_chunks_match_device(dev, per_line_tv):
+    """>= 16 lines take the two-stream chunked host path (uneven last chunk):
+    same doubles and block counts as one device-resident K2 call."""
+    import torch
+    n, tau, lines = 2048, 0.02, 37
+    drifts = api.gen_c2_drifts(256)[:lines * 6:6].copy()
+    rng = np.random.default_rng(11)
+    u = np.cumsum(rng.uniform(-1.0 / n, 1.0 / n, (lines, n)), axis=1)
+    u -= np.linspace(0, 1, n, endpoint=False)[None, :] * u[:, -1:]
+    v = api.gen_potential(2, n)
+    tv = api.tau_v(np.stack([v * (1 + 0.01 * l) for l in range(lines)]) if per_line_tv else v, tau)
+    stride = n if per_line_tv else 0
+    blocks = np.empty(lines, np.int64)
+    out = dev.step_host(u, drifts, tau, tv=tv, tv_stride=stride, blocks=blocks)
+    du, dout = to_dev(u), torch.empty((lines, n), dtype=torch.float64, device="cuda")
+    db = torch.empty(lines, dtype=torch.int64, device="cuda")
+    ws = torch.empty(dev.fast_workspace_bytes(lines, n), dtype=torch.uint8, device="cuda")
+    dev.fast_f64(du, dout, to_dev(drifts), tau, tv=to_dev(tv), tv_stride=stride, blocks=db, workspace=ws)
+    torch.cuda.synchronize()
+    assert np.array_equal(out, dout.cpu().numpy())
+    assert np.array_equal(blocks, db.cpu().numpy())
