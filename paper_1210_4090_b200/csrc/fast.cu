@@ -58,7 +58,6 @@ constexpr int kC = 3584;       // sources staged per chunk (a typical tile + hal
 #define LOB_VCAP 1120
 #endif
 constexpr int kVCap = LOB_VCAP;  // v_d values staged per tile (TMA, with the first chunk)
-constexpr int kPfMargin = 256; // L2 prefetch margin around the central source range
 
 struct LineConst {
     long long first;  // window displacement of w = 0
@@ -391,9 +390,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
         "r"(phase)
         : "memory");
 }
-__device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;  // +inf
@@ -582,21 +578,6 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
     if (tile == 0 && tid < 4) b.line_reset[line * 4 + tid] = (tid & 1) ? 0ull : ~0ull;
 
     // ---- warp 0: line gate, candidate sub-tiles, first TMA issue ----
-#ifndef LOB_NO_PF
-    if (tid == 0 && big) {
-#else
-    if (false) {
-#endif
-        // the sources near the line's central displacement start moving to L2
-        // while the statistics round trips below are in flight
-        const int center = first + n;
-        int y0 = (jlo - center - kPfMargin) % n;
-        y0 = (y0 < 0 ? y0 + n : y0) & ~1;
-        const int cnt = min((jspan + 2 * kPfMargin + 4) & ~1, n);
-        const int c1 = min(cnt, n - y0);
-        prefetch_l2(ul + y0, static_cast<unsigned>(c1) * 8u);
-        if (cnt > c1) prefetch_l2(ul, static_cast<unsigned>(cnt - c1) * 8u);
-    }
     if (warp == 0) {
         // line statistics: oscillation gate and global displacement bounds
         const unsigned long long* L = b.line_in + line * 4;
