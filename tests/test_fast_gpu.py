@@ -163,3 +163,55 @@ def test_stats_valid_with_foreign_input_is_recomputed(dev, orc):
     fast_step(dev, u1, 0.2, tau, ws=ws)
     got, _ = fast_step(dev, u2, 0.2, tau, ws=ws, flags=api.FAST_STATS_VALID)
     assert np.array_equal(got.cpu().numpy(), oracle_step(orc, u2, 0.2, tau))
+
+
+def _k1_step(dev, u, drifts, tau, tv):
+    import torch
+    lines, n = u.shape
+    ks = [dev.build_kernel(n, tau, float(p)) for p in drifts]
+    kt = to_dev(np.stack([k.window for k in ks]))
+    fi = to_dev(np.array([k.first for k in ks], np.int64))
+    out = torch.empty_like(u)
+    dev.direct_f64(u, out, kt, fi, tv=tv, ktab_stride=2 * n + 1)
+    return out
+
+
+def test_fast_equals_direct_c2_full_size(dev):
+    """C2 at full size (256 lines x N=65536, 60 K2 steps from u0 = 0): one more
+    K2 step equals one K1 step (bit-exact, the direct path pinned to the
+    reference) on every line, with no fallback outputs."""
+    import torch
+    n, tau, lines = 65536, 0.02, 256
+    drifts = api.gen_c2_drifts(lines)
+    dd, dtv = to_dev(drifts), to_dev(api.tau_v(api.gen_potential(2, n), tau))
+    u = torch.zeros((lines, n), dtype=torch.float64, device="cuda")
+    v = torch.empty_like(u)
+    ws = torch.empty(dev.fast_workspace_bytes(lines, n), dtype=torch.uint8, device="cuda")
+    for i in range(60):
+        dev.fast_f64(u, v, dd, tau, tv=dtv, workspace=ws, flags=api.FAST_STATS_VALID if i else 0)
+        u, v = v, u
+    ws2 = torch.empty_like(ws)
+    dev.fast_f64(u, v, dd, tau, tv=dtv, workspace=ws2)
+    w = _k1_step(dev, u, drifts, tau, dtv)
+    torch.cuda.synchronize()
+    assert torch.equal(v, w)
+    assert dev.fast_diagnostics(ws2, lines, n) == 0
+
+
+def test_fast_equals_direct_c5_full_line(dev):
+    """C5 at full line length (N=2^20): 20 K2 steps on 2 lines, then K2 == K1."""
+    import torch
+    n, tau = 1 << 20, 0.005
+    u = to_dev(api.gen_c5_lines(0, 2, n))
+    v = torch.empty_like(u)
+    dd, dtv = to_dev(np.full(2, 0.25)), to_dev(api.tau_v(api.gen_potential(3, n), tau))
+    ws = torch.empty(dev.fast_workspace_bytes(2, n), dtype=torch.uint8, device="cuda")
+    for i in range(20):
+        dev.fast_f64(u, v, dd, tau, tv=dtv, workspace=ws, flags=api.FAST_STATS_VALID if i else 0)
+        u, v = v, u
+    ws2 = torch.empty_like(ws)
+    dev.fast_f64(u, v, dd, tau, tv=dtv, workspace=ws2)
+    w = _k1_step(dev, u, [0.25, 0.25], tau, dtv)
+    torch.cuda.synchronize()
+    assert torch.equal(v, w)
+    assert dev.fast_diagnostics(ws2, 2, n) == 0
