@@ -51,7 +51,10 @@ constexpr int kNT = 256;       // threads per CTA
 constexpr int kG = 256;        // sub-tile (slope statistics granularity)
 constexpr int kSub = kT / kG;  // sub-tiles per tile (= warps per CTA)
 constexpr int kPer = kT / kNT; // outputs / sources per thread
-constexpr int kKCap = 2048;    // K values staged in shared memory
+#ifndef LOB_EMIT_UNROLL
+#define LOB_EMIT_UNROLL 1
+#endif
+constexpr int kEmitUnroll = LOB_EMIT_UNROLL;  // sources in flight per lane in the emission loop
 constexpr int kQCap = 256;     // queued source intervals (long / contended) per chunk
 constexpr int kC = 3584;       // sources staged per chunk (a typical tile + halo in one pass)
 #ifndef LOB_VCAP
@@ -106,9 +109,6 @@ __device__ __forceinline__ double kval(const double* vtab, int64_t vofs, int64_t
 // States: 0 undetermined, 1 convex, 2 concave.  A "vector" packs the current
 // state of the three runs started in U, Cx, Cc (2 bits each); the LUT maps
 // (vector, class) -> next vector | emits<<6 (one bit per run).
-__device__ __forceinline__ int fsm_class(double inc, double eta) {
-    return inc > eta ? 0 : (inc < -eta ? 1 : (inc == inc ? 2 : 3));
-}
 __host__ __device__ inline int fsm_next(int q, int c, int* emit) {
     if (q == 0) {
         *emit = 0;
@@ -160,27 +160,6 @@ __device__ __forceinline__ unsigned long long warp_fsm(unsigned long long f) {
     return f;  // valid in lane 0
 }
 
-__device__ __forceinline__ double warp_min(double x) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) x = fmin(x, __shfl_xor_sync(0xffffffffu, x, o));
-    return x;
-}
-__device__ __forceinline__ double warp_max(double x) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
-    return x;
-}
-__device__ __forceinline__ long long warp_min_ll(long long x) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) x = min(x, __shfl_xor_sync(0xffffffffu, x, o));
-    return x;
-}
-__device__ __forceinline__ long long warp_max_ll(long long x) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
-    return x;
-}
-
 struct EpiShared {
     unsigned kred[2][kNT / 32];
     unsigned long long fsm[kNT];
@@ -190,8 +169,6 @@ struct EpiShared {
 // contiguous (stride-8) access patterns are bank-conflict free.
 __host__ __device__ __forceinline__ constexpr int P8(int i) { return i + (i >> 3); }
 
-__device__ __forceinline__ double dmin2(double a, double b) { return b < a ? b : a; }
-__device__ __forceinline__ double dmax2(double a, double b) { return b > a ? b : a; }
 
 // High 32 bits of the order-preserving key: a monotone coarse key.  The
 // smallest (largest) double with a given coarse key is a lower (upper) bound
@@ -460,7 +437,7 @@ __device__ __forceinline__ void process_chunk(MainShared& S, const ChunkArgs& a)
     const int per = ((a.clen + kNT - 1) / kNT) * 32;
     const int iend = min(a.clen, (warp + 1) * per);
     unsigned ninl = 0;
-#pragma unroll 2
+#pragma unroll kEmitUnroll
     for (int i = warp * per + lane; i < iend; i += 32) {
         const double ul0 = a.ub[i], u0 = a.ub[i + 1], ur0 = a.ub[i + 2];
         const double zl = __dmul_rn(__dadd_rn(__dsub_rn(u0, ul0), a.pe), a.ia);
@@ -698,49 +675,60 @@ __global__ void __launch_bounds__(kNT, 4) fast_kernel(
     // threads 0..2 also evaluate the halo outputs jlo, j0+Tl, j0+Tl+1.
     const double* tvl = tv ? tv + line * tv_stride : nullptr;
     double* vals = S.ubuf;  // reuse: vals[i] = u^{n+1}(jlo + i), i = 0 .. Tl+2
-    auto finish = [&](int i, int j, double tvj) -> double {
-        const unsigned long long kk = S.keys[i];
-        double best;
-        if (kk == kInfBits) {
-            if (ok && diag) atomicAdd(diag, 1ull);
-            // direct scan of the full window (proj/tests/unit_scheme.cpp:184-190)
-            best = INFINITY;
-            int y = (j - first) % n;
-            if (y < 0) y += n;
-            for (int w = 0; w <= 2 * n; ++w) {
-                const double c2 = __dadd_rn(ul[y], kval(p.vtab, p.vofs, first + w, lc.drift, tau));
-                best = c2 < best ? c2 : best;
-                y = y == 0 ? n - 1 : y - 1;
-            }
-        } else {
-            best = __longlong_as_double(static_cast<long long>(kk));
+    // direct scan of the full window (proj/tests/unit_scheme.cpp:184-190) for outputs no
+    // interval reached (never, when the statistics gate holds); one copy of the loop
+    auto scan = [&](int j) -> double {
+        if (ok && diag) atomicAdd(diag, 1ull);
+        double best = INFINITY;
+        int y = (j - first) % n;
+        if (y < 0) y += n;
+        for (int w = 0; w <= 2 * n; ++w) {
+            const double c2 = __dadd_rn(ul[y], kval(p.vtab, p.vofs, first + w, lc.drift, tau));
+            best = c2 < best ? c2 : best;
+            y = y == 0 ? n - 1 : y - 1;
         }
-        return tvl ? __dsub_rn(best, tvj) : best;
+        return best;
     };
     {
-        // outputs j0 + t + kNT*m (vals index 1 + t + kNT*m): coalesced, conflict-free
-        double tvv[kPer];
+        // outputs j0 + t + kNT*m (vals index 1 + t + kNT*m): coalesced, conflict-free;
+        // the halo outputs jlo, j0+Tl, j0+Tl+1 (vals 0, Tl+1, Tl+2) go to threads 0..2 as m = kPer
+        double tvv[kPer + 1];
 #pragma unroll
         for (int m = 0; m < kPer; ++m) {
             const int i = 1 + tid + kNT * m;
             tvv[m] = (tvl && i <= Tl) ? __ldg(tvl + j0 + i - 1) : 0.0;
         }
+        const int ih = tid == 0 ? 0 : Tl + tid;  // halo vals index (tid < 3)
+        int jh = jlo + ih;
+        jh += jh < 0 ? n : 0;
+        jh -= jh >= n ? n : 0;
+        tvv[kPer] = (tvl && tid < 3) ? __ldg(tvl + jh) : 0.0;
         double* ol = out + line * p.n + j0;
+        unsigned miss = 0;
 #pragma unroll
-        for (int m = 0; m < kPer; ++m) {
-            const int i = 1 + tid + kNT * m;
-            if (i <= Tl) {
-                const double o = finish(i, j0 + i - 1, tvv[m]);
-                vals[P8(i)] = o;
-                ol[i - 1] = o;
+        for (int m = 0; m <= kPer; ++m) {
+            const int i = m < kPer ? 1 + tid + kNT * m : ih;
+            if (m < kPer ? i <= Tl : tid < 3) {
+                const unsigned long long kk = S.keys[i];
+                if (kk != kInfBits) {
+                    const double best = __longlong_as_double(static_cast<long long>(kk));
+                    const double o = tvl ? __dsub_rn(best, tvv[m]) : best;
+                    vals[P8(i)] = o;
+                    if (m < kPer) ol[i - 1] = o;
+                } else {
+                    miss |= 1u << m;
+                }
             }
         }
-        if (tid < 3) {
-            const int i = tid == 0 ? 0 : Tl + tid;
-            int j = jlo + i;
-            if (j < 0) j += n;
-            j %= n;
-            vals[P8(i)] = finish(i, j, tvl ? __ldg(tvl + j) : 0.0);
+        while (miss) {  // cold
+            const int m = __ffs(miss) - 1;
+            miss &= miss - 1;
+            const int i = m < kPer ? 1 + tid + kNT * m : ih;
+            const int j = m < kPer ? j0 + i - 1 : jh;
+            const double best = scan(j);
+            const double o = tvl ? __dsub_rn(best, __ldg(tvl + j)) : best;
+            vals[P8(i)] = o;
+            if (m < kPer) ol[i - 1] = o;
         }
         // FSM table for tile_stats (ubuf's tail is free once emission is done)
         unsigned* lut = reinterpret_cast<unsigned*>(S.post().lut);
