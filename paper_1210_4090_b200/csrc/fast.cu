@@ -55,10 +55,19 @@ constexpr int kPer = kT / kNT; // outputs / sources per thread
 #define LOB_EMIT_UNROLL 1
 #endif
 constexpr int kEmitUnroll = LOB_EMIT_UNROLL;  // sources in flight per lane in the emission loop
-constexpr int kQCap = 256;     // queued source intervals (long / contended) per chunk
-constexpr int kC = 3584;       // sources staged per chunk (a typical tile + halo in one pass)
+#ifndef LOB_FAST_MINB
+#define LOB_FAST_MINB 5  // CTAs per SM the main kernel is built for (registers, shared memory)
+#endif
+#ifndef LOB_QCAP
+#define LOB_QCAP 128
+#endif
+#ifndef LOB_KC
+#define LOB_KC 2840
+#endif
+constexpr int kQCap = LOB_QCAP;  // queued source intervals (long / contended) per chunk
+constexpr int kC = LOB_KC;       // sources staged per chunk (a typical tile + halo in one pass)
 #ifndef LOB_VCAP
-#define LOB_VCAP 1120
+#define LOB_VCAP 512
 #endif
 constexpr int kVCap = LOB_VCAP;  // v_d values staged per tile (TMA, with the first chunk)
 
@@ -339,7 +348,7 @@ struct MainShared {
     __device__ PostShared& post() { return *reinterpret_cast<PostShared*>(ubuf + kValsLen); }
 };
 static_assert(kValsLen * 8 + sizeof(PostShared) <= (kC + 8) * 8, "post-emission scratch fits in ubuf");
-static_assert(4 * (sizeof(MainShared) + 1024) <= 233472, "four CTAs per SM");
+static_assert(LOB_FAST_MINB * (sizeof(MainShared) + 1024) <= 233472, "LOB_FAST_MINB CTAs per SM");
 
 // ---- TMA bulk copies (cp.async.bulk) completed on an mbarrier ------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -526,7 +535,7 @@ __global__ void line_setup_kernel(const double* __restrict__ drift_arr, int64_t 
 // Main K2 kernel: one CTA = (tile of kT outputs, line); grid (tiles, lines).
 // All index arithmetic is 32-bit (n <= 2^29); "unrolled" source/output
 // indices y, j may lie in (-3n, 3n) and are reduced mod n only on access.
-__global__ void __launch_bounds__(kNT, 4) fast_kernel(
+__global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
     const double* __restrict__ u, double* __restrict__ out, const LineConst* __restrict__ lcs,
     const double* __restrict__ tv, int64_t tv_stride, int64_t* __restrict__ blocks_out,
     unsigned long long* __restrict__ diag, FastParams p, FastBuffers b) {
