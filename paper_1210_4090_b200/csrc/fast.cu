@@ -46,9 +46,12 @@
 
 namespace lob {
 
-constexpr int kT = 2048;       // outputs per CTA tile
+#ifndef LOB_KT
+#define LOB_KT 2048
+#endif
+constexpr int kT = LOB_KT;     // outputs per CTA tile
 constexpr int kNT = 256;       // threads per CTA
-constexpr int kG = 256;        // sub-tile (slope statistics granularity)
+constexpr int kG = kT / 8;     // sub-tile (slope statistics granularity): one warp each
 constexpr int kSub = kT / kG;  // sub-tiles per tile (= warps per CTA)
 constexpr int kPer = kT / kNT; // outputs / sources per thread
 #ifndef LOB_EMIT_UNROLL
@@ -62,12 +65,12 @@ constexpr int kEmitUnroll = LOB_EMIT_UNROLL;  // sources in flight per lane in t
 #define LOB_QCAP 128
 #endif
 #ifndef LOB_KC
-#define LOB_KC 2840
+#define LOB_KC 2400
 #endif
 constexpr int kQCap = LOB_QCAP;  // queued source intervals (long / contended) per chunk
 constexpr int kC = LOB_KC;       // sources staged per chunk (a typical tile + halo in one pass)
 #ifndef LOB_VCAP
-#define LOB_VCAP 512
+#define LOB_VCAP 1024
 #endif
 constexpr int kVCap = LOB_VCAP;  // v_d values staged per tile (TMA, with the first chunk)
 
@@ -155,7 +158,7 @@ __device__ __forceinline__ unsigned long long fsm_compose(unsigned long long a, 
 // Pair table: entry (v, c0, c1) = v' | emit_run0 << 6 | emit_run1 << 9 | emit_run2 << 12
 // after classes c0 then c1 (class 3 = no increment).  A run emits at most once
 // per pair (an emission leaves it undetermined), so 4 pairs accumulate into
-// 3-bit fields.  1024 x 2 B, copied to shared memory by each CTA.
+// 3-bit fields.  1024 x 2 B, read through the L1 (__ldg).
 __device__ unsigned short g_fsm_lut2[64 * 16];
 constexpr int kLut2 = 64 * 16;
 
@@ -240,7 +243,7 @@ __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line,
     };
 #pragma unroll
     for (int k = 0; k < kPer; k += 2) {
-        const unsigned x = lut[v * 16 + cls(k) * 4 + cls(k + 1)];
+        const unsigned x = __ldg(lut + v * 16 + cls(k) * 4 + cls(k + 1));
         v = static_cast<int>(x & 63u);
         acc += x >> 6;
     }
@@ -282,8 +285,7 @@ __global__ void __launch_bounds__(kNT) stats_kernel(const double* __restrict__ u
                                                     FastBuffers b) {
     __shared__ __align__(16) double vals[P8(kT + 3) + 1];
     __shared__ EpiShared sh;
-    __shared__ unsigned short lut[kLut2];
-    for (int i = threadIdx.x; i < kLut2; i += kNT) lut[i] = __ldg(g_fsm_lut2 + i);
+    const unsigned short* lut = g_fsm_lut2;
     const int64_t line = blockIdx.x / p.tiles;
     const int64_t tile = blockIdx.x - line * p.tiles;
     const int64_t j0 = tile * kT;
@@ -330,24 +332,21 @@ __global__ void combine_blocks_kernel(const unsigned long long* __restrict__ fsm
     blocks[line] = 1 + em;
 }
 
-// After the emission phase the tail of ubuf holds the epilogue's reduction
-// scratch and the FSM table (u^{n+1} occupies the first P8(kT + 3) + 1 doubles).
+// u^{n+1} of the tile (padded, for tile_stats) reuses ubuf after the emission
+// phase; the statistics' reduction scratch reuses keys after the epilogue.
 constexpr int kValsLen = P8(kT + 3) + 2;
-struct PostShared {
-    EpiShared epi;
-    unsigned short lut[kLut2];
-};
 struct MainShared {
     unsigned long long keys[kT + 4];   // exact-min slots (+inf bits = empty), lane-interleaved access
     unsigned long long mbar;           // TMA completion barrier for the source chunk
-    __align__(16) double ubuf[kC + 8];  // sources (unpadded) / then u^{n+1} (padded, stats) + PostShared
+    __align__(16) double ubuf[kC + 8];  // sources (unpadded) / then u^{n+1} (padded, stats)
     int3 queue[kQCap];
     __align__(16) double vbuf[kVCap];  // v_d of the tile's displacement range, converted to K(d)
     int ya, yb, nq, dlo, dhi, DLg, DRg, ok;
     unsigned int c_inline, c_queued, c_src, c_qent;
-    __device__ PostShared& post() { return *reinterpret_cast<PostShared*>(ubuf + kValsLen); }
+    __device__ EpiShared& epi() { return *reinterpret_cast<EpiShared*>(keys); }
 };
-static_assert(kValsLen * 8 + sizeof(PostShared) <= (kC + 8) * 8, "post-emission scratch fits in ubuf");
+static_assert(kValsLen <= kC + 8, "u^{n+1} of the tile fits in ubuf");
+static_assert(sizeof(EpiShared) <= (kT + 4) * 8, "statistics scratch fits in keys");
 static_assert(LOB_FAST_MINB * (sizeof(MainShared) + 1024) <= 233472, "LOB_FAST_MINB CTAs per SM");
 
 // ---- TMA bulk copies (cp.async.bulk) completed on an mbarrier ------------
@@ -739,9 +738,6 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
             vals[P8(i)] = o;
             if (m < kPer) ol[i - 1] = o;
         }
-        // FSM table for tile_stats (ubuf's tail is free once emission is done)
-        unsigned* lut = reinterpret_cast<unsigned*>(S.post().lut);
-        for (int i = tid; i < kLut2 / 2; i += kNT) lut[i] = __ldg(reinterpret_cast<const unsigned*>(g_fsm_lut2) + i);
     }
     __syncthreads();
     if (tid == 0 && diag) {
@@ -751,7 +747,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
         atomicAdd(diag + 4, static_cast<unsigned long long>(S.c_qent));
         atomicAdd(diag + 5, 1ull);
     }
-    tile_stats(vals, Tl, j0, line, tile, p, b, S.post().epi, S.post().lut);
+    tile_stats(vals, Tl, j0, line, tile, p, b, S.epi(), g_fsm_lut2);
     // block count of the INPUT u (decompose on the closed period): warp 0 of
     // the line's first tile composes the tile summaries
     if (blocks_out && tile == 0 && warp == 0) {
