@@ -41,6 +41,7 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <type_traits>
 
 #include "lob_internal.cuh"
 
@@ -208,6 +209,8 @@ __device__ __forceinline__ double hkey_upper(unsigned k) {
 //    proj/src/minplus.cpp:161-187).  For eta == 0 the increment class is the
 //    exact comparison of consecutive slopes (fl(a-b) > 0 <=> a > b for finite
 //    doubles; -0 == +0 like the reference's inc == 0).
+// FULL: a whole tile that is not the line's last (no bounds checks).
+template <bool FULL>
 __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line, int64_t tile,
                            const FastParams& p, const FastBuffers& b, EpiShared& sh,
                            const unsigned short* lut) {
@@ -215,14 +218,14 @@ __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line,
     const int i0 = kPer * tid;  // vals index of u(j0 + 8t - 1)
     double w[kPer + 3];
 #pragma unroll
-    for (int m = 0; m < kPer + 3; ++m) w[m] = (i0 + m <= Tl + 2) ? vals[P8(i0 + m)] : 0.0;
+    for (int m = 0; m < kPer + 3; ++m) w[m] = (FULL || i0 + m <= Tl + 2) ? vals[P8(i0 + m)] : 0.0;
     double sl[kPer + 2];
 #pragma unroll
     for (int m = 0; m < kPer + 2; ++m) sl[m] = __dsub_rn(w[m + 1], w[m]);
     unsigned kmin = 0xffffffffu, kmax = 0u;
 #pragma unroll
     for (int m = 0; m <= kPer; ++m) {
-        if (m <= Tl - i0) {  // s(j0 - 1 + 8t + m), up to s(j0 + Tl - 1)
+        if (FULL || m <= Tl - i0) {  // s(j0 - 1 + 8t + m), up to s(j0 + Tl - 1)
             const unsigned k = hkey(sl[m]);
             kmin = min(kmin, k);
             kmax = max(kmax, k);
@@ -236,7 +239,7 @@ __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line,
     const bool exact_cmp = p.eta == 0.0;
     auto cls = [&](int k) -> int {  // class of increment e = j0 + i0 + 1 + k
         const int i = i0 + 1 + k;
-        if (!(i <= Tl && j0 + i <= p.n - 1)) return 3;
+        if (!FULL && !(i <= Tl && j0 + i <= p.n - 1)) return 3;
         if (exact_cmp) return sl[k + 2] > sl[k + 1] ? 0 : (sl[k + 2] < sl[k + 1] ? 1 : 2);
         const double inc = __dsub_rn(sl[k + 2], sl[k + 1]);
         return inc > p.eta ? 0 : (inc < -p.eta ? 1 : 2);
@@ -254,7 +257,7 @@ __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line,
     kmax = __reduce_max_sync(0xffffffffu, kmax);
     if (lane == 0) {
         const double smn = hkey_lower(kmin), smx = hkey_upper(kmax);
-        if (warp * kG < Tl) {
+        if (FULL || warp * kG < Tl) {
             const int64_t q = (j0 + warp * kG) / kG;
             b.sub_out[line * p.subs + q] = make_double2(smn, smx);
         }
@@ -298,7 +301,10 @@ __global__ void __launch_bounds__(kNT) stats_kernel(const double* __restrict__ u
         vals[P8(i)] = ul[j];
     }
     __syncthreads();
-    tile_stats(vals, Tl, j0, line, tile, p, b, sh, lut);
+    if (Tl == kT && j0 + kT <= p.n - 1)
+        tile_stats<true>(vals, Tl, j0, line, tile, p, b, sh, lut);
+    else
+        tile_stats<false>(vals, Tl, j0, line, tile, p, b, sh, lut);
 }
 
 __global__ void line_init_kernel(unsigned long long* L, int64_t lines) {
@@ -697,14 +703,15 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
         }
         return best;
     };
-    {
+    auto epilogue = [&](auto full_tile) {
+        constexpr bool FULL = decltype(full_tile)::value;  // a whole tile: no bounds checks
         // outputs j0 + t + kNT*m (vals index 1 + t + kNT*m): coalesced, conflict-free;
         // the halo outputs jlo, j0+Tl, j0+Tl+1 (vals 0, Tl+1, Tl+2) go to threads 0..2 as m = kPer
         double tvv[kPer + 1];
 #pragma unroll
         for (int m = 0; m < kPer; ++m) {
             const int i = 1 + tid + kNT * m;
-            tvv[m] = (tvl && i <= Tl) ? __ldg(tvl + j0 + i - 1) : 0.0;
+            tvv[m] = (tvl && (FULL || i <= Tl)) ? __ldg(tvl + j0 + i - 1) : 0.0;
         }
         const int ih = tid == 0 ? 0 : Tl + tid;  // halo vals index (tid < 3)
         int jh = jlo + ih;
@@ -716,7 +723,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
 #pragma unroll
         for (int m = 0; m <= kPer; ++m) {
             const int i = m < kPer ? 1 + tid + kNT * m : ih;
-            if (m < kPer ? i <= Tl : tid < 3) {
+            if (m < kPer ? (FULL || i <= Tl) : tid < 3) {
                 const unsigned long long kk = S.keys[i];
                 if (kk != kInfBits) {
                     const double best = __longlong_as_double(static_cast<long long>(kk));
@@ -738,7 +745,11 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
             vals[P8(i)] = o;
             if (m < kPer) ol[i - 1] = o;
         }
-    }
+    };
+    if (Tl == kT)
+        epilogue(std::true_type{});
+    else
+        epilogue(std::false_type{});
     __syncthreads();
     if (tid == 0 && diag) {
         atomicAdd(diag + 1, static_cast<unsigned long long>(S.c_src));
@@ -747,7 +758,10 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
         atomicAdd(diag + 4, static_cast<unsigned long long>(S.c_qent));
         atomicAdd(diag + 5, 1ull);
     }
-    tile_stats(vals, Tl, j0, line, tile, p, b, S.epi(), g_fsm_lut2);
+    if (Tl == kT && j0 + kT <= n - 1)
+        tile_stats<true>(vals, Tl, j0, line, tile, p, b, S.epi(), g_fsm_lut2);
+    else
+        tile_stats<false>(vals, Tl, j0, line, tile, p, b, S.epi(), g_fsm_lut2);
     // block count of the INPUT u (decompose on the closed period): warp 0 of
     // the line's first tile composes the tile summaries
     if (blocks_out && tile == 0 && warp == 0) {
