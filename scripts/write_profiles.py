@@ -30,9 +30,9 @@ b1 = src_line(F, "__syncthreads();  // keys, LUT, gate")
 pc = src_line(F, "process_chunk<true>(S, ca);")
 pf = src_line(F, "process_chunk<false>(S, ca);")
 ep = src_line(F, "// ---- epilogue: exact min")
-ts = src_line(F, "tile_stats(vals, Tl, j0, line, tile, p, b, S.post().epi, S.post().lut);")
+ts = src_line(F, "tile_stats<true>(vals, Tl, j0, line, tile, p, b, S.epi(), g_fsm_lut2);") - 1
 ranges = (f"init:{k}-{w0 - 1},warp0_gate_scan_tma:{w0}-{b1},chunk_setup:{b1 + 1}-{pc - 1},emit_staged:{pc}-{pc},"
-          f"emit_unstaged:{pf}-{pf},epilogue:{ep}-{ts - 1},tile_stats:{ts}-{ts},blocks_tail:{ts + 1}-{ts + 30}")
+          f"emit_unstaged:{pf}-{pf},epilogue:{ep}-{ts - 1},tile_stats:{ts}-{ts + 3},blocks_tail:{ts + 4}-{ts + 30}")
 with open(os.path.join(ROOT, "profiles", f"{tag}_k2_fast_c2_ncu_summary.txt"), "w") as f:
     f.write("# K2 fast_kernel, C2 (256 x 65536) after 1000 steps; one launch, ncu --set full --clock-control none\n")
     f.write(run("scripts/ncu_summary.py", k2))
