@@ -115,12 +115,13 @@ int lob_minplus_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lin
                          int flags, void* stream);
 
 /* Fast-engine counters, cumulative since the last call without
- * LOB_FAST_STATS_VALID on this workspace (counters[16]):
+ * LOB_FAST_STATS_VALID on this workspace (counters[8]):
  *  [0] outputs for which the local-minimum walk produced no candidate and the
  *      exact direct scan was used instead (0 in correct operation),
  *  [1] sources scanned, [2] candidates emitted inline, [3] candidates from
- *  queued long intervals, [4] queued intervals, [5] tiles processed,
- *  [8..13] per-phase SM cycles when LOB_FAST_PROFILE is set in the environment. */
+ *  queued intervals, [4] queued intervals, [5] tiles processed,
+ *  [6] tiles whose K range did not fit the shared-memory stage, [7] sum of
+ *  the tiles' K range lengths. */
 int lob_fast_diagnostics(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n,
                          uint64_t* counters);
 

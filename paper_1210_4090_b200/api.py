@@ -185,11 +185,12 @@ class Device:
         self._check(st, "lob_minplus_fast_f64")
 
     def fast_counters(self, workspace, lines: int, n: int) -> dict:
-        v = (ctypes.c_uint64 * 16)()
+        """The fast engine's work counters (include/laxol_b200.h, lob_fast_diagnostics)."""
+        v = (ctypes.c_uint64 * 8)()
         st = self.lib.lob_fast_diagnostics(self.ctx, _ptr(workspace), lines, n, v)
         self._check(st, "lob_fast_diagnostics")
         keys = ["missed_outputs", "sources", "inline_candidates", "queued_candidates", "queued_intervals",
-                "tiles", "tiles_k_unstaged", "k_range_sum", "cyc_init", "cyc_scan", "cyc_load", "cyc_emit", "cyc_epilogue", "cyc_stats"]
+                "tiles", "tiles_k_unstaged", "k_range_sum"]
         return {k: int(v[i]) for i, k in enumerate(keys)}
 
     def fast_diagnostics(self, workspace, lines: int, n: int) -> int:
