@@ -81,12 +81,9 @@ int launch_cfg(lob_ctx* ctx, const T* u, T* out, int64_t lines, int64_t n, const
     constexpr int L = TJ + TW;
     const size_t smem = (padded<R>(L) + 1 + TW) * sizeof(T);
     auto kern = direct_kernel<T, R, NT, TW>;
-    static bool attr_set = false;
-    if (!attr_set) {
+    if (first_time(ctx, reinterpret_cast<const void*>(kern)))
         LOB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(smem)));
-        attr_set = true;
-    }
     const int64_t tiles = (n + TJ - 1) / TJ;
     const int64_t blocks = tiles * lines;
     if (blocks > 0x7fffffffll) return set_error(ctx, LOB_INVALID_INPUT, "direct: grid too large");

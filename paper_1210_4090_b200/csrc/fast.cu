@@ -802,10 +802,9 @@ static WsLayout ws_layout(int64_t lines, int64_t n) {
 
 size_t fast_workspace_bytes(int64_t lines, int64_t n) { return ws_layout(lines, n).total; }
 
-static bool g_lut_ready = false;
 
 static int ensure_lut(lob_ctx* ctx) {
-    if (g_lut_ready) return LOB_OK;
+    if (!first_time(ctx, reinterpret_cast<const void*>(&g_fsm_lut2))) return LOB_OK;
     unsigned short lut[kLut2];
     for (int v = 0; v < 64; ++v)
         for (int c0 = 0; c0 < 4; ++c0)
@@ -825,7 +824,6 @@ static int ensure_lut(lob_ctx* ctx) {
                 lut[v * 16 + c0 * 4 + c1] = static_cast<unsigned short>(static_cast<unsigned>(nv) | (em << 6));
             }
     LOB_CUDA_TRY(ctx, cudaMemcpyToSymbol(g_fsm_lut2, lut, sizeof(lut)));
-    g_lut_ready = true;
     return LOB_OK;
 }
 
@@ -931,12 +929,9 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
         ctx->launches += 3;
         LOB_CUDA_TRY(ctx, cudaGetLastError());
     }
-    static bool attr = false;
-    if (!attr) {
+    if (first_time(ctx, reinterpret_cast<const void*>(fast_kernel)))
         LOB_CUDA_TRY(ctx, cudaFuncSetAttribute(fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(sizeof(MainShared))));
-        attr = true;
-    }
     dim3 grid(static_cast<unsigned>(p.tiles), static_cast<unsigned>(lines));
     fast_kernel<<<grid, kNT, sizeof(MainShared), s>>>(u, out, lcs, tv, tv_stride, blocks, diag, p, b);
     ctx->launches += 1;

@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <map>
+#include <set>
 #include <string>
 #include <tuple>
 
@@ -37,12 +38,17 @@ struct lob_ctx {
     // per-chunk events (inputs ready, step done) + one for the shared inputs
     cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t aux_ev[33] = {};
+    // one-time per-device setup done through this context (kernel attributes, tables)
+    std::set<const void*> done_once;
     // scratch for host entry points
     void* scratch = nullptr;
     size_t scratch_bytes = 0;
 };
 
 namespace lob {
+
+// true the first time `key` is seen by this context (per-device state is per context)
+inline bool first_time(lob_ctx* ctx, const void* key) { return ctx->done_once.insert(key).second; }
 
 inline int set_error(lob_ctx* ctx, int code, const std::string& msg) {
     if (ctx) ctx->last_error = msg;
