@@ -540,6 +540,7 @@ __global__ void line_setup_kernel(const double* __restrict__ drift_arr, int64_t 
 // Main K2 kernel: one CTA = (tile of kT outputs, line); grid (tiles, lines).
 // All index arithmetic is 32-bit (n <= 2^29); "unrolled" source/output
 // indices y, j may lie in (-3n, 3n) and are reduced mod n only on access.
+template <bool TMA>
 __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
     const double* __restrict__ u, double* __restrict__ out, const LineConst* __restrict__ lcs,
     const double* __restrict__ tv, int64_t tv_stride, int64_t* __restrict__ blocks_out,
@@ -556,7 +557,9 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
     const int jlo = j0 - 1;     // outputs evaluated: jlo .. jlo + jspan (unrolled)
     const int jspan = Tl + 2;
     const int jhi = jlo + jspan;
-    const bool big = n >= kC + 8;  // one conditional wrap suffices for source loads
+    // TMA bulk copies (16-byte granules: even n, aligned rows; TMA) when the line is long
+    // enough for one conditional wrap per chunk; else a cooperative load
+    const bool big = TMA && n >= kC + 8;
     const double* ul = u + line * p.n;
     const LineConst lc = lcs[line];
     const double tau = p.tau, ia = p.ia, pe = lc.pe, hl = lc.hl, hr = lc.hr;
@@ -899,6 +902,8 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     if (st) return st;
     const int64_t nblk = lines * p.tiles;
     if (nblk > 0x7fffffffll) return set_error(ctx, LOB_INVALID_INPUT, "fast: grid too large");
+    const bool tma = (n % 2 == 0) && (reinterpret_cast<uintptr_t>(u) % 16 == 0);
+    auto kern = tma ? fast_kernel<true> : fast_kernel<false>;
     if (ctx->ws_shape[workspace] != std::make_pair(lines, n)) {
         ctx->ws_shape[workspace] = std::make_pair(lines, n);
         flags &= ~LOB_FAST_STATS_VALID;
@@ -929,11 +934,11 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
         ctx->launches += 3;
         LOB_CUDA_TRY(ctx, cudaGetLastError());
     }
-    if (first_time(ctx, reinterpret_cast<const void*>(fast_kernel)))
-        LOB_CUDA_TRY(ctx, cudaFuncSetAttribute(fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (first_time(ctx, reinterpret_cast<const void*>(kern)))
+        LOB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(sizeof(MainShared))));
     dim3 grid(static_cast<unsigned>(p.tiles), static_cast<unsigned>(lines));
-    fast_kernel<<<grid, kNT, sizeof(MainShared), s>>>(u, out, lcs, tv, tv_stride, blocks, diag, p, b);
+    kern<<<grid, kNT, sizeof(MainShared), s>>>(u, out, lcs, tv, tv_stride, blocks, diag, p, b);
     ctx->launches += 1;
     LOB_CUDA_TRY(ctx, cudaGetLastError());
     counter += 1;

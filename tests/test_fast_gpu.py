@@ -215,3 +215,24 @@ def test_fast_equals_direct_c5_full_line(dev):
     torch.cuda.synchronize()
     assert torch.equal(v, w)
     assert dev.fast_diagnostics(ws2, 2, n) == 0
+
+
+@pytest.mark.parametrize("n,offset", [(4097, 0), (6001, 0), (8192, 1), (5000, 1), (2050, 0)])
+def test_fast_odd_lengths_and_unaligned_rows(dev, orc, n, offset):
+    """Odd n (rows not 16-byte aligned for bulk copies), rows starting at an odd
+    element offset, and partial last tiles: the cooperative-load path, == oracle."""
+    import torch
+    tau, lines = 0.02, 3
+    rng = np.random.default_rng(n + offset)
+    u = np.cumsum(rng.uniform(-1.0 / n, 1.0 / n, (lines, n)), axis=1)
+    u -= np.linspace(0, 1, n, endpoint=False)[None, :] * u[:, -1:]
+    drifts = np.array([-0.8, 0.1, 1.3])
+    buf = torch.zeros(lines * n + offset, dtype=torch.float64, device="cuda")
+    du = buf[offset:].view(lines, n)
+    du.copy_(to_dev(u))
+    out = torch.empty((lines, n), dtype=torch.float64, device="cuda")
+    ws = torch.empty(dev.fast_workspace_bytes(lines, n), dtype=torch.uint8, device="cuda")
+    dev.fast_f64(du, out, to_dev(drifts), tau, workspace=ws)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), oracle_step(orc, u, drifts, tau))
+    assert dev.fast_diagnostics(ws, lines, n) == 0
