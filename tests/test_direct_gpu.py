@@ -158,3 +158,13 @@ def test_direct_screen_nan_inputs_match_reference_min(dev, orc):
     u[0, 17] = np.nan
     got, want = run_direct(dev, u, K, first), orc.direct(u, K, first)
     assert np.array_equal(got, want, equal_nan=True)
+
+
+@pytest.mark.parametrize("n", [2049, 4097, 515])
+def test_direct_odd_lengths(dev, orc, n):
+    """Odd n on the 16-output and 8-output register tilings (partial last tiles and chunks)."""
+    rng = np.random.default_rng(n)
+    K, first, _, _ = orc.kernel(n, 0.03, -0.4)
+    u = np.cumsum(rng.uniform(-1.0 / n, 1.0 / n, (3, n)), axis=1)
+    tv = rng.uniform(-1e-3, 1e-3, n)
+    assert np.array_equal(run_direct(dev, u, K, first, tv=tv), orc.direct(u, K, first, tv=tv))

@@ -72,3 +72,22 @@ def test_split_separable_data_stays_separable(dev, orc):
     f1 = orc.direct(f[None, :], K, first)[0]
     g1 = orc.direct(g[None, :], K, first)[0]
     assert np.max(np.abs(got - (f1[:, None] + g1[None, :]))) <= 1e-13 * np.max(np.abs(got))
+
+
+@pytest.mark.parametrize("engine", [api.ENGINE_DIRECT, api.ENGINE_FAST])
+@pytest.mark.parametrize("n", [100, 513])
+def test_split_non_tile_multiple_sizes(dev, orc, ref, engine, n):
+    """n not a multiple of the 32x32 transpose tile (and odd): == reference at 100, == oracle at 513."""
+    tau, t = 0.02, 0.1
+    u = api.gen_c4_u0(n)
+    a = api.gen_cos(n)
+    b = api.c4_time_term(t + tau)
+    got = run_split(dev, u, tau, 0.3, -0.7, a1=a, a2=a, b=b, engine=engine)
+    if n <= 128:
+        want = ref.split_step_2d(u, tau, 0.3, -0.7, pot_kind=1, t=t)
+    else:
+        k1, f1, _, _ = orc.kernel(n, tau, 0.3)
+        k2, f2, _, _ = orc.kernel(n, tau, -0.7)
+        tv = api.tau_v(np.add.outer(a, np.zeros(n)) * a[None, :] + b, tau)
+        want = orc.split2d(u, k1, f1, k2, f2, tv=tv)
+    assert np.array_equal(got, want)
