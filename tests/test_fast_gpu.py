@@ -236,3 +236,29 @@ def test_fast_odd_lengths_and_unaligned_rows(dev, orc, n, offset):
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), oracle_step(orc, u, drifts, tau))
     assert dev.fast_diagnostics(ws, lines, n) == 0
+
+
+@pytest.mark.parametrize("eta", [1e-7, 1e-4, 0.05])
+def test_fast_eta_blocks_match_reference_naive(dev, orc, ref, eta):
+    """eta > 0: the step stays exact and the block count is decompose(u, eta)'s, as the
+    reference's Naive engine reports it (proj/src/scheme.cpp:118-121)."""
+    import torch
+    n, tau, lines = 1024, 0.05, 4
+    rng = np.random.default_rng(int(eta * 1e7) + 5)
+    u = np.cumsum(rng.uniform(-2.0 / n, 2.0 / n, (lines, n)), axis=1)
+    u -= np.linspace(0, 1, n, endpoint=False)[None, :] * u[:, -1:]
+    got, blocks = fast_step(dev, u, 0.5, tau, blocks=True)
+    assert np.array_equal(got.cpu().numpy(), oracle_step(orc, u, 0.5, tau))
+    for l in range(lines):
+        _, rb, st = ref.kinetic_convolve(u[l], n, tau, 0.5, eta=eta, engine=1)
+        assert st == 0
+    db = torch.empty(lines, dtype=torch.int64, device="cuda")
+    ws = torch.empty(dev.fast_workspace_bytes(lines, n), dtype=torch.uint8, device="cuda")
+    out = torch.empty((lines, n), dtype=torch.float64, device="cuda")
+    dev.fast_f64(to_dev(u), out, to_dev(np.full(lines, 0.5)), tau, eta=eta, blocks=db, workspace=ws)
+    dev.block_counts(to_dev(u), db2 := torch.empty(lines, dtype=torch.int64, device="cuda"), eta=eta)
+    torch.cuda.synchronize()
+    want = [ref.kinetic_convolve(u[l], n, tau, 0.5, eta=eta, engine=1)[1] for l in range(lines)]
+    assert list(db.cpu().numpy()) == want
+    assert list(db2.cpu().numpy()) == want
+    assert np.array_equal(out.cpu().numpy(), oracle_step(orc, u, 0.5, tau))
