@@ -567,7 +567,12 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
     const int dmin_w = first + 1, dmax_w = first + 2 * n - 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
+    // programmatic dependent launch: the next step's grid may start its prologue once
+    // every CTA of this one is running; this grid waits for the previous one (its u,
+    // statistics and the buffers it still reads) before touching global memory
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     for (int i = tid; i <= jspan; i += kNT) S.keys[i] = kInfBits;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     // reset the line statistics buffer two steps ahead
     if (tile == 0 && tid < 4) b.line_reset[line * 4 + tid] = (tid & 1) ? 0ull : ~0ull;
 
@@ -938,7 +943,18 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
         LOB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(sizeof(MainShared))));
     dim3 grid(static_cast<unsigned>(p.tiles), static_cast<unsigned>(lines));
-    kern<<<grid, kNT, sizeof(MainShared), s>>>(u, out, lcs, tv, tv_stride, blocks, diag, p, b);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kNT);
+    cfg.dynamicSmemBytes = sizeof(MainShared);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    LOB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, u, out, const_cast<const LineConst*>(lcs), tv, tv_stride,
+                                         blocks, diag, p, b));
     ctx->launches += 1;
     LOB_CUDA_TRY(ctx, cudaGetLastError());
     counter += 1;
