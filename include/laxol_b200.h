@@ -108,6 +108,11 @@ int lob_minplus_window_f64(lob_ctx* ctx, const double* u, double* out, int64_t l
  * the same workspace, drift, tau and n (the device-resident evolve loop),
  * else 0 and the statistics are recomputed (one extra read of u). */
 #define LOB_FAST_STATS_VALID 1
+/* With LOB_FAST_STATS_VALID: nothing else ran on `stream` since the previous
+ * lob_minplus_fast_f64 call on this workspace (whose out is this u), so each
+ * tile may start as soon as its own line's previous step is done instead of
+ * after the whole previous grid (back-to-back stepping loops). */
+#define LOB_FAST_CHAINED 2
 int lob_fast_workspace_bytes(int64_t lines, int64_t n, size_t* bytes);
 int lob_minplus_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
                          const double* drift, double tau, const double* tv, int64_t tv_stride,

@@ -21,6 +21,7 @@ LOB_CUDA_ERROR = 3
 ENGINE_DIRECT = 0
 ENGINE_FAST = 1
 FAST_STATS_VALID = 1
+FAST_CHAINED = 2
 DIRECT_SCREENED = 0
 DIRECT_PLAIN = 1
 

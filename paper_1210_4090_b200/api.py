@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _capi
-from ._capi import (DIRECT_PLAIN, DIRECT_SCREENED, ENGINE_DIRECT, ENGINE_FAST, FAST_STATS_VALID, EvaluationError,  # noqa: F401
+from ._capi import (DIRECT_PLAIN, DIRECT_SCREENED, ENGINE_DIRECT, ENGINE_FAST, FAST_CHAINED, FAST_STATS_VALID, EvaluationError,  # noqa: F401
                     InvalidInput, check)
 
 

@@ -540,11 +540,25 @@ __global__ void line_setup_kernel(const double* __restrict__ drift_arr, int64_t 
 // Main K2 kernel: one CTA = (tile of kT outputs, line); grid (tiles, lines).
 // All index arithmetic is 32-bit (n <= 2^29); "unrolled" source/output
 // indices y, j may lie in (-3n, 3n) and are reduced mod n only on access.
-template <bool TMA>
+// Loads of data the previous step's grid may still be finishing (chained mode):
+// through L2, never a stale L1 line.
+template <bool CHAIN, typename T>
+__device__ __forceinline__ T xload(const T* p) {
+    if constexpr (CHAIN) return __ldcg(p);
+    else return *p;
+}
+
+// TMA: rows may be bulk-copied (even n, aligned).  CHAIN: the previous operation on
+// the stream was the previous step on this workspace (and it released); a tile waits
+// only for the warps of its own line at that step (per-line release counters, `need`)
+// instead of the whole previous grid, so consecutive steps overlap.  RELEASE: count
+// this step's warps into the per-line counters for a chained successor.
+template <bool TMA, bool CHAIN, bool RELEASE>
 __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
     const double* __restrict__ u, double* __restrict__ out, const LineConst* __restrict__ lcs,
     const double* __restrict__ tv, int64_t tv_stride, int64_t* __restrict__ blocks_out,
-    unsigned long long* __restrict__ diag, FastParams p, FastBuffers b) {
+    unsigned long long* __restrict__ diag, FastParams p, FastBuffers b, unsigned* __restrict__ done,
+    unsigned need) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     MainShared& S = *reinterpret_cast<MainShared*>(smem_raw);
 
@@ -572,7 +586,26 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
     // statistics and the buffers it still reads) before touching global memory
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     for (int i = tid; i <= jspan; i += kNT) S.keys[i] = kInfBits;
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if constexpr (CHAIN) {
+        if (warp == 0) {
+            if (lane == 0) {
+                unsigned v;
+                const long long t0 = clock64();
+                for (;;) {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(done + line) : "memory");
+                    if (v >= need) break;
+                    __nanosleep(128);
+                    // a misused LOB_FAST_CHAINED (the previous step is not on this stream) ends
+                    // in an error, not a hang
+                    if (clock64() - t0 > (1ll << 33)) __trap();
+                }
+                asm volatile("fence.proxy.async.global;" ::: "memory");  // for the TMA reads of u
+            }
+            __syncwarp();
+        }
+    } else {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
     // reset the line statistics buffer two steps ahead
     if (tile == 0 && tid < 4) b.line_reset[line * 4 + tid] = (tid & 1) ? 0ull : ~0ull;
 
@@ -580,7 +613,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
     if (warp == 0) {
         // line statistics: oscillation gate and global displacement bounds
         const unsigned long long* L = b.line_in + line * 4;
-        const double smin = dkey_inv(L[2]), smax = dkey_inv(L[3]);
+        const double smin = dkey_inv(xload<CHAIN>(L + 2)), smax = dkey_inv(xload<CHAIN>(L + 3));
         int DLg = dmin_w, DRg = dmax_w;
         // oscillation of a periodic line <= (n/2) max|slope| (shorter arc)
         const double osc_bound = 0.5 * static_cast<double>(n) * fmax(fabs(smin), fabs(smax));
@@ -605,7 +638,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
             for (int Q = Q0 + lane; Q <= Q1; Q += 32) {
                 const int k = Q >= 0 ? Q / subs : -((subs - 1 - Q) / subs);
                 const int q = Q - k * subs;
-                const double2 sb = b.sub_in[line * p.subs + q];
+                const double2 sb = xload<CHAIN>(b.sub_in + line * p.subs + q);
                 const int ys = k * n + q * kG;
                 const int ye = ys + min(kG, n - q * kG) - 1;
                 const int dl = max(__double2int_ru(__dmul_rn(__dadd_rn(sb.x, pe), ia) + hl), DLg);
@@ -679,7 +712,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
                 }
             } else {
                 const int bm = wrap_idx(yc - 1, n);
-                for (int i = tid; i < clen + 2; i += kNT) S.ubuf[i] = __ldg(ul + (bm + i) % n);
+                for (int i = tid; i < clen + 2; i += kNT) S.ubuf[i] = CHAIN ? __ldcg(ul + (bm + i) % n) : __ldg(ul + (bm + i) % n);
                 __syncthreads();
             }
             const double* ub = S.ubuf + sh;
@@ -705,7 +738,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
         int y = (j - first) % n;
         if (y < 0) y += n;
         for (int w = 0; w <= 2 * n; ++w) {
-            const double c2 = __dadd_rn(ul[y], kval(p.vtab, p.vofs, first + w, lc.drift, tau));
+            const double c2 = __dadd_rn(xload<CHAIN>(ul + y), kval(p.vtab, p.vofs, first + w, lc.drift, tau));
             best = c2 < best ? c2 : best;
             y = y == 0 ? n - 1 : y - 1;
         }
@@ -776,7 +809,8 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
         int q = 0;
         int64_t em = 0;
         for (int t0 = 0; t0 < tiles; t0 += 32) {
-            const unsigned long long mine = t0 + lane < tiles ? b.fsm_in[line * p.tiles + t0 + lane] : fsm_identity();
+            const unsigned long long mine =
+                t0 + lane < tiles ? xload<CHAIN>(b.fsm_in + line * p.tiles + t0 + lane) : fsm_identity();
             const int cnt = min(32, tiles - t0);
             for (int k = 0; k < cnt; ++k) {
                 const unsigned long long f = __shfl_sync(0xffffffffu, mine, k);
@@ -786,6 +820,13 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
         }
         if (lane == 0) blocks_out[line] = 1 + em;
     }
+    // release this warp's share of the tile to the next step's tiles of the line: a
+    // gpu-scope release reduction by one lane, cumulative over the warp's writes (no CTA
+    // barrier: warps retire independently; the line is done at kNT/32 * tiles counts)
+    if constexpr (RELEASE) {
+        __syncwarp();
+        if (lane == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(done + line) : "memory");
+    }
 }
 
 }  // namespace
@@ -794,7 +835,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
 // workspace: sub[2][lines][subs] double2 | fsm[2][lines][tiles] u64 |
 //            line[3][lines][4] u64 | LineConst[lines] | diag u64
 struct WsLayout {
-    size_t sub, fsm, line, lc, diag, total;
+    size_t sub, fsm, line, lc, diag, done, total;
 };
 static WsLayout ws_layout(int64_t lines, int64_t n) {
     const int64_t tiles = (n + kT - 1) / kT, subs = (n + kG - 1) / kG;
@@ -804,7 +845,8 @@ static WsLayout ws_layout(int64_t lines, int64_t n) {
     w.line = w.fsm + 2 * static_cast<size_t>(lines * tiles) * sizeof(unsigned long long);
     w.lc = w.line + 3 * static_cast<size_t>(lines) * 4 * sizeof(unsigned long long);
     w.diag = w.lc + static_cast<size_t>(lines) * sizeof(LineConst);
-    w.total = w.diag + 64;
+    w.done = w.diag + 64;  // [lines] tiles finished since the statistics were (re)computed
+    w.total = w.done + (static_cast<size_t>(lines) * sizeof(unsigned) + 255) / 256 * 256;
     return w;
 }
 
@@ -908,7 +950,6 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     const int64_t nblk = lines * p.tiles;
     if (nblk > 0x7fffffffll) return set_error(ctx, LOB_INVALID_INPUT, "fast: grid too large");
     const bool tma = (n % 2 == 0) && (reinterpret_cast<uintptr_t>(u) % 16 == 0);
-    auto kern = tma ? fast_kernel<true> : fast_kernel<false>;
     if (ctx->ws_shape[workspace] != std::make_pair(lines, n)) {
         ctx->ws_shape[workspace] = std::make_pair(lines, n);
         flags &= ~LOB_FAST_STATS_VALID;
@@ -916,6 +957,8 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     // the statistics describe the previous call's output: any other input recomputes them
     if (ctx->ws_last_out[workspace] != static_cast<const void*>(u)) flags &= ~LOB_FAST_STATS_VALID;
     ctx->ws_last_out[workspace] = out;
+    // the per-line done counters restart with the statistics (keeps them in range)
+    if (ctx->ws_chain[workspace] * p.tiles * (kNT / 32) > 0xf0000000ll) flags &= ~LOB_FAST_STATS_VALID;
     int64_t& counter = ctx->ws_counter[workspace];
     FastBuffers b = make_buffers(workspace, lines, n, counter);
     const WsLayout w = ws_layout(lines, n);
@@ -926,6 +969,8 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
         // per-line constants (valid while drift/tau/n and the workspace are unchanged)
         line_setup_kernel<<<static_cast<unsigned>((lines + 127) / 128), 128, 0, s>>>(drift, lines, p, lcs);
         LOB_CUDA_TRY(ctx, cudaMemsetAsync(diag, 0, 8 * sizeof(unsigned long long), s));
+        LOB_CUDA_TRY(ctx, cudaMemsetAsync(static_cast<char*>(workspace) + w.done, 0, lines * sizeof(unsigned), s));
+        ctx->ws_chain[workspace] = 0;
         ctx->launches += 1;
         // statistics of the given u into the "in" buffers; "out" line stats reset
         FastBuffers sb = b;
@@ -939,6 +984,24 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
         ctx->launches += 3;
         LOB_CUDA_TRY(ctx, cudaGetLastError());
     }
+    // chained: every LOB_FAST_CHAINED call releases per-line counters; it waits on them
+    // (instead of on the whole previous grid) when the previous call on this workspace
+    // released too (the counters then hold chain * tiles * warps counts per line)
+    int64_t& chain = ctx->ws_chain[workspace];
+    const bool release = flags & LOB_FAST_CHAINED;
+    const bool chained = release && (flags & LOB_FAST_STATS_VALID) && chain > 0;
+    if (!release) chain = 0;  // the counters no longer describe the previous call
+    unsigned* done = reinterpret_cast<unsigned*>(static_cast<char*>(workspace) + w.done);
+    if (release && chain == 0) LOB_CUDA_TRY(ctx, cudaMemsetAsync(done, 0, lines * sizeof(unsigned), s));
+    using KernT = void (*)(const double*, double*, const LineConst*, const double*, int64_t, int64_t*,
+                           unsigned long long*, FastParams, FastBuffers, unsigned*, unsigned);
+    static const KernT kerns[2][2][2] = {
+        {{fast_kernel<false, false, false>, fast_kernel<false, false, true>},
+         {fast_kernel<false, true, false>, fast_kernel<false, true, true>}},
+        {{fast_kernel<true, false, false>, fast_kernel<true, false, true>},
+         {fast_kernel<true, true, false>, fast_kernel<true, true, true>}}};
+    auto kern = kerns[tma][chained][release];
+    const unsigned need = static_cast<unsigned>(chain * p.tiles * (kNT / 32));
     if (first_time(ctx, reinterpret_cast<const void*>(kern)))
         LOB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(sizeof(MainShared))));
@@ -954,7 +1017,8 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     LOB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, u, out, const_cast<const LineConst*>(lcs), tv, tv_stride,
-                                         blocks, diag, p, b));
+                                         blocks, diag, p, b, done, need));
+    if (release) chain += 1;
     ctx->launches += 1;
     LOB_CUDA_TRY(ctx, cudaGetLastError());
     counter += 1;

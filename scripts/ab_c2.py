@@ -18,10 +18,12 @@ tv = torch.from_numpy(api.tau_v(api.gen_potential(2, n), tau)).cuda()
 x = torch.zeros((L, n), dtype=torch.float64, device="cuda"); y = torch.empty_like(x)
 ws = torch.empty(dev.fast_workspace_bytes(L, n), dtype=torch.uint8, device="cuda")
 bl = torch.empty(L, dtype=torch.int64, device="cuda")
+CH = getattr(api, "FAST_CHAINED", 0) if __CHAINED__ else 0
 def run(k, i0):
     global x, y
     for i in range(k):
-        dev.fast_f64(x, y, dr, tau, tv=tv, blocks=bl, workspace=ws, flags=api.FAST_STATS_VALID if i0 + i else 0)
+        dev.fast_f64(x, y, dr, tau, tv=tv, blocks=bl, workspace=ws,
+                     flags=CH | (api.FAST_STATS_VALID if i0 + i else 0))
         x, y = y, x
 run(1000, 0)
 res = []
@@ -31,9 +33,12 @@ for r in range(5):
     run(50, 1)
     e1.record(); torch.cuda.synchronize()
     res.append(e0.elapsed_time(e1) / 50)
-print(json.dumps({"lib": __LIB__, "ms": sorted(res)}))
+print(json.dumps({"lib": __LIB__, "chained": __CHAINED__, "ms": sorted(res)}))
 '''
 for lib in sys.argv[1:]:
+    chained = lib.endswith(":chained")
+    lib = lib.split(":")[0]
     code = CHILD.replace("__ROOT__", repr(ROOT)).replace("__LIB__", repr(os.path.abspath(lib)))
+    code = code.replace("__CHAINED__", repr(chained))
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
     print(r.stdout.strip() or r.stderr[-2000:], flush=True)

@@ -262,3 +262,32 @@ def test_fast_eta_blocks_match_reference_naive(dev, orc, ref, eta):
     assert list(db.cpu().numpy()) == want
     assert list(db2.cpu().numpy()) == want
     assert np.array_equal(out.cpu().numpy(), oracle_step(orc, u, 0.5, tau))
+
+
+def test_fast_chained_steps_equal_plain_steps(dev):
+    """LOB_FAST_CHAINED back-to-back steps (per-line dependencies across grids) ==
+    ordinary steps: states and block counts, 12 steps of 24 C2 lines."""
+    import torch
+    n, tau, lines, steps = 65536, 0.02, 24, 12
+    drifts = api.gen_c2_drifts(256)[np.linspace(0, 255, lines).astype(int)]
+    dd, dtv = to_dev(drifts), to_dev(api.tau_v(api.gen_potential(2, n), tau))
+    res = []
+    plain = [0] * steps
+    chained = [api.FAST_CHAINED] * steps
+    mixed = [api.FAST_CHAINED, api.FAST_CHAINED, 0, api.FAST_CHAINED, api.FAST_CHAINED, api.FAST_CHAINED, 0, 0,
+             api.FAST_CHAINED, api.FAST_CHAINED, api.FAST_CHAINED, api.FAST_CHAINED]
+    for pattern in (plain, chained, mixed):
+        a = torch.zeros((lines, n), dtype=torch.float64, device="cuda")
+        b = torch.empty_like(a)
+        ws = torch.empty(dev.fast_workspace_bytes(lines, n), dtype=torch.uint8, device="cuda")
+        bl = torch.empty((steps, lines), dtype=torch.int64, device="cuda")
+        for i in range(steps):
+            dev.fast_f64(a, b, dd, tau, tv=dtv, blocks=bl[i], workspace=ws,
+                         flags=pattern[i] | (api.FAST_STATS_VALID if i else 0))
+            a, b = b, a
+        torch.cuda.synchronize()
+        assert dev.fast_diagnostics(ws, lines, n) == 0
+        res.append((a.clone(), bl.clone()))
+    for k in (1, 2):
+        assert torch.equal(res[0][0], res[k][0])
+        assert torch.equal(res[0][1], res[k][1])
