@@ -37,7 +37,8 @@ with open(os.path.join(ROOT, "profiles", f"{tag}_k2_fast_c2_ncu_summary.txt"), "
     f.write("# K2 fast_kernel, C2 (256 x 65536) after 1000 steps; one launch, ncu --set full --clock-control none\n")
     f.write(run("scripts/ncu_summary.py", k2))
     f.write("\n# instructions / stall samples by kernel phase (outermost source line; scripts/ncu_phases.py)\n")
-    f.write(run("scripts/ncu_phases.py", k2, os.path.join(tmp, "fast.sm_100a.cubin"), "fast_kernel", "fast.cu", ranges))
+    f.write(run("scripts/ncu_phases.py", k2, os.path.join(tmp, "fast.sm_100a.cubin"), "fast_kernelILb1ELb0ELb0E", "fast.cu",
+                ranges))
 with open(os.path.join(ROOT, "profiles", f"{tag}_k1_screen_c3_ncu_summary.txt"), "w") as f:
     f.write("# K1 screened (fp32 screen + fp64 span pass), C3 4096 x 4096 fp64, one launch\n")
     f.write(run("scripts/ncu_summary.py", k1s))
