@@ -184,6 +184,54 @@ int lob_block_counts(lob_ctx* ctx, const double* u, int64_t lines, int64_t n, do
 int lob_bench_fp64(lob_ctx* ctx, double* minplus_cand_per_s, double* dadd_ops_per_s,
                    double* sm_clock_ghz);
 
+/* ---- Weak-KAM consumers of the step (proj/src/weakkam.cpp) ----
+ * Dense min-plus matrices are row-major doubles, cost[y*n + x] = cost of going
+ * from source y to target x (MinPlusMatrix, proj/include/laxol/weakkam.hpp:22-29).
+ * Every output is one minimum over single IEEE sums taken in increasing
+ * contraction index with a strict "<", exactly the reference's loops. */
+
+/* C[m x n] = A[m x k] (x) B[k x n]:  C[i][x] = min_z A[i][z] + B[z][x]
+ * (device buffers, leading dimensions in elements).  Replaces
+ * minplus_product (proj/src/weakkam.cpp:130-146; m = n = k) and minplus_apply
+ * (:148-158; A = the line(s) u, B = the period matrix). */
+int lob_minplus_gemm_f64(lob_ctx* ctx, const double* A, int64_t lda, const double* B, int64_t ldb,
+                         double* C, int64_t ldc, int64_t m, int64_t n, int64_t k, void* stream);
+
+/* Host helper: the quotient kinetic cost kinc[r] = min over displacements
+ * d = r (mod n) in [first, first + 2n] of window[d - first]
+ * (proj/src/weakkam.cpp:106-118), r = 0..n-1. */
+int lob_period_kinetic_host(const double* window, int64_t first, int64_t n, double* kinc);
+
+/* build_period_matrix (proj/src/weakkam.cpp:88-128): C = step_0 (x) ... (x)
+ * step_{ell-1}, step_i[y][x] = kinc[(x - y) mod n] - tvs[i*n + x] (tvs = the
+ * host-rounded tau*V at step i's sampling time, NULL = V == 0).  Device
+ * buffers; scratch holds 2*n*n doubles. */
+int lob_period_matrix_f64(lob_ctx* ctx, const double* kinc, const double* tvs, int64_t n,
+                          int64_t ell, double* C, double* scratch, void* stream);
+
+/* eigenvalue_karp (proj/src/weakkam.cpp:160-189) of the device n x n matrix M;
+ * synchronous, *lambda on the host.  LOB_INVALID_INPUT for n < 1 or a
+ * non-finite entry. */
+int lob_eigenvalue_karp_f64(lob_ctx* ctx, const double* M, int64_t n, double* lambda);
+
+/* estimate_hbar_drift (proj/src/weakkam.cpp:43-86) for one periodic line of n
+ * samples (host buffers): whole periods of ell = 1/tau fully discrete steps
+ * on the device (engine K1 or K2, exact), the per-period increment
+ * statistics on the host in the reference's order.  tvs: tv_count host tables
+ * of n rounded tau*V values — 0 (V == 0), 1 (autonomous) or ell (table i for
+ * step i of every period: the in-period time labels of apply_one_period,
+ * :33-39).  Outputs (nullable): h_bar, residual, n_steps, converged, and
+ * u_final (n doubles, the last state). */
+int lob_hbar_drift_host_f64(lob_ctx* ctx, const double* u0, int64_t n, double drift, double tau,
+                            const double* tvs, int64_t tv_count, int engine, int max_periods,
+                            double tol, double* h_bar, double* residual, int64_t* n_steps,
+                            int* converged, double* u_final);
+
+/* fixed_point_residual (proj/src/weakkam.cpp:191-201): sup_j |T^1 u - u - h_bar|. */
+int lob_fixed_point_residual_host_f64(lob_ctx* ctx, const double* u, int64_t n, double h_bar,
+                                      double drift, double tau, const double* tvs,
+                                      int64_t tv_count, int engine, double* residual);
+
 /* Number of kernel launches issued by this context since creation. */
 int64_t lob_launch_count(const lob_ctx* ctx);
 

@@ -26,6 +26,7 @@
 #include "laxol/parallel.hpp"
 #include "laxol/scheme.hpp"
 #include "laxol/splitting.hpp"
+#include "laxol/weakkam.hpp"
 
 using namespace laxol;
 
@@ -71,6 +72,32 @@ Potential table_potential(const double* vtab, int n) {
             return tab[static_cast<std::size_t>(j)];
         },
         1e300, false);
+}
+
+// Time-dependent tabulated potential for the weak-KAM entry points:
+// V(t, x_j) = tabs[(llround(t/tau) mod nt)][j] (nt tables of n values; nt == 0: V == 0,
+// nt == 1: autonomous).  With Arrival sampling step i of a period samples table (i+1) mod nt.
+Potential time_table_potential(const double* tabs, int64_t nt, int n, double tau) {
+    if (!tabs || nt == 0) return potential_zero();
+    if (nt == 1) return table_potential(tabs, n);
+    std::vector<double> tab(tabs, tabs + nt * n);
+    const double step = 1.0 / static_cast<double>(n);
+    return potential_custom(
+        [tab, n, nt, step, tau](double t, double x) {
+            long long j = std::llround(x / step);
+            j = ((j % n) + n) % n;
+            long long k = std::llround(t / tau);
+            k = ((k % nt) + nt) % nt;
+            return tab[static_cast<std::size_t>(k * n + j)];
+        },
+        1e300, true);
+}
+
+MinPlusMatrix matrix_of(const double* a, int64_t n) {
+    MinPlusMatrix m;
+    m.n = static_cast<std::size_t>(n);
+    m.cost.assign(a, a + n * n);
+    return m;
 }
 
 ConvEngine engine_of(int e) { return e == 1 ? ConvEngine::Naive : ConvEngine::Fast; }
@@ -236,6 +263,61 @@ int ref_conv(int which, const double* a, int64_t na, const double* b, int64_t nb
             r = std::move(fr.fn);
         }
         std::memcpy(out, r.values.data(), r.values.size() * sizeof(double));
+    });
+}
+
+// ---- weak-KAM consumers (proj/src/weakkam.cpp) ----
+int ref_minplus_product(const double* a, const double* b, int64_t n, double* c) {
+    return guarded([&] {
+        const MinPlusMatrix r = minplus_product(matrix_of(a, n), matrix_of(b, n));
+        std::memcpy(c, r.cost.data(), n * n * sizeof(double));
+    });
+}
+
+int ref_minplus_apply(const double* cm, int64_t n, const double* u, double* out) {
+    return guarded([&] {
+        const GridFn g = make_periodic(std::vector<double>(u, u + n), 1.0 / static_cast<double>(n));
+        const GridFn r = minplus_apply(matrix_of(cm, n), g);
+        std::memcpy(out, r.values.data(), n * sizeof(double));
+    });
+}
+
+int ref_eigenvalue_karp(const double* cm, int64_t n, double* lambda) {
+    return guarded([&] { *lambda = eigenvalue_karp(matrix_of(cm, n)); });
+}
+
+int ref_build_period_matrix(int n_space, double tau, double drift, const double* vtabs, int64_t nt,
+                            double* c) {
+    return guarded([&] {
+        const SchemeParams p = params_of(n_space, tau, 0.0);
+        const HamiltonianSpec spec{mechanical(drift), time_table_potential(vtabs, nt, n_space, tau), true, true};
+        const MinPlusMatrix r = build_period_matrix(spec, p);
+        std::memcpy(c, r.cost.data(), r.cost.size() * sizeof(double));
+    });
+}
+
+int ref_estimate_hbar_drift(const double* u0, int n_space, double tau, double drift, const double* vtabs,
+                            int64_t nt, int max_periods, double tol, double* h_bar, double* residual,
+                            int64_t* n_steps, int* converged) {
+    return guarded([&] {
+        const SchemeParams p = params_of(n_space, tau, 0.0);
+        const HamiltonianSpec spec{mechanical(drift), time_table_potential(vtabs, nt, n_space, tau), true, true};
+        const GridFn g = make_periodic(std::vector<double>(u0, u0 + n_space), p.epsilon());
+        const EffectiveHEstimate e = estimate_hbar_drift(g, spec, p, max_periods, tol);
+        *h_bar = e.h_bar;
+        *residual = e.residual;
+        *n_steps = e.n_steps;
+        *converged = e.converged ? 1 : 0;
+    });
+}
+
+int ref_fixed_point_residual(const double* u, int n_space, double tau, double drift, const double* vtabs,
+                             int64_t nt, double h_bar, double* residual) {
+    return guarded([&] {
+        const SchemeParams p = params_of(n_space, tau, 0.0);
+        const HamiltonianSpec spec{mechanical(drift), time_table_potential(vtabs, nt, n_space, tau), true, true};
+        const GridFn g = make_periodic(std::vector<double>(u, u + n_space), p.epsilon());
+        *residual = fixed_point_residual(g, h_bar, spec, p);
     });
 }
 

@@ -52,6 +52,16 @@ SIGNATURES = {
     "lob_launch_count": (c_int64, [_P]),
     "lob_ctx_set_direct_mode": (c_int, [_P, c_int]),
     "lob_direct_stats": (c_int, [_P, POINTER(c_uint64), POINTER(c_uint64), c_int]),
+    # weak-KAM consumers (proj/src/weakkam.cpp)
+    "lob_minplus_gemm_f64": (c_int, [_P, _P, c_int64, _P, c_int64, _P, c_int64, c_int64, c_int64, c_int64, _P]),
+    "lob_period_kinetic_host": (c_int, [_P, c_int64, c_int64, _P]),
+    "lob_period_matrix_f64": (c_int, [_P, _P, _P, c_int64, c_int64, _P, _P, _P]),
+    "lob_eigenvalue_karp_f64": (c_int, [_P, _P, c_int64, POINTER(c_double)]),
+    "lob_hbar_drift_host_f64": (c_int, [_P, _P, c_int64, c_double, c_double, _P, c_int64, c_int, c_int, c_double,
+                                        POINTER(c_double), POINTER(c_double), POINTER(c_int64), POINTER(c_int),
+                                        _P]),
+    "lob_fixed_point_residual_host_f64": (c_int, [_P, _P, c_int64, c_double, c_double, c_double, _P, c_int64,
+                                                  c_int, POINTER(c_double)]),
     # synthetic workloads (include/laxol_b200_configs.h)
     "lob_gen_sin": (None, [c_int64, _P]),
     "lob_gen_cos": (None, [c_int64, _P]),

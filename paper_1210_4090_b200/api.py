@@ -236,6 +236,74 @@ class Device:
                                        _stream_ptr(stream))
         self._check(st, "lob_block_counts")
 
+    # ---- weak-KAM consumers (proj/src/weakkam.cpp; include/laxol_b200.h) ----
+    def minplus_gemm(self, a, b, out, stream=None):
+        """out = a (x) b in the min-plus semiring (minplus_product / minplus_apply)."""
+        m, k = a.shape
+        k2, n = b.shape
+        if k2 != k or tuple(out.shape) != (m, n):
+            raise InvalidInput("minplus_gemm: shape mismatch")
+        st = self.lib.lob_minplus_gemm_f64(self.ctx, _ptr(a), a.stride(0), _ptr(b), b.stride(0), _ptr(out),
+                                           out.stride(0), m, n, k, _stream_ptr(stream))
+        self._check(st, "lob_minplus_gemm_f64")
+
+    @staticmethod
+    def period_kinetic(kernel: "Kernel") -> np.ndarray:
+        """kin[r] = min over displacements = r (mod n) in the window (proj/src/weakkam.cpp:106-118)."""
+        w = np.ascontiguousarray(kernel.window, np.float64)
+        n = (w.size - 1) // 2
+        kinc = np.empty(n)
+        st = _capi.load().lob_period_kinetic_host(w.ctypes.data, int(kernel.first), n, kinc.ctypes.data)
+        _capi.check(st, None, "lob_period_kinetic_host")
+        return kinc
+
+    def period_matrix(self, kinc, tvs, ell, out, scratch, stream=None):
+        """build_period_matrix (proj/src/weakkam.cpp:88-128) on device buffers."""
+        n = kinc.shape[0]
+        st = self.lib.lob_period_matrix_f64(self.ctx, _ptr(kinc), _ptr(tvs), n, int(ell), _ptr(out),
+                                            _ptr(scratch), _stream_ptr(stream))
+        self._check(st, "lob_period_matrix_f64")
+
+    def eigenvalue_karp(self, m) -> float:
+        lam = ctypes.c_double()
+        st = self.lib.lob_eigenvalue_karp_f64(self.ctx, _ptr(m), m.shape[0], ctypes.byref(lam))
+        self._check(st, "lob_eigenvalue_karp_f64")
+        return lam.value
+
+    @staticmethod
+    def _tvs(tvs):
+        if tvs is None:
+            return None, 0
+        t = np.ascontiguousarray(np.atleast_2d(tvs), np.float64)
+        return t, t.shape[0]
+
+    def hbar_drift_host(self, u0, drift, tau, tvs=None, engine=ENGINE_FAST, max_periods=100, tol=1e-10):
+        """estimate_hbar_drift (proj/src/weakkam.cpp:43-86) of one periodic line (host arrays);
+        tvs: None, one table, or one rounded tau*V table per in-period step."""
+        u0 = np.ascontiguousarray(u0, np.float64)
+        t, nt = self._tvs(tvs)
+        hb, res, ns, cv = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64(), ctypes.c_int()
+        uf = np.empty_like(u0)
+        st = self.lib.lob_hbar_drift_host_f64(self.ctx, u0.ctypes.data, u0.size, float(drift), float(tau),
+                                              None if t is None else t.ctypes.data, nt, int(engine),
+                                              int(max_periods), float(tol), ctypes.byref(hb),
+                                              ctypes.byref(res), ctypes.byref(ns), ctypes.byref(cv),
+                                              uf.ctypes.data)
+        self._check(st, "lob_hbar_drift_host_f64")
+        return {"h_bar": hb.value, "residual": res.value, "n_steps": ns.value, "converged": bool(cv.value),
+                "u": uf}
+
+    def fixed_point_residual_host(self, u, drift, tau, h_bar, tvs=None, engine=ENGINE_FAST) -> float:
+        u = np.ascontiguousarray(u, np.float64)
+        t, nt = self._tvs(tvs)
+        r = ctypes.c_double()
+        st = self.lib.lob_fixed_point_residual_host_f64(self.ctx, u.ctypes.data, u.size, float(h_bar),
+                                                        float(drift), float(tau),
+                                                        None if t is None else t.ctypes.data, nt, int(engine),
+                                                        ctypes.byref(r))
+        self._check(st, "lob_fixed_point_residual_host_f64")
+        return r.value
+
     def bench_fp64(self):
         a, b, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
         st = self.lib.lob_bench_fp64(self.ctx, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c))

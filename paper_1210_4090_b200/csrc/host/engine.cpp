@@ -370,4 +370,159 @@ TensorFn Engine::split_step_nd(const TensorFn& u, double t, const SplitSpec2D& s
     return out;
 }
 
+// ---- weak-KAM consumers (proj/src/weakkam.cpp) ------------------------------
+
+namespace {
+
+// proj/src/weakkam.cpp:17-31
+int64_t steps_per_period(const SchemeParams& params, const char* who) {
+    const int64_t ell = std::llround(1.0 / params.tau);
+    if (ell < 1 || std::abs(static_cast<double>(ell) * params.tau - 1.0) > 1e-9)
+        throw InvalidInput(std::string(who) + ": tau must be a unit fraction of the time period");
+    return ell;
+}
+
+void require_time_periodic(const Potential& V, const char* who) {
+    if (V && V.time_dependent && !V.time_periodic)
+        throw InvalidInput(std::string(who) + ": spec must be time-periodic with period 1");
+}
+
+// tau*V tables of one period's steps (in-period time labels i*tau,
+// proj/src/weakkam.cpp:33-39): none, one (autonomous) or ell
+std::vector<double> period_tables(const GridFn& u, const Potential& V, const SchemeParams& params, int64_t ell,
+                                  int64_t* count) {
+    const std::size_t n = u.n();
+    if (!V) {
+        *count = 0;
+        return {};
+    }
+    const int64_t nt = V.time_dependent ? ell : 1;
+    std::vector<double> tabs;
+    tabs.reserve(static_cast<size_t>(nt) * n);
+    for (int64_t i = 0; i < nt; ++i) {
+        const std::vector<double> tv =
+            tabulate_tv(u, V, potential_time(static_cast<double>(i) * params.tau, params), params.tau, n);
+        tabs.insert(tabs.end(), tv.begin(), tv.end());
+    }
+    *count = nt;
+    return tabs;
+}
+
+void check_matrix(const MinPlusMatrix& m, const char* who) {
+    if (m.cost.size() != m.n * m.n) throw InvalidInput(std::string(who) + ": cost is not n x n");
+}
+
+}  // namespace
+
+EffectiveHEstimate Engine::estimate_hbar_drift(const GridFn& u0, double drift, const Potential& V,
+                                               const SchemeParams& params, int max_periods, double tol,
+                                               ConvEngine engine) {
+    require_time_periodic(V, "estimate_hbar_drift");
+    if (!u0.periodic) throw InvalidInput("estimate_hbar_drift: spec must be space-periodic");
+    const int64_t ell = steps_per_period(params, "estimate_hbar_drift");
+    if (max_periods < 1) throw InvalidInput("estimate_hbar_drift: max_periods must be >= 1");
+    check_u_grid(u0, params, "estimate_hbar_drift");
+    int64_t nt = 0;
+    const std::vector<double> tabs = period_tables(u0, V, params, ell, &nt);
+    EffectiveHEstimate est;
+    int conv = 0;
+    check_status(lob_hbar_drift_host_f64(ctx_, u0.values.data(), static_cast<int64_t>(u0.n()), drift, params.tau,
+                                         nt ? tabs.data() : nullptr, nt, engine_code(engine), max_periods, tol,
+                                         &est.h_bar, &est.residual, &est.n_steps, &conv, nullptr),
+                 ctx_, "estimate_hbar_drift");
+    est.converged = conv != 0;
+    return est;
+}
+
+double Engine::fixed_point_residual(const GridFn& u, double h_bar, double drift, const Potential& V,
+                                    const SchemeParams& params, ConvEngine engine) {
+    require_time_periodic(V, "fixed_point_residual");
+    if (!u.periodic) throw InvalidInput("fixed_point_residual: spec must be space-periodic");
+    steps_per_period(params, "fixed_point_residual");
+    check_u_grid(u, params, "fixed_point_residual");
+    int64_t nt = 0;
+    const std::vector<double> tabs = period_tables(u, V, params, steps_per_period(params, "fixed_point_residual"), &nt);
+    double r = 0.0;
+    check_status(lob_fixed_point_residual_host_f64(ctx_, u.values.data(), static_cast<int64_t>(u.n()), h_bar, drift,
+                                                   params.tau, nt ? tabs.data() : nullptr, nt, engine_code(engine),
+                                                   &r),
+                 ctx_, "fixed_point_residual");
+    return r;
+}
+
+MinPlusMatrix Engine::build_period_matrix(double drift, const Potential& V, const SchemeParams& params) {
+    require_time_periodic(V, "build_period_matrix");
+    const int64_t ell = steps_per_period(params, "build_period_matrix");
+    const int64_t n = params.n_space;
+    if (n > 512) throw InvalidInput("build_period_matrix: n_space exceeds the dense guard (512)");
+    const KernelWindow k = build_kernel_mech(n, params.tau, drift);
+    std::vector<double> kinc(static_cast<size_t>(n));
+    lob_period_kinetic_host(k.window.data(), k.first, n, kinc.data());
+    // tau*V(t_i', x*eps) per step (proj/src/weakkam.cpp:103-104,120-121)
+    const double eps = params.epsilon();
+    std::vector<double> tvs;
+    if (V) {
+        tvs.resize(static_cast<size_t>(ell * n));
+        for (int64_t i = 0; i < ell; ++i) {
+            const double tt = potential_time(static_cast<double>(i) * params.tau, params);
+            for (int64_t x = 0; x < n; ++x) {
+                const double vx = V(tt, static_cast<double>(x) * eps);
+                tvs[static_cast<size_t>(i * n + x)] = params.tau * vx;
+            }
+        }
+    }
+    DevBuf<double> dk(n), dtv(tvs.size()), dc(n * n), dscr(2 * n * n);
+    dk.upload(kinc.data(), n);
+    if (!tvs.empty()) dtv.upload(tvs.data(), tvs.size());
+    check_status(lob_period_matrix_f64(ctx_, dk.p, tvs.empty() ? nullptr : dtv.p, n, ell, dc.p, dscr.p, nullptr),
+                 ctx_, "build_period_matrix");
+    MinPlusMatrix C;
+    C.n = static_cast<size_t>(n);
+    C.cost.resize(static_cast<size_t>(n * n));
+    dc.download(C.cost.data(), C.cost.size());
+    return C;
+}
+
+MinPlusMatrix Engine::minplus_product(const MinPlusMatrix& A, const MinPlusMatrix& B) {
+    check_matrix(A, "minplus_product");
+    check_matrix(B, "minplus_product");
+    if (A.n != B.n) throw InvalidInput("minplus_product: size mismatch");
+    const int64_t n = static_cast<int64_t>(A.n);
+    MinPlusMatrix C;
+    C.n = A.n;
+    C.cost.resize(A.cost.size());
+    if (n == 0) return C;
+    DevBuf<double> da(n * n), db(n * n), dc(n * n);
+    da.upload(A.cost.data(), n * n);
+    db.upload(B.cost.data(), n * n);
+    check_status(lob_minplus_gemm_f64(ctx_, da.p, n, db.p, n, dc.p, n, n, n, n, nullptr), ctx_, "minplus_product");
+    dc.download(C.cost.data(), n * n);
+    return C;
+}
+
+GridFn Engine::minplus_apply(const MinPlusMatrix& C, const GridFn& u) {
+    check_matrix(C, "minplus_apply");
+    if (!u.periodic || u.n() != C.n)
+        throw InvalidInput("minplus_apply: u must be periodic over the quotient grid");
+    const int64_t n = static_cast<int64_t>(C.n);
+    DevBuf<double> du(n), dc(n * n), dout(n);
+    du.upload(u.values.data(), n);
+    dc.upload(C.cost.data(), n * n);
+    check_status(lob_minplus_gemm_f64(ctx_, du.p, n, dc.p, n, dout.p, n, 1, n, n, nullptr), ctx_, "minplus_apply");
+    std::vector<double> out(static_cast<size_t>(n));
+    dout.download(out.data(), n);
+    return make_periodic(std::move(out), u.step, u.origin);
+}
+
+double Engine::eigenvalue_karp(const MinPlusMatrix& C) {
+    check_matrix(C, "eigenvalue_karp");
+    if (C.n == 0) throw InvalidInput("eigenvalue_karp: empty matrix");
+    const int64_t n = static_cast<int64_t>(C.n);
+    DevBuf<double> dc(n * n);
+    dc.upload(C.cost.data(), n * n);
+    double lam = 0.0;
+    check_status(lob_eigenvalue_karp_f64(ctx_, dc.p, n, &lam), ctx_, "eigenvalue_karp");
+    return lam;
+}
+
 }  // namespace laxol_b200

@@ -77,6 +77,7 @@ void validate(const SchemeParams& p);
 struct Potential {
     std::function<double(double, double)> fn;
     bool time_dependent = false;
+    bool time_periodic = true;  // HamiltonianSpec::time_periodic (period 1), for the weak-KAM consumers
     double operator()(double t, double x) const { return fn ? fn(t, x) : 0.0; }
     explicit operator bool() const { return static_cast<bool>(fn); }
 };
@@ -124,6 +125,20 @@ struct SplitSpec2D {
     SeparablePotential2D potential;
 };
 
+// proj/include/laxol/weakkam.hpp:12-29
+struct EffectiveHEstimate {
+    double h_bar = 0.0;
+    int64_t n_steps = 0;
+    double residual = 0.0;
+    bool converged = false;
+};
+struct MinPlusMatrix {
+    std::size_t n = 0;
+    std::vector<double> cost;  // cost[y*n + x]: source y -> target x
+    double at(std::size_t y, std::size_t x) const { return cost[y * n + x]; }
+    double& at(std::size_t y, std::size_t x) { return cost[y * n + x]; }
+};
+
 // The device engine: owns a lob_ctx, device buffers and workspaces.
 class Engine {
 public:
@@ -148,6 +163,20 @@ public:
     TensorFn split_step_nd(const TensorFn& u, double t, const SplitSpec2D& spec,
                            const SchemeParams& params,
                            ConvEngine engine = ConvEngine::GpuDirect);
+
+    // Weak-KAM consumers (proj/src/weakkam.cpp), the step and the products on the device.
+    // :43-86 (mechanical(drift) kinetics, periodic u0, tau = 1/l)
+    EffectiveHEstimate estimate_hbar_drift(const GridFn& u0, double drift, const Potential& V,
+                                           const SchemeParams& params, int max_periods, double tol,
+                                           ConvEngine engine = ConvEngine::GpuFast);
+    // :88-128
+    MinPlusMatrix build_period_matrix(double drift, const Potential& V, const SchemeParams& params);
+    // :130-146, :148-158, :160-189, :191-201
+    MinPlusMatrix minplus_product(const MinPlusMatrix& A, const MinPlusMatrix& B);
+    GridFn minplus_apply(const MinPlusMatrix& C, const GridFn& u);
+    double eigenvalue_karp(const MinPlusMatrix& C);
+    double fixed_point_residual(const GridFn& u, double h_bar, double drift, const Potential& V,
+                                const SchemeParams& params, ConvEngine engine = ConvEngine::GpuFast);
 
     lob_ctx* ctx() const { return ctx_; }
 

@@ -124,6 +124,14 @@ int fast_diag_count(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n, uin
 int launch_block_counts(lob_ctx* ctx, const double* u, int64_t lines, int64_t n, double eta,
                         int64_t* blocks, cudaStream_t s);
 
+// weak-KAM consumers (weakkam.cu)
+int launch_tropical_gemm(lob_ctx* ctx, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                         int64_t ldc, int64_t m, int64_t n, int64_t k, cudaStream_t s);
+int launch_karp(lob_ctx* ctx, const double* M, int64_t n, double* D, double* lambda_dev, int* flag,
+                cudaStream_t s);
+int launch_period_matrix(lob_ctx* ctx, const double* kinc, const double* tvs, int64_t n, int64_t ell, double* C,
+                         double* scratch, cudaStream_t s);
+
 int launch_transpose(lob_ctx* ctx, const double* src, double* dst, int64_t n, cudaStream_t s);
 int launch_potential2d(lob_ctx* ctx, double* out, const double* a1, const double* a2, double b,
                        double tau, int64_t n, cudaStream_t s);

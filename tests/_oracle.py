@@ -122,6 +122,15 @@ class Reference:
                                           c_double, c_int, _P]),
             "ref_decompose": (c_int64, [_P, c_int64, c_double, _P, _P, _P, c_int64]),
             "ref_conv": (c_int, [c_int, _P, c_int64, _P, c_int64, c_double, _P, _P]),
+            "ref_minplus_product": (c_int, [_P, _P, c_int64, _P]),
+            "ref_minplus_apply": (c_int, [_P, c_int64, _P, _P]),
+            "ref_eigenvalue_karp": (c_int, [_P, c_int64, POINTER(c_double)]),
+            "ref_build_period_matrix": (c_int, [c_int, c_double, c_double, _P, c_int64, _P]),
+            "ref_estimate_hbar_drift": (c_int, [_P, c_int, c_double, c_double, _P, c_int64, c_int, c_double,
+                                                POINTER(c_double), POINTER(c_double), POINTER(c_int64),
+                                                POINTER(c_int)]),
+            "ref_fixed_point_residual": (c_int, [_P, c_int, c_double, c_double, _P, c_int64, c_double,
+                                                 POINTER(c_double)]),
         }
         for k, (r, a) in sig.items():
             f = getattr(lib, k)
@@ -198,6 +207,66 @@ class Reference:
         st = self.lib.ref_conv(which, a.ctypes.data, a.size, b.ctypes.data, b.size, eta, out.ctypes.data,
                                ctypes.byref(blocks))
         return out, blocks.value, st
+
+    # ---- weak-KAM consumers (proj/src/weakkam.cpp) ----
+    def minplus_product(self, a, b):
+        a = np.ascontiguousarray(a, np.float64)
+        b = np.ascontiguousarray(b, np.float64)
+        c = np.empty_like(a)
+        st = self.lib.ref_minplus_product(a.ctypes.data, b.ctypes.data, a.shape[0], c.ctypes.data)
+        if st:
+            raise RuntimeError(self.err())
+        return c
+
+    def minplus_apply(self, cm, u):
+        cm = np.ascontiguousarray(cm, np.float64)
+        u = np.ascontiguousarray(u, np.float64)
+        out = np.empty_like(u)
+        st = self.lib.ref_minplus_apply(cm.ctypes.data, cm.shape[0], u.ctypes.data, out.ctypes.data)
+        if st:
+            raise RuntimeError(self.err())
+        return out
+
+    def karp(self, cm):
+        cm = np.ascontiguousarray(cm, np.float64)
+        lam = c_double()
+        st = self.lib.ref_eigenvalue_karp(cm.ctypes.data, cm.shape[0], ctypes.byref(lam))
+        return lam.value, st
+
+    @staticmethod
+    def _tabs(vtabs):
+        if vtabs is None:
+            return None, 0
+        v = np.ascontiguousarray(np.atleast_2d(vtabs), np.float64)
+        return v, v.shape[0]
+
+    def period_matrix(self, n, tau, drift, vtabs=None):
+        v, nt = self._tabs(vtabs)
+        c = np.empty((n, n))
+        st = self.lib.ref_build_period_matrix(n, tau, drift, None if v is None else v.ctypes.data, nt,
+                                              c.ctypes.data)
+        if st:
+            raise RuntimeError(self.err())
+        return c
+
+    def hbar_drift(self, u0, tau, drift, vtabs=None, max_periods=100, tol=1e-10):
+        u0 = np.ascontiguousarray(u0, np.float64)
+        v, nt = self._tabs(vtabs)
+        hb, res, ns, cv = c_double(), c_double(), c_int64(), c_int()
+        st = self.lib.ref_estimate_hbar_drift(u0.ctypes.data, u0.size, tau, drift,
+                                              None if v is None else v.ctypes.data, nt, max_periods, tol,
+                                              ctypes.byref(hb), ctypes.byref(res), ctypes.byref(ns),
+                                              ctypes.byref(cv))
+        return {"h_bar": hb.value, "residual": res.value, "n_steps": ns.value, "converged": bool(cv.value),
+                "status": st}
+
+    def fixed_point_residual(self, u, tau, drift, h_bar, vtabs=None):
+        u = np.ascontiguousarray(u, np.float64)
+        v, nt = self._tabs(vtabs)
+        r = c_double()
+        st = self.lib.ref_fixed_point_residual(u.ctypes.data, u.size, tau, drift,
+                                               None if v is None else v.ctypes.data, nt, h_bar, ctypes.byref(r))
+        return r.value, st
 
 
 _ORC = None

@@ -3,6 +3,7 @@
 // (proj/tests/unit_scheme.cpp, proj/tests/unit_splitting.cpp), with
 // independent brute-force oracles.  Needs a CUDA device; prints one
 // PASS/FAIL line per check and exits non-zero on any failure.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <limits>
@@ -168,6 +169,72 @@ int main() {
                 }
             CHECK(ok, "split_step_nd == 2-D brute force, engine %d", static_cast<int>(e));
         }
+    }
+    // 7. weak-KAM consumers (proj/tests/unit_weakkam.cpp)
+    {
+        auto cosv = [](double, double x) { return 1.0 - std::cos(2.0 * 3.141592653589793 * x); };
+        // applying the period matrix equals one period of steps (unit_weakkam.cpp:114-130)
+        const SchemeParams p = params_of(32, 0.2);
+        Potential V{cosv, false};
+        const MinPlusMatrix C = eng.build_period_matrix(1.0, V, p);
+        const KernelWindow k = build_kernel_mech(32, 0.2, 1.0);
+        for (int rep = 0; rep < 4; ++rep) {
+            const GridFn u0 = random_periodic(rng, 32, 1.0, p.epsilon());
+            GridFn st = u0;
+            for (int i = 0; i < 5; ++i) st = eng.step_fully_discrete(st, 0.2 * i, V, p, k);
+            const GridFn ap = eng.minplus_apply(C, u0);
+            double d = 0.0;
+            for (std::size_t j = 0; j < ap.values.size(); ++j) d = std::max(d, std::abs(ap.values[j] - st.values[j]));
+            CHECK(d <= 1e-10, "minplus_apply(period matrix) == one period of steps (%.3e)", d);
+        }
+        // product associativity up to roundoff (unit_weakkam.cpp:132-147)
+        std::uniform_real_distribution<double> ud(-1.0, 1.0);
+        auto rnd = [&](std::size_t n) {
+            MinPlusMatrix M;
+            M.n = n;
+            M.cost.resize(n * n);
+            for (double& v : M.cost) v = ud(rng);
+            return M;
+        };
+        const MinPlusMatrix A = rnd(12), B = rnd(12), D = rnd(12);
+        const MinPlusMatrix l = eng.minplus_product(eng.minplus_product(A, B), D);
+        const MinPlusMatrix r = eng.minplus_product(A, eng.minplus_product(B, D));
+        bool ok = true;
+        for (std::size_t i = 0; i < l.cost.size(); ++i) ok = ok && std::abs(l.cost[i] - r.cost[i]) <= 1e-12 * std::abs(r.cost[i]) + 1e-15;
+        CHECK(ok, "minplus_product associative");
+        // Karp closed forms (unit_weakkam.cpp:149-158)
+        MinPlusMatrix Z;
+        Z.n = 5;
+        Z.cost.assign(25, 0.0);
+        CHECK(eng.eigenvalue_karp(Z) == 0.0, "karp(zeros) == 0");
+        MinPlusMatrix T2;
+        T2.n = 2;
+        T2.cost = {0.0, 5.0, 1.0, 0.0};
+        CHECK(eng.eigenvalue_karp(T2) == 0.0, "karp(two free self-loops) == 0");
+        // drift and eigenvalue estimates agree (unit_weakkam.cpp:172-192)
+        const SchemeParams q = params_of(48, 0.125);
+        std::vector<double> u0v(48);
+        for (int i = 0; i < 48; ++i) u0v[i] = std::cos(2.0 * (2.0 * 3.141592653589793 * i / 48.0 - 3.141592653589793));
+        const GridFn u0 = make_periodic(u0v, q.epsilon());
+        for (ConvEngine e : {ConvEngine::GpuFast, ConvEngine::GpuDirect}) {
+            const EffectiveHEstimate est = eng.estimate_hbar_drift(u0, 1.0, V, q, 600, 1e-8, e);
+            const double karp = eng.eigenvalue_karp(eng.build_period_matrix(1.0, V, q));
+            CHECK(est.converged && std::abs(est.h_bar - karp) < 1e-7, "drift %.12f vs karp %.12f", est.h_bar, karp);
+        }
+        // constant potential shifts the rate by -c (unit_weakkam.cpp:76-84)
+        const SchemeParams pc = params_of(32, 0.1);
+        std::vector<double> c1(32);
+        for (int i = 0; i < 32; ++i) c1[i] = std::cos(2.0 * 3.141592653589793 * i / 32.0 - 3.141592653589793);
+        const EffectiveHEstimate ec =
+            eng.estimate_hbar_drift(make_periodic(c1, pc.epsilon()), 0.0, Potential{[](double, double) { return 0.8125; }, false}, pc, 200, 1e-10);
+        CHECK(ec.converged && std::abs(ec.h_bar + 0.8125) <= 1e-12, "constant potential: %.15f", ec.h_bar);
+        bool threw = false;
+        try {
+            eng.estimate_hbar_drift(make_periodic(c1, 1.0 / 32), 0.0, Potential{}, params_of(32, 0.15), 10, 1e-8);
+        } catch (const InvalidInput&) {
+            threw = true;
+        }
+        CHECK(threw, "tau must divide the period");
     }
     std::printf("%s: %d passed, %d failed\n", g_fail ? "FAIL" : "ALL PASS", g_pass, g_fail);
     return g_fail ? 1 : 0;
