@@ -232,6 +232,42 @@ int lob_fixed_point_residual_host_f64(lob_ctx* ctx, const double* u, int64_t n, 
                                       double drift, double tau, const double* tvs,
                                       int64_t tv_count, int engine, double* residual);
 
+/* ---- step_semidiscrete (proj/src/scheme.cpp:166-206) ----
+ * The reference's built-in potential kinds (proj/include/laxol/hamiltonian.hpp:34-66):
+ *   ZERO: 0;  CONST: value;
+ *   COSINE: offset + amplitude * mod(omega*t) * cos(frequency * theta(x)),
+ *           mod = 1 (TMOD_NONE), sin (TMOD_SIN) or cos (TMOD_COS),
+ *           theta(x) = 2 pi (x - floor x) - pi. */
+#define LOB_POTENTIAL_ZERO 0
+#define LOB_POTENTIAL_CONST 1
+#define LOB_POTENTIAL_COSINE 2
+#define LOB_TMOD_NONE 0
+#define LOB_TMOD_SIN 1
+#define LOB_TMOD_COS 2
+typedef struct lob_potential {
+    int kind;
+    double value;
+    double offset;
+    double amplitude;
+    int frequency;
+    int tmod;
+    double omega;
+} lob_potential;
+
+/* One semi-discrete step of `lines` lines sharing the kernel window ktab
+ * (2*n_space+1 device doubles at displacements first..first+2n) and V:
+ *   out[l][j] = min_w u[l][src] + (ktab[w] - tau/q * trapezoid(V along y -> x_j))
+ * periodic != 0: m == n_space samples per line (fundamental domain, sources
+ * mod n); else m samples of a windowed domain starting at `origin`, sources
+ * outside [0, m) skipped and LOB_EVALUATION_ERROR if an output has none.
+ * quad_points in [1, 64].  Synchronous.  ZERO/CONST potentials give the
+ * reference's doubles exactly; COSINE agrees to <= 1e-12 relative (the
+ * spatial cos is the device's). */
+int lob_step_semidiscrete_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t m,
+                              int64_t n_space, int periodic, double origin, const double* ktab,
+                              int64_t first, double t, double tau, const lob_potential* V,
+                              int quad_points, void* stream);
+
 /* Number of kernel launches issued by this context since creation. */
 int64_t lob_launch_count(const lob_ctx* ctx);
 

@@ -321,4 +321,28 @@ int ref_fixed_point_residual(const double* u, int n_space, double tau, double dr
     });
 }
 
+// step_semidiscrete (proj/src/scheme.cpp:166-206) with a built-in potential kind
+// (0 zero, 1 const, 2 cosine; tmod 0 none, 1 sin, 2 cos).  periodic: u holds the
+// fundamental domain (n_space samples) and out receives n_space values; else m samples.
+int ref_step_semidiscrete(const double* u, int64_t m, int periodic, double origin, int n_space, double tau,
+                          double drift, int kind, double value, double offset, double amplitude, int frequency,
+                          int tmod, double omega, double t, int q, double* out) {
+    return guarded([&] {
+        const SchemeParams p = params_of(n_space, tau, 0.0);
+        Potential pot = potential_zero();
+        if (kind == 1) pot = potential_const(value);
+        if (kind == 2)
+            pot = potential_cosine(offset, amplitude, frequency,
+                                   tmod == 1 ? Potential::TimeMod::Sin
+                                             : (tmod == 2 ? Potential::TimeMod::Cos : Potential::TimeMod::None),
+                                   omega);
+        const HamiltonianSpec spec{mechanical(drift), pot, periodic != 0, false};
+        const GridFn g = periodic ? make_periodic(std::vector<double>(u, u + n_space), p.epsilon(), origin)
+                                  : make_grid_fn(std::vector<double>(u, u + m), p.epsilon(), origin);
+        const GridFn r = step_semidiscrete(g, t, spec, p, q);
+        std::memcpy(out, r.values.data(), (periodic ? n_space : m) * sizeof(double));
+        if (periodic && r.values.back() != r.values.front()) throw EvaluationError("seam differs");
+    });
+}
+
 }  // extern "C"

@@ -24,6 +24,14 @@ FAST_STATS_VALID = 1
 FAST_CHAINED = 2
 DIRECT_SCREENED = 0
 DIRECT_PLAIN = 1
+POTENTIAL_ZERO, POTENTIAL_CONST, POTENTIAL_COSINE = 0, 1, 2
+TMOD_NONE, TMOD_SIN, TMOD_COS = 0, 1, 2
+
+
+class LobPotential(ctypes.Structure):
+    """lob_potential (include/laxol_b200.h)"""
+    _fields_ = [("kind", c_int), ("value", c_double), ("offset", c_double), ("amplitude", c_double),
+                ("frequency", c_int), ("tmod", c_int), ("omega", c_double)]
 
 # name -> (restype, argtypes); every symbol declared in include/laxol_b200.h
 # and include/laxol_b200_configs.h.
@@ -62,6 +70,8 @@ SIGNATURES = {
                                         _P]),
     "lob_fixed_point_residual_host_f64": (c_int, [_P, _P, c_int64, c_double, c_double, c_double, _P, c_int64,
                                                   c_int, POINTER(c_double)]),
+    "lob_step_semidiscrete_f64": (c_int, [_P, _P, _P, c_int64, c_int64, c_int64, c_int, c_double, _P, c_int64,
+                                          c_double, c_double, _P, c_int, _P]),
     # synthetic workloads (include/laxol_b200_configs.h)
     "lob_gen_sin": (None, [c_int64, _P]),
     "lob_gen_cos": (None, [c_int64, _P]),

@@ -236,6 +236,20 @@ class Device:
                                        _stream_ptr(stream))
         self._check(st, "lob_block_counts")
 
+    # ---- step_semidiscrete (proj/src/scheme.cpp:166-206) -----------------------
+    def step_semidiscrete(self, u, out, ktab, first, t, tau, potential=None, quad_points=1, periodic=True,
+                          origin=0.0, n_space=None, stream=None):
+        """One semi-discrete step of lines x m device samples (periodic: m == n_space)."""
+        lines, m = u.shape
+        n = m if n_space is None else int(n_space)
+        pot = potential_zero() if potential is None else potential
+        p = _capi.LobPotential(pot["kind"], pot["value"], pot["offset"], pot["amplitude"], pot["frequency"],
+                               pot["tmod"], pot["omega"])
+        st = self.lib.lob_step_semidiscrete_f64(self.ctx, _ptr(u), _ptr(out), lines, m, n, int(periodic),
+                                                float(origin), _ptr(ktab), int(first), float(t), float(tau),
+                                                ctypes.byref(p), int(quad_points), _stream_ptr(stream))
+        self._check(st, "lob_step_semidiscrete_f64")
+
     # ---- weak-KAM consumers (proj/src/weakkam.cpp; include/laxol_b200.h) ----
     def minplus_gemm(self, a, b, out, stream=None):
         """out = a (x) b in the min-plus semiring (minplus_product / minplus_apply)."""
@@ -309,6 +323,23 @@ class Device:
         st = self.lib.lob_bench_fp64(self.ctx, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c))
         self._check(st, "lob_bench_fp64")
         return {"minplus_cand_per_s": a.value, "dadd_ops_per_s": b.value, "sm_clock_ghz": c.value}
+
+
+# ---- built-in potentials (proj/src/hamiltonian.cpp:77-117) --------------------
+def potential_zero() -> dict:
+    return dict(kind=_capi.POTENTIAL_ZERO, value=0.0, offset=0.0, amplitude=0.0, frequency=1,
+                tmod=_capi.TMOD_NONE, omega=0.0)
+
+
+def potential_const(c: float) -> dict:
+    return dict(potential_zero(), kind=_capi.POTENTIAL_CONST, value=float(c))
+
+
+def potential_cosine(offset: float, amplitude: float, frequency: int, tmod: int = 0, omega: float = 0.0) -> dict:
+    if frequency < 1:
+        raise InvalidInput("potential_cosine: frequency must be >= 1")
+    return dict(potential_zero(), kind=_capi.POTENTIAL_COSINE, offset=float(offset), amplitude=float(amplitude),
+                frequency=int(frequency), tmod=int(tmod), omega=float(omega))
 
 
 # ---- synthetic workloads (include/laxol_b200_configs.h) ---------------------

@@ -525,4 +525,82 @@ double Engine::eigenvalue_karp(const MinPlusMatrix& C) {
     return lam;
 }
 
+// ---- built-in potentials and step_semidiscrete --------------------------------
+
+double BuiltinPotential::operator()(double t, double x) const {
+    // proj/src/hamiltonian.cpp:18-21,98-117
+    switch (kind) {
+        case Kind::Zero:
+            return 0.0;
+        case Kind::Const:
+            return value;
+        case Kind::Cosine: {
+            double mod = 1.0;
+            if (tmod == TimeMod::Sin) mod = std::sin(omega * t);
+            else if (tmod == TimeMod::Cos) mod = std::cos(omega * t);
+            const double r = x - std::floor(x);
+            const double th = (2.0 * 3.141592653589793) * r - 3.141592653589793;
+            return offset + amplitude * mod * std::cos(static_cast<double>(frequency) * th);
+        }
+    }
+    return 0.0;
+}
+
+Potential BuiltinPotential::callback() const {
+    if (kind == Kind::Zero) return Potential{};
+    const BuiltinPotential self = *this;
+    Potential p;
+    p.fn = [self](double t, double x) { return self(t, x); };
+    p.time_dependent = kind == Kind::Cosine && tmod != TimeMod::None && amplitude != 0.0;
+    return p;
+}
+
+BuiltinPotential potential_zero() { return BuiltinPotential{}; }
+
+BuiltinPotential potential_const(double c) {
+    BuiltinPotential p;
+    p.kind = BuiltinPotential::Kind::Const;
+    p.value = c;
+    return p;
+}
+
+BuiltinPotential potential_cosine(double offset, double amplitude, int frequency, BuiltinPotential::TimeMod tmod,
+                                  double omega) {
+    if (frequency < 1) throw InvalidInput("potential_cosine: frequency must be >= 1");
+    BuiltinPotential p;
+    p.kind = BuiltinPotential::Kind::Cosine;
+    p.offset = offset;
+    p.amplitude = amplitude;
+    p.frequency = frequency;
+    p.tmod = tmod;
+    p.omega = omega;
+    return p;
+}
+
+GridFn Engine::step_semidiscrete(const GridFn& u, double t, double drift, const BuiltinPotential& V,
+                                 const SchemeParams& params, int quad_points) {
+    if (quad_points < 1) throw InvalidInput("step_semidiscrete: quad_points must be >= 1");
+    check_u_grid(u, params, "step_semidiscrete");
+    const KernelWindow k = build_kernel_mech(params.n_space, params.tau, drift);
+    lob_potential lp{};
+    lp.kind = static_cast<int>(V.kind);
+    lp.value = V.value;
+    lp.offset = V.offset;
+    lp.amplitude = V.amplitude;
+    lp.frequency = V.frequency;
+    lp.tmod = static_cast<int>(V.tmod);
+    lp.omega = V.omega;
+    const int64_t m = u.periodic ? static_cast<int64_t>(u.n()) : static_cast<int64_t>(u.size());
+    DevBuf<double> du(m), dout(m), dk(k.window.size());
+    du.upload(u.values.data(), m);
+    dk.upload(k.window.data(), k.window.size());
+    check_status(lob_step_semidiscrete_f64(ctx_, du.p, dout.p, 1, m, params.n_space, u.periodic ? 1 : 0, u.origin,
+                                           dk.p, k.first, t, params.tau, &lp, quad_points, nullptr),
+                 ctx_, "step_semidiscrete");
+    std::vector<double> out(u.size());
+    dout.download(out.data(), m);
+    if (u.periodic) out[m] = out[0];  // sample_coord wraps the seam index (proj/src/scheme.cpp:32-35)
+    return GridFn{std::move(out), u.step, u.origin, u.periodic};
+}
+
 }  // namespace laxol_b200

@@ -82,6 +82,27 @@ struct Potential {
     explicit operator bool() const { return static_cast<bool>(fn); }
 };
 
+// The reference's built-in potential kinds (proj/include/laxol/hamiltonian.hpp:34-66,
+// proj/src/hamiltonian.cpp:77-117), which the device can evaluate itself
+// (step_semidiscrete samples V off the grid).
+struct BuiltinPotential {
+    enum class Kind { Zero, Const, Cosine };
+    enum class TimeMod { None, Sin, Cos };
+    Kind kind = Kind::Zero;
+    double value = 0.0;  // Const
+    double offset = 0.0, amplitude = 0.0;  // Cosine: offset + amplitude*mod(omega t)*cos(frequency*theta(x))
+    int frequency = 1;
+    TimeMod tmod = TimeMod::None;
+    double omega = 0.0;
+    double operator()(double t, double x) const;  // host evaluation (the reference's formula)
+    Potential callback() const;                   // as a host callback for the other entry points
+};
+BuiltinPotential potential_zero();
+BuiltinPotential potential_const(double c);
+BuiltinPotential potential_cosine(double offset, double amplitude, int frequency,
+                                  BuiltinPotential::TimeMod tmod = BuiltinPotential::TimeMod::None,
+                                  double omega = 0.0);
+
 struct StepStats {
     int64_t block_count = 0;
 };
@@ -155,6 +176,10 @@ public:
                                const SchemeParams& params, const KernelWindow& kernel,
                                ConvEngine engine = ConvEngine::GpuFast,
                                StepStats* stats = nullptr);
+    // proj/src/scheme.cpp:166-206: trapezoid-integrated V along each segment
+    // (mechanical(drift) kinetics; the device evaluates V)
+    GridFn step_semidiscrete(const GridFn& u, double t, double drift, const BuiltinPotential& V,
+                             const SchemeParams& params, int quad_points);
     // proj/src/scheme.cpp:208-272 (time-independent V: device-resident loop)
     EvolutionTrace evolve(const GridFn& u0, double t0, int64_t steps, double drift,
                           const Potential& V, const SchemeParams& params,

@@ -123,6 +123,9 @@ class Reference:
             "ref_decompose": (c_int64, [_P, c_int64, c_double, _P, _P, _P, c_int64]),
             "ref_conv": (c_int, [c_int, _P, c_int64, _P, c_int64, c_double, _P, _P]),
             "ref_minplus_product": (c_int, [_P, _P, c_int64, _P]),
+            "ref_step_semidiscrete": (c_int, [_P, c_int64, c_int, c_double, c_int, c_double, c_double, c_int,
+                                              c_double, c_double, c_double, c_int, c_int, c_double, c_double,
+                                              c_int, _P]),
             "ref_minplus_apply": (c_int, [_P, c_int64, _P, _P]),
             "ref_eigenvalue_karp": (c_int, [_P, c_int64, POINTER(c_double)]),
             "ref_build_period_matrix": (c_int, [c_int, c_double, c_double, _P, c_int64, _P]),
@@ -207,6 +210,15 @@ class Reference:
         st = self.lib.ref_conv(which, a.ctypes.data, a.size, b.ctypes.data, b.size, eta, out.ctypes.data,
                                ctypes.byref(blocks))
         return out, blocks.value, st
+
+    def step_semidiscrete(self, u, n_space, tau, drift, pot, t, q, periodic=True, origin=0.0):
+        """pot: dict(kind, value, offset, amplitude, frequency, tmod, omega) (api.potential_*)."""
+        u = np.ascontiguousarray(u, np.float64)
+        out = np.empty(n_space if periodic else u.size)
+        st = self.lib.ref_step_semidiscrete(u.ctypes.data, u.size, int(periodic), origin, n_space, tau, drift,
+                                            pot["kind"], pot["value"], pot["offset"], pot["amplitude"],
+                                            pot["frequency"], pot["tmod"], pot["omega"], t, q, out.ctypes.data)
+        return out, st
 
     # ---- weak-KAM consumers (proj/src/weakkam.cpp) ----
     def minplus_product(self, a, b):

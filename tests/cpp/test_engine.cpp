@@ -236,6 +236,32 @@ int main() {
         }
         CHECK(threw, "tau must divide the period");
     }
+    // 8. step_semidiscrete (unit_scheme.cpp:209-233)
+    {
+        const SchemeParams p = params_of(24, 0.25);
+        const KernelWindow k = build_kernel_mech(24, 0.25, 0.25);
+        const GridFn u = random_periodic(rng, 24, 1.0, p.epsilon());
+        const GridFn full = eng.step_fully_discrete(u, 0.0, Potential{}, p, k, ConvEngine::GpuDirect);
+        const GridFn semi = eng.step_semidiscrete(u, 0.0, 0.25, potential_zero(), p, 4);
+        bool same = semi.values.size() == full.values.size();
+        for (std::size_t i = 0; same && i < full.size(); ++i) same = semi.values[i] == full.values[i];
+        CHECK(same, "semi-discrete(V = 0) == fully discrete step");
+        bool threw = false;
+        try {
+            eng.step_semidiscrete(u, 0.0, 0.25, potential_zero(), p, 0);
+        } catch (const InvalidInput&) {
+            threw = true;
+        }
+        CHECK(threw, "quad_points 0 rejected");
+        const SchemeParams p2 = params_of(32, 0.25);
+        const BuiltinPotential pot = potential_cosine(0.0, 0.5, 1);
+        const GridFn u2 = random_periodic(rng, 32, 0.5, p2.epsilon());
+        const GridFn f2 = eng.step_fully_discrete(u2, 0.0, pot.callback(), p2, build_kernel_mech(32, 0.25, 0.0));
+        const GridFn s2 = eng.step_semidiscrete(u2, 0.0, 0.0, pot, p2, 32);
+        double d = 0.0;
+        for (std::size_t i = 0; i < f2.size(); ++i) d = std::max(d, std::abs(f2.values[i] - s2.values[i]));
+        CHECK(d <= 0.25 * 0.5 * 2.0 * 3.141592653589793 + 1e-9, "endpoint sampling error bound (%.3e)", d);
+    }
     std::printf("%s: %d passed, %d failed\n", g_fail ? "FAIL" : "ALL PASS", g_pass, g_fail);
     return g_fail ? 1 : 0;
 }
