@@ -365,6 +365,36 @@ def extras(dev):
     t = timeit(lambda: dev.fast_f64(u, o, z, 0.01, workspace=ws), 10)
     out["k2_fast_c3"] = {"ms": t * 1e3, "updates_per_s": 4096 * 4096 / t,
                          "hbm_frac": 4096 * 4096 * 16 / t / 1e9 / measured_peaks()[0]}
+    del u, o, u32, o32, ws
+
+    # weak-KAM consumers: tropical product at the dense guard n = 512, Karp, period matrix
+    m = 512
+    rng = np.random.default_rng(0)
+    A = torch.from_numpy(rng.uniform(-1, 1, (m, m))).cuda()
+    B = torch.from_numpy(rng.uniform(-1, 1, (m, m))).cuda()
+    C = torch.empty_like(A)
+    t = timeit(lambda: dev.minplus_gemm(A, B, C), 20)
+    out["minplus_product_512"] = {"ms": t * 1e3, "cand_per_s": m ** 3 / t,
+                                  "frac_of_minplus_mix_peak": m ** 3 / t / fp["minplus_cand_per_s"]}
+    dev.eigenvalue_karp(A)
+    t0 = time.perf_counter()
+    dev.eigenvalue_karp(A)
+    out["eigenvalue_karp_512"] = {"ms": (time.perf_counter() - t0) * 1e3, "gemv_launches": m}
+    kinc = torch.from_numpy(api.Device.period_kinetic(dev.build_kernel(m, 0.125, 0.3))).cuda()
+    tvs = torch.from_numpy(np.tile(0.125 * api.gen_potential(1, m), (8, 1))).cuda()
+    scratch = torch.empty(2 * m * m, dtype=torch.float64, device="cuda")
+    t = timeit(lambda: dev.period_matrix(kinc, tvs, 8, C, scratch), 5)
+    out["period_matrix_512_ell8"] = {"ms": t * 1e3, "cand_per_s": 7 * m ** 3 / t}
+    # step_semidiscrete: C1's grid and V = cos(2 pi x) = potential_cosine(0, -1, 1), q = 4
+    n1, tau1 = 1024, 0.05
+    k1 = dev.build_kernel(n1, tau1, 0.5)
+    us = torch.from_numpy(api.gen_sin(n1)[None, :].repeat(64, 0)).cuda()
+    os_ = torch.empty_like(us)
+    kt = torch.from_numpy(k1.window).cuda()
+    pot = api.potential_cosine(0.0, -1.0, 1)
+    t = timeit(lambda: dev.step_semidiscrete(us, os_, kt, k1.first, 0.0, tau1, pot, 4), 3)
+    out["semidiscrete_c1x64_q4"] = {"ms": t * 1e3, "lines": 64, "n": n1,
+                                    "cand_per_s": 64 * n1 * (2 * n1 + 1) / t}
     return out
 
 

@@ -74,11 +74,14 @@ constexpr int kC = LOB_KC;       // sources staged per chunk (a typical tile + h
 #define LOB_VCAP 1024
 #endif
 constexpr int kVCap = LOB_VCAP;  // v_d values staged per tile (TMA, with the first chunk)
+#ifndef LOB_FAST_WORK_COUNTERS
+#define LOB_FAST_WORK_COUNTERS 0  // per-source inline-candidate count (diagnostic builds only)
+#endif
 
 struct LineConst {
     long long first;  // window displacement of w = 0
     double pe;        // drift * eps
-    double hl, hr;    // dL = ceil(z + hl), dR = floor(z + hr), z = (s + pe)/a
+    double hl, hr;    // dL = ceil(s/a + hl), dR = floor(s/a + hr): hl/hr = P eps/a -/+ (1/2 + delta)
     double gap;       // min(K(first), K(first+2n)) - min K: the oscillation gate
     double drift;
 };
@@ -426,7 +429,7 @@ __device__ __forceinline__ void issue_chunk(MainShared& S, const double* ul, int
 struct ChunkArgs {
     const double* ub;  // ub[i + 1] = U(yc + i), i in [-1, clen]
     int clen, base, jspan;
-    double pe, ia, hl, hr;
+    double ia, hl, hr;
     int dlo, dhi;       // the tile's displacement range (clamp)
     const double* skt;  // K(d) staged in shared memory (KS) ...
     const double* gvt;  // ... or v_d in global memory
@@ -454,13 +457,14 @@ __device__ __forceinline__ void process_chunk(MainShared& S, const ChunkArgs& a)
 #pragma unroll kEmitUnroll
     for (int i = warp * per + lane; i < iend; i += 32) {
         const double ul0 = a.ub[i], u0 = a.ub[i + 1], ur0 = a.ub[i + 2];
-        const double zl = __dmul_rn(__dadd_rn(__dsub_rn(u0, ul0), a.pe), a.ia);
-        const double zr = __dmul_rn(__dadd_rn(__dsub_rn(ur0, u0), a.pe), a.ia);
+        // z(s) -/+ (1/2 + delta) with one fused rounding (delta bounds it, csrc/host/kernel_build.cpp)
+        const double zl = __fma_rn(__dsub_rn(u0, ul0), a.ia, a.hl);
+        const double zr = __fma_rn(__dsub_rn(ur0, u0), a.ia, a.hr);
         const int off = a.base + i;  // output index of this source at d = 0
         // every candidate lies in [dlo, dhi] when the statistics describe u;
         // the clamp keeps stale statistics memory-safe (wrong, never out of bounds)
-        const int dl = max(max(__double2int_ru(zl + a.hl), a.dlo), -off);
-        const int dr = min(min(__double2int_rd(zr + a.hr), a.dhi), a.jspan - off);
+        const int dl = max(max(__double2int_ru(zl), a.dlo), -off);
+        const int dr = min(min(__double2int_rd(zr), a.dhi), a.jspan - off);
         if (dl <= dr) {
             unsigned long long* slot = &S.keys[off + dl];
             const double c0 = __dadd_rn(u0, kvalue<KS>(a, dl));
@@ -473,7 +477,7 @@ __device__ __forceinline__ void process_chunk(MainShared& S, const ChunkArgs& a)
                     atomicCAS(slot + 1, kInfBits, static_cast<unsigned long long>(__double_as_longlong(c1)));
                 r1 = o1 != kInfBits && c1 < __longlong_as_double(static_cast<long long>(o1));
             }
-            ninl += min(dr - dl + 1, 2);
+            if constexpr (LOB_FAST_WORK_COUNTERS) ninl += min(dr - dl + 1, 2);
             const bool longer = dl + 2 <= dr;
             if (r0 | r1 | longer) {
                 const int qlo = r0 ? dl : (r1 ? dl + 1 : dl + 2);
@@ -487,7 +491,7 @@ __device__ __forceinline__ void process_chunk(MainShared& S, const ChunkArgs& a)
             }
         }
     }
-    if (ninl) atomicAdd(&S.c_inline, ninl);
+    if (LOB_FAST_WORK_COUNTERS && ninl) atomicAdd(&S.c_inline, ninl);
     __syncthreads();
     const int nq = min(S.nq, kQCap);
     if (nq) {
@@ -530,8 +534,9 @@ __global__ void line_setup_kernel(const double* __restrict__ drift_arr, int64_t 
     LineConst c;
     c.first = first;
     c.pe = __dmul_rn(drift, eps);
-    c.hl = -0.5 - delta;
-    c.hr = 0.5 + delta;
+    const double pz = __dmul_rn(c.pe, p.ia);  // P eps / a
+    c.hl = pz - (0.5 + delta);
+    c.hr = pz + (0.5 + delta);
     c.gap = fmin(kfirst, klast) - kmin;
     c.drift = drift;
     lc[line] = c;
@@ -576,7 +581,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
     const bool big = TMA && n >= kC + 8;
     const double* ul = u + line * p.n;
     const LineConst lc = lcs[line];
-    const double tau = p.tau, ia = p.ia, pe = lc.pe, hl = lc.hl, hr = lc.hr;
+    const double tau = p.tau, ia = p.ia, hl = lc.hl, hr = lc.hr;
     const int first = static_cast<int>(lc.first);
     const int dmin_w = first + 1, dmax_w = first + 2 * n - 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -585,7 +590,12 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
     // every CTA of this one is running; this grid waits for the previous one (its u,
     // statistics and the buffers it still reads) before touching global memory
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    for (int i = tid; i <= jspan; i += kNT) S.keys[i] = kInfBits;
+    {
+        // +inf sentinels for keys[0 .. jspan] (jspan + 1 <= kT + 3 <= kT + 4 slots, 16-byte stores)
+        ulonglong2* k2 = reinterpret_cast<ulonglong2*>(S.keys);
+#pragma unroll
+        for (int i = tid; i < (kT + 4) / 2; i += kNT) k2[i] = make_ulonglong2(kInfBits, kInfBits);
+    }
     if constexpr (CHAIN) {
         if (warp == 0) {
             if (lane == 0) {
@@ -620,8 +630,8 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
         bool okl = (osc_bound * (1.0 + 1e-12) < lc.gap * (1.0 - 1e-12)) && n >= 3 && isfinite(smin) &&
                    isfinite(smax);
         if (okl) {
-            DLg = max(__double2int_ru(__dmul_rn(__dadd_rn(smin, pe), ia) + hl), dmin_w);
-            DRg = min(__double2int_rd(__dmul_rn(__dadd_rn(smax, pe), ia) + hr), dmax_w);
+            DLg = max(__double2int_ru(__fma_rn(smin, ia, hl)), dmin_w);
+            DRg = min(__double2int_rd(__fma_rn(smax, ia, hr)), dmax_w);
             okl = DLg <= DRg;
         }
         int ya = INT_MAX, yb = INT_MIN, dlo = INT_MAX, dhi = INT_MIN;
@@ -641,8 +651,8 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
                 const double2 sb = xload<CHAIN>(b.sub_in + line * p.subs + q);
                 const int ys = k * n + q * kG;
                 const int ye = ys + min(kG, n - q * kG) - 1;
-                const int dl = max(__double2int_ru(__dmul_rn(__dadd_rn(sb.x, pe), ia) + hl), DLg);
-                const int dr = min(__double2int_rd(__dmul_rn(__dadd_rn(sb.y, pe), ia) + hr), DRg);
+                const int dl = max(__double2int_ru(__fma_rn(sb.x, ia, hl)), DLg);
+                const int dr = min(__double2int_rd(__fma_rn(sb.y, ia, hr)), DRg);
                 if (dl <= dr && ys + dl <= jhi && ye + dr >= jlo) {
                     ya = min(ya, ys);
                     yb = max(yb, ye);
@@ -717,7 +727,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
             }
             const double* ub = S.ubuf + sh;
             if (tid == 0) S.c_src += static_cast<unsigned>(clen);
-            const ChunkArgs ca{ub, clen, base, jspan, pe, ia, hl, hr, dlo_t, dhi_t, skt, gvt, kdrift, tau};
+            const ChunkArgs ca{ub, clen, base, jspan, ia, hl, hr, dlo_t, dhi_t, skt, gvt, kdrift, tau};
             if (kstage)
                 process_chunk<true>(S, ca);
             else
