@@ -49,6 +49,8 @@ extern "C" {
  * two device engines. */
 #define LOB_ENGINE_DIRECT 0 /* K1: exact O(n^2) min-plus, bit-identical to ConvEngine::Naive */
 #define LOB_ENGINE_FAST 1   /* K2: exact O(n) local-minimum walk (mechanical kinetics) */
+#define LOB_ENGINE_RELAXED 2 /* the reference's ConvEngine::Fast with eta (relaxed for eta > 0), see
+                              * lob_minplus_relaxed_f64; evolve and the host step accept it */
 
 typedef struct lob_ctx lob_ctx;
 
@@ -267,6 +269,22 @@ int lob_step_semidiscrete_f64(lob_ctx* ctx, const double* u, double* out, int64_
                               int64_t n_space, int periodic, double origin, const double* ktab,
                               int64_t first, double t, double tau, const lob_potential* V,
                               int quad_points, void* stream);
+
+/* ---- The reference's relaxed fast engine, eta > 0 ----
+ * kinetic_convolve(u, kernel, eta, ConvEngine::Fast) + the potential for
+ * periodic lines: decompose(u, eta) with the 48-sample cap, the slope merge /
+ * envelope of every block with the whole window, min_pointwise, aliasing
+ * (proj/src/minplus.cpp:152-276, proj/src/scheme.cpp:107-164).  For eta > 0
+ * this is the reference's approximation, reproduced bit for bit; for
+ * eta == 0 it is exact (== K1).  Same table conventions as
+ * lob_minplus_direct_f64; blocks (nullable, device int64[lines]) receives the
+ * reference's block_count (capped for eta > 0).  O(blocks x n) work, like the
+ * reference.  Synchronous (reports min_pointwise's gap error). */
+int lob_relaxed_workspace_bytes(int64_t lines, int64_t n, size_t* bytes);
+int lob_minplus_relaxed_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
+                            const double* ktab, int64_t ktab_stride, const int64_t* first,
+                            const double* tv, int64_t tv_stride, double eta, int64_t* blocks,
+                            void* workspace, size_t workspace_bytes, void* stream);
 
 /* Number of kernel launches issued by this context since creation. */
 int64_t lob_launch_count(const lob_ctx* ctx);

@@ -20,6 +20,7 @@ LOB_CUDA_ERROR = 3
 
 ENGINE_DIRECT = 0
 ENGINE_FAST = 1
+ENGINE_RELAXED = 2
 FAST_STATS_VALID = 1
 FAST_CHAINED = 2
 DIRECT_SCREENED = 0
@@ -72,6 +73,9 @@ SIGNATURES = {
                                                   c_int, POINTER(c_double)]),
     "lob_step_semidiscrete_f64": (c_int, [_P, _P, _P, c_int64, c_int64, c_int64, c_int, c_double, _P, c_int64,
                                           c_double, c_double, _P, c_int, _P]),
+    "lob_relaxed_workspace_bytes": (c_int, [c_int64, c_int64, POINTER(c_size_t)]),
+    "lob_minplus_relaxed_f64": (c_int, [_P, _P, _P, c_int64, c_int64, _P, c_int64, _P, _P, c_int64, c_double, _P,
+                                        _P, c_size_t, _P]),
     # synthetic workloads (include/laxol_b200_configs.h)
     "lob_gen_sin": (None, [c_int64, _P]),
     "lob_gen_cos": (None, [c_int64, _P]),

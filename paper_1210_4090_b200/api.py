@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _capi
-from ._capi import (DIRECT_PLAIN, DIRECT_SCREENED, ENGINE_DIRECT, ENGINE_FAST, FAST_CHAINED, FAST_STATS_VALID, EvaluationError,  # noqa: F401
+from ._capi import (DIRECT_PLAIN, DIRECT_SCREENED, ENGINE_DIRECT, ENGINE_FAST, ENGINE_RELAXED, FAST_CHAINED, FAST_STATS_VALID, EvaluationError,  # noqa: F401
                     InvalidInput, check)
 
 
@@ -235,6 +235,24 @@ class Device:
         st = self.lib.lob_block_counts(self.ctx, _ptr(u), lines, n, float(eta), _ptr(blocks),
                                        _stream_ptr(stream))
         self._check(st, "lob_block_counts")
+
+    # ---- the reference's relaxed fast engine, eta > 0 (proj/src/minplus.cpp:152-276) ----
+    def relaxed_workspace_bytes(self, lines: int, n: int) -> int:
+        b = ctypes.c_size_t()
+        self._check(self.lib.lob_relaxed_workspace_bytes(lines, n, ctypes.byref(b)), "lob_relaxed_workspace_bytes")
+        return int(b.value)
+
+    def relaxed_f64(self, u, out, ktab, first, eta, tv=None, ktab_stride=0, tv_stride=0, blocks=None,
+                    workspace=None, stream=None):
+        lines, n = u.shape
+        if workspace is None:
+            import torch
+            workspace = torch.empty(self.relaxed_workspace_bytes(lines, n), dtype=torch.uint8, device=u.device)
+        ws_bytes = workspace.numel() * workspace.element_size()
+        st = self.lib.lob_minplus_relaxed_f64(self.ctx, _ptr(u), _ptr(out), lines, n, _ptr(ktab), ktab_stride,
+                                              _ptr(first), _ptr(tv), tv_stride, float(eta), _ptr(blocks),
+                                              _ptr(workspace), ws_bytes, _stream_ptr(stream))
+        self._check(st, "lob_minplus_relaxed_f64")
 
     # ---- step_semidiscrete (proj/src/scheme.cpp:166-206) -----------------------
     def step_semidiscrete(self, u, out, ktab, first, t, tau, potential=None, quad_points=1, periodic=True,

@@ -281,8 +281,16 @@ int lob_evolve_f64(lob_ctx* ctx, double* u, double* scratch, int64_t lines, int6
     double* ktab = nullptr;
     int64_t* firsts = nullptr;
     int* halt = nullptr;
+    void* rws = nullptr;
+    size_t rwsb = 0;
     const int64_t W = 2 * n + 1;
-    if (engine == LOB_ENGINE_DIRECT) {
+    if (engine != LOB_ENGINE_DIRECT && engine != LOB_ENGINE_FAST && engine != LOB_ENGINE_RELAXED)
+        return set_error(ctx, LOB_INVALID_INPUT, "evolve: unknown engine");
+    if (engine == LOB_ENGINE_RELAXED) {
+        rwsb = relaxed_workspace_bytes(lines, n);
+        LOB_CUDA_TRY(ctx, cudaMallocAsync(&rws, rwsb, s));
+    }
+    if (engine != LOB_ENGINE_FAST) {
         LOB_CUDA_TRY(ctx, cudaMallocAsync(&ktab, lines * W * sizeof(double), s));
         LOB_CUDA_TRY(ctx, cudaMallocAsync(&firsts, lines * sizeof(int64_t), s));
         std::vector<double> hk(static_cast<size_t>(lines * W));
@@ -312,6 +320,9 @@ int lob_evolve_f64(lob_ctx* ctx, double* u, double* scratch, int64_t lines, int6
             st = launch_direct_f64(ctx, cur, nxt, lines, n, ktab, W, firsts, tv, tv_stride, s);
             if (st == LOB_OK && step_blocks)
                 st = launch_block_counts(ctx, cur, lines, n, eta, step_blocks + i * lines, s);
+        } else if (engine == LOB_ENGINE_RELAXED) {
+            st = launch_relaxed_f64(ctx, cur, nxt, lines, n, ktab, W, firsts, tv, tv_stride, eta,
+                                    step_blocks ? step_blocks + i * lines : nullptr, rws, rwsb, s);
         } else {
             st = launch_fast_f64(ctx, cur, nxt, lines, n, drift, tau, tv, tv_stride, eta,
                                  step_blocks ? step_blocks + i * lines : nullptr, workspace,
@@ -340,6 +351,7 @@ int lob_evolve_f64(lob_ctx* ctx, double* u, double* scratch, int64_t lines, int6
                                           cudaMemcpyDeviceToDevice, s));
     if (ktab) cudaFreeAsync(ktab, s);
     if (firsts) cudaFreeAsync(firsts, s);
+    if (rws) cudaFreeAsync(rws, s);
     cudaFreeAsync(halt, s);
     LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
     if (completed_steps) *completed_steps = done;
@@ -366,9 +378,12 @@ int lob_step_host_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines,
     const int64_t per_chunk = (lines + kHostChunks - 1) / kHostChunks;
     const size_t wsb_chunk = fast_workspace_bytes(per_chunk, n);
     const int64_t W = 2 * n + 1;
-    const size_t kb = engine == LOB_ENGINE_DIRECT ? static_cast<size_t>(lines * W) * sizeof(double) : 0;
+    if (engine != LOB_ENGINE_DIRECT && engine != LOB_ENGINE_FAST && engine != LOB_ENGINE_RELAXED)
+        return set_error(ctx, LOB_INVALID_INPUT, "step: unknown engine");
+    const size_t kb = engine != LOB_ENGINE_FAST ? static_cast<size_t>(lines * W) * sizeof(double) : 0;
+    const size_t rwsb = engine == LOB_ENGINE_RELAXED ? relaxed_workspace_bytes(lines, n) : 0;
     const size_t need = 2 * ub + tvn * sizeof(double) + lines * (sizeof(double) + 2 * sizeof(int64_t)) +
-                        wsb + 2 * wsb_chunk + kb + 10 * 256;
+                        wsb + 2 * wsb_chunk + kb + rwsb + 11 * 256;
     if (ctx->scratch_bytes < need) {
         if (ctx->scratch) cudaFree(ctx->scratch);
         ctx->scratch = nullptr;
@@ -391,11 +406,12 @@ int lob_step_host_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines,
     double* dk = reinterpret_cast<double*>(take(kb));
     void* ws = take(wsb);
     void* ws_chunk[2] = {take(wsb_chunk), take(wsb_chunk)};
-    const bool piped = engine != LOB_ENGINE_DIRECT && lines >= 2 * kHostChunks;
+    void* rws = take(rwsb);
+    const bool piped = engine == LOB_ENGINE_FAST && lines >= 2 * kHostChunks;
     if (!piped) LOB_CUDA_TRY(ctx, cudaMemcpyAsync(du, u, ub, cudaMemcpyHostToDevice, s));
     if (tv) LOB_CUDA_TRY(ctx, cudaMemcpyAsync(dtv, tv, tvn * sizeof(double), cudaMemcpyHostToDevice, s));
     LOB_CUDA_TRY(ctx, cudaMemcpyAsync(ddrift, drift, lines * sizeof(double), cudaMemcpyHostToDevice, s));
-    if (engine == LOB_ENGINE_DIRECT) {
+    if (engine != LOB_ENGINE_FAST) {
         std::vector<double> hk(static_cast<size_t>(lines * W));
         std::vector<int64_t> hf(static_cast<size_t>(lines));
         for (int64_t l = 0; l < lines; ++l) {
@@ -406,8 +422,13 @@ int lob_step_host_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines,
         }
         LOB_CUDA_TRY(ctx, cudaMemcpyAsync(dk, hk.data(), hk.size() * sizeof(double), cudaMemcpyHostToDevice, s));
         LOB_CUDA_TRY(ctx, cudaMemcpyAsync(dfirst, hf.data(), hf.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-        st = launch_direct_f64(ctx, du, dout, lines, n, dk, W, dfirst, tv ? dtv : nullptr, tv_stride, s);
-        if (st == LOB_OK && blocks) st = launch_block_counts(ctx, du, lines, n, eta, dblocks, s);
+        if (engine == LOB_ENGINE_RELAXED) {
+            st = launch_relaxed_f64(ctx, du, dout, lines, n, dk, W, dfirst, tv ? dtv : nullptr, tv_stride, eta,
+                                    blocks ? dblocks : nullptr, rws, rwsb, s);
+        } else {
+            st = launch_direct_f64(ctx, du, dout, lines, n, dk, W, dfirst, tv ? dtv : nullptr, tv_stride, s);
+            if (st == LOB_OK && blocks) st = launch_block_counts(ctx, du, lines, n, eta, dblocks, s);
+        }
         LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));  // host vectors go out of scope
     } else if (lines >= 2 * kHostChunks) {
         // pipelined over line chunks: uploads, steps and downloads run on three

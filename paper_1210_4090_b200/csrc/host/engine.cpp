@@ -91,8 +91,10 @@ std::vector<double> tabulate_tv(const GridFn& u, const Potential& V, double tt, 
     return tv;
 }
 
-int engine_code(ConvEngine e) {
-    if (e == ConvEngine::GpuFast) return LOB_ENGINE_FAST;
+// ConvEngine::GpuFast with eta > 0 is the reference's relaxed fast engine
+// (ConvEngine::Fast, proj/src/minplus.cpp:195-252); at eta == 0 both are exact.
+int engine_code(ConvEngine e, double eta = 0.0) {
+    if (e == ConvEngine::GpuFast) return eta > 0.0 ? LOB_ENGINE_RELAXED : LOB_ENGINE_FAST;
     if (e == ConvEngine::GpuDirect) return LOB_ENGINE_DIRECT;
     throw InvalidInput(
         "laxol_b200: ConvEngine::Fast/Naive are the reference's CPU engines; use GpuFast or GpuDirect");
@@ -134,7 +136,7 @@ Engine::~Engine() { lob_ctx_destroy(ctx_); }
 GridFn Engine::kinetic_convolve(const GridFn& u, const KernelWindow& kernel, double eta,
                                 ConvEngine engine, int64_t* blocks) {
     const int64_t n = kernel.n_space;
-    const int code = engine_code(engine);
+    const int code = engine_code(engine, eta);
     if (u.periodic) {
         if (static_cast<int64_t>(u.n()) != n)
             throw InvalidInput("kinetic_convolve: periodic u must hold one unit period");
@@ -150,6 +152,18 @@ GridFn Engine::kinetic_convolve(const GridFn& u, const KernelWindow& kernel, dou
             DevBuf<int64_t> db(1);
             check_status(lob_minplus_fast_f64(ctx_, du.p, dout.p, 1, n, dd.p, kernel.tau, nullptr, 0, eta,
                                               db.p, ws.p, wsb, 0, nullptr),
+                         ctx_, "kinetic_convolve");
+            db.download(&b, 1);
+        } else if (code == LOB_ENGINE_RELAXED) {
+            DevBuf<double> dk(kernel.window.size());
+            dk.upload(kernel.window.data(), kernel.window.size());
+            DevBuf<int64_t> df(1), db(1);
+            df.upload(&kernel.first, 1);
+            size_t wsb = 0;
+            lob_relaxed_workspace_bytes(1, n, &wsb);
+            DevBuf<unsigned char> ws(wsb);
+            check_status(lob_minplus_relaxed_f64(ctx_, du.p, dout.p, 1, n, dk.p, 0, df.p, nullptr, 0, eta, db.p, ws.p,
+                                                 wsb, nullptr),
                          ctx_, "kinetic_convolve");
             db.download(&b, 1);
         } else {
@@ -234,7 +248,7 @@ EvolutionTrace Engine::evolve(const GridFn& u0, double t0, int64_t steps, double
     check_u_grid(u0, params, "evolve");
     validate(params);
     if (!u0.periodic) throw InvalidInput("laxol_b200 evolve: periodic domains only");
-    const int code = engine_code(options.engine);
+    const int code = engine_code(options.engine, params.eta);
     const int64_t n = params.n_space;
 
     int64_t stride = options.snapshot_stride;

@@ -124,6 +124,11 @@ int fast_diag_count(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n, uin
 int launch_block_counts(lob_ctx* ctx, const double* u, int64_t lines, int64_t n, double eta,
                         int64_t* blocks, cudaStream_t s);
 
+// the reference's relaxed fast engine (relaxed.cu)
+size_t relaxed_workspace_bytes(int64_t lines, int64_t n);
+int launch_relaxed_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n, const double* ktab,
+                       int64_t ktab_stride, const int64_t* first, const double* tv, int64_t tv_stride, double eta,
+                       int64_t* blocks, void* workspace, size_t ws_bytes, cudaStream_t s);
 // weak-KAM consumers (weakkam.cu)
 int launch_tropical_gemm(lob_ctx* ctx, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                          int64_t ldc, int64_t m, int64_t n, int64_t k, cudaStream_t s);

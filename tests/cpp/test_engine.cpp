@@ -262,6 +262,26 @@ int main() {
         for (std::size_t i = 0; i < f2.size(); ++i) d = std::max(d, std::abs(f2.values[i] - s2.values[i]));
         CHECK(d <= 0.25 * 0.5 * 2.0 * 3.141592653589793 + 1e-9, "endpoint sampling error bound (%.3e)", d);
     }
+    // 9. GpuFast with eta > 0 is the reference's relaxed fast engine: an upper bound of the
+    //    exact minimum, equal to it at eta == 0 (proj/src/minplus.cpp:195-252)
+    {
+        const SchemeParams p = params_of(256, 0.05);
+        const KernelWindow k = build_kernel_mech(256, 0.05, 0.3);
+        const GridFn u = random_periodic(rng, 256, 0.01, p.epsilon());
+        int64_t b0 = 0, b1 = 0;
+        const GridFn ex = eng.kinetic_convolve(u, k, 0.0, ConvEngine::GpuFast, &b0);
+        const GridFn rx = eng.kinetic_convolve(u, k, 1e-2, ConvEngine::GpuFast, &b1);
+        bool ge = true, eq0 = true;
+        int strict = 0;
+        for (std::size_t j = 0; j < u.n(); ++j) {
+            const double want = def_min(u, k, static_cast<int64_t>(j));
+            eq0 = eq0 && ex.values[j] == want;
+            ge = ge && rx.values[j] >= want;
+            strict += rx.values[j] > want;
+        }
+        CHECK(eq0 && ge && strict > 0 && b1 >= 256 / 48, "relaxed engine: exact at eta 0, upper bound at eta > 0 (%d)",
+              strict);
+    }
     std::printf("%s: %d passed, %d failed\n", g_fail ? "FAIL" : "ALL PASS", g_pass, g_fail);
     return g_fail ? 1 : 0;
 }
