@@ -211,10 +211,10 @@ int lob_period_kinetic_host(const double* window, int64_t first, int64_t n, doub
 int lob_period_matrix_f64(lob_ctx* ctx, const double* kinc, const double* tvs, int64_t n,
                           int64_t ell, double* C, double* scratch, void* stream);
 
-/* eigenvalue_karp (proj/src/weakkam.cpp:160-189) of the device n x n matrix M;
- * synchronous, *lambda on the host.  LOB_INVALID_INPUT for n < 1 or a
- * non-finite entry. */
-int lob_eigenvalue_karp_f64(lob_ctx* ctx, const double* M, int64_t n, double* lambda);
+/* eigenvalue_karp (proj/src/weakkam.cpp:160-189) of the device n x n matrix M:
+ * runs on `stream` (after whatever produced M there) and synchronizes it;
+ * *lambda on the host.  LOB_INVALID_INPUT for n < 1 or a non-finite entry. */
+int lob_eigenvalue_karp_f64(lob_ctx* ctx, const double* M, int64_t n, double* lambda, void* stream);
 
 /* estimate_hbar_drift (proj/src/weakkam.cpp:43-86) for one periodic line of n
  * samples (host buffers): whole periods of ell = 1/tau fully discrete steps

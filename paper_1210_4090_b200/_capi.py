@@ -65,7 +65,7 @@ SIGNATURES = {
     "lob_minplus_gemm_f64": (c_int, [_P, _P, c_int64, _P, c_int64, _P, c_int64, c_int64, c_int64, c_int64, _P]),
     "lob_period_kinetic_host": (c_int, [_P, c_int64, c_int64, _P]),
     "lob_period_matrix_f64": (c_int, [_P, _P, _P, c_int64, c_int64, _P, _P, _P]),
-    "lob_eigenvalue_karp_f64": (c_int, [_P, _P, c_int64, POINTER(c_double)]),
+    "lob_eigenvalue_karp_f64": (c_int, [_P, _P, c_int64, POINTER(c_double), _P]),
     "lob_hbar_drift_host_f64": (c_int, [_P, _P, c_int64, c_double, c_double, _P, c_int64, c_int, c_int, c_double,
                                         POINTER(c_double), POINTER(c_double), POINTER(c_int64), POINTER(c_int),
                                         _P]),

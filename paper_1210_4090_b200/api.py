@@ -296,9 +296,9 @@ class Device:
                                             _ptr(scratch), _stream_ptr(stream))
         self._check(st, "lob_period_matrix_f64")
 
-    def eigenvalue_karp(self, m) -> float:
+    def eigenvalue_karp(self, m, stream=None) -> float:
         lam = ctypes.c_double()
-        st = self.lib.lob_eigenvalue_karp_f64(self.ctx, _ptr(m), m.shape[0], ctypes.byref(lam))
+        st = self.lib.lob_eigenvalue_karp_f64(self.ctx, _ptr(m), m.shape[0], ctypes.byref(lam), _stream_ptr(stream))
         self._check(st, "lob_eigenvalue_karp_f64")
         return lam.value
 

@@ -45,6 +45,13 @@ int lob_ctx_create(int device, lob_ctx** out) {
         return LOB_CUDA_ERROR;
     }
     cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+    // stream-ordered scratch (cudaMallocAsync) stays cached in the device's default pool
+    // instead of being returned to the driver at every synchronisation
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
         delete ctx;
         return LOB_CUDA_ERROR;

@@ -1038,6 +1038,8 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
 int fast_diag_count(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n, uint64_t* count,
                     cudaStream_t s) {
     const WsLayout w = ws_layout(lines, n);
+    // the counters are written by K2 launches on the caller's streams: wait for all of them
+    LOB_CUDA_TRY(ctx, cudaDeviceSynchronize());
     LOB_CUDA_TRY(ctx, cudaMemcpyAsync(count, static_cast<char*>(workspace) + w.diag,
                                       8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));

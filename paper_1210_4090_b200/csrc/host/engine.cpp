@@ -535,7 +535,7 @@ double Engine::eigenvalue_karp(const MinPlusMatrix& C) {
     DevBuf<double> dc(n * n);
     dc.upload(C.cost.data(), n * n);
     double lam = 0.0;
-    check_status(lob_eigenvalue_karp_f64(ctx_, dc.p, n, &lam), ctx_, "eigenvalue_karp");
+    check_status(lob_eigenvalue_karp_f64(ctx_, dc.p, n, &lam, nullptr), ctx_, "eigenvalue_karp");
     return lam;
 }
 

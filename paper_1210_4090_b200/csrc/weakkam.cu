@@ -18,6 +18,8 @@
 //
 // Roofline: the FP64 pipe, like K1 (DADD + DSETP + 2 FSEL per candidate; the
 // candidate ceiling measured by lob_bench_fp64).
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cmath>
 #include <string>
@@ -25,50 +27,57 @@
 
 #include "lob_internal.cuh"
 
+namespace cg = cooperative_groups;
+
 namespace lob {
 namespace {
 
-constexpr int kBM = 32, kBN = 32, kBK = 32;  // CTA tile of C and the contraction chunk
+constexpr int kBM = 64, kBN = 64, kBK = 16;  // CTA tile of C and the contraction chunk
 constexpr int kTT = 4;                       // outputs per thread per dimension
-constexpr int kGT = (kBM / kTT) * (kBN / kTT);  // 64 threads
+constexpr int kTX = kBN / kTT, kTY = kBM / kTT;
+constexpr int kGT = kTX * kTY;               // 256 threads
 
 __device__ __forceinline__ double pmin(double best, double c) { return c < best ? c : best; }
 
-// C[m x n] = A[m x k] (x) B[k x n]; row-major with leading dimensions.
-// Thread (tx, ty) owns rows ty + 8 i and columns tx + 8 j (i, j < 4).
+// C[m x n] = A[m x k] (x) B[k x n] over the contraction slice z in [z_begin, z_end) of
+// blockIdx.z (row-major, leading dimensions); the slice's partial minima go to
+// C + blockIdx.z * slice_stride.  Thread (tx, ty) owns rows ty + 16 i and columns
+// tx + 16 j (i, j < 4): per contraction index 4 + 4 shared loads feed 16 candidates.
 __global__ void __launch_bounds__(kGT) tropical_gemm_kernel(const double* __restrict__ A, int64_t lda,
                                                             const double* __restrict__ B, int64_t ldb,
                                                             double* __restrict__ C, int64_t ldc, int64_t m,
-                                                            int64_t n, int64_t k) {
+                                                            int64_t n, int64_t k, int64_t kslice,
+                                                            int64_t slice_stride) {
     __shared__ double As[kBK][kBM + 1];  // transposed: As[z][r]
     __shared__ double Bs[kBK][kBN];
-    const int tid = threadIdx.x, tx = tid % (kBN / kTT), ty = tid / (kBN / kTT);
+    const int tid = threadIdx.x, tx = tid % kTX, ty = tid / kTX;
     const int64_t r0 = static_cast<int64_t>(blockIdx.y) * kBM, c0 = static_cast<int64_t>(blockIdx.x) * kBN;
+    const int64_t zb = static_cast<int64_t>(blockIdx.z) * kslice, ze = min(k, zb + kslice);
     double acc[kTT][kTT];
 #pragma unroll
     for (int i = 0; i < kTT; ++i)
 #pragma unroll
         for (int j = 0; j < kTT; ++j) acc[i][j] = INFINITY;
-    for (int64_t z0 = 0; z0 < k; z0 += kBK) {
+    for (int64_t z0 = zb; z0 < ze; z0 += kBK) {
         // out-of-range operands are +inf: inf + x is inf or NaN, never "<" a best
         for (int e = tid; e < kBM * kBK; e += kGT) {
             const int r = e / kBK, z = e % kBK;  // consecutive threads: consecutive z (coalesced)
             const int64_t gr = r0 + r, gz = z0 + z;
-            As[z][r] = (gr < m && gz < k) ? __ldg(A + gr * lda + gz) : INFINITY;
+            As[z][r] = (gr < m && gz < ze) ? __ldg(A + gr * lda + gz) : INFINITY;
         }
         for (int e = tid; e < kBK * kBN; e += kGT) {
             const int z = e / kBN, c = e % kBN;
             const int64_t gz = z0 + z, gc = c0 + c;
-            Bs[z][c] = (gz < k && gc < n) ? __ldg(B + gz * ldb + gc) : INFINITY;
+            Bs[z][c] = (gz < ze && gc < n) ? __ldg(B + gz * ldb + gc) : INFINITY;
         }
         __syncthreads();
 #pragma unroll 4
         for (int z = 0; z < kBK; ++z) {
             double a[kTT], b[kTT];
 #pragma unroll
-            for (int i = 0; i < kTT; ++i) a[i] = As[z][ty + 8 * i];
+            for (int i = 0; i < kTT; ++i) a[i] = As[z][ty + kTY * i];
 #pragma unroll
-            for (int j = 0; j < kTT; ++j) b[j] = Bs[z][tx + 8 * j];
+            for (int j = 0; j < kTT; ++j) b[j] = Bs[z][tx + kTX * j];
 #pragma unroll
             for (int i = 0; i < kTT; ++i)
 #pragma unroll
@@ -76,13 +85,25 @@ __global__ void __launch_bounds__(kGT) tropical_gemm_kernel(const double* __rest
         }
         __syncthreads();
     }
+    double* Cs = C + blockIdx.z * slice_stride;
 #pragma unroll
     for (int i = 0; i < kTT; ++i)
 #pragma unroll
         for (int j = 0; j < kTT; ++j) {
-            const int64_t gr = r0 + ty + 8 * i, gc = c0 + tx + 8 * j;
-            if (gr < m && gc < n) C[gr * ldc + gc] = acc[i][j];
+            const int64_t gr = r0 + ty + kTY * i, gc = c0 + tx + kTX * j;
+            if (gr < m && gc < n) Cs[gr * ldc + gc] = acc[i][j];
         }
+}
+
+// split contraction: C = ordered min over the slices (slice order = contraction
+// order, strict "<": the first minimum wins exactly as in one sequential loop)
+__global__ void tropical_combine_kernel(const double* __restrict__ P, int slices, int64_t m, int64_t n,
+                                        double* __restrict__ C, int64_t ldc) {
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= m * n) return;
+    double best = P[e];
+    for (int s = 1; s < slices; ++s) best = pmin(best, P[s * m * n + e]);
+    C[(e / n) * ldc + e % n] = best;
 }
 
 // out[x] = min_y v[y] + M[y][x] (n x n): 32 columns per CTA, 8 warps each
@@ -106,6 +127,68 @@ __global__ void __launch_bounds__(32 * kVW) tropical_gemv_kernel(const double* _
 #pragma unroll
         for (int q = 1; q < kVW; ++q) b = pmin(b, part[q][lane]);
         out[x] = b;
+    }
+}
+
+// Karp's n sequential vector x matrix products in ONE launch: a 16-CTA thread-block
+// cluster keeps C resident in shared memory (CTA c holds columns [32c, 32c + 32),
+// n <= 512 -> <= 128 KB), computes its 32 entries of D[k] (8 warps over contiguous
+// row ranges, combined in row order), broadcasts them into every peer's next-row
+// buffer through distributed shared memory and meets the others at the hardware
+// cluster barrier; rows of D go to global memory for the final reduction.
+constexpr int kKC = 16;   // CTAs per cluster (non-portable size, B200 allows 16)
+constexpr int kKW = 32;   // columns per CTA
+constexpr int kKNmax = kKC * kKW;
+constexpr int kKWarps = 8;  // row ranges per step; each warp splits its range in kKAcc contiguous parts
+constexpr int kKAcc = 2;
+constexpr int kKParts = kKWarps * kKAcc;
+__global__ void __launch_bounds__(32 * kKWarps, 1) karp_cluster_kernel(const double* __restrict__ M, int n,
+                                                                       double* __restrict__ D) {
+    extern __shared__ __align__(16) double ksm[];
+    double* Cs = ksm;                      // [n][kKW] column block of C
+    double* Db = Cs + n * kKW;             // [2][kKNmax] current / next row of D
+    double* part = Db + 2 * kKNmax;        // [kKParts][kKW]
+    cg::cluster_group cluster = cg::this_cluster();
+    const int c = static_cast<int>(cluster.block_rank());
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int x = c * kKW + lane;
+    for (int e = threadIdx.x; e < n * kKW; e += blockDim.x) {
+        const int y = e / kKW, cc = c * kKW + e % kKW;
+        Cs[e] = cc < n ? M[static_cast<int64_t>(y) * n + cc] : INFINITY;
+    }
+    for (int e = threadIdx.x; e < n; e += blockDim.x) Db[e] = e == 0 ? 0.0 : INFINITY;  // D[0]
+    if (c == 0)
+        for (int e = threadIdx.x; e < n; e += blockDim.x) D[e] = e == 0 ? 0.0 : INFINITY;
+    cluster.sync();
+    // part q = kKAcc * w + a covers rows [q * per, (q + 1) * per): independent min chains,
+    // combined in row order (first minimum wins, as in one sequential loop)
+    const int per = (n + kKParts - 1) / kKParts;
+    for (int k = 1; k <= n; ++k) {
+        const double* cur = Db + ((k - 1) & 1) * kKNmax;
+        double best[kKAcc];
+#pragma unroll
+        for (int a = 0; a < kKAcc; ++a) best[a] = INFINITY;
+        for (int t = 0; t < per; ++t) {
+#pragma unroll
+            for (int a = 0; a < kKAcc; ++a) {
+                const int y = (kKAcc * w + a) * per + t;
+                if (y < n) best[a] = pmin(best[a], __dadd_rn(cur[y], Cs[y * kKW + lane]));
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < kKAcc; ++a) part[(kKAcc * w + a) * kKW + lane] = best[a];
+        __syncthreads();
+        if (w == 0) {
+            double b = part[lane];
+            for (int q = 1; q < kKParts; ++q) b = pmin(b, part[q * kKW + lane]);
+            if (x < n) {
+                D[static_cast<int64_t>(k) * n + x] = b;
+                // broadcast into every CTA's next row (distributed shared memory)
+                double* nxt = Db + (k & 1) * kKNmax;
+                for (int r = 0; r < kKC; ++r) *cluster.map_shared_rank(nxt + x, r) = b;
+            }
+        }
+        cluster.sync();
     }
 }
 
@@ -167,9 +250,26 @@ int launch_tropical_gemm(lob_ctx* ctx, const double* A, int64_t lda, const doubl
     if (m == 0 || n == 0) return LOB_OK;
     const int64_t gx = (n + kBN - 1) / kBN, gy = (m + kBM - 1) / kBM;
     if (gx > 0x7fffffffll || gy > 65535) return set_error(ctx, LOB_INVALID_INPUT, "minplus_gemm: too large");
-    tropical_gemm_kernel<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy)), kGT, 0, s>>>(
-        A, lda, B, ldb, C, ldc, m, n, k);
-    ctx->launches += 1;
+    // split the contraction when the output tiles alone cannot fill ~4 CTAs per SM
+    // (keeping >= 4 chunks per slice); partial minima are combined in slice order
+    const int64_t tiles = gx * gy, chunks = (k + kBK - 1) / kBK;
+    int64_t slices = std::min<int64_t>((4 * ctx->sm_count + tiles - 1) / tiles, std::max<int64_t>(1, chunks / 4));
+    slices = std::max<int64_t>(1, std::min<int64_t>(slices, 64));
+    const int64_t kslice = ((chunks + slices - 1) / slices) * kBK;
+    slices = k > 0 ? (k + kslice - 1) / kslice : 1;
+    const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy), static_cast<unsigned>(slices));
+    if (slices == 1) {
+        tropical_gemm_kernel<<<grid, kGT, 0, s>>>(A, lda, B, ldb, C, ldc, m, n, k, k > 0 ? k : 1, 0);
+        ctx->launches += 1;
+        return cuda_status(ctx, cudaGetLastError(), "minplus_gemm");
+    }
+    double* P = nullptr;
+    LOB_CUDA_TRY(ctx, cudaMallocAsync(&P, static_cast<size_t>(slices) * m * n * sizeof(double), s));
+    tropical_gemm_kernel<<<grid, kGT, 0, s>>>(A, lda, B, ldb, P, n, m, n, k, kslice, m * n);
+    tropical_combine_kernel<<<static_cast<unsigned>((m * n + 255) / 256), 256, 0, s>>>(P, static_cast<int>(slices),
+                                                                                       m, n, C, ldc);
+    ctx->launches += 2;
+    cudaFreeAsync(P, s);
     return cuda_status(ctx, cudaGetLastError(), "minplus_gemm");
 }
 
@@ -177,12 +277,45 @@ int launch_karp(lob_ctx* ctx, const double* M, int64_t n, double* D, double* lam
                 cudaStream_t s) {
     const unsigned g = static_cast<unsigned>(std::min<int64_t>((n * n + 255) / 256, 4096));
     nonfinite_kernel<<<g, 256, 0, s>>>(M, n * n, flag);
-    karp_init_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(D, n);
-    ctx->launches += 2;
-    const unsigned gv = static_cast<unsigned>((n + 31) / 32);
-    for (int64_t k = 1; k <= n; ++k) {
-        tropical_gemv_kernel<<<gv, 32 * kVW, 0, s>>>(D + (k - 1) * n, M, n, D + k * n);
+    ctx->launches += 1;
+    bool clustered = false;
+    if (n <= kKNmax) {
+        const size_t smem = (static_cast<size_t>(n) * kKW + 2 * kKNmax + kKParts * kKW) * sizeof(double);
+        if (first_time(ctx, reinterpret_cast<const void*>(&karp_cluster_kernel))) {
+            cudaFuncSetAttribute(karp_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            cudaFuncSetAttribute(karp_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>((static_cast<size_t>(kKNmax) * kKW + 2 * kKNmax + kKParts * kKW) *
+                                                  sizeof(double)));
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(kKC);
+        cfg.blockDim = dim3(32 * kKWarps);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = kKC;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int clusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&clusters, karp_cluster_kernel, &cfg) == cudaSuccess && clusters > 0) {
+            LOB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, karp_cluster_kernel, M, static_cast<int>(n), D));
+            ctx->launches += 1;
+            clustered = true;
+        } else {
+            cudaGetLastError();  // cluster launch unavailable: the launch loop below
+        }
+    }
+    if (!clustered) {
+        karp_init_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(D, n);
         ctx->launches += 1;
+        const unsigned gv = static_cast<unsigned>((n + 31) / 32);
+        for (int64_t k = 1; k <= n; ++k) {
+            tropical_gemv_kernel<<<gv, 32 * kVW, 0, s>>>(D + (k - 1) * n, M, n, D + k * n);
+            ctx->launches += 1;
+        }
     }
     // worst_v scratch: after the (n+1) x n table
     karp_final_kernel<<<1, 512, 0, s>>>(D, n, D + (n + 1) * n, lambda_dev);
@@ -348,10 +481,10 @@ int lob_period_matrix_f64(lob_ctx* ctx, const double* kinc, const double* tvs, i
     return launch_period_matrix(ctx, kinc, tvs, n, ell, C, scratch, static_cast<cudaStream_t>(stream));
 }
 
-int lob_eigenvalue_karp_f64(lob_ctx* ctx, const double* M, int64_t n, double* lambda) {
+int lob_eigenvalue_karp_f64(lob_ctx* ctx, const double* M, int64_t n, double* lambda, void* stream) {
     if (!ctx || !lambda) return LOB_INVALID_INPUT;
     if (n < 1) return set_error(ctx, LOB_INVALID_INPUT, "eigenvalue_karp: empty matrix");
-    cudaStream_t s = ctx->stream;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);  // ordered after the producer of M
     double* D = nullptr;
     int* flag = nullptr;
     LOB_CUDA_TRY(ctx, cudaMallocAsync(&D, ((n + 2) * n + 1) * sizeof(double), s));

@@ -128,7 +128,7 @@ def tie_heavy(rng, shape):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n", [1, 12, 31, 64, 200, 512])
+@pytest.mark.parametrize("n", [1, 12, 31, 64, 200, 512, 700])
 def test_minplus_product_equals_reference(dev, ref, n):
     rng = np.random.default_rng(52 + n)
     for a, b in [(rng.uniform(-1, 1, (n, n)), rng.uniform(-1, 1, (n, n))),
@@ -212,7 +212,7 @@ def test_karp_known_answers_and_errors(dev, ref):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n,reps", [(1, 3), (8, 25), (33, 4), (128, 2), (512, 1)])
+@pytest.mark.parametrize("n,reps", [(1, 3), (8, 25), (33, 4), (128, 2), (512, 1), (600, 1)])
 def test_karp_equals_reference(dev, ref, n, reps):
     rng = np.random.default_rng(53 + n)
     for _ in range(reps):
