@@ -146,6 +146,12 @@ int lob_split_step_2d_f64(lob_ctx* ctx, const double* u, double* out, double* tm
                           const double* a2, double b, int engine, void* workspace,
                           size_t workspace_bytes, void* stream);
 
+/* The potential pass of K3 on a rows x n row slab (the multi-GPU split step's
+ * rows [r0, r0 + rows) of an n x n tensor): out[i][k] -= tau*(a1[i]*a2[k] + b),
+ * each product / sum one IEEE rounding (a1 points at the slab's first row). */
+int lob_potential2d_rows_f64(lob_ctx* ctx, double* out, int64_t rows, int64_t n, const double* a1,
+                             const double* a2, double b, double tau, void* stream);
+
 /* Device-resident batched evolve (proj/src/scheme.cpp:208-272): `steps`
  * steps of `lines` periodic lines with a shared, time-independent tv.  u is
  * updated in place (double-buffered against `scratch`, n*lines doubles).

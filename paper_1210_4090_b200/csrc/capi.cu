@@ -482,5 +482,12 @@ int lob_step_host_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines,
     return LOB_OK;
 }
 
-}  // extern "C"
+int lob_potential2d_rows_f64(lob_ctx* ctx, double* out, int64_t rows, int64_t n, const double* a1,
+                             const double* a2, double b, double tau, void* stream) {
+    if (!ctx) return LOB_INVALID_INPUT;
+    if (rows < 0 || n < 1 || !a1 || !a2)
+        return set_error(ctx, LOB_INVALID_INPUT, "lob_potential2d_rows_f64: bad arguments");
+    return launch_potential2d(ctx, out, a1, a2, b, tau, n, static_cast<cudaStream_t>(stream), rows);
+}
 
+}  // extern "C"

@@ -139,7 +139,7 @@ int launch_period_matrix(lob_ctx* ctx, const double* kinc, const double* tvs, in
 
 int launch_transpose(lob_ctx* ctx, const double* src, double* dst, int64_t n, cudaStream_t s);
 int launch_potential2d(lob_ctx* ctx, double* out, const double* a1, const double* a2, double b,
-                       double tau, int64_t n, cudaStream_t s);
+                       double tau, int64_t n, cudaStream_t s, int64_t rows = -1);
 int launch_drift(lob_ctx* ctx, const double* nxt, const double* cur, int64_t lines, int64_t n,
                  double* drift_out, int* halt, int step, cudaStream_t s);
 

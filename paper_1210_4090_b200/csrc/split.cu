@@ -34,12 +34,13 @@ __global__ void __launch_bounds__(256) transpose_kernel(const double* __restrict
     }
 }
 
+// rows x n block (rows = n for the whole tensor; a row slab of it for the multi-GPU step)
 __global__ void __launch_bounds__(256) potential2d_kernel(double* __restrict__ out,
                                                           const double* __restrict__ a1,
                                                           const double* __restrict__ a2, double b,
-                                                          double tau, int64_t n) {
+                                                          double tau, int64_t n, int64_t rows) {
     const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= n * n) return;
+    if (idx >= rows * n) return;
     const int64_t i = idx / n, k = idx - i * n;
     // V = a1*a2 + b; out -= tau*V   (no contraction)
     const double v = __dadd_rn(__dmul_rn(a1[i], a2[k]), b);
@@ -85,10 +86,12 @@ int launch_transpose(lob_ctx* ctx, const double* src, double* dst, int64_t n, cu
 }
 
 int launch_potential2d(lob_ctx* ctx, double* out, const double* a1, const double* a2, double b,
-                       double tau, int64_t n, cudaStream_t s) {
-    const int64_t total = n * n;
+                       double tau, int64_t n, cudaStream_t s, int64_t rows) {
+    if (rows < 0) rows = n;
+    const int64_t total = rows * n;
+    if (total == 0) return LOB_OK;
     potential2d_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(out, a1, a2, b,
-                                                                                  tau, n);
+                                                                                  tau, n, rows);
     ctx->launches += 1;
     return cuda_status(ctx, cudaGetLastError(), "potential2d_kernel");
 }

@@ -1,0 +1,101 @@
+"""Multi-GPU 2-D dimension splitting (SURVEY.md §8(e), config C4 sharded by rows).
+
+One process per GPU; the n x n state is partitioned into equal row slabs
+(rank r holds rows [r*b, (r+1)*b), b = n / world).  The reference's split step
+(proj/src/splitting.cpp:37-99) sweeps axis 0 (columns: whole columns are
+needed, the window spans two periods), then axis 1 (rows: local), then
+subtracts tau*V once.  Per step:
+
+    slab of U  --all-to-all transpose-->  slab of U^T  --K1/K2 row sweep (kernel 1)-->
+    --all-to-all transpose back-->  slab  --K1/K2 row sweep (kernel 2)-->  - tau*V (row slab)
+
+i.e. two exchanges of the whole tensor per step (``torch.distributed.all_to_all_single``,
+NCCL over NVLink/NVSwitch on the GPU box), each carrying (world-1)/world of the state;
+the sweeps and the potential are the same device kernels as the single-GPU
+``lob_split_step_2d_f64``, with the same IEEE operations, so every rank's slab equals the
+corresponding rows of the single-GPU step bit for bit.
+
+The exchange (``transpose_slabs``) is pure data movement; it is tested with
+world_size 2 over gloo on CPU (tests/test_dist_cpu.py) and composed with the CUDA
+kernels in ``split_step_2d_dist``.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _capi
+from .api import ENGINE_DIRECT, ENGINE_FAST, Device, InvalidInput, _ptr, _stream_ptr
+
+
+def _world(group):
+    import torch.distributed as dist
+
+    if not dist.is_available() or not dist.is_initialized():
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
+def transpose_slabs(x, group=None):
+    """x: this rank's row slab (b x n, contiguous) of a row-partitioned n x n matrix X
+    (b = n / world).  Returns this rank's row slab of X^T:
+    y[c][p*b + i] = X[p*b + i][r*b + c]."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank = _world(group)
+    b, n = x.shape
+    if b * world != n:
+        raise InvalidInput("transpose_slabs: the row slabs must partition the square evenly")
+    if world == 1:
+        return x.t().contiguous()
+    # block q of the send buffer = X[rank rows][q cols]^T : send[q][c][i] = x[i][q*b + c]
+    send = x.view(b, world, b).permute(1, 2, 0).contiguous()
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv, send, group=group)
+    # recv[p][c][i] = X[p*b + i][rank*b + c]  ->  y[c][p*b + i]
+    return recv.permute(1, 0, 2).reshape(b, n).contiguous()
+
+
+def split_step_2d_dist(dev: Device, u_slab, tau: float, drift1: float, drift2: float, a1=None, a2=None,
+                       b: float = 0.0, engine: int = ENGINE_DIRECT, group=None, workspaces=None):
+    """One split step of the row-partitioned periodic n x n tensor (this rank's slab,
+    rows [r*b, (r+1)*b) as a torch CUDA tensor).  a1 (length n, the x1 factor of the whole
+    grid) and a2 (length n) describe V = a1(x1) a2(x2) + b at the step's sampling time,
+    like lob_split_step_2d_f64.  Returns the new slab."""
+    import torch
+
+    world, rank = _world(group)
+    bl, n = u_slab.shape
+    if bl * world != n:
+        raise InvalidInput("split_step_2d_dist: rows per rank must be n / world")
+    if engine not in (ENGINE_DIRECT, ENGINE_FAST):
+        raise InvalidInput("split_step_2d_dist: engine must be ENGINE_DIRECT or ENGINE_FAST")
+
+    def sweep(src, drift, key):
+        out = torch.empty_like(src)
+        if engine == ENGINE_FAST:
+            ws = None if workspaces is None else workspaces.get(key)
+            if ws is None:
+                ws = torch.empty(dev.fast_workspace_bytes(bl, n), dtype=torch.uint8, device=src.device)
+                if workspaces is not None:
+                    workspaces[key] = ws
+            d = torch.full((bl,), drift, dtype=torch.float64, device=src.device)
+            dev.fast_f64(src, out, d, tau, workspace=ws)
+        else:
+            k = dev.build_kernel(n, tau, drift)
+            kt = torch.from_numpy(k.window).to(src.device)
+            fr = torch.full((bl,), k.first, dtype=torch.int64, device=src.device)
+            dev.direct_f64(src, out, kt, fr)
+        return out
+
+    t = transpose_slabs(u_slab, group)          # slab of U^T: columns of U as rows
+    t = sweep(t, drift1, "axis0")               # axis 0 (kernel 1)
+    v = transpose_slabs(t, group)               # back to rows
+    w = sweep(v, drift2, "axis1")               # axis 1 (kernel 2)
+    if a1 is not None:
+        a1d = torch.as_tensor(np.ascontiguousarray(a1[rank * bl:(rank + 1) * bl]), device=w.device)
+        a2d = torch.as_tensor(np.ascontiguousarray(a2), device=w.device)
+        st = dev.lib.lob_potential2d_rows_f64(dev.ctx, _ptr(w), bl, n, _ptr(a1d), _ptr(a2d), float(b), float(tau),
+                                              _stream_ptr(None))
+        _capi.check(st, dev.ctx, "lob_potential2d_rows_f64")
+    return w

@@ -55,3 +55,48 @@ def test_bench_reference_arm_two_ranks():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "updates/s"
+
+
+def _transpose_worker(rank, world, port, q, n):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    sys.path.insert(0, ROOT)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1210_4090_b200.dist import transpose_slabs
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    X = np.arange(n * n, dtype=np.float64).reshape(n, n) * 1.5 - 7.0
+    b = n // world
+    x = torch.from_numpy(X[rank * b:(rank + 1) * b].copy())
+    y = transpose_slabs(x)
+    z = transpose_slabs(y)  # back
+    q.put((rank, y.numpy(), z.numpy()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 8), (2, 12), (4, 16)])
+def test_all_to_all_transpose_of_row_slabs_gloo(world, n):
+    """The C4 multi-GPU exchange (paper_1210_4090_b200/dist.py): every rank's slab of the
+    all-to-all transpose is the matching rows of X^T, and transposing twice is the identity."""
+    import numpy as np
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29541 + world + n
+    procs = [ctx.Process(target=_transpose_worker, args=(r, world, port, q, n)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in procs:
+        r, y, z = q.get(timeout=180)
+        res[r] = (y, z)
+    for p in procs:
+        p.join(timeout=60)
+    X = np.arange(n * n, dtype=np.float64).reshape(n, n) * 1.5 - 7.0
+    b = n // world
+    for r in range(world):
+        assert np.array_equal(res[r][0], X.T[r * b:(r + 1) * b])
+        assert np.array_equal(res[r][1], X[r * b:(r + 1) * b])
