@@ -45,50 +45,62 @@ __device__ __forceinline__ double vpot(const SemiPot& P, int r, double x) {
     return __dadd_rn(P.offset, __dmul_rn(P.am[r], cos(__dmul_rn(P.freq, theta(x)))));
 }
 
-__global__ void __launch_bounds__(128) semidiscrete_kernel(const double* __restrict__ u, double* __restrict__ out,
-                                                           int64_t m, int64_t n, int periodic, double origin,
-                                                           double step, const double* __restrict__ ktab,
-                                                           int64_t first, double tau, int q, SemiPot P,
-                                                           int* __restrict__ err) {
+// CTA = 32 consecutive outputs x kParts contiguous parts of the window (one warp per
+// part, lanes = outputs: coalesced u reads); the parts' minima are combined in window
+// order with a strict "<" (the reference's first minimum wins).
+constexpr int kParts = 4;
+__global__ void __launch_bounds__(32 * kParts) semidiscrete_kernel(
+    const double* __restrict__ u, double* __restrict__ out, int64_t m, int64_t n, int periodic, double origin,
+    double step, const double* __restrict__ ktab, int64_t first, double tau, int q, SemiPot P,
+    int* __restrict__ err) {
+    __shared__ double part[kParts][32];
     const int64_t line = blockIdx.y;
-    const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (j >= m) return;
+    const int lane = threadIdx.x & 31, pw = threadIdx.x >> 5;
+    const int64_t j = static_cast<int64_t>(blockIdx.x) * 32 + lane;
     const double* ul = u + line * m;
-    // sample_coord (proj/src/scheme.cpp:32-35)
-    int64_t jc = j;
-    if (periodic && jc >= n) jc -= n * (jc / n);
-    const double x = __dadd_rn(origin, __dmul_rn(static_cast<double>(jc), step));
-    const double vx = vpot(P, q, x);  // V(t + tau, x)
-    const double tq = __ddiv_rn(tau, static_cast<double>(q));
     const int64_t W = 2 * n + 1;
+    const int64_t per = (W + kParts - 1) / kParts;
+    const int64_t w0 = pw * per, w1 = min(W, w0 + per);
     double best = INFINITY;
-    for (int64_t w = 0; w < W; ++w) {
-        const int64_t d = first + w;
-        int64_t src = j - d;
-        if (periodic) {
-            src %= n;
-            if (src < 0) src += n;
-        } else if (src < 0 || src >= m) {
-            continue;
-        }
-        const double y = __dsub_rn(x, __dmul_rn(static_cast<double>(d), step));
-        double acc = __dmul_rn(0.5, __dadd_rn(vpot(P, 0, y), vx));
-        if (P.kind != LOB_POTENTIAL_ZERO) {
-            const double xy = __dsub_rn(x, y);
-            for (int r = 1; r < q; ++r) {
-                const double frac = __ddiv_rn(static_cast<double>(r), static_cast<double>(q));
-                acc = __dadd_rn(acc, vpot(P, r, __dadd_rn(y, __dmul_rn(frac, xy))));
+    if (j < m) {
+        // sample_coord (proj/src/scheme.cpp:32-35)
+        int64_t jc = j;
+        if (periodic && jc >= n) jc -= n * (jc / n);
+        const double x = __dadd_rn(origin, __dmul_rn(static_cast<double>(jc), step));
+        const double vx = vpot(P, q, x);  // V(t + tau, x)
+        const double tq = __ddiv_rn(tau, static_cast<double>(q));
+        for (int64_t w = w0; w < w1; ++w) {
+            const int64_t d = first + w;
+            int64_t src = j - d;
+            if (periodic) {
+                src %= n;
+                if (src < 0) src += n;
+            } else if (src < 0 || src >= m) {
+                continue;
             }
-        } else {
-            for (int r = 1; r < q; ++r) acc = __dadd_rn(acc, 0.0);
+            const double y = __dsub_rn(x, __dmul_rn(static_cast<double>(d), step));
+            double acc = __dmul_rn(0.5, __dadd_rn(vpot(P, 0, y), vx));
+            if (P.kind != LOB_POTENTIAL_ZERO) {
+                const double xy = __dsub_rn(x, y);
+                for (int r = 1; r < q; ++r) {
+                    const double frac = __ddiv_rn(static_cast<double>(r), static_cast<double>(q));
+                    acc = __dadd_rn(acc, vpot(P, r, __dadd_rn(y, __dmul_rn(frac, xy))));
+                }
+            }
+            const double integral = __dmul_rn(tq, acc);
+            const double cost = __dsub_rn(__ldg(ktab + w), integral);
+            const double c = __dadd_rn(__ldg(ul + src), cost);
+            best = c < best ? c : best;  // std::min(best, c)
         }
-        const double integral = __dmul_rn(tq, acc);
-        const double cost = __dsub_rn(__ldg(ktab + w), integral);
-        const double c = __dadd_rn(__ldg(ul + src), cost);
-        best = c < best ? c : best;  // std::min(best, c)
     }
-    if (best == INFINITY) atomicOr(err, 1);
-    out[line * m + j] = best;
+    part[pw][lane] = best;
+    __syncthreads();
+    if (pw == 0 && j < m) {
+#pragma unroll
+        for (int k = 1; k < kParts; ++k) best = part[k][lane] < best ? part[k][lane] : best;
+        if (best == INFINITY) atomicOr(err, 1);
+        out[line * m + j] = best;
+    }
 }
 
 }  // namespace
@@ -135,9 +147,9 @@ extern "C" int lob_step_semidiscrete_f64(lob_ctx* ctx, const double* u, double* 
     LOB_CUDA_TRY(ctx, cudaMallocAsync(&err, sizeof(int), s));
     LOB_CUDA_TRY(ctx, cudaMemsetAsync(err, 0, sizeof(int), s));
     const double step = 1.0 / static_cast<double>(n_space);
-    const dim3 grid(static_cast<unsigned>((m + 127) / 128), static_cast<unsigned>(lines));
+    const dim3 grid(static_cast<unsigned>((m + 31) / 32), static_cast<unsigned>(lines));
     if (lines > 65535) return set_error(ctx, LOB_INVALID_INPUT, "step_semidiscrete: at most 65535 lines");
-    semidiscrete_kernel<<<grid, 128, 0, s>>>(u, out, m, n_space, periodic, origin, step, ktab, first, tau,
+    semidiscrete_kernel<<<grid, 32 * kParts, 0, s>>>(u, out, m, n_space, periodic, origin, step, ktab, first, tau,
                                              quad_points, P, err);
     ctx->launches += 1;
     int herr = 0;

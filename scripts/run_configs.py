@@ -273,9 +273,14 @@ def main():
     args = ap.parse_args()
     dev = api.Device(0)
     doc = {"device": torch.cuda.get_device_name(0), "hbm_peak_gbs": HBM}
+    from bench import ClockSampler
+
     for name in args.only.split(","):
         t0 = time.perf_counter()
+        clk = ClockSampler(0)
+        clk.start()
         doc[name] = globals()[name](dev)
+        doc[name]["clocks"] = clk.stop()
         doc[name]["wall_s"] = time.perf_counter() - t0
         print(name, json.dumps(doc[name])[:600], flush=True)
     with open(args.out, "w") as f:
