@@ -317,6 +317,24 @@ int lob_evolve_f64(lob_ctx* ctx, double* u, double* scratch, int64_t lines, int6
     LOB_CUDA_TRY(ctx, cudaMallocAsync(&halt, sizeof(int), s));
     const int big = 0x7fffffff;
     LOB_CUDA_TRY(ctx, cudaMemcpyAsync(halt, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+    if (engine == LOB_ENGINE_FAST && fast_resident_ok(n)) {
+        // short lines: every step in one launch, the lines resident in shared memory (K2R)
+        void* lcb = nullptr;
+        LOB_CUDA_TRY(ctx, cudaMallocAsync(&lcb, static_cast<size_t>(lines) * 64, s));
+        st = launch_fast_resident_f64(ctx, u, lines, n, drift, tau, tv, tv_stride, eta, steps, step_drift,
+                                      step_blocks, halt, lcb, s);
+        int hstep = big;
+        if (st == LOB_OK)
+            LOB_CUDA_TRY(ctx, cudaMemcpyAsync(&hstep, halt, sizeof(int), cudaMemcpyDeviceToHost, s));
+        cudaFreeAsync(lcb, s);
+        cudaFreeAsync(halt, s);
+        LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+        if (st) return st;
+        if (completed_steps) *completed_steps = hstep != big ? hstep + 1 : steps;
+        if (hstep != big)
+            return set_error(ctx, LOB_EVALUATION_ERROR, "non-finite value after step " + std::to_string(hstep + 1));
+        return LOB_OK;
+    }
     double* cur = u;
     double* nxt = scratch;
     int64_t done = 0;

@@ -38,6 +38,7 @@
 //    statistics of u^{n+1} for the next step, including decompose()'s block
 //    count (proj/src/minplus.cpp:152-188) as a composable 3-state
 //    transition summary per tile.
+#include <algorithm>
 #include <climits>
 #include <cmath>
 #include <cstring>
@@ -839,6 +840,183 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
     }
 }
 
+
+// ---- K2R: resident evolve for short lines --------------------------------
+// One CTA per line keeps the line in shared memory for ALL steps of an evolve
+// call (C1: 2000 steps of n = 1024 in one launch instead of 2000 launch-bound
+// steps).  Each step is the K2 walk with every source of the line scanned (no
+// tile statistics are needed: the whole line is resident), the oscillation
+// gate from a block reduction of the slope extremes, the exact direct scan for
+// any output the walk missed (never when the gate holds), the potential, the
+// per-step drift (block tree sum, <= 1e-12 vs the reference's sequential sum)
+// and decompose()'s block count of the step's input (the FSM of
+// proj/src/minplus.cpp:161-187, per-thread segments composed in order).
+constexpr int kRT = 512;  // max threads per resident CTA
+constexpr int kResidentMaxN = 4096;  // shared memory: two line buffers, the keys, the K table (40 n bytes)
+
+struct ResidentShared {
+    double red[2][kRT / 32];
+    unsigned long long fsm[kRT / 32];
+    int flag;
+};
+
+__global__ void __launch_bounds__(kRT) resident_kernel(double* __restrict__ u, int n, const LineConst* __restrict__ lcs,
+                                                       FastParams p, const double* __restrict__ tv, int64_t tv_stride,
+                                                       int steps, double* __restrict__ step_drift,
+                                                       int64_t* __restrict__ step_blocks, int64_t lines,
+                                                       int* __restrict__ halt) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* U0 = reinterpret_cast<double*>(smem_raw);
+    double* U1 = U0 + n;
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(U1 + n);
+    double* Ks = reinterpret_cast<double*>(keys + n);  // K(first + w), w = 0..2n: the step's fixed table
+    __shared__ ResidentShared R;
+    const int64_t line = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nt = blockDim.x, nw = nt >> 5;  // <= kRT
+    const LineConst lc = lcs[line];
+    const int first = static_cast<int>(lc.first);
+    const int dmin_w = first + 1, dmax_w = first + 2 * n - 1;
+    const double ia = p.ia, hl = lc.hl, hr = lc.hr, tau = p.tau;
+    const double* tvl = tv ? tv + line * tv_stride : nullptr;
+    double* ul = u + line * n;
+    for (int j = tid; j < n; j += nt) U0[j] = ul[j];
+    for (int w = tid; w <= 2 * n; w += nt) Ks[w] = kval(p.vtab, p.vofs, first + w, lc.drift, tau);
+    const double* Kd = Ks - first;  // Kd[d] = K(d)
+    // thread t's contiguous segment of sources / increments
+    const int seg = (n + nt - 1) / nt, sa = min(n, tid * seg), sb = min(n, sa + seg);
+    const bool exact_cmp = p.eta == 0.0;
+    int k = 0;
+    for (; k < steps; ++k) {
+        double* cur = (k & 1) ? U1 : U0;
+        double* nxt = (k & 1) ? U0 : U1;
+        __syncthreads();
+        // slope extremes (gate) and the FSM summary of this thread's increments
+        double smn = INFINITY, smx = -INFINITY;
+        int v = 0 | (1 << 2) | (2 << 4);
+        int cnt[3] = {0, 0, 0};
+        double sprev = 0.0;
+        for (int y = sa; y < sb; ++y) {
+            const double s = __dsub_rn(cur[y + 1 == n ? 0 : y + 1], cur[y]);
+            smn = fmin(smn, s);
+            smx = fmax(smx, s);
+            if (step_blocks) {
+                if (y == sa) sprev = y > 0 ? __dsub_rn(cur[y], cur[y - 1]) : 0.0;
+                if (y >= 1) {  // increment e = y: s(y) - s(y-1), e in [1, n-1]
+                    int c;
+                    if (exact_cmp) c = s > sprev ? 0 : (s < sprev ? 1 : 2);
+                    else {
+                        const double inc = __dsub_rn(s, sprev);
+                        c = inc > p.eta ? 0 : (inc < -p.eta ? 1 : 2);
+                    }
+                    int nv = 0;
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {
+                        int e;
+                        const int st = fsm_next((v >> (2 * q)) & 3, c, &e);
+                        nv |= st << (2 * q);
+                        cnt[q] += e;
+                    }
+                    v = nv;
+                }
+                sprev = s;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            smn = fmin(smn, __shfl_xor_sync(0xffffffffu, smn, o));
+            smx = fmax(smx, __shfl_xor_sync(0xffffffffu, smx, o));
+        }
+        if (step_blocks) {
+            const unsigned long long f = warp_fsm(fsm_pack(v, cnt));
+            if (lane == 0) R.fsm[warp] = f;
+        }
+        if (lane == 0) {
+            R.red[0][warp] = smn;
+            R.red[1][warp] = smx;
+        }
+        for (int j = tid; j < n; j += nt) keys[j] = kInfBits;
+        __syncthreads();
+        if (warp == 0) {
+            double a0 = lane < nw ? R.red[0][lane] : INFINITY, a1 = lane < nw ? R.red[1][lane] : -INFINITY;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                a0 = fmin(a0, __shfl_xor_sync(0xffffffffu, a0, o));
+                a1 = fmax(a1, __shfl_xor_sync(0xffffffffu, a1, o));
+            }
+            if (lane == 0) {
+                const double osc_bound = 0.5 * static_cast<double>(n) * fmax(fabs(a0), fabs(a1));
+                R.flag = (osc_bound * (1.0 + 1e-12) < lc.gap * (1.0 - 1e-12)) && n >= 3 && isfinite(a0) &&
+                         isfinite(a1);
+            }
+            if (step_blocks) {  // the warps' summaries composed in order (lanes >= warps: identity)
+                const unsigned long long f = warp_fsm(lane < nw ? R.fsm[lane] : fsm_identity());
+                if (lane == 0)
+                    step_blocks[static_cast<int64_t>(k) * lines + line] = 1 + static_cast<int64_t>((f >> 16) & 0xffff);
+            }
+        }
+        __syncthreads();
+        const bool ok = R.flag;
+        if (ok) {
+            // every source's local-minimum interval (fast.cu header), exact CAS-min
+            for (int y = sa; y < sb; ++y) {
+                const double u0 = cur[y];
+                const double sl = __dsub_rn(u0, cur[y == 0 ? n - 1 : y - 1]);
+                const double sr = __dsub_rn(cur[y + 1 == n ? 0 : y + 1], u0);
+                const int dl = max(__double2int_ru(__fma_rn(sl, ia, hl)), dmin_w);
+                const int dr = min(__double2int_rd(__fma_rn(sr, ia, hr)), dmax_w);
+                int j = (y + dl) % n;
+                if (j < 0) j += n;
+                for (int d = dl; d <= dr; ++d) {
+                    smem_fmin(&keys[j], __dadd_rn(u0, Kd[d]));
+                    j = j + 1 == n ? 0 : j + 1;
+                }
+            }
+        }
+        __syncthreads();
+        // epilogue: exact min (direct scan where the walk left nothing), potential, drift
+        double acc = 0.0;
+        bool bad = false;
+        for (int j = tid; j < n; j += nt) {
+            double best;
+            const unsigned long long kk = keys[j];
+            if (ok && kk != kInfBits) {
+                best = __longlong_as_double(static_cast<long long>(kk));
+            } else {
+                best = INFINITY;  // proj/tests/unit_scheme.cpp:184-190
+                int y = (j - first) % n;
+                if (y < 0) y += n;
+                for (int w = 0; w <= 2 * n; ++w) {
+                    const double c2 = __dadd_rn(cur[y], Ks[w]);
+                    best = c2 < best ? c2 : best;
+                    y = y == 0 ? n - 1 : y - 1;
+                }
+            }
+            const double o = tvl ? __dsub_rn(best, tvl[j]) : best;
+            nxt[j] = o;
+            acc += o - cur[j];
+            bad |= !isfinite(o);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        bad = __syncthreads_or(bad);
+        if (lane == 0) R.red[0][warp] = acc;
+        __syncthreads();
+        if (tid == 0) {
+            double sum = 0.0;
+            for (int w = 0; w < nw; ++w) sum += R.red[0][w];
+            if (step_drift) step_drift[static_cast<int64_t>(k) * lines + line] = sum / static_cast<double>(n);
+            if (bad) atomicMin(halt, k);
+        }
+        if (bad) {
+            ++k;
+            break;
+        }
+    }
+    __syncthreads();
+    const double* fin = (k & 1) ? U1 : U0;
+    for (int j = tid; j < n; j += nt) ul[j] = fin[j];
+}
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -1033,6 +1211,37 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     LOB_CUDA_TRY(ctx, cudaGetLastError());
     counter += 1;
     return LOB_OK;
+}
+
+
+size_t fast_resident_smem(int64_t n) { return static_cast<size_t>(n) * 24 + static_cast<size_t>(2 * n + 1) * 8; }
+bool fast_resident_ok(int64_t n) { return n >= 3 && n <= kResidentMaxN; }
+
+// `steps` K2 steps of `lines` short lines in ONE launch (K2R above); u in place.
+int launch_fast_resident_f64(lob_ctx* ctx, double* u, int64_t lines, int64_t n, const double* drift, double tau,
+                             const double* tv, int64_t tv_stride, double eta, int64_t steps, double* step_drift,
+                             int64_t* step_blocks, int* halt, void* lc_buf, cudaStream_t s) {
+    if (!fast_resident_ok(n)) return set_error(ctx, LOB_INVALID_INPUT, "resident K2: n out of range");
+    if (lines > 0x7fffffffll || steps > 0x7fffffffll) return set_error(ctx, LOB_INVALID_INPUT, "resident K2: too large");
+    int st = ensure_lut(ctx);
+    if (st) return st;
+    FastParams p = make_params(n, tau, eta);
+    st = ensure_vtab(ctx, n, tau, &p.vtab, &p.vofs, s);
+    if (st) return st;
+    LineConst* lcs = static_cast<LineConst*>(lc_buf);
+    line_setup_kernel<<<static_cast<unsigned>((lines + 127) / 128), 128, 0, s>>>(drift, lines, p, lcs);
+    const size_t smem = fast_resident_smem(n);
+    if (first_time(ctx, reinterpret_cast<const void*>(&resident_kernel)))
+        LOB_CUDA_TRY(ctx, cudaFuncSetAttribute(resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(fast_resident_smem(kResidentMaxN))));
+    // two sources per thread (up to kRT; measured on C1: 512 threads 8.8 us/step, 1024 threads
+    // 10.8, 128 threads 13.9)
+    const int nt = static_cast<int>(std::min<int64_t>(kRT, std::max<int64_t>(64, ((n / 2 + 31) / 32) * 32)));
+    resident_kernel<<<static_cast<unsigned>(lines), nt, smem, s>>>(u, static_cast<int>(n), lcs, p, tv, tv_stride,
+                                                                     static_cast<int>(steps), step_drift, step_blocks,
+                                                                     lines, halt);
+    ctx->launches += 2;
+    return cuda_status(ctx, cudaGetLastError(), "resident K2");
 }
 
 int fast_diag_count(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n, uint64_t* count,
