@@ -118,6 +118,10 @@ class Device:
     def launches(self) -> int:
         return int(self.lib.lob_launch_count(self.ctx))
 
+    def set_evolve_resident(self, on: bool) -> None:
+        """evolve through the on-chip resident kernels (K2R / K2C) where the lines fit (default)."""
+        self._check(self.lib.lob_ctx_set_evolve_resident(self.ctx, int(bool(on))), "lob_ctx_set_evolve_resident")
+
     def set_direct_mode(self, mode: int) -> None:
         """DIRECT_SCREENED (default: fp32 screen + fp64 re-evaluation) or DIRECT_PLAIN."""
         self._check(self.lib.lob_ctx_set_direct_mode(self.ctx, int(mode)), "lob_ctx_set_direct_mode")

@@ -86,6 +86,12 @@ int lob_ctx_set_direct_mode(lob_ctx* ctx, int mode) {
     return LOB_OK;
 }
 
+int lob_ctx_set_evolve_resident(lob_ctx* ctx, int on) {
+    if (!ctx) return LOB_INVALID_INPUT;
+    ctx->resident = on ? 1 : 0;
+    return LOB_OK;
+}
+
 int lob_direct_stats(lob_ctx* ctx, uint64_t* full_outputs, uint64_t* fp64_candidates, int reset) {
     if (!ctx) return LOB_INVALID_INPUT;
     cudaSetDevice(ctx->device);
@@ -317,7 +323,7 @@ int lob_evolve_f64(lob_ctx* ctx, double* u, double* scratch, int64_t lines, int6
     LOB_CUDA_TRY(ctx, cudaMallocAsync(&halt, sizeof(int), s));
     const int big = 0x7fffffff;
     LOB_CUDA_TRY(ctx, cudaMemcpyAsync(halt, &big, sizeof(int), cudaMemcpyHostToDevice, s));
-    if (engine == LOB_ENGINE_FAST && fast_resident_ok(n)) {
+    if (engine == LOB_ENGINE_FAST && ctx->resident && fast_resident_ok(n)) {
         // short lines: every step in one launch, the lines resident in shared memory (K2R)
         void* lcb = nullptr;
         LOB_CUDA_TRY(ctx, cudaMallocAsync(&lcb, static_cast<size_t>(lines) * 64, s));

@@ -1017,6 +1017,7 @@ __global__ void __launch_bounds__(kRT) resident_kernel(double* __restrict__ u, i
     const double* fin = (k & 1) ? U1 : U0;
     for (int j = tid; j < n; j += nt) ul[j] = fin[j];
 }
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -1243,6 +1244,7 @@ int launch_fast_resident_f64(lob_ctx* ctx, double* u, int64_t lines, int64_t n, 
     ctx->launches += 2;
     return cuda_status(ctx, cudaGetLastError(), "resident K2");
 }
+
 
 int fast_diag_count(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n, uint64_t* count,
                     cudaStream_t s) {
