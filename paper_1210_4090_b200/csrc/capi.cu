@@ -341,6 +341,9 @@ int lob_evolve_f64(lob_ctx* ctx, double* u, double* scratch, int64_t lines, int6
             return set_error(ctx, LOB_EVALUATION_ERROR, "non-finite value after step " + std::to_string(hstep + 1));
         return LOB_OK;
     }
+    double* dpart = nullptr;
+    if (engine == LOB_ENGINE_FAST)
+        LOB_CUDA_TRY(ctx, cudaMallocAsync(&dpart, static_cast<size_t>(lines * fast_tiles(n)) * sizeof(double), s));
     double* cur = u;
     double* nxt = scratch;
     int64_t done = 0;
@@ -355,13 +358,18 @@ int lob_evolve_f64(lob_ctx* ctx, double* u, double* scratch, int64_t lines, int6
             st = launch_relaxed_f64(ctx, cur, nxt, lines, n, ktab, W, firsts, tv, tv_stride, eta,
                                     step_blocks ? step_blocks + i * lines : nullptr, rws, rwsb, s);
         } else {
+            // the drift's per-tile partial sums come out of the K2 epilogue (no second pass over u)
             st = launch_fast_f64(ctx, cur, nxt, lines, n, drift, tau, tv, tv_stride, eta,
                                  step_blocks ? step_blocks + i * lines : nullptr, workspace,
-                                 workspace_bytes, i == 0 ? 0 : LOB_FAST_STATS_VALID, s);
+                                 workspace_bytes, i == 0 ? 0 : LOB_FAST_STATS_VALID, s, dpart);
+            if (st == LOB_OK)
+                st = launch_drift_tiles(ctx, dpart, lines, n, step_drift ? step_drift + i * lines : nullptr, halt,
+                                        static_cast<int>(i), s);
         }
         if (st) break;
-        st = launch_drift(ctx, nxt, cur, lines, n, step_drift ? step_drift + i * lines : nullptr,
-                          halt, static_cast<int>(i), s);
+        if (engine != LOB_ENGINE_FAST)
+            st = launch_drift(ctx, nxt, cur, lines, n, step_drift ? step_drift + i * lines : nullptr,
+                              halt, static_cast<int>(i), s);
         if (st) break;
         std::swap(cur, nxt);
         done = i + 1;
@@ -383,6 +391,7 @@ int lob_evolve_f64(lob_ctx* ctx, double* u, double* scratch, int64_t lines, int6
     if (ktab) cudaFreeAsync(ktab, s);
     if (firsts) cudaFreeAsync(firsts, s);
     if (rws) cudaFreeAsync(rws, s);
+    if (dpart) cudaFreeAsync(dpart, s);
     cudaFreeAsync(halt, s);
     LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
     if (completed_steps) *completed_steps = done;

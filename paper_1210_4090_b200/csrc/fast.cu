@@ -311,6 +311,17 @@ __global__ void __launch_bounds__(kNT) stats_kernel(const double* __restrict__ u
         tile_stats<false>(vals, Tl, j0, line, tile, p, b, sh, lut);
 }
 
+// per-line drift from the K2 tiles' partial sums, in tile order; non-finite -> halt
+__global__ void drift_tiles_kernel(const double* __restrict__ dpart, int64_t lines, int64_t tiles, int64_t n,
+                                   double* __restrict__ drift_out, int* __restrict__ halt, int step) {
+    const int64_t line = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (line >= lines) return;
+    double sum = 0.0;
+    for (int64_t t = 0; t < tiles; ++t) sum += dpart[line * tiles + t];
+    if (drift_out) drift_out[line] = sum / static_cast<double>(n);
+    if (!isfinite(sum) && halt) atomicMin(halt, step);
+}
+
 __global__ void line_init_kernel(unsigned long long* L, int64_t lines) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= lines) return;
@@ -564,7 +575,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
     const double* __restrict__ u, double* __restrict__ out, const LineConst* __restrict__ lcs,
     const double* __restrict__ tv, int64_t tv_stride, int64_t* __restrict__ blocks_out,
     unsigned long long* __restrict__ diag, FastParams p, FastBuffers b, unsigned* __restrict__ done,
-    unsigned need) {
+    unsigned need, double* __restrict__ dpart) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     MainShared& S = *reinterpret_cast<MainShared*>(smem_raw);
 
@@ -803,6 +814,26 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
     else
         epilogue(std::false_type{});
     __syncthreads();
+    if (dpart) {
+        // evolve's per-step drift (proj/src/scheme.cpp:244-250): this tile's sum of u^{n+1} - u^n
+        // (the tile's u^{n+1} is in vals; u^n from global, coalesced); summed per line in tile order
+        double acc = 0.0;
+#pragma unroll
+        for (int m = 0; m < kPer; ++m) {
+            const int i = 1 + tid + kNT * m;
+            if (i <= Tl) acc += vals[P8(i)] - xload<CHAIN>(ul + j0 + i - 1);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        double* red = reinterpret_cast<double*>(S.queue);  // the queue is dead after the emission
+        if (lane == 0) red[warp] = acc;
+        __syncthreads();
+        if (tid == 0) {
+            double sum = 0.0;
+            for (int w = 0; w < kNT / 32; ++w) sum += red[w];
+            dpart[line * tiles + tile] = sum;
+        }
+    }
     if (tid == 0 && diag) {
         atomicAdd(diag + 1, static_cast<unsigned long long>(S.c_src));
         atomicAdd(diag + 2, static_cast<unsigned long long>(S.c_inline));
@@ -1126,7 +1157,7 @@ static FastBuffers make_buffers(void* ws, int64_t lines, int64_t n, int64_t coun
 int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
                     const double* drift, double tau, const double* tv, int64_t tv_stride,
                     double eta, int64_t* blocks, void* workspace, size_t ws_bytes, int flags,
-                    cudaStream_t s) {
+                    cudaStream_t s, double* dpart) {
     if (ws_bytes < fast_workspace_bytes(lines, n) || !workspace)
         return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_fast_f64: workspace too small");
     if (n > (1ll << 29)) return set_error(ctx, LOB_INVALID_INPUT, "fast: n too large");
@@ -1183,7 +1214,7 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     unsigned* done = reinterpret_cast<unsigned*>(static_cast<char*>(workspace) + w.done);
     if (release && chain == 0) LOB_CUDA_TRY(ctx, cudaMemsetAsync(done, 0, lines * sizeof(unsigned), s));
     using KernT = void (*)(const double*, double*, const LineConst*, const double*, int64_t, int64_t*,
-                           unsigned long long*, FastParams, FastBuffers, unsigned*, unsigned);
+                           unsigned long long*, FastParams, FastBuffers, unsigned*, unsigned, double*);
     static const KernT kerns[2][2][2] = {
         {{fast_kernel<false, false, false>, fast_kernel<false, false, true>},
          {fast_kernel<false, true, false>, fast_kernel<false, true, true>}},
@@ -1206,7 +1237,7 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     LOB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, u, out, const_cast<const LineConst*>(lcs), tv, tv_stride,
-                                         blocks, diag, p, b, done, need));
+                                         blocks, diag, p, b, done, need, dpart));
     if (release) chain += 1;
     ctx->launches += 1;
     LOB_CUDA_TRY(ctx, cudaGetLastError());
@@ -1245,6 +1276,16 @@ int launch_fast_resident_f64(lob_ctx* ctx, double* u, int64_t lines, int64_t n, 
     return cuda_status(ctx, cudaGetLastError(), "resident K2");
 }
 
+
+int64_t fast_tiles(int64_t n) { return (n + kT - 1) / kT; }
+
+int launch_drift_tiles(lob_ctx* ctx, const double* dpart, int64_t lines, int64_t n, double* drift_out, int* halt,
+                       int step, cudaStream_t s) {
+    drift_tiles_kernel<<<static_cast<unsigned>((lines + 127) / 128), 128, 0, s>>>(dpart, lines, fast_tiles(n), n,
+                                                                                  drift_out, halt, step);
+    ctx->launches += 1;
+    return cuda_status(ctx, cudaGetLastError(), "drift_tiles_kernel");
+}
 
 int fast_diag_count(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n, uint64_t* count,
                     cudaStream_t s) {

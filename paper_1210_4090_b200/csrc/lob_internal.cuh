@@ -116,10 +116,14 @@ int launch_window_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines,
                       const double* tv, int64_t tv_stride, int* d_err, cudaStream_t s);
 
 size_t fast_workspace_bytes(int64_t lines, int64_t n);
+// dpart (nullable): per-tile sums of u^{n+1} - u^n for evolve's drift ([lines][fast_tiles(n)])
 int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
                     const double* drift, double tau, const double* tv, int64_t tv_stride,
                     double eta, int64_t* blocks, void* workspace, size_t ws_bytes, int flags,
-                    cudaStream_t s);
+                    cudaStream_t s, double* dpart = nullptr);
+int64_t fast_tiles(int64_t n);
+int launch_drift_tiles(lob_ctx* ctx, const double* dpart, int64_t lines, int64_t n, double* drift_out, int* halt,
+                       int step, cudaStream_t s);
 // K2R: all steps of an evolve of short lines (n <= 8192) in one launch, one CTA per line
 bool fast_resident_ok(int64_t n);
 int launch_fast_resident_f64(lob_ctx* ctx, double* u, int64_t lines, int64_t n, const double* drift, double tau,

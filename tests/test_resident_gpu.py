@@ -43,3 +43,30 @@ def test_resident_evolve_equals_launch_loop(dev, n, lines, steps, tau):
     assert np.array_equal(a[0], b[0])
     assert np.array_equal(a[2], b[2])
     assert np.max(np.abs(a[1] - b[1])) <= 1e-12
+
+
+def test_evolve_loop_fused_drift(dev):
+    """n > 4096 runs the step-by-step K2 loop with the drift's partial sums fused into the
+    K2 epilogue: states == single K2 steps, drift <= 1e-12 of mean(u_next - u) per step"""
+    import torch
+
+    n, lines, steps, tau = 8192, 3, 12, 0.02
+    rng = np.random.default_rng(3)
+    x = np.arange(n) / n
+    u0 = np.stack([np.sin(2 * np.pi * x + rng.uniform(0, 6)) for _ in range(lines)])
+    drifts = np.array([0.3, -1.1, 1.7])
+    tv = api.tau_v(api.gen_potential(2, n), tau)
+    a = _evolve(dev, u0, drifts, tau, steps, tv, True)
+    u = torch.from_numpy(u0.copy()).cuda()
+    out = torch.empty_like(u)
+    ws = torch.empty(dev.fast_workspace_bytes(lines, n), dtype=torch.uint8, device="cuda")
+    dr = torch.from_numpy(drifts).cuda()
+    dtv = torch.from_numpy(tv).cuda()
+    bl = torch.empty(lines, dtype=torch.int64, device="cuda")
+    for k in range(steps):
+        dev.fast_f64(u, out, dr, tau, tv=dtv, blocks=bl, workspace=ws, flags=api.FAST_STATS_VALID if k else 0)
+        want = (out - u).mean(dim=1).cpu().numpy()
+        assert np.max(np.abs(a[1][k * lines:(k + 1) * lines] - want)) <= 1e-12
+        assert np.array_equal(a[2][k * lines:(k + 1) * lines], bl.cpu().numpy())
+        u, out = out, u
+    assert np.array_equal(a[0], u.cpu().numpy())
