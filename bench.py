@@ -367,6 +367,21 @@ def extras(dev):
                          "hbm_frac": 4096 * 4096 * 16 / t / 1e9 / measured_peaks()[0]}
     del u, o, u32, o32, ws
 
+    # C2 through the reference's evolve API (lob_evolve_f64: per-step drift and block counts fused)
+    st = torch.zeros((LINES, N_SPACE), dtype=torch.float64, device="cuda")
+    scr = torch.empty_like(st)
+    dr = torch.from_numpy(api.gen_c2_drifts(LINES)).cuda()
+    tvd = torch.from_numpy(api.tau_v(api.gen_potential(2, N_SPACE), TAU)).cuda()
+    wse = torch.empty(dev.fast_workspace_bytes(LINES, N_SPACE), dtype=torch.uint8, device="cuda")
+    dev.evolve(st, scr, dr, TAU, 200, tv=tvd, workspace=wse)
+    ne = 100
+    sd = torch.empty(ne * LINES, dtype=torch.float64, device="cuda")
+    sb = torch.empty(ne * LINES, dtype=torch.int64, device="cuda")
+    t = timeit(lambda: dev.evolve(st, scr, dr, TAU, ne, tv=tvd, step_drift=sd, step_blocks=sb, workspace=wse), 1)
+    out["c2_evolve_api"] = {"ms_per_step": t * 1e3 / ne, "updates_per_s": LINES * N_SPACE * ne / t,
+                            "includes": "per-step drift and decompose block counts (proj/src/scheme.cpp:208-272)"}
+    del st, scr, wse
+
     # weak-KAM consumers: tropical product at the dense guard n = 512, Karp, period matrix
     m = 512
     rng = np.random.default_rng(0)

@@ -167,8 +167,9 @@ int lob_evolve_f64(lob_ctx* ctx, double* u, double* scratch, int64_t lines, int6
                    size_t workspace_bytes, void* stream);
 
 /* lob_evolve_f64 with LOB_ENGINE_FAST runs every step of the call in ONE launch with the
- * lines resident in shared memory when n <= 4096 (K2R, one CTA per line).  Same doubles as
- * the step-by-step loop.  on = 0 selects the step-by-step K2 launches (default 1). */
+ * lines resident in shared memory (K2R, one CTA per line) when n <= 4096 and the batch is
+ * too small to fill the GPU step by step (lines * ceil(n/2048) <= 4 * SMs).  Same doubles as
+ * the step-by-step loop.  on = 0 always selects the step-by-step K2 launches (default 1). */
 int lob_ctx_set_evolve_resident(lob_ctx* ctx, int on);
 
 /* Host-buffer entry point (the e2e path): one step of `lines` lines whose u,

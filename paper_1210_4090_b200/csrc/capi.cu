@@ -323,8 +323,10 @@ int lob_evolve_f64(lob_ctx* ctx, double* u, double* scratch, int64_t lines, int6
     LOB_CUDA_TRY(ctx, cudaMallocAsync(&halt, sizeof(int), s));
     const int big = 0x7fffffff;
     LOB_CUDA_TRY(ctx, cudaMemcpyAsync(halt, &big, sizeof(int), cudaMemcpyHostToDevice, s));
-    if (engine == LOB_ENGINE_FAST && ctx->resident && fast_resident_ok(n)) {
-        // short lines: every step in one launch, the lines resident in shared memory (K2R)
+    // short lines in batches too small to fill the GPU with step-by-step launches (which are then
+    // latency bound): every step in one launch, the lines resident in shared memory (K2R)
+    if (engine == LOB_ENGINE_FAST && ctx->resident && fast_resident_ok(n) &&
+        lines * fast_tiles(n) <= 4 * static_cast<int64_t>(ctx->sm_count)) {
         void* lcb = nullptr;
         LOB_CUDA_TRY(ctx, cudaMallocAsync(&lcb, static_cast<size_t>(lines) * 64, s));
         st = launch_fast_resident_f64(ctx, u, lines, n, drift, tau, tv, tv_stride, eta, steps, step_drift,
