@@ -893,6 +893,7 @@ struct ResidentShared {
 
 __global__ void __launch_bounds__(kRT) resident_kernel(double* __restrict__ u, int n, const LineConst* __restrict__ lcs,
                                                        FastParams p, const double* __restrict__ tv, int64_t tv_stride,
+                                                       int tv_period, int64_t tv_step_stride,
                                                        int steps, double* __restrict__ step_drift,
                                                        int64_t* __restrict__ step_blocks, int64_t lines,
                                                        int* __restrict__ halt) {
@@ -909,7 +910,7 @@ __global__ void __launch_bounds__(kRT) resident_kernel(double* __restrict__ u, i
     const int first = static_cast<int>(lc.first);
     const int dmin_w = first + 1, dmax_w = first + 2 * n - 1;
     const double ia = p.ia, hl = lc.hl, hr = lc.hr, tau = p.tau;
-    const double* tvl = tv ? tv + line * tv_stride : nullptr;
+    const double* tvl0 = tv ? tv + line * tv_stride : nullptr;
     double* ul = u + line * n;
     for (int j = tid; j < n; j += nt) U0[j] = ul[j];
     for (int w = tid; w <= 2 * n; w += nt) Ks[w] = kval(p.vtab, p.vofs, first + w, lc.drift, tau);
@@ -921,6 +922,8 @@ __global__ void __launch_bounds__(kRT) resident_kernel(double* __restrict__ u, i
     for (; k < steps; ++k) {
         double* cur = (k & 1) ? U1 : U0;
         double* nxt = (k & 1) ? U0 : U1;
+        // tau*V of this step: one table, or table k mod tv_period (in-period time labels)
+        const double* tvl = tvl0 && tv_period > 1 ? tvl0 + (k % tv_period) * tv_step_stride : tvl0;
         __syncthreads();
         // slope extremes (gate) and the FSM summary of this thread's increments
         double smn = INFINITY, smx = -INFINITY;
@@ -1252,7 +1255,8 @@ bool fast_resident_ok(int64_t n) { return n >= 3 && n <= kResidentMaxN; }
 // `steps` K2 steps of `lines` short lines in ONE launch (K2R above); u in place.
 int launch_fast_resident_f64(lob_ctx* ctx, double* u, int64_t lines, int64_t n, const double* drift, double tau,
                              const double* tv, int64_t tv_stride, double eta, int64_t steps, double* step_drift,
-                             int64_t* step_blocks, int* halt, void* lc_buf, cudaStream_t s) {
+                             int64_t* step_blocks, int* halt, void* lc_buf, cudaStream_t s, int tv_period,
+                             int64_t tv_step_stride) {
     if (!fast_resident_ok(n)) return set_error(ctx, LOB_INVALID_INPUT, "resident K2: n out of range");
     if (lines > 0x7fffffffll || steps > 0x7fffffffll) return set_error(ctx, LOB_INVALID_INPUT, "resident K2: too large");
     int st = ensure_lut(ctx);
@@ -1270,8 +1274,8 @@ int launch_fast_resident_f64(lob_ctx* ctx, double* u, int64_t lines, int64_t n, 
     // 10.8, 128 threads 13.9)
     const int nt = static_cast<int>(std::min<int64_t>(kRT, std::max<int64_t>(64, ((n / 2 + 31) / 32) * 32)));
     resident_kernel<<<static_cast<unsigned>(lines), nt, smem, s>>>(u, static_cast<int>(n), lcs, p, tv, tv_stride,
-                                                                     static_cast<int>(steps), step_drift, step_blocks,
-                                                                     lines, halt);
+                                                                     tv_period, tv_step_stride, static_cast<int>(steps),
+                                                                     step_drift, step_blocks, lines, halt);
     ctx->launches += 2;
     return cuda_status(ctx, cudaGetLastError(), "resident K2");
 }

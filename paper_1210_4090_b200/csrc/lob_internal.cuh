@@ -126,9 +126,11 @@ int launch_drift_tiles(lob_ctx* ctx, const double* dpart, int64_t lines, int64_t
                        int step, cudaStream_t s);
 // K2R: all steps of an evolve of short lines (n <= 8192) in one launch, one CTA per line
 bool fast_resident_ok(int64_t n);
+// tv_period > 1: step k uses table tv + (k mod tv_period) * tv_step_stride (per line: + line * tv_stride)
 int launch_fast_resident_f64(lob_ctx* ctx, double* u, int64_t lines, int64_t n, const double* drift, double tau,
                              const double* tv, int64_t tv_stride, double eta, int64_t steps, double* step_drift,
-                             int64_t* step_blocks, int* halt, void* lc_buf, cudaStream_t s);
+                             int64_t* step_blocks, int* halt, void* lc_buf, cudaStream_t s, int tv_period = 1,
+                             int64_t tv_step_stride = 0);
 int fast_diag_count(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n, uint64_t* count,
                     cudaStream_t s);
 int launch_block_counts(lob_ctx* ctx, const double* u, int64_t lines, int64_t n, double eta,

@@ -377,6 +377,9 @@ struct PeriodRunner {
     void* ws = nullptr;
     size_t wsb = 0;
     int64_t steps_done = 0;
+    bool resident = false;  // a whole period in one K2R launch (short lines)
+    void* lcb = nullptr;
+    int* halt = nullptr;
 
     int init(const double* u0, const double* tvs) {
         s = ctx->stream;
@@ -406,13 +409,27 @@ struct PeriodRunner {
         } else {
             wsb = fast_workspace_bytes(1, n);
             LOB_CUDA_TRY(ctx, cudaMalloc(&ws, wsb));
+            resident = ctx->resident && fast_resident_ok(n);
+            if (resident) {
+                LOB_CUDA_TRY(ctx, cudaMalloc(&lcb, 64));
+                LOB_CUDA_TRY(ctx, cudaMalloc(&halt, sizeof(int)));
+            }
         }
         LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
         return LOB_OK;
     }
     // one whole period on the device; the state is copied to host[n]
     int period(double* host) {
-        for (int64_t i = 0; i < ell; ++i) {
+        if (resident) {
+            const int big = 0x7fffffff;
+            LOB_CUDA_TRY(ctx, cudaMemcpyAsync(halt, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+            const int st = launch_fast_resident_f64(ctx, du, 1, n, ddrift, tau, tv_count ? dtv : nullptr, 0, 0.0, ell,
+                                                    nullptr, nullptr, halt, lcb, s,
+                                                    static_cast<int>(tv_count > 1 ? tv_count : 1), n);
+            if (st) return st;
+            steps_done += ell;
+        }
+        for (int64_t i = 0; i < (resident ? 0 : ell); ++i) {
             const double* tv = tv_count == 0 ? nullptr : dtv + (tv_count == 1 ? 0 : i) * n;
             int st;
             if (engine == LOB_ENGINE_DIRECT)
@@ -433,7 +450,8 @@ struct PeriodRunner {
     }
     ~PeriodRunner() {
         for (void* p : {static_cast<void*>(du), static_cast<void*>(dscr), static_cast<void*>(dtv),
-                        static_cast<void*>(ddrift), static_cast<void*>(ktab), static_cast<void*>(dfirst), ws})
+                        static_cast<void*>(ddrift), static_cast<void*>(ktab), static_cast<void*>(dfirst), ws, lcb,
+                        static_cast<void*>(halt)})
             if (p) cudaFree(p);
     }
 };
