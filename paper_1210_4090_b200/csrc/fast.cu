@@ -52,8 +52,11 @@ namespace lob {
 #define LOB_KT 2048
 #endif
 constexpr int kT = LOB_KT;     // outputs per CTA tile
-constexpr int kNT = 256;       // threads per CTA
-constexpr int kG = kT / 8;     // sub-tile (slope statistics granularity): one warp each
+#ifndef LOB_NT
+#define LOB_NT 256
+#endif
+constexpr int kNT = LOB_NT;           // threads per CTA
+constexpr int kG = kT / (kNT / 32);   // sub-tile (slope statistics granularity): one warp each
 constexpr int kSub = kT / kG;  // sub-tiles per tile (= warps per CTA)
 constexpr int kPer = kT / kNT; // outputs / sources per thread
 #ifndef LOB_EMIT_UNROLL
