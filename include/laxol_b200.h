@@ -186,6 +186,14 @@ int lob_step_host_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines,
 int lob_kernel_mech_host(lob_ctx* ctx, int64_t n, double tau, double drift, double* window,
                          int64_t* first, int64_t* argmin, double* delta);
 
+/* Kernel window of a TABULATED conjugate (proj/src/hamiltonian.cpp:30-82 tabulated /
+ * kstar / argmin_velocity, proj/src/scheme.cpp:59-105 with its monotone slope repair):
+ * `count` convex samples at velocities v0 + i*dv.  window[2n+1], first, argmin as for
+ * lob_kernel_mech_host.  Use with the direct (K1) and relaxed engines, which take any
+ * table; K2 is for the mechanical conjugate.  ctx may be NULL. */
+int lob_kernel_tabulated_host(lob_ctx* ctx, int64_t n, double tau, const double* samples, int64_t count,
+                              double v0, double dv, double* window, int64_t* first, int64_t* argmin);
+
 /* Decomposition block counts of device lines (decompose, proj/src/minplus.cpp:152-188,
  * on the closed period; capped counts are not supported: eta must be 0 or the
  * uncapped count is returned). blocks: device int64[lines]. */

@@ -345,4 +345,28 @@ int ref_step_semidiscrete(const double* u, int64_t m, int periodic, double origi
     });
 }
 
+// Tabulated kinetics: the kernel window (proj/src/scheme.cpp:59-105) and kinetic_convolve of a
+// periodic u (fundamental domain) with it.
+int ref_kernel_tabulated(int n_space, double tau, const double* samples, int64_t count, double v0, double dv,
+                         double* window, int64_t* center, int64_t* argmin) {
+    return guarded([&] {
+        const Kernel k = build_kernel(tabulated(std::vector<double>(samples, samples + count), v0, dv),
+                                      params_of(n_space, tau, 0.0));
+        std::memcpy(window, k.window.values.data(), k.window.values.size() * sizeof(double));
+        if (center) *center = k.center_index;
+        if (argmin) *argmin = k.argmin_index;
+    });
+}
+
+int ref_convolve_tabulated(const double* u, int n_space, double tau, const double* samples, int64_t count,
+                           double v0, double dv, double eta, int engine, double* out, int64_t* blocks) {
+    return guarded([&] {
+        const SchemeParams p = params_of(n_space, tau, eta);
+        const Kernel k = build_kernel(tabulated(std::vector<double>(samples, samples + count), v0, dv), p);
+        const GridFn g = make_periodic(std::vector<double>(u, u + n_space), p.epsilon());
+        const GridFn r = kinetic_convolve(g, k, eta, engine_of(engine), blocks);
+        std::memcpy(out, r.values.data(), n_space * sizeof(double));
+    });
+}
+
 }  // extern "C"

@@ -152,6 +152,17 @@ class Device:
         return Kernel(win, int(first.value), int(arg.value), int(first.value) + n_space, n_space,
                       tau, drift, float(delta.value))
 
+    @staticmethod
+    def build_kernel_tabulated(n_space: int, tau: float, samples, v0: float, dv: float) -> Kernel:
+        """Host build_kernel for tabulated(samples, v0, dv) (proj/src/scheme.cpp:59-105)."""
+        smp = np.ascontiguousarray(samples, np.float64)
+        win = np.empty(2 * n_space + 1, dtype=np.float64)
+        first, arg = ctypes.c_int64(), ctypes.c_int64()
+        st = _capi.load().lob_kernel_tabulated_host(None, n_space, tau, smp.ctypes.data, smp.size, v0, dv,
+                                                     win.ctypes.data, ctypes.byref(first), ctypes.byref(arg))
+        check(st, None, "build_kernel_tabulated")
+        return Kernel(win, int(first.value), int(arg.value), int(first.value) + n_space, n_space, tau, float("nan"))
+
     def direct_f64(self, u, out, ktab, first, tv=None, ktab_stride=0, tv_stride=0, stream=None):
         lines, n = u.shape
         st = self.lib.lob_minplus_direct_f64(self.ctx, _ptr(u), _ptr(out), lines, n, _ptr(ktab),

@@ -136,7 +136,10 @@ Engine::~Engine() { lob_ctx_destroy(ctx_); }
 GridFn Engine::kinetic_convolve(const GridFn& u, const KernelWindow& kernel, double eta,
                                 ConvEngine engine, int64_t* blocks) {
     const int64_t n = kernel.n_space;
-    const int code = engine_code(engine, eta);
+    int code = engine_code(engine, eta);
+    // K2 walks the mechanical conjugate; for a tabulated window the fast engine is the
+    // reference's conv_fast itself (exact at eta == 0), which the relaxed engine reproduces
+    if (code == LOB_ENGINE_FAST && !kernel.mechanical) code = LOB_ENGINE_RELAXED;
     if (u.periodic) {
         if (static_cast<int64_t>(u.n()) != n)
             throw InvalidInput("kinetic_convolve: periodic u must hold one unit period");

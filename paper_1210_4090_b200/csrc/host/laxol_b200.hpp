@@ -53,8 +53,12 @@ struct KernelWindow {
     double tau = 0.0;
     double drift = 0.0;
     double delta = 0.0;  // fast-engine slope-inversion tolerance
+    bool mechanical = true;  // false: a tabulated conjugate (drift holds its argmin velocity)
 };
 KernelWindow build_kernel_mech(int64_t n_space, double tau, double drift);
+// proj/include/laxol/hamiltonian.hpp:27 tabulated(samples, v0, dv) + build_kernel
+KernelWindow build_kernel_tab(int64_t n_space, double tau, const std::vector<double>& samples, double v0,
+                              double dv);
 double fast_delta(int64_t n_space, double tau, double drift, int64_t first);
 
 enum class ConvEngine { Fast, Naive, GpuFast, GpuDirect };

@@ -123,6 +123,10 @@ class Reference:
             "ref_decompose": (c_int64, [_P, c_int64, c_double, _P, _P, _P, c_int64]),
             "ref_conv": (c_int, [c_int, _P, c_int64, _P, c_int64, c_double, _P, _P]),
             "ref_minplus_product": (c_int, [_P, _P, c_int64, _P]),
+            "ref_kernel_tabulated": (c_int, [c_int, c_double, _P, c_int64, c_double, c_double, _P, POINTER(c_int64),
+                                             POINTER(c_int64)]),
+            "ref_convolve_tabulated": (c_int, [_P, c_int, c_double, _P, c_int64, c_double, c_double, c_double, c_int,
+                                               _P, POINTER(c_int64)]),
             "ref_step_semidiscrete": (c_int, [_P, c_int64, c_int, c_double, c_int, c_double, c_double, c_int,
                                               c_double, c_double, c_double, c_int, c_int, c_double, c_double,
                                               c_int, _P]),
@@ -210,6 +214,23 @@ class Reference:
         st = self.lib.ref_conv(which, a.ctypes.data, a.size, b.ctypes.data, b.size, eta, out.ctypes.data,
                                ctypes.byref(blocks))
         return out, blocks.value, st
+
+    def kernel_tabulated(self, n, tau, samples, v0, dv):
+        smp = np.ascontiguousarray(samples, np.float64)
+        w = np.empty(2 * n + 1)
+        c, a = c_int64(), c_int64()
+        st = self.lib.ref_kernel_tabulated(n, tau, smp.ctypes.data, smp.size, v0, dv, w.ctypes.data,
+                                           ctypes.byref(c), ctypes.byref(a))
+        return w, c.value - n, a.value, st
+
+    def convolve_tabulated(self, u, tau, samples, v0, dv, eta=0.0, engine=0):
+        u = np.ascontiguousarray(u, np.float64)
+        smp = np.ascontiguousarray(samples, np.float64)
+        out = np.empty_like(u)
+        b = c_int64()
+        st = self.lib.ref_convolve_tabulated(u.ctypes.data, u.size, tau, smp.ctypes.data, smp.size, v0, dv, eta,
+                                             engine, out.ctypes.data, ctypes.byref(b))
+        return out, b.value, st
 
     def step_semidiscrete(self, u, n_space, tau, drift, pot, t, q, periodic=True, origin=0.0):
         """pot: dict(kind, value, offset, amplitude, frequency, tmod, omega) (api.potential_*)."""
