@@ -146,6 +146,19 @@ int lob_split_step_2d_f64(lob_ctx* ctx, const double* u, double* out, double* tm
                           const double* a2, double b, int engine, void* workspace,
                           size_t workspace_bytes, void* stream);
 
+/* split_step_nd (proj/src/splitting.cpp:37-99) for a periodic rank-`rank` tensor of n^rank
+ * samples (row-major, every axis one unit period): sweep axis 0, 1, ..., rank-1 in the
+ * reference's order (lines along axis a gathered by batched tiled transposes), then
+ * out -= tv (tau*V of every point at the step's sampling time, rounded on the host; NULL =
+ * V == 0).  Engines: LOB_ENGINE_DIRECT / LOB_ENGINE_RELAXED take the per-axis windows
+ * ktabs[a*(2n+1) + w] (device) with firsts[a] (host) — any convex window, mechanical or
+ * tabulated; LOB_ENGINE_FAST takes drifts[a] (host, mechanical axes) and a workspace of
+ * lob_fast_workspace_bytes(n^(rank-1), n).  eta: the relaxed engine's tolerance.  u, out,
+ * tmp: distinct device buffers of n^rank doubles.  Synchronous. */
+int lob_split_step_nd_f64(lob_ctx* ctx, const double* u, double* out, double* tmp, int rank, int64_t n, double tau,
+                          const double* ktabs, const int64_t* firsts, const double* drifts, const double* tv,
+                          double eta, int engine, void* workspace, size_t workspace_bytes, void* stream);
+
 /* The potential pass of K3 on a rows x n row slab (the multi-GPU split step's
  * rows [r0, r0 + rows) of an n x n tensor): out[i][k] -= tau*(a1[i]*a2[k] + b),
  * each product / sum one IEEE rounding (a1 points at the slab's first row). */

@@ -369,4 +369,36 @@ int ref_convolve_tabulated(const double* u, int n_space, double tau, const doubl
     });
 }
 
+// split_step_nd of a periodic rank-`rank` tensor (n^rank, row-major) with mechanical(drifts[a]) per axis
+// and V given as a full table of n^rank values (V(t, x) = table[flat index of x], time independent).
+int ref_split_step_nd(const double* u, int rank, int n_space, double tau, const double* drifts, const double* vtab,
+                      double t, double eta, double* out) {
+    return guarded([&] {
+        const SchemeParams p = params_of(n_space, tau, eta);
+        std::size_t total = 1;
+        for (int a = 0; a < rank; ++a) total *= static_cast<std::size_t>(n_space);
+        const TensorFn tu = make_tensor(std::vector<double>(u, u + total),
+                                        std::vector<std::size_t>(rank, static_cast<std::size_t>(n_space)),
+                                        p.epsilon(), std::vector<double>(rank, 0.0), true);
+        SplitSpec spec;
+        for (int a = 0; a < rank; ++a) spec.kinetics.push_back(mechanical(drifts[a]));
+        if (vtab) {
+            std::vector<double> tab(vtab, vtab + total);
+            const double step = p.epsilon();
+            const int n = n_space;
+            spec.potential = [tab, step, n](double, std::span<const double> x) {
+                std::size_t flat = 0;
+                for (double xa : x) {
+                    long long j = std::llround(xa / step);
+                    j = ((j % n) + n) % n;
+                    flat = flat * static_cast<std::size_t>(n) + static_cast<std::size_t>(j);
+                }
+                return tab[flat];
+            };
+        }
+        const TensorFn r = split_step_nd(tu, t, spec, p);
+        std::memcpy(out, r.values.data(), total * sizeof(double));
+    });
+}
+
 }  // extern "C"

@@ -221,6 +221,24 @@ class Device:
                                             _stream_ptr(stream))
         self._check(st, "lob_split_step_2d_f64")
 
+    def split_step_nd(self, u, out, tmp, rank, n, tau, kernels=None, drifts=None, tv=None, eta=0.0,
+                      engine=ENGINE_DIRECT, workspace=None, stream=None):
+        """split_step_nd (proj/src/splitting.cpp:37-99) of a periodic rank-`rank` tensor (n^rank
+        device doubles).  kernels: per-axis Kernel windows (direct / relaxed engines); drifts:
+        per-axis mechanical drifts (fast engine); tv: device tau*V of every point or None."""
+        import torch
+        kt = fr = dr = None
+        if kernels is not None:
+            kt = torch.from_numpy(np.concatenate([k.window for k in kernels])).to(u.device)
+            fr = (ctypes.c_int64 * rank)(*[int(k.first) for k in kernels])
+        if drifts is not None:
+            dr = (ctypes.c_double * rank)(*[float(d) for d in drifts])
+        ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+        st = self.lib.lob_split_step_nd_f64(self.ctx, _ptr(u), _ptr(out), _ptr(tmp), int(rank), int(n), float(tau),
+                                            _ptr(kt), fr, dr, _ptr(tv), float(eta), int(engine), _ptr(workspace),
+                                            ws_bytes, _stream_ptr(stream))
+        self._check(st, "lob_split_step_nd_f64")
+
     def evolve(self, u, scratch, drift, tau, steps, tv=None, tv_stride=0, eta=0.0,
                engine=ENGINE_FAST, step_drift=None, step_blocks=None, workspace=None, stream=None):
         lines, n = u.shape

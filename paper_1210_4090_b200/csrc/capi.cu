@@ -525,4 +525,89 @@ int lob_potential2d_rows_f64(lob_ctx* ctx, double* out, int64_t rows, int64_t n,
     return launch_potential2d(ctx, out, a1, a2, b, tau, n, static_cast<cudaStream_t>(stream), rows);
 }
 
+int lob_split_step_nd_f64(lob_ctx* ctx, const double* u, double* out, double* tmp, int rank, int64_t n, double tau,
+                          const double* ktabs, const int64_t* firsts, const double* drifts, const double* tv,
+                          double eta, int engine, void* workspace, size_t workspace_bytes, void* stream) {
+    if (!ctx) return LOB_INVALID_INPUT;
+    if (rank < 1 || rank > 8 || n < 1)
+        return set_error(ctx, LOB_INVALID_INPUT, "split_step_nd: rank must be 1..8 and n >= 1");
+    if (!u || !out || !tmp || u == out || u == tmp || out == tmp)
+        return set_error(ctx, LOB_INVALID_INPUT, "split_step_nd: need distinct u/out/tmp");
+    if (engine != LOB_ENGINE_DIRECT && engine != LOB_ENGINE_FAST && engine != LOB_ENGINE_RELAXED)
+        return set_error(ctx, LOB_INVALID_INPUT, "split_step_nd: unknown engine");
+    if (engine != LOB_ENGINE_FAST && (!ktabs || !firsts))
+        return set_error(ctx, LOB_INVALID_INPUT, "split_step_nd: the direct / relaxed engines need the kernel tables");
+    if (engine == LOB_ENGINE_FAST && !drifts)
+        return set_error(ctx, LOB_INVALID_INPUT, "split_step_nd: the fast engine needs the drifts");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int64_t total = 1;
+    for (int a = 0; a < rank; ++a) {
+        if (total > (int64_t(1) << 40) / n) return set_error(ctx, LOB_INVALID_INPUT, "split_step_nd: too large");
+        total *= n;
+    }
+    const int64_t lines = total / n, W = 2 * n + 1;
+    // per-line first / drift arrays and the relaxed engine's workspace
+    int64_t* dfirst = nullptr;
+    double* ddrift = nullptr;
+    void* rws = nullptr;
+    size_t rwsb = 0;
+    LOB_CUDA_TRY(ctx, cudaMallocAsync(&dfirst, static_cast<size_t>(lines) * sizeof(int64_t), s));
+    LOB_CUDA_TRY(ctx, cudaMallocAsync(&ddrift, static_cast<size_t>(lines) * sizeof(double), s));
+    if (engine == LOB_ENGINE_RELAXED) {
+        rwsb = relaxed_workspace_bytes(lines, n);
+        LOB_CUDA_TRY(ctx, cudaMallocAsync(&rws, rwsb, s));
+    }
+    std::vector<int64_t> hf(static_cast<size_t>(lines));
+    std::vector<double> hd(static_cast<size_t>(lines));
+    // proj/src/splitting.cpp:53-77: axis 0 first; a line of axis a has stride n^(rank-1-a)
+    const double* cur = u;
+    double* bufs[2] = {out, tmp};
+    int nb = 0;  // next buffer to write
+    int st = LOB_OK;
+    for (int a = 0; a < rank && st == LOB_OK; ++a) {
+        int64_t B = 1;
+        for (int b = a + 1; b < rank; ++b) B *= n;
+        const int64_t A = total / (n * B);
+        std::fill(hf.begin(), hf.end(), firsts ? firsts[a] : 0);
+        std::fill(hd.begin(), hd.end(), drifts ? drifts[a] : 0.0);
+        LOB_CUDA_TRY(ctx, cudaMemcpyAsync(dfirst, hf.data(), hf.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        LOB_CUDA_TRY(ctx, cudaMemcpyAsync(ddrift, hd.data(), hd.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+        LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));  // host vectors reused next axis
+        const double* lines_src = cur;
+        if (B > 1) {  // gather the axis' lines as contiguous rows
+            double* t = bufs[nb];
+            nb ^= 1;
+            if ((st = launch_transpose_batched(ctx, cur, t, A, n, B, s))) break;
+            lines_src = t;
+        }
+        double* dst = bufs[nb];
+        nb ^= 1;
+        const double* kt = ktabs ? ktabs + a * W : nullptr;
+        if (engine == LOB_ENGINE_DIRECT)
+            st = launch_direct_f64(ctx, lines_src, dst, lines, n, kt, 0, dfirst, nullptr, 0, s);
+        else if (engine == LOB_ENGINE_RELAXED)
+            st = launch_relaxed_f64(ctx, lines_src, dst, lines, n, kt, 0, dfirst, nullptr, 0, eta, nullptr, rws, rwsb, s);
+        else
+            st = launch_fast_f64(ctx, lines_src, dst, lines, n, ddrift, tau, nullptr, 0, 0.0, nullptr, workspace,
+                                 workspace_bytes, 0, s);
+        if (st) break;
+        cur = dst;
+        if (B > 1) {  // scatter back: rows (a, b) of length n -> (a, l, b)
+            double* back = bufs[nb];
+            nb ^= 1;
+            if ((st = launch_transpose_batched(ctx, cur, back, A, B, n, s))) break;
+            cur = back;
+        }
+    }
+    if (st == LOB_OK && tv) st = launch_sub_table(ctx, const_cast<double*>(cur), tv, total, s);
+    if (st == LOB_OK && cur != out)
+        st = cuda_status(ctx, cudaMemcpyAsync(out, cur, static_cast<size_t>(total) * sizeof(double),
+                                              cudaMemcpyDeviceToDevice, s), "split_step_nd copy");
+    cudaFreeAsync(dfirst, s);
+    cudaFreeAsync(ddrift, s);
+    if (rws) cudaFreeAsync(rws, s);
+    LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    return st;
+}
+
 }  // extern "C"

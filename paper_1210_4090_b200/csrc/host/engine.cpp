@@ -620,4 +620,74 @@ GridFn Engine::step_semidiscrete(const GridFn& u, double t, double drift, const 
     return GridFn{std::move(out), u.step, u.origin, u.periodic};
 }
 
+// ---- split_step_nd for any rank -------------------------------------------------
+
+TensorFn Engine::split_step_nd(const TensorFn& u, double t, const SplitSpecND& spec, const SchemeParams& params,
+                               ConvEngine engine) {
+    // proj/src/splitting.cpp:37-49 validation
+    const std::size_t rank = u.dims.size();
+    if (spec.kernels.size() != rank)
+        throw InvalidInput("split_step_nd: kinetic part is not separable over the tensor axes");
+    if (u.step != params.epsilon()) throw InvalidInput("split_step_nd: tensor step does not match params.epsilon()");
+    if (!u.periodic) throw InvalidInput("laxol_b200 split_step_nd: periodic tensors only");
+    for (std::size_t d : u.dims)
+        if (d != static_cast<std::size_t>(params.n_space))
+            throw InvalidInput("split_step_nd: periodic axes must hold one unit period");
+    if (u.origins.size() != rank) throw InvalidInput("split_step_nd: one origin per axis");
+    const int64_t n = params.n_space, W = 2 * n + 1;
+    std::size_t total = u.values.size();
+    bool mech = true;
+    for (const KernelWindow& k : spec.kernels) {
+        if (k.n_space != n || static_cast<int64_t>(k.window.size()) != W)
+            throw InvalidInput("split_step_nd: kernel window does not match n_space");
+        mech = mech && k.mechanical;
+    }
+    int code;
+    if (engine == ConvEngine::GpuDirect) code = LOB_ENGINE_DIRECT;
+    else if (engine == ConvEngine::GpuFast) code = (params.eta > 0.0 || !mech) ? LOB_ENGINE_RELAXED : LOB_ENGINE_FAST;
+    else code = engine_code(engine);
+    std::vector<double> kt(static_cast<size_t>(rank * W));
+    std::vector<int64_t> firsts(rank);
+    std::vector<double> drifts(rank);
+    for (std::size_t a = 0; a < rank; ++a) {
+        std::copy(spec.kernels[a].window.begin(), spec.kernels[a].window.end(), kt.begin() + a * W);
+        firsts[a] = spec.kernels[a].first;
+        drifts[a] = spec.kernels[a].drift;
+    }
+    // tau*V per point in the reference's coordinates (proj/src/splitting.cpp:85-97)
+    std::vector<double> tv;
+    if (spec.potential) {
+        tv.resize(total);
+        const double tt = potential_time(t, params);
+        std::vector<std::size_t> strides(rank, 1);
+        for (std::size_t a = rank; a-- > 1;) strides[a - 1] = strides[a] * u.dims[a];
+        std::vector<double> coords(rank);
+        for (std::size_t flat = 0; flat < total; ++flat) {
+            std::size_t rem = flat;
+            for (std::size_t a = 0; a < rank; ++a) {
+                const std::size_t idx = rem / strides[a];
+                rem %= strides[a];
+                coords[a] = u.origins[a] + static_cast<double>(idx) * u.step;
+            }
+            const double v = spec.potential(tt, coords);
+            if (!std::isfinite(v)) throw EvaluationError("split_step_nd: potential sample is not finite");
+            tv[flat] = params.tau * v;
+        }
+    }
+    DevBuf<double> du(total), dout(total), dtmp(total), dk(kt.size()), dtv(tv.size());
+    du.upload(u.values.data(), total);
+    dk.upload(kt.data(), kt.size());
+    if (!tv.empty()) dtv.upload(tv.data(), tv.size());
+    size_t wsb = 0;
+    lob_fast_workspace_bytes(static_cast<int64_t>(total / n), n, &wsb);
+    DevBuf<unsigned char> ws(code == LOB_ENGINE_FAST ? wsb : 0);
+    check_status(lob_split_step_nd_f64(ctx_, du.p, dout.p, dtmp.p, static_cast<int>(rank), n, params.tau, dk.p,
+                                       firsts.data(), drifts.data(), tv.empty() ? nullptr : dtv.p, params.eta, code,
+                                       ws.p, wsb, nullptr),
+                 ctx_, "split_step_nd");
+    TensorFn out = u;
+    dout.download(out.values.data(), total);
+    return out;
+}
+
 }  // namespace laxol_b200

@@ -149,6 +149,12 @@ struct SplitSpec2D {
     double drift1 = 0.0, drift2 = 0.0;
     SeparablePotential2D potential;
 };
+// proj/include/laxol/splitting.hpp:20-33 for any rank: one kernel window per axis (mechanical
+// or tabulated) and PotentialNd(t, coords) evaluated on the host per grid point
+struct SplitSpecND {
+    std::vector<KernelWindow> kernels;
+    std::function<double(double, std::span<const double>)> potential;  // empty = V == 0
+};
 
 // proj/include/laxol/weakkam.hpp:12-29
 struct EffectiveHEstimate {
@@ -191,6 +197,10 @@ public:
     // proj/src/splitting.cpp:37-99
     TensorFn split_step_nd(const TensorFn& u, double t, const SplitSpec2D& spec,
                            const SchemeParams& params,
+                           ConvEngine engine = ConvEngine::GpuDirect);
+
+    // proj/src/splitting.cpp:37-99 for periodic tensors of any rank (all axes n_space)
+    TensorFn split_step_nd(const TensorFn& u, double t, const SplitSpecND& spec, const SchemeParams& params,
                            ConvEngine engine = ConvEngine::GpuDirect);
 
     // Weak-KAM consumers (proj/src/weakkam.cpp), the step and the products on the device.

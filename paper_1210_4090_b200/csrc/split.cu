@@ -10,6 +10,8 @@
 // out = out - tau*V (two roundings, no FMA; proj/src/splitting.cpp:95).
 // Also: the per-step drift / finiteness check of evolve
 // (proj/src/scheme.cpp:244-264).
+#include <algorithm>
+
 #include "lob_internal.cuh"
 
 namespace lob {
@@ -76,7 +78,54 @@ __global__ void __launch_bounds__(256) drift_kernel(const double* __restrict__ n
     }
 }
 
+// dst[a][b][l] = src[a][l][b] for a < A, l < L, b < B (32x32 tiles of the (L, B) planes)
+__global__ void __launch_bounds__(256) transpose_batched_kernel(const double* __restrict__ src,
+                                                                double* __restrict__ dst, int64_t A, int64_t L,
+                                                                int64_t B) {
+    __shared__ double tile[kTD][kTD + 1];
+    const int64_t b0 = static_cast<int64_t>(blockIdx.x) * kTD;  // column block (b)
+    const int64_t l0 = static_cast<int64_t>(blockIdx.y) * kTD;  // row block (l)
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int64_t a = blockIdx.z; a < A; a += gridDim.z) {
+        const double* sa = src + a * L * B;
+        double* da = dst + a * L * B;
+        for (int r = ty; r < kTD; r += 8) {
+            const int64_t l = l0 + r, b = b0 + tx;
+            if (l < L && b < B) tile[r][tx] = sa[l * B + b];
+        }
+        __syncthreads();
+        for (int r = ty; r < kTD; r += 8) {
+            const int64_t b = b0 + r, l = l0 + tx;
+            if (l < L && b < B) da[b * L + l] = tile[tx][r];
+        }
+        __syncthreads();
+    }
+}
+
+// out[i] -= tv[i] (tau*V of every grid point, rounded on the host): one IEEE subtraction
+__global__ void sub_table_kernel(double* __restrict__ out, const double* __restrict__ tv, int64_t count) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = __dsub_rn(out[i], tv[i]);
+}
+
 }  // namespace
+
+int launch_transpose_batched(lob_ctx* ctx, const double* src, double* dst, int64_t A, int64_t L, int64_t B,
+                             cudaStream_t s) {
+    const dim3 grid(static_cast<unsigned>((B + kTD - 1) / kTD), static_cast<unsigned>((L + kTD - 1) / kTD),
+                    static_cast<unsigned>(std::min<int64_t>(A, 65535)));
+    transpose_batched_kernel<<<grid, 256, 0, s>>>(src, dst, A, L, B);
+    ctx->launches += 1;
+    return cuda_status(ctx, cudaGetLastError(), "transpose_batched_kernel");
+}
+
+int launch_sub_table(lob_ctx* ctx, double* out, const double* tv, int64_t count, cudaStream_t s) {
+    const unsigned g = static_cast<unsigned>(std::min<int64_t>((count + 255) / 256, 148 * 32));
+    sub_table_kernel<<<g, 256, 0, s>>>(out, tv, count);
+    ctx->launches += 1;
+    return cuda_status(ctx, cudaGetLastError(), "sub_table_kernel");
+}
 
 int launch_transpose(lob_ctx* ctx, const double* src, double* dst, int64_t n, cudaStream_t s) {
     dim3 grid(static_cast<unsigned>((n + kTD - 1) / kTD), static_cast<unsigned>((n + kTD - 1) / kTD));

@@ -123,6 +123,7 @@ class Reference:
             "ref_decompose": (c_int64, [_P, c_int64, c_double, _P, _P, _P, c_int64]),
             "ref_conv": (c_int, [c_int, _P, c_int64, _P, c_int64, c_double, _P, _P]),
             "ref_minplus_product": (c_int, [_P, _P, c_int64, _P]),
+            "ref_split_step_nd": (c_int, [_P, c_int, c_int, c_double, _P, _P, c_double, c_double, _P]),
             "ref_kernel_tabulated": (c_int, [c_int, c_double, _P, c_int64, c_double, c_double, _P, POINTER(c_int64),
                                              POINTER(c_int64)]),
             "ref_convolve_tabulated": (c_int, [_P, c_int, c_double, _P, c_int64, c_double, c_double, c_double, c_int,
@@ -214,6 +215,17 @@ class Reference:
         st = self.lib.ref_conv(which, a.ctypes.data, a.size, b.ctypes.data, b.size, eta, out.ctypes.data,
                                ctypes.byref(blocks))
         return out, blocks.value, st
+
+    def split_step_nd(self, u, rank, n, tau, drifts, vtab=None, t=0.0, eta=0.0):
+        u = np.ascontiguousarray(u, np.float64).ravel()
+        d = np.ascontiguousarray(drifts, np.float64)
+        out = np.empty_like(u)
+        st = self.lib.ref_split_step_nd(u.ctypes.data, rank, n, tau, d.ctypes.data,
+                                        None if vtab is None else np.ascontiguousarray(vtab).ctypes.data, t, eta,
+                                        out.ctypes.data)
+        if st:
+            raise RuntimeError(self.err())
+        return out
 
     def kernel_tabulated(self, n, tau, samples, v0, dv):
         smp = np.ascontiguousarray(samples, np.float64)
