@@ -250,7 +250,52 @@ EvolutionTrace Engine::evolve(const GridFn& u0, double t0, int64_t steps, double
     if (steps < 0) throw InvalidInput("evolve: steps must be >= 0");
     check_u_grid(u0, params, "evolve");
     validate(params);
-    if (!u0.periodic) throw InvalidInput("laxol_b200 evolve: periodic domains only");
+    if (!u0.periodic) {
+        // windowed domain (proj/src/scheme.cpp:208-272 with kinetic_convolve's wall branch,
+        // :135-144): step by step through the windowed K1 kernel, the drift and the
+        // non-finite check on the host in the reference's order
+        const KernelWindow kernel = build_kernel_mech(params.n_space, params.tau, drift);
+        int64_t stride = options.snapshot_stride;
+        if (stride <= 0) stride = steps <= 1024 ? 1 : (steps + 1023) / 1024;
+        std::vector<int64_t> capture = options.capture_steps;
+        std::sort(capture.begin(), capture.end());
+        auto keep = [&](int64_t i) {
+            return i == 0 || i == steps || i % stride == 0 || std::binary_search(capture.begin(), capture.end(), i);
+        };
+        EvolutionTrace trace;
+        trace.times.push_back(t0);
+        trace.snapshot_steps.push_back(0);
+        trace.snapshots.push_back(u0);
+        GridFn u = u0;
+        for (int64_t i = 0; i < steps; ++i) {
+            const double t = t0 + static_cast<double>(i) * params.tau;
+            const auto started = std::chrono::steady_clock::now();
+            StepStats stats;
+            GridFn next = step_fully_discrete(u, t, V, params, kernel, ConvEngine::GpuDirect, &stats);
+            const std::chrono::duration<double> el = std::chrono::steady_clock::now() - started;
+            double d = 0.0;
+            bool finite = true;
+            for (std::size_t j = 0; j < u.size(); ++j) {
+                d += next.values[j] - u.values[j];
+                finite = finite && std::isfinite(next.values[j]);
+            }
+            d /= static_cast<double>(u.size());
+            const double t_next = t0 + static_cast<double>(i + 1) * params.tau;
+            trace.per_step.push_back({t_next, stats.block_count, d, el.count()});
+            u = std::move(next);
+            if (!finite || keep(i + 1)) {
+                trace.times.push_back(t_next);
+                trace.snapshot_steps.push_back(i + 1);
+                trace.snapshots.push_back(u);
+            }
+            if (!finite) {
+                trace.completed = false;
+                trace.abort_reason = "non-finite value after step " + std::to_string(i + 1);
+                break;
+            }
+        }
+        return trace;
+    }
     const int code = engine_code(options.engine, params.eta);
     const int64_t n = params.n_space;
 
