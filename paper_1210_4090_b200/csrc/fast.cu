@@ -786,20 +786,26 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
         tvv[kPer] = (tvl && tid < 3) ? __ldg(tvl + jh) : 0.0;
         double* ol = out + line * p.n + j0;
         unsigned miss = 0;
+        // best - tv with tv = 0 when there is no potential: the same double (x - 0 == x, -0 - 0 == -0)
+        const int pb = P8(1 + tid);  // P8(1 + tid + kNT m) = pb + (kNT + kNT / 8) m
 #pragma unroll
-        for (int m = 0; m <= kPer; ++m) {
-            const int i = m < kPer ? 1 + tid + kNT * m : ih;
-            if (m < kPer ? (FULL || i <= Tl) : tid < 3) {
+        for (int m = 0; m < kPer; ++m) {
+            const int i = 1 + tid + kNT * m;
+            if (FULL || i <= Tl) {
                 const unsigned long long kk = S.keys[i];
-                if (kk != kInfBits) {
-                    const double best = __longlong_as_double(static_cast<long long>(kk));
-                    const double o = tvl ? __dsub_rn(best, tvv[m]) : best;
-                    vals[P8(i)] = o;
-                    if (m < kPer) ol[i - 1] = o;
-                } else {
-                    miss |= 1u << m;
-                }
+                // an empty slot (+inf) is stored too and rewritten by the cold scan below
+                const double o = __dsub_rn(__longlong_as_double(static_cast<long long>(kk)), tvv[m]);
+                vals[pb + (kNT + kNT / 8) * m] = o;
+                ol[i - 1] = o;
+                miss |= static_cast<unsigned>(kk == kInfBits) << m;
             }
+        }
+        if (tid < 3) {
+            const unsigned long long kk = S.keys[ih];
+            if (kk != kInfBits)
+                vals[P8(ih)] = __dsub_rn(__longlong_as_double(static_cast<long long>(kk)), tvv[kPer]);
+            else
+                miss |= 1u << kPer;
         }
         while (miss) {  // cold
             const int m = __ffs(miss) - 1;
@@ -807,7 +813,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
             const int i = m < kPer ? 1 + tid + kNT * m : ih;
             const int j = m < kPer ? j0 + i - 1 : jh;
             const double best = scan(j);
-            const double o = tvl ? __dsub_rn(best, __ldg(tvl + j)) : best;
+            const double o = __dsub_rn(best, tvl ? __ldg(tvl + j) : 0.0);
             vals[P8(i)] = o;
             if (m < kPer) ol[i - 1] = o;
         }
