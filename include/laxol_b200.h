@@ -159,6 +159,13 @@ int lob_split_step_nd_f64(lob_ctx* ctx, const double* u, double* out, double* tm
                           const double* ktabs, const int64_t* firsts, const double* drifts, const double* tv,
                           double eta, int engine, void* workspace, size_t workspace_bytes, void* stream);
 
+/* The same for a windowed (non-periodic) tensor of dims[0] x ... x dims[rank-1] samples:
+ * each axis swept with the wall branch of kinetic_convolve (K1 windowed, exact;
+ * LOB_EVALUATION_ERROR when a grid index has no candidate, proj/src/scheme.cpp:138-141). */
+int lob_split_step_nd_window_f64(lob_ctx* ctx, const double* u, double* out, double* tmp, int rank,
+                                 const int64_t* dims, int64_t n, double tau, const double* ktabs,
+                                 const int64_t* firsts, const double* tv, void* stream);
+
 /* The potential pass of K3 on a rows x n row slab (the multi-GPU split step's
  * rows [r0, r0 + rows) of an n x n tensor): out[i][k] -= tau*(a1[i]*a2[k] + b),
  * each product / sum one IEEE rounding (a1 points at the slab's first row). */

@@ -401,4 +401,33 @@ int ref_split_step_nd(const double* u, int rank, int n_space, double tau, const 
     });
 }
 
+// split_step_nd of a windowed (non-periodic) tensor dims[0] x ... with origins, mechanical(drifts[a])
+// per axis and V a full table indexed by llround((x_a - origin_a) / step).
+int ref_split_step_nd_window(const double* u, int rank, const int64_t* dims, const double* origins, int n_space,
+                             double tau, const double* drifts, const double* vtab, double t, double* out) {
+    return guarded([&] {
+        const SchemeParams p = params_of(n_space, tau, 0.0);
+        std::vector<std::size_t> d(dims, dims + rank);
+        std::size_t total = 1;
+        for (std::size_t x : d) total *= x;
+        const TensorFn tu = make_tensor(std::vector<double>(u, u + total), d, p.epsilon(),
+                                        std::vector<double>(origins, origins + rank), false);
+        SplitSpec spec;
+        for (int a = 0; a < rank; ++a) spec.kinetics.push_back(mechanical(drifts[a]));
+        if (vtab) {
+            std::vector<double> tab(vtab, vtab + total);
+            std::vector<double> org(origins, origins + rank);
+            const double step = p.epsilon();
+            spec.potential = [tab, step, d, org](double, std::span<const double> x) {
+                std::size_t flat = 0;
+                for (std::size_t a = 0; a < x.size(); ++a)
+                    flat = flat * d[a] + static_cast<std::size_t>(std::llround((x[a] - org[a]) / step));
+                return tab[flat];
+            };
+        }
+        const TensorFn r = split_step_nd(tu, t, spec, p);
+        std::memcpy(out, r.values.data(), total * sizeof(double));
+    });
+}
+
 }  // extern "C"

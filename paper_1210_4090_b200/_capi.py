@@ -81,6 +81,7 @@ SIGNATURES = {
                                         _P, c_size_t, _P]),
     "lob_split_step_nd_f64": (c_int, [_P, _P, _P, _P, c_int, c_int64, c_double, _P, _P, _P, _P, c_double, c_int,
                                       _P, c_size_t, _P]),
+    "lob_split_step_nd_window_f64": (c_int, [_P, _P, _P, _P, c_int, _P, c_int64, c_double, _P, _P, _P, _P]),
     "lob_potential2d_rows_f64": (c_int, [_P, _P, c_int64, c_int64, _P, _P, c_double, c_double, _P]),
     # synthetic workloads (include/laxol_b200_configs.h)
     "lob_gen_sin": (None, [c_int64, _P]),

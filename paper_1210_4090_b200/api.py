@@ -239,6 +239,17 @@ class Device:
                                             ws_bytes, _stream_ptr(stream))
         self._check(st, "lob_split_step_nd_f64")
 
+    def split_step_nd_window(self, u, out, tmp, dims, n, tau, kernels, tv=None, stream=None):
+        """split_step_nd of a windowed tensor (walls) of shape dims (device doubles, row-major)."""
+        import torch
+        rank = len(dims)
+        kt = torch.from_numpy(np.concatenate([k.window for k in kernels])).to(u.device)
+        fr = (ctypes.c_int64 * rank)(*[int(k.first) for k in kernels])
+        dm = (ctypes.c_int64 * rank)(*[int(x) for x in dims])
+        st = self.lib.lob_split_step_nd_window_f64(self.ctx, _ptr(u), _ptr(out), _ptr(tmp), rank, dm, int(n),
+                                                   float(tau), _ptr(kt), fr, _ptr(tv), _stream_ptr(stream))
+        self._check(st, "lob_split_step_nd_window_f64")
+
     def evolve(self, u, scratch, drift, tau, steps, tv=None, tv_stride=0, eta=0.0,
                engine=ENGINE_FAST, step_drift=None, step_blocks=None, workspace=None, stream=None):
         lines, n = u.shape

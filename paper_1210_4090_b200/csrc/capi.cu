@@ -610,4 +610,77 @@ int lob_split_step_nd_f64(lob_ctx* ctx, const double* u, double* out, double* tm
     return st;
 }
 
+int lob_split_step_nd_window_f64(lob_ctx* ctx, const double* u, double* out, double* tmp, int rank,
+                                 const int64_t* dims, int64_t n, double tau, const double* ktabs,
+                                 const int64_t* firsts, const double* tv, void* stream) {
+    if (!ctx) return LOB_INVALID_INPUT;
+    if (rank < 1 || rank > 8 || n < 1 || !dims || !ktabs || !firsts)
+        return set_error(ctx, LOB_INVALID_INPUT, "split_step_nd (windowed): bad arguments");
+    if (!u || !out || !tmp || u == out || u == tmp || out == tmp)
+        return set_error(ctx, LOB_INVALID_INPUT, "split_step_nd: need distinct u/out/tmp");
+    (void)tau;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int64_t total = 1;
+    for (int a = 0; a < rank; ++a) {
+        if (dims[a] < 1) return set_error(ctx, LOB_INVALID_INPUT, "make_tensor: empty axis");
+        total *= dims[a];
+    }
+    const int64_t W = 2 * n + 1;
+    int64_t* dfirst = nullptr;
+    int* d_err = nullptr;
+    int64_t maxlines = 0;
+    for (int a = 0; a < rank; ++a) maxlines = std::max(maxlines, total / dims[a]);
+    LOB_CUDA_TRY(ctx, cudaMallocAsync(&dfirst, static_cast<size_t>(maxlines) * sizeof(int64_t), s));
+    LOB_CUDA_TRY(ctx, cudaMallocAsync(&d_err, sizeof(int), s));
+    LOB_CUDA_TRY(ctx, cudaMemsetAsync(d_err, 0, sizeof(int), s));
+    std::vector<int64_t> hf(static_cast<size_t>(maxlines));
+    const double* cur = u;
+    double* bufs[2] = {out, tmp};
+    int nb = 0;
+    int st = LOB_OK;
+    // proj/src/splitting.cpp:53-77 with kinetic_convolve's wall branch (proj/src/scheme.cpp:135-144)
+    for (int a = 0; a < rank && st == LOB_OK; ++a) {
+        const int64_t L = dims[a];
+        int64_t B = 1;
+        for (int b = a + 1; b < rank; ++b) B *= dims[b];
+        const int64_t A = total / (L * B), lines = A * B;
+        if (lines > 65535) {
+            st = set_error(ctx, LOB_INVALID_INPUT, "split_step_nd (windowed): more than 65535 lines per axis");
+            break;
+        }
+        std::fill(hf.begin(), hf.begin() + lines, firsts[a]);
+        LOB_CUDA_TRY(ctx, cudaMemcpyAsync(dfirst, hf.data(), lines * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+        const double* src = cur;
+        if (B > 1) {
+            double* t = bufs[nb];
+            nb ^= 1;
+            if ((st = launch_transpose_batched(ctx, cur, t, A, L, B, s))) break;
+            src = t;
+        }
+        double* dst = bufs[nb];
+        nb ^= 1;
+        if ((st = launch_window_f64(ctx, src, dst, lines, L, n, ktabs + a * W, 0, dfirst, nullptr, 0, d_err, s))) break;
+        cur = dst;
+        if (B > 1) {
+            double* back = bufs[nb];
+            nb ^= 1;
+            if ((st = launch_transpose_batched(ctx, cur, back, A, B, L, s))) break;
+            cur = back;
+        }
+    }
+    if (st == LOB_OK && tv) st = launch_sub_table(ctx, const_cast<double*>(cur), tv, total, s);
+    if (st == LOB_OK && cur != out)
+        st = cuda_status(ctx, cudaMemcpyAsync(out, cur, static_cast<size_t>(total) * sizeof(double),
+                                              cudaMemcpyDeviceToDevice, s), "split_step_nd copy");
+    int herr = 0;
+    if (st == LOB_OK) LOB_CUDA_TRY(ctx, cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+    cudaFreeAsync(dfirst, s);
+    cudaFreeAsync(d_err, s);
+    LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    if (st) return st;
+    if (herr) return set_error(ctx, LOB_EVALUATION_ERROR, "kinetic_convolve: kernel window does not reach a grid index");
+    return LOB_OK;
+}
+
 }  // extern "C"

@@ -674,10 +674,10 @@ TensorFn Engine::split_step_nd(const TensorFn& u, double t, const SplitSpecND& s
     if (spec.kernels.size() != rank)
         throw InvalidInput("split_step_nd: kinetic part is not separable over the tensor axes");
     if (u.step != params.epsilon()) throw InvalidInput("split_step_nd: tensor step does not match params.epsilon()");
-    if (!u.periodic) throw InvalidInput("laxol_b200 split_step_nd: periodic tensors only");
-    for (std::size_t d : u.dims)
-        if (d != static_cast<std::size_t>(params.n_space))
-            throw InvalidInput("split_step_nd: periodic axes must hold one unit period");
+    if (u.periodic)
+        for (std::size_t d : u.dims)
+            if (d != static_cast<std::size_t>(params.n_space))
+                throw InvalidInput("split_step_nd: periodic axes must hold one unit period");
     if (u.origins.size() != rank) throw InvalidInput("split_step_nd: one origin per axis");
     const int64_t n = params.n_space, W = 2 * n + 1;
     std::size_t total = u.values.size();
@@ -723,6 +723,16 @@ TensorFn Engine::split_step_nd(const TensorFn& u, double t, const SplitSpecND& s
     du.upload(u.values.data(), total);
     dk.upload(kt.data(), kt.size());
     if (!tv.empty()) dtv.upload(tv.data(), tv.size());
+    if (!u.periodic) {  // walls: the exact windowed sweeps
+        std::vector<int64_t> dims(u.dims.begin(), u.dims.end());
+        check_status(lob_split_step_nd_window_f64(ctx_, du.p, dout.p, dtmp.p, static_cast<int>(rank), dims.data(), n,
+                                                  params.tau, dk.p, firsts.data(), tv.empty() ? nullptr : dtv.p,
+                                                  nullptr),
+                     ctx_, "split_step_nd");
+        TensorFn out = u;
+        dout.download(out.values.data(), total);
+        return out;
+    }
     size_t wsb = 0;
     lob_fast_workspace_bytes(static_cast<int64_t>(total / n), n, &wsb);
     DevBuf<unsigned char> ws(code == LOB_ENGINE_FAST ? wsb : 0);

@@ -124,6 +124,7 @@ class Reference:
             "ref_conv": (c_int, [c_int, _P, c_int64, _P, c_int64, c_double, _P, _P]),
             "ref_minplus_product": (c_int, [_P, _P, c_int64, _P]),
             "ref_split_step_nd": (c_int, [_P, c_int, c_int, c_double, _P, _P, c_double, c_double, _P]),
+            "ref_split_step_nd_window": (c_int, [_P, c_int, _P, _P, c_int, c_double, _P, _P, c_double, _P]),
             "ref_kernel_tabulated": (c_int, [c_int, c_double, _P, c_int64, c_double, c_double, _P, POINTER(c_int64),
                                              POINTER(c_int64)]),
             "ref_convolve_tabulated": (c_int, [_P, c_int, c_double, _P, c_int64, c_double, c_double, c_double, c_int,
@@ -226,6 +227,18 @@ class Reference:
         if st:
             raise RuntimeError(self.err())
         return out
+
+    def split_step_nd_window(self, u, n_space, tau, drifts, origins, vtab=None, t=0.0):
+        u = np.ascontiguousarray(u, np.float64)
+        dims = np.ascontiguousarray(u.shape, np.int64)
+        org = np.ascontiguousarray(origins, np.float64)
+        d = np.ascontiguousarray(drifts, np.float64)
+        out = np.empty(u.size)
+        st = self.lib.ref_split_step_nd_window(u.ctypes.data, u.ndim, dims.ctypes.data, org.ctypes.data, n_space,
+                                               tau, d.ctypes.data,
+                                               None if vtab is None else np.ascontiguousarray(vtab).ctypes.data,
+                                               t, out.ctypes.data)
+        return out, st
 
     def kernel_tabulated(self, n, tau, samples, v0, dv):
         smp = np.ascontiguousarray(samples, np.float64)

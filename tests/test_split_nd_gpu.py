@@ -58,3 +58,22 @@ def test_split_nd_rank2_matches_the_2d_entry(dev):
     v = a1[:, None] * a2[None, :] + b  # the same two IEEE roundings as the device (product, sum)
     got = _run(dev, u, 2, n, tau, [d1, d2], tau * v, 0.0, api.ENGINE_DIRECT)
     assert np.array_equal(got, out.cpu().numpy().ravel())
+
+
+@pytest.mark.parametrize("dims,n,tau", [((40,), 16, 0.25), ((20, 30), 16, 0.25), ((12, 16, 10), 8, 0.25)])
+def test_split_nd_windowed_equals_reference(dev, ref, dims, n, tau):
+    """walls (non-periodic tensors, proj/src/splitting.cpp:66-76 with scheme.cpp:135-144)"""
+    import torch
+
+    rng = np.random.default_rng(sum(dims))
+    u = rng.uniform(-1, 1, dims)
+    origins = [-0.5, 0.25, 0.0][:len(dims)]
+    drifts = [0.0, 0.5, -0.25][:len(dims)]
+    v = rng.uniform(-1, 1, dims)
+    want, st = ref.split_step_nd_window(u, n, tau, drifts, origins, vtab=v)
+    assert st == 0
+    du = torch.from_numpy(u.ravel().copy()).cuda()
+    out, tmp = torch.empty_like(du), torch.empty_like(du)
+    ks = [dev.build_kernel(n, tau, d) for d in drifts]
+    dev.split_step_nd_window(du, out, tmp, dims, n, tau, ks, tv=torch.from_numpy((tau * v).ravel()).cuda())
+    assert np.array_equal(out.cpu().numpy(), want)
