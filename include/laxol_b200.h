@@ -326,6 +326,23 @@ int lob_minplus_relaxed_f64(lob_ctx* ctx, const double* u, double* out, int64_t 
                             const double* tv, int64_t tv_stride, double eta, int64_t* blocks,
                             void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- The reference's min-plus primitives on plain sequences (proj/include/laxol/minplus.hpp) ----
+ * conv_naive (proj/src/minplus.cpp:116-126): out[k] = min_{i+j=k} f[i] + g[j], nf + ng - 1
+ * outputs (device buffers), the reference's loop order (i ascending, strict "<"). */
+int lob_minplus_conv_naive_f64(lob_ctx* ctx, const double* f, int64_t nf, const double* g, int64_t ng,
+                               double* out, void* stream);
+/* decompose (proj/src/minplus.cpp:152-188) of m device samples with tolerance eta: the block
+ * list (kinds 0 convex / 1 concave, [start, end] sample ranges sharing boundary samples) up
+ * to `capacity` entries on the host, *count = the number of blocks.  Synchronous. */
+int lob_decompose_f64(lob_ctx* ctx, const double* u, int64_t m, double eta, int* kinds, int64_t* starts,
+                      int64_t* ends, int64_t capacity, int64_t* count, void* stream);
+/* conv_fast (proj/src/minplus.cpp:190-252) of a convex kernel (nk device samples) with a plain
+ * sequence (nu device samples): out[nk + nu - 1] (device), *blocks (host) = the block count
+ * (capped for eta > 0).  For eta > 0 the reference's relaxed approximation, bit for bit.
+ * Synchronous (min_pointwise's gap check -> LOB_INVALID_INPUT). */
+int lob_conv_fast_f64(lob_ctx* ctx, const double* kern, int64_t nk, const double* u, int64_t nu, double eta,
+                      double* out, int64_t* blocks, void* stream);
+
 /* Number of kernel launches issued by this context since creation. */
 int64_t lob_launch_count(const lob_ctx* ctx);
 

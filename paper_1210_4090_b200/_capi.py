@@ -83,6 +83,9 @@ SIGNATURES = {
                                       _P, c_size_t, _P]),
     "lob_split_step_nd_window_f64": (c_int, [_P, _P, _P, _P, c_int, _P, c_int64, c_double, _P, _P, _P, _P]),
     "lob_potential2d_rows_f64": (c_int, [_P, _P, c_int64, c_int64, _P, _P, c_double, c_double, _P]),
+    "lob_minplus_conv_naive_f64": (c_int, [_P, _P, c_int64, _P, c_int64, _P, _P]),
+    "lob_decompose_f64": (c_int, [_P, _P, c_int64, c_double, _P, _P, _P, c_int64, POINTER(c_int64), _P]),
+    "lob_conv_fast_f64": (c_int, [_P, _P, c_int64, _P, c_int64, c_double, _P, POINTER(c_int64), _P]),
     # synthetic workloads (include/laxol_b200_configs.h)
     "lob_gen_sin": (None, [c_int64, _P]),
     "lob_gen_cos": (None, [c_int64, _P]),

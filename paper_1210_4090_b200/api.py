@@ -298,6 +298,34 @@ class Device:
                                               _ptr(workspace), ws_bytes, _stream_ptr(stream))
         self._check(st, "lob_minplus_relaxed_f64")
 
+    # ---- min-plus primitives on plain sequences (proj/include/laxol/minplus.hpp) ----
+    def conv_naive(self, f, g, out, stream=None):
+        st = self.lib.lob_minplus_conv_naive_f64(self.ctx, _ptr(f), f.numel(), _ptr(g), g.numel(), _ptr(out),
+                                                 _stream_ptr(stream))
+        self._check(st, "lob_minplus_conv_naive_f64")
+
+    def decompose(self, u, eta=0.0, stream=None):
+        """[(kind, start, end)] with kind 0 convex / 1 concave (proj/src/minplus.cpp:152-188)."""
+        m = u.numel()
+        cap = max(m, 1)
+        kinds = np.empty(cap, np.int32)
+        starts = np.empty(cap, np.int64)
+        ends = np.empty(cap, np.int64)
+        cnt = ctypes.c_int64()
+        st = self.lib.lob_decompose_f64(self.ctx, _ptr(u), m, float(eta), kinds.ctypes.data, starts.ctypes.data,
+                                        ends.ctypes.data, cap, ctypes.byref(cnt), _stream_ptr(stream))
+        self._check(st, "lob_decompose_f64")
+        c = int(cnt.value)
+        return kinds[:c], starts[:c], ends[:c]
+
+    def conv_fast(self, kern, u, out, eta=0.0, stream=None) -> int:
+        """conv_fast (proj/src/minplus.cpp:190-252); returns the block count."""
+        b = ctypes.c_int64()
+        st = self.lib.lob_conv_fast_f64(self.ctx, _ptr(kern), kern.numel(), _ptr(u), u.numel(), float(eta),
+                                        _ptr(out), ctypes.byref(b), _stream_ptr(stream))
+        self._check(st, "lob_conv_fast_f64")
+        return int(b.value)
+
     # ---- step_semidiscrete (proj/src/scheme.cpp:166-206) -----------------------
     def step_semidiscrete(self, u, out, ktab, first, t, tau, potential=None, quad_points=1, periodic=True,
                           origin=0.0, n_space=None, stream=None):

@@ -31,8 +31,11 @@
 //
 // Work is O(pieces x n) like the reference's conv_fast (every piece is
 // merged with the whole window): a parity engine, not a fast path.
+#include <algorithm>
+#include <climits>
 #include <cmath>
 #include <string>
+#include <vector>
 
 #include "lob_internal.cuh"
 
@@ -76,16 +79,20 @@ RelaxedWs relaxed_layout(void* base, int64_t lines, int64_t n) {
 // proj/src/minplus.cpp:152-188, one thread per line; blocks are emitted as
 // pieces of at most kCap slopes.  blocks_out: capped count for eta > 0
 // (capped_blocks), the decomposition's own count for eta == 0.
+// n = slopes of the line: the period (periodic: samples u[0..n-1], u[n] = u[0]) or the
+// samples - 1 of a plain sequence; cap = 48 (the relaxed walk's pieces) or INT_MAX (decompose).
 __global__ void relaxed_decompose_kernel(const double* __restrict__ u, int64_t lines, int64_t n, double eta,
                                          int2* __restrict__ pieces, int* __restrict__ npieces,
-                                         int64_t* __restrict__ blocks_out, int* __restrict__ flag) {
+                                         int64_t* __restrict__ blocks_out, int* __restrict__ flag,
+                                         int periodic = 1, int64_t cap = kCap) {
     const int64_t line = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (line >= lines) return;
-    const double* ul = u + line * n;
+    const int64_t ls = periodic ? n : n + 1;  // samples stored per line
+    const double* ul = u + line * ls;
     int2* pl = pieces + line * n;
-    auto val = [&](int64_t i) { return ul[i == n ? 0 : i]; };
+    auto val = [&](int64_t i) { return ul[periodic && i == n ? 0 : i]; };
     auto slope = [&](int64_t i) { return __dsub_rn(val(i + 1), val(i)); };
-    for (int64_t i = 0; i < n; ++i)
+    for (int64_t i = 0; i < ls; ++i)
         if (!isfinite(ul[i])) atomicOr(flag, 2);
     int np = 0;
     int64_t nb = 0;
@@ -114,11 +121,11 @@ __global__ void relaxed_decompose_kernel(const double* __restrict__ u, int64_t l
             sp = se;
             ++e;
         }
-        for (int64_t s = b; s < e; s += kCap) {
-            pl[np++] = make_int2(static_cast<int>(s), static_cast<int>(min(e, s + kCap)) | (kind << 31));
+        for (int64_t s = b; s < e; s += cap) {
+            pl[np++] = make_int2(static_cast<int>(s), static_cast<int>(min(e, s + cap)) | (kind << 31));
             ++nb;
         }
-        if (eta <= 0.0) nb -= (e - b + kCap - 1) / kCap - 1;  // eta == 0: blocks are not capped
+        if (eta <= 0.0) nb -= (e - b + cap - 1) / cap - 1;  // eta == 0: blocks are not capped
         b = e;
     }
     npieces[line] = np;
@@ -142,25 +149,28 @@ __device__ __forceinline__ int count_below(const double* __restrict__ K, int cnt
 
 // One CTA per (line, piece-slot): merge / envelope of each piece with the
 // window, scattered into the line's conv keys with exact global min.
+// n: slopes of u (see the decompose kernel); nf: slopes of the kernel (2n for the step);
+// conv rows hold nf + n + 1 keys.
 __global__ void __launch_bounds__(kNTs) relaxed_scatter_kernel(const double* __restrict__ u, int64_t n,
                                                                const double* __restrict__ ktab,
                                                                int64_t ktab_stride, const int2* __restrict__ pieces,
                                                                const int* __restrict__ npieces,
-                                                               unsigned long long* __restrict__ conv) {
+                                                               unsigned long long* __restrict__ conv,
+                                                               int periodic = 1, int64_t nf_arg = -1) {
     __shared__ double gv[kCap + 1], gs[kCap];
     __shared__ int I[kCap + 1];  // merge: I_j; envelope: i_j (index 0 = P0)
     const int64_t line = blockIdx.y;
-    const double* ul = u + line * n;
+    const double* ul = u + line * (periodic ? n : n + 1);
     const double* K = ktab + line * ktab_stride;
-    const int nf = static_cast<int>(2 * n);  // kernel slopes
-    unsigned long long* cl = conv + line * (3 * n + 1);
+    const int nf = static_cast<int>(nf_arg < 0 ? 2 * n : nf_arg);  // kernel slopes
+    unsigned long long* cl = conv + line * (nf + n + 1);
     const int np = npieces[line];
     for (int p = blockIdx.x; p < np; p += gridDim.x) {
         const int2 pc = pieces[line * n + p];
         const int start = pc.x, end = pc.y & 0x7fffffff;
         const bool concave = pc.y < 0;
         const int m = end - start;
-        for (int t = threadIdx.x; t <= m; t += kNTs) gv[t] = ul[start + t == n ? 0 : start + t];
+        for (int t = threadIdx.x; t <= m; t += kNTs) gv[t] = ul[periodic && start + t == n ? 0 : start + t];
         __syncthreads();
         for (int t = threadIdx.x; t < m; t += kNTs) {
             gs[t] = __dsub_rn(gv[t + 1], gv[t]);
@@ -237,6 +247,33 @@ __global__ void relaxed_finalize_kernel(const unsigned long long* __restrict__ c
     out[line * n + j] = tv ? __dsub_rn(best, tv[line * tv_stride + j]) : best;
 }
 
+// plain (non-periodic) conv_fast: out[k] = the pointwise min of the parts, every position written
+// (min_pointwise's gap check, proj/src/minplus.cpp:271-272)
+__global__ void plain_finalize_kernel(const unsigned long long* __restrict__ conv, int64_t len, double* __restrict__ out,
+                                      int* __restrict__ flag) {
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < len;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const unsigned long long key = conv[k];
+        if (key == kEmpty) atomicOr(flag, 1);
+        out[k] = key == kEmpty ? INFINITY : dkey_inv(key);
+    }
+}
+
+// conv_naive (proj/src/minplus.cpp:116-126): out[k] = min over i + j = k of f[i] + g[j], i ascending
+__global__ void conv_naive_kernel(const double* __restrict__ f, int64_t nf, const double* __restrict__ g, int64_t ng,
+                                  double* __restrict__ out) {
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < nf + ng - 1;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double best = INFINITY;
+        const int64_t i0 = k - (ng - 1) > 0 ? k - (ng - 1) : 0, i1 = k < nf - 1 ? k : nf - 1;
+        for (int64_t i = i0; i <= i1; ++i) {
+            const double c = __dadd_rn(__ldg(f + i), __ldg(g + k - i));
+            best = c < best ? c : best;  // std::min(out[k], a[i] + b[j])
+        }
+        out[k] = best;
+    }
+}
+
 }  // namespace
 
 size_t relaxed_workspace_bytes(int64_t lines, int64_t n) { return relaxed_layout(nullptr, lines, n).total; }
@@ -287,4 +324,99 @@ extern "C" int lob_minplus_relaxed_f64(lob_ctx* ctx, const double* u, double* ou
     if (lines == 0) return LOB_OK;
     return launch_relaxed_f64(ctx, u, out, lines, n, ktab, ktab_stride, first, tv, tv_stride, eta, blocks, workspace,
                               workspace_bytes, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int lob_minplus_conv_naive_f64(lob_ctx* ctx, const double* f, int64_t nf, const double* g, int64_t ng,
+                                          double* out, void* stream) {
+    if (!ctx) return LOB_INVALID_INPUT;
+    if (nf < 1 || ng < 1 || !f || !g || !out) return set_error(ctx, LOB_INVALID_INPUT, "conv_naive: empty input");
+    const int64_t len = nf + ng - 1;
+    conv_naive_kernel<<<static_cast<unsigned>(std::min<int64_t>((len + 127) / 128, 148 * 16)), 128, 0,
+                        static_cast<cudaStream_t>(stream)>>>(f, nf, g, ng, out);
+    ctx->launches += 1;
+    return cuda_status(ctx, cudaGetLastError(), "conv_naive");
+}
+
+extern "C" int lob_decompose_f64(lob_ctx* ctx, const double* u, int64_t m, double eta, int* kinds, int64_t* starts,
+                                 int64_t* ends, int64_t capacity, int64_t* count, void* stream) {
+    if (!ctx || !count) return LOB_INVALID_INPUT;
+    if (!(eta >= 0.0)) return set_error(ctx, LOB_INVALID_INPUT, "decompose: eta must be >= 0");
+    if (m < 1 || !u) return set_error(ctx, LOB_INVALID_INPUT, "decompose: empty sample vector");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t ns = m - 1;  // slopes
+    if (ns == 0) {  // proj/src/minplus.cpp:158-161
+        *count = 1;
+        if (capacity >= 1) {
+            if (kinds) kinds[0] = 0;
+            if (starts) starts[0] = 0;
+            if (ends) ends[0] = 0;
+        }
+        return LOB_OK;
+    }
+    int2* pieces = nullptr;
+    int *np = nullptr, *flag = nullptr;
+    LOB_CUDA_TRY(ctx, cudaMallocAsync(&pieces, static_cast<size_t>(ns) * sizeof(int2), s));
+    LOB_CUDA_TRY(ctx, cudaMallocAsync(&np, 2 * sizeof(int), s));
+    flag = np + 1;
+    LOB_CUDA_TRY(ctx, cudaMemsetAsync(flag, 0, sizeof(int), s));
+    relaxed_decompose_kernel<<<1, 1, 0, s>>>(u, 1, ns, eta, pieces, np, nullptr, flag, 0, ns + 1);  // uncapped
+    ctx->launches += 1;
+    int hn = 0, hf = 0;
+    LOB_CUDA_TRY(ctx, cudaMemcpyAsync(&hn, np, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LOB_CUDA_TRY(ctx, cudaMemcpyAsync(&hf, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    std::vector<int2> hp(static_cast<size_t>(hn));
+    if (hn) LOB_CUDA_TRY(ctx, cudaMemcpy(hp.data(), pieces, hn * sizeof(int2), cudaMemcpyDeviceToHost));
+    cudaFree(pieces);
+    cudaFree(np);
+    *count = hn;
+    for (int64_t i = 0; i < hn && i < capacity; ++i) {
+        if (kinds) kinds[i] = hp[i].y < 0 ? 1 : 0;
+        if (starts) starts[i] = hp[i].x;
+        if (ends) ends[i] = hp[i].y & 0x7fffffff;
+    }
+    return LOB_OK;
+}
+
+extern "C" int lob_conv_fast_f64(lob_ctx* ctx, const double* kern, int64_t nk, const double* u, int64_t nu, double eta,
+                                 double* out, int64_t* blocks, void* stream) {
+    if (!ctx) return LOB_INVALID_INPUT;
+    if (!(eta >= 0.0)) return set_error(ctx, LOB_INVALID_INPUT, "decompose: eta must be >= 0");
+    if (nk < 2 || nu < 2 || !kern || !u || !out)
+        return set_error(ctx, LOB_INVALID_INPUT, "conv_fast: need at least two samples on each side");
+    if (nk + nu > (1ll << 30)) return set_error(ctx, LOB_INVALID_INPUT, "conv_fast: too long");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t m = nu - 1, nf = nk - 1, len = nf + m + 1;
+    unsigned long long* conv = nullptr;
+    int2* pieces = nullptr;
+    int *np = nullptr, *flag = nullptr;
+    int64_t* db = nullptr;
+    LOB_CUDA_TRY(ctx, cudaMallocAsync(&conv, static_cast<size_t>(len) * 8, s));
+    LOB_CUDA_TRY(ctx, cudaMallocAsync(&pieces, static_cast<size_t>(m) * sizeof(int2), s));
+    LOB_CUDA_TRY(ctx, cudaMallocAsync(&np, 2 * sizeof(int), s));
+    LOB_CUDA_TRY(ctx, cudaMallocAsync(&db, sizeof(int64_t), s));
+    flag = np + 1;
+    LOB_CUDA_TRY(ctx, cudaMemsetAsync(conv, 0xff, static_cast<size_t>(len) * 8, s));
+    LOB_CUDA_TRY(ctx, cudaMemsetAsync(flag, 0, sizeof(int), s));
+    // kernel convexity is the caller's contract (proj/src/minplus.cpp:190-194 require_convex)
+    relaxed_decompose_kernel<<<1, 1, 0, s>>>(u, 1, m, eta, pieces, np, db, flag, 0, kCap);
+    const unsigned gx = static_cast<unsigned>(std::min<int64_t>(m, std::max<int64_t>(1, 2 * ctx->sm_count)));
+    relaxed_scatter_kernel<<<dim3(gx, 1), kNTs, 0, s>>>(u, m, kern, 0, pieces, np, conv, 0, nf);
+    plain_finalize_kernel<<<static_cast<unsigned>(std::min<int64_t>((len + 255) / 256, 148 * 8)), 256, 0, s>>>(
+        conv, len, out, flag);
+    ctx->launches += 3;
+    int hf = 0;
+    LOB_CUDA_TRY(ctx, cudaGetLastError());
+    LOB_CUDA_TRY(ctx, cudaMemcpyAsync(&hf, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    int64_t hb = 0;
+    LOB_CUDA_TRY(ctx, cudaMemcpyAsync(&hb, db, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    cudaFreeAsync(conv, s);
+    cudaFreeAsync(pieces, s);
+    cudaFreeAsync(np, s);
+    cudaFreeAsync(db, s);
+    LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    if (blocks) *blocks = hb;
+    if (hf & 2) return set_error(ctx, LOB_INVALID_INPUT, "conv_fast: non-finite sample");
+    if (hf & 1) return set_error(ctx, LOB_INVALID_INPUT, "min_pointwise: index ranges leave a gap");
+    return LOB_OK;
 }
