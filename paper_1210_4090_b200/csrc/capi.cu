@@ -405,7 +405,10 @@ int lob_evolve_f64(lob_ctx* ctx, double* u, double* scratch, int64_t lines, int6
 }
 
 // line chunks of the pipelined host step (fast engine)
-constexpr int64_t kHostChunks = 8;  // <= 16 (two events per chunk in lob_ctx::aux_ev)
+#ifndef LOB_HOST_CHUNKS
+#define LOB_HOST_CHUNKS 8
+#endif
+constexpr int64_t kHostChunks = LOB_HOST_CHUNKS;  // <= 16 (two events per chunk in lob_ctx::aux_ev)
 
 int lob_step_host_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
                       const double* drift, double tau, const double* tv, int64_t tv_stride,
