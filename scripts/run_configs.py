@@ -266,10 +266,36 @@ def c5(dev, steps=200, checks=(1, 100, 199)):
             "blocks_per_line_final": {"mean": float(bl.mean()), "max": int(bl.max())}}
 
 
+def c2_karp(dev, n=512, count=16):
+    """C2's H-bar(P) two independent ways on the device at N = 512 (the period-matrix guard):
+    the whole-period drift estimator (estimate_hbar_drift, K2 steps) and Karp's min-plus
+    eigenvalue of the one-period matrix (build_period_matrix + eigenvalue_karp); the reference
+    checks the same agreement at N = 128 (proj/tests/acceptance.cpp:351-366)."""
+    tau = 0.02
+    ell = int(round(1 / tau))
+    v = api.gen_potential(2, n)
+    tv = api.tau_v(v, tau)
+    drifts = api.gen_c2_drifts(256)[np.linspace(0, 255, count).round().astype(int)]
+    rows = []
+    t0 = time.perf_counter()
+    for P in drifts:
+        est = dev.hbar_drift_host(np.zeros(n), float(P), tau, tv, api.ENGINE_FAST, 2000, 1e-11)
+        k = dev.build_kernel(n, tau, float(P))
+        kinc = dev_t(api.Device.period_kinetic(k))
+        C = torch.empty((n, n), dtype=torch.float64, device="cuda")
+        scr = torch.empty(2 * n * n, dtype=torch.float64, device="cuda")
+        dev.period_matrix(kinc, dev_t(np.tile(tv, (ell, 1))), ell, C, scr)
+        lam = dev.eigenvalue_karp(C)
+        rows.append({"P": float(P), "drift_hbar": est["h_bar"], "karp_hbar": lam, "periods": est["n_steps"] // ell,
+                     "converged": est["converged"], "abs_diff": abs(est["h_bar"] - lam)})
+    return {"n": n, "tau": tau, "lines": rows, "max_abs_diff": max(r["abs_diff"] for r in rows),
+            "seconds": time.perf_counter() - t0}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_full_configs.json"))
-    ap.add_argument("--only", default="c1,c2,c3,c4,c5")
+    ap.add_argument("--only", default="c1,c2,c3,c4,c5,c2_karp")
     args = ap.parse_args()
     dev = api.Device(0)
     doc = {"device": torch.cuda.get_device_name(0), "hbm_peak_gbs": HBM}
