@@ -32,7 +32,13 @@ namespace cg = cooperative_groups;
 namespace lob {
 namespace {
 
-constexpr int kBM = 64, kBN = 64, kBK = 16;  // CTA tile of C and the contraction chunk
+#ifndef LOB_GEMM_BK
+#define LOB_GEMM_BK 16
+#endif
+#ifndef LOB_GEMM_CTAS_PER_SM
+#define LOB_GEMM_CTAS_PER_SM 4
+#endif
+constexpr int kBM = 64, kBN = 64, kBK = LOB_GEMM_BK;  // CTA tile of C and the contraction chunk
 constexpr int kTT = 4;                       // outputs per thread per dimension
 constexpr int kTX = kBN / kTT, kTY = kBM / kTT;
 constexpr int kGT = kTX * kTY;               // 256 threads
@@ -253,7 +259,8 @@ int launch_tropical_gemm(lob_ctx* ctx, const double* A, int64_t lda, const doubl
     // split the contraction when the output tiles alone cannot fill ~4 CTAs per SM
     // (keeping >= 4 chunks per slice); partial minima are combined in slice order
     const int64_t tiles = gx * gy, chunks = (k + kBK - 1) / kBK;
-    int64_t slices = std::min<int64_t>((4 * ctx->sm_count + tiles - 1) / tiles, std::max<int64_t>(1, chunks / 4));
+    int64_t slices = std::min<int64_t>((LOB_GEMM_CTAS_PER_SM * ctx->sm_count + tiles - 1) / tiles,
+                                       std::max<int64_t>(1, chunks / 4));
     slices = std::max<int64_t>(1, std::min<int64_t>(slices, 64));
     const int64_t kslice = ((chunks + slices - 1) / slices) * kBK;
     slices = k > 0 ? (k + kslice - 1) / kslice : 1;
