@@ -122,7 +122,8 @@ __global__ void relaxed_decompose_kernel(const double* __restrict__ u, int64_t l
             ++e;
         }
         for (int64_t s = b; s < e; s += cap) {
-            pl[np++] = make_int2(static_cast<int>(s), static_cast<int>(min(e, s + cap)) | (kind << 31));
+            const unsigned endk = static_cast<unsigned>(min(e, s + cap)) | (static_cast<unsigned>(kind) << 31);
+            pl[np++] = make_int2(static_cast<int>(s), static_cast<int>(endk));
             ++nb;
         }
         if (eta <= 0.0) nb -= (e - b + cap - 1) / cap - 1;  // eta == 0: blocks are not capped

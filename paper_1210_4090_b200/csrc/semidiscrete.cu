@@ -142,13 +142,13 @@ extern "C" int lob_step_semidiscrete_f64(lob_ctx* ctx, const double* u, double* 
             P.am[r] = V->amplitude * mod;
         }
     }
+    if (lines > 65535) return set_error(ctx, LOB_INVALID_INPUT, "step_semidiscrete: at most 65535 lines");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     int* err = nullptr;
     LOB_CUDA_TRY(ctx, cudaMallocAsync(&err, sizeof(int), s));
     LOB_CUDA_TRY(ctx, cudaMemsetAsync(err, 0, sizeof(int), s));
     const double step = 1.0 / static_cast<double>(n_space);
     const dim3 grid(static_cast<unsigned>((m + 31) / 32), static_cast<unsigned>(lines));
-    if (lines > 65535) return set_error(ctx, LOB_INVALID_INPUT, "step_semidiscrete: at most 65535 lines");
     semidiscrete_kernel<<<grid, 32 * kParts, 0, s>>>(u, out, m, n_space, periodic, origin, step, ktab, first, tau,
                                              quad_points, P, err);
     ctx->launches += 1;
