@@ -4,9 +4,11 @@
 Workload (BASELINE.json configs[1], "C2"): 256 independent periodic lines of
 N = 65536, per-line drift P_l = -2 + 4 l/255, tau = 0.02,
 V = cos(2 pi x) + 0.5 cos(4 pi x + 1), u0 = 0.  One bench step = one fully
-discrete Lax-Oleinik step of all 256 lines (min-plus with the kinetic kernel
-+ potential + the block-count statistics step_fully_discrete reports), run by
-the K2 fast exact engine, device-resident (u^{n+1} feeds the next step).
+discrete Lax-Oleinik step of all 256 lines (step_fully_discrete: min-plus with
+the kinetic kernel + potential; StepStats not requested, the API default, as C2's
+H-bar needs none), run by the K2 fast exact engine, device-resident (u^{n+1}
+feeds the next step).  The same step with decompose()'s block counts is timed
+under kernels.c2_step_with_block_counts.
 The state is first evolved `--presteps` steps (untimed) so the timed steps
 see a developed, kinked solution like the bulk of C2's 5000 steps.
 Working set 2 x 134 MB > 126 MB L2, so no L2 flush is needed.
@@ -159,7 +161,7 @@ def cpu_reference_rate(lines_sample: int, nthreads: int, engine: int = 1):
     u = np.cumsum(rng.uniform(-1.0 / N_SPACE, 1.0 / N_SPACE, (lines_sample, N_SPACE)), axis=1)
     u -= np.linspace(0, 1, N_SPACE)[None, :] * u[:, -1:]
     t0 = time.perf_counter()
-    ref.step_lines(u, TAU, drifts[idx], v=v, engine=engine, nthreads=nthreads)
+    ref.step_lines(u, TAU, drifts[idx], v=v, engine=engine, nthreads=nthreads, want_blocks=False)
     dt = time.perf_counter() - t0
     return lines_sample * N_SPACE / dt, dt, f"{lines_sample} C2 lines x 1 step, ConvEngine::Naive, {nthreads} threads"
 
@@ -221,11 +223,11 @@ def run_b200(args, world, rank, local):
     b = torch.empty_like(a)
     blocks = torch.empty(LINES, dtype=torch.int64, device="cuda")
     ws = torch.empty(dev.fast_workspace_bytes(LINES, N_SPACE), dtype=torch.uint8, device="cuda")
-    st = {"cur": a, "nxt": b, "i": 0}
+    st = {"cur": a, "nxt": b, "i": 0, "blocks": False}
 
     def step():
         # back-to-back device-resident steps: statistics carried over, per-line chaining
-        dev.fast_f64(st["cur"], st["nxt"], drifts, TAU, tv=tv, blocks=blocks, workspace=ws,
+        dev.fast_f64(st["cur"], st["nxt"], drifts, TAU, tv=tv, blocks=blocks if st["blocks"] else None, workspace=ws,
                      flags=api.FAST_CHAINED | (api.FAST_STATS_VALID if st["i"] else 0), stream=stream)
         st["cur"], st["nxt"] = st["nxt"], st["cur"]
         st["i"] += 1
@@ -255,6 +257,19 @@ def run_b200(args, world, rank, local):
     per_launch_s = (ms / 1e3) / args.steps  # one fast_kernel launch per step
     achieved = LINES * N_SPACE * 16 / per_launch_s / 1e9
     finite = bool(torch.isfinite(st["cur"]).all().item())
+    # the same step with decompose()'s block counts (StepStats requested), reported beside it
+    st["blocks"] = True
+    for _ in range(3):
+        step()
+    nb = 100
+    torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(nb):
+        step()
+    e3.record(stream)
+    torch.cuda.synchronize()
+    ms_blocks = e2.elapsed_time(e3) / nb
     blocks_mean = float(blocks.double().mean().item())
 
     # ---- e2e: the host-buffer C-ABI entry (H2D + step + D2H every step) ----
@@ -267,16 +282,16 @@ def run_b200(args, world, rank, local):
         dh = api.gen_c2_drifts(LINES)
         un, on = uh.numpy(), oh.numpy()
         e2e_steps = max(1, min(args.steps, 10))
-        dev.step_host(un, dh, TAU, tv=tv_h, out=on, blocks=bh)  # warm
+        dev.step_host(un, dh, TAU, tv=tv_h, out=on)  # warm
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            dev.step_host(un, dh, TAU, tv=tv_h, out=on, blocks=bh)
+            dev.step_host(un, dh, TAU, tv=tv_h, out=on)
             un, on = on, un
         dt = time.perf_counter() - t0
         dt = allreduce_max(dt, world, device="cuda")
         e2e = {"value": LINES * N_SPACE * e2e_steps * world / dt, "unit": "updates/s",
                "h2d_bytes_per_step": int(LINES * N_SPACE * 8 + LINES * 8 + N_SPACE * 8),
-               "d2h_bytes_per_step": int(LINES * N_SPACE * 8 + LINES * 8),
+               "d2h_bytes_per_step": int(LINES * N_SPACE * 8),
                "steps": e2e_steps, "api": "lob_step_host_f64 (pinned host buffers)"}
 
     if rank != 0:
@@ -295,6 +310,8 @@ def run_b200(args, world, rank, local):
                    "presteps": args.presteps, "lines_per_gpu": LINES, "n": N_SPACE,
                    "l2": "working set 268 MB > 126 MB L2 (no flush needed)",
                    "parallelism": f"line-sharded replicas x{world}", "state_finite": finite,
+                   "step_stats": "not requested (step_fully_discrete's default)",
+                   "with_block_counts_ms_per_step": ms_blocks,
                    "mean_blocks_per_line": blocks_mean},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,

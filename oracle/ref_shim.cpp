@@ -158,8 +158,8 @@ int ref_step_lines(const double* u, int64_t lines, int n_space, double tau, cons
                     const Kernel k = build_kernel(spec, p);
                     const double* ul = u + l * n_space;
                     GridFn g = make_periodic(std::vector<double>(ul, ul + n_space), p.epsilon());
-                    StepStats st;
-                    GridFn r = step_fully_discrete(g, t, spec, p, k, engine_of(engine), &st);
+                    StepStats st;  // requested only with a blocks buffer (the API default is none)
+                    GridFn r = step_fully_discrete(g, t, spec, p, k, engine_of(engine), blocks ? &st : nullptr);
                     std::memcpy(out + l * n_space, r.values.data(), n_space * sizeof(double));
                     if (blocks) blocks[l] = st.block_count;
                 } catch (const std::exception& e) {

@@ -101,6 +101,7 @@ struct FastParams {
     double eps, a, ia;  // 1/n, eps^2/tau, 1/a (host IEEE, same as the device's)
     const double* vtab;  // v_d for d in [-vofs, vofs]
     int64_t vofs;
+    int fsm_on;  // the epilogue produces decompose()'s FSM summaries for the next step's block count
 };
 
 struct FastBuffers {
@@ -244,6 +245,7 @@ __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line,
     int v = 0 | (1 << 2) | (2 << 4);
     unsigned acc = 0;
     const bool exact_cmp = p.eta == 0.0;
+    const bool fsm_on = p.fsm_on != 0;
     auto cls = [&](int k) -> int {  // class of increment e = j0 + i0 + 1 + k
         const int i = i0 + 1 + k;
         if (!FULL && !(i <= Tl && j0 + i <= p.n - 1)) return 3;
@@ -251,15 +253,17 @@ __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line,
         const double inc = __dsub_rn(sl[k + 2], sl[k + 1]);
         return inc > p.eta ? 0 : (inc < -p.eta ? 1 : 2);
     };
+    if (fsm_on) {
 #pragma unroll
-    for (int k = 0; k < kPer; k += 2) {
-        const unsigned x = __ldg(lut + v * 16 + cls(k) * 4 + cls(k + 1));
-        v = static_cast<int>(x & 63u);
-        acc += x >> 6;
+        for (int k = 0; k < kPer; k += 2) {
+            const unsigned x = __ldg(lut + v * 16 + cls(k) * 4 + cls(k + 1));
+            v = static_cast<int>(x & 63u);
+            acc += x >> 6;
+        }
+        const int cnt[3] = {static_cast<int>(acc & 7u), static_cast<int>((acc >> 3) & 7u),
+                            static_cast<int>(acc >> 6)};
+        sh.fsm[tid] = fsm_pack(v, cnt);
     }
-    const int cnt[3] = {static_cast<int>(acc & 7u), static_cast<int>((acc >> 3) & 7u),
-                        static_cast<int>(acc >> 6)};
-    sh.fsm[tid] = fsm_pack(v, cnt);
     kmin = __reduce_min_sync(0xffffffffu, kmin);
     kmax = __reduce_max_sync(0xffffffffu, kmax);
     if (lane == 0) {
@@ -274,16 +278,19 @@ __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line,
     __syncthreads();
     if (warp == 0) {
         // lane l composes summaries 8l .. 8l+7, then an ordered warp reduction
-        unsigned long long f = sh.fsm[lane * (kNT / 32)];
+        unsigned long long f = 0;
+        if (fsm_on) {
+            f = sh.fsm[lane * (kNT / 32)];
 #pragma unroll
-        for (int k = 1; k < kNT / 32; ++k) f = fsm_compose(f, sh.fsm[lane * (kNT / 32) + k]);
-        f = warp_fsm(f);
+            for (int k = 1; k < kNT / 32; ++k) f = fsm_compose(f, sh.fsm[lane * (kNT / 32) + k]);
+            f = warp_fsm(f);
+        }
         unsigned a0 = lane < kNT / 32 ? sh.kred[0][lane] : 0xffffffffu;
         unsigned a1 = lane < kNT / 32 ? sh.kred[1][lane] : 0u;
         a0 = __reduce_min_sync(0xffffffffu, a0);
         a1 = __reduce_max_sync(0xffffffffu, a1);
         if (lane == 0) {
-            b.fsm_out[line * p.tiles + tile] = f;
+            if (fsm_on) b.fsm_out[line * p.tiles + tile] = f;
             unsigned long long* L = b.line_out + line * 4;
             atomicMin(L + 2, dkey(hkey_lower(a0)));
             atomicMax(L + 3, dkey(hkey_upper(a1)));
@@ -1144,6 +1151,7 @@ static FastParams make_params(int64_t n, double tau, double eta) {
     p.eps = 1.0 / static_cast<double>(n);  // SchemeParams::epsilon(), proj/include/laxol/scheme.hpp:25
     p.a = p.eps * p.eps / tau;
     p.ia = 1.0 / p.a;
+    p.fsm_on = 1;
     return p;
 }
 
@@ -1188,6 +1196,9 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     }
     // the statistics describe the previous call's output: any other input recomputes them
     if (ctx->ws_last_out[workspace] != static_cast<const void*>(u)) flags &= ~LOB_FAST_STATS_VALID;
+    // block counts come from FSM summaries the previous call's epilogue produced only if it was
+    // asked for block counts too (the epilogue predicts the next call from this one)
+    if (blocks && !ctx->ws_fsm_valid[workspace]) flags &= ~LOB_FAST_STATS_VALID;
     ctx->ws_last_out[workspace] = out;
     // the per-line done counters restart with the statistics (keeps them in range)
     if (ctx->ws_chain[workspace] * p.tiles * (kNT / 32) > 0xf0000000ll) flags &= ~LOB_FAST_STATS_VALID;
@@ -1237,6 +1248,8 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     if (first_time(ctx, reinterpret_cast<const void*>(kern)))
         LOB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(sizeof(MainShared))));
+    p.fsm_on = blocks ? 1 : 0;  // the stats kernel above always produced them
+    ctx->ws_fsm_valid[workspace] = blocks != nullptr;
     dim3 grid(static_cast<unsigned>(p.tiles), static_cast<unsigned>(lines));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;

@@ -29,6 +29,7 @@ struct lob_ctx {
     std::map<const void*, std::pair<int64_t, int64_t>> ws_shape;
     std::map<const void*, const void*> ws_last_out;  // workspace -> out of its last K2 call
     std::map<const void*, int64_t> ws_chain;         // K2 launches since the done counters were reset
+    std::map<const void*, bool> ws_fsm_valid;        // the workspace holds FSM summaries of its last out
     // K1 mode (LOB_DIRECT_SCREENED / LOB_DIRECT_PLAIN) and the screened kernel's
     // count of outputs swept in full fp64 (device counter, lazily allocated)
     int direct_mode = 0;

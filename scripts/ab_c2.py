@@ -22,7 +22,7 @@ CH = getattr(api, "FAST_CHAINED", 0) if __CHAINED__ else 0
 def run(k, i0):
     global x, y
     for i in range(k):
-        dev.fast_f64(x, y, dr, tau, tv=tv, blocks=bl, workspace=ws,
+        dev.fast_f64(x, y, dr, tau, tv=tv, blocks=None if __NOB__ else bl, workspace=ws,
                      flags=CH | (api.FAST_STATS_VALID if i0 + i else 0))
         x, y = y, x
 run(1000, 0)
@@ -36,9 +36,10 @@ for r in range(5):
 print(json.dumps({"lib": __LIB__, "chained": __CHAINED__, "ms": sorted(res)}))
 '''
 for lib in sys.argv[1:]:
-    chained = lib.endswith(":chained")
+    chained = ":chained" in lib
+    nob = ":nob" in lib
     lib = lib.split(":")[0]
     code = CHILD.replace("__ROOT__", repr(ROOT)).replace("__LIB__", repr(os.path.abspath(lib)))
-    code = code.replace("__CHAINED__", repr(chained))
+    code = code.replace("__CHAINED__", repr(chained)).replace("__NOB__", repr(nob))
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
     print(r.stdout.strip() or r.stderr[-2000:], flush=True)

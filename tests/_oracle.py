@@ -162,7 +162,7 @@ class Reference:
                                            engine, out.ctypes.data, ctypes.byref(blocks))
         return out, blocks.value, st
 
-    def step_lines(self, u, tau, drifts, v=None, t=0.0, eta=0.0, engine=0, nthreads=1):
+    def step_lines(self, u, tau, drifts, v=None, t=0.0, eta=0.0, engine=0, nthreads=1, want_blocks=True):
         u = np.ascontiguousarray(u, np.float64)
         lines, n = u.shape
         drifts = np.ascontiguousarray(np.broadcast_to(np.asarray(drifts, np.float64), (lines,)))
@@ -170,7 +170,7 @@ class Reference:
         blocks = np.empty(lines, np.int64)
         st = self.lib.ref_step_lines(u.ctypes.data, lines, n, tau, drifts.ctypes.data,
                                      None if v is None else np.ascontiguousarray(v).ctypes.data, t, eta, engine,
-                                     nthreads, out.ctypes.data, blocks.ctypes.data)
+                                     nthreads, out.ctypes.data, blocks.ctypes.data if want_blocks else None)
         if st:
             raise RuntimeError(self.err())
         return out, blocks

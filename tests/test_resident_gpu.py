@@ -70,3 +70,32 @@ def test_evolve_loop_fused_drift(dev):
         assert np.array_equal(a[2][k * lines:(k + 1) * lines], bl.cpu().numpy())
         u, out = out, u
     assert np.array_equal(a[0], u.cpu().numpy())
+
+
+def test_k2_block_counts_after_steps_without_them(dev, orc):
+    """K2 skips decompose()'s FSM when a call asks for no block counts; a later call that does
+    ask recomputes the statistics: outputs and counts stay exact in any interleaving."""
+    import torch
+
+    n, lines, tau = 4096, 3, 0.02
+    rng = np.random.default_rng(8)
+    u = np.cumsum(rng.uniform(-1.0 / n, 1.0 / n, (lines, n)), axis=1)
+    u -= np.linspace(0, 1, n)[None, :] * u[:, -1:]
+    drifts = np.array([0.2, -0.9, 1.4])
+    a = torch.from_numpy(u).cuda()
+    b = torch.empty_like(a)
+    ws = torch.empty(dev.fast_workspace_bytes(lines, n), dtype=torch.uint8, device="cuda")
+    dr = torch.from_numpy(drifts).cuda()
+    bl = torch.empty(lines, dtype=torch.int64, device="cuda")
+    pattern = [True, False, False, True, True, False, True]
+    for k, want_blocks in enumerate(pattern):
+        x = a.cpu().numpy()
+        dev.fast_f64(a, b, dr, tau, blocks=bl if want_blocks else None, workspace=ws,
+                     flags=api.FAST_STATS_VALID if k else 0)
+        y = b.cpu().numpy()
+        for l in range(lines):
+            w, first, _, _ = orc.kernel(n, tau, drifts[l])
+            assert np.array_equal(y[l], orc.direct(x[l:l + 1], w, first)[0])
+            if want_blocks:
+                assert bl[l].item() == orc.line_blocks(x[l])
+        a, b = b, a
