@@ -293,6 +293,25 @@ def run_b200(args, world, rank, local):
                "h2d_bytes_per_step": int(LINES * N_SPACE * 8 + LINES * 8 + N_SPACE * 8),
                "d2h_bytes_per_step": int(LINES * N_SPACE * 8),
                "steps": e2e_steps, "api": "lob_step_host_f64 (pinned host buffers)"}
+        # the e2e roofline: the same bytes moved by plain copies alone (H2D and D2H on two
+        # streams at once, pinned buffers, no compute) - the host link bounds the e2e number
+        dbuf_in = torch.empty_like(uh, device="cuda")
+        dbuf_out = torch.empty_like(uh, device="cuda")
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        for rep in range(e2e_steps + 1):
+            if rep == 1:
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+            with torch.cuda.stream(s_in):
+                dbuf_in.copy_(uh, non_blocking=True)
+            with torch.cuda.stream(s_out):
+                oh.copy_(dbuf_out, non_blocking=True)
+        torch.cuda.synchronize()
+        dtc = allreduce_max(time.perf_counter() - t0, world, device="cuda")
+        bound = LINES * N_SPACE * e2e_steps * world / dtc
+        e2e["copy_bound"] = {"value": bound, "unit": "updates/s", "frac": e2e["value"] / bound,
+                             "what": "concurrent pinned H2D + D2H of one step's state, no compute"}
+        del dbuf_in, dbuf_out
 
     if rank != 0:
         return
