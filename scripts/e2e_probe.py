@@ -23,10 +23,10 @@ tvh = api.tau_v(api.gen_potential(2, N), TAU)
 bh = np.empty(L, np.int64)
 res = {"pinned": bool(uh.is_pinned())}
 for lines in (256, 8):
-    dev.step_host(un[:lines], dh[:lines], TAU, tv=tvh, out=on[:lines], blocks=bh[:lines])
+    dev.step_host(un[:lines], dh[:lines], TAU, tv=tvh, out=on[:lines])
     t0 = time.perf_counter()
     for _ in range(5):
-        dev.step_host(un[:lines], dh[:lines], TAU, tv=tvh, out=on[:lines], blocks=bh[:lines])
+        dev.step_host(un[:lines], dh[:lines], TAU, tv=tvh, out=on[:lines])
     res[f"step_host_ms_{lines}"] = (time.perf_counter() - t0) / 5 * 1e3
 d = torch.empty((L, N), dtype=torch.float64, device="cuda")
 torch.cuda.synchronize()
