@@ -291,3 +291,51 @@ def test_fast_chained_steps_equal_plain_steps(dev):
     for k in (1, 2):
         assert torch.equal(res[0][0], res[k][0])
         assert torch.equal(res[0][1], res[k][1])
+
+
+def _structured_lines(n, rng):
+    """Adversarial line shapes for the local-minimum walk: constant (every source
+    lands on the same displacement: maximal CAS contention), exact ties (a sawtooth
+    whose teeth repeat exactly), jumps (huge slopes: long intervals, the queue and
+    its overflow, displacement ranges beyond the staged K buffer), large magnitudes,
+    a single spike, and tiny noise on a constant (near-ties everywhere)."""
+    x = np.arange(n) / n
+    teeth = 8
+    lines = [
+        np.zeros(n),
+        np.full(n, 3.25),
+        (np.arange(n) % (n // teeth)) / n,                       # exact repeated teeth
+        np.where(x < 0.5, 0.0, 1.0),                             # two jumps per period
+        np.where((np.arange(n) // max(1, n // 16)) % 2 == 0, -2.0, 2.0),  # square wave
+        1e8 * np.sin(2 * np.pi * x),                              # large magnitude
+        np.where(np.arange(n) == n // 3, -50.0, 0.0),             # one deep well
+        np.where(np.arange(n) == n // 3, 50.0, 0.0),              # one spike
+        1e-13 * rng.standard_normal(n),                           # near-ties
+        rng.uniform(-1, 1, n) * (x < 0.1),                        # rough patch, flat elsewhere
+    ]
+    return np.stack(lines)
+
+
+@pytest.mark.parametrize("n,tau", [(64, 0.1), (1000, 0.03), (4096, 0.01)])
+@pytest.mark.parametrize("drift", [0.0, 0.85])
+def test_fast_structured_inputs_bit_exact(dev, orc, n, tau, drift):
+    """Constant, tied, discontinuous, huge and spiky lines through K2 == the oracle's
+    direct sweep bit for bit, with block counts == decompose()'s; the cold fallback
+    count is reported, never required to be zero (exactness is the contract)."""
+    rng = np.random.default_rng(n * 7 + int(drift * 100))
+    u = _structured_lines(n, rng)
+    got, blocks = fast_step(dev, u, drift, tau, blocks=True)
+    want = oracle_step(orc, u, drift, tau)
+    assert np.array_equal(got.cpu().numpy(), want)
+    assert [orc.line_blocks(u[l]) for l in range(u.shape[0])] == list(blocks)
+    # and a second step on K2's own output with STATS_VALID (statistics written by step 1)
+    import torch
+    du = to_dev(u)
+    a = torch.empty_like(du)
+    b = torch.empty_like(du)
+    ws = torch.empty(dev.fast_workspace_bytes(u.shape[0], n), dtype=torch.uint8, device="cuda")
+    dd = to_dev(np.full(u.shape[0], drift))
+    dev.fast_f64(du, a, dd, tau, workspace=ws)
+    dev.fast_f64(a, b, dd, tau, workspace=ws, flags=api.FAST_STATS_VALID)
+    torch.cuda.synchronize()
+    assert np.array_equal(b.cpu().numpy(), oracle_step(orc, want, drift, tau))

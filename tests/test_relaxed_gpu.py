@@ -162,3 +162,21 @@ def test_relaxed_host_step_equals_reference(dev, ref):
     want, wb = ref.step_lines(u, tau, drifts, v=v, eta=eta, engine=0)
     assert np.array_equal(got, want)
     assert np.array_equal(bl, wb)
+
+
+@pytest.mark.parametrize("eta", [0.0, 1e-6, 1e-2])
+@pytest.mark.parametrize("n,tau", [(64, 0.1), (1000, 0.03)])
+def test_relaxed_structured_inputs_equal_reference(dev, ref, eta, n, tau):
+    """The adversarial shapes of tests/test_fast_gpu.py (constant, exact ties, jumps,
+    1e8 magnitudes, spikes, near-ties) through the relaxed engine == the reference's
+    ConvEngine::Fast: values and block counts."""
+    from tests.test_fast_gpu import _structured_lines
+
+    u = _structured_lines(n, np.random.default_rng(n + 1))
+    drifts = list(np.linspace(-0.9, 1.3, u.shape[0]))
+    got, blocks = run(dev, u, tau, drifts, eta)
+    for l, d in enumerate(drifts):
+        want, wb, st = ref.kinetic_convolve(u[l], n, tau, d, eta=eta, engine=0)
+        assert st == 0
+        assert np.array_equal(got[l], want), (l, eta, np.max(np.abs(got[l] - want)))
+        assert blocks[l] == wb

@@ -99,3 +99,18 @@ def test_k2_block_counts_after_steps_without_them(dev, orc):
             if want_blocks:
                 assert bl[l].item() == orc.line_blocks(x[l])
         a, b = b, a
+
+
+@pytest.mark.parametrize("n,tau", [(64, 0.1), (1000, 0.03), (4096, 0.01)])
+def test_resident_structured_inputs(dev, n, tau):
+    """K2R on the adversarial shapes of tests/test_fast_gpu.py (constant, exact ties, jumps,
+    1e8 magnitudes, spikes, near-ties) == the K2 launch loop: states and block counts."""
+    from tests.test_fast_gpu import _structured_lines
+
+    u0 = _structured_lines(n, np.random.default_rng(n))
+    drifts = np.linspace(-0.9, 1.3, u0.shape[0])
+    a = _evolve(dev, u0, drifts, tau, 25, None, True)
+    b = _evolve(dev, u0, drifts, tau, 25, None, False)
+    assert np.array_equal(a[0], b[0])
+    assert np.array_equal(a[2], b[2])
+    assert np.max(np.abs(a[1] - b[1])) <= 1e-12 * max(1.0, float(np.max(np.abs(u0))))
