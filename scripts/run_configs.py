@@ -257,7 +257,16 @@ def c5(dev, steps=200, checks=(1, 100, 199)):
             mism, miss = direct_equals_fast(dev, sub, np.full(2, p), tau, tv)
             chk.append({"step": stop, "lines": 2, "k2_vs_k1_mismatches": mism, "k2_fallback_outputs": miss})
     bl = blocks.cpu().numpy()
+    # the same chained steps from the final state without StepStats (no block counts)
+    x, y = a.clone(), torch.empty_like(a)
+    nb = 20
+    with Timer() as t:
+        for i in range(nb):
+            dev.fast_f64(x, y, drifts, tau, tv=tv, workspace=ws, flags=api.FAST_CHAINED | api.FAST_STATS_VALID)
+            x, y = y, x
+    del x, y
     return {"steps": steps, "ms": total_ms, "ms_per_step": total_ms / steps,
+            "ms_per_step_without_block_counts": t.ms / nb,
             "updates_per_s": lines * n * steps / (total_ms * 1e-3),
             "hbm_frac": lines * n * 16 * steps / (total_ms * 1e-3) / 1e9 / HBM,
             "host_u0_generation_s": gen_s, "k2_vs_k1_checks": chk,
