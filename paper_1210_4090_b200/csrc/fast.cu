@@ -366,6 +366,7 @@ __global__ void combine_blocks_kernel(const unsigned long long* __restrict__ fsm
 // u^{n+1} of the tile (padded, for tile_stats) reuses ubuf after the emission
 // phase; the statistics' reduction scratch reuses keys after the epilogue.
 constexpr int kValsLen = P8(kT + 3) + 2;
+constexpr int kRuns = 8;  // source runs per wide tile (more are merged into the last)
 struct MainShared {
     unsigned long long keys[kT + 4];   // exact-min slots (+inf bits = empty), lane-interleaved access
     unsigned long long mbar;           // TMA completion barrier for the source chunk
@@ -373,6 +374,7 @@ struct MainShared {
     int3 queue[kQCap];
     __align__(16) double vbuf[kVCap];  // v_d of the tile's displacement range, converted to K(d)
     int ya, yb, nq, dlo, dhi, DLg, DRg, ok;
+    int nruns, rs[kRuns], re[kRuns];  // runs of reaching sub-tiles (unrolled source ranges)
     unsigned int c_inline, c_queued, c_src, c_qent;
     __device__ EpiShared& epi() { return *reinterpret_cast<EpiShared*>(keys); }
 };
@@ -667,15 +669,21 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
             int k1 = k0;
             while (y1 - k1 * n >= n) ++k1;
             const int Q1 = k1 * subs + (y1 - k1 * n) / kG;
-            for (int Q = Q0 + lane; Q <= Q1; Q += 32) {
+            // sub-tile Q of the unrolled source axis: its sources [ys, ye] and whether
+            // their slope-implied displacements reach this tile's outputs
+            auto reach = [&](int Q, int& ys, int& ye, int& dl, int& dr) {
                 const int k = Q >= 0 ? Q / subs : -((subs - 1 - Q) / subs);
                 const int q = Q - k * subs;
                 const double2 sb = xload<CHAIN>(b.sub_in + line * p.subs + q);
-                const int ys = k * n + q * kG;
-                const int ye = ys + min(kG, n - q * kG) - 1;
-                const int dl = max(__double2int_ru(__fma_rn(sb.x, ia, hl)), DLg);
-                const int dr = min(__double2int_rd(__fma_rn(sb.y, ia, hr)), DRg);
-                if (dl <= dr && ys + dl <= jhi && ye + dr >= jlo) {
+                ys = k * n + q * kG;
+                ye = ys + min(kG, n - q * kG) - 1;
+                dl = max(__double2int_ru(__fma_rn(sb.x, ia, hl)), DLg);
+                dr = min(__double2int_rd(__fma_rn(sb.y, ia, hr)), DRg);
+                return dl <= dr && ys + dl <= jhi && ye + dr >= jlo;
+            };
+            for (int Q = Q0 + lane; Q <= Q1; Q += 32) {
+                int ys, ye, dl, dr;
+                if (reach(Q, ys, ye, dl, dr)) {
                     ya = min(ya, ys);
                     yb = max(yb, ye);
                     dlo = min(dlo, max(dl, jlo - ye));
@@ -686,12 +694,48 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
             yb = __reduce_max_sync(0xffffffffu, yb);
             dlo = __reduce_min_sync(0xffffffffu, dlo);
             dhi = __reduce_max_sync(0xffffffffu, dhi);
+            // a wide tile (displacement range beyond the staged K buffer: a shock in a nearby
+            // sub-tile) scans only the runs of reaching sub-tiles, not the gaps between them
+            int nr = 1;
+            if (ya <= yb && dhi - dlo + 2 > kVCap && Q1 - Q0 < 64) {
+                unsigned long long hmask = 0;
+                for (int Qb = Q0; Qb <= Q1; Qb += 32) {
+                    int ys, ye, dl, dr;
+                    const bool hit = Qb + lane <= Q1 && reach(Qb + lane, ys, ye, dl, dr);
+                    hmask |= static_cast<unsigned long long>(__ballot_sync(0xffffffffu, hit)) << (Qb - Q0);
+                }
+                if (lane == 0) {
+                    nr = 0;
+                    unsigned long long m = hmask;
+                    while (m) {
+                        const int b0 = __ffsll(static_cast<long long>(m)) - 1;
+                        const unsigned long long inv = ~(m >> b0);
+                        const int len = inv ? __ffsll(static_cast<long long>(inv)) - 1 : 64 - b0;
+                        int ys, ye, ys2, ye2, dl, dr;
+                        reach(Q0 + b0, ys, ye, dl, dr);
+                        reach(Q0 + b0 + len - 1, ys2, ye2, dl, dr);
+                        if (nr < kRuns) {
+                            S.rs[nr] = ys;
+                            S.re[nr] = ye2;
+                            ++nr;
+                        } else {
+                            S.re[kRuns - 1] = ye2;
+                        }
+                        m = b0 + len >= 64 ? 0ull : (m >> (b0 + len)) << (b0 + len);
+                    }
+                }
+            } else if (lane == 0) {
+                S.rs[0] = ya;
+                S.re[0] = yb;
+            }
+            if (lane == 0) S.nruns = ya <= yb ? nr : 0;
         }
         if (lane == 0) {
             S.ok = okl;
             S.DLg = DLg;
             S.DRg = DRg;
             S.ya = ya;
+            if (!okl) S.nruns = 0;
             S.yb = yb;
             S.dlo = dlo;
             S.dhi = dhi;
@@ -703,7 +747,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
                 // first source chunk + the tile's v_d range, in flight across the barrier
                 const int vd0 = dlo - ((dlo + static_cast<int>(p.vofs)) & 1);
                 const int vcnt = (dhi - vd0 + 2) & ~1;
-                issue_chunk(S, ul, n, ya, min(kC, yb - ya + 1), vcnt <= kVCap ? p.vtab + p.vofs + vd0 : nullptr,
+                issue_chunk(S, ul, n, ya, min(kC, S.re[0] - ya + 1), vcnt <= kVCap ? p.vtab + p.vofs + vd0 : nullptr,
                             vcnt);
             }
         }
@@ -728,8 +772,9 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
         }
         // ---- sources in chunks of kC ----
         unsigned mphase = 0;
-        for (int yc = ya; yc <= yb; yc += kC) {
-            const int clen = min(kC, yb - yc + 1);
+        const int nruns = S.nruns;
+        for (int run = 0, yc = ya, yr = nruns ? S.re[0] : 0; run < nruns;) {
+            const int clen = min(kC, yr - yc + 1);
             const int base = yc - jlo;  // output index of source i at d: base + i + d
             int sh = 0;
             if (big) {
@@ -754,6 +799,11 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
                 process_chunk<true>(S, ca);
             else
                 process_chunk<false>(S, ca);
+            yc += clen;
+            if (yc > yr && ++run < nruns) {
+                yc = S.rs[run];
+                yr = S.re[run];
+            }
         }
     }
 
