@@ -366,6 +366,9 @@ __global__ void combine_blocks_kernel(const unsigned long long* __restrict__ fsm
 // u^{n+1} of the tile (padded, for tile_stats) reuses ubuf after the emission
 // phase; the statistics' reduction scratch reuses keys after the epilogue.
 constexpr int kValsLen = P8(kT + 3) + 2;
+#ifndef LOB_WIDE_RANGE
+#define LOB_WIDE_RANGE kVCap  // displacement range above which a tile scans source runs
+#endif
 constexpr int kRuns = 8;  // source runs per wide tile (more are merged into the last)
 struct MainShared {
     unsigned long long keys[kT + 4];   // exact-min slots (+inf bits = empty), lane-interleaved access
@@ -697,7 +700,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
             // a wide tile (displacement range beyond the staged K buffer: a shock in a nearby
             // sub-tile) scans only the runs of reaching sub-tiles, not the gaps between them
             int nr = 1;
-            if (ya <= yb && dhi - dlo + 2 > kVCap && Q1 - Q0 < 64) {
+            if (ya <= yb && dhi - dlo + 2 > LOB_WIDE_RANGE && Q1 - Q0 < 64) {
                 unsigned long long hmask = 0;
                 for (int Qb = Q0; Qb <= Q1; Qb += 32) {
                     int ys, ye, dl, dr;
