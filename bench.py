@@ -172,7 +172,7 @@ REF_BUDGET_S = 150.0  # wall-clock budget of the reference arm (it must finish w
 def run_reference(args, world, rank):
     """The reference's CPU path on all host threads.  One reference step of a C2 sample
     (one line per thread, ConvEngine::Naive) takes seconds, so the arm times at most
-    as many steps as fit REF_BUDGET_S (after at most one warm-up step) and reports
+    as many steps as fit REF_BUDGET_S (after at most three warm-up steps) and reports
     the rate; `steps` is the number actually timed, `steps_requested` the driver's K."""
     if rank != 0:
         return
@@ -180,7 +180,7 @@ def run_reference(args, world, rank):
     lines_sample = args.ref_lines or max(1, min(nthreads, 64))
     rates, times = [], []
     t_start = time.perf_counter()
-    warm = min(args.warmup, 1)
+    warm = min(args.warmup, 3)
     i = 0
     while i < warm + args.steps:
         r = cpu_reference_rate(lines_sample, nthreads)
