@@ -8,7 +8,7 @@ discrete Lax-Oleinik step of all 256 lines (step_fully_discrete: min-plus with
 the kinetic kernel + potential; StepStats not requested, the API default, as C2's
 H-bar needs none), run by the K2 fast exact engine, device-resident (u^{n+1}
 feeds the next step).  The same step with decompose()'s block counts is timed
-under kernels.c2_step_with_block_counts.
+under config.with_block_counts_ms_per_step.
 The state is first evolved `--presteps` steps (untimed) so the timed steps
 see a developed, kinked solution like the bulk of C2's 5000 steps.
 Working set 2 x 134 MB > 126 MB L2, so no L2 flush is needed.
