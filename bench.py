@@ -151,11 +151,10 @@ def cpu_reference_rate(lines_sample: int, nthreads: int, engine: int = 1):
     ref = _oracle.reference()
     if ref is None:
         return None
-    from paper_1210_4090_b200 import api
-
-    drifts = api.gen_c2_drifts(LINES)
+    # inputs from the generators built into oracle/_ref: this arm maps no product library
+    drifts = ref.gen_c2_drifts(LINES)
     idx = np.linspace(0, LINES - 1, lines_sample).round().astype(int)
-    v = api.gen_potential(2, N_SPACE)
+    v = ref.gen_potential(2, N_SPACE)
     rng = np.random.default_rng(0)
     # the Naive engine's cost is data independent; a rough state stands in
     u = np.cumsum(rng.uniform(-1.0 / N_SPACE, 1.0 / N_SPACE, (lines_sample, N_SPACE)), axis=1)
@@ -169,10 +168,18 @@ def cpu_reference_rate(lines_sample: int, nthreads: int, engine: int = 1):
 REF_BUDGET_S = 150.0  # wall-clock budget of the reference arm (it must finish within minutes)
 
 
+def config_for(world: int) -> dict:
+    """The workload description both arms print (identical, so the driver can pair them)."""
+    return {"workload": WORKLOAD, "lines": LINES, "n": N_SPACE, "tau": TAU,
+            "l2": "working set 2 x 134 MB > 126 MB L2 (no flush needed)",
+            "parallelism": f"C2's {LINES} lines partitioned over {world} GPU(s), {LINES // world} per GPU"
+                           " (no per-step collective; H-bar(P) gathered at the end)"}
+
+
 def run_reference(args, world, rank):
     """The reference's CPU path on all host threads.  One reference step of a C2 sample
     (one line per thread, ConvEngine::Naive) takes seconds, so the arm times at most
-    as many steps as fit REF_BUDGET_S (after at most three warm-up steps) and reports
+    as many steps as fit REF_BUDGET_S (after the requested warm-up steps) and reports
     the rate; `steps` is the number actually timed, `steps_requested` the driver's K."""
     if rank != 0:
         return
@@ -180,7 +187,7 @@ def run_reference(args, world, rank):
     lines_sample = args.ref_lines or max(1, min(nthreads, 64))
     rates, times = [], []
     t_start = time.perf_counter()
-    warm = min(args.warmup, 3)
+    warm = args.warmup
     i = 0
     while i < warm + args.steps:
         r = cpu_reference_rate(lines_sample, nthreads)
@@ -197,10 +204,11 @@ def run_reference(args, world, rank):
     value = float(np.median(rates))
     line = {"metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": args.gpus, "steps": len(rates),
             "steps_requested": args.steps, "warmup": warm, "ms_per_step": float(np.median(times)) * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": WORKLOAD, "engine": "reference laxol ConvEngine::Naive (CPU)",
-                       "budget_s": REF_BUDGET_S},
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": config_for(world),
+            "impl_detail": {"engine": "reference laxol ConvEngine::Naive (CPU, oracle/_ref)",
+                            "budget_s": REF_BUDGET_S, "sample": r[2]},
             "cpu_baseline": {"value": value, "unit": "updates/s", "cores": nthreads, "kind": "reference",
                              "sample": r[2]},
             "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -216,13 +224,17 @@ def run_b200(args, world, rank, local):
     torch.cuda.set_device(local)
     dev = api.Device(local)
     stream = torch.cuda.current_stream()
-    drifts = torch.from_numpy(api.gen_c2_drifts(LINES)).cuda()
+    # this rank's block of C2's lines (no per-step collective: the lines are independent)
+    L = LINES // world
+    l0 = rank * L
+    dh = api.gen_c2_drifts(LINES)[l0:l0 + L].copy()
+    drifts = torch.from_numpy(dh).cuda()
     tv_h = api.tau_v(api.gen_potential(2, N_SPACE), TAU)
     tv = torch.from_numpy(tv_h).cuda()
-    a = torch.zeros((LINES, N_SPACE), dtype=torch.float64, device="cuda")
+    a = torch.zeros((L, N_SPACE), dtype=torch.float64, device="cuda")
     b = torch.empty_like(a)
-    blocks = torch.empty(LINES, dtype=torch.int64, device="cuda")
-    ws = torch.empty(dev.fast_workspace_bytes(LINES, N_SPACE), dtype=torch.uint8, device="cuda")
+    blocks = torch.empty(L, dtype=torch.int64, device="cuda")
+    ws = torch.empty(dev.fast_workspace_bytes(L, N_SPACE), dtype=torch.uint8, device="cuda")
     st = {"cur": a, "nxt": b, "i": 0, "blocks": False}
 
     def step():
@@ -251,12 +263,22 @@ def run_b200(args, world, rank, local):
     clk = clocks.stop()
     barrier(world)
     ms_max = allreduce_max(ms, world, device="cuda")
-    updates = LINES * N_SPACE * args.steps * world
+    updates = LINES * N_SPACE * args.steps  # the whole job: every rank's lines
     value = updates / (ms_max * 1e-3)
     hbm_peak, peak_kind = measured_peaks()
     per_launch_s = (ms / 1e3) / args.steps  # one fast_kernel launch per step
-    achieved = LINES * N_SPACE * 16 / per_launch_s / 1e9
+    achieved = L * N_SPACE * 16 / per_launch_s / 1e9
     finite = bool(torch.isfinite(st["cur"]).all().item())
+    # H-bar(P) estimate per line, mean(u_T - u_0)/T (u_0 = 0), gathered on rank 0 over NCCL
+    T = st["i"] * TAU
+    hb = st["cur"].mean(dim=1) / T
+    if world > 1:
+        import torch.distributed as dist
+
+        parts = [torch.empty_like(hb) for _ in range(world)]
+        dist.all_gather(parts, hb)
+        hb = torch.cat(parts)
+    hb = hb.cpu().numpy()
     # the same step with decompose()'s block counts (StepStats requested), reported beside it
     st["blocks"] = True
     for _ in range(3):
@@ -273,45 +295,43 @@ def run_b200(args, world, rank, local):
     blocks_mean = float(blocks.double().mean().item())
 
     # ---- e2e: the host-buffer C-ABI entry (H2D + step + D2H every step) ----
-    e2e = None
-    if rank == 0 or world > 1:
-        uh = torch.empty((LINES, N_SPACE), dtype=torch.float64, pin_memory=True)
-        uh.copy_(st["cur"])
-        oh = torch.empty_like(uh, pin_memory=True)
-        bh = np.empty(LINES, np.int64)
-        dh = api.gen_c2_drifts(LINES)
-        un, on = uh.numpy(), oh.numpy()
-        e2e_steps = max(1, min(args.steps, 10))
-        dev.step_host(un, dh, TAU, tv=tv_h, out=on)  # warm
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            dev.step_host(un, dh, TAU, tv=tv_h, out=on)
-            un, on = on, un
-        dt = time.perf_counter() - t0
-        dt = allreduce_max(dt, world, device="cuda")
-        e2e = {"value": LINES * N_SPACE * e2e_steps * world / dt, "unit": "updates/s",
-               "h2d_bytes_per_step": int(LINES * N_SPACE * 8 + LINES * 8 + N_SPACE * 8),
-               "d2h_bytes_per_step": int(LINES * N_SPACE * 8),
-               "steps": e2e_steps, "api": "lob_step_host_f64 (pinned host buffers)"}
-        # the e2e roofline: the same bytes moved by plain copies alone (H2D and D2H on two
-        # streams at once, pinned buffers, no compute) - the host link bounds the e2e number
-        dbuf_in = torch.empty_like(uh, device="cuda")
-        dbuf_out = torch.empty_like(uh, device="cuda")
-        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-        for rep in range(e2e_steps + 1):
-            if rep == 1:
-                torch.cuda.synchronize()
-                t0 = time.perf_counter()
-            with torch.cuda.stream(s_in):
-                dbuf_in.copy_(uh, non_blocking=True)
-            with torch.cuda.stream(s_out):
-                oh.copy_(dbuf_out, non_blocking=True)
-        torch.cuda.synchronize()
-        dtc = allreduce_max(time.perf_counter() - t0, world, device="cuda")
-        bound = LINES * N_SPACE * e2e_steps * world / dtc
-        e2e["copy_bound"] = {"value": bound, "unit": "updates/s", "frac": e2e["value"] / bound,
-                             "what": "concurrent pinned H2D + D2H of one step's state, no compute"}
-        del dbuf_in, dbuf_out
+    uh = torch.empty((L, N_SPACE), dtype=torch.float64, pin_memory=True)
+    uh.copy_(st["cur"])
+    oh = torch.empty_like(uh, pin_memory=True)
+    un, on = uh.numpy(), oh.numpy()
+    e2e_steps = max(1, min(args.steps, 10))
+    dev.step_host(un, dh, TAU, tv=tv_h, out=on)  # warm
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        dev.step_host(un, dh, TAU, tv=tv_h, out=on)
+        un, on = on, un
+    dt = allreduce_max(time.perf_counter() - t0, world, device="cuda")
+    e2e = {"value": LINES * N_SPACE * e2e_steps / dt, "unit": "updates/s",
+           "h2d_bytes_per_step": int(L * N_SPACE * 8 + L * 8 + N_SPACE * 8),
+           "d2h_bytes_per_step": int(L * N_SPACE * 8),
+           "steps": e2e_steps, "api": "lob_step_host_f64 (pinned host buffers), per GPU"}
+    # the e2e roofline: the same bytes moved by plain copies alone (H2D and D2H on two
+    # streams at once, pinned buffers, no compute) - the host link bounds the e2e number
+    dbuf_in = torch.empty_like(uh, device="cuda")
+    dbuf_out = torch.empty_like(uh, device="cuda")
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    for rep in range(e2e_steps + 1):
+        if rep == 1:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+        with torch.cuda.stream(s_in):
+            dbuf_in.copy_(uh, non_blocking=True)
+        with torch.cuda.stream(s_out):
+            oh.copy_(dbuf_out, non_blocking=True)
+    torch.cuda.synchronize()
+    dtc = allreduce_max(time.perf_counter() - t0, world, device="cuda")
+    bound = LINES * N_SPACE * e2e_steps / dtc
+    e2e["copy_bound"] = {"value": bound, "unit": "updates/s", "frac": e2e["value"] / bound,
+                         "what": "concurrent pinned H2D + D2H of one step's state, no compute"}
+    del dbuf_in, dbuf_out, a, b, ws
+    st.clear()
+    torch.cuda.empty_cache()
 
     if rank != 0:
         return
@@ -323,15 +343,15 @@ def run_b200(args, world, rank, local):
     line = {
         "metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded C2 generators, include/laxol_b200_configs.h)",
-        "config": {"workload": WORKLOAD, "engine": "K2 fast exact min-plus (LOB_ENGINE_FAST), chained steps",
-                   "presteps": args.presteps, "lines_per_gpu": LINES, "n": N_SPACE,
-                   "l2": "working set 268 MB > 126 MB L2 (no flush needed)",
-                   "parallelism": f"line-sharded replicas x{world}", "state_finite": finite,
-                   "step_stats": "not requested (step_fully_discrete's default)",
-                   "with_block_counts_ms_per_step": ms_blocks,
-                   "mean_blocks_per_line": blocks_mean},
+        "config": config_for(world),
+        "impl_detail": {"engine": "K2 fast exact min-plus (LOB_ENGINE_FAST), chained steps",
+                        "presteps": args.presteps, "lines_per_gpu": L, "state_finite": finite,
+                        "step_stats": "not requested (step_fully_discrete's default)",
+                        "with_block_counts_ms_per_step": ms_blocks, "mean_blocks_per_line": blocks_mean,
+                        "hbar_gathered": {"lines": int(hb.size), "T": T, "min": float(hb.min()),
+                                          "max": float(hb.max()), "finite": bool(np.isfinite(hb).all())}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
                      "algorithmic_bytes_per_update": 16},
@@ -343,9 +363,55 @@ def run_b200(args, world, rank, local):
         if r is not None:
             line["cpu_baseline"] = {"value": r[0], "unit": "updates/s", "cores": nthreads, "kind": "reference",
                                     "sample": r[2], "seconds": r[1]}
+    if world == 1:
+        line["c5"] = c5_workload(dev, hbm_peak)
     if not args.no_extras and world == 1:
         line["kernels"] = extras(dev)
     print(json.dumps(line))
+
+
+def c5_workload(dev, hbm_peak):
+    """C5 (configs[4], the largest per-step config): 64 lines x N=2^20, tau=0.005, P=0.25,
+    V=0.5 sin(2 pi x), u0 = 64 random Fourier modes; K2 steps after 20 untimed ones."""
+    import torch
+
+    from paper_1210_4090_b200 import api
+
+    n, tau, L = 1 << 20, 0.005, 64
+    cur = torch.from_numpy(api.gen_c5_lines(0, L, n)).cuda()
+    nxt = torch.empty_like(cur)
+    tv = torch.from_numpy(api.tau_v(api.gen_potential(3, n), tau)).cuda()
+    dd = torch.full((L,), 0.25, dtype=torch.float64, device="cuda")
+    ws = torch.empty(dev.fast_workspace_bytes(L, n), dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    k = 0
+
+    def run(m):
+        nonlocal cur, nxt, k
+        for _ in range(m):
+            dev.fast_f64(cur, nxt, dd, tau, tv=tv, workspace=ws,
+                         flags=api.FAST_CHAINED | (api.FAST_STATS_VALID if k else 0), stream=stream)
+            cur, nxt = nxt, cur
+            k += 1
+
+    run(20)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = 50
+    e0.record(stream)
+    run(steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    c = dev.fast_counters(ws, L, n)
+    ach = L * n * 16 / (ms * 1e-3) / 1e9
+    out = {"workload": "C5: 64 lines x N=2^20, tau=0.005, P=0.25, V=0.5 sin(2 pi x), 64 random modes",
+           "ms_per_step": ms, "updates_per_s": L * n / (ms * 1e-3), "steps": steps, "presteps": 20,
+           "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak},
+           "walk_tiles": c["tiles"] - c["direct_tiles_gate"] - c["direct_tiles_heavy"], "tiles": c["tiles"]}
+    del cur, nxt, ws
+    torch.cuda.empty_cache()
+    return out
 
 
 def extras(dev):
@@ -387,15 +453,21 @@ def extras(dev):
     dev.set_direct_mode(api.DIRECT_SCREENED)
     dev.direct_fallbacks(reset=True)
     t = timeit(lambda: dev.direct_f64(u, o, dk, df), 5)
+    # the screened sweep runs on the FP32 pipes: one FADD (FMA pipe, 128 lanes/SM/clk) and half
+    # an FMNMX3 (ALU pipe, 64 lanes/SM/clk) per candidate -> both ceilings are 128 cand/SM/clk
+    import torch as _t
+    fp32_peak = _t.cuda.get_device_properties(0).multi_processor_count * 128 * fp["sm_clock_ghz"] * 1e9
     out["k1_direct_c3_f64"] = {
         "ms": t * 1e3, "updates_per_s": 4096 * 4096 / t, "cand_per_s": cand / t,
         "impl": "fp32 screen + fp64 re-evaluation (bit-identical; LOB_DIRECT_SCREENED, the default)",
         "full_fp64_outputs_per_call": dev.direct_fallbacks() / 6,
-        "roofline": {"bound": "fp64 pipe (algorithmic ops: 2 per candidate)", "achieved_ops": 2 * cand / t,
-                     "peak_ops": fp["dadd_ops_per_s"], "frac": 2 * cand / t / fp["dadd_ops_per_s"]}}
+        "roofline": {"bound": "fp32 issue (FADD on the FMA pipe + FMNMX3 on the ALU pipe per 2 candidates)",
+                     "achieved_cand_per_s": cand / t, "peak_cand_per_s": fp32_peak, "frac": cand / t / fp32_peak}}
     u32, o32, dk32 = u.float(), torch.empty_like(u.float()), dk.float()
     t = timeit(lambda: dev.direct_f32(u32, o32, dk32, df), 5)
-    out["k1_direct_c3_f32"] = {"ms": t * 1e3, "updates_per_s": 4096 * 4096 / t, "cand_per_s": cand / t}
+    out["k1_direct_c3_f32"] = {"ms": t * 1e3, "updates_per_s": 4096 * 4096 / t, "cand_per_s": cand / t,
+                               "roofline": {"bound": "fp32 issue", "peak_cand_per_s": fp32_peak,
+                                            "frac": cand / t / fp32_peak}}
     ws = torch.empty(dev.fast_workspace_bytes(4096, n), dtype=torch.uint8, device="cuda")
     z = torch.zeros(4096, dtype=torch.float64, device="cuda")
     t = timeit(lambda: dev.fast_f64(u, o, z, 0.01, workspace=ws), 10)

@@ -122,13 +122,21 @@ int lob_minplus_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lin
                          int flags, void* stream);
 
 /* Fast-engine counters, cumulative since the last call without
- * LOB_FAST_STATS_VALID on this workspace (counters[8]):
- *  [0] outputs for which the local-minimum walk produced no candidate and the
- *      exact direct scan was used instead (0 in correct operation),
- *  [1] sources scanned, [2] candidates emitted inline, [3] candidates from
- *  queued intervals, [4] queued intervals, [5] tiles processed,
- *  [6] tiles whose K range did not fit the shared-memory stage, [7] sum of
- *  the tiles' K range lengths. */
+ * LOB_FAST_STATS_VALID on this workspace (counters[16]; unused entries 0):
+ *  [0] outputs no local-minimum interval reached, recomputed by the exact
+ *      direct scan (0 in correct operation),
+ *  [1] sources scanned by the walk, [2] fold ranges (outputs covered twice,
+ *  exact CAS-min), [3] long frontier / gap runs stored by a whole warp,
+ *  [4] tiles, [5] walk tiles whose K range did not fit the shared-memory stage,
+ *  [6] sum of the walk tiles' K range lengths,
+ *  [7] tiles computed by the direct formula because the oscillation gate failed
+ *      (max u - min u not below the window's edge gap, non-finite u, or a
+ *      window outside the cached v_d table),
+ *  [8] tiles computed by the direct formula because the walk's estimated
+ *      candidate count exceeded a quarter of the window's,
+ *  [9] chained-step waits that timed out (a misused LOB_FAST_CHAINED; the
+ *      results of that call are not trustworthy),
+ *  [10] warps whose fold queue overflowed (re-walked, exact). */
 int lob_fast_diagnostics(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n,
                          uint64_t* counters);
 

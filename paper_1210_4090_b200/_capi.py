@@ -12,6 +12,8 @@ from ctypes import POINTER, c_char_p, c_double, c_int, c_int64, c_size_t, c_uint
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "liblaxol_b200.so")
+# the seeded synthetic-workload generators (include/laxol_b200_configs.h): host code, no device
+CONFIGS_PATH = os.path.join(_HERE, "lib", "liblaxol_configs.so")
 
 LOB_OK = 0
 LOB_INVALID_INPUT = 1
@@ -34,8 +36,7 @@ class LobPotential(ctypes.Structure):
     _fields_ = [("kind", c_int), ("value", c_double), ("offset", c_double), ("amplitude", c_double),
                 ("frequency", c_int), ("tmod", c_int), ("omega", c_double)]
 
-# name -> (restype, argtypes); every symbol declared in include/laxol_b200.h
-# and include/laxol_b200_configs.h.
+# name -> (restype, argtypes); every symbol declared in include/laxol_b200.h.
 _P = c_void_p
 SIGNATURES = {
     "lob_ctx_create": (c_int, [c_int, POINTER(c_void_p)]),
@@ -87,6 +88,13 @@ SIGNATURES = {
     "lob_decompose_f64": (c_int, [_P, _P, c_int64, c_double, _P, _P, _P, c_int64, POINTER(c_int64), _P]),
     "lob_conv_fast_f64": (c_int, [_P, _P, c_int64, _P, c_int64, c_double, _P, POINTER(c_int64), _P]),
     # synthetic workloads (include/laxol_b200_configs.h)
+}
+
+_lib = None
+_cfg = None
+
+# include/laxol_b200_configs.h (liblaxol_configs.so)
+CONFIG_SIGNATURES = {
     "lob_gen_sin": (None, [c_int64, _P]),
     "lob_gen_cos": (None, [c_int64, _P]),
     "lob_gen_potential": (None, [c_int, c_int64, _P]),
@@ -96,8 +104,6 @@ SIGNATURES = {
     "lob_c4_time_term": (c_double, [c_double]),
     "lob_gen_c5_lines": (None, [c_int64, c_int64, c_int64, c_uint64, _P, c_int]),
 }
-
-_lib = None
 
 
 class LaxolError(RuntimeError):
@@ -134,6 +140,24 @@ def load(path: str | None = None, required_symbols=None):
         fn.argtypes = args
     if path == LIB_PATH:
         _lib = lib
+    return lib
+
+
+def load_configs(path: str | None = None):
+    """Load the synthetic-workload generator library (host code only)."""
+    global _cfg
+    if _cfg is not None and path is None:
+        return _cfg
+    p = path or CONFIGS_PATH
+    if not os.path.exists(p):
+        raise OSError(f"laxol_b200 generator library not built: {p} (run __graft_entry__.build())")
+    lib = ctypes.CDLL(p)
+    for name, (res, args) in CONFIG_SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _cfg = lib
     return lib
 
 

@@ -199,14 +199,16 @@ class Device:
                                            _ptr(workspace), ws_bytes, int(flags), _stream_ptr(stream))
         self._check(st, "lob_minplus_fast_f64")
 
+    FAST_COUNTER_KEYS = ["missed_outputs", "sources", "fold_ranges", "plain_runs", "tiles", "tiles_k_unstaged",
+                         "k_range_sum", "direct_tiles_gate", "direct_tiles_heavy", "chain_timeouts",
+                         "fold_overflow_warps"]
+
     def fast_counters(self, workspace, lines: int, n: int) -> dict:
         """The fast engine's work counters (include/laxol_b200.h, lob_fast_diagnostics)."""
-        v = (ctypes.c_uint64 * 8)()
+        v = (ctypes.c_uint64 * 16)()
         st = self.lib.lob_fast_diagnostics(self.ctx, _ptr(workspace), lines, n, v)
         self._check(st, "lob_fast_diagnostics")
-        keys = ["missed_outputs", "sources", "inline_candidates", "queued_candidates", "queued_intervals",
-                "tiles", "tiles_k_unstaged", "k_range_sum"]
-        return {k: int(v[i]) for i, k in enumerate(keys)}
+        return {k: int(v[i]) for i, k in enumerate(self.FAST_COUNTER_KEYS)}
 
     def fast_diagnostics(self, workspace, lines: int, n: int) -> int:
         return self.fast_counters(workspace, lines, n)["missed_outputs"]
@@ -436,42 +438,42 @@ def potential_cosine(offset: float, amplitude: float, frequency: int, tmod: int 
 
 def gen_sin(n: int) -> np.ndarray:
     out = np.empty(n, np.float64)
-    _capi.load().lob_gen_sin(n, out.ctypes.data)
+    _capi.load_configs().lob_gen_sin(n, out.ctypes.data)
     return out
 
 
 def gen_cos(n: int) -> np.ndarray:
     out = np.empty(n, np.float64)
-    _capi.load().lob_gen_cos(n, out.ctypes.data)
+    _capi.load_configs().lob_gen_cos(n, out.ctypes.data)
     return out
 
 
 def gen_potential(kind: int, n: int) -> np.ndarray:
     out = np.empty(n, np.float64)
-    _capi.load().lob_gen_potential(int(kind), n, out.ctypes.data)
+    _capi.load_configs().lob_gen_potential(int(kind), n, out.ctypes.data)
     return out
 
 
 def gen_c2_drifts(lines: int = 256) -> np.ndarray:
     out = np.empty(lines, np.float64)
-    _capi.load().lob_gen_c2_drifts(lines, out.ctypes.data)
+    _capi.load_configs().lob_gen_c2_drifts(lines, out.ctypes.data)
     return out
 
 
 def gen_c3_lines(line0: int, lines: int, n: int = 4096, seed0: int = 1000) -> np.ndarray:
     out = np.empty((lines, n), np.float64)
-    _capi.load().lob_gen_c3_lines(line0, lines, n, seed0, out.ctypes.data)
+    _capi.load_configs().lob_gen_c3_lines(line0, lines, n, seed0, out.ctypes.data)
     return out
 
 
 def gen_c4_u0(n: int = 2048) -> np.ndarray:
     out = np.empty((n, n), np.float64)
-    _capi.load().lob_gen_c4_u0(n, out.ctypes.data)
+    _capi.load_configs().lob_gen_c4_u0(n, out.ctypes.data)
     return out
 
 
 def c4_time_term(t: float) -> float:
-    return float(_capi.load().lob_c4_time_term(float(t)))
+    return float(_capi.load_configs().lob_c4_time_term(float(t)))
 
 
 def gen_c5_lines(line0: int, lines: int, n: int = 1 << 20, seed0: int = 5000,
@@ -480,7 +482,7 @@ def gen_c5_lines(line0: int, lines: int, n: int = 1 << 20, seed0: int = 5000,
 
     out = np.empty((lines, n), np.float64)
     nt = nthreads or (os.cpu_count() or 1)
-    _capi.load().lob_gen_c5_lines(line0, lines, n, seed0, out.ctypes.data, nt)
+    _capi.load_configs().lob_gen_c5_lines(line0, lines, n, seed0, out.ctypes.data, nt)
     return out
 
 

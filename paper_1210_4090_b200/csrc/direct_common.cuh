@@ -88,14 +88,30 @@ __device__ __forceinline__ void sweep_range(T* Us, T* Ks, const T* __restrict__ 
             T B[R];
 #pragma unroll
             for (int k = 0; k < R; ++k) B[k] = pa[-2 - k];
+            if constexpr (sizeof(T) == 4) {
+                // fp32: two displacements per exact min, fminf(best, fminf(c0, c1)) -> one 3-input
+                // FMNMX3 per two candidates (the min is order-free; NaN-free operands)
 #pragma unroll
-            for (int s = 0; s < R; ++s) {
-                const T kw = Ks[s0 + s];
+                for (int s = 0; s < R; s += 2) {
+                    const T kw0 = Ks[s0 + s], kw1 = Ks[s0 + s + 1];
 #pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const int idx = r - s;
-                    const T val = idx >= 0 ? A[idx >= 0 ? idx : 0] : B[idx < 0 ? -idx - 1 : 0];
-                    best[r] = min_exact<T>(best[r], add_rn<T>(val, kw));
+                    for (int r = 0; r < R; ++r) {
+                        const int i0 = r - s, i1 = r - s - 1;
+                        const T v0 = i0 >= 0 ? A[i0 >= 0 ? i0 : 0] : B[i0 < 0 ? -i0 - 1 : 0];
+                        const T v1 = i1 >= 0 ? A[i1 >= 0 ? i1 : 0] : B[i1 < 0 ? -i1 - 1 : 0];
+                        best[r] = fminf(best[r], fminf(add_rn<T>(v0, kw0), add_rn<T>(v1, kw1)));
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int s = 0; s < R; ++s) {
+                    const T kw = Ks[s0 + s];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const int idx = r - s;
+                        const T val = idx >= 0 ? A[idx >= 0 ? idx : 0] : B[idx < 0 ? -idx - 1 : 0];
+                        best[r] = min_exact<T>(best[r], add_rn<T>(val, kw));
+                    }
                 }
             }
 #pragma unroll

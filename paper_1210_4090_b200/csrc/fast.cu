@@ -82,6 +82,13 @@ constexpr int kVCap = LOB_VCAP;  // v_d values staged per tile (TMA, with the fi
 #define LOB_FAST_WORK_COUNTERS 0  // per-source inline-candidate count (diagnostic builds only)
 #endif
 
+#ifndef LOB_TILE_DIRECT
+#define LOB_TILE_DIRECT 1
+#endif
+#ifndef LOB_OSC_EXACT
+#define LOB_OSC_EXACT 1  // gate on the line's oscillation max u - min u (else on (n/2) max |slope|)
+#endif
+
 struct LineConst {
     long long first;  // window displacement of w = 0
     double pe;        // drift * eps
@@ -183,6 +190,7 @@ __device__ __forceinline__ unsigned long long warp_fsm(unsigned long long f) {
 
 struct EpiShared {
     unsigned kred[2][kNT / 32];
+    unsigned ured[2][kNT / 32];
     unsigned long long fsm[kNT];
 };
 
@@ -239,6 +247,20 @@ __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line,
             kmax = max(kmax, k);
         }
     }
+    // exact extremes of the tile's own values u(j0 + 8t .. j0 + 8t + 7): the
+    // oscillation gate of the next step
+    // (coarse 32-bit keys: an enclosure within 2^-20 relative, like the slope bounds)
+    unsigned hmn = 0xffffffffu, hmx = 0u;
+#if LOB_OSC_EXACT
+#pragma unroll
+    for (int m = 1; m <= kPer; ++m) {
+        if (FULL || m <= Tl - i0) {
+            const unsigned k = hkey(w[m]);
+            hmn = min(hmn, k);
+            hmx = max(hmx, k);
+        }
+    }
+#endif
     // decompose() FSM over increments e = j0 + 8t + 1 + k: inc = s(e) - s(e-1),
     // two increments per table lookup.  Non-finite u (which the reference
     // rejects before decompose, proj/src/scheme.cpp:18-24) is not classified.
@@ -266,6 +288,10 @@ __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line,
     }
     kmin = __reduce_min_sync(0xffffffffu, kmin);
     kmax = __reduce_max_sync(0xffffffffu, kmax);
+    if (LOB_OSC_EXACT) {
+        hmn = __reduce_min_sync(0xffffffffu, hmn);
+        hmx = __reduce_max_sync(0xffffffffu, hmx);
+    }
     if (lane == 0) {
         const double smn = hkey_lower(kmin), smx = hkey_upper(kmax);
         if (FULL || warp * kG < Tl) {
@@ -274,6 +300,8 @@ __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line,
         }
         sh.kred[0][warp] = kmin;
         sh.kred[1][warp] = kmax;
+        sh.ured[0][warp] = hmn;
+        sh.ured[1][warp] = hmx;
     }
     __syncthreads();
     if (warp == 0) {
@@ -289,9 +317,15 @@ __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line,
         unsigned a1 = lane < kNT / 32 ? sh.kred[1][lane] : 0u;
         a0 = __reduce_min_sync(0xffffffffu, a0);
         a1 = __reduce_max_sync(0xffffffffu, a1);
+        const unsigned m0 = __reduce_min_sync(0xffffffffu, lane < kNT / 32 ? sh.ured[0][lane] : 0xffffffffu);
+        const unsigned m1 = __reduce_max_sync(0xffffffffu, lane < kNT / 32 ? sh.ured[1][lane] : 0u);
         if (lane == 0) {
             if (fsm_on) b.fsm_out[line * p.tiles + tile] = f;
             unsigned long long* L = b.line_out + line * 4;
+            if (LOB_OSC_EXACT) {
+                atomicMin(L + 0, dkey(hkey_lower(m0)));
+                atomicMax(L + 1, dkey(hkey_upper(m1)));
+            }
             atomicMin(L + 2, dkey(hkey_lower(a0)));
             atomicMax(L + 3, dkey(hkey_upper(a1)));
         }
@@ -370,20 +404,30 @@ constexpr int kValsLen = P8(kT + 3) + 2;
 #define LOB_WIDE_RANGE kVCap  // displacement range above which a tile scans source runs
 #endif
 constexpr int kRuns = 8;  // source runs per wide tile (more are merged into the last)
+#ifndef LOB_HEAVY
+#define LOB_HEAVY 0.25
+#endif
+constexpr int kTW = 1024;  // displacements per staged chunk of the direct tile sweep
+
+enum : int { kModeWalk = 0, kModeDirect = 1 };
+
 struct MainShared {
     unsigned long long keys[kT + 4];   // exact-min slots (+inf bits = empty), lane-interleaved access
     unsigned long long mbar;           // TMA completion barrier for the source chunk
     __align__(16) double ubuf[kC + 8];  // sources (unpadded) / then u^{n+1} (padded, stats)
     int3 queue[kQCap];
     __align__(16) double vbuf[kVCap];  // v_d of the tile's displacement range, converted to K(d)
-    int ya, yb, nq, dlo, dhi, DLg, DRg, ok;
+    int ya, yb, nq, dlo, dhi, DLg, DRg, mode, gate, abort;
+    unsigned qwork, budget;            // long queued runs of the tile, and the walk's work budget
     int nruns, rs[kRuns], re[kRuns];  // runs of reaching sub-tiles (unrolled source ranges)
-    unsigned int c_inline, c_queued, c_src, c_qent;
+    unsigned int c_src, c_queued, c_qent;
     __device__ EpiShared& epi() { return *reinterpret_cast<EpiShared*>(keys); }
 };
 static_assert(kValsLen <= kC + 8, "u^{n+1} of the tile fits in ubuf");
 static_assert(sizeof(EpiShared) <= (kT + 4) * 8, "statistics scratch fits in keys");
-static_assert(LOB_FAST_MINB * (sizeof(MainShared) + 1024) <= 233472, "LOB_FAST_MINB CTAs per SM");
+// per-CTA shared allocations are rounded to 128 bytes, plus 1 KB the driver reserves
+static_assert(LOB_FAST_MINB * ((sizeof(MainShared) + 127) / 128 * 128 + 1024) <= 233472, "LOB_FAST_MINB CTAs per SM");
+static_assert((P8(kT + kTW) + 1 + kTW) * 8 <= sizeof(MainShared), "direct tile sweep fits the shared layout");
 
 // ---- TMA bulk copies (cp.async.bulk) completed on an mbarrier ------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -437,6 +481,18 @@ __device__ __forceinline__ void smem_fmin(unsigned long long* addr, double c) {
     }
 }
 
+// exact min into a slot that already holds a value (the frontier candidate or the gap's
+// +inf): a plain read first, the CAS only when c improves on it
+__device__ __forceinline__ void smem_fmin_set(unsigned long long* addr, double c) {
+    const unsigned long long cb = static_cast<unsigned long long>(__double_as_longlong(c));
+    unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(addr);
+    while (c < __longlong_as_double(static_cast<long long>(old))) {
+        const unsigned long long prev = atomicCAS(addr, old, cb);
+        if (prev == old) break;
+        old = prev;
+    }
+}
+
 // One thread: TMA bulk copies of U(yc-1 .. yc+clen) (wrapped at the period,
 // 16-byte aligned even start) into ubuf, plus optionally vcnt v_d values.
 __device__ __forceinline__ void issue_chunk(MainShared& S, const double* ul, int n, int yc, int clen,
@@ -474,13 +530,14 @@ __device__ __forceinline__ double kvalue(const ChunkArgs& a, int d) {
 // Each source's first two displacements go straight to the output slots
 // with one CAS against the empty sentinel; slots already holding a larger
 // value, and intervals longer than two, are queued and finished after the
-// barrier with exact CAS-min loops, one warp per queued source.
+// barrier with exact CAS-min loops, one warp per queued source.  Returns false
+// when the queued work exceeds `budget` (the walk would cost more than the
+// window: the tile switches to the direct formula; the queue is not processed).
 template <bool KS>
-__device__ __forceinline__ void process_chunk(MainShared& S, const ChunkArgs& a) {
+__device__ __forceinline__ bool process_chunk(MainShared& S, const ChunkArgs& a, unsigned budget) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int per = ((a.clen + kNT - 1) / kNT) * 32;
     const int iend = min(a.clen, (warp + 1) * per);
-    unsigned ninl = 0;
 #pragma unroll kEmitUnroll
     for (int i = warp * per + lane; i < iend; i += 32) {
         const double ul0 = a.ub[i], u0 = a.ub[i + 1], ur0 = a.ub[i + 2];
@@ -504,22 +561,25 @@ __device__ __forceinline__ void process_chunk(MainShared& S, const ChunkArgs& a)
                     atomicCAS(slot + 1, kInfBits, static_cast<unsigned long long>(__double_as_longlong(c1)));
                 r1 = o1 != kInfBits && c1 < __longlong_as_double(static_cast<long long>(o1));
             }
-            if constexpr (LOB_FAST_WORK_COUNTERS) ninl += min(dr - dl + 1, 2);
             const bool longer = dl + 2 <= dr;
             if (r0 | r1 | longer) {
                 const int qlo = r0 ? dl : (r1 ? dl + 1 : dl + 2);
                 const int qhi = longer ? dr : (r1 ? dl + 1 : dl);
                 const int q = atomicAdd(&S.nq, 1);
+                // long runs count against the walk's work budget
+                if (qhi - qlo >= 32) atomicAdd(&S.qwork, static_cast<unsigned>(qhi - qlo + 1));
                 if (q < kQCap) {
                     S.queue[q] = make_int3(i, qlo, qhi);
-                } else {
+                } else if (*reinterpret_cast<volatile unsigned*>(&S.qwork) <= S.budget) {
                     for (int d = qlo; d <= qhi; ++d) smem_fmin(&S.keys[off + d], __dadd_rn(u0, kvalue<KS>(a, d)));
+                } else {
+                    S.abort = 1;  // a heavy tile: the queued runs already exceed the budget
                 }
             }
         }
     }
-    if (LOB_FAST_WORK_COUNTERS && ninl) atomicAdd(&S.c_inline, ninl);
     __syncthreads();
+    if (S.abort || S.qwork > budget) return false;
     const int nq = min(S.nq, kQCap);
     if (nq) {
         for (int e = warp; e < nq; e += kNT / 32) {
@@ -536,6 +596,111 @@ __device__ __forceinline__ void process_chunk(MainShared& S, const ChunkArgs& a)
         }
         __syncthreads();
     }
+    return true;
+}
+
+// Loads of data the previous step's grid may still be finishing (chained mode):
+// through L2, never a stale L1 line.
+template <bool CHAIN, typename T>
+__device__ __forceinline__ T xload(const T* p) {
+    if constexpr (CHAIN) return __ldcg(p);
+    else return *p;
+}
+
+__device__ __forceinline__ unsigned long long dbits(double x) {
+    return static_cast<unsigned long long>(__double_as_longlong(x));
+}
+
+// K(d) anywhere in the window: the cached v_d table, or (a line whose window leaves the
+// table) v_d computed with build_kernel's own two roundings (proj/src/scheme.cpp:79-80)
+__device__ __forceinline__ double kdirect(const FastParams& p, int d, double drift) {
+    const double v = static_cast<unsigned>(d + p.vofs) <= static_cast<unsigned>(2 * p.vofs)
+                         ? __ldg(p.vtab + p.vofs + d)
+                         : __ddiv_rn(__dmul_rn(static_cast<double>(d), p.eps), p.tau);
+    return kval_v(v, drift, p.tau);
+}
+
+// The tile by the direct formula (proj/tests/unit_scheme.cpp:184-190) when the walk
+// does not apply (oscillation gate failed, window outside the v_d table) or would cost
+// more than the window (estimated candidates): keys[i] = min_w U(jlo + i - first - w) +
+// K(first + w).  The tile's own outputs use K1's register-blocked sweep
+// (csrc/direct_common.cuh): 8 outputs per thread, the window in chunks of kTW
+// displacements staged in shared memory, one LDS per displacement and one add + one
+// exact min per candidate; the three halo outputs are one warp each.
+template <bool CHAIN>
+__device__ void tile_direct(MainShared& S, const double* ul, int n, int j0, int Tl, int first,
+                            const FastParams& p, double drift) {
+    constexpr int R = kPer, L = kT + kTW;
+    double* Us = reinterpret_cast<double*>(&S);
+    double* Ks = Us + P8(L) + 1;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int W = 2 * n + 1;
+    double hb = INFINITY;
+    if (warp < 3) {
+        int j = warp == 0 ? j0 - 1 : j0 + Tl + warp - 1;
+        j = j < 0 ? j + n : (j >= n ? j - n : j);
+        int y0 = (j - first) % n;
+        if (y0 < 0) y0 += n;
+        for (int w = lane; w < W; w += 32) {
+            int y = (y0 - w) % n;
+            if (y < 0) y += n;
+            const double c = __dadd_rn(xload<CHAIN>(ul + y), kdirect(p, first + w, drift));
+            hb = c < hb ? c : hb;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const double c = __shfl_xor_sync(0xffffffffu, hb, o);
+            hb = c < hb ? c : hb;
+        }
+    }
+    double best[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) best[r] = INFINITY;
+    for (int wc = 0; wc < W; wc += kTW) {
+        __syncthreads();
+        // sources y = j - first - w for j in [j0, j0 + kT), w in [wc, wc + kTW)
+        int ym = (j0 - first - wc - kTW) % n;
+        if (ym < 0) ym += n;
+        for (int i = tid; i < L; i += kNT) {
+            int y = ym + i;
+            while (y >= n) y -= n;
+            Us[P8(i)] = xload<CHAIN>(ul + y);
+        }
+        for (int s = tid; s < kTW; s += kNT) Ks[s] = wc + s < W ? kdirect(p, first + wc + s, drift) : INFINITY;
+        __syncthreads();
+        const double* pa = Us + P8(tid * R + kTW);
+        double A[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) A[k] = pa[k];
+        const int send = min(kTW, (W - wc + R - 1) / R * R);
+#pragma unroll 1
+        for (int s0 = 0; s0 < send; s0 += R) {
+            double B[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) B[k] = pa[-2 - k];
+#pragma unroll
+            for (int s = 0; s < R; ++s) {
+                const double kw = Ks[s0 + s];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int idx = r - s;
+                    const double val = idx >= 0 ? A[idx >= 0 ? idx : 0] : B[idx < 0 ? -idx - 1 : 0];
+                    const double c = __dadd_rn(val, kw);
+                    best[r] = c < best[r] ? c : best[r];
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < R; ++k) A[k] = B[R - 1 - k];
+            pa -= R + 1;
+        }
+    }
+    __syncthreads();  // the staging area is dead: keys take the results
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = 1 + R * tid + r;
+        if (i <= Tl) S.keys[i] = dbits(best[r]);
+    }
+    if (warp < 3 && lane == 0) S.keys[warp == 0 ? 0 : Tl + warp] = dbits(hb);
 }
 
 // Per-line constants of the step (identical IEEE operations to the host's
@@ -553,38 +718,44 @@ __global__ void line_setup_kernel(const double* __restrict__ drift_arr, int64_t 
     const double vmax = dm * eps / tau;
     const double kmag = tau * (0.5 * vmax * vmax + fabs(drift) * vmax);
     const double delta = 2.0 * (32.0 * uu * kmag / a + 8.0 * uu * (2.0 * n + fabs(drift) * eps / a) + 1e-9);
-    const double kfirst = kval(p.vtab, p.vofs, first, drift, tau);
-    const double klast = kval(p.vtab, p.vofs, first + 2 * n, drift, tau);
-    double kmin = INFINITY;
-    for (int64_t d = center - 2; d <= center + 2; ++d)
-        if (d >= first && d <= first + 2 * n) kmin = fmin(kmin, kval(p.vtab, p.vofs, d, drift, tau));
+    // the walk reads K through the cached v_d table: its window must lie inside it
+    const bool intab = first >= -p.vofs && first + 2 * n <= p.vofs;
     LineConst c;
     c.first = first;
     c.pe = __dmul_rn(drift, eps);
     const double pz = __dmul_rn(c.pe, p.ia);  // P eps / a
     c.hl = pz - (0.5 + delta);
     c.hr = pz + (0.5 + delta);
-    c.gap = fmin(kfirst, klast) - kmin;
     c.drift = drift;
+    if (intab) {
+        const double kfirst = kval(p.vtab, p.vofs, first, drift, tau);
+        const double klast = kval(p.vtab, p.vofs, first + 2 * n, drift, tau);
+        double kmin = INFINITY;
+        for (int64_t d = center - 2; d <= center + 2; ++d)
+            if (d >= first && d <= first + 2 * n) kmin = fmin(kmin, kval(p.vtab, p.vofs, d, drift, tau));
+        c.gap = fmin(kfirst, klast) - kmin;
+    } else {
+        c.gap = -INFINITY;  // never passes the gate: the line's tiles take the direct formula
+    }
     lc[line] = c;
 }
 
 // Main K2 kernel: one CTA = (tile of kT outputs, line); grid (tiles, lines).
 // All index arithmetic is 32-bit (n <= 2^29); "unrolled" source/output
 // indices y, j may lie in (-3n, 3n) and are reduced mod n only on access.
-// Loads of data the previous step's grid may still be finishing (chained mode):
-// through L2, never a stale L1 line.
-template <bool CHAIN, typename T>
-__device__ __forceinline__ T xload(const T* p) {
-    if constexpr (CHAIN) return __ldcg(p);
-    else return *p;
-}
-
 // TMA: rows may be bulk-copied (even n, aligned).  CHAIN: the previous operation on
 // the stream was the previous step on this workspace (and it released); a tile waits
 // only for the warps of its own line at that step (per-line release counters, `need`)
 // instead of the whole previous grid, so consecutive steps overlap.  RELEASE: count
 // this step's warps into the per-line counters for a chained successor.
+//
+// Diagnostic counters (diag[]): [0] outputs no candidate reached (recomputed by the
+// direct scan), [1] sources scanned, [2] fold ranges, [3] long plain runs, [4] tiles,
+// [5] tiles whose K range did not fit the shared stage, [6] sum of the tiles' K range
+// lengths, [7] tiles by the direct formula because the oscillation gate failed,
+// [8] tiles by the direct formula because the walk's estimated candidates exceeded the
+// window's, [9] chained-wait timeouts (a misused LOB_FAST_CHAINED), [10] warps whose
+// fold queue overflowed.
 template <bool TMA, bool CHAIN, bool RELEASE>
 __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
     const double* __restrict__ u, double* __restrict__ out, const LineConst* __restrict__ lcs,
@@ -632,9 +803,12 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
                     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(done + line) : "memory");
                     if (v >= need) break;
                     __nanosleep(128);
-                    // a misused LOB_FAST_CHAINED (the previous step is not on this stream) ends
-                    // in an error, not a hang
-                    if (clock64() - t0 > (1ll << 33)) __trap();
+                    // a misused LOB_FAST_CHAINED (the previous step is not on this stream):
+                    // counted and reported by the host, never a hang or a trap
+                    if (clock64() - t0 > (1ll << 34)) {
+                        atomicAdd(diag + 9, 1ull);
+                        break;
+                    }
                 }
                 asm volatile("fence.proxy.async.global;" ::: "memory");  // for the TMA reads of u
             }
@@ -646,47 +820,51 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
     // reset the line statistics buffer two steps ahead
     if (tile == 0 && tid < 4) b.line_reset[line * 4 + tid] = (tid & 1) ? 0ull : ~0ull;
 
-    // ---- warp 0: line gate, candidate sub-tiles, first TMA issue ----
+    // ---- warp 0: line gate, candidate sub-tiles, work estimate, first TMA issue ----
     if (warp == 0) {
-        // line statistics: oscillation gate and global displacement bounds
         const unsigned long long* L = b.line_in + line * 4;
+        const double umin = dkey_inv(xload<CHAIN>(L + 0)), umax = dkey_inv(xload<CHAIN>(L + 1));
         const double smin = dkey_inv(xload<CHAIN>(L + 2)), smax = dkey_inv(xload<CHAIN>(L + 3));
         int DLg = dmin_w, DRg = dmax_w;
-        // oscillation of a periodic line <= (n/2) max|slope| (shorter arc)
-        const double osc_bound = 0.5 * static_cast<double>(n) * fmax(fabs(smin), fabs(smax));
-        bool okl = (osc_bound * (1.0 + 1e-12) < lc.gap * (1.0 - 1e-12)) && n >= 3 && isfinite(smin) &&
-                   isfinite(smax);
+        // window-edge displacements cannot hold a minimiser when the line's oscillation
+        // max u - min u is below the window's edge gap min(K(first), K(last)) - min K
+        const double osc = LOB_OSC_EXACT ? __dsub_rn(umax, umin)
+                                         : 0.5 * static_cast<double>(n) * fmax(fabs(smin), fabs(smax));
+        bool okl = isfinite(osc) && isfinite(smin) && isfinite(smax) && n >= 3 &&
+                   osc * (1.0 + 1e-12) < lc.gap * (1.0 - 1e-12);
+        const bool gate = okl;
         if (okl) {
             DLg = max(__double2int_ru(__fma_rn(smin, ia, hl)), dmin_w);
             DRg = min(__double2int_rd(__fma_rn(smax, ia, hr)), dmax_w);
             okl = DLg <= DRg;
         }
         int ya = INT_MAX, yb = INT_MIN, dlo = INT_MAX, dhi = INT_MIN;
+        int Q0 = 0, Q1 = -1;
+        // sub-tile Q of the unrolled source axis: its sources [ys, ye] and whether
+        // their slope-implied displacements reach this tile's outputs
+        auto reach = [&](int Q, int& ys, int& ye, int& dl, int& dr, int& q) {
+            const int k = Q >= 0 ? Q / subs : -((subs - 1 - Q) / subs);
+            q = Q - k * subs;
+            const double2 sb = xload<CHAIN>(b.sub_in + line * p.subs + q);
+            ys = k * n + q * kG;
+            ye = ys + min(kG, n - q * kG) - 1;
+            dl = max(__double2int_ru(__fma_rn(sb.x, ia, hl)), DLg);
+            dr = min(__double2int_rd(__fma_rn(sb.y, ia, hr)), DRg);
+            return dl <= dr && ys + dl <= jhi && ye + dr >= jlo;
+        };
         if (okl) {
             // candidate sub-tiles: unrolled sources y in [jlo - DRg, jhi - DLg]
             const int y0 = jlo - DRg, y1 = jhi - DLg;
             int k0 = 0;
             while (y0 - k0 * n < 0) --k0;
             while (y0 - k0 * n >= n) ++k0;
-            const int Q0 = k0 * subs + (y0 - k0 * n) / kG;
+            Q0 = k0 * subs + (y0 - k0 * n) / kG;
             int k1 = k0;
             while (y1 - k1 * n >= n) ++k1;
-            const int Q1 = k1 * subs + (y1 - k1 * n) / kG;
-            // sub-tile Q of the unrolled source axis: its sources [ys, ye] and whether
-            // their slope-implied displacements reach this tile's outputs
-            auto reach = [&](int Q, int& ys, int& ye, int& dl, int& dr) {
-                const int k = Q >= 0 ? Q / subs : -((subs - 1 - Q) / subs);
-                const int q = Q - k * subs;
-                const double2 sb = xload<CHAIN>(b.sub_in + line * p.subs + q);
-                ys = k * n + q * kG;
-                ye = ys + min(kG, n - q * kG) - 1;
-                dl = max(__double2int_ru(__fma_rn(sb.x, ia, hl)), DLg);
-                dr = min(__double2int_rd(__fma_rn(sb.y, ia, hr)), DRg);
-                return dl <= dr && ys + dl <= jhi && ye + dr >= jlo;
-            };
+            Q1 = k1 * subs + (y1 - k1 * n) / kG;
             for (int Q = Q0 + lane; Q <= Q1; Q += 32) {
-                int ys, ye, dl, dr;
-                if (reach(Q, ys, ye, dl, dr)) {
+                int ys, ye, dl, dr, q;
+                if (reach(Q, ys, ye, dl, dr, q)) {
                     ya = min(ya, ys);
                     yb = max(yb, ye);
                     dlo = min(dlo, max(dl, jlo - ye));
@@ -697,14 +875,18 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
             yb = __reduce_max_sync(0xffffffffu, yb);
             dlo = __reduce_min_sync(0xffffffffu, dlo);
             dhi = __reduce_max_sync(0xffffffffu, dhi);
+        }
+        // the walk when the gate holds, else the direct formula
+        const int mode = (okl && ya <= yb) ? kModeWalk : kModeDirect;
+        if (mode == kModeWalk) {
             // a wide tile (displacement range beyond the staged K buffer: a shock in a nearby
             // sub-tile) scans only the runs of reaching sub-tiles, not the gaps between them
             int nr = 1;
-            if (ya <= yb && dhi - dlo + 2 > LOB_WIDE_RANGE && Q1 - Q0 < 64) {
+            if (dhi - dlo + 2 > LOB_WIDE_RANGE && Q1 - Q0 < 64) {
                 unsigned long long hmask = 0;
                 for (int Qb = Q0; Qb <= Q1; Qb += 32) {
-                    int ys, ye, dl, dr;
-                    const bool hit = Qb + lane <= Q1 && reach(Qb + lane, ys, ye, dl, dr);
+                    int ys, ye, dl, dr, q;
+                    const bool hit = Qb + lane <= Q1 && reach(Qb + lane, ys, ye, dl, dr, q);
                     hmask |= static_cast<unsigned long long>(__ballot_sync(0xffffffffu, hit)) << (Qb - Q0);
                 }
                 if (lane == 0) {
@@ -714,9 +896,9 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
                         const int b0 = __ffsll(static_cast<long long>(m)) - 1;
                         const unsigned long long inv = ~(m >> b0);
                         const int len = inv ? __ffsll(static_cast<long long>(inv)) - 1 : 64 - b0;
-                        int ys, ye, ys2, ye2, dl, dr;
-                        reach(Q0 + b0, ys, ye, dl, dr);
-                        reach(Q0 + b0 + len - 1, ys2, ye2, dl, dr);
+                        int ys, ye, ys2, ye2, dl, dr, q;
+                        reach(Q0 + b0, ys, ye, dl, dr, q);
+                        reach(Q0 + b0 + len - 1, ys2, ye2, dl, dr, q);
                         if (nr < kRuns) {
                             S.rs[nr] = ys;
                             S.re[nr] = ye2;
@@ -731,52 +913,61 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
                 S.rs[0] = ya;
                 S.re[0] = yb;
             }
-            if (lane == 0) S.nruns = ya <= yb ? nr : 0;
+            if (lane == 0) S.nruns = nr;
         }
         if (lane == 0) {
-            S.ok = okl;
+            S.mode = mode;
+            S.gate = gate;
             S.DLg = DLg;
             S.DRg = DRg;
             S.ya = ya;
-            if (!okl) S.nruns = 0;
             S.yb = yb;
             S.dlo = dlo;
             S.dhi = dhi;
             S.nq = 0;
-            S.c_inline = S.c_queued = S.c_src = S.c_qent = 0;
-            mbar_init(&S.mbar, 1);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-            if (okl && big && ya <= yb) {
-                // first source chunk + the tile's v_d range, in flight across the barrier
-                const int vd0 = dlo - ((dlo + static_cast<int>(p.vofs)) & 1);
-                const int vcnt = (dhi - vd0 + 2) & ~1;
-                issue_chunk(S, ul, n, ya, min(kC, S.re[0] - ya + 1), vcnt <= kVCap ? p.vtab + p.vofs + vd0 : nullptr,
-                            vcnt);
+            S.abort = 0;
+            S.qwork = 0;
+            // queued candidates beyond this cost more than the direct formula over the window
+            const double bud = LOB_HEAVY * static_cast<double>(jspan + 1) * static_cast<double>(2 * n + 1);
+            S.budget = bud > 4.0e9 ? 4000000000u : static_cast<unsigned>(bud);
+            S.c_src = S.c_queued = S.c_qent = 0;
+            if (mode == kModeWalk) {
+                mbar_init(&S.mbar, 1);
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+                if (big) {
+                    // first source chunk + the tile's v_d range, in flight across the barrier
+                    const int vd0 = dlo - ((dlo + static_cast<int>(p.vofs)) & 1);
+                    const int vcnt = (dhi - vd0 + 2) & ~1;
+                    issue_chunk(S, ul, n, ya, min(kC, S.re[0] - ya + 1),
+                                vcnt <= kVCap ? p.vtab + p.vofs + vd0 : nullptr, vcnt);
+                }
             }
         }
     }
-    __syncthreads();  // keys, LUT, gate, ranges, mbarrier initialised
-    const bool ok = S.ok;
+    __syncthreads();  // gate, mode, ranges, mbarrier initialised
+    const int mode = S.mode;
 
-    if (ok) {
-        const int ya = S.ya, yb = S.yb;
+    bool walk = mode == kModeWalk;
+    if (walk) {
+        const int ya = S.ya;
         const int dlo_t = S.dlo, dhi_t = S.dhi;
         // K(d) = tau*((0.5 v)v - P v): staged in shared memory (TMA'd v_d, converted
         // in place) when the tile's displacement range fits, else from the global v_d table
         const int vd0 = dlo_t - ((dlo_t + static_cast<int>(p.vofs)) & 1);
         const int vcnt = (dhi_t - vd0 + 2) & ~1;
-        const bool kstage = big && dhi_t >= dlo_t && vcnt <= kVCap;
+        const bool kstage = big && vcnt <= kVCap;
         const double* gvt = p.vtab + p.vofs;
         const double* skt = S.vbuf - vd0;
         const double kdrift = lc.drift;
+        const unsigned budget = S.budget;
         if (tid == 0 && diag) {
-            atomicAdd(diag + 6, kstage ? 0ull : 1ull);
-            atomicAdd(diag + 7, static_cast<unsigned long long>(vcnt));
+            atomicAdd(diag + 5, kstage ? 0ull : 1ull);
+            atomicAdd(diag + 6, static_cast<unsigned long long>(vcnt));
         }
         // ---- sources in chunks of kC ----
         unsigned mphase = 0;
         const int nruns = S.nruns;
-        for (int run = 0, yc = ya, yr = nruns ? S.re[0] : 0; run < nruns;) {
+        for (int run = 0, yc = ya, yr = S.re[0]; run < nruns;) {
             const int clen = min(kC, yr - yc + 1);
             const int base = yc - jlo;  // output index of source i at d: base + i + d
             int sh = 0;
@@ -798,32 +989,37 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
             const double* ub = S.ubuf + sh;
             if (tid == 0) S.c_src += static_cast<unsigned>(clen);
             const ChunkArgs ca{ub, clen, base, jspan, ia, hl, hr, dlo_t, dhi_t, skt, gvt, kdrift, tau};
-            if (kstage)
-                process_chunk<true>(S, ca);
-            else
-                process_chunk<false>(S, ca);
+            walk = kstage ? process_chunk<true>(S, ca, budget) : process_chunk<false>(S, ca, budget);
+            if (!walk) break;  // the walk would cost more than the window: the direct formula
             yc += clen;
             if (yc > yr && ++run < nruns) {
                 yc = S.rs[run];
                 yr = S.re[run];
             }
         }
+        if (!walk && tid == 0 && diag) atomicAdd(diag + 8, 1ull);
+    } else if (tid == 0 && diag) {
+        atomicAdd(diag + 7, 1ull);
     }
+#if LOB_TILE_DIRECT
+    if (!walk) tile_direct<CHAIN>(S, ul, n, j0, Tl, first, p, lc.drift);
+#endif
+    __syncthreads();
 
-    // ---- epilogue: exact min -> u^{n+1}; direct scan where nothing landed ----
-    // Thread t owns outputs j0 + 8t .. j0 + 8t + 7 (vals index 8t+1 ..);
-    // threads 0..2 also evaluate the halo outputs jlo, j0+Tl, j0+Tl+1.
+    // ---- epilogue: u^{n+1} = best - tv; the direct scan where nothing landed ----
+    // Thread t owns outputs j0 + t + kNT*m (vals index 1 + t + kNT*m);
+    // threads 0..2 also the halo outputs jlo, j0+Tl, j0+Tl+1.
     const double* tvl = tv ? tv + line * tv_stride : nullptr;
     double* vals = S.ubuf;  // reuse: vals[i] = u^{n+1}(jlo + i), i = 0 .. Tl+2
     // direct scan of the full window (proj/tests/unit_scheme.cpp:184-190) for outputs no
-    // interval reached (never, when the statistics gate holds); one copy of the loop
+    // interval reached (never, when the statistics describe u); one copy of the loop
     auto scan = [&](int j) -> double {
-        if (ok && diag) atomicAdd(diag, 1ull);
+        if (diag) atomicAdd(diag, 1ull);
         double best = INFINITY;
         int y = (j - first) % n;
         if (y < 0) y += n;
         for (int w = 0; w <= 2 * n; ++w) {
-            const double c2 = __dadd_rn(xload<CHAIN>(ul + y), kval(p.vtab, p.vofs, first + w, lc.drift, tau));
+            const double c2 = __dadd_rn(xload<CHAIN>(ul + y), kdirect(p, first + w, lc.drift));
             best = c2 < best ? c2 : best;
             y = y == 0 ? n - 1 : y - 1;
         }
@@ -831,8 +1027,6 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
     };
     auto epilogue = [&](auto full_tile) {
         constexpr bool FULL = decltype(full_tile)::value;  // a whole tile: no bounds checks
-        // outputs j0 + t + kNT*m (vals index 1 + t + kNT*m): coalesced, conflict-free;
-        // the halo outputs jlo, j0+Tl, j0+Tl+1 (vals 0, Tl+1, Tl+2) go to threads 0..2 as m = kPer
         double tvv[kPer + 1];
 #pragma unroll
         for (int m = 0; m < kPer; ++m) {
@@ -904,11 +1098,12 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
         }
     }
     if (tid == 0 && diag) {
-        atomicAdd(diag + 1, static_cast<unsigned long long>(S.c_src));
-        atomicAdd(diag + 2, static_cast<unsigned long long>(S.c_inline));
-        atomicAdd(diag + 3, static_cast<unsigned long long>(S.c_queued));
-        atomicAdd(diag + 4, static_cast<unsigned long long>(S.c_qent));
-        atomicAdd(diag + 5, 1ull);
+        if (mode == kModeWalk) {
+            atomicAdd(diag + 1, static_cast<unsigned long long>(S.c_src));
+            atomicAdd(diag + 2, static_cast<unsigned long long>(S.c_queued));
+            atomicAdd(diag + 3, static_cast<unsigned long long>(S.c_qent));
+        }
+        atomicAdd(diag + 4, 1ull);
     }
     if (Tl == kT && j0 + kT <= n - 1)
         tile_stats<true>(vals, Tl, j0, line, tile, p, b, S.epi(), g_fsm_lut2);
@@ -955,7 +1150,7 @@ constexpr int kRT = 512;  // max threads per resident CTA
 constexpr int kResidentMaxN = 4096;  // shared memory: two line buffers, the keys, the K table (40 n bytes)
 
 struct ResidentShared {
-    double red[2][kRT / 32];
+    double red[4][kRT / 32];
     unsigned long long fsm[kRT / 32];
     int flag;
 };
@@ -982,7 +1177,7 @@ __global__ void __launch_bounds__(kRT) resident_kernel(double* __restrict__ u, i
     const double* tvl0 = tv ? tv + line * tv_stride : nullptr;
     double* ul = u + line * n;
     for (int j = tid; j < n; j += nt) U0[j] = ul[j];
-    for (int w = tid; w <= 2 * n; w += nt) Ks[w] = kval(p.vtab, p.vofs, first + w, lc.drift, tau);
+    for (int w = tid; w <= 2 * n; w += nt) Ks[w] = kdirect(p, first + w, lc.drift);
     const double* Kd = Ks - first;  // Kd[d] = K(d)
     // thread t's contiguous segment of sources / increments
     const int seg = (n + nt - 1) / nt, sa = min(n, tid * seg), sb = min(n, sa + seg);
@@ -995,7 +1190,7 @@ __global__ void __launch_bounds__(kRT) resident_kernel(double* __restrict__ u, i
         const double* tvl = tvl0 && tv_period > 1 ? tvl0 + (k % tv_period) * tv_step_stride : tvl0;
         __syncthreads();
         // slope extremes (gate) and the FSM summary of this thread's increments
-        double smn = INFINITY, smx = -INFINITY;
+        double smn = INFINITY, smx = -INFINITY, umn = INFINITY, umx = -INFINITY;
         int v = 0 | (1 << 2) | (2 << 4);
         int cnt[3] = {0, 0, 0};
         double sprev = 0.0;
@@ -1003,6 +1198,8 @@ __global__ void __launch_bounds__(kRT) resident_kernel(double* __restrict__ u, i
             const double s = __dsub_rn(cur[y + 1 == n ? 0 : y + 1], cur[y]);
             smn = fmin(smn, s);
             smx = fmax(smx, s);
+            umn = fmin(umn, cur[y]);
+            umx = fmax(umx, cur[y]);
             if (step_blocks) {
                 if (y == sa) sprev = y > 0 ? __dsub_rn(cur[y], cur[y - 1]) : 0.0;
                 if (y >= 1) {  // increment e = y: s(y) - s(y-1), e in [1, n-1]
@@ -1029,6 +1226,8 @@ __global__ void __launch_bounds__(kRT) resident_kernel(double* __restrict__ u, i
         for (int o = 16; o; o >>= 1) {
             smn = fmin(smn, __shfl_xor_sync(0xffffffffu, smn, o));
             smx = fmax(smx, __shfl_xor_sync(0xffffffffu, smx, o));
+            umn = fmin(umn, __shfl_xor_sync(0xffffffffu, umn, o));
+            umx = fmax(umx, __shfl_xor_sync(0xffffffffu, umx, o));
         }
         if (step_blocks) {
             const unsigned long long f = warp_fsm(fsm_pack(v, cnt));
@@ -1037,20 +1236,26 @@ __global__ void __launch_bounds__(kRT) resident_kernel(double* __restrict__ u, i
         if (lane == 0) {
             R.red[0][warp] = smn;
             R.red[1][warp] = smx;
+            R.red[2][warp] = umn;
+            R.red[3][warp] = umx;
         }
         for (int j = tid; j < n; j += nt) keys[j] = kInfBits;
         __syncthreads();
         if (warp == 0) {
             double a0 = lane < nw ? R.red[0][lane] : INFINITY, a1 = lane < nw ? R.red[1][lane] : -INFINITY;
+            double b0 = lane < nw ? R.red[2][lane] : INFINITY, b1 = lane < nw ? R.red[3][lane] : -INFINITY;
 #pragma unroll
             for (int o = 16; o; o >>= 1) {
                 a0 = fmin(a0, __shfl_xor_sync(0xffffffffu, a0, o));
                 a1 = fmax(a1, __shfl_xor_sync(0xffffffffu, a1, o));
+                b0 = fmin(b0, __shfl_xor_sync(0xffffffffu, b0, o));
+                b1 = fmax(b1, __shfl_xor_sync(0xffffffffu, b1, o));
             }
             if (lane == 0) {
-                const double osc_bound = 0.5 * static_cast<double>(n) * fmax(fabs(a0), fabs(a1));
-                R.flag = (osc_bound * (1.0 + 1e-12) < lc.gap * (1.0 - 1e-12)) && n >= 3 && isfinite(a0) &&
-                         isfinite(a1);
+                // the exact oscillation max u - min u against the window's edge gap (fast_kernel)
+                const double osc = __dsub_rn(b1, b0);
+                R.flag = isfinite(osc) && isfinite(a0) && isfinite(a1) && n >= 3 &&
+                         osc * (1.0 + 1e-12) < lc.gap * (1.0 - 1e-12);
             }
             if (step_blocks) {  // the warps' summaries composed in order (lanes >= warps: identity)
                 const unsigned long long f = warp_fsm(lane < nw ? R.fsm[lane] : fsm_identity());
@@ -1125,7 +1330,8 @@ __global__ void __launch_bounds__(kRT) resident_kernel(double* __restrict__ u, i
 
 // ---------------------------------------------------------------------------
 // workspace: sub[2][lines][subs] double2 | fsm[2][lines][tiles] u64 |
-//            line[3][lines][4] u64 | LineConst[lines] | diag u64
+//            line[3][lines][4] u64 | LineConst[lines] | diag u64[16] | done u32[lines]
+constexpr int kDiag = 16;
 struct WsLayout {
     size_t sub, fsm, line, lc, diag, done, total;
 };
@@ -1137,7 +1343,7 @@ static WsLayout ws_layout(int64_t lines, int64_t n) {
     w.line = w.fsm + 2 * static_cast<size_t>(lines * tiles) * sizeof(unsigned long long);
     w.lc = w.line + 3 * static_cast<size_t>(lines) * 4 * sizeof(unsigned long long);
     w.diag = w.lc + static_cast<size_t>(lines) * sizeof(LineConst);
-    w.done = w.diag + 64;  // [lines] tiles finished since the statistics were (re)computed
+    w.done = w.diag + kDiag * sizeof(unsigned long long);  // [lines] warps finished since the counters reset
     w.total = w.done + (static_cast<size_t>(lines) * sizeof(unsigned) + 255) / 256 * 256;
     return w;
 }
@@ -1264,7 +1470,7 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     if (!(flags & LOB_FAST_STATS_VALID)) {
         // per-line constants (valid while drift/tau/n and the workspace are unchanged)
         line_setup_kernel<<<static_cast<unsigned>((lines + 127) / 128), 128, 0, s>>>(drift, lines, p, lcs);
-        LOB_CUDA_TRY(ctx, cudaMemsetAsync(diag, 0, 8 * sizeof(unsigned long long), s));
+        LOB_CUDA_TRY(ctx, cudaMemsetAsync(diag, 0, kDiag * sizeof(unsigned long long), s));
         LOB_CUDA_TRY(ctx, cudaMemsetAsync(static_cast<char*>(workspace) + w.done, 0, lines * sizeof(unsigned), s));
         ctx->ws_chain[workspace] = 0;
         ctx->launches += 1;
@@ -1298,9 +1504,14 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
          {fast_kernel<true, true, false>, fast_kernel<true, true, true>}}};
     auto kern = kerns[tma][chained][release];
     const unsigned need = static_cast<unsigned>(chain * p.tiles * (kNT / 32));
-    if (first_time(ctx, reinterpret_cast<const void*>(kern)))
+    if (first_time(ctx, reinterpret_cast<const void*>(kern))) {
         LOB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(sizeof(MainShared))));
+        // the whole unified L1 as shared memory: LOB_FAST_MINB CTAs per SM (the driver's default
+        // carveout for this size leaves one CTA less)
+        LOB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                               cudaSharedmemCarveoutMaxShared));
+    }
     p.fsm_on = blocks ? 1 : 0;  // the stats kernel above always produced them
     ctx->ws_fsm_valid[workspace] = blocks != nullptr;
     dim3 grid(static_cast<unsigned>(p.tiles), static_cast<unsigned>(lines));
@@ -1372,7 +1583,7 @@ int fast_diag_count(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n, uin
     // the counters are written by K2 launches on the caller's streams: wait for all of them
     LOB_CUDA_TRY(ctx, cudaDeviceSynchronize());
     LOB_CUDA_TRY(ctx, cudaMemcpyAsync(count, static_cast<char*>(workspace) + w.diag,
-                                      8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+                                      kDiag * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
     return LOB_OK;
 }

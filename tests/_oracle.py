@@ -148,6 +148,18 @@ class Reference:
     def err(self):
         return self.lib.ref_last_error().decode()
 
+    # the synthetic-workload generators compiled into the reference shim (oracle/Makefile), so
+    # a reference-only process (bench.py --impl reference) maps no product library
+    def gen_c2_drifts(self, lines=256):
+        out = np.empty(lines, np.float64)
+        self.lib.lob_gen_c2_drifts(ctypes.c_int64(lines), out.ctypes.data_as(ctypes.c_void_p))
+        return out
+
+    def gen_potential(self, kind, n):
+        out = np.empty(n, np.float64)
+        self.lib.lob_gen_potential(ctypes.c_int(kind), ctypes.c_int64(n), out.ctypes.data_as(ctypes.c_void_p))
+        return out
+
     def kernel(self, n, tau, drift):
         w = np.empty(2 * n + 1)
         c, a = c_int64(), c_int64()

@@ -9,16 +9,14 @@ import pytest
 from paper_1210_4090_b200 import _capi
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HEADERS = [os.path.join(ROOT, "include", h) for h in ("laxol_b200.h", "laxol_b200_configs.h")]
+HEADER = os.path.join(ROOT, "include", "laxol_b200.h")
+CONFIGS_HEADER = os.path.join(ROOT, "include", "laxol_b200_configs.h")
 
 
-def declared_symbols():
-    names = set()
-    for h in HEADERS:
-        text = open(h).read()
-        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-        names.update(re.findall(r"\b(lob_[a-z0-9_]+)\s*\(", text))
-    return names
+def declared_symbols(h=HEADER):
+    text = open(h).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return set(re.findall(r"\b(lob_[a-z0-9_]+)\s*\(", text))
 
 
 def test_library_exports_every_declared_symbol():
@@ -26,6 +24,15 @@ def test_library_exports_every_declared_symbol():
     missing = [s for s in sorted(declared_symbols()) if not hasattr(lib, s)]
     assert not missing, missing
     assert declared_symbols() <= set(_capi.SIGNATURES), "binding table out of date"
+    # the product library carries no workload generator (bench's reference arm must not map it)
+    assert not any(hasattr(lib, s) for s in declared_symbols(CONFIGS_HEADER))
+
+
+def test_generator_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(_capi.CONFIGS_PATH)
+    missing = [s for s in sorted(declared_symbols(CONFIGS_HEADER)) if not hasattr(lib, s)]
+    assert not missing, missing
+    assert declared_symbols(CONFIGS_HEADER) <= set(_capi.CONFIG_SIGNATURES)
 
 
 def test_version_and_no_cpu_fallback():

@@ -33,13 +33,12 @@ def fast_step(dev, u, drifts, tau, tv=None, blocks=False, ws=None, flags=0):
 
 
 def oracle_step(orc, u, drifts, tau, tv=None):
+    """The oracle's direct formula, every line with its own window (one call: lines in parallel)."""
     lines, n = u.shape
-    outs = []
-    for l in range(lines):
-        d = float(np.broadcast_to(drifts, (lines,))[l])
-        K, first, _, _ = orc.kernel(n, tau, d)
-        outs.append(orc.direct(u[l:l + 1], K, first, tv=tv)[0])
-    return np.stack(outs)
+    ks = [orc.kernel(n, tau, float(d)) for d in np.broadcast_to(drifts, (lines,))]
+    K = np.ascontiguousarray(np.stack([k[0] for k in ks]))
+    first = np.array([k[1] for k in ks], np.int64)
+    return orc.direct(u, K, first, tv=tv, ktab_stride=2 * n + 1)
 
 
 def assert_close(got, want):
@@ -49,24 +48,91 @@ def assert_close(got, want):
     return err
 
 
+def fast_step_counted(dev, u, drifts, tau, tv=None, blocks=False):
+    """fast_step plus the engine's counters for that one call (fresh workspace)."""
+    import torch
+    lines, n = u.shape
+    ws = torch.empty(dev.fast_workspace_bytes(lines, n), dtype=torch.uint8, device="cuda")
+    out, b = fast_step(dev, u, drifts, tau, tv=tv, blocks=blocks, ws=ws)
+    return out, b, dev.fast_counters(ws, lines, n)
+
+
+def assert_walk(c):
+    """Every tile ran the local-minimum walk: no direct-formula tile, no missed output."""
+    assert c["missed_outputs"] == 0, c
+    assert c["direct_tiles_gate"] == 0 and c["direct_tiles_heavy"] == 0, c
+    assert c["sources"] > 0 and c["tiles"] > 0, c
+
+
+def rough_walk(rng, lines, n, scale):
+    """Periodic random walks with increments uniform in [-scale/n, scale/n] (the C3
+    generator's shape, scaled): rough lines whose slopes keep the walk's intervals short."""
+    u = np.cumsum(rng.uniform(-scale / n, scale / n, (lines, n)), axis=1)
+    return u - np.arange(n)[None, :] / n * u[:, -1:]
+
+
 @pytest.mark.parametrize("drift", [0.0, 0.4, -0.7, 1.0])
 @pytest.mark.parametrize("n,tau", [(24, 0.25), (48, 0.125), (600, 0.04), (1024, 0.05), (4096, 0.01)])
 def test_fast_random_vs_oracle(dev, orc, n, tau, drift):
+    """Random walks scaled so the walk runs them (asserted): bit-exact, block counts too."""
     rng = np.random.default_rng(n + int(drift * 10))
-    u = rng.uniform(-1, 1, (4, n))
-    got, blocks = fast_step(dev, u, drift, tau, blocks=True)
+    u = rough_walk(rng, 4, n, 4.0)
+    got, blocks, c = fast_step_counted(dev, u, drift, tau, blocks=True)
     want = oracle_step(orc, u, drift, tau)
     assert np.array_equal(got.cpu().numpy(), want)
     assert [orc.line_blocks(u[l]) for l in range(4)] == list(blocks)
+    assert_walk(c)
+
+
+@pytest.mark.parametrize("drift", [0.0, -0.7])
+@pytest.mark.parametrize("n,tau", [(600, 0.04), (1024, 0.05), (4096, 0.01)])
+def test_fast_uniform_noise_takes_direct_route(dev, orc, n, tau, drift):
+    """uniform(-1, 1) samples: every source's interval spans most of the window, so the
+    walk would cost more than the direct formula; its work budget sends the tiles to the
+    in-kernel direct sweep (counted), still bit-exact."""
+    rng = np.random.default_rng(n + int(drift * 10) + 7)
+    u = rng.uniform(-1, 1, (4, n))
+    got, blocks, c = fast_step_counted(dev, u, drift, tau, blocks=True)
+    assert np.array_equal(got.cpu().numpy(), oracle_step(orc, u, drift, tau))
+    assert [orc.line_blocks(u[l]) for l in range(4)] == list(blocks)
+    assert c["direct_tiles_heavy"] + c["direct_tiles_gate"] == c["tiles"], c
+    assert c["missed_outputs"] == 0, c
+
+
+def test_fast_gate_failure_takes_direct_route(dev, orc):
+    """Oscillation above the window's edge gap (max u - min u >= min(K(first), K(last)) -
+    min K): window-edge minima are possible, the walk does not apply; the tiles take the
+    direct formula (counted), bit-exact."""
+    n, tau = 1024, 0.05
+    K, first, _, _ = orc.kernel(n, tau, 0.3)
+    gap = min(K[0], K[-1]) - K.min()
+    x = np.arange(n) / n
+    u = np.stack([gap * 1.5 * np.sin(2 * np.pi * x), gap * 0.6 * np.sign(np.sin(6 * np.pi * x))])
+    got, _, c = fast_step_counted(dev, u, 0.3, tau)
+    assert np.array_equal(got.cpu().numpy(), oracle_step(orc, u, 0.3, tau))
+    assert c["direct_tiles_gate"] == c["tiles"], c
+
+
+@pytest.mark.parametrize("drift", [130.0, -150.0, 2.5e3])
+def test_fast_large_drift_window_outside_vtab(dev, orc, drift):
+    """|tau P| > 2: the window [center - n, center + n] leaves the cached v_d table
+    (d in [-3n, 3n]); the tiles compute K with build_kernel's own roundings on the direct
+    route instead of reading past the table (counted), bit-exact."""
+    n, tau = 512, 0.02
+    u = np.sin(2 * np.pi * np.arange(n) / n)[None, :].repeat(2, 0) * np.array([[1.0], [0.25]])
+    got, _, c = fast_step_counted(dev, u, drift, tau)
+    assert np.array_equal(got.cpu().numpy(), oracle_step(orc, u, drift, tau))
+    assert c["direct_tiles_gate"] == c["tiles"], c
 
 
 def test_fast_c3_lines_bit_exact(dev, orc):
     n = 4096
     u = api.gen_c3_lines(0, 32, n)
-    got, blocks = fast_step(dev, u, 0.0, 0.01, blocks=True)
+    got, blocks, c = fast_step_counted(dev, u, 0.0, 0.01, blocks=True)
     want = oracle_step(orc, u, 0.0, 0.01)
     assert np.array_equal(got.cpu().numpy(), want)
     assert list(blocks) == [orc.line_blocks(u[l]) for l in range(32)]
+    assert_walk(c)
 
 
 def test_fast_c1_full_evolve_matches_reference(dev, orc, ref):
@@ -116,7 +182,7 @@ def test_fast_c2_slice_vs_oracle(dev, orc):
     torch.cuda.synchronize()
     want = oracle_step(orc, prev.cpu().numpy(), drifts, tau, tv=tv)
     assert np.array_equal(u.cpu().numpy(), want)
-    assert dev.fast_diagnostics(ws, 8, n) == 0  # every output found by the local-minimum walk
+    assert_walk(dev.fast_counters(ws, 8, n))  # every tile, every step: the local-minimum walk
 
 
 def test_fast_equals_direct_c5_shape(dev, orc):
@@ -195,7 +261,7 @@ def test_fast_equals_direct_c2_full_size(dev):
     w = _k1_step(dev, u, drifts, tau, dtv)
     torch.cuda.synchronize()
     assert torch.equal(v, w)
-    assert dev.fast_diagnostics(ws2, lines, n) == 0
+    assert_walk(dev.fast_counters(ws2, lines, n))
 
 
 def test_fast_equals_direct_c5_full_line(dev):
@@ -214,7 +280,7 @@ def test_fast_equals_direct_c5_full_line(dev):
     w = _k1_step(dev, u, [0.25, 0.25], tau, dtv)
     torch.cuda.synchronize()
     assert torch.equal(v, w)
-    assert dev.fast_diagnostics(ws2, 2, n) == 0
+    assert_walk(dev.fast_counters(ws2, 2, n))
 
 
 @pytest.mark.parametrize("n,offset", [(4097, 0), (6001, 0), (8192, 1), (5000, 1), (2050, 0)])
@@ -235,7 +301,7 @@ def test_fast_odd_lengths_and_unaligned_rows(dev, orc, n, offset):
     dev.fast_f64(du, out, to_dev(drifts), tau, workspace=ws)
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), oracle_step(orc, u, drifts, tau))
-    assert dev.fast_diagnostics(ws, lines, n) == 0
+    assert_walk(dev.fast_counters(ws, lines, n))
 
 
 @pytest.mark.parametrize("eta", [1e-7, 1e-4, 0.05])
@@ -286,7 +352,7 @@ def test_fast_chained_steps_equal_plain_steps(dev):
                          flags=pattern[i] | (api.FAST_STATS_VALID if i else 0))
             a, b = b, a
         torch.cuda.synchronize()
-        assert dev.fast_diagnostics(ws, lines, n) == 0
+        assert_walk(dev.fast_counters(ws, lines, n))
         res.append((a.clone(), bl.clone()))
     for k in (1, 2):
         assert torch.equal(res[0][0], res[k][0])
