@@ -121,6 +121,24 @@ int lob_minplus_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lin
                          double eta, int64_t* blocks, void* workspace, size_t workspace_bytes,
                          int flags, void* stream);
 
+/* K2 for ANY convex kernel window: the same exact O(n) walk, with each source's
+ * local-minimum interval found by a hinted search over the window's
+ * nondecreasing slopes sigma(w) = ktab[w+1] - ktab[w] (rounding of both sides
+ * of every slope comparison relaxed, so the candidate set still encloses every
+ * minimiser) and K read from the table itself.  This is the engine that plugs
+ * into kinetic_convolve(u, kernel, eta, engine, blocks)
+ * (proj/include/laxol/scheme.hpp:52-53; dispatch proj/src/scheme.cpp:114-121):
+ * the reference's Kernel carries exactly the window (mechanical or tabulated,
+ * proj/src/scheme.cpp:59-105).  Table conventions as lob_minplus_direct_f64
+ * (ktab_stride 0 = one window for all lines; first: device int64[lines]);
+ * tau > 0 only scales the work budget; flags/workspace/blocks as
+ * lob_minplus_fast_f64 (the workspace remembers the table: another table
+ * recomputes the statistics). */
+int lob_minplus_fast_window_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
+                                const double* ktab, int64_t ktab_stride, const int64_t* first, double tau,
+                                const double* tv, int64_t tv_stride, double eta, int64_t* blocks, void* workspace,
+                                size_t workspace_bytes, int flags, void* stream);
+
 /* Fast-engine counters, cumulative since the last call without
  * LOB_FAST_STATS_VALID on this workspace (counters[16]; unused entries 0):
  *  [0] outputs no local-minimum interval reached, recomputed by the exact
@@ -136,7 +154,11 @@ int lob_minplus_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lin
  *      candidate count exceeded a quarter of the window's,
  *  [9] chained-step waits that timed out (a misused LOB_FAST_CHAINED; the
  *      results of that call are not trustworthy),
- *  [10] warps whose fold queue overflowed (re-walked, exact). */
+ *  [10] unused,
+ *  [11] tiles whose carried line constants (LOB_FAST_STATS_VALID) no longer
+ *       matched the caller's drift / window (another table at a reused address,
+ *       a drift changed in place): computed by the direct formula with the
+ *       current inputs (exact). */
 int lob_fast_diagnostics(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n,
                          uint64_t* counters);
 

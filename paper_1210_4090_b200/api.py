@@ -199,9 +199,21 @@ class Device:
                                            _ptr(workspace), ws_bytes, int(flags), _stream_ptr(stream))
         self._check(st, "lob_minplus_fast_f64")
 
+    def fast_window_f64(self, u, out, ktab, first, tau, tv=None, tv_stride=0, eta=0.0, blocks=None,
+                        workspace=None, flags=0, ktab_stride=0, stream=None):
+        """K2 over any convex kernel window (lob_minplus_fast_window_f64): the engine for
+        kinetic_convolve's Kernel (mechanical or tabulated)."""
+        lines, n = u.shape
+        ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+        st = self.lib.lob_minplus_fast_window_f64(self.ctx, _ptr(u), _ptr(out), lines, n, _ptr(ktab), ktab_stride,
+                                                  _ptr(first), float(tau), _ptr(tv), tv_stride, float(eta),
+                                                  _ptr(blocks), _ptr(workspace), ws_bytes, int(flags),
+                                                  _stream_ptr(stream))
+        self._check(st, "lob_minplus_fast_window_f64")
+
     FAST_COUNTER_KEYS = ["missed_outputs", "sources", "fold_ranges", "plain_runs", "tiles", "tiles_k_unstaged",
                          "k_range_sum", "direct_tiles_gate", "direct_tiles_heavy", "chain_timeouts",
-                         "fold_overflow_warps"]
+                         "unused10", "stale_line_constants"]
 
     def fast_counters(self, workspace, lines: int, n: int) -> dict:
         """The fast engine's work counters (include/laxol_b200.h, lob_fast_diagnostics)."""

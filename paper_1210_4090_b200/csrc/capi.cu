@@ -188,6 +188,24 @@ int lob_minplus_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lin
                            workspace_bytes, flags, static_cast<cudaStream_t>(stream));
 }
 
+int lob_minplus_fast_window_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
+                                const double* ktab, int64_t ktab_stride, const int64_t* first, double tau,
+                                const double* tv, int64_t tv_stride, double eta, int64_t* blocks, void* workspace,
+                                size_t workspace_bytes, int flags, void* stream) {
+    int st = check_lines(ctx, lines, n, "lob_minplus_fast_window_f64");
+    if (st) return st;
+    if (lines == 0) return LOB_OK;
+    if (!u || !out || !ktab || !first)
+        return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_fast_window_f64: null buffer");
+    if (u == out) return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_fast_window_f64: out must not alias u");
+    if (!(tau > 0.0)) return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_fast_window_f64: tau must be positive");
+    if (ktab_stride != 0 && ktab_stride < 2 * n + 1)
+        return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_fast_window_f64: ktab_stride < 2n+1");
+    const FastTable tab{ktab, ktab_stride, first};
+    return launch_fast_f64(ctx, u, out, lines, n, nullptr, tau, tv, tv_stride, eta, blocks, workspace,
+                           workspace_bytes, flags, static_cast<cudaStream_t>(stream), nullptr, &tab);
+}
+
 int lob_fast_diagnostics(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n,
                          uint64_t* counters) {
     if (!ctx || !workspace || !counters) return LOB_INVALID_INPUT;

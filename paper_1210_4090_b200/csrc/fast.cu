@@ -95,6 +95,12 @@ struct LineConst {
     double hl, hr;    // dL = ceil(s/a + hl), dR = floor(s/a + hr): hl/hr = P eps/a -/+ (1/2 + delta)
     double gap;       // min(K(first), K(first+2n)) - min K: the oscillation gate
     double drift;
+    // window-table mode (any convex window, lob_minplus_fast_window_f64):
+    const double* kt;  // K(d) = kt[d] for d in [first, first + 2n] (the line's table, offset by -first)
+    double tol;        // slope comparisons are relaxed by tol * (|s| + max |sigma|) (rounding of both sides)
+    double smax;       // max |sigma(d)| over the window, sigma(d) = K(d+1) - K(d)
+    double sg0, sgi;   // search hint: d ~ first + (s - sigma(first)) * sgi (slopes linear in d)
+    double k0, kmid, kend;  // window samples at w = 0, n, 2n (staleness check of carried constants)
 };
 static_assert(kSub == kNT / 32, "one warp per sub-tile in the epilogue");
 static_assert(kPer % 2 == 0, "FSM pairs");
@@ -109,6 +115,11 @@ struct FastParams {
     const double* vtab;  // v_d for d in [-vofs, vofs]
     int64_t vofs;
     int fsm_on;  // the epilogue produces decompose()'s FSM summaries for the next step's block count
+    // the caller's current per-line inputs (checked against the carried line constants)
+    const double* drift_arr;                      // mechanical mode
+    const double* ktab;                           // table mode: windows ...
+    int64_t kstride;                              // ... their stride (0: shared) ...
+    const int64_t* kfirst;                        // ... and first displacements
 };
 
 struct FastBuffers {
@@ -515,14 +526,79 @@ struct ChunkArgs {
     double ia, hl, hr;
     int dlo, dhi;       // the tile's displacement range (clamp)
     const double* skt;  // K(d) staged in shared memory (KS) ...
-    const double* gvt;  // ... or v_d in global memory
+    const double* gvt;  // ... or v_d (mechanical) / K(d) (window table) in global memory
     double drift, tau;
+    const LineConst* lc;  // window-table mode: the slope search's constants
 };
 
-template <bool KS>
+template <bool TAB, bool KS>
 __device__ __forceinline__ double kvalue(const ChunkArgs& a, int d) {
     if constexpr (KS) return a.skt[d];
+    else if constexpr (TAB) return __ldg(a.gvt + d);
     else return kval_v(__ldg(a.gvt + d), a.drift, a.tau);
+}
+
+// ---- window-table mode: local-minimum intervals by slope search --------------
+// For any convex window the local-minimum conditions of the fast.cu header read
+// S(y-1) <= Sigma(d) and Sigma(d-1) <= S(y) in exact arithmetic, Sigma(d) = K(d+1) - K(d)
+// (nondecreasing: build_kernel's convexity check, proj/src/scheme.cpp:94-97).  With the
+// rounded differences s, sigma (each within u |.| of the real value) they imply
+// sigma(d) >= s(y-1) - t and sigma(d-1) <= s(y) + t, t = tol (|s| + max|sigma|), so
+//   dL = min { d : sigma(d) >= s(y-1) - t },   dR = min { d : sigma(d) > s(y) + t }
+// enclose every minimiser.  Each is a lower bound over the nondecreasing sigma, found
+// by a galloping search from the linear-slope hint and a binary search in the bracket.
+// smallest d in [lo, hi + 1] with sig(d) >= x (STRICT: > x); sig nondecreasing
+template <bool STRICT, class SIG>
+__device__ __forceinline__ int slope_search(SIG sig, double x, int lo, int hi, int hint) {
+    auto ok = [&](int d) { return STRICT ? sig(d) > x : sig(d) >= x; };
+    int d = min(max(hint, lo), hi + 1);
+    int a, b;  // the answer lies in [a, b]
+    if (d <= hi && !ok(d)) {
+        a = d + 1;
+        b = hi + 1;
+        for (int step = 1;; step <<= 1) {
+            const int e = d + step;
+            if (e > hi) break;
+            if (ok(e)) {
+                b = e;
+                break;
+            }
+            a = e + 1;
+            d = e;
+        }
+    } else {
+        a = lo;
+        b = d;
+        for (int step = 1;; step <<= 1) {
+            const int e = d - step;
+            if (e < lo) break;
+            if (!ok(e)) {
+                a = e + 1;
+                break;
+            }
+            b = e;
+            d = e;
+        }
+    }
+    while (a < b) {
+        const int m = (a + b) >> 1;
+        if (ok(m)) b = m;
+        else a = m + 1;
+    }
+    return a;
+}
+__device__ __forceinline__ int slope_hint(const LineConst& lc, double s) {
+    const double g = static_cast<double>(lc.first) + (s - lc.sg0) * lc.sgi;
+    return g > 1.0e9 ? 1000000000 : (g < -1.0e9 ? -1000000000 : __double2int_rd(g));
+}
+// [dL, dR] of slopes (sl, sr) with sigma from `sig`, searched inside [lo, hi] (the
+// answers are clamped to [lo, hi + 1] / [lo - 1, hi] by construction)
+template <class SIG>
+__device__ __forceinline__ void tab_interval(SIG sig, const LineConst& lc, double sl, double sr, int lo, int hi,
+                                             int& dl, int& dr) {
+    const double tl = lc.tol * (fabs(sl) + lc.smax), tr = lc.tol * (fabs(sr) + lc.smax);
+    dl = slope_search<false>(sig, sl - tl, lo, hi, slope_hint(lc, sl));
+    dr = slope_search<true>(sig, sr + tr, lo - 1, hi - 1, slope_hint(lc, sr) + 1);
 }
 
 // Candidates of one staged source chunk.  Warp w takes sources w*per + lane +
@@ -533,7 +609,7 @@ __device__ __forceinline__ double kvalue(const ChunkArgs& a, int d) {
 // barrier with exact CAS-min loops, one warp per queued source.  Returns false
 // when the queued work exceeds `budget` (the walk would cost more than the
 // window: the tile switches to the direct formula; the queue is not processed).
-template <bool KS>
+template <bool TAB, bool KS>
 __device__ __forceinline__ bool process_chunk(MainShared& S, const ChunkArgs& a, unsigned budget) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int per = ((a.clen + kNT - 1) / kNT) * 32;
@@ -541,22 +617,28 @@ __device__ __forceinline__ bool process_chunk(MainShared& S, const ChunkArgs& a,
 #pragma unroll kEmitUnroll
     for (int i = warp * per + lane; i < iend; i += 32) {
         const double ul0 = a.ub[i], u0 = a.ub[i + 1], ur0 = a.ub[i + 2];
-        // z(s) -/+ (1/2 + delta) with one fused rounding (delta bounds it, csrc/host/kernel_build.cpp)
-        const double zl = __fma_rn(__dsub_rn(u0, ul0), a.ia, a.hl);
-        const double zr = __fma_rn(__dsub_rn(ur0, u0), a.ia, a.hr);
+        int dl, dr;
+        if constexpr (TAB) {
+            auto sig = [&](int d) { return __dsub_rn(kvalue<TAB, KS>(a, d + 1), kvalue<TAB, KS>(a, d)); };
+            tab_interval(sig, *a.lc, __dsub_rn(u0, ul0), __dsub_rn(ur0, u0), a.dlo, a.dhi, dl, dr);
+        } else {
+            // z(s) -/+ (1/2 + delta) with one fused rounding (delta bounds it, csrc/host/kernel_build.cpp)
+            dl = __double2int_ru(__fma_rn(__dsub_rn(u0, ul0), a.ia, a.hl));
+            dr = __double2int_rd(__fma_rn(__dsub_rn(ur0, u0), a.ia, a.hr));
+        }
         const int off = a.base + i;  // output index of this source at d = 0
         // every candidate lies in [dlo, dhi] when the statistics describe u;
         // the clamp keeps stale statistics memory-safe (wrong, never out of bounds)
-        const int dl = max(max(__double2int_ru(zl), a.dlo), -off);
-        const int dr = min(min(__double2int_rd(zr), a.dhi), a.jspan - off);
+        dl = max(max(dl, a.dlo), -off);
+        dr = min(min(dr, a.dhi), a.jspan - off);
         if (dl <= dr) {
             unsigned long long* slot = &S.keys[off + dl];
-            const double c0 = __dadd_rn(u0, kvalue<KS>(a, dl));
+            const double c0 = __dadd_rn(u0, kvalue<TAB, KS>(a, dl));
             const unsigned long long o0 = atomicCAS(slot, kInfBits, static_cast<unsigned long long>(__double_as_longlong(c0)));
             const bool r0 = o0 != kInfBits && c0 < __longlong_as_double(static_cast<long long>(o0));
             bool r1 = false;
             if (dl < dr) {
-                const double c1 = __dadd_rn(u0, kvalue<KS>(a, dl + 1));
+                const double c1 = __dadd_rn(u0, kvalue<TAB, KS>(a, dl + 1));
                 const unsigned long long o1 =
                     atomicCAS(slot + 1, kInfBits, static_cast<unsigned long long>(__double_as_longlong(c1)));
                 r1 = o1 != kInfBits && c1 < __longlong_as_double(static_cast<long long>(o1));
@@ -571,7 +653,7 @@ __device__ __forceinline__ bool process_chunk(MainShared& S, const ChunkArgs& a,
                 if (q < kQCap) {
                     S.queue[q] = make_int3(i, qlo, qhi);
                 } else if (*reinterpret_cast<volatile unsigned*>(&S.qwork) <= S.budget) {
-                    for (int d = qlo; d <= qhi; ++d) smem_fmin(&S.keys[off + d], __dadd_rn(u0, kvalue<KS>(a, d)));
+                    for (int d = qlo; d <= qhi; ++d) smem_fmin(&S.keys[off + d], __dadd_rn(u0, kvalue<TAB, KS>(a, d)));
                 } else {
                     S.abort = 1;  // a heavy tile: the queued runs already exceed the budget
                 }
@@ -587,7 +669,7 @@ __device__ __forceinline__ bool process_chunk(MainShared& S, const ChunkArgs& a,
             const double uy = a.ub[qe.x + 1];
             const int off = a.base + qe.x;
             if (lane == 0) atomicAdd(&S.c_queued, static_cast<unsigned>(qe.z - qe.y + 1));
-            for (int d = qe.y + lane; d <= qe.z; d += 32) smem_fmin(&S.keys[off + d], __dadd_rn(uy, kvalue<KS>(a, d)));
+            for (int d = qe.y + lane; d <= qe.z; d += 32) smem_fmin(&S.keys[off + d], __dadd_rn(uy, kvalue<TAB, KS>(a, d)));
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -627,9 +709,8 @@ __device__ __forceinline__ double kdirect(const FastParams& p, int d, double dri
 // (csrc/direct_common.cuh): 8 outputs per thread, the window in chunks of kTW
 // displacements staged in shared memory, one LDS per displacement and one add + one
 // exact min per candidate; the three halo outputs are one warp each.
-template <bool CHAIN>
-__device__ void tile_direct(MainShared& S, const double* ul, int n, int j0, int Tl, int first,
-                            const FastParams& p, double drift) {
+template <bool CHAIN, class KF>
+__device__ void tile_direct(MainShared& S, const double* ul, int n, int j0, int Tl, int first, KF kf) {
     constexpr int R = kPer, L = kT + kTW;
     double* Us = reinterpret_cast<double*>(&S);
     double* Ks = Us + P8(L) + 1;
@@ -644,7 +725,7 @@ __device__ void tile_direct(MainShared& S, const double* ul, int n, int j0, int 
         for (int w = lane; w < W; w += 32) {
             int y = (y0 - w) % n;
             if (y < 0) y += n;
-            const double c = __dadd_rn(xload<CHAIN>(ul + y), kdirect(p, first + w, drift));
+            const double c = __dadd_rn(xload<CHAIN>(ul + y), kf(first + w));
             hb = c < hb ? c : hb;
         }
 #pragma unroll
@@ -666,7 +747,7 @@ __device__ void tile_direct(MainShared& S, const double* ul, int n, int j0, int 
             while (y >= n) y -= n;
             Us[P8(i)] = xload<CHAIN>(ul + y);
         }
-        for (int s = tid; s < kTW; s += kNT) Ks[s] = wc + s < W ? kdirect(p, first + wc + s, drift) : INFINITY;
+        for (int s = tid; s < kTW; s += kNT) Ks[s] = wc + s < W ? kf(first + wc + s) : INFINITY;
         __syncthreads();
         const double* pa = Us + P8(tid * R + kTW);
         double A[R];
@@ -740,6 +821,42 @@ __global__ void line_setup_kernel(const double* __restrict__ drift_arr, int64_t 
     lc[line] = c;
 }
 
+// Per-line constants of a window-table step: one warp per line reduces the window's
+// minimum and maximum |slope| (the gate and the search tolerance).
+__global__ void line_setup_tab_kernel(const double* __restrict__ ktab, int64_t stride,
+                                      const int64_t* __restrict__ first_arr, int64_t lines, int64_t n,
+                                      LineConst* __restrict__ lc) {
+    const int64_t line = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (line >= lines) return;
+    const double* K = ktab + line * stride;
+    double kmin = INFINITY, smx = 0.0;
+    for (int64_t w = lane; w <= 2 * n; w += 32) {
+        kmin = fmin(kmin, K[w]);
+        if (w < 2 * n) smx = fmax(smx, fabs(__dsub_rn(K[w + 1], K[w])));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        kmin = fmin(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+        smx = fmax(smx, __shfl_xor_sync(0xffffffffu, smx, o));
+    }
+    if (lane) return;
+    LineConst c{};
+    const int64_t first = first_arr[line];
+    c.first = first;
+    c.kt = K - first;
+    c.gap = fmin(K[0], K[2 * n]) - kmin;
+    c.smax = smx;
+    c.tol = 4.0 * 1.1102230246251565e-16;  // >= u/(1-u) on each side of the comparison, 2x spare
+    c.sg0 = __dsub_rn(K[1], K[0]);
+    const double sg1 = __dsub_rn(K[2 * n], K[2 * n - 1]);
+    c.sgi = sg1 > c.sg0 ? static_cast<double>(2 * n - 1) / (sg1 - c.sg0) : 0.0;
+    c.k0 = K[0];
+    c.kmid = K[n];
+    c.kend = K[2 * n];
+    lc[line] = c;
+}
+
 // Main K2 kernel: one CTA = (tile of kT outputs, line); grid (tiles, lines).
 // All index arithmetic is 32-bit (n <= 2^29); "unrolled" source/output
 // indices y, j may lie in (-3n, 3n) and are reduced mod n only on access.
@@ -756,7 +873,7 @@ __global__ void line_setup_kernel(const double* __restrict__ drift_arr, int64_t 
 // [8] tiles by the direct formula because the walk's estimated candidates exceeded the
 // window's, [9] chained-wait timeouts (a misused LOB_FAST_CHAINED), [10] warps whose
 // fold queue overflowed.
-template <bool TMA, bool CHAIN, bool RELEASE>
+template <bool TAB, bool TMA, bool CHAIN, bool RELEASE>
 __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
     const double* __restrict__ u, double* __restrict__ out, const LineConst* __restrict__ lcs,
     const double* __restrict__ tv, int64_t tv_stride, int64_t* __restrict__ blocks_out,
@@ -778,11 +895,40 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
     // enough for one conditional wrap per chunk; else a cooperative load
     const bool big = TMA && n >= kC + 8;
     const double* ul = u + line * p.n;
-    const LineConst lc = lcs[line];
+    LineConst lc = lcs[line];
+    // carried line constants (LOB_FAST_STATS_VALID) must describe the caller's current drift /
+    // window: a mismatch (another table at a reused address, a drift changed in place) takes
+    // the direct formula with the current inputs (exact) and is counted
+    bool stale;
+    if constexpr (TAB) {
+        const double* Kl = p.ktab + line * p.kstride;
+        const long long f = __ldg(p.kfirst + line);
+        stale = f != lc.first || __double_as_longlong(__ldg(Kl)) != __double_as_longlong(lc.k0) ||
+                __double_as_longlong(__ldg(Kl + n)) != __double_as_longlong(lc.kmid) ||
+                __double_as_longlong(__ldg(Kl + 2 * n)) != __double_as_longlong(lc.kend);
+        if (stale) {
+            lc.first = f;
+            lc.kt = Kl - f;
+        }
+    } else {
+        const double d = __ldg(p.drift_arr + line);
+        stale = __double_as_longlong(d) != __double_as_longlong(lc.drift);
+        if (stale) {
+            lc.drift = d;
+            lc.first = llround(__ddiv_rn(__dmul_rn(p.tau, d), p.eps)) - p.n;  // line_setup_kernel's formula
+        }
+    }
     const double tau = p.tau, ia = p.ia, hl = lc.hl, hr = lc.hr;
     const int first = static_cast<int>(lc.first);
     const int dmin_w = first + 1, dmax_w = first + 2 * n - 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // K(d) anywhere in the window: the line's table (TAB) or build_kernel's formula over v_d
+    auto kf = [&](int d) -> double {
+        if constexpr (TAB) return __ldg(lc.kt + d);
+        else return kdirect(p, d, lc.drift);
+    };
+    // window slopes sigma(d) = K(d+1) - K(d) from global memory (table mode)
+    auto sigg = [&](int d) -> double { return __dsub_rn(__ldg(lc.kt + d + 1), __ldg(lc.kt + d)); };
 
     // programmatic dependent launch: the next step's grid may start its prologue once
     // every CTA of this one is running; this grid waits for the previous one (its u,
@@ -830,12 +976,20 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
         // max u - min u is below the window's edge gap min(K(first), K(last)) - min K
         const double osc = LOB_OSC_EXACT ? __dsub_rn(umax, umin)
                                          : 0.5 * static_cast<double>(n) * fmax(fabs(smin), fabs(smax));
-        bool okl = isfinite(osc) && isfinite(smin) && isfinite(smax) && n >= 3 &&
+        bool okl = !stale && isfinite(osc) && isfinite(smin) && isfinite(smax) && n >= 3 &&
                    osc * (1.0 + 1e-12) < lc.gap * (1.0 - 1e-12);
         const bool gate = okl;
+        if (stale && lane == 0 && diag) atomicAdd(diag + 11, 1ull);
         if (okl) {
-            DLg = max(__double2int_ru(__fma_rn(smin, ia, hl)), dmin_w);
-            DRg = min(__double2int_rd(__fma_rn(smax, ia, hr)), dmax_w);
+            if constexpr (TAB) {
+                int dl, dr;
+                tab_interval(sigg, lc, smin, smax, dmin_w, dmax_w, dl, dr);
+                DLg = max(dl, dmin_w);
+                DRg = min(dr, dmax_w);
+            } else {
+                DLg = max(__double2int_ru(__fma_rn(smin, ia, hl)), dmin_w);
+                DRg = min(__double2int_rd(__fma_rn(smax, ia, hr)), dmax_w);
+            }
             okl = DLg <= DRg;
         }
         int ya = INT_MAX, yb = INT_MIN, dlo = INT_MAX, dhi = INT_MIN;
@@ -848,8 +1002,14 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
             const double2 sb = xload<CHAIN>(b.sub_in + line * p.subs + q);
             ys = k * n + q * kG;
             ye = ys + min(kG, n - q * kG) - 1;
-            dl = max(__double2int_ru(__fma_rn(sb.x, ia, hl)), DLg);
-            dr = min(__double2int_rd(__fma_rn(sb.y, ia, hr)), DRg);
+            if constexpr (TAB) {
+                tab_interval(sigg, lc, sb.x, sb.y, DLg, DRg, dl, dr);
+                dl = max(dl, DLg);
+                dr = min(dr, DRg);
+            } else {
+                dl = max(__double2int_ru(__fma_rn(sb.x, ia, hl)), DLg);
+                dr = min(__double2int_rd(__fma_rn(sb.y, ia, hr)), DRg);
+            }
             return dl <= dr && ys + dl <= jhi && ye + dr >= jlo;
         };
         if (okl) {
@@ -935,11 +1095,11 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
                 mbar_init(&S.mbar, 1);
                 asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
                 if (big) {
-                    // first source chunk + the tile's v_d range, in flight across the barrier
+                    // first source chunk + (mechanical) the tile's v_d range, in flight across the barrier
                     const int vd0 = dlo - ((dlo + static_cast<int>(p.vofs)) & 1);
                     const int vcnt = (dhi - vd0 + 2) & ~1;
                     issue_chunk(S, ul, n, ya, min(kC, S.re[0] - ya + 1),
-                                vcnt <= kVCap ? p.vtab + p.vofs + vd0 : nullptr, vcnt);
+                                (!TAB && vcnt <= kVCap) ? p.vtab + p.vofs + vd0 : nullptr, vcnt);
                 }
             }
         }
@@ -952,11 +1112,13 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
         const int ya = S.ya;
         const int dlo_t = S.dlo, dhi_t = S.dhi;
         // K(d) = tau*((0.5 v)v - P v): staged in shared memory (TMA'd v_d, converted
-        // in place) when the tile's displacement range fits, else from the global v_d table
-        const int vd0 = dlo_t - ((dlo_t + static_cast<int>(p.vofs)) & 1);
-        const int vcnt = (dhi_t - vd0 + 2) & ~1;
-        const bool kstage = big && vcnt <= kVCap;
-        const double* gvt = p.vtab + p.vofs;
+        // in place) when the tile's displacement range fits, else from the global v_d table.
+        // Table mode: K(dlo - 1 .. dhi + 1) (the slope search reads sigma one step outside
+        // [dlo, dhi]) copied from the line's window, else read from it.
+        const int vd0 = TAB ? dlo_t - 2 : dlo_t - ((dlo_t + static_cast<int>(p.vofs)) & 1);
+        const int vcnt = TAB ? ((dhi_t + 2 - vd0 + 1) + 1) & ~1 : (dhi_t - vd0 + 2) & ~1;
+        const bool kstage = (TAB || big) && vcnt <= kVCap;
+        const double* gvt = TAB ? lc.kt : p.vtab + p.vofs;
         const double* skt = S.vbuf - vd0;
         const double kdrift = lc.drift;
         const unsigned budget = S.budget;
@@ -977,7 +1139,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
                 if (warp == 0) mbar_wait(&S.mbar, mphase);
                 mphase ^= 1u;
                 __syncthreads();
-                if (yc == ya && kstage) {
+                if (yc == ya && kstage && !TAB) {
                     for (int i = tid; i < vcnt; i += kNT) S.vbuf[i] = kval_v(S.vbuf[i], kdrift, tau);
                     __syncthreads();
                 }
@@ -986,10 +1148,15 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
                 for (int i = tid; i < clen + 2; i += kNT) S.ubuf[i] = CHAIN ? __ldcg(ul + (bm + i) % n) : __ldg(ul + (bm + i) % n);
                 __syncthreads();
             }
+            if (TAB && yc == ya && kstage) {
+                // the window's K values of the tile's displacement range (clamped to the window)
+                for (int i = tid; i < vcnt; i += kNT) S.vbuf[i] = __ldg(lc.kt + min(max(vd0 + i, first), first + 2 * n));
+                __syncthreads();
+            }
             const double* ub = S.ubuf + sh;
             if (tid == 0) S.c_src += static_cast<unsigned>(clen);
-            const ChunkArgs ca{ub, clen, base, jspan, ia, hl, hr, dlo_t, dhi_t, skt, gvt, kdrift, tau};
-            walk = kstage ? process_chunk<true>(S, ca, budget) : process_chunk<false>(S, ca, budget);
+            const ChunkArgs ca{ub, clen, base, jspan, ia, hl, hr, dlo_t, dhi_t, skt, gvt, kdrift, tau, &lc};
+            walk = kstage ? process_chunk<TAB, true>(S, ca, budget) : process_chunk<TAB, false>(S, ca, budget);
             if (!walk) break;  // the walk would cost more than the window: the direct formula
             yc += clen;
             if (yc > yr && ++run < nruns) {
@@ -1002,7 +1169,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
         atomicAdd(diag + 7, 1ull);
     }
 #if LOB_TILE_DIRECT
-    if (!walk) tile_direct<CHAIN>(S, ul, n, j0, Tl, first, p, lc.drift);
+    if (!walk) tile_direct<CHAIN>(S, ul, n, j0, Tl, first, kf);
 #endif
     __syncthreads();
 
@@ -1019,7 +1186,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
         int y = (j - first) % n;
         if (y < 0) y += n;
         for (int w = 0; w <= 2 * n; ++w) {
-            const double c2 = __dadd_rn(xload<CHAIN>(ul + y), kdirect(p, first + w, lc.drift));
+            const double c2 = __dadd_rn(xload<CHAIN>(ul + y), kf(first + w));
             best = c2 < best ? c2 : best;
             y = y == 0 ? n - 1 : y - 1;
         }
@@ -1436,7 +1603,7 @@ static FastBuffers make_buffers(void* ws, int64_t lines, int64_t n, int64_t coun
 int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
                     const double* drift, double tau, const double* tv, int64_t tv_stride,
                     double eta, int64_t* blocks, void* workspace, size_t ws_bytes, int flags,
-                    cudaStream_t s, double* dpart) {
+                    cudaStream_t s, double* dpart, const FastTable* tab) {
     if (ws_bytes < fast_workspace_bytes(lines, n) || !workspace)
         return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_fast_f64: workspace too small");
     if (n > (1ll << 29)) return set_error(ctx, LOB_INVALID_INPUT, "fast: n too large");
@@ -1444,10 +1611,24 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     int st = ensure_lut(ctx);
     if (st) return st;
     FastParams p = make_params(n, tau, eta);
-    st = ensure_vtab(ctx, n, tau, &p.vtab, &p.vofs, s);
-    if (st) return st;
+    if (!tab) {
+        st = ensure_vtab(ctx, n, tau, &p.vtab, &p.vofs, s);
+        if (st) return st;
+    }
     const int64_t nblk = lines * p.tiles;
     if (nblk > 0x7fffffffll) return set_error(ctx, LOB_INVALID_INPUT, "fast: grid too large");
+    p.drift_arr = drift;
+    if (tab) {
+        p.ktab = tab->ktab;
+        p.kstride = tab->stride;
+        p.kfirst = tab->first;
+    }
+    // the per-line constants hold the window table: another table recomputes them
+    const void* tkey = tab ? static_cast<const void*>(tab->ktab) : nullptr;
+    if (ctx->ws_table[workspace] != tkey) {
+        ctx->ws_table[workspace] = tkey;
+        flags &= ~LOB_FAST_STATS_VALID;
+    }
     const bool tma = (n % 2 == 0) && (reinterpret_cast<uintptr_t>(u) % 16 == 0);
     if (ctx->ws_shape[workspace] != std::make_pair(lines, n)) {
         ctx->ws_shape[workspace] = std::make_pair(lines, n);
@@ -1468,8 +1649,12 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
         reinterpret_cast<unsigned long long*>(static_cast<char*>(workspace) + w.diag);
     LineConst* lcs = reinterpret_cast<LineConst*>(static_cast<char*>(workspace) + w.lc);
     if (!(flags & LOB_FAST_STATS_VALID)) {
-        // per-line constants (valid while drift/tau/n and the workspace are unchanged)
-        line_setup_kernel<<<static_cast<unsigned>((lines + 127) / 128), 128, 0, s>>>(drift, lines, p, lcs);
+        // per-line constants (valid while drift/tau/n (or the table) and the workspace are unchanged)
+        if (tab)
+            line_setup_tab_kernel<<<static_cast<unsigned>((lines * 32 + 127) / 128), 128, 0, s>>>(
+                tab->ktab, tab->stride, tab->first, lines, n, lcs);
+        else
+            line_setup_kernel<<<static_cast<unsigned>((lines + 127) / 128), 128, 0, s>>>(drift, lines, p, lcs);
         LOB_CUDA_TRY(ctx, cudaMemsetAsync(diag, 0, kDiag * sizeof(unsigned long long), s));
         LOB_CUDA_TRY(ctx, cudaMemsetAsync(static_cast<char*>(workspace) + w.done, 0, lines * sizeof(unsigned), s));
         ctx->ws_chain[workspace] = 0;
@@ -1497,12 +1682,16 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     if (release && chain == 0) LOB_CUDA_TRY(ctx, cudaMemsetAsync(done, 0, lines * sizeof(unsigned), s));
     using KernT = void (*)(const double*, double*, const LineConst*, const double*, int64_t, int64_t*,
                            unsigned long long*, FastParams, FastBuffers, unsigned*, unsigned, double*);
-    static const KernT kerns[2][2][2] = {
-        {{fast_kernel<false, false, false>, fast_kernel<false, false, true>},
-         {fast_kernel<false, true, false>, fast_kernel<false, true, true>}},
-        {{fast_kernel<true, false, false>, fast_kernel<true, false, true>},
-         {fast_kernel<true, true, false>, fast_kernel<true, true, true>}}};
-    auto kern = kerns[tma][chained][release];
+    static const KernT kerns[2][2][2][2] = {
+        {{{fast_kernel<false, false, false, false>, fast_kernel<false, false, false, true>},
+          {fast_kernel<false, false, true, false>, fast_kernel<false, false, true, true>}},
+         {{fast_kernel<false, true, false, false>, fast_kernel<false, true, false, true>},
+          {fast_kernel<false, true, true, false>, fast_kernel<false, true, true, true>}}},
+        {{{fast_kernel<true, false, false, false>, fast_kernel<true, false, false, true>},
+          {fast_kernel<true, false, true, false>, fast_kernel<true, false, true, true>}},
+         {{fast_kernel<true, true, false, false>, fast_kernel<true, true, false, true>},
+          {fast_kernel<true, true, true, false>, fast_kernel<true, true, true, true>}}}};
+    auto kern = kerns[tab != nullptr][tma][chained][release];
     const unsigned need = static_cast<unsigned>(chain * p.tiles * (kNT / 32));
     if (first_time(ctx, reinterpret_cast<const void*>(kern))) {
         LOB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

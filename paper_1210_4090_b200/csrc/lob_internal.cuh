@@ -30,6 +30,7 @@ struct lob_ctx {
     std::map<const void*, const void*> ws_last_out;  // workspace -> out of its last K2 call
     std::map<const void*, int64_t> ws_chain;         // K2 launches since the done counters were reset
     std::map<const void*, bool> ws_fsm_valid;        // the workspace holds FSM summaries of its last out
+    std::map<const void*, const void*> ws_table;     // workspace -> window table of its line constants
     // K1 mode (LOB_DIRECT_SCREENED / LOB_DIRECT_PLAIN) and the screened kernel's
     // count of outputs swept in full fp64 (device counter, lazily allocated)
     int direct_mode = 0;
@@ -117,11 +118,19 @@ int launch_window_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines,
                       const double* tv, int64_t tv_stride, int* d_err, cudaStream_t s);
 
 size_t fast_workspace_bytes(int64_t lines, int64_t n);
-// dpart (nullable): per-tile sums of u^{n+1} - u^n for evolve's drift ([lines][fast_tiles(n)])
+// window-table mode of K2: line l's window is ktab[l*stride + w], w = 0..2n, at
+// displacements first[l] + w (device arrays)
+struct FastTable {
+    const double* ktab;
+    int64_t stride;
+    const int64_t* first;
+};
+// dpart (nullable): per-tile sums of u^{n+1} - u^n for evolve's drift ([lines][fast_tiles(n)]);
+// tab (nullable): any convex window per line instead of the mechanical drift
 int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
                     const double* drift, double tau, const double* tv, int64_t tv_stride,
                     double eta, int64_t* blocks, void* workspace, size_t ws_bytes, int flags,
-                    cudaStream_t s, double* dpart = nullptr);
+                    cudaStream_t s, double* dpart = nullptr, const FastTable* tab = nullptr);
 int64_t fast_tiles(int64_t n);
 int launch_drift_tiles(lob_ctx* ctx, const double* dpart, int64_t lines, int64_t n, double* drift_out, int* halt,
                        int step, cudaStream_t s);
