@@ -131,7 +131,7 @@ int lob_minplus_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lin
  * the reference's Kernel carries exactly the window (mechanical or tabulated,
  * proj/src/scheme.cpp:59-105).  Table conventions as lob_minplus_direct_f64
  * (ktab_stride 0 = one window for all lines; first: device int64[lines]);
- * tau > 0 only scales the work budget; flags/workspace/blocks as
+ * tau must be > 0 but is otherwise unused (every cost comes from the window); flags/workspace/blocks as
  * lob_minplus_fast_f64 (the workspace remembers the table: another table
  * recomputes the statistics). */
 int lob_minplus_fast_window_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,

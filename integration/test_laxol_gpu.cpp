@@ -1,0 +1,208 @@
+// The drop-in shim (laxol_gpu) against the reference's own CPU engines, in one process
+// linked with the unmodified reference library (built from its sources by oracle/Makefile)
+// and liblaxol_b200.so.  Every comparison is ==; prints one PASS/FAIL line per case and
+// exits non-zero on any failure.  Run by tests/test_integration_gpu.py on the GPU box.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <numbers>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "laxol/errors.hpp"
+#include "laxol/grid_fn.hpp"
+#include "laxol/hamiltonian.hpp"
+#include "laxol/scheme.hpp"
+#include "laxol_gpu.hpp"
+
+using laxol_gpu::Engine;
+
+static int g_fail = 0;
+
+static void report(const std::string& name, bool ok) {
+    std::printf("%s %s\n", ok ? "PASS" : "FAIL", name.c_str());
+    if (!ok) ++g_fail;
+}
+
+static bool same(const laxol::GridFn& a, const laxol::GridFn& b) {
+    if (a.values.size() != b.values.size() || a.step != b.step || a.origin != b.origin || a.periodic != b.periodic)
+        return false;
+    for (std::size_t i = 0; i < a.values.size(); ++i)
+        if (!(a.values[i] == b.values[i])) return false;
+    return true;
+}
+
+static laxol::SchemeParams params_of(int n, double tau, double eta = 0.0) {
+    laxol::SchemeParams p;
+    p.n_space = n;
+    p.tau = tau;
+    p.eta = eta;
+    return p;
+}
+
+// seeded periodic random walk (fundamental domain), made periodic by removing the drift
+static std::vector<double> walk(int n, double scale, std::uint64_t seed) {
+    std::mt19937_64 g(seed);
+    std::uniform_real_distribution<double> d(-scale / n, scale / n);
+    std::vector<double> w(n + 1, 0.0);
+    for (int i = 0; i < n; ++i) w[i + 1] = w[i] + d(g);
+    std::vector<double> u(n);
+    for (int i = 0; i < n; ++i) u[i] = w[i] - w[n] * i / n;
+    return u;
+}
+
+int main() {
+    laxol_gpu::Device dev(0);
+    constexpr double kTwoPi = 2.0 * std::numbers::pi;
+
+    // 1. kinetic_convolve, mechanical and tabulated windows, both device engines == Naive
+    for (int n : {24, 600, 1024, 4096}) {
+        const double tau = n == 24 ? 0.25 : (n == 4096 ? 0.01 : 0.04);
+        for (double drift : {0.0, 0.4, -0.7}) {
+            const laxol::SchemeParams p = params_of(n, tau);
+            const laxol::Kernel k = laxol::build_kernel(laxol::mechanical(drift), p);
+            const laxol::GridFn u = laxol::make_periodic(walk(n, 4.0, 100 + n), p.epsilon());
+            std::int64_t bref = 0, bf = 0, bd = 0;
+            const laxol::GridFn want = laxol::kinetic_convolve(u, k, 0.0, laxol::ConvEngine::Naive, &bref);
+            const laxol::GridFn gf = dev.kinetic_convolve(u, k, 0.0, Engine::GpuFast, &bf);
+            const laxol::GridFn gd = dev.kinetic_convolve(u, k, 0.0, Engine::GpuDirect, &bd);
+            report("kinetic_convolve mechanical n=" + std::to_string(n) + " P=" + std::to_string(drift),
+                   same(gf, want) && same(gd, want) && bf == bref && bd == bref);
+        }
+    }
+    {
+        // tabulated conjugates the reference accepts at these grids (its convexity check)
+        struct Tab {
+            const char* name;
+            double v0, dv;
+            int count, n;
+            double tau;
+            double (*f)(double);
+        };
+        const Tab tabs[] = {
+            {"|v|^1.5", -25.0, 0.5, 101, 64, 0.1, [](double v) { return std::pow(std::abs(v), 1.5); }},
+            {"piecewise", -50.0, 2.5, 41, 256, 0.1,
+             [](double v) { return std::max(std::max(-v, 0.5 * v), 0.25 * v + 1.0); }},
+            {"flat bottom", -40.0, 1.0, 81, 512, 0.25,
+             [](double v) { return std::pow(std::max(std::abs(v) - 2.0, 0.0), 2.0); }},
+        };
+        for (const Tab& tb : tabs) {
+            std::vector<double> samples;
+            for (int i = 0; i < tb.count; ++i) samples.push_back(tb.f(tb.v0 + i * tb.dv));
+            const laxol::SchemeParams p = params_of(tb.n, tb.tau);
+            const laxol::Kernel k = laxol::build_kernel(laxol::tabulated(samples, tb.v0, tb.dv), p);
+            const laxol::GridFn u = laxol::make_periodic(walk(tb.n, 0.5, 7 + tb.n), p.epsilon());
+            const laxol::GridFn want = laxol::kinetic_convolve(u, k, 0.0, laxol::ConvEngine::Naive);
+            report(std::string("kinetic_convolve tabulated ") + tb.name + " n=" + std::to_string(tb.n),
+                   same(dev.kinetic_convolve(u, k, 0.0, Engine::GpuFast), want) &&
+                       same(dev.kinetic_convolve(u, k, 0.0, Engine::GpuDirect), want));
+        }
+    }
+    // 2. eta > 0: GpuFast == the reference's relaxed ConvEngine::Fast (values and capped blocks)
+    for (double eta : {1e-6, 1e-3}) {
+        const int n = 600;
+        const laxol::SchemeParams p = params_of(n, 0.04, eta);
+        const laxol::Kernel k = laxol::build_kernel(laxol::mechanical(1.0), p);
+        const laxol::GridFn u = laxol::make_periodic(walk(n, 2.0, 55), p.epsilon());
+        std::int64_t bref = 0, bg = 0;
+        const laxol::GridFn want = laxol::kinetic_convolve(u, k, eta, laxol::ConvEngine::Fast, &bref);
+        report("kinetic_convolve relaxed eta=" + std::to_string(eta),
+               same(dev.kinetic_convolve(u, k, eta, Engine::GpuFast, &bg), want) && bg == bref);
+    }
+    // 3. windowed (wall) domain == Naive; a window that cannot reach raises EvaluationError
+    {
+        const int n = 128;
+        const laxol::SchemeParams p = params_of(n, 0.05);
+        const laxol::Kernel k = laxol::build_kernel(laxol::mechanical(0.3), p);
+        std::vector<double> w = walk(n, 1.0, 3);
+        w.resize(96);
+        const laxol::GridFn u = laxol::make_grid_fn(w, p.epsilon(), 0.25);
+        const laxol::GridFn want = laxol::kinetic_convolve(u, k, 0.0, laxol::ConvEngine::Naive);
+        report("kinetic_convolve windowed", same(dev.kinetic_convolve(u, k, 0.0, Engine::GpuDirect), want) &&
+                                                same(dev.kinetic_convolve(u, k, 0.0, Engine::GpuFast), want));
+        bool ref_threw = false, gpu_threw = false;
+        const laxol::Kernel kfar = laxol::build_kernel(laxol::mechanical(40.0), p);
+        try {
+            laxol::kinetic_convolve(u, kfar, 0.0, laxol::ConvEngine::Naive);
+        } catch (const laxol::EvaluationError&) {
+            ref_threw = true;
+        }
+        try {
+            dev.kinetic_convolve(u, kfar, 0.0, Engine::GpuDirect);
+        } catch (const laxol::EvaluationError&) {
+            gpu_threw = true;
+        }
+        report("kinetic_convolve windowed unreachable -> EvaluationError", ref_threw && gpu_threw);
+    }
+    // 4. step_fully_discrete with a time-dependent custom potential (Arrival and Departure)
+    for (auto sampling : {laxol::PotentialSampling::Arrival, laxol::PotentialSampling::Departure}) {
+        const int n = 1024;
+        laxol::SchemeParams p = params_of(n, 0.05);
+        p.v_sampling = sampling;
+        const laxol::HamiltonianSpec spec = laxol::make_spec(
+            laxol::mechanical(0.5),
+            laxol::potential_custom([&](double t, double x) { return std::cos(kTwoPi * x) + 0.3 * std::sin(kTwoPi * t); },
+                                    1.3, true),
+            true, false);
+        const laxol::Kernel k = laxol::build_kernel(spec, p);
+        std::vector<double> u0(n);
+        for (int j = 0; j < n; ++j) u0[j] = std::sin(kTwoPi * (static_cast<double>(j) * p.epsilon()));
+        const laxol::GridFn u = laxol::make_periodic(u0, p.epsilon());
+        laxol::StepStats sr, sf, sd;
+        const laxol::GridFn want = laxol::step_fully_discrete(u, 0.35, spec, p, k, laxol::ConvEngine::Naive, &sr);
+        const laxol::GridFn gf = dev.step_fully_discrete(u, 0.35, spec, p, k, Engine::GpuFast, &sf);
+        const laxol::GridFn gd = dev.step_fully_discrete(u, 0.35, spec, p, k, Engine::GpuDirect, &sd);
+        report(std::string("step_fully_discrete custom V ") +
+                   (sampling == laxol::PotentialSampling::Arrival ? "arrival" : "departure"),
+               same(gf, want) && same(gd, want) && sf.block_count == sr.block_count &&
+                   sd.block_count == sr.block_count);
+    }
+    // 5. evolve: C1 in full (N=1024, tau=0.05, P=0.5, V=cos 2 pi x, u0=sin 2 pi x, 2000 steps)
+    {
+        const int n = 1024;
+        const laxol::SchemeParams p = params_of(n, 0.05);
+        const laxol::HamiltonianSpec spec = laxol::make_spec(
+            laxol::mechanical(0.5), laxol::potential_custom([&](double, double x) { return std::cos(kTwoPi * x); }, 1.0, false),
+            true, true);
+        std::vector<double> u0(n);
+        for (int j = 0; j < n; ++j) u0[j] = std::sin(kTwoPi * (static_cast<double>(j) * p.epsilon()));
+        const laxol::GridFn u = laxol::make_periodic(u0, p.epsilon());
+        laxol::EvolveOptions o;
+        o.engine = laxol::ConvEngine::Naive;
+        const laxol::EvolutionTrace want = laxol::evolve(u, 0.0, 2000, spec, p, o);
+        for (Engine e : {Engine::GpuFast, Engine::GpuDirect}) {
+            const laxol::EvolutionTrace got = dev.evolve(u, 0.0, 2000, spec, p, e, {});
+            bool ok = got.completed == want.completed && got.snapshots.size() == want.snapshots.size() &&
+                      got.per_step.size() == want.per_step.size() && got.times == want.times &&
+                      got.snapshot_steps == want.snapshot_steps;
+            for (std::size_t i = 0; ok && i < want.snapshots.size(); ++i) ok = same(got.snapshots[i], want.snapshots[i]);
+            for (std::size_t i = 0; ok && i < want.per_step.size(); ++i)
+                ok = got.per_step[i].drift == want.per_step[i].drift && got.per_step[i].blocks == want.per_step[i].blocks &&
+                     got.per_step[i].time == want.per_step[i].time;
+            report(std::string("evolve C1 2000 steps ") + (e == Engine::GpuFast ? "GpuFast" : "GpuDirect"), ok);
+        }
+    }
+    // 6. the reference's argument errors surface as its own exception types
+    {
+        const laxol::SchemeParams p = params_of(64, 0.05);
+        const laxol::Kernel k = laxol::build_kernel(laxol::mechanical(0.0), p);
+        const laxol::GridFn u = laxol::make_periodic(std::vector<double>(32, 0.0), 1.0 / 32);
+        bool threw = false;
+        try {
+            dev.kinetic_convolve(u, k, 0.0, Engine::GpuFast);
+        } catch (const laxol::InvalidInput&) {
+            threw = true;
+        }
+        bool threw2 = false;
+        const laxol::HamiltonianSpec spec = laxol::make_spec(laxol::mechanical(0.0), laxol::potential_zero(), true, true);
+        try {
+            dev.evolve(u, 0.0, 3, spec, p, Engine::GpuFast, {});
+        } catch (const laxol::InvalidInput&) {
+            threw2 = true;
+        }
+        report("InvalidInput on a grid of another period", threw && threw2);
+    }
+    std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "ALL PASS", g_fail);
+    return g_fail ? 1 : 0;
+}
