@@ -143,8 +143,8 @@ int lob_minplus_fast_window_f64(lob_ctx* ctx, const double* u, double* out, int6
  * LOB_FAST_STATS_VALID on this workspace (counters[16]; unused entries 0):
  *  [0] outputs no local-minimum interval reached, recomputed by the exact
  *      direct scan (0 in correct operation),
- *  [1] sources scanned by the walk, [2] fold ranges (outputs covered twice,
- *  exact CAS-min), [3] long frontier / gap runs stored by a whole warp,
+ *  [1] sources scanned by the walk, [2] candidates of queued intervals (long
+ *  or contended: finished by a whole warp), [3] queued intervals,
  *  [4] tiles, [5] walk tiles whose K range did not fit the shared-memory stage,
  *  [6] sum of the walk tiles' K range lengths,
  *  [7] tiles computed by the direct formula because the oscillation gate failed
@@ -169,8 +169,14 @@ int lob_fast_diagnostics(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n
  * rounding, as the C++ expression a1*a2 + b), i.e. the reference's
  * PotentialNd callback evaluated on the host per axis and per step;
  * a1 == NULL means V == 0.  tmp: device scratch of n*n doubles.
- * engine LOB_ENGINE_DIRECT or LOB_ENGINE_FAST (fast needs workspace of
- * lob_fast_workspace_bytes(n, n)). */
+ * engine LOB_ENGINE_DIRECT or LOB_ENGINE_FAST.  With LOB_ENGINE_FAST and a
+ * workspace of 2 x lob_fast_workspace_bytes(n, n) the step is fused into four
+ * launches: transpose + the fast engine's input statistics, sweep axis 0,
+ * transpose + statistics, sweep axis 1 with tau*(a1*a2 + b) in its epilogue (one
+ * workspace half per axis; consecutive steps keep each axis' line constants);
+ * with a single lob_fast_workspace_bytes(n, n) the unfused sequence runs.
+ * Asynchronous on `stream` (the per-axis kernel tables are built once per
+ * (n, tau, drift) and cached by the context). */
 int lob_split_step_2d_f64(lob_ctx* ctx, const double* u, double* out, double* tmp, int64_t n,
                           double tau, double drift1, double drift2, const double* a1,
                           const double* a2, double b, int engine, void* workspace,

@@ -211,7 +211,7 @@ class Device:
                                                   _stream_ptr(stream))
         self._check(st, "lob_minplus_fast_window_f64")
 
-    FAST_COUNTER_KEYS = ["missed_outputs", "sources", "fold_ranges", "plain_runs", "tiles", "tiles_k_unstaged",
+    FAST_COUNTER_KEYS = ["missed_outputs", "sources", "queued_candidates", "queued_intervals", "tiles", "tiles_k_unstaged",
                          "k_range_sum", "direct_tiles_gate", "direct_tiles_heavy", "chain_timeouts",
                          "unused10", "stale_line_constants"]
 

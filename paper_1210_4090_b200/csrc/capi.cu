@@ -64,6 +64,7 @@ int lob_ctx_destroy(lob_ctx* ctx) {
     if (!ctx) return LOB_OK;
     cudaSetDevice(ctx->device);
     for (auto& kv : ctx->vtabs) cudaFree(kv.second.dev);
+    for (auto& kv : ctx->split_axes) cudaFree(kv.second);
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->direct_full) cudaFree(ctx->direct_full);
     if (ctx->direct_umax) cudaFree(ctx->direct_umax);
@@ -221,6 +222,43 @@ int lob_block_counts(lob_ctx* ctx, const double* u, int64_t lines, int64_t n, do
     return launch_block_counts(ctx, u, lines, n, eta, blocks, static_cast<cudaStream_t>(stream));
 }
 
+// Per-axis device inputs of a mechanical split step, built once per (n, tau, drift) and kept
+// by the context (never rewritten: no reuse race with work still queued on any stream):
+// the kernel window (K1), n copies of first (K1) and of the drift (K2).
+static int split_axis_inputs(lob_ctx* ctx, int64_t n, double tau, double drift, const double** ktab,
+                             const int64_t** firsts, const double** drifts, cudaStream_t s) {
+    uint64_t tb, db;
+    std::memcpy(&tb, &tau, 8);
+    std::memcpy(&db, &drift, 8);
+    const auto key = std::make_tuple(n, tb, db);
+    auto it = ctx->split_axes.find(key);
+    if (it == ctx->split_axes.end()) {
+        const size_t W = static_cast<size_t>(2 * n + 1);
+        std::vector<double> h(W);
+        int64_t f, arg;
+        double dl;
+        if (lob_kernel_mech_host(ctx, n, tau, drift, h.data(), &f, &arg, &dl))
+            return set_error(ctx, LOB_INVALID_INPUT, "split_step_nd: invalid kernel parameters");
+        std::vector<int64_t> hf(static_cast<size_t>(n), f);
+        std::vector<double> hd(static_cast<size_t>(n), drift);
+        char* buf = nullptr;
+        const size_t bytes = W * 8 + static_cast<size_t>(n) * 16;
+        LOB_CUDA_TRY(ctx, cudaMalloc(&buf, bytes));
+        LOB_CUDA_TRY(ctx, cudaMemcpyAsync(buf, h.data(), W * 8, cudaMemcpyHostToDevice, s));
+        LOB_CUDA_TRY(ctx, cudaMemcpyAsync(buf + W * 8, hf.data(), n * 8, cudaMemcpyHostToDevice, s));
+        LOB_CUDA_TRY(ctx, cudaMemcpyAsync(buf + W * 8 + n * 8, hd.data(), n * 8, cudaMemcpyHostToDevice, s));
+        // the host vectors die here: complete the (one-time) upload
+        LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+        it = ctx->split_axes.emplace(key, buf).first;
+    }
+    char* buf = static_cast<char*>(it->second);
+    const size_t W = static_cast<size_t>(2 * n + 1);
+    *ktab = reinterpret_cast<const double*>(buf);
+    *firsts = reinterpret_cast<const int64_t*>(buf + W * 8);
+    *drifts = reinterpret_cast<const double*>(buf + W * 8 + n * 8);
+    return LOB_OK;
+}
+
 int lob_split_step_2d_f64(lob_ctx* ctx, const double* u, double* out, double* tmp, int64_t n,
                           double tau, double drift1, double drift2, const double* a1,
                           const double* a2, double b, int engine, void* workspace,
@@ -230,63 +268,43 @@ int lob_split_step_2d_f64(lob_ctx* ctx, const double* u, double* out, double* tm
     if (!u || !out || !tmp || u == out || u == tmp || out == tmp)
         return set_error(ctx, LOB_INVALID_INPUT, "lob_split_step_2d_f64: need distinct u/out/tmp");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    // kernel tables / drifts for the two axes live in the context scratch
-    const size_t W = static_cast<size_t>(2 * n + 1);
-    const size_t need = 2 * W * sizeof(double) + 2 * n * sizeof(int64_t) + 2 * n * sizeof(double);
-    if (ctx->scratch_bytes < need) {
-        if (ctx->scratch) cudaFree(ctx->scratch);
-        ctx->scratch = nullptr;
-        LOB_CUDA_TRY(ctx, cudaMalloc(&ctx->scratch, need));
-        ctx->scratch_bytes = need;
+    const double *k1, *k2, *d1, *d2;
+    const int64_t *f1, *f2;
+    if ((st = split_axis_inputs(ctx, n, tau, drift1, &k1, &f1, &d1, s))) return st;
+    if ((st = split_axis_inputs(ctx, n, tau, drift2, &k2, &f2, &d2, s))) return st;
+    const size_t wsz = fast_workspace_bytes(n, n);
+    if (engine == LOB_ENGINE_FAST && workspace && workspace_bytes >= 2 * wsz) {
+        // fused: transpose + K2 statistics -> sweep axis 0 -> transpose + statistics ->
+        // sweep axis 1 with tau*V = tau*(a1[i]*a2[k] + b) in its epilogue.  One workspace per
+        // axis keeps each axis' line constants across steps.
+        void* wa = workspace;
+        void* wb = static_cast<char*>(workspace) + wsz;
+        if ((st = launch_transpose_stats(ctx, u, tmp, n, wa, s))) return st;
+        if ((st = launch_fast_f64(ctx, tmp, out, n, n, d1, tau, nullptr, 0, 0.0, nullptr, wa, wsz, kFastStatsGiven,
+                                  s)))
+            return st;
+        if ((st = launch_transpose_stats(ctx, out, tmp, n, wb, s))) return st;
+        const FastSepPot sep{a1, a2, b};
+        return launch_fast_f64(ctx, tmp, out, n, n, d2, tau, nullptr, 0, 0.0, nullptr, wb, wsz, kFastStatsGiven, s,
+                               nullptr, nullptr, (a1 && a2) ? &sep : nullptr);
     }
-    double* k1 = static_cast<double*>(ctx->scratch);
-    double* k2 = k1 + W;
-    int64_t* firsts = reinterpret_cast<int64_t*>(k2 + W);  // n entries per axis
-    double* drifts = reinterpret_cast<double*>(firsts + 2 * n);
-    std::vector<double> h1, h2;
-    int64_t f1, f2, arg;
-    double dl;
-    h1.resize(W);
-    h2.resize(W);
-    if (lob_kernel_mech_host(ctx, n, tau, drift1, h1.data(), &f1, &arg, &dl) ||
-        lob_kernel_mech_host(ctx, n, tau, drift2, h2.data(), &f2, &arg, &dl))
-        return set_error(ctx, LOB_INVALID_INPUT, "split_step_nd: invalid kernel parameters");
-    std::vector<int64_t> hf(static_cast<size_t>(2 * n));
-    for (int64_t i = 0; i < n; ++i) {
-        hf[i] = f1;
-        hf[n + i] = f2;
-    }
-    std::vector<double> hd(static_cast<size_t>(2 * n));
-    for (int64_t i = 0; i < n; ++i) {
-        hd[i] = drift1;
-        hd[n + i] = drift2;
-    }
-    // tables are tiny; synchronous upload keeps the host vectors' lifetime simple
-    LOB_CUDA_TRY(ctx, cudaMemcpyAsync(k1, h1.data(), W * sizeof(double), cudaMemcpyHostToDevice, s));
-    LOB_CUDA_TRY(ctx, cudaMemcpyAsync(k2, h2.data(), W * sizeof(double), cudaMemcpyHostToDevice, s));
-    LOB_CUDA_TRY(ctx, cudaMemcpyAsync(firsts, hf.data(), hf.size() * sizeof(int64_t),
-                                      cudaMemcpyHostToDevice, s));
-    LOB_CUDA_TRY(ctx, cudaMemcpyAsync(drifts, hd.data(), hd.size() * sizeof(double),
-                                      cudaMemcpyHostToDevice, s));
-    LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
     // axis 0: columns of u are rows of u^T
     if ((st = launch_transpose(ctx, u, tmp, n, s))) return st;
     if (engine == LOB_ENGINE_FAST) {
-        if ((st = launch_fast_f64(ctx, tmp, out, n, n, drifts, tau, nullptr, 0, 0.0, nullptr,
-                                  workspace, workspace_bytes, 0, s)))
+        if ((st = launch_fast_f64(ctx, tmp, out, n, n, d1, tau, nullptr, 0, 0.0, nullptr, workspace,
+                                  workspace_bytes, 0, s)))
             return st;
     } else {
-        if ((st = launch_direct_f64(ctx, tmp, out, n, n, k1, 0, firsts, nullptr, 0, s))) return st;
+        if ((st = launch_direct_f64(ctx, tmp, out, n, n, k1, 0, f1, nullptr, 0, s))) return st;
     }
     if ((st = launch_transpose(ctx, out, tmp, n, s))) return st;
     // axis 1: contiguous rows
     if (engine == LOB_ENGINE_FAST) {
-        if ((st = launch_fast_f64(ctx, tmp, out, n, n, drifts + n, tau, nullptr, 0, 0.0, nullptr,
-                                  workspace, workspace_bytes, 0, s)))
+        if ((st = launch_fast_f64(ctx, tmp, out, n, n, d2, tau, nullptr, 0, 0.0, nullptr, workspace,
+                                  workspace_bytes, 0, s)))
             return st;
     } else {
-        if ((st = launch_direct_f64(ctx, tmp, out, n, n, k2, 0, firsts + n, nullptr, 0, s)))
-            return st;
+        if ((st = launch_direct_f64(ctx, tmp, out, n, n, k2, 0, f2, nullptr, 0, s))) return st;
     }
     if (a1 && a2) return launch_potential2d(ctx, out, a1, a2, b, tau, n, s);
     return LOB_OK;

@@ -117,6 +117,11 @@ struct FastParams {
     int fsm_on;  // the epilogue produces decompose()'s FSM summaries for the next step's block count
     // the caller's current per-line inputs (checked against the carried line constants)
     const double* drift_arr;                      // mechanical mode
+    // separable potential (the 2-D split step's second sweep): tau*V(line, j) =
+    // tau * (sa1[line] * sa2[j] + sb) with the C++ expression's roundings (no FMA)
+    const double* sa1;
+    const double* sa2;
+    double sb;
     const double* ktab;                           // table mode: windows ...
     int64_t kstride;                              // ... their stride (0: shared) ...
     const int64_t* kfirst;                        // ... and first displacements
@@ -366,6 +371,70 @@ __global__ void __launch_bounds__(kNT) stats_kernel(const double* __restrict__ u
         tile_stats<false>(vals, Tl, j0, line, tile, p, b, sh, lut);
 }
 
+// The 2-D split step's transposes (proj/src/splitting.cpp:67-76 gathers strided lines) fused
+// with K2's input statistics of the transposed lines: dst = src^T for an n x n row-major
+// tensor, and for every line of dst (a column of src) the per-256-sample sub-tile slope
+// bounds and the line's u / slope extremes that tile_stats produces (same coarse keys), so
+// the following K2 sweep needs no statistics pass.  CTA = kTSL columns x one sub-tile of rows.
+constexpr int kTSL = 8;
+static_assert(kTSL == 8, "one warp per transposed line (256 threads)");
+__global__ void __launch_bounds__(256) transpose_stats_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                                              int64_t n, int64_t subs, double2* __restrict__ sub,
+                                                              unsigned long long* __restrict__ L) {
+    __shared__ double tile[kG + 2][kTSL + 1];  // rows r0-1 .. r0+len (periodic) x kTSL columns
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kTSL;
+    const int64_t q = blockIdx.y;
+    const int64_t r0 = q * kG;
+    const int len = static_cast<int>(min(static_cast<int64_t>(kG), n - r0));
+    {
+        // thread (row group, column): 32 rows of kTSL columns per pass, 64-byte row segments
+        const int c = threadIdx.x % kTSL, rg = threadIdx.x / kTSL;
+        const bool cok = c0 + c < n;
+        for (int r = rg; r < len + 2; r += 256 / kTSL) {
+            int64_t row = r0 - 1 + r;
+            row = row < 0 ? row + n : (row >= n ? row - n : row);
+            tile[r][c] = cok ? __ldg(src + row * n + c0 + c) : 0.0;
+        }
+    }
+    __syncthreads();
+    {
+        // warp w writes line c0 + w: contiguous, coalesced
+        const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (w < kTSL && c0 + w < n) {
+            double* d = dst + (c0 + w) * n + r0;
+            for (int i = lane; i < len; i += 32) d[i] = tile[i + 1][w];
+        }
+    }
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (w < kTSL && c0 + w < n) {
+        // slopes s(r0 - 1 .. r0 + len - 1) and values u(r0 .. r0 + len - 1) of line c0 + w
+        unsigned smn = 0xffffffffu, smx = 0u, umn = 0xffffffffu, umx = 0u;
+        for (int r = lane; r <= len; r += 32) {
+            const unsigned k = hkey(__dsub_rn(tile[r + 1][w], tile[r][w]));
+            smn = min(smn, k);
+            smx = max(smx, k);
+            if (r < len) {
+                const unsigned ku = hkey(tile[r + 1][w]);
+                umn = min(umn, ku);
+                umx = max(umx, ku);
+            }
+        }
+        smn = __reduce_min_sync(0xffffffffu, smn);
+        smx = __reduce_max_sync(0xffffffffu, smx);
+        umn = __reduce_min_sync(0xffffffffu, umn);
+        umx = __reduce_max_sync(0xffffffffu, umx);
+        if (lane == 0) {
+            const int64_t line = c0 + w;
+            sub[line * subs + q] = make_double2(hkey_lower(smn), hkey_upper(smx));
+            unsigned long long* Ll = L + line * 4;
+            atomicMin(Ll + 0, dkey(hkey_lower(umn)));
+            atomicMax(Ll + 1, dkey(hkey_upper(umx)));
+            atomicMin(Ll + 2, dkey(hkey_lower(smn)));
+            atomicMax(Ll + 3, dkey(hkey_upper(smx)));
+        }
+    }
+}
+
 // per-line drift from the K2 tiles' partial sums, in tile order; non-finite -> halt
 __global__ void drift_tiles_kernel(const double* __restrict__ dpart, int64_t lines, int64_t tiles, int64_t n,
                                    double* __restrict__ drift_out, int* __restrict__ halt, int step) {
@@ -504,19 +573,22 @@ __device__ __forceinline__ void smem_fmin_set(unsigned long long* addr, double c
     }
 }
 
-// One thread: TMA bulk copies of U(yc-1 .. yc+clen) (wrapped at the period,
-// 16-byte aligned even start) into ubuf, plus optionally vcnt v_d values.
+// One thread: TMA bulk copies of U(yc-1 .. yc+clen) (wrapped at the period as often as
+// needed: short lines; 16-byte aligned even start) into ubuf, plus optionally vcnt v_d values.
 __device__ __forceinline__ void issue_chunk(MainShared& S, const double* ul, int n, int yc, int clen,
                                             const double* vsrc, int vcnt) {
     const int bm = wrap_idx(yc - 1, n);
     const int sh = bm & 1;
     const int s0 = bm - sh;                    // even, in [0, n)
     const int cnt = (clen + 2 + sh + 1) & ~1;  // even count
-    const int c1 = min(cnt, n - s0);           // first segment (n even)
     fence_proxy_async();
     mbar_expect_tx(&S.mbar, static_cast<unsigned>(cnt + (vsrc ? vcnt : 0)) * 8u);
-    tma_load_1d(S.ubuf, ul + s0, static_cast<unsigned>(c1) * 8u, &S.mbar);
-    if (cnt > c1) tma_load_1d(S.ubuf + c1, ul, static_cast<unsigned>(cnt - c1) * 8u, &S.mbar);
+    // segments [s0, n), [0, n), ..., [0, rest): even lengths and offsets (n even)
+    for (int pos = s0, dst = 0; dst < cnt; pos = 0) {
+        const int seg = min(cnt - dst, n - pos);
+        tma_load_1d(S.ubuf + dst, ul + pos, static_cast<unsigned>(seg) * 8u, &S.mbar);
+        dst += seg;
+    }
     if (vsrc) tma_load_1d(S.vbuf, vsrc, static_cast<unsigned>(vcnt) * 8u, &S.mbar);
 }
 
@@ -891,9 +963,9 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
     const int jlo = j0 - 1;     // outputs evaluated: jlo .. jlo + jspan (unrolled)
     const int jspan = Tl + 2;
     const int jhi = jlo + jspan;
-    // TMA bulk copies (16-byte granules: even n, aligned rows; TMA) when the line is long
-    // enough for one conditional wrap per chunk; else a cooperative load
-    const bool big = TMA && n >= kC + 8;
+    // TMA bulk copies (16-byte granules: even n, aligned rows; TMA) for lines long enough that
+    // a chunk takes a few wrapped segments; else a cooperative load
+    const bool big = TMA && n >= 256;
     const double* ul = u + line * p.n;
     LineConst lc = lcs[line];
     // carried line constants (LOB_FAST_STATS_VALID) must describe the caller's current drift /
@@ -1145,7 +1217,11 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
                 }
             } else {
                 const int bm = wrap_idx(yc - 1, n);
-                for (int i = tid; i < clen + 2; i += kNT) S.ubuf[i] = CHAIN ? __ldcg(ul + (bm + i) % n) : __ldg(ul + (bm + i) % n);
+                for (int i = tid; i < clen + 2; i += kNT) {
+                    int y = bm + i;
+                    while (y >= n) y -= n;
+                    S.ubuf[i] = CHAIN ? __ldcg(ul + y) : __ldg(ul + y);
+                }
                 __syncthreads();
             }
             if (TAB && yc == ya && kstage) {
@@ -1177,6 +1253,13 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
     // Thread t owns outputs j0 + t + kNT*m (vals index 1 + t + kNT*m);
     // threads 0..2 also the halo outputs jlo, j0+Tl, j0+Tl+1.
     const double* tvl = tv ? tv + line * tv_stride : nullptr;
+    // tau*V at output j: the table, the separable descriptor, or 0 (x - 0 == x)
+    const double sa1l = p.sa1 ? __ldg(p.sa1 + line) : 0.0;
+    auto tvat = [&](int j) -> double {
+        if (tvl) return __ldg(tvl + j);
+        if (p.sa1) return __dmul_rn(tau, __dadd_rn(__dmul_rn(sa1l, __ldg(p.sa2 + j)), p.sb));
+        return 0.0;
+    };
     double* vals = S.ubuf;  // reuse: vals[i] = u^{n+1}(jlo + i), i = 0 .. Tl+2
     // direct scan of the full window (proj/tests/unit_scheme.cpp:184-190) for outputs no
     // interval reached (never, when the statistics describe u); one copy of the loop
@@ -1198,13 +1281,13 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
 #pragma unroll
         for (int m = 0; m < kPer; ++m) {
             const int i = 1 + tid + kNT * m;
-            tvv[m] = (tvl && (FULL || i <= Tl)) ? __ldg(tvl + j0 + i - 1) : 0.0;
+            tvv[m] = (FULL || i <= Tl) ? tvat(j0 + i - 1) : 0.0;
         }
         const int ih = tid == 0 ? 0 : Tl + tid;  // halo vals index (tid < 3)
         int jh = jlo + ih;
         jh += jh < 0 ? n : 0;
         jh -= jh >= n ? n : 0;
-        tvv[kPer] = (tvl && tid < 3) ? __ldg(tvl + jh) : 0.0;
+        tvv[kPer] = tid < 3 ? tvat(jh) : 0.0;
         double* ol = out + line * p.n + j0;
         unsigned miss = 0;
         // best - tv with tv = 0 when there is no potential: the same double (x - 0 == x, -0 - 0 == -0)
@@ -1234,7 +1317,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
             const int i = m < kPer ? 1 + tid + kNT * m : ih;
             const int j = m < kPer ? j0 + i - 1 : jh;
             const double best = scan(j);
-            const double o = __dsub_rn(best, tvl ? __ldg(tvl + j) : 0.0);
+            const double o = __dsub_rn(best, tvat(j));
             vals[P8(i)] = o;
             if (m < kPer) ol[i - 1] = o;
         }
@@ -1603,7 +1686,7 @@ static FastBuffers make_buffers(void* ws, int64_t lines, int64_t n, int64_t coun
 int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
                     const double* drift, double tau, const double* tv, int64_t tv_stride,
                     double eta, int64_t* blocks, void* workspace, size_t ws_bytes, int flags,
-                    cudaStream_t s, double* dpart, const FastTable* tab) {
+                    cudaStream_t s, double* dpart, const FastTable* tab, const FastSepPot* sep) {
     if (ws_bytes < fast_workspace_bytes(lines, n) || !workspace)
         return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_fast_f64: workspace too small");
     if (n > (1ll << 29)) return set_error(ctx, LOB_INVALID_INPUT, "fast: n too large");
@@ -1618,6 +1701,11 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     const int64_t nblk = lines * p.tiles;
     if (nblk > 0x7fffffffll) return set_error(ctx, LOB_INVALID_INPUT, "fast: grid too large");
     p.drift_arr = drift;
+    if (sep) {
+        p.sa1 = sep->a1;
+        p.sa2 = sep->a2;
+        p.sb = sep->b;
+    }
     if (tab) {
         p.ktab = tab->ktab;
         p.kstride = tab->stride;
@@ -1648,7 +1736,23 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     unsigned long long* diag =
         reinterpret_cast<unsigned long long*>(static_cast<char*>(workspace) + w.diag);
     LineConst* lcs = reinterpret_cast<LineConst*>(static_cast<char*>(workspace) + w.lc);
+    // statistics of u produced by the caller (fast_given_stats_buffers + a transpose kernel):
+    // the line constants are recomputed only for a new workspace (the device check catches a
+    // changed drift)
+    const bool given = flags & kFastStatsGiven;
+    if (given) {
+        flags |= LOB_FAST_STATS_VALID;
+        if (!ctx->ws_lc_valid[workspace]) {
+            line_setup_kernel<<<static_cast<unsigned>((lines + 127) / 128), 128, 0, s>>>(drift, lines, p, lcs);
+            LOB_CUDA_TRY(ctx, cudaMemsetAsync(diag, 0, kDiag * sizeof(unsigned long long), s));
+            ctx->launches += 1;
+            ctx->ws_lc_valid[workspace] = true;
+        }
+        flags &= ~LOB_FAST_CHAINED;
+        ctx->ws_chain[workspace] = 0;
+    }
     if (!(flags & LOB_FAST_STATS_VALID)) {
+        ctx->ws_lc_valid[workspace] = !tab;
         // per-line constants (valid while drift/tau/n (or the table) and the workspace are unchanged)
         if (tab)
             line_setup_tab_kernel<<<static_cast<unsigned>((lines * 32 + 127) / 128), 128, 0, s>>>(
@@ -1798,6 +1902,34 @@ int launch_block_counts(lob_ctx* ctx, const double* u, int64_t lines, int64_t n,
     ctx->launches += 3;
     cudaFreeAsync(ws, s);
     return cuda_status(ctx, cudaGetLastError(), "block counts");
+}
+
+int fast_given_stats_buffers(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n, double2** sub,
+                             unsigned long long** line_keys) {
+    if (ctx->ws_shape[workspace] != std::make_pair(lines, n)) {
+        ctx->ws_shape[workspace] = std::make_pair(lines, n);
+        ctx->ws_lc_valid[workspace] = false;
+    }
+    const FastBuffers b = make_buffers(workspace, lines, n, ctx->ws_counter[workspace]);
+    *sub = const_cast<double2*>(b.sub_in);
+    *line_keys = const_cast<unsigned long long*>(b.line_in);
+    return LOB_OK;
+}
+
+// dst = src^T (n x n) and the statistics of dst's lines for the next K2 call on `workspace`
+int launch_transpose_stats(lob_ctx* ctx, const double* src, double* dst, int64_t n, void* workspace,
+                           cudaStream_t s) {
+    double2* sub = nullptr;
+    unsigned long long* L = nullptr;
+    fast_given_stats_buffers(ctx, workspace, n, n, &sub, &L);
+    // line keys: minima start at ~0, maxima at 0 ([umin, umax, smin, smax] per line)
+    LOB_CUDA_TRY(ctx, cudaMemset2DAsync(L, 16, 0xff, 8, static_cast<size_t>(2 * n), s));
+    LOB_CUDA_TRY(ctx, cudaMemset2DAsync(L + 1, 16, 0x00, 8, static_cast<size_t>(2 * n), s));
+    const int64_t subs = (n + kG - 1) / kG;
+    dim3 grid(static_cast<unsigned>((n + kTSL - 1) / kTSL), static_cast<unsigned>(subs));
+    transpose_stats_kernel<<<grid, 256, 0, s>>>(src, dst, n, subs, sub, L);
+    ctx->launches += 1;
+    return cuda_status(ctx, cudaGetLastError(), "transpose_stats_kernel");
 }
 
 }  // namespace lob

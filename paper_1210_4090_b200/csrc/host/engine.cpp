@@ -421,6 +421,7 @@ TensorFn Engine::split_step_nd(const TensorFn& u, double t, const SplitSpec2D& s
     }
     size_t wsb = 0;
     lob_fast_workspace_bytes(n, n, &wsb);
+    wsb *= 2;  // one half per axis: the fused four-launch step
     DevBuf<unsigned char> ws(code == LOB_ENGINE_FAST ? wsb : 0);
     check_status(lob_split_step_2d_f64(ctx_, du.p, dout.p, dtmp.p, n, params.tau, spec.drift1, spec.drift2,
                                        hasv ? da1.p : nullptr, hasv ? da2.p : nullptr, b, code, ws.p, wsb,

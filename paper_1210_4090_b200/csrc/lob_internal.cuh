@@ -24,6 +24,8 @@ struct lob_ctx {
         int64_t dmin = 0, count = 0;
     };
     std::map<std::pair<int64_t, uint64_t>, VTab> vtabs;
+    // split-step axis inputs (kernel window, firsts, drifts) keyed by (n, tau bits, drift bits)
+    std::map<std::tuple<int64_t, uint64_t, uint64_t>, void*> split_axes;
     // fast-engine workspaces: which statistics buffer holds the current u
     std::map<const void*, int64_t> ws_counter;
     std::map<const void*, std::pair<int64_t, int64_t>> ws_shape;
@@ -31,6 +33,7 @@ struct lob_ctx {
     std::map<const void*, int64_t> ws_chain;         // K2 launches since the done counters were reset
     std::map<const void*, bool> ws_fsm_valid;        // the workspace holds FSM summaries of its last out
     std::map<const void*, const void*> ws_table;     // workspace -> window table of its line constants
+    std::map<const void*, bool> ws_lc_valid;         // the workspace holds line constants (mechanical)
     // K1 mode (LOB_DIRECT_SCREENED / LOB_DIRECT_PLAIN) and the screened kernel's
     // count of outputs swept in full fp64 (device counter, lazily allocated)
     int direct_mode = 0;
@@ -125,12 +128,32 @@ struct FastTable {
     int64_t stride;
     const int64_t* first;
 };
+// separable potential tau * (a1[line] * a2[j] + b) applied in K2's epilogue (device a1, a2)
+struct FastSepPot {
+    const double* a1;
+    const double* a2;
+    double b;
+};
+// launch_fast_f64 flag: the "in" statistics of u were written by the caller into the buffers
+// fast_given_stats_buffers returned for this workspace (no statistics pass, no pointer check)
+constexpr int kFastStatsGiven = 1 << 8;
 // dpart (nullable): per-tile sums of u^{n+1} - u^n for evolve's drift ([lines][fast_tiles(n)]);
-// tab (nullable): any convex window per line instead of the mechanical drift
+// tab (nullable): any convex window per line instead of the mechanical drift;
+// sep (nullable): a separable potential instead of the tv table
 int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
                     const double* drift, double tau, const double* tv, int64_t tv_stride,
                     double eta, int64_t* blocks, void* workspace, size_t ws_bytes, int flags,
-                    cudaStream_t s, double* dpart = nullptr, const FastTable* tab = nullptr);
+                    cudaStream_t s, double* dpart = nullptr, const FastTable* tab = nullptr,
+                    const FastSepPot* sep = nullptr);
+// the statistics buffers the next launch_fast_f64 call on `workspace` reads (for kFastStatsGiven):
+// per-256-sample sub-tile slope bounds [lines][subs] (double2: min, max) and per-line keys
+// [lines][4] (umin, umax, smin, smax as order-preserving keys; the caller resets them)
+int fast_given_stats_buffers(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n, double2** sub,
+                             unsigned long long** line_keys);
+// dst = src^T of an n x n tensor plus the statistics of dst's lines for the next
+// launch_fast_f64(..., kFastStatsGiven) on `workspace` (lines = n)
+int launch_transpose_stats(lob_ctx* ctx, const double* src, double* dst, int64_t n, void* workspace,
+                           cudaStream_t s);
 int64_t fast_tiles(int64_t n);
 int launch_drift_tiles(lob_ctx* ctx, const double* dpart, int64_t lines, int64_t n, double* drift_out, int* halt,
                        int step, cudaStream_t s);

@@ -8,13 +8,18 @@ from paper_1210_4090_b200 import api
 pytestmark = pytest.mark.gpu
 
 
+FUSED = 100  # pseudo-engine of these tests: ENGINE_FAST with the two-half workspace (fused step)
+
+
 def run_split(dev, u, tau, d1, d2, a1=None, a2=None, b=0.0, engine=api.ENGINE_DIRECT):
     import torch
     n = u.shape[0]
     du = torch.from_numpy(np.ascontiguousarray(u)).cuda()
     out = torch.empty_like(du)
     tmp = torch.empty_like(du)
-    ws = torch.empty(dev.fast_workspace_bytes(n, n), dtype=torch.uint8, device="cuda")
+    halves = 2 if engine == FUSED else 1
+    engine = api.ENGINE_FAST if engine == FUSED else engine
+    ws = torch.empty(halves * dev.fast_workspace_bytes(n, n), dtype=torch.uint8, device="cuda")
     ta1 = None if a1 is None else torch.from_numpy(a1).cuda()
     ta2 = None if a2 is None else torch.from_numpy(a2).cuda()
     dev.split_step_2d(du, out, tmp, tau, d1, d2, a1=ta1, a2=ta2, b=b, engine=engine, workspace=ws)
@@ -22,7 +27,7 @@ def run_split(dev, u, tau, d1, d2, a1=None, a2=None, b=0.0, engine=api.ENGINE_DI
     return out.cpu().numpy()
 
 
-@pytest.mark.parametrize("engine", [api.ENGINE_DIRECT, api.ENGINE_FAST])
+@pytest.mark.parametrize("engine", [api.ENGINE_DIRECT, api.ENGINE_FAST, FUSED])
 def test_split_16_vs_reference(dev, orc, ref, engine):
     # proj/tests/unit_splitting.cpp:103-121 / acceptance criterion 5
     rng = np.random.default_rng(42)
@@ -33,7 +38,7 @@ def test_split_16_vs_reference(dev, orc, ref, engine):
         assert np.array_equal(got, ref.split_step_2d(u, tau, 0.0, 0.5))
 
 
-@pytest.mark.parametrize("engine", [api.ENGINE_DIRECT, api.ENGINE_FAST])
+@pytest.mark.parametrize("engine", [api.ENGINE_DIRECT, api.ENGINE_FAST, FUSED])
 def test_split_c4_potential_vs_reference(dev, ref, engine):
     """C4's kinetics and potential V = cos(2 pi x1) cos(2 pi x2) + 0.2 sin(2 pi t) at t+tau."""
     n, tau, t = 64, 0.05, 0.35
@@ -56,7 +61,7 @@ def test_split_c4_full_size_vs_oracle(dev, orc):
     k2, f2, _, _ = orc.kernel(n, tau, -0.7)
     tv = api.tau_v(np.add(np.multiply(a[:, None], a[None, :]), b), tau)
     want = orc.split2d(u, k1, f1, k2, f2, tv=tv)
-    for engine in (api.ENGINE_DIRECT, api.ENGINE_FAST):
+    for engine in (api.ENGINE_DIRECT, api.ENGINE_FAST, FUSED):
         got = run_split(dev, u, tau, 0.3, -0.7, a1=a, a2=a, b=b, engine=engine)
         assert np.array_equal(got, want), engine
 
@@ -74,7 +79,7 @@ def test_split_separable_data_stays_separable(dev, orc):
     assert np.max(np.abs(got - (f1[:, None] + g1[None, :]))) <= 1e-13 * np.max(np.abs(got))
 
 
-@pytest.mark.parametrize("engine", [api.ENGINE_DIRECT, api.ENGINE_FAST])
+@pytest.mark.parametrize("engine", [api.ENGINE_DIRECT, api.ENGINE_FAST, FUSED])
 @pytest.mark.parametrize("n", [100, 513])
 def test_split_non_tile_multiple_sizes(dev, orc, ref, engine, n):
     """n not a multiple of the 32x32 transpose tile (and odd): == reference at 100, == oracle at 513."""
