@@ -208,6 +208,14 @@ int lob_split_step_nd_window_f64(lob_ctx* ctx, const double* u, double* out, dou
 int lob_potential2d_rows_f64(lob_ctx* ctx, double* out, int64_t rows, int64_t n, const double* a1,
                              const double* a2, double b, double tau, void* stream);
 
+/* The multi-GPU split step's all-to-all exchange of row slabs (paper_1210_4090_b200/dist.py;
+ * rank r holds rows [r*b, (r+1)*b) of an n x n tensor, n = b*world):
+ * pack:   send[q][c][i] = x[i][q*b + c]  (block q goes to rank q; the slab transposed),
+ * unpack: y[c][p*b + i] = recv[p][c][i]  (this rank's slab of the transposed tensor).
+ * Device buffers of b*n doubles, asynchronous on `stream`. */
+int lob_slab_pack_f64(lob_ctx* ctx, const double* x, int64_t b, int64_t world, double* send, void* stream);
+int lob_slab_unpack_f64(lob_ctx* ctx, const double* recv, int64_t b, int64_t world, double* y, void* stream);
+
 /* Device-resident batched evolve (proj/src/scheme.cpp:208-272): `steps`
  * steps of `lines` periodic lines with a shared, time-independent tv.  u is
  * updated in place (double-buffered against `scratch`, n*lines doubles).

@@ -60,6 +60,8 @@ SIGNATURES = {
                                           POINTER(c_int64), POINTER(c_int64)]),
     "lob_minplus_fast_window_f64": (c_int, [_P, _P, _P, c_int64, c_int64, _P, c_int64, _P, c_double, _P, c_int64,
                                             c_double, _P, _P, c_size_t, c_int, _P]),
+    "lob_slab_pack_f64": (c_int, [_P, _P, c_int64, c_int64, _P, _P]),
+    "lob_slab_unpack_f64": (c_int, [_P, _P, c_int64, c_int64, _P, _P]),
     "lob_fast_diagnostics": (c_int, [_P, _P, c_int64, c_int64, _P]),
     "lob_block_counts": (c_int, [_P, _P, c_int64, c_int64, c_double, _P, _P]),
     "lob_bench_fp64": (c_int, [_P, POINTER(c_double), POINTER(c_double), POINTER(c_double)]),

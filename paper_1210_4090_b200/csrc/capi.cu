@@ -310,6 +310,19 @@ int lob_split_step_2d_f64(lob_ctx* ctx, const double* u, double* out, double* tm
     return LOB_OK;
 }
 
+int lob_slab_pack_f64(lob_ctx* ctx, const double* x, int64_t b, int64_t world, double* send, void* stream) {
+    if (!ctx || !x || !send || b < 1 || world < 1 || x == send)
+        return set_error(ctx, LOB_INVALID_INPUT, "lob_slab_pack_f64: invalid arguments");
+    // send[q][c][i] = x[i][q*b + c]: the b x n slab transposed (= world blocks of b x b)
+    return launch_transpose_batched(ctx, x, send, 1, b, b * world, static_cast<cudaStream_t>(stream));
+}
+
+int lob_slab_unpack_f64(lob_ctx* ctx, const double* recv, int64_t b, int64_t world, double* y, void* stream) {
+    if (!ctx || !recv || !y || b < 1 || world < 1 || recv == y)
+        return set_error(ctx, LOB_INVALID_INPUT, "lob_slab_unpack_f64: invalid arguments");
+    return launch_slab_unpack(ctx, recv, y, b, world, static_cast<cudaStream_t>(stream));
+}
+
 int lob_evolve_f64(lob_ctx* ctx, double* u, double* scratch, int64_t lines, int64_t n,
                    const double* drift, double tau, const double* tv, int64_t tv_stride,
                    double eta, int engine, int64_t steps, double* step_drift,

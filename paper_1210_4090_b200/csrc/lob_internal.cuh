@@ -186,6 +186,7 @@ int launch_transpose(lob_ctx* ctx, const double* src, double* dst, int64_t n, cu
 int launch_transpose_batched(lob_ctx* ctx, const double* src, double* dst, int64_t A, int64_t L, int64_t B,
                              cudaStream_t s);
 int launch_sub_table(lob_ctx* ctx, double* out, const double* tv, int64_t count, cudaStream_t s);
+int launch_slab_unpack(lob_ctx* ctx, const double* recv, double* y, int64_t b, int64_t world, cudaStream_t s);
 int launch_potential2d(lob_ctx* ctx, double* out, const double* a1, const double* a2, double b,
                        double tau, int64_t n, cudaStream_t s, int64_t rows = -1);
 int launch_drift(lob_ctx* ctx, const double* nxt, const double* cur, int64_t lines, int64_t n,

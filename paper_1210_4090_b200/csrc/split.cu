@@ -102,6 +102,16 @@ __global__ void __launch_bounds__(256) transpose_batched_kernel(const double* __
     }
 }
 
+// the multi-GPU exchange's receive side: y[c][p*b + i] = recv[p][c][i] (world blocks of b x b)
+__global__ void slab_unpack_kernel(const double* __restrict__ recv, double* __restrict__ y, int64_t b, int64_t world) {
+    const int64_t n = b * world;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < b * n;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t c = e / n, r = e - c * n, p = r / b, i = r - p * b;
+        y[e] = recv[(p * b + c) * b + i];
+    }
+}
+
 // out[i] -= tv[i] (tau*V of every grid point, rounded on the host): one IEEE subtraction
 __global__ void sub_table_kernel(double* __restrict__ out, const double* __restrict__ tv, int64_t count) {
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
@@ -118,6 +128,13 @@ int launch_transpose_batched(lob_ctx* ctx, const double* src, double* dst, int64
     transpose_batched_kernel<<<grid, 256, 0, s>>>(src, dst, A, L, B);
     ctx->launches += 1;
     return cuda_status(ctx, cudaGetLastError(), "transpose_batched_kernel");
+}
+
+int launch_slab_unpack(lob_ctx* ctx, const double* recv, double* y, int64_t b, int64_t world, cudaStream_t s) {
+    const unsigned g = static_cast<unsigned>(std::min<int64_t>((b * b * world + 255) / 256, 148 * 32));
+    slab_unpack_kernel<<<g, 256, 0, s>>>(recv, y, b, world);
+    ctx->launches += 1;
+    return cuda_status(ctx, cudaGetLastError(), "slab_unpack_kernel");
 }
 
 int launch_sub_table(lob_ctx* ctx, double* out, const double* tv, int64_t count, cudaStream_t s) {

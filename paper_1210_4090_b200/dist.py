@@ -35,10 +35,15 @@ def _world(group):
     return dist.get_world_size(group), dist.get_rank(group)
 
 
-def transpose_slabs(x, group=None):
+def transpose_slabs(x, group=None, dev: Device | None = None, host_staged: bool = False):
     """x: this rank's row slab (b x n, contiguous) of a row-partitioned n x n matrix X
     (b = n / world).  Returns this rank's row slab of X^T:
-    y[c][p*b + i] = X[p*b + i][r*b + c]."""
+    y[c][p*b + i] = X[p*b + i][r*b + c].
+
+    CUDA tensors with `dev`: the send buffer is packed and the receive buffer unpacked by the
+    library's kernels (lob_slab_pack_f64 / lob_slab_unpack_f64: one coalesced pass each) and
+    the exchange is NCCL's all_to_all_single over NVLink/NVSwitch; host_staged=True moves the
+    packed blocks through host memory instead (a gloo group: the multi-process test on one GPU)."""
     import torch
     import torch.distributed as dist
 
@@ -46,18 +51,40 @@ def transpose_slabs(x, group=None):
     b, n = x.shape
     if b * world != n:
         raise InvalidInput("transpose_slabs: the row slabs must partition the square evenly")
-    if world == 1:
-        return x.t().contiguous()
-    # block q of the send buffer = X[rank rows][q cols]^T : send[q][c][i] = x[i][q*b + c]
-    send = x.view(b, world, b).permute(1, 2, 0).contiguous()
-    recv = torch.empty_like(send)
-    dist.all_to_all_single(recv, send, group=group)
+    on_dev = dev is not None and x.is_cuda
+    if on_dev:
+        send = torch.empty_like(x)
+        _capi.check(dev.lib.lob_slab_pack_f64(dev.ctx, _ptr(x), b, world, _ptr(send), _stream_ptr(None)), dev.ctx,
+                    "lob_slab_pack_f64")
+        if world == 1:
+            return send.view(b, n)
+    else:
+        if world == 1:
+            return x.t().contiguous()
+        # block q of the send buffer = X[rank rows][q cols]^T : send[q][c][i] = x[i][q*b + c]
+        send = x.view(b, world, b).permute(1, 2, 0).contiguous()
+    if host_staged:
+        if on_dev:
+            torch.cuda.synchronize()
+        hs = send.cpu()
+        hr = torch.empty_like(hs)
+        dist.all_to_all_single(hr, hs, group=group)
+        recv = hr.to(x.device)
+    else:
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(recv, send, group=group)
     # recv[p][c][i] = X[p*b + i][rank*b + c]  ->  y[c][p*b + i]
-    return recv.permute(1, 0, 2).reshape(b, n).contiguous()
+    if on_dev:
+        y = torch.empty_like(x)
+        _capi.check(dev.lib.lob_slab_unpack_f64(dev.ctx, _ptr(recv), b, world, _ptr(y), _stream_ptr(None)), dev.ctx,
+                    "lob_slab_unpack_f64")
+        return y
+    return recv.view(world, b, b).permute(1, 0, 2).reshape(b, n).contiguous()
 
 
 def split_step_2d_dist(dev: Device, u_slab, tau: float, drift1: float, drift2: float, a1=None, a2=None,
-                       b: float = 0.0, engine: int = ENGINE_DIRECT, group=None, workspaces=None):
+                       b: float = 0.0, engine: int = ENGINE_DIRECT, group=None, workspaces=None,
+                       host_staged: bool = False):
     """One split step of the row-partitioned periodic n x n tensor (this rank's slab,
     rows [r*b, (r+1)*b) as a torch CUDA tensor).  a1 (length n, the x1 factor of the whole
     grid) and a2 (length n) describe V = a1(x1) a2(x2) + b at the step's sampling time,
@@ -88,9 +115,9 @@ def split_step_2d_dist(dev: Device, u_slab, tau: float, drift1: float, drift2: f
             dev.direct_f64(src, out, kt, fr)
         return out
 
-    t = transpose_slabs(u_slab, group)          # slab of U^T: columns of U as rows
-    t = sweep(t, drift1, "axis0")               # axis 0 (kernel 1)
-    v = transpose_slabs(t, group)               # back to rows
+    t = transpose_slabs(u_slab, group, dev, host_staged)  # slab of U^T: columns of U as rows
+    t = sweep(t, drift1, "axis0")                          # axis 0 (kernel 1)
+    v = transpose_slabs(t, group, dev, host_staged)       # back to rows
     w = sweep(v, drift2, "axis1")               # axis 1 (kernel 2)
     if a1 is not None:
         a1d = torch.as_tensor(np.ascontiguousarray(a1[rank * bl:(rank + 1) * bl]), device=w.device)

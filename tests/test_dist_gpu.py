@@ -34,3 +34,72 @@ def test_dist_split_step_equals_single_gpu(dev, engine, n):
         v = split_step_2d_dist(dev, v, tau, d1, d2, a1=a1, a2=a2, b=b, engine=engine, workspaces=wss)
         torch.cuda.synchronize()
         assert torch.equal(u, v), step
+
+
+def _slab_worker(rank, world, port, q, n, engine, steps):
+    """One rank of the row-partitioned split step on the shared GPU; the all-to-all exchange is
+    host-staged over gloo (the ranks' kernels never wait on one another)."""
+    import os
+    import sys
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1210_4090_b200 import api
+    from paper_1210_4090_b200.dist import split_step_2d_dist
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = api.Device(0)
+    tau, d1, d2 = 0.01, 0.3, -0.7
+    u0 = api.gen_c4_u0(n)
+    a = api.gen_cos(n)
+    b = n // world
+    v = torch.from_numpy(np.ascontiguousarray(u0[rank * b:(rank + 1) * b])).cuda()
+    wss = {}
+    for step in range(steps):
+        v = split_step_2d_dist(dev, v, tau, d1, d2, a1=a, a2=a, b=api.c4_time_term((step + 1) * tau),
+                               engine=engine, workspaces=wss, host_staged=True)
+    torch.cuda.synchronize()
+    q.put((rank, v.cpu().numpy()))
+    dist.destroy_process_group()
+    dev.close()
+
+
+@pytest.mark.parametrize("engine", [api.ENGINE_FAST, api.ENGINE_DIRECT])
+def test_dist_split_step_two_ranks_equals_single_gpu(dev, engine):
+    """world_size 2: two processes, each its row slab on the one GPU, the two all-to-all
+    transposes per step host-staged over gloo (pack / unpack by the library's kernels); after
+    3 steps the stacked slabs == the single-GPU lob_split_step_2d_f64 chain (C4's kinetics and
+    potential, n = 256)."""
+    import torch
+    import torch.multiprocessing as mp
+
+    n, steps, world = 256, 3, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29611 + engine
+    procs = [ctx.Process(target=_slab_worker, args=(r, world, port, q, n, engine, steps)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in procs:
+        r, slab = q.get(timeout=300)
+        res[r] = slab
+    for p in procs:
+        p.join(timeout=60)
+    got = np.concatenate([res[r] for r in range(world)])
+    tau = 0.01
+    u = torch.from_numpy(api.gen_c4_u0(n)).cuda()
+    out, tmp = torch.empty_like(u), torch.empty_like(u)
+    a = torch.from_numpy(api.gen_cos(n)).cuda()
+    ws = torch.empty(2 * dev.fast_workspace_bytes(n, n), dtype=torch.uint8, device="cuda")
+    for step in range(steps):
+        dev.split_step_2d(u, out, tmp, tau, 0.3, -0.7, a1=a, a2=a, b=api.c4_time_term((step + 1) * tau),
+                          engine=engine, workspace=ws)
+        u, out = out, u
+    torch.cuda.synchronize()
+    assert np.array_equal(got, u.cpu().numpy())
