@@ -330,6 +330,15 @@ def run_b200(args, world, rank, local):
     e2e["copy_bound"] = {"value": bound, "unit": "updates/s", "frac": e2e["value"] / bound,
                          "what": "concurrent pinned H2D + D2H of one step's state, no compute"}
     del dbuf_in, dbuf_out, a, b, ws
+    # e2e through the C++ API a reference user calls (Engine::step_fully_discrete, one pageable
+    # std::vector line per call, V evaluated per point on the host like the reference)
+    exe = os.path.join(ROOT, "tests", "cpp", "test_engine")
+    if world == 1 and os.path.exists(exe):
+        try:
+            r = subprocess.run([exe, "--bench", "16"], capture_output=True, text=True, timeout=300)
+            e2e["cpp_api_pageable"] = json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception as exc:  # reported, not fatal
+            e2e["cpp_api_pageable"] = {"error": str(exc)[:200]}
     st.clear()
     torch.cuda.empty_cache()
 

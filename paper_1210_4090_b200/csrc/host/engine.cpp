@@ -124,71 +124,130 @@ void validate(const SchemeParams& p) {
                            " violates the bound epsilon/tau < h0 = " + std::to_string(p.h0));
 }
 
+// Device state kept between calls: grow-only buffers, the K2 workspace, and the last
+// output still on the device (so a step whose input is the previous step's output uploads
+// nothing and keeps the fast engine's statistics: LOB_FAST_STATS_VALID).
+struct Engine::StepCache {
+    cudaStream_t stream = nullptr;
+    void *u = nullptr, *out = nullptr, *ktab = nullptr, *first = nullptr, *drift = nullptr, *tv = nullptr,
+         *blocks = nullptr, *ws = nullptr;
+    size_t cap[8] = {};
+    std::vector<double> last_out, last_window;  // host copies of the device `u` and window
+    int64_t last_n = -1;
+    int last_code = -1;
+    bool resident = false;  // the device `u` buffer holds last_out
+    void* get(int slot, void*& p, size_t bytes) {
+        if (bytes > cap[slot]) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            check_cuda(cudaMalloc(&p, bytes), "cudaMalloc");
+            cap[slot] = bytes;
+        }
+        return p;
+    }
+    ~StepCache() {
+        for (void* p : {u, out, ktab, first, drift, tv, blocks, ws})
+            if (p) cudaFree(p);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
 Engine::Engine(int device) {
     const int st = lob_ctx_create(device, &ctx_);
     if (st != LOB_OK)
         throw std::runtime_error("laxol_b200: no usable CUDA device (status " + std::to_string(st) +
                                  "); there is no CPU fallback");
+    cache_ = std::make_unique<StepCache>();
+    check_cuda(cudaStreamCreateWithFlags(&cache_->stream, cudaStreamNonBlocking), "cudaStreamCreate");
 }
 
-Engine::~Engine() { lob_ctx_destroy(ctx_); }
+Engine::~Engine() {
+    cache_.reset();
+    lob_ctx_destroy(ctx_);
+}
+
+// One periodic step: min-plus with the window (+ tau*V from `tv`, fused on the device).
+GridFn Engine::periodic_step(const GridFn& u, const KernelWindow& kernel, double eta, ConvEngine engine,
+                             const std::vector<double>* tv, int64_t* blocks) {
+    StepCache& C = *cache_;
+    const int64_t n = kernel.n_space;
+    if (static_cast<int64_t>(u.n()) != n) throw InvalidInput("kinetic_convolve: periodic u must hold one unit period");
+    int code = engine_code(engine, eta);
+    const size_t nb = static_cast<size_t>(n) * sizeof(double), wb = kernel.window.size() * sizeof(double);
+    // the input is the previous call's output (same values, same window and engine): already on the
+    // device, with its statistics
+    const bool same_window = C.last_window.size() == kernel.window.size() &&
+                             std::memcmp(C.last_window.data(), kernel.window.data(), wb) == 0;
+    const bool resident = C.resident && C.last_n == n && C.last_code == code && same_window &&
+                          std::memcmp(C.last_out.data(), u.values.data(), nb) == 0;
+    double* du = static_cast<double*>(C.get(0, C.u, nb));
+    double* dout = static_cast<double*>(C.get(1, C.out, nb));
+    if (!resident) check_cuda(cudaMemcpyAsync(du, u.values.data(), nb, cudaMemcpyHostToDevice, C.stream), "H2D");
+    if (!same_window) {
+        C.last_window = kernel.window;
+        check_cuda(cudaMemcpyAsync(C.get(2, C.ktab, wb), kernel.window.data(), wb, cudaMemcpyHostToDevice, C.stream),
+                   "H2D");
+        check_cuda(cudaMemcpyAsync(C.get(3, C.first, 8), &kernel.first, 8, cudaMemcpyHostToDevice, C.stream), "H2D");
+        check_cuda(cudaMemcpyAsync(C.get(4, C.drift, 8), &kernel.drift, 8, cudaMemcpyHostToDevice, C.stream), "H2D");
+        check_cuda(cudaStreamSynchronize(C.stream), "H2D");  // the host copies above are stack/temporary
+    }
+    const double* dtv = nullptr;
+    if (tv) {
+        dtv = static_cast<double*>(C.get(5, C.tv, nb));
+        check_cuda(cudaMemcpyAsync(const_cast<double*>(dtv), tv->data(), nb, cudaMemcpyHostToDevice, C.stream), "H2D");
+    }
+    int64_t* db = static_cast<int64_t*>(C.get(6, C.blocks, 8));
+    const double* dk = static_cast<const double*>(C.ktab);
+    const int64_t* df = static_cast<const int64_t*>(C.first);
+    if (code == LOB_ENGINE_FAST) {
+        size_t wsb = 0;
+        lob_fast_workspace_bytes(1, n, &wsb);
+        void* ws = C.get(7, C.ws, wsb);
+        const int flags = resident ? LOB_FAST_STATS_VALID : 0;
+        if (kernel.mechanical)
+            check_status(lob_minplus_fast_f64(ctx_, du, dout, 1, n, static_cast<const double*>(C.drift), kernel.tau,
+                                              dtv, 0, eta, blocks ? db : nullptr, ws, wsb, flags, C.stream),
+                         ctx_, "kinetic_convolve");
+        else  // any convex window (tabulated conjugates): the window engine
+            check_status(lob_minplus_fast_window_f64(ctx_, du, dout, 1, n, dk, 0, df, kernel.tau, dtv, 0, eta,
+                                                     blocks ? db : nullptr, ws, wsb, flags, C.stream),
+                         ctx_, "kinetic_convolve");
+    } else if (code == LOB_ENGINE_RELAXED) {
+        size_t wsb = 0;
+        lob_relaxed_workspace_bytes(1, n, &wsb);
+        void* ws = C.get(7, C.ws, std::max(wsb, C.cap[7]));
+        check_status(lob_minplus_relaxed_f64(ctx_, du, dout, 1, n, dk, 0, df, dtv, 0, eta, blocks ? db : nullptr, ws,
+                                             C.cap[7], C.stream),
+                     ctx_, "kinetic_convolve");
+    } else {
+        check_status(lob_minplus_direct_f64(ctx_, du, dout, 1, n, dk, 0, df, dtv, 0, C.stream), ctx_,
+                     "kinetic_convolve");
+        if (blocks) check_status(lob_block_counts(ctx_, du, 1, n, eta, db, C.stream), ctx_, "block counts");
+    }
+    std::vector<double> out(static_cast<size_t>(n) + 1);
+    check_cuda(cudaMemcpyAsync(out.data(), dout, nb, cudaMemcpyDeviceToHost, C.stream), "D2H");
+    int64_t bh = 0;
+    if (blocks) check_cuda(cudaMemcpyAsync(&bh, db, 8, cudaMemcpyDeviceToHost, C.stream), "D2H");
+    check_cuda(cudaStreamSynchronize(C.stream), "kinetic_convolve");
+    out[n] = out[0];
+    if (blocks) *blocks = bh;
+    // the output becomes the next call's resident input (the fast engine reads u_{k+1}'s
+    // statistics written by this call's epilogue; the K2 workspace tracks pointers, so
+    // swap the buffers rather than copying)
+    std::swap(C.u, C.out);
+    std::swap(C.cap[0], C.cap[1]);
+    C.last_out.assign(out.begin(), out.begin() + n);
+    C.last_n = n;
+    C.last_code = code;
+    C.resident = true;
+    return GridFn{std::move(out), u.step, u.origin, true};
+}
 
 GridFn Engine::kinetic_convolve(const GridFn& u, const KernelWindow& kernel, double eta,
                                 ConvEngine engine, int64_t* blocks) {
     const int64_t n = kernel.n_space;
-    int code = engine_code(engine, eta);
-    // K2 walks the mechanical conjugate; for a tabulated window the fast engine is the
-    // reference's conv_fast itself (exact at eta == 0), which the relaxed engine reproduces
-    if (code == LOB_ENGINE_FAST && !kernel.mechanical) code = LOB_ENGINE_RELAXED;
-    if (u.periodic) {
-        if (static_cast<int64_t>(u.n()) != n)
-            throw InvalidInput("kinetic_convolve: periodic u must hold one unit period");
-        DevBuf<double> du(n), dout(n);
-        du.upload(u.values.data(), n);
-        int64_t b = 0;
-        if (code == LOB_ENGINE_FAST) {
-            size_t wsb = 0;
-            lob_fast_workspace_bytes(1, n, &wsb);
-            DevBuf<unsigned char> ws(wsb);
-            DevBuf<double> dd(1);
-            dd.upload(&kernel.drift, 1);
-            DevBuf<int64_t> db(1);
-            check_status(lob_minplus_fast_f64(ctx_, du.p, dout.p, 1, n, dd.p, kernel.tau, nullptr, 0, eta,
-                                              db.p, ws.p, wsb, 0, nullptr),
-                         ctx_, "kinetic_convolve");
-            db.download(&b, 1);
-        } else if (code == LOB_ENGINE_RELAXED) {
-            DevBuf<double> dk(kernel.window.size());
-            dk.upload(kernel.window.data(), kernel.window.size());
-            DevBuf<int64_t> df(1), db(1);
-            df.upload(&kernel.first, 1);
-            size_t wsb = 0;
-            lob_relaxed_workspace_bytes(1, n, &wsb);
-            DevBuf<unsigned char> ws(wsb);
-            check_status(lob_minplus_relaxed_f64(ctx_, du.p, dout.p, 1, n, dk.p, 0, df.p, nullptr, 0, eta, db.p, ws.p,
-                                                 wsb, nullptr),
-                         ctx_, "kinetic_convolve");
-            db.download(&b, 1);
-        } else {
-            DevBuf<double> dk(kernel.window.size());
-            dk.upload(kernel.window.data(), kernel.window.size());
-            DevBuf<int64_t> df(1);
-            df.upload(&kernel.first, 1);
-            check_status(lob_minplus_direct_f64(ctx_, du.p, dout.p, 1, n, dk.p, 0, df.p, nullptr, 0, nullptr),
-                         ctx_, "kinetic_convolve");
-            if (blocks) {
-                DevBuf<int64_t> db(1);
-                check_status(lob_block_counts(ctx_, du.p, 1, n, eta, db.p, nullptr), ctx_, "block counts");
-                db.download(&b, 1);
-            }
-        }
-        check_cuda(cudaDeviceSynchronize(), "kinetic_convolve");
-        std::vector<double> out(static_cast<size_t>(n) + 1);
-        dout.download(out.data(), n);
-        out[n] = out[0];
-        if (blocks) *blocks = b;
-        return GridFn{std::move(out), u.step, u.origin, true};
-    }
+    (void)engine_code(engine, eta);  // rejects the CPU engines
+    if (u.periodic) return periodic_step(u, kernel, eta, engine, nullptr, blocks);
     // windowed domain: direct engine (proj/src/scheme.cpp:135-144)
     const int64_t m = static_cast<int64_t>(u.size());
     DevBuf<double> du(m), dout(m), dk(kernel.window.size());
@@ -233,14 +292,20 @@ GridFn Engine::step_fully_discrete(const GridFn& u, double t, const Potential& V
                                    const SchemeParams& params, const KernelWindow& kernel,
                                    ConvEngine engine, StepStats* stats) {
     check_u_grid(u, params, "step_fully_discrete");
+    const double tt = potential_time(t, params);
+    const std::size_t fund = u.periodic ? u.n() : u.size();
+    // out[j] -= tau*V(t', x_{j mod n}) (proj/src/scheme.cpp:156-162): tau*V rounded on the host,
+    // subtracted in the kernel's epilogue (periodic) or here (windowed)
+    const std::vector<double> tv = tabulate_tv(u, V, tt, params.tau, fund);
     int64_t blocks = 0;
+    if (u.periodic) {
+        GridFn out = periodic_step(u, kernel, params.eta, engine, &tv, &blocks);
+        if (stats) stats->block_count = blocks;
+        return out;
+    }
     GridFn out = kinetic_convolve(u, kernel, params.eta, engine, &blocks);
     if (stats) stats->block_count = blocks;
-    const double tt = potential_time(t, params);
-    // out[j] -= tau*V(t', x_{j mod n}) (proj/src/scheme.cpp:156-162)
-    const std::size_t fund = u.periodic ? u.n() : u.size();
-    const std::vector<double> tv = tabulate_tv(u, V, tt, params.tau, fund);
-    for (std::size_t j = 0; j < out.size(); ++j) out.values[j] -= tv[u.periodic ? j % fund : j];
+    for (std::size_t j = 0; j < out.size(); ++j) out.values[j] -= tv[j];
     return out;
 }
 

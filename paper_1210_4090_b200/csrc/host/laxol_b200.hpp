@@ -11,6 +11,7 @@
 
 #include <cstdint>
 #include <functional>
+#include <memory>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -220,7 +221,11 @@ public:
     lob_ctx* ctx() const { return ctx_; }
 
 private:
+    struct StepCache;
+    GridFn periodic_step(const GridFn& u, const KernelWindow& kernel, double eta, ConvEngine engine,
+                         const std::vector<double>* tv, int64_t* blocks);
     lob_ctx* ctx_ = nullptr;
+    std::unique_ptr<StepCache> cache_;  // device buffers and the resident last output
 };
 
 }  // namespace laxol_b200

@@ -4,6 +4,9 @@
 // independent brute-force oracles.  Needs a CUDA device; prints one
 // PASS/FAIL line per check and exits non-zero on any failure.
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
+#include <string>
 #include <cmath>
 #include <cstdio>
 #include <limits>
@@ -52,9 +55,77 @@ static double def_min(const GridFn& u, const KernelWindow& k, int64_t j) {
     return want;
 }
 
-int main() {
+// e2e through the C++ API a reference user calls: Engine::step_fully_discrete on pageable
+// std::vector lines of C2 (N = 65536, tau = 0.02, per-line drift, V = cos 2 pi x + 0.5 cos(4 pi x + 1)),
+// the reference's loop order (every step, every line).  Prints one JSON object.
+static int bench(int lines, int steps) {
+    Engine eng(0);
+    const int n = 65536;
+    const double tau = 0.02;
+    const SchemeParams p = params_of(n, tau);
+    constexpr double kTwoPi = 2.0 * 3.14159265358979323846;
+    Potential V;
+    V.fn = [](double, double x) { return std::cos(kTwoPi * x) + 0.5 * std::cos(2.0 * kTwoPi * x + 1.0); };
+    std::vector<KernelWindow> ks;
+    std::vector<GridFn> us;
+    for (int l = 0; l < lines; ++l) {
+        const double drift = -2.0 + 4.0 * (l * (255.0 / std::max(1, lines - 1))) / 255.0;
+        ks.push_back(build_kernel_mech(n, tau, drift));
+        us.push_back(make_periodic(std::vector<double>(n, 0.0), p.epsilon()));
+    }
+    auto run = [&](bool line_major) {
+        const auto t0 = std::chrono::steady_clock::now();
+        if (line_major) {
+            for (int l = 0; l < lines; ++l)
+                for (int k = 0; k < steps; ++k)
+                    us[l] = eng.step_fully_discrete(us[l], k * tau, V, p, ks[l], ConvEngine::GpuFast);
+        } else {
+            for (int k = 0; k < steps; ++k)
+                for (int l = 0; l < lines; ++l)
+                    us[l] = eng.step_fully_discrete(us[l], k * tau, V, p, ks[l], ConvEngine::GpuFast);
+        }
+        return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    };
+    run(false);  // warm
+    const double ts = run(false), tl = run(true);
+    const double upd = static_cast<double>(lines) * steps * n;
+    std::printf("{\"api\": \"laxol_b200::Engine::step_fully_discrete (pageable std::vector, one line per call)\", "
+                "\"lines\": %d, \"n\": %d, \"steps\": %d, \"step_major_updates_per_s\": %.6g, "
+                "\"line_major_updates_per_s\": %.6g}\n",
+                lines, n, steps, upd / ts, upd / tl);
+    return 0;
+}
+
+int main(int argc, char** argv) {
+    if (argc > 1 && std::string(argv[1]) == "--bench") return bench(argc > 2 ? std::atoi(argv[2]) : 16, 5);
     Engine eng(0);
     std::mt19937_64 rng(39);
+    // 0. consecutive steps through the resident device state (the output of one call is the
+    // next call's input: no upload, the fast engine's statistics carried) == a fresh engine's
+    // step from the same host input, both engines, and a foreign input in between
+    {
+        const int n = 1024;
+        const SchemeParams p = params_of(n, 0.05);
+        const KernelWindow k = build_kernel_mech(n, 0.05, 0.5);
+        Potential V;
+        V.fn = [](double, double x) { return std::cos(6.283185307179586 * x); };
+        GridFn u = random_periodic(rng, n, 0.01, p.epsilon());
+        bool ok = true;
+        for (int step = 0; step < 30 && ok; ++step) {
+            Engine fresh(0);
+            const GridFn a = eng.step_fully_discrete(u, step * 0.05, V, p, k, ConvEngine::GpuFast);
+            const GridFn b = fresh.step_fully_discrete(u, step * 0.05, V, p, k, ConvEngine::GpuDirect);
+            ok = a.values == b.values;
+            if (step == 12) {  // a foreign input must not be mistaken for the resident one
+                const GridFn f = random_periodic(rng, n, 0.01, p.epsilon());
+                const GridFn c = eng.step_fully_discrete(f, 0.0, V, p, k, ConvEngine::GpuFast);
+                const GridFn d = fresh.step_fully_discrete(f, 0.0, V, p, k, ConvEngine::GpuDirect);
+                ok = ok && c.values == d.values;
+            }
+            u = a;
+        }
+        CHECK(ok, "resident consecutive steps == fresh direct steps");
+    }
     // 1. kinetic_convolve == definition-level minimum, both device engines
     for (double drift : {0.0, 0.4, -0.7, 1.0}) {
         const SchemeParams p = params_of(24, 0.25);
