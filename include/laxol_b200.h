@@ -139,6 +139,13 @@ int lob_minplus_fast_window_f64(lob_ctx* ctx, const double* u, double* out, int6
                                 const double* tv, int64_t tv_stride, double eta, int64_t* blocks, void* workspace,
                                 size_t workspace_bytes, int flags, void* stream);
 
+/* Diagnostic hook: replace the fast engine's slope-inversion tolerance delta (in
+ * displacement units) for the line constants computed from now
+ * on; NaN restores the computed bound.  A delta below the bound lets the walk miss
+ * minimisers: those outputs are recomputed by the exact direct scan and counted
+ * (lob_fast_diagnostics [0]), so results stay exact but the walk is shown to fail. */
+int lob_ctx_set_fast_delta(lob_ctx* ctx, double delta);
+
 /* Fast-engine counters, cumulative since the last call without
  * LOB_FAST_STATS_VALID on this workspace (counters[16]; unused entries 0):
  *  [0] outputs no local-minimum interval reached, recomputed by the exact

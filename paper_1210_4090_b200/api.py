@@ -211,6 +211,10 @@ class Device:
                                                   _stream_ptr(stream))
         self._check(st, "lob_minplus_fast_window_f64")
 
+    def set_fast_delta(self, delta: float = float("nan")) -> None:
+        """Diagnostic: override the fast engine's rounding tolerance delta (NaN: the computed bound)."""
+        self._check(self.lib.lob_ctx_set_fast_delta(self.ctx, float(delta)), "lob_ctx_set_fast_delta")
+
     FAST_COUNTER_KEYS = ["missed_outputs", "sources", "queued_candidates", "queued_intervals", "tiles", "tiles_k_unstaged",
                          "k_range_sum", "direct_tiles_gate", "direct_tiles_heavy", "chain_timeouts",
                          "unused10", "stale_line_constants"]

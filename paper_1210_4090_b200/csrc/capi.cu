@@ -87,6 +87,12 @@ int lob_ctx_set_direct_mode(lob_ctx* ctx, int mode) {
     return LOB_OK;
 }
 
+int lob_ctx_set_fast_delta(lob_ctx* ctx, double delta) {
+    if (!ctx) return LOB_INVALID_INPUT;
+    ctx->fast_delta_override = delta;
+    return LOB_OK;
+}
+
 int lob_ctx_set_evolve_resident(lob_ctx* ctx, int on) {
     if (!ctx) return LOB_INVALID_INPUT;
     ctx->resident = on ? 1 : 0;

@@ -115,6 +115,7 @@ struct FastParams {
     const double* vtab;  // v_d for d in [-vofs, vofs]
     int64_t vofs;
     int fsm_on;  // the epilogue produces decompose()'s FSM summaries for the next step's block count
+    double delta_override;  // NaN: the computed rounding bound delta (diagnostic hook, lob_ctx_set_fast_delta)
     // the caller's current per-line inputs (checked against the carried line constants)
     const double* drift_arr;                      // mechanical mode
     // separable potential (the 2-D split step's second sweep): tau*V(line, j) =
@@ -870,7 +871,8 @@ __global__ void line_setup_kernel(const double* __restrict__ drift_arr, int64_t 
     const double dm = fmax(fabs(static_cast<double>(first)), fabs(static_cast<double>(first + 2 * n)));
     const double vmax = dm * eps / tau;
     const double kmag = tau * (0.5 * vmax * vmax + fabs(drift) * vmax);
-    const double delta = 2.0 * (32.0 * uu * kmag / a + 8.0 * uu * (2.0 * n + fabs(drift) * eps / a) + 1e-9);
+    double delta = 2.0 * (32.0 * uu * kmag / a + 8.0 * uu * (2.0 * n + fabs(drift) * eps / a) + 1e-9);
+    if (p.delta_override == p.delta_override) delta = p.delta_override;
     // the walk reads K through the cached v_d table: its window must lie inside it
     const bool intab = first >= -p.vofs && first + 2 * n <= p.vofs;
     LineConst c;
@@ -1661,6 +1663,7 @@ static FastParams make_params(int64_t n, double tau, double eta) {
     p.a = p.eps * p.eps / tau;
     p.ia = 1.0 / p.a;
     p.fsm_on = 1;
+    p.delta_override = __builtin_nan("");
     return p;
 }
 
@@ -1694,6 +1697,7 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     int st = ensure_lut(ctx);
     if (st) return st;
     FastParams p = make_params(n, tau, eta);
+    p.delta_override = ctx->fast_delta_override;
     if (!tab) {
         st = ensure_vtab(ctx, n, tau, &p.vtab, &p.vofs, s);
         if (st) return st;

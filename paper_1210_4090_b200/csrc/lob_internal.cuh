@@ -38,6 +38,7 @@ struct lob_ctx {
     // count of outputs swept in full fp64 (device counter, lazily allocated)
     int direct_mode = 0;
     int resident = 1;  // evolve of short lines through the on-chip resident kernel (K2R)
+    double fast_delta_override = __builtin_nan("");  // lob_ctx_set_fast_delta (diagnostic)
     unsigned long long* direct_full = nullptr;  // [0] outputs swept in full, [1] fp64 candidates
     double* direct_umax = nullptr;              // per-line max |u| (screen bound)
     int64_t direct_umax_cap = 0;

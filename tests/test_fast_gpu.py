@@ -405,3 +405,27 @@ def test_fast_structured_inputs_bit_exact(dev, orc, n, tau, drift):
     dev.fast_f64(a, b, dd, tau, workspace=ws, flags=api.FAST_STATS_VALID)
     torch.cuda.synchronize()
     assert np.array_equal(b.cpu().numpy(), oracle_step(orc, want, drift, tau))
+
+
+@pytest.mark.parametrize("delta", [-0.75, -0.25])
+def test_shrunk_delta_bound_makes_the_walk_miss(dev, orc, delta):
+    """The rounding bound delta is load-bearing: with the local-minimum intervals shrunk below
+    it the walk loses minimisers — outputs that no interval reaches (counted, rescued by the
+    exact scan) and, worse, outputs that some other source still reaches with a larger value
+    (wrong, undetectable by the walk itself).  With the computed bound the same inputs are
+    exact and miss nothing."""
+    n, tau = 600, 0.04
+    rng = np.random.default_rng(17)
+    u = rough_walk(rng, 3, n, 3.0)
+    want = oracle_step(orc, u, 0.4, tau)
+    try:
+        dev.set_fast_delta(delta)
+        got, _, c = fast_step_counted(dev, u, 0.4, tau)
+    finally:
+        dev.set_fast_delta(float("nan"))
+    g = got.cpu().numpy()
+    assert not np.array_equal(g, want) or c["missed_outputs"] > 0, c
+    assert np.all(g >= want)  # every emitted candidate is a real sum: never below the minimum
+    got, _, c = fast_step_counted(dev, u, 0.4, tau)
+    assert np.array_equal(got.cpu().numpy(), want)
+    assert_walk(c)
