@@ -67,15 +67,18 @@ constexpr int kEmitUnroll = LOB_EMIT_UNROLL;  // sources in flight per lane in t
 #define LOB_FAST_MINB 5  // CTAs per SM the main kernel is built for (registers, shared memory)
 #endif
 #ifndef LOB_QCAP
-#define LOB_QCAP 128
+#define LOB_QCAP 96
 #endif
 #ifndef LOB_KC
-#define LOB_KC 2400
+#define LOB_KC 2560
+#endif
+#ifndef LOB_EMIT_SERIAL
+#define LOB_EMIT_SERIAL 0  // 1: each thread walks a contiguous block of sources (else lane-interleaved)
 #endif
 constexpr int kQCap = LOB_QCAP;  // queued source intervals (long / contended) per chunk
 constexpr int kC = LOB_KC;       // sources staged per chunk (a typical tile + halo in one pass)
 #ifndef LOB_VCAP
-#define LOB_VCAP 1024
+#define LOB_VCAP 896
 #endif
 constexpr int kVCap = LOB_VCAP;  // v_d values staged per tile (TMA, with the first chunk)
 #ifndef LOB_FAST_WORK_COUNTERS
@@ -85,9 +88,8 @@ constexpr int kVCap = LOB_VCAP;  // v_d values staged per tile (TMA, with the fi
 #ifndef LOB_TILE_DIRECT
 #define LOB_TILE_DIRECT 1
 #endif
-#ifndef LOB_OSC_EXACT
-#define LOB_OSC_EXACT 1  // gate on the line's oscillation max u - min u (else on (n/2) max |slope|)
-#endif
+// The oscillation gate of a line (fast_kernel): max u - min u (exact extremes, collected by the
+// epilogue when the line needs them) or the cheap bound (n/2) max |slope|, whichever passes.
 
 struct LineConst {
     long long first;  // window displacement of w = 0
@@ -246,7 +248,7 @@ __device__ __forceinline__ double hkey_upper(unsigned k) {
 template <bool FULL>
 __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line, int64_t tile,
                            const FastParams& p, const FastBuffers& b, EpiShared& sh,
-                           const unsigned short* lut) {
+                           const unsigned short* lut, bool osc_exact = true) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int i0 = kPer * tid;  // vals index of u(j0 + 8t - 1)
     double w[kPer + 3];
@@ -268,16 +270,16 @@ __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line,
     // oscillation gate of the next step
     // (coarse 32-bit keys: an enclosure within 2^-20 relative, like the slope bounds)
     unsigned hmn = 0xffffffffu, hmx = 0u;
-#if LOB_OSC_EXACT
+    if (osc_exact) {
 #pragma unroll
-    for (int m = 1; m <= kPer; ++m) {
-        if (FULL || m <= Tl - i0) {
-            const unsigned k = hkey(w[m]);
-            hmn = min(hmn, k);
-            hmx = max(hmx, k);
+        for (int m = 1; m <= kPer; ++m) {
+            if (FULL || m <= Tl - i0) {
+                const unsigned k = hkey(w[m]);
+                hmn = min(hmn, k);
+                hmx = max(hmx, k);
+            }
         }
     }
-#endif
     // decompose() FSM over increments e = j0 + 8t + 1 + k: inc = s(e) - s(e-1),
     // two increments per table lookup.  Non-finite u (which the reference
     // rejects before decompose, proj/src/scheme.cpp:18-24) is not classified.
@@ -305,7 +307,7 @@ __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line,
     }
     kmin = __reduce_min_sync(0xffffffffu, kmin);
     kmax = __reduce_max_sync(0xffffffffu, kmax);
-    if (LOB_OSC_EXACT) {
+    if (osc_exact) {
         hmn = __reduce_min_sync(0xffffffffu, hmn);
         hmx = __reduce_max_sync(0xffffffffu, hmx);
     }
@@ -339,7 +341,7 @@ __device__ void tile_stats(const double* vals, int Tl, int64_t j0, int64_t line,
         if (lane == 0) {
             if (fsm_on) b.fsm_out[line * p.tiles + tile] = f;
             unsigned long long* L = b.line_out + line * 4;
-            if (LOB_OSC_EXACT) {
+            if (osc_exact) {
                 atomicMin(L + 0, dkey(hkey_lower(m0)));
                 atomicMax(L + 1, dkey(hkey_upper(m1)));
             }
@@ -498,7 +500,7 @@ struct MainShared {
     __align__(16) double ubuf[kC + 8];  // sources (unpadded) / then u^{n+1} (padded, stats)
     int3 queue[kQCap];
     __align__(16) double vbuf[kVCap];  // v_d of the tile's displacement range, converted to K(d)
-    int ya, yb, nq, dlo, dhi, DLg, DRg, mode, gate, abort;
+    int ya, yb, nq, dlo, dhi, DLg, DRg, mode, gate, abort, osc_exact;
     unsigned qwork, budget;            // long queued runs of the tile, and the walk's work budget
     int nruns, rs[kRuns], re[kRuns];  // runs of reaching sub-tiles (unrolled source ranges)
     unsigned int c_src, c_queued, c_qent;
@@ -685,19 +687,36 @@ __device__ __forceinline__ void tab_interval(SIG sig, const LineConst& lc, doubl
 template <bool TAB, bool KS>
 __device__ __forceinline__ bool process_chunk(MainShared& S, const ChunkArgs& a, unsigned budget) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#if LOB_EMIT_SERIAL
+    // thread t walks the sources t*k .. t*k+k-1 (k odd: conflict-free strided shared loads), each
+    // value and slope read once and carried to the next source
+    const int k = ((a.clen + kNT - 1) / kNT) | 1;
+    const int ib = min(static_cast<int>(threadIdx.x) * k, a.clen);
+    const int iend = min(ib + k, a.clen);
+    double uc = a.ub[ib + 1], slc = __dsub_rn(uc, a.ub[ib]);
+    for (int i = ib; i < iend; ++i) {
+        const double u0 = uc;
+        const double un = a.ub[i + 2];
+        const double sl = slc, sr = __dsub_rn(un, u0);
+        uc = un;
+        slc = sr;
+#else
+    (void)lane;
     const int per = ((a.clen + kNT - 1) / kNT) * 32;
     const int iend = min(a.clen, (warp + 1) * per);
 #pragma unroll kEmitUnroll
     for (int i = warp * per + lane; i < iend; i += 32) {
         const double ul0 = a.ub[i], u0 = a.ub[i + 1], ur0 = a.ub[i + 2];
+        const double sl = __dsub_rn(u0, ul0), sr = __dsub_rn(ur0, u0);
+#endif
         int dl, dr;
         if constexpr (TAB) {
             auto sig = [&](int d) { return __dsub_rn(kvalue<TAB, KS>(a, d + 1), kvalue<TAB, KS>(a, d)); };
-            tab_interval(sig, *a.lc, __dsub_rn(u0, ul0), __dsub_rn(ur0, u0), a.dlo, a.dhi, dl, dr);
+            tab_interval(sig, *a.lc, sl, sr, a.dlo, a.dhi, dl, dr);
         } else {
             // z(s) -/+ (1/2 + delta) with one fused rounding (delta bounds it, csrc/host/kernel_build.cpp)
-            dl = __double2int_ru(__fma_rn(__dsub_rn(u0, ul0), a.ia, a.hl));
-            dr = __double2int_rd(__fma_rn(__dsub_rn(ur0, u0), a.ia, a.hr));
+            dl = __double2int_ru(__fma_rn(sl, a.ia, a.hl));
+            dr = __double2int_rd(__fma_rn(sr, a.ia, a.hr));
         }
         const int off = a.base + i;  // output index of this source at d = 0
         // every candidate lies in [dlo, dhi] when the statistics describe u;
@@ -1048,10 +1067,15 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
         int DLg = dmin_w, DRg = dmax_w;
         // window-edge displacements cannot hold a minimiser when the line's oscillation
         // max u - min u is below the window's edge gap min(K(first), K(last)) - min K
-        const double osc = LOB_OSC_EXACT ? __dsub_rn(umax, umin)
-                                         : 0.5 * static_cast<double>(n) * fmax(fabs(smin), fabs(smax));
-        bool okl = !stale && isfinite(osc) && isfinite(smin) && isfinite(smax) && n >= 3 &&
-                   osc * (1.0 + 1e-12) < lc.gap * (1.0 - 1e-12);
+        // (the exact extremes are absent, NaN, when the previous step did not collect them)
+        const double osc = __dsub_rn(umax, umin);
+        const double loose = 0.5 * static_cast<double>(n) * fmax(fabs(smin), fabs(smax));
+        const bool exact_ok = isfinite(osc) && osc * (1.0 + 1e-12) < lc.gap * (1.0 - 1e-12);
+        const bool loose_ok = loose * (1.0 + 1e-12) < lc.gap * (1.0 - 1e-12);
+        bool okl = !stale && (exact_ok || loose_ok) && isfinite(smin) && isfinite(smax) && n >= 3;
+        // this step's epilogue collects the exact extremes of u^{n+1} unless the cheap bound of
+        // u^n passes with a factor 2 to spare (the same decision in every tile of the line)
+        if (lane == 0) S.osc_exact = !(loose * 2.0 < lc.gap) || !isfinite(loose);
         const bool gate = okl;
         if (stale && lane == 0 && diag) atomicAdd(diag + 11, 1ull);
         if (okl) {
@@ -1180,6 +1204,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
     }
     __syncthreads();  // gate, mode, ranges, mbarrier initialised
     const int mode = S.mode;
+    const bool osc_exact = S.osc_exact;  // read before the epilogue reuses the shared layout
 
     bool walk = mode == kModeWalk;
     if (walk) {
@@ -1358,9 +1383,9 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
         atomicAdd(diag + 4, 1ull);
     }
     if (Tl == kT && j0 + kT <= n - 1)
-        tile_stats<true>(vals, Tl, j0, line, tile, p, b, S.epi(), g_fsm_lut2);
+        tile_stats<true>(vals, Tl, j0, line, tile, p, b, S.epi(), g_fsm_lut2, osc_exact);
     else
-        tile_stats<false>(vals, Tl, j0, line, tile, p, b, S.epi(), g_fsm_lut2);
+        tile_stats<false>(vals, Tl, j0, line, tile, p, b, S.epi(), g_fsm_lut2, osc_exact);
     // block count of the INPUT u (decompose on the closed period): warp 0 of
     // the line's first tile composes the tile summaries
     if (blocks_out && tile == 0 && warp == 0) {

@@ -5,7 +5,11 @@ import sys
 import torch
 
 sys.path.insert(0, ".")
-from paper_1210_4090_b200 import api  # noqa: E402
+from paper_1210_4090_b200 import _capi, api  # noqa: E402
+import os  # noqa: E402
+
+if os.environ.get("LOB_LIB"):
+    _capi.LIB_PATH = os.path.abspath(os.environ["LOB_LIB"])
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=3)
