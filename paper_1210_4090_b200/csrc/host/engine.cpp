@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -119,9 +120,13 @@ void validate(const SchemeParams& p) {
     if (!(p.tau > 0.0)) throw InvalidInput("SchemeParams: tau must be positive");
     if (p.eta < 0.0) throw InvalidInput("SchemeParams: eta must be >= 0");
     if (!(p.h0 > 0.0)) throw InvalidInput("SchemeParams: h0 must be positive");
-    if (p.epsilon() / p.tau >= p.h0)
-        throw InvalidInput("SchemeParams: epsilon/tau = " + std::to_string(p.epsilon() / p.tau) +
-                           " violates the bound epsilon/tau < h0 = " + std::to_string(p.h0));
+    const double ratio = p.epsilon() / p.tau;
+    if (ratio >= p.h0) {
+        if (p.anti_cfl == AntiCflMode::Fail)
+            throw InvalidInput("SchemeParams: epsilon/tau = " + std::to_string(ratio) +
+                               " violates the bound epsilon/tau < h0 = " + std::to_string(p.h0));
+        std::fprintf(stderr, "laxol: warning: epsilon/tau = %g exceeds h0 = %g\n", ratio, p.h0);
+    }
 }
 
 // Device state kept between calls: grow-only buffers, the K2 workspace, and the last
@@ -319,7 +324,7 @@ EvolutionTrace Engine::evolve(const GridFn& u0, double t0, int64_t steps, double
         // windowed domain (proj/src/scheme.cpp:208-272 with kinetic_convolve's wall branch,
         // :135-144): step by step through the windowed K1 kernel, the drift and the
         // non-finite check on the host in the reference's order
-        const KernelWindow kernel = build_kernel_mech(params.n_space, params.tau, drift);
+        const KernelWindow kernel = build_kernel_mech(params, drift);
         int64_t stride = options.snapshot_stride;
         if (stride <= 0) stride = steps <= 1024 ? 1 : (steps + 1023) / 1024;
         std::vector<int64_t> capture = options.capture_steps;
@@ -380,7 +385,7 @@ EvolutionTrace Engine::evolve(const GridFn& u0, double t0, int64_t steps, double
     trace.snapshots.push_back(u0);
     if (steps == 0) return trace;
 
-    DevBuf<double> du(n), dscr(n), dd(1), dtv(n);
+    DevBuf<double> du(n), dscr(n), dd(1), dtv(n), dstart(n);
     du.upload(u0.values.data(), n);
     dd.upload(&drift, 1);
     size_t wsb = 0;
@@ -409,6 +414,9 @@ EvolutionTrace Engine::evolve(const GridFn& u0, double t0, int64_t steps, double
             dtv.upload(tv.data(), n);
         }
         int64_t completed = 0;
+        // the chunk's start state, for an exact replay after a non-finite abort (the last kept
+        // snapshot is older than the chunk when V is time dependent and steps > 1024)
+        check_cuda(cudaMemcpy(dstart.p, du.p, n * sizeof(double), cudaMemcpyDeviceToDevice), "D2D");
         const auto started = std::chrono::steady_clock::now();
         const int st = lob_evolve_f64(ctx_, du.p, dscr.p, 1, n, dd.p, params.tau, V ? dtv.p : nullptr, 0,
                                       params.eta, code, chunk, dstep_drift.p + done,
@@ -439,7 +447,7 @@ EvolutionTrace Engine::evolve(const GridFn& u0, double t0, int64_t steps, double
             // check interval: replay exactly `completed` steps from the chunk start
             trace.completed = false;
             trace.abort_reason = "non-finite value after step " + std::to_string(done);
-            du.upload(trace.snapshots.back().values.data(), n);
+            check_cuda(cudaMemcpy(du.p, dstart.p, n * sizeof(double), cudaMemcpyDeviceToDevice), "D2D");
             int64_t again = 0;
             lob_evolve_f64(ctx_, du.p, dscr.p, 1, n, dd.p, params.tau, V ? dtv.p : nullptr, 0, params.eta,
                            code, completed, nullptr, nullptr, &again, ws.p, wsb, nullptr);
@@ -709,7 +717,7 @@ GridFn Engine::step_semidiscrete(const GridFn& u, double t, double drift, const 
                                  const SchemeParams& params, int quad_points) {
     if (quad_points < 1) throw InvalidInput("step_semidiscrete: quad_points must be >= 1");
     check_u_grid(u, params, "step_semidiscrete");
-    const KernelWindow k = build_kernel_mech(params.n_space, params.tau, drift);
+    const KernelWindow k = build_kernel_mech(params, drift);
     lob_potential lp{};
     lp.kind = static_cast<int>(V.kind);
     lp.value = V.value;

@@ -13,6 +13,10 @@
 
 namespace laxol_b200 {
 
+namespace {
+KernelWindow mech_window(int64_t n_space, double tau, double drift);
+}
+
 KernelWindow build_kernel_mech(int64_t n_space, double tau, double drift) {
     if (n_space < 1) throw InvalidInput("SchemeParams: n_space must be >= 1");
     if (!(tau > 0.0)) throw InvalidInput("SchemeParams: tau must be positive");
@@ -20,6 +24,17 @@ KernelWindow build_kernel_mech(int64_t n_space, double tau, double drift) {
     if (eps / tau >= 1.0)
         throw InvalidInput("SchemeParams: epsilon/tau = " + std::to_string(eps / tau) +
                            " violates the bound epsilon/tau < h0 = 1");
+    return mech_window(n_space, tau, drift);
+}
+
+KernelWindow build_kernel_mech(const SchemeParams& params, double drift) {
+    validate(params);  // the guard with the params' h0 and anti-CFL mode
+    return mech_window(params.n_space, params.tau, drift);
+}
+
+namespace {
+KernelWindow mech_window(int64_t n_space, double tau, double drift) {
+    const double eps = 1.0 / static_cast<double>(n_space);
     KernelWindow k;
     k.n_space = n_space;
     k.tau = tau;
@@ -48,6 +63,7 @@ KernelWindow build_kernel_mech(int64_t n_space, double tau, double drift) {
     k.delta = fast_delta(n_space, tau, drift, k.first);
     return k;
 }
+}  // namespace
 
 // build_kernel for a tabulated conjugate (proj/src/hamiltonian.cpp:30-82 kstar /
 // argmin_velocity / v_min / v_max of Kind::Tabulated, proj/src/scheme.cpp:59-105 incl.

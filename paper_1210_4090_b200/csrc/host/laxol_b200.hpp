@@ -64,6 +64,7 @@ double fast_delta(int64_t n_space, double tau, double drift, int64_t first);
 
 enum class ConvEngine { Fast, Naive, GpuFast, GpuDirect };
 enum class PotentialSampling { Arrival, Departure };
+enum class AntiCflMode { Fail, Warn };
 
 // proj/include/laxol/scheme.hpp:17-26
 struct SchemeParams {
@@ -72,9 +73,16 @@ struct SchemeParams {
     double eta = 0.0;
     double h0 = 1.0;
     PotentialSampling v_sampling = PotentialSampling::Arrival;
+    AntiCflMode anti_cfl = AntiCflMode::Fail;
     double epsilon() const { return 1.0 / static_cast<double>(n_space); }
 };
+// proj/src/scheme.cpp:39-53: ranges, and the anti-CFL guard epsilon/tau < h0 (throws, or warns on
+// stderr with AntiCflMode::Warn)
 void validate(const SchemeParams& p);
+// build_kernel(kinetic, params) (proj/src/scheme.cpp:59-105): validate(params) first, so h0 and the
+// anti-CFL mode apply; the (n_space, tau, ...) builders below keep the default guard h0 = 1, Fail
+struct KernelWindow;
+KernelWindow build_kernel_mech(const SchemeParams& params, double drift);
 
 // V(t, x) callback (proj/include/laxol/hamiltonian.hpp:34-73 reduced to what
 // the hot path calls): evaluated on the host per grid point, like the

@@ -17,7 +17,7 @@ full size:
   C5  200 steps x 64 lines x N=2^20 (K2); at sampled steps the K2 step == K1
       on 2 lines.
 
-Writes one JSON document (default: profiles/r01_full_configs.json).
+Writes one JSON document (default: profiles/r02_full_configs.json).
 """
 from __future__ import annotations
 
@@ -191,10 +191,12 @@ def c4(dev, steps=500):
     a = dev_t(api.gen_cos(n))
     res = {}
     finals = {}
-    for name, eng in (("k1_direct", api.ENGINE_DIRECT), ("k2_fast", api.ENGINE_FAST)):
+    for name, eng, halves in (("k1_direct", api.ENGINE_DIRECT, 1), ("k2_fast", api.ENGINE_FAST, 2),
+                              ("k2_fast_unfused", api.ENGINE_FAST, 1)):
         u = dev_t(api.gen_c4_u0(n))
         o, tmp = torch.empty_like(u), torch.empty_like(u)
-        ws = torch.empty(dev.fast_workspace_bytes(n, n), dtype=torch.uint8, device="cuda")
+        # two workspace halves: the fused four-launch step (transpose + statistics, sweep, x2)
+        ws = torch.empty(halves * dev.fast_workspace_bytes(n, n), dtype=torch.uint8, device="cuda")
         bs = [api.c4_time_term(i * tau + tau) for i in range(steps)]
         with Timer() as t:
             for i in range(steps):
@@ -206,7 +208,8 @@ def c4(dev, steps=500):
         if eng == api.ENGINE_DIRECT:
             cand = 2 * n * n * (2 * n + 1) * steps
             res[name]["cand_per_s"] = cand / (t.ms * 1e-3)
-    res["k1_k2_trajectories_bit_exact"] = bool(np.array_equal(finals["k1_direct"], finals["k2_fast"]))
+    res["k1_k2_trajectories_bit_exact"] = bool(np.array_equal(finals["k1_direct"], finals["k2_fast"]) and
+                                              np.array_equal(finals["k2_fast"], finals["k2_fast_unfused"]))
     res["mean_u_T_over_T"] = float(finals["k2_fast"].mean() / (steps * tau))
     gp = os.path.join(GOLD, "c4_n128.npz")
     if os.path.exists(gp):
@@ -303,7 +306,7 @@ def c2_karp(dev, n=512, count=16):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_full_configs.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_full_configs.json"))
     ap.add_argument("--only", default="c1,c2,c3,c4,c5,c2_karp")
     args = ap.parse_args()
     dev = api.Device(0)

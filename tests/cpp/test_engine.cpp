@@ -126,6 +126,23 @@ int main(int argc, char** argv) {
         }
         CHECK(ok, "resident consecutive steps == fresh direct steps");
     }
+    // 0b. the anti-CFL guard honours h0 and AntiCflMode (proj/src/scheme.cpp:39-53)
+    {
+        SchemeParams p = params_of(16, 0.1);  // epsilon/tau = 0.625
+        p.h0 = 0.5;
+        bool threw = false;
+        try {
+            build_kernel_mech(p, 0.0);
+        } catch (const InvalidInput&) {
+            threw = true;
+        }
+        p.anti_cfl = AntiCflMode::Warn;
+        const KernelWindow kw = build_kernel_mech(p, 0.0);  // warns, builds
+        SchemeParams q = params_of(16, 0.05);                // epsilon/tau = 1.25 < h0 = 2
+        q.h0 = 2.0;
+        const KernelWindow kq = build_kernel_mech(q, 0.3);
+        CHECK(threw && kw.window.size() == 33 && kq.window.size() == 33, "anti-CFL guard: h0 and Warn");
+    }
     // 1. kinetic_convolve == definition-level minimum, both device engines
     for (double drift : {0.0, 0.4, -0.7, 1.0}) {
         const SchemeParams p = params_of(24, 0.25);
