@@ -242,6 +242,11 @@ int lob_evolve_f64(lob_ctx* ctx, double* u, double* scratch, int64_t lines, int6
  * too small to fill the GPU step by step (lines * ceil(n/2048) <= 4 * SMs).  Same doubles as
  * the step-by-step loop.  on = 0 always selects the step-by-step K2 launches (default 1). */
 int lob_ctx_set_evolve_resident(lob_ctx* ctx, int on);
+/* Diagnostic switch (default on): the fast engine on lines of n <= 2048 samples without block
+ * counts runs one CTA per whole line with the oscillation gate and displacement range reduced
+ * from the staged line (K2L; the 2-D split step's axis-0 sweep then reads and writes columns in
+ * place).  Off: the tiled kernel with carried statistics.  Both give the same doubles. */
+int lob_ctx_set_fast_line(lob_ctx* ctx, int on);
 
 /* Host-buffer entry point (the e2e path): one step of `lines` lines whose u,
  * out, drift and tv live in host memory (pinned or pageable).  Copies in,

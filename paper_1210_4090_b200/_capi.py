@@ -69,6 +69,7 @@ SIGNATURES = {
     "lob_launch_count": (c_int64, [_P]),
     "lob_ctx_set_direct_mode": (c_int, [_P, c_int]),
     "lob_ctx_set_evolve_resident": (c_int, [_P, c_int]),
+    "lob_ctx_set_fast_line": (c_int, [_P, c_int]),
     "lob_direct_stats": (c_int, [_P, POINTER(c_uint64), POINTER(c_uint64), c_int]),
     # weak-KAM consumers (proj/src/weakkam.cpp)
     "lob_minplus_gemm_f64": (c_int, [_P, _P, c_int64, _P, c_int64, _P, c_int64, c_int64, c_int64, c_int64, _P]),

@@ -122,6 +122,10 @@ class Device:
         """evolve through the on-chip resident kernels (K2R / K2C) where the lines fit (default)."""
         self._check(self.lib.lob_ctx_set_evolve_resident(self.ctx, int(bool(on))), "lob_ctx_set_evolve_resident")
 
+    def set_fast_line(self, on: bool) -> None:
+        """Short lines (n <= 2048) on the whole-line fast kernel (K2L, default) or the tiled one."""
+        self._check(self.lib.lob_ctx_set_fast_line(self.ctx, int(on)), "lob_ctx_set_fast_line")
+
     def set_direct_mode(self, mode: int) -> None:
         """DIRECT_SCREENED (default: fp32 screen + fp64 re-evaluation) or DIRECT_PLAIN."""
         self._check(self.lib.lob_ctx_set_direct_mode(self.ctx, int(mode)), "lob_ctx_set_direct_mode")

@@ -93,6 +93,12 @@ int lob_ctx_set_fast_delta(lob_ctx* ctx, double delta) {
     return LOB_OK;
 }
 
+int lob_ctx_set_fast_line(lob_ctx* ctx, int on) {
+    if (!ctx) return LOB_INVALID_INPUT;
+    ctx->fast_line = on < 0 ? 0 : on;  // 2, 3: split-step layouts measured against the default (1)
+    return LOB_OK;
+}
+
 int lob_ctx_set_evolve_resident(lob_ctx* ctx, int on) {
     if (!ctx) return LOB_INVALID_INPUT;
     ctx->resident = on ? 1 : 0;
@@ -279,6 +285,26 @@ int lob_split_step_2d_f64(lob_ctx* ctx, const double* u, double* out, double* tm
     if ((st = split_axis_inputs(ctx, n, tau, drift1, &k1, &f1, &d1, s))) return st;
     if ((st = split_axis_inputs(ctx, n, tau, drift2, &k2, &f2, &d2, s))) return st;
     const size_t wsz = fast_workspace_bytes(n, n);
+    if (engine == LOB_ENGINE_FAST && ctx->fast_line && n <= fast_line_max()) {
+        // K2L twice, tau*V = tau*(a1[i]*a2[k] + b) in the second sweep's epilogue
+        const FastSepPot sep{a1, a2, b};
+        const FastSepPot* sp = (a1 && a2) ? &sep : nullptr;
+        if (ctx->fast_line == 2) {  // transposes around row sweeps (the default: measured fastest)
+            if ((st = launch_transpose(ctx, u, tmp, n, s))) return st;
+            if ((st = launch_line_f64(ctx, tmp, out, n, n, d1, tau, nullptr, 0, nullptr, false, false, nullptr, s)))
+                return st;
+            if ((st = launch_transpose(ctx, out, tmp, n, s))) return st;
+            return launch_line_f64(ctx, tmp, out, n, n, d2, tau, nullptr, 0, sp, false, false, nullptr, s);
+        }
+        if (ctx->fast_line == 3) {  // both sweeps read columns and write rows (tmp = the transposed state)
+            if ((st = launch_line_f64(ctx, u, tmp, n, n, d1, tau, nullptr, 0, nullptr, true, false, nullptr, s)))
+                return st;
+            return launch_line_f64(ctx, tmp, out, n, n, d2, tau, nullptr, 0, sp, true, false, nullptr, s);
+        }
+        // axis 0 reads and writes the columns of u in place, axis 1 sweeps the rows
+        if ((st = launch_line_f64(ctx, u, tmp, n, n, d1, tau, nullptr, 0, nullptr, true, true, nullptr, s))) return st;
+        return launch_line_f64(ctx, tmp, out, n, n, d2, tau, nullptr, 0, sp, false, false, nullptr, s);
+    }
     if (engine == LOB_ENGINE_FAST && workspace && workspace_bytes >= 2 * wsz) {
         // fused: transpose + K2 statistics -> sweep axis 0 -> transpose + statistics ->
         // sweep axis 1 with tau*V = tau*(a1[i]*a2[k] + b) in its epilogue.  One workspace per

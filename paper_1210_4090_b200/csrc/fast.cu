@@ -76,6 +76,10 @@ constexpr int kEmitUnroll = LOB_EMIT_UNROLL;  // sources in flight per lane in t
 #define LOB_EMIT_SERIAL 0  // 1: each thread walks a contiguous block of sources (else lane-interleaved)
 #endif
 constexpr int kQCap = LOB_QCAP;  // queued source intervals (long / contended) per chunk
+#ifndef LOB_QSHORT
+#define LOB_QSHORT 8
+#endif
+constexpr int kQShort = LOB_QSHORT;  // queued runs shorter than this are finished by one thread
 constexpr int kC = LOB_KC;       // sources staged per chunk (a typical tile + halo in one pass)
 #ifndef LOB_VCAP
 #define LOB_VCAP 896
@@ -756,13 +760,26 @@ __device__ __forceinline__ bool process_chunk(MainShared& S, const ChunkArgs& a,
     if (S.abort || S.qwork > budget) return false;
     const int nq = min(S.nq, kQCap);
     if (nq) {
+        // short queued runs one thread each, long ones one warp each
+        unsigned qc = 0;
+        for (int e = threadIdx.x; e < nq; e += kNT) {
+            const int3 qe = S.queue[e];
+            if (qe.z - qe.y < kQShort) {
+                const double uy = a.ub[qe.x + 1];
+                const int off = a.base + qe.x;
+                qc += static_cast<unsigned>(qe.z - qe.y + 1);
+                for (int d = qe.y; d <= qe.z; ++d) smem_fmin(&S.keys[off + d], __dadd_rn(uy, kvalue<TAB, KS>(a, d)));
+            }
+        }
         for (int e = warp; e < nq; e += kNT / 32) {
             const int3 qe = S.queue[e];
+            if (qe.z - qe.y < kQShort) continue;
             const double uy = a.ub[qe.x + 1];
             const int off = a.base + qe.x;
-            if (lane == 0) atomicAdd(&S.c_queued, static_cast<unsigned>(qe.z - qe.y + 1));
+            if (lane == 0) qc += static_cast<unsigned>(qe.z - qe.y + 1);
             for (int d = qe.y + lane; d <= qe.z; d += 32) smem_fmin(&S.keys[off + d], __dadd_rn(uy, kvalue<TAB, KS>(a, d)));
         }
+        if (qc) atomicAdd(&S.c_queued, qc);
         __syncthreads();
         if (threadIdx.x == 0) {
             S.c_qent += nq;
@@ -802,7 +819,8 @@ __device__ __forceinline__ double kdirect(const FastParams& p, int d, double dri
 // displacements staged in shared memory, one LDS per displacement and one add + one
 // exact min per candidate; the three halo outputs are one warp each.
 template <bool CHAIN, class KF>
-__device__ void tile_direct(MainShared& S, const double* ul, int n, int j0, int Tl, int first, KF kf) {
+__device__ void tile_direct(MainShared& S, const double* ul, int n, int j0, int Tl, int first, KF kf,
+                            int64_t us = 1) {
     constexpr int R = kPer, L = kT + kTW;
     double* Us = reinterpret_cast<double*>(&S);
     double* Ks = Us + P8(L) + 1;
@@ -817,7 +835,7 @@ __device__ void tile_direct(MainShared& S, const double* ul, int n, int j0, int 
         for (int w = lane; w < W; w += 32) {
             int y = (y0 - w) % n;
             if (y < 0) y += n;
-            const double c = __dadd_rn(xload<CHAIN>(ul + y), kf(first + w));
+            const double c = __dadd_rn(xload<CHAIN>(ul + y * us), kf(first + w));
             hb = c < hb ? c : hb;
         }
 #pragma unroll
@@ -837,7 +855,7 @@ __device__ void tile_direct(MainShared& S, const double* ul, int n, int j0, int 
         for (int i = tid; i < L; i += kNT) {
             int y = ym + i;
             while (y >= n) y -= n;
-            Us[P8(i)] = xload<CHAIN>(ul + y);
+            Us[P8(i)] = xload<CHAIN>(ul + y * us);
         }
         for (int s = tid; s < kTW; s += kNT) Ks[s] = wc + s < W ? kf(first + wc + s) : INFINITY;
         __syncthreads();
@@ -878,12 +896,9 @@ __device__ void tile_direct(MainShared& S, const double* ul, int n, int j0, int 
 
 // Per-line constants of the step (identical IEEE operations to the host's
 // build_kernel for first/center; the tolerance only needs to be a bound).
-__global__ void line_setup_kernel(const double* __restrict__ drift_arr, int64_t lines, FastParams p,
-                                  LineConst* __restrict__ lc) {
-    const int64_t line = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (line >= lines) return;
+__device__ __forceinline__ LineConst line_const(double drift, const FastParams& p) {
     const int64_t n = p.n;
-    const double drift = drift_arr[line], tau = p.tau, eps = p.eps, a = p.a;
+    const double tau = p.tau, eps = p.eps, a = p.a;
     const int64_t center = llround(__ddiv_rn(__dmul_rn(tau, drift), eps));
     const int64_t first = center - n;
     const double uu = 1.1102230246251565e-16;
@@ -894,7 +909,7 @@ __global__ void line_setup_kernel(const double* __restrict__ drift_arr, int64_t 
     if (p.delta_override == p.delta_override) delta = p.delta_override;
     // the walk reads K through the cached v_d table: its window must lie inside it
     const bool intab = first >= -p.vofs && first + 2 * n <= p.vofs;
-    LineConst c;
+    LineConst c{};
     c.first = first;
     c.pe = __dmul_rn(drift, eps);
     const double pz = __dmul_rn(c.pe, p.ia);  // P eps / a
@@ -911,7 +926,14 @@ __global__ void line_setup_kernel(const double* __restrict__ drift_arr, int64_t 
     } else {
         c.gap = -INFINITY;  // never passes the gate: the line's tiles take the direct formula
     }
-    lc[line] = c;
+    return c;
+}
+
+__global__ void line_setup_kernel(const double* __restrict__ drift_arr, int64_t lines, FastParams p,
+                                  LineConst* __restrict__ lc) {
+    const int64_t line = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (line >= lines) return;
+    lc[line] = line_const(drift_arr[line], p);
 }
 
 // Per-line constants of a window-table step: one warp per line reduces the window's
@@ -1413,6 +1435,213 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
 }
 
 
+// ---- K2L: one step of short lines, one CTA per whole line ---------------------
+// For n <= kT the whole line is one tile, so the statistics K2 carries between steps
+// (sub-tile slope bounds, line extremes) are computed from the staged line itself: the
+// exact oscillation gate and the line's displacement range [DLg, DRg] come from a block
+// reduction, no workspace statistics are read or written, and the candidate emission,
+// the direct fallbacks and the epilogue are fast_kernel's.  COLIN / COLOUT: line l is
+// column l of an n x n row-major tensor (the 2-D split step's axis-0 sweep reads and
+// writes columns in place: proj/src/splitting.cpp:67-76 gathers and scatters them).
+// Outputs follow fast_kernel's slot convention (slot i = output i - 1; slots 0 and n + 1
+// are halo outputs nobody reads).
+struct LineShared {  // overlays S.vbuf before the K staging
+    unsigned kred[4][kNT / 32];
+    double hl, hr, gap, drift;
+    long long first;
+};
+static_assert(sizeof(LineShared) <= sizeof(double) * kVCap, "line scratch fits vbuf");
+
+template <bool COLIN, bool COLOUT>
+__global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* __restrict__ u, double* __restrict__ out,
+                                                                  const double* __restrict__ drift_arr,
+                                                                  const double* __restrict__ tv, int64_t tv_stride,
+                                                                  unsigned long long* __restrict__ diag, FastParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    MainShared& S = *reinterpret_cast<MainShared*>(smem_raw);
+    LineShared& L = *reinterpret_cast<LineShared*>(S.vbuf);
+    const int n = static_cast<int>(p.n);
+    const int64_t line = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t is = COLIN ? p.n : 1, os = COLOUT ? p.n : 1;
+    const double* ul = COLIN ? u + line : u + line * p.n;
+    double* ol = COLOUT ? out + line : out + line * p.n;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // the line into shared memory (the keys area: U[j], j < n <= kT)
+    double* U = reinterpret_cast<double*>(S.keys);
+    for (int j = tid; j < n; j += kNT) U[j] = ul[j * is];
+    if (tid == 0) {
+        const LineConst c = line_const(__ldg(drift_arr + line), p);
+        L.hl = c.hl;
+        L.hr = c.hr;
+        L.gap = c.gap;
+        L.drift = c.drift;
+        L.first = c.first;
+    }
+    __syncthreads();
+    // enclosures of u and of its slopes s(j) = U(j+1) - U(j) (periodic): coarse order-preserving
+    // keys (within 2^-20 relative, tile_stats' keys) reduced with REDUX
+    {
+        unsigned kmn = 0xffffffffu, kmx = 0u, hmn = 0xffffffffu, hmx = 0u;
+#pragma unroll 4
+        for (int j = tid; j < n; j += kNT) {
+            const double uj = U[j];
+            const unsigned ks = hkey(__dsub_rn(U[j + 1 < n ? j + 1 : 0], uj)), ku = hkey(uj);
+            kmn = min(kmn, ks);
+            kmx = max(kmx, ks);
+            hmn = min(hmn, ku);
+            hmx = max(hmx, ku);
+        }
+        kmn = __reduce_min_sync(0xffffffffu, kmn);
+        kmx = __reduce_max_sync(0xffffffffu, kmx);
+        hmn = __reduce_min_sync(0xffffffffu, hmn);
+        hmx = __reduce_max_sync(0xffffffffu, hmx);
+        if (lane == 0) {
+            L.kred[0][warp] = kmn;
+            L.kred[1][warp] = kmx;
+            L.kred[2][warp] = hmn;
+            L.kred[3][warp] = hmx;
+        }
+    }
+    __syncthreads();
+    const int first = static_cast<int>(L.first);
+    const double drift = L.drift, tau = p.tau, ia = p.ia, hl = L.hl, hr = L.hr;
+    const int dmin_w = first + 1, dmax_w = first + 2 * n - 1;
+    constexpr int jlo = -1;
+    const int jspan = n + 1;
+    if (warp == 0) {
+        const bool in = lane < kNT / 32;
+        const unsigned a0 = __reduce_min_sync(0xffffffffu, in ? L.kred[0][lane] : 0xffffffffu);
+        const unsigned a1 = __reduce_max_sync(0xffffffffu, in ? L.kred[1][lane] : 0u);
+        const unsigned b0 = __reduce_min_sync(0xffffffffu, in ? L.kred[2][lane] : 0xffffffffu);
+        const unsigned b1 = __reduce_max_sync(0xffffffffu, in ? L.kred[3][lane] : 0u);
+        if (lane == 0) {
+            // window-edge displacements cannot hold a minimiser when max u - min u (here an upper
+            // bound) is below the window's edge gap (fast_kernel's gate)
+            const double smin = hkey_lower(a0), smax = hkey_upper(a1);
+            const double osc = __dsub_rn(hkey_upper(b1), hkey_lower(b0));
+            bool ok = isfinite(osc) && isfinite(smin) && isfinite(smax) && n >= 3 &&
+                      osc * (1.0 + 1e-12) < L.gap * (1.0 - 1e-12);
+            int DLg = dmin_w, DRg = dmax_w;
+            if (ok) {
+                DLg = max(__double2int_ru(__fma_rn(smin, ia, hl)), dmin_w);
+                DRg = min(__double2int_rd(__fma_rn(smax, ia, hr)), dmax_w);
+                ok = DLg <= DRg;
+            }
+            S.mode = ok ? kModeWalk : kModeDirect;
+            S.gate = ok;
+            // unrolled sources that can reach outputs jlo .. jlo + jspan
+            S.ya = jlo - DRg;
+            S.yb = jlo + jspan - DLg;
+            S.dlo = DLg;
+            S.dhi = DRg;
+            S.nq = 0;
+            S.abort = 0;
+            S.qwork = 0;
+            const double bud = LOB_HEAVY * static_cast<double>(jspan + 1) * static_cast<double>(2 * n + 1);
+            S.budget = bud > 4.0e9 ? 4000000000u : static_cast<unsigned>(bud);
+            S.c_src = S.c_queued = S.c_qent = 0;
+        }
+    }
+    __syncthreads();
+    bool walk = S.mode == kModeWalk;
+    auto kf = [&](int d) -> double { return kdirect(p, d, drift); };
+    if (walk) {
+        const int ya = S.ya, yb = S.yb, dlo = S.dlo, dhi = S.dhi;
+        const unsigned budget = S.budget;
+        // the first source chunk straight from the staged line, before the keys take its place
+        int clen = min(kC, yb - ya + 1);
+        {
+            int y0 = (ya - 1) % n;
+            y0 += y0 < 0 ? n : 0;
+            if (clen + 2 <= 2 * n) {  // at most two wraps
+                for (int i = tid; i < clen + 2; i += kNT) {
+                    int y = y0 + i;
+                    y -= y >= n ? n : 0;
+                    S.ubuf[i] = U[y >= n ? y - n : y];
+                }
+            } else {
+                for (int i = tid; i < clen + 2; i += kNT) S.ubuf[i] = U[(y0 + i) % n];
+            }
+        }
+        __syncthreads();
+        {
+            ulonglong2* k2 = reinterpret_cast<ulonglong2*>(S.keys);
+            for (int i = tid; i < (kT + 4) / 2; i += kNT) k2[i] = make_ulonglong2(kInfBits, kInfBits);
+        }
+        // K(d) of the line's displacement range in shared memory when it fits (vbuf: the line
+        // scratch above is dead once the constants are in registers)
+        const int vcnt = dhi - dlo + 1;
+        const bool kstage = vcnt <= kVCap;
+        if (kstage)
+            for (int i = tid; i < vcnt; i += kNT) S.vbuf[i] = kf(dlo + i);
+        __syncthreads();
+        const double* skt = S.vbuf - dlo;
+        if (tid == 0 && diag) {
+            atomicAdd(diag + 5, kstage ? 0ull : 1ull);
+            atomicAdd(diag + 6, static_cast<unsigned long long>(vcnt));
+        }
+        for (int yc = ya; yc <= yb;) {
+            if (yc != ya) {
+                clen = min(kC, yb - yc + 1);
+                __syncthreads();
+                int y0 = (yc - 1) % n;
+                y0 += y0 < 0 ? n : 0;
+                for (int i = tid; i < clen + 2; i += kNT) S.ubuf[i] = ul[((y0 + i) % n) * is];
+                __syncthreads();
+            }
+            if (tid == 0) S.c_src += static_cast<unsigned>(clen);
+            const ChunkArgs ca{S.ubuf, clen, yc - jlo, jspan, ia, hl, hr, dlo, dhi, skt, p.vtab + p.vofs, drift, tau,
+                               nullptr};
+            walk = kstage ? process_chunk<false, true>(S, ca, budget) : process_chunk<false, false>(S, ca, budget);
+            if (!walk) break;  // the walk would cost more than the window: the direct formula
+            yc += clen;
+        }
+        if (!walk && tid == 0 && diag) atomicAdd(diag + 8, 1ull);
+    } else if (tid == 0 && diag) {
+        atomicAdd(diag + 7, 1ull);
+    }
+    if (!walk) {
+        __syncthreads();
+        tile_direct<false>(S, ul, n, 0, n, first, kf, is);
+    }
+    __syncthreads();
+    // epilogue: u^{n+1} = best - tau V; the direct scan where nothing landed (cold)
+    const double* tvl = tv ? tv + line * tv_stride : nullptr;
+    const double sa1l = p.sa1 ? __ldg(p.sa1 + line) : 0.0;
+    const double* sa2 = p.sa2;
+    const double sb = p.sb;
+#pragma unroll 4
+    for (int j = tid; j < n; j += kNT) {
+        const unsigned long long kk = S.keys[j + 1];
+        double best = __longlong_as_double(static_cast<long long>(kk));
+        if (kk == kInfBits) {
+            if (diag) atomicAdd(diag, 1ull);
+            best = INFINITY;
+            int y = (j - first) % n;
+            if (y < 0) y += n;
+            for (int w = 0; w <= 2 * n; ++w) {
+                const double c2 = __dadd_rn(ul[y * is], kf(first + w));
+                best = c2 < best ? c2 : best;
+                y = y == 0 ? n - 1 : y - 1;
+            }
+        }
+        double t = 0.0;
+        if (tvl) t = __ldg(tvl + j);
+        else if (sa2) t = __dmul_rn(tau, __dadd_rn(__dmul_rn(sa1l, __ldg(sa2 + j)), sb));
+        ol[j * os] = __dsub_rn(best, t);
+    }
+    if (tid == 0 && diag) {
+        if (S.mode == kModeWalk) {
+            atomicAdd(diag + 1, static_cast<unsigned long long>(S.c_src));
+            atomicAdd(diag + 2, static_cast<unsigned long long>(S.c_queued));
+            atomicAdd(diag + 3, static_cast<unsigned long long>(S.c_qent));
+        }
+        atomicAdd(diag + 4, 1ull);
+    }
+}
+
 // ---- K2R: resident evolve for short lines --------------------------------
 // One CTA per line keeps the line in shared memory for ALL steps of an evolve
 // call (C1: 2000 steps of n = 1024 in one launch instead of 2000 launch-bound
@@ -1711,6 +1940,49 @@ static FastBuffers make_buffers(void* ws, int64_t lines, int64_t n, int64_t coun
     return b;
 }
 
+int64_t fast_line_max() { return kT; }
+
+int launch_line_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n, const double* drift,
+                    double tau, const double* tv, int64_t tv_stride, const FastSepPot* sep, bool colin, bool colout,
+                    unsigned long long* diag, cudaStream_t s) {
+    if (n < 3 || n > kT) return set_error(ctx, LOB_INVALID_INPUT, "fast line kernel: 3 <= n <= 2048");
+    if ((colin || colout) && lines != n) return set_error(ctx, LOB_INVALID_INPUT, "fast line kernel: columns need lines == n");
+    if (lines < 1 || lines > 0x7fffffffll) return set_error(ctx, LOB_INVALID_INPUT, "fast line kernel: lines");
+    FastParams p = make_params(n, tau, 0.0);
+    p.delta_override = ctx->fast_delta_override;
+    int st = ensure_vtab(ctx, n, tau, &p.vtab, &p.vofs, s);
+    if (st) return st;
+    if (sep) {
+        p.sa1 = sep->a1;
+        p.sa2 = sep->a2;
+        p.sb = sep->b;
+    }
+    using KernT = void (*)(const double*, double*, const double*, const double*, int64_t, unsigned long long*,
+                           FastParams);
+    static const KernT kerns[2][2] = {{line_kernel<false, false>, line_kernel<false, true>},
+                                      {line_kernel<true, false>, line_kernel<true, true>}};
+    auto kern = kerns[colin][colout];
+    if (first_time(ctx, reinterpret_cast<const void*>(kern))) {
+        LOB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(sizeof(MainShared))));
+        LOB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                               cudaSharedmemCarveoutMaxShared));
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(lines));
+    cfg.blockDim = dim3(kNT);
+    cfg.dynamicSmemBytes = sizeof(MainShared);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    LOB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, u, out, drift, tv, tv_stride, diag, p));
+    ctx->launches += 1;
+    return cuda_status(ctx, cudaGetLastError(), "fast line kernel");
+}
+
 int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
                     const double* drift, double tau, const double* tv, int64_t tv_stride,
                     double eta, int64_t* blocks, void* workspace, size_t ws_bytes, int flags,
@@ -1757,6 +2029,22 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     // asked for block counts too (the epilogue predicts the next call from this one)
     if (blocks && !ctx->ws_fsm_valid[workspace]) flags &= ~LOB_FAST_STATS_VALID;
     ctx->ws_last_out[workspace] = out;
+    // short lines without block counts / drift partials: K2L (statistics from the staged line)
+    if (ctx->fast_line && !tab && n <= kT && n >= 3 && !blocks && !dpart && !(flags & kFastStatsGiven)) {
+        const WsLayout wl = ws_layout(lines, n);
+        unsigned long long* dg = reinterpret_cast<unsigned long long*>(static_cast<char*>(workspace) + wl.diag);
+        if (!(flags & LOB_FAST_STATS_VALID))
+            LOB_CUDA_TRY(ctx, cudaMemsetAsync(dg, 0, kDiag * sizeof(unsigned long long), s));
+        ctx->ws_nostats[workspace] = true;  // a later tiled call recomputes its statistics
+        ctx->ws_chain[workspace] = 0;
+        ctx->ws_lc_valid[workspace] = false;
+        const FastSepPot* sp = sep;
+        return launch_line_f64(ctx, u, out, lines, n, drift, tau, tv, tv_stride, sp, false, false, dg, s);
+    }
+    if (ctx->ws_nostats[workspace]) {
+        ctx->ws_nostats[workspace] = false;
+        flags &= ~(LOB_FAST_STATS_VALID | kFastStatsGiven);
+    }
     // the per-line done counters restart with the statistics (keeps them in range)
     if (ctx->ws_chain[workspace] * p.tiles * (kNT / 32) > 0xf0000000ll) flags &= ~LOB_FAST_STATS_VALID;
     int64_t& counter = ctx->ws_counter[workspace];

@@ -34,6 +34,8 @@ struct lob_ctx {
     std::map<const void*, bool> ws_fsm_valid;        // the workspace holds FSM summaries of its last out
     std::map<const void*, const void*> ws_table;     // workspace -> window table of its line constants
     std::map<const void*, bool> ws_lc_valid;         // the workspace holds line constants (mechanical)
+    std::map<const void*, bool> ws_nostats;          // its last call (K2L) left no statistics of its out
+    int fast_line = 2;  // n <= 2048: one CTA per whole line with in-kernel statistics (K2L); 2-D layout 2
     // K1 mode (LOB_DIRECT_SCREENED / LOB_DIRECT_PLAIN) and the screened kernel's
     // count of outputs swept in full fp64 (device counter, lazily allocated)
     int direct_mode = 0;
@@ -156,6 +158,12 @@ int fast_given_stats_buffers(lob_ctx* ctx, void* workspace, int64_t lines, int64
 int launch_transpose_stats(lob_ctx* ctx, const double* src, double* dst, int64_t n, void* workspace,
                            cudaStream_t s);
 int64_t fast_tiles(int64_t n);
+// K2L: one step of short lines (n <= fast_line_max()) with statistics from the staged line itself;
+// colin / colout: line l is column l of an n x n row-major tensor (lines == n)
+int64_t fast_line_max();
+int launch_line_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n, const double* drift,
+                    double tau, const double* tv, int64_t tv_stride, const FastSepPot* sep, bool colin, bool colout,
+                    unsigned long long* diag, cudaStream_t s);
 int launch_drift_tiles(lob_ctx* ctx, const double* dpart, int64_t lines, int64_t n, double* drift_out, int* halt,
                        int step, cudaStream_t s);
 // K2R: all steps of an evolve of short lines (n <= 8192) in one launch, one CTA per line

@@ -23,7 +23,7 @@ for ln in dis.splitlines():
     if m:
         chain = [(m.group(1), int(m.group(2)))] + [(f, int(l)) for f, l in re.findall(r'inlined at "([^"]+)", line (\d+)', m.group(3))]
         outer = [l for f, l in chain if f.endswith(srcbase)]
-        cur = outer[-1] if outer else None
+        cur = (outer[0] if __import__("os").environ.get("INNER") else outer[-1]) if outer else None
         continue
     m = re.search(r"/\*([0-9a-f]{4,})\*/\s+([^;]*);", ln)
     if m and cur_fn and kname in cur_fn:
@@ -56,5 +56,5 @@ for r in data:
 ti = sum(v[0] for v in agg.values()) or 1
 ts = sum(v[1] for v in agg.values()) or 1
 print(f"total warp instr {ti}, stall samples {ts}, opcode mismatches {mism}/{len(data)}")
-for k, v in sorted(agg.items(), key=lambda kv: -kv[1][0])[:30]:
+for k, v in sorted(agg.items(), key=lambda kv: -kv[1][0])[:int(__import__("os").environ.get("TOPN", "30"))]:
     print(f"{k:22s} instr {v[0]/ti*100:5.1f}%  stalls {v[1]/ts*100:5.1f}%")

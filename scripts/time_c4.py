@@ -1,0 +1,52 @@
+"""C4 split step timing, K2L (whole-line kernel, columns in place) vs the tiled fused path,
+and a 20-step trajectory comparison of the two (bit-exact) plus K1.
+usage: python scripts/time_c4.py [--steps K]"""
+import argparse
+import json
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_1210_4090_b200 import api  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--steps", type=int, default=50)
+a = ap.parse_args()
+n, tau = 2048, 0.01
+dev = api.Device(0)
+am = torch.from_numpy(api.gen_cos(n)).cuda()
+u0 = torch.from_numpy(api.gen_c4_u0(n)).cuda()
+ws = torch.empty(2 * dev.fast_workspace_bytes(n, n), dtype=torch.uint8, device="cuda")
+
+
+def run(line, engine, k0, k, u):
+    dev.set_fast_line(line)
+    o, t = torch.empty_like(u), torch.empty_like(u)
+    u = u.clone()
+    for i in range(k0, k0 + k):
+        dev.split_step_2d(u, o, t, tau, 0.3, -0.7, a1=am, a2=am, b=api.c4_time_term(i * tau + tau), engine=engine,
+                          workspace=ws)
+        u, o = o, u
+    return u
+
+
+res = {}
+ref = run(True, api.ENGINE_DIRECT, 0, 20, u0)
+for line in (1, 2, 3, 0):
+    got = run(line, api.ENGINE_FAST, 0, 20, u0)
+    torch.cuda.synchronize()
+    res[f"line={line} == K1 after 20 steps"] = bool(torch.equal(got, ref))
+for line in (1, 2, 3, 0):
+    u = run(line, api.ENGINE_FAST, 0, 5, u0)
+    torch.cuda.synchronize()
+    best = []
+    for r in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        u = run(line, api.ENGINE_FAST, 5, a.steps, u)
+        e1.record()
+        torch.cuda.synchronize()
+        best.append(e0.elapsed_time(e1) / a.steps)
+    res[f"line={line} ms/step"] = sorted(best)
+print(json.dumps(res))
