@@ -301,6 +301,13 @@ int lob_split_step_2d_f64(lob_ctx* ctx, const double* u, double* out, double* tm
                 return st;
             return launch_line_f64(ctx, tmp, out, n, n, d2, tau, nullptr, 0, sp, true, false, nullptr, s);
         }
+        if (ctx->fast_line == 4 && n % 8 == 0) {
+            // axis 0 on columns exchanged through distributed shared memory (clusters of 8 CTAs =
+            // 8 adjacent columns, 64-byte row segments), axis 1 on rows
+            if ((st = launch_line_f64(ctx, u, tmp, n, n, d1, tau, nullptr, 0, nullptr, true, true, nullptr, s, true)))
+                return st;
+            return launch_line_f64(ctx, tmp, out, n, n, d2, tau, nullptr, 0, sp, false, false, nullptr, s);
+        }
         // axis 0 reads and writes the columns of u in place, axis 1 sweeps the rows
         if ((st = launch_line_f64(ctx, u, tmp, n, n, d1, tau, nullptr, 0, nullptr, true, true, nullptr, s))) return st;
         return launch_line_f64(ctx, tmp, out, n, n, d2, tau, nullptr, 0, sp, false, false, nullptr, s);

@@ -44,9 +44,12 @@
 #include <cstring>
 #include <type_traits>
 
+#include <cooperative_groups.h>
+
 #include "lob_internal.cuh"
 
 namespace lob {
+namespace cg = cooperative_groups;
 
 #ifndef LOB_KT
 #define LOB_KT 2048
@@ -1452,7 +1455,9 @@ struct LineShared {  // overlays S.vbuf before the K staging
 };
 static_assert(sizeof(LineShared) <= sizeof(double) * kVCap, "line scratch fits vbuf");
 
-template <bool COLIN, bool COLOUT>
+constexpr int kLC = 8;  // CTAs (= adjacent columns) per cluster of the column-exchange variant
+
+template <bool COLIN, bool COLOUT, bool CLU>
 __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* __restrict__ u, double* __restrict__ out,
                                                                   const double* __restrict__ drift_arr,
                                                                   const double* __restrict__ tv, int64_t tv_stride,
@@ -1470,7 +1475,23 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
     asm volatile("griddepcontrol.wait;" ::: "memory");
     // the line into shared memory (the keys area: U[j], j < n <= kT)
     double* U = reinterpret_cast<double*>(S.keys);
-    for (int j = tid; j < n; j += kNT) U[j] = ul[j * is];
+    if constexpr (CLU) {
+        // a cluster of kLC CTAs holds kLC adjacent columns c0 .. c0 + kLC - 1; CTA r reads rows
+        // [r n/kLC, (r+1) n/kLC) of all kLC columns (64-byte row segments) and stores each value
+        // into its column's CTA through distributed shared memory
+        cg::cluster_group cluster = cg::this_cluster();
+        const int r = static_cast<int>(cluster.block_rank());
+        const int64_t c0 = line - r;
+        const int rows = n / kLC;
+        cluster.sync();  // every CTA of the cluster runs: its shared memory may be written
+        for (int e = tid; e < rows * kLC; e += kNT) {
+            const int row = r * rows + e / kLC, col = e % kLC;
+            *cluster.map_shared_rank(U + row, col) = u[static_cast<int64_t>(row) * p.n + c0 + col];
+        }
+        cluster.sync();
+    } else {
+        for (int j = tid; j < n; j += kNT) U[j] = ul[j * is];
+    }
     if (tid == 0) {
         const LineConst c = line_const(__ldg(drift_arr + line), p);
         L.hl = c.hl;
@@ -1612,6 +1633,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
     const double sa1l = p.sa1 ? __ldg(p.sa1 + line) : 0.0;
     const double* sa2 = p.sa2;
     const double sb = p.sb;
+    double* ostage = S.ubuf;  // CLU && COLOUT: the new line, for the cluster's row-segment stores
 #pragma unroll 4
     for (int j = tid; j < n; j += kNT) {
         const unsigned long long kk = S.keys[j + 1];
@@ -1630,7 +1652,21 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
         double t = 0.0;
         if (tvl) t = __ldg(tvl + j);
         else if (sa2) t = __dmul_rn(tau, __dadd_rn(__dmul_rn(sa1l, __ldg(sa2 + j)), sb));
-        ol[j * os] = __dsub_rn(best, t);
+        const double o = __dsub_rn(best, t);
+        if constexpr (CLU && COLOUT) ostage[j] = o;
+        else ol[j * os] = o;
+    }
+    if constexpr (CLU && COLOUT) {
+        cg::cluster_group cluster = cg::this_cluster();
+        const int r = static_cast<int>(cluster.block_rank());
+        const int64_t c0 = line - r;
+        const int rows = n / kLC;
+        cluster.sync();
+        for (int e = tid; e < rows * kLC; e += kNT) {
+            const int row = r * rows + e / kLC, col = e % kLC;
+            out[static_cast<int64_t>(row) * p.n + c0 + col] = *cluster.map_shared_rank(ostage + row, col);
+        }
+        cluster.sync();  // no CTA leaves while its line is still being read
     }
     if (tid == 0 && diag) {
         if (S.mode == kModeWalk) {
@@ -1944,8 +1980,10 @@ int64_t fast_line_max() { return kT; }
 
 int launch_line_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n, const double* drift,
                     double tau, const double* tv, int64_t tv_stride, const FastSepPot* sep, bool colin, bool colout,
-                    unsigned long long* diag, cudaStream_t s) {
+                    unsigned long long* diag, cudaStream_t s, bool cluster) {
     if (n < 3 || n > kT) return set_error(ctx, LOB_INVALID_INPUT, "fast line kernel: 3 <= n <= 2048");
+    if (cluster && (!(colin || colout) || n % kLC != 0))
+        return set_error(ctx, LOB_INVALID_INPUT, "fast line kernel: cluster columns need n % 8 == 0");
     if ((colin || colout) && lines != n) return set_error(ctx, LOB_INVALID_INPUT, "fast line kernel: columns need lines == n");
     if (lines < 1 || lines > 0x7fffffffll) return set_error(ctx, LOB_INVALID_INPUT, "fast line kernel: lines");
     FastParams p = make_params(n, tau, 0.0);
@@ -1959,9 +1997,11 @@ int launch_line_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     }
     using KernT = void (*)(const double*, double*, const double*, const double*, int64_t, unsigned long long*,
                            FastParams);
-    static const KernT kerns[2][2] = {{line_kernel<false, false>, line_kernel<false, true>},
-                                      {line_kernel<true, false>, line_kernel<true, true>}};
-    auto kern = kerns[colin][colout];
+    static const KernT kerns[2][2][2] = {{{line_kernel<false, false, false>, line_kernel<false, false, false>},
+                                          {line_kernel<false, true, false>, line_kernel<false, true, true>}},
+                                         {{line_kernel<true, false, false>, line_kernel<true, false, true>},
+                                          {line_kernel<true, true, false>, line_kernel<true, true, true>}}};
+    auto kern = kerns[colin][colout][cluster];
     if (first_time(ctx, reinterpret_cast<const void*>(kern))) {
         LOB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(sizeof(MainShared))));
@@ -1973,11 +2013,15 @@ int launch_line_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     cfg.blockDim = dim3(kNT);
     cfg.dynamicSmemBytes = sizeof(MainShared);
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = kLC;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = cluster ? 2 : 1;
     LOB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, u, out, drift, tv, tv_stride, diag, p));
     ctx->launches += 1;
     return cuda_status(ctx, cudaGetLastError(), "fast line kernel");

@@ -163,7 +163,7 @@ int64_t fast_tiles(int64_t n);
 int64_t fast_line_max();
 int launch_line_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n, const double* drift,
                     double tau, const double* tv, int64_t tv_stride, const FastSepPot* sep, bool colin, bool colout,
-                    unsigned long long* diag, cudaStream_t s);
+                    unsigned long long* diag, cudaStream_t s, bool cluster = false);
 int launch_drift_tiles(lob_ctx* ctx, const double* dpart, int64_t lines, int64_t n, double* drift_out, int* halt,
                        int step, cudaStream_t s);
 // K2R: all steps of an evolve of short lines (n <= 8192) in one launch, one CTA per line

@@ -3,14 +3,15 @@
 //   axis 0 (columns, kernel 1) -> axis 1 (rows, kernel 2) -> out -= tau*V.
 // The reference gathers each strided column into a temporary line and
 // scatters it back (proj/src/splitting.cpp:67-76).  Here a tiled transpose
-// (32x64 tiles through shared memory, coalesced 128-bit global accesses on
-// both sides) turns columns into rows so both sweeps run the batched line
-// kernels; the potential pass evaluates the separable descriptor
+// (64x64 tiles through shared memory, 16-byte global accesses on both sides
+// for even n; 32x32 scalar tiles otherwise) turns columns into rows so both
+// sweeps run the batched line kernels; the potential pass evaluates the separable descriptor
 // V = a1[i]*a2[k] + b with the C++ expression's roundings and applies
 // out = out - tau*V (two roundings, no FMA; proj/src/splitting.cpp:95).
 // Also: the per-step drift / finiteness check of evolve
 // (proj/src/scheme.cpp:244-264).
 #include <algorithm>
+#include <cstdint>
 
 #include "lob_internal.cuh"
 
@@ -33,6 +34,37 @@ __global__ void __launch_bounds__(256) transpose_kernel(const double* __restrict
     for (int r = ty; r < kTD; r += 8) {
         const int64_t k = bx + r, i = by + tx;  // dst[k][i] = src[i][k]
         if (i < n && k < n) dst[k * n + i] = tile[tx][r];
+    }
+}
+
+// 64 x 64 tiles, 256 threads, double2 loads and stores (even n, 16-byte aligned rows); the
+// tile pitch of 65 doubles keeps the column reads at two wavefronts per half warp.  Launched
+// with programmatic dependent launch: the previous kernel's tail overlaps this prologue.
+constexpr int kTV = 64;
+__global__ void __launch_bounds__(256) transpose64_kernel(const double* __restrict__ src,
+                                                          double* __restrict__ dst, int64_t n) {
+    __shared__ double tile[kTV][kTV + 1];
+    const int64_t bx = static_cast<int64_t>(blockIdx.x) * kTV;  // column block of src
+    const int64_t by = static_cast<int64_t>(blockIdx.y) * kTV;  // row block of src
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int64_t k = bx + 2 * lane;
+#pragma unroll
+    for (int r = w; r < kTV; r += 8) {
+        const int64_t i = by + r;
+        double2 v = make_double2(0.0, 0.0);
+        if (i < n && k < n) v = *reinterpret_cast<const double2*>(src + i * n + k);
+        tile[r][2 * lane] = v.x;
+        tile[r][2 * lane + 1] = v.y;
+    }
+    __syncthreads();
+    const int64_t i = by + 2 * lane;
+#pragma unroll
+    for (int c = w; c < kTV; c += 8) {
+        const int64_t kk = bx + c;  // dst[kk][i] = src[i][kk]
+        if (kk < n && i < n)
+            *reinterpret_cast<double2*>(dst + kk * n + i) = make_double2(tile[2 * lane][c], tile[2 * lane + 1][c]);
     }
 }
 
@@ -145,6 +177,20 @@ int launch_sub_table(lob_ctx* ctx, double* out, const double* tv, int64_t count,
 }
 
 int launch_transpose(lob_ctx* ctx, const double* src, double* dst, int64_t n, cudaStream_t s) {
+    if (n % 2 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>((n + kTV - 1) / kTV), static_cast<unsigned>((n + kTV - 1) / kTV));
+        cfg.blockDim = dim3(256);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        LOB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, transpose64_kernel, src, dst, n));
+        ctx->launches += 1;
+        return cuda_status(ctx, cudaGetLastError(), "transpose64_kernel");
+    }
     dim3 grid(static_cast<unsigned>((n + kTD - 1) / kTD), static_cast<unsigned>((n + kTD - 1) / kTD));
     transpose_kernel<<<grid, 256, 0, s>>>(src, dst, n);
     ctx->launches += 1;

@@ -13,6 +13,14 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-12
 
 
+@pytest.fixture(params=[2, 0], ids=["K2L", "tiled"])
+def kernel_mode(request, dev):
+    """Short lines (n <= 2048) through the whole-line kernel (K2L, default) and the tiled one."""
+    dev.set_fast_line(request.param)
+    yield request.param
+    dev.set_fast_line(2)
+
+
 def to_dev(x):
     import torch
     return torch.from_numpy(np.ascontiguousarray(x)).cuda()
@@ -73,7 +81,7 @@ def rough_walk(rng, lines, n, scale):
 
 @pytest.mark.parametrize("drift", [0.0, 0.4, -0.7, 1.0])
 @pytest.mark.parametrize("n,tau", [(24, 0.25), (48, 0.125), (600, 0.04), (1024, 0.05), (4096, 0.01)])
-def test_fast_random_vs_oracle(dev, orc, n, tau, drift):
+def test_fast_random_vs_oracle(dev, orc, n, tau, drift, kernel_mode):
     """Random walks scaled so the walk runs them (asserted): bit-exact, block counts too."""
     rng = np.random.default_rng(n + int(drift * 10))
     u = rough_walk(rng, 4, n, 4.0)
@@ -86,7 +94,7 @@ def test_fast_random_vs_oracle(dev, orc, n, tau, drift):
 
 @pytest.mark.parametrize("drift", [0.0, -0.7])
 @pytest.mark.parametrize("n,tau", [(600, 0.04), (1024, 0.05), (4096, 0.01)])
-def test_fast_uniform_noise_takes_direct_route(dev, orc, n, tau, drift):
+def test_fast_uniform_noise_takes_direct_route(dev, orc, n, tau, drift, kernel_mode):
     """uniform(-1, 1) samples: every source's interval spans most of the window, so the
     walk would cost more than the direct formula; its work budget sends the tiles to the
     in-kernel direct sweep (counted), still bit-exact."""
@@ -99,7 +107,7 @@ def test_fast_uniform_noise_takes_direct_route(dev, orc, n, tau, drift):
     assert c["missed_outputs"] == 0, c
 
 
-def test_fast_gate_failure_takes_direct_route(dev, orc):
+def test_fast_gate_failure_takes_direct_route(dev, orc, kernel_mode):
     """Oscillation above the window's edge gap (max u - min u >= min(K(first), K(last)) -
     min K): window-edge minima are possible, the walk does not apply; the tiles take the
     direct formula (counted), bit-exact."""
@@ -114,7 +122,7 @@ def test_fast_gate_failure_takes_direct_route(dev, orc):
 
 
 @pytest.mark.parametrize("drift", [130.0, -150.0, 2.5e3])
-def test_fast_large_drift_window_outside_vtab(dev, orc, drift):
+def test_fast_large_drift_window_outside_vtab(dev, orc, drift, kernel_mode):
     """|tau P| > 2: the window [center - n, center + n] leaves the cached v_d table
     (d in [-3n, 3n]); the tiles compute K with build_kernel's own roundings on the direct
     route instead of reading past the table (counted), bit-exact."""
@@ -284,7 +292,7 @@ def test_fast_equals_direct_c5_full_line(dev):
 
 
 @pytest.mark.parametrize("n,offset", [(4097, 0), (6001, 0), (8192, 1), (5000, 1), (2050, 0)])
-def test_fast_odd_lengths_and_unaligned_rows(dev, orc, n, offset):
+def test_fast_odd_lengths_and_unaligned_rows(dev, orc, n, offset, kernel_mode):
     """Odd n (rows not 16-byte aligned for bulk copies), rows starting at an odd
     element offset, and partial last tiles: the cooperative-load path, == oracle."""
     import torch
@@ -384,7 +392,7 @@ def _structured_lines(n, rng):
 
 @pytest.mark.parametrize("n,tau", [(64, 0.1), (1000, 0.03), (4096, 0.01)])
 @pytest.mark.parametrize("drift", [0.0, 0.85])
-def test_fast_structured_inputs_bit_exact(dev, orc, n, tau, drift):
+def test_fast_structured_inputs_bit_exact(dev, orc, n, tau, drift, kernel_mode):
     """Constant, tied, discontinuous, huge and spiky lines through K2 == the oracle's
     direct sweep bit for bit, with block counts == decompose()'s; the cold fallback
     count is reported, never required to be zero (exactness is the contract)."""
@@ -408,7 +416,7 @@ def test_fast_structured_inputs_bit_exact(dev, orc, n, tau, drift):
 
 
 @pytest.mark.parametrize("delta", [-0.75, -0.25])
-def test_shrunk_delta_bound_makes_the_walk_miss(dev, orc, delta):
+def test_shrunk_delta_bound_makes_the_walk_miss(dev, orc, delta, kernel_mode):
     """The rounding bound delta is load-bearing: with the local-minimum intervals shrunk below
     it the walk loses minimisers — outputs that no interval reaches (counted, rescued by the
     exact scan) and, worse, outputs that some other source still reaches with a larger value

@@ -117,9 +117,11 @@ def test_window_table_change_recomputes_statistics(dev, orc):
     assert dev.fast_counters(ws, 2, n)["stale_line_constants"] > 0
 
 
-def test_drift_changed_in_place_is_detected(dev, orc):
+@pytest.mark.parametrize("line_kernel", [False, True])
+def test_drift_changed_in_place_is_detected(dev, orc, line_kernel):
     """lob_minplus_fast_f64 with carried statistics after the drift array was rewritten in place:
-    the tiles see the mismatch, take the direct formula with the current drift (exact), counted."""
+    the tiles see the mismatch, take the direct formula with the current drift (exact), counted.
+    The whole-line kernel (K2L, n <= 2048) carries nothing: it reads the current drift."""
     import torch
     n, tau = 2048, 0.02
     rng = np.random.default_rng(9)
@@ -127,9 +129,17 @@ def test_drift_changed_in_place_is_detected(dev, orc):
     dd = to_dev(np.full(3, 0.2))
     x, y = torch.empty_like(du), torch.empty_like(du)
     ws = torch.empty(dev.fast_workspace_bytes(3, n), dtype=torch.uint8, device="cuda")
-    dev.fast_f64(du, x, dd, tau, workspace=ws)
-    dd.fill_(-1.3)
-    dev.fast_f64(x, y, dd, tau, workspace=ws, flags=api.FAST_STATS_VALID)
-    torch.cuda.synchronize()
+    dev.set_fast_line(line_kernel)
+    try:
+        dev.fast_f64(du, x, dd, tau, workspace=ws)
+        dd.fill_(-1.3)
+        dev.fast_f64(x, y, dd, tau, workspace=ws, flags=api.FAST_STATS_VALID)
+        torch.cuda.synchronize()
+    finally:
+        dev.set_fast_line(2)
     assert np.array_equal(y.cpu().numpy(), oracle_step(orc, x.cpu().numpy(), -1.3, tau))
-    assert dev.fast_counters(ws, 3, n)["stale_line_constants"] > 0
+    c = dev.fast_counters(ws, 3, n)
+    if line_kernel:
+        assert c["stale_line_constants"] == 0 and c["missed_outputs"] == 0, c
+    else:
+        assert c["stale_line_constants"] > 0, c
