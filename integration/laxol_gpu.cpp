@@ -277,4 +277,160 @@ laxol::EvolutionTrace Device::evolve(const laxol::GridFn& u0, double t0, std::in
     return trace;
 }
 
+
+laxol::TensorFn Device::split_step_nd(const laxol::TensorFn& u, double t, const laxol::SplitSpec& spec,
+                                      const laxol::SchemeParams& params, Engine engine) {
+    // the reference's argument checks (proj/src/splitting.cpp:39-50), same messages
+    if (spec.kinetics.size() != u.rank())
+        throw laxol::InvalidInput("split_step_nd: kinetic part is not separable over the tensor axes (" +
+                                  std::to_string(spec.kinetics.size()) + " conjugates for rank " +
+                                  std::to_string(u.rank()) + ")");
+    if (u.step != params.epsilon())
+        throw laxol::InvalidInput("split_step_nd: tensor step does not match params.epsilon()");
+    if (u.periodic) {
+        for (std::size_t d : u.dims)
+            if (d != static_cast<std::size_t>(params.n_space))
+                throw laxol::InvalidInput("split_step_nd: periodic axes must hold one unit period");
+    }
+    Impl& I = *impl_;
+    const int rank = static_cast<int>(u.rank());
+    const std::int64_t n = params.n_space, W = 2 * n + 1;
+    // per-axis windows: the reference's build_kernel (proj/src/splitting.cpp:55)
+    std::vector<double> ktabs(static_cast<std::size_t>(rank * W));
+    std::vector<std::int64_t> firsts(rank), dims(rank);
+    std::vector<double> drifts(rank);
+    bool mechanical = true;
+    for (int a = 0; a < rank; ++a) {
+        const laxol::Kernel k = laxol::build_kernel(spec.kinetics[a], params);
+        if (k.window.size() != static_cast<std::size_t>(W))
+            throw laxol::InvalidInput("split_step_nd: kernel window must hold 2 n_space + 1 samples");
+        std::copy(k.window.values.begin(), k.window.values.end(), ktabs.begin() + a * W);
+        firsts[a] = k.center_index - n;
+        drifts[a] = spec.kinetics[a].drift;
+        dims[a] = static_cast<std::int64_t>(u.dims[a]);
+        mechanical = mechanical && spec.kinetics[a].kind == laxol::Kinetic::Kind::Mechanical;
+    }
+    // tau*V of every point, the reference's loop (proj/src/splitting.cpp:79-97)
+    const std::size_t total = u.size();
+    std::vector<double> tv;
+    if (spec.potential) {
+        tv.resize(total);
+        const double tt = params.v_sampling == laxol::PotentialSampling::Arrival ? t + params.tau : t;
+        std::vector<std::size_t> strides(rank, 1);
+        for (int a = rank - 1; a > 0; --a) strides[a - 1] = strides[a] * u.dims[a];
+        std::vector<double> coords(rank);
+        for (std::size_t flat = 0; flat < total; ++flat) {
+            std::size_t rem = flat;
+            for (int a = 0; a < rank; ++a) {
+                const std::size_t idx = rem / strides[a];
+                rem %= strides[a];
+                coords[a] = u.origins[a] + static_cast<double>(idx) * u.step;
+            }
+            const double v = spec.potential(tt, coords);
+            if (!std::isfinite(v)) throw laxol::EvaluationError("split_step_nd: potential sample is not finite");
+            tv[flat] = params.tau * v;
+        }
+    }
+    DevBuf tmpb;
+    const double* du = I.up(I.u, u.values.data(), total);
+    double* dout = static_cast<double*>(I.out.get(total * sizeof(double)));
+    double* dtmp = static_cast<double*>(tmpb.get(total * sizeof(double)));
+    const double* dk = I.up(I.ktab, ktabs.data(), ktabs.size());
+    const double* dtv = spec.potential ? I.up(I.tv, tv.data(), total) : nullptr;
+    if (u.periodic) {
+        int eng = LOB_ENGINE_DIRECT;
+        if (engine == Engine::GpuFast) eng = (params.eta > 0.0 || !mechanical) ? LOB_ENGINE_RELAXED : LOB_ENGINE_FAST;
+        std::size_t wb = 0;
+        void* ws = nullptr;
+        if (eng == LOB_ENGINE_FAST) {
+            I.ok(lob_fast_workspace_bytes(static_cast<std::int64_t>(total) / n, n, &wb), "split_step_nd");
+            ws = I.ws.get(wb);
+        }
+        I.ok(lob_split_step_nd_f64(I.ctx, du, dout, dtmp, rank, n, params.tau, dk, firsts.data(), drifts.data(), dtv,
+                                   params.eta, eng, ws, wb, I.stream),
+             "split_step_nd");
+    } else {
+        // the wall branch (proj/src/scheme.cpp:135-144): the exact windowed sweeps; ConvEngine::Fast with
+        // eta > 0 is the reference's relaxed approximation, which runs periodic lines only here
+        if (engine == Engine::GpuFast && params.eta > 0.0)
+            throw laxol::InvalidInput(
+                "split_step_nd: the relaxed (eta > 0) fast engine runs periodic tensors; use GpuDirect or eta = 0");
+        I.ok(lob_split_step_nd_window_f64(I.ctx, du, dout, dtmp, rank, dims.data(), n, params.tau, dk, firsts.data(),
+                                          dtv, I.stream),
+             "split_step_nd");
+    }
+    laxol::TensorFn out = u;
+    I.down(out.values.data(), dout, total);
+    return out;
+}
+
+laxol::GridFn Device::step_semidiscrete(const laxol::GridFn& u, double t, const laxol::HamiltonianSpec& spec,
+                                        const laxol::SchemeParams& params, int quad_points) {
+    if (quad_points < 1) throw laxol::InvalidInput("step_semidiscrete: quad_points must be >= 1");
+    check_u_grid(u, params, "step_semidiscrete");
+    const laxol::Kernel kernel = laxol::build_kernel(spec, params);
+    Impl& I = *impl_;
+    const double tau = params.tau;
+    const std::int64_t n = params.n_space, period = static_cast<std::int64_t>(u.n());
+    const std::int64_t first = kernel.center_index - static_cast<std::int64_t>(kernel.window.n() / 2);
+    const std::size_t m = u.periodic ? u.n() : u.size();  // fundamental samples (sources and outputs)
+    const laxol::Potential& V = spec.potential;
+    std::vector<double> out(u.size());
+    if (V.kind == laxol::Potential::Kind::Zero || V.kind == laxol::Potential::Kind::Const) {
+        // V integrates exactly on the device for these kinds
+        lob_potential lp{};
+        lp.kind = V.kind == laxol::Potential::Kind::Zero ? LOB_POTENTIAL_ZERO : LOB_POTENTIAL_CONST;
+        lp.value = V.value;
+        const double* du = I.up(I.u, u.values.data(), m);
+        const double* dk = I.up(I.ktab, kernel.window.values.data(), kernel.window.size());
+        double* dout = static_cast<double*>(I.out.get(m * sizeof(double)));
+        I.ok(lob_step_semidiscrete_f64(I.ctx, du, dout, 1, static_cast<std::int64_t>(m), n, u.periodic ? 1 : 0,
+                                       u.origin, dk, first, t, tau, &lp, quad_points, I.stream),
+             "step_semidiscrete");
+        I.down(out.data(), dout, m);
+    } else {
+        // the candidate costs with the reference's callbacks and IEEE order (proj/src/scheme.cpp:180-196),
+        // C[y][j] = min over the windows' displacements d with source y of cost(j, d); the minimum over
+        // sources min_y u[y] + C[y][j] is the reference's min over d (fl() is monotone)
+        const int q = quad_points;
+        constexpr double kInf = std::numeric_limits<double>::infinity();
+        std::vector<double> C(m * m, kInf);
+        for (std::size_t j = 0; j < m; ++j) {
+            const double x = sample_coord(u, j);
+            for (std::size_t w = 0; w < kernel.window.size(); ++w) {
+                const std::int64_t d = first + static_cast<std::int64_t>(w);
+                const std::int64_t src = static_cast<std::int64_t>(j) - d;
+                std::int64_t src_idx = src;
+                if (u.periodic)
+                    src_idx = ((src % period) + period) % period;
+                else if (src < 0 || src >= static_cast<std::int64_t>(u.size()))
+                    continue;
+                const double y = x - static_cast<double>(d) * u.step;
+                double acc = 0.5 * (V(t, y) + V(t + tau, x));
+                for (int r = 1; r < q; ++r) {
+                    const double frac = static_cast<double>(r) / static_cast<double>(q);
+                    acc += V(t + frac * tau, y + frac * (x - y));
+                }
+                const double integral = tau / static_cast<double>(q) * acc;
+                const double cost = kernel.window.values[w] - integral;
+                double& c = C[static_cast<std::size_t>(src_idx) * m + j];
+                c = std::min(c, cost);
+            }
+        }
+        DevBuf cb;
+        double* dC = static_cast<double*>(cb.get(C.size() * sizeof(double)));
+        check_cuda(cudaMemcpyAsync(dC, C.data(), C.size() * sizeof(double), cudaMemcpyHostToDevice, I.stream), "upload");
+        const double* du = I.up(I.u, u.values.data(), m);
+        double* dout = static_cast<double*>(I.out.get(m * sizeof(double)));
+        const std::int64_t mm = static_cast<std::int64_t>(m);
+        I.ok(lob_minplus_gemm_f64(I.ctx, du, mm, dC, mm, dout, mm, 1, mm, mm, I.stream), "step_semidiscrete");
+        I.down(out.data(), dout, m);
+    }
+    for (std::size_t j = 0; j < m; ++j)
+        if (out[j] == std::numeric_limits<double>::infinity())
+            throw laxol::EvaluationError("step_semidiscrete: no candidate source for grid index " + std::to_string(j));
+    if (u.periodic) out[m] = out[0];  // x and the sources of j = n are those of j = 0
+    return laxol::GridFn{std::move(out), u.step, u.origin, u.periodic};
+}
+
 }  // namespace laxol_gpu

@@ -25,6 +25,7 @@
 #include <memory>
 
 #include "laxol/scheme.hpp"
+#include "laxol/splitting.hpp"
 
 namespace laxol_gpu {
 
@@ -52,6 +53,24 @@ public:
     laxol::EvolutionTrace evolve(const laxol::GridFn& u0, double t0, std::int64_t steps,
                                  const laxol::HamiltonianSpec& spec, const laxol::SchemeParams& params,
                                  Engine engine, const laxol::EvolveOptions& options = {});
+
+    // split_step_nd (proj/include/laxol/splitting.hpp:40-41, proj/src/splitting.cpp:37-99): the
+    // axis sweeps in the reference's order on the device (periodic: K2 / relaxed / K1 per
+    // lob_split_step_nd_f64; windowed: the exact wall-branch sweeps), tau*V of every point from
+    // the reference's PotentialNd callback on the host, subtracted once on the device.  The
+    // reference hard-wires ConvEngine::Fast (splitting.cpp:75); `engine` widens it like the
+    // other entry points.  Periodic tensors hold n_space samples per axis (the reference's check).
+    laxol::TensorFn split_step_nd(const laxol::TensorFn& u, double t, const laxol::SplitSpec& spec,
+                                  const laxol::SchemeParams& params, Engine engine = Engine::GpuFast);
+
+    // step_semidiscrete (proj/include/laxol/scheme.hpp:63-64, proj/src/scheme.cpp:166-206) for every
+    // Potential kind of the spec: Zero / Const through the device kernel that integrates V itself
+    // (lob_step_semidiscrete_f64); Cosine and Custom potentials (any std::function) through the
+    // reference's own callbacks on the host -- the candidate costs K[w] - tau/q * trapezoid(V), in
+    // its IEEE order, folded over periodic aliases into a source x target matrix -- and the
+    // minimum over sources on the device (the tropical GEMM, lob_minplus_gemm_f64).
+    laxol::GridFn step_semidiscrete(const laxol::GridFn& u, double t, const laxol::HamiltonianSpec& spec,
+                                    const laxol::SchemeParams& params, int quad_points);
 
 private:
     struct Impl;

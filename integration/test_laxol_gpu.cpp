@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <numbers>
 #include <random>
+#include <span>
 #include <string>
 #include <vector>
 
@@ -14,6 +15,7 @@
 #include "laxol/grid_fn.hpp"
 #include "laxol/hamiltonian.hpp"
 #include "laxol/scheme.hpp"
+#include "laxol/splitting.hpp"
 #include "laxol_gpu.hpp"
 
 using laxol_gpu::Engine;
@@ -27,6 +29,16 @@ static void report(const std::string& name, bool ok) {
 
 static bool same(const laxol::GridFn& a, const laxol::GridFn& b) {
     if (a.values.size() != b.values.size() || a.step != b.step || a.origin != b.origin || a.periodic != b.periodic)
+        return false;
+    for (std::size_t i = 0; i < a.values.size(); ++i)
+        if (!(a.values[i] == b.values[i])) return false;
+    return true;
+}
+
+
+static bool same_t(const laxol::TensorFn& a, const laxol::TensorFn& b) {
+    if (a.values.size() != b.values.size() || a.dims != b.dims || a.step != b.step || a.origins != b.origins ||
+        a.periodic != b.periodic)
         return false;
     for (std::size_t i = 0; i < a.values.size(); ++i)
         if (!(a.values[i] == b.values[i])) return false;
@@ -181,6 +193,91 @@ int main() {
                 ok = got.per_step[i].drift == want.per_step[i].drift && got.per_step[i].blocks == want.per_step[i].blocks &&
                      got.per_step[i].time == want.per_step[i].time;
             report(std::string("evolve C1 2000 steps ") + (e == Engine::GpuFast ? "GpuFast" : "GpuDirect"), ok);
+        }
+    }
+    // 7. split_step_nd over laxol::TensorFn / SplitSpec / PotentialNd == the reference's split_step_nd
+    {
+        const laxol::PotentialNd vnd = [&](double t, std::span<const double> x) {
+            double v = 0.2 * std::sin(kTwoPi * t);
+            double c = 1.0;
+            for (double xi : x) c *= std::cos(kTwoPi * xi);
+            return c + v;
+        };
+        for (int rank : {2, 3}) {
+            const int n = rank == 2 ? 64 : 16;
+            for (double eta : {0.0, 1e-7}) {
+                const laxol::SchemeParams p = params_of(n, rank == 2 ? 0.02 : 0.1, eta);  // eps/tau < 1 (anti-CFL)
+                std::size_t total = 1;
+                for (int a = 0; a < rank; ++a) total *= static_cast<std::size_t>(n);
+                std::vector<double> vals(total);
+                std::mt19937_64 g(77 + rank);
+                std::uniform_real_distribution<double> ud(-0.5, 0.5);
+                for (std::size_t i = 0; i < total; ++i) {
+                    const double x0 = static_cast<double>(i / (total / n)) / n;
+                    vals[i] = std::sin(kTwoPi * x0) + 0.01 * ud(g);
+                }
+                const laxol::TensorFn u = laxol::make_tensor(vals, std::vector<std::size_t>(rank, n), p.epsilon(),
+                                                             std::vector<double>(rank, 0.0), true);
+                laxol::SplitSpec spec;
+                for (int a = 0; a < rank; ++a) spec.kinetics.push_back(laxol::mechanical(a == 0 ? 0.3 : -0.7 + 0.2 * a));
+                if (rank == 3) {  // a tabulated convex conjugate on the last axis (velocities 100 = 1/tau)
+                    std::vector<double> tab;
+                    for (int i = 0; i <= 240; ++i) tab.push_back(0.5 * (i - 120.0) * (i - 120.0) + 0.1 * (i - 120.0));
+                    spec.kinetics[2] = laxol::tabulated(tab, -120.0, 1.0);
+                }
+                spec.potential = vnd;
+                const laxol::TensorFn want = laxol::split_step_nd(u, 0.25, spec, p);
+                for (Engine e : {Engine::GpuFast, Engine::GpuDirect}) {
+                    if (e == Engine::GpuDirect && eta > 0.0) continue;  // Naive != the relaxed Fast for eta > 0
+                    const laxol::TensorFn got = dev.split_step_nd(u, 0.25, spec, p, e);
+                    report("split_step_nd periodic rank " + std::to_string(rank) + (eta > 0.0 ? " eta 1e-7" : " eta 0") +
+                               (e == Engine::GpuFast ? " GpuFast" : " GpuDirect"),
+                           same_t(got, want));
+                }
+            }
+        }
+        // windowed (wall) 2-D tensor with origins, eta = 0
+        const laxol::SchemeParams p = params_of(50, 0.03);
+        std::vector<double> vals(37 * 41);
+        for (std::size_t i = 0; i < vals.size(); ++i) vals[i] = 0.3 * std::cos(0.1 * static_cast<double>(i % 41)) + 0.01 * (i / 41);
+        const laxol::TensorFn u = laxol::make_tensor(vals, {37, 41}, p.epsilon(), {0.25, -0.5}, false);
+        laxol::SplitSpec spec{{laxol::mechanical(0.1), laxol::mechanical(-0.4)}, vnd};
+        const laxol::TensorFn want = laxol::split_step_nd(u, 0.1, spec, p);
+        report("split_step_nd windowed 37x41", same_t(dev.split_step_nd(u, 0.1, spec, p, Engine::GpuFast), want) &&
+                                                   same_t(dev.split_step_nd(u, 0.1, spec, p, Engine::GpuDirect), want));
+        bool threw = false;
+        try {
+            laxol::SplitSpec bad{{laxol::mechanical(0.0)}, {}};
+            dev.split_step_nd(u, 0.0, bad, p);
+        } catch (const laxol::InvalidInput&) {
+            threw = true;
+        }
+        report("split_step_nd InvalidInput on a non-separable spec", threw);
+    }
+    // 8. step_semidiscrete with every potential kind (Custom: any std::function) == the reference
+    {
+        const int n = 96;
+        const laxol::SchemeParams p = params_of(n, 0.05);
+        std::vector<double> u0(n);
+        for (int j = 0; j < n; ++j) u0[j] = std::sin(kTwoPi * j / n) + 0.3 * std::cos(3.0 * kTwoPi * j / n);
+        const laxol::GridFn u = laxol::make_periodic(u0, p.epsilon());
+        std::vector<double> w0(70);
+        for (int j = 0; j < 70; ++j) w0[j] = 0.2 * std::sin(0.2 * j);
+        const laxol::GridFn uw{w0, p.epsilon(), -0.3, false};
+        const std::vector<std::pair<std::string, laxol::Potential>> pots = {
+            {"zero", laxol::potential_zero()},
+            {"const", laxol::potential_const(0.75)},
+            {"cosine", laxol::potential_cosine(0.1, 0.8, 2, laxol::Potential::TimeMod::Sin, 3.0)},
+            {"custom", laxol::potential_custom(
+                           [](double t, double x) { return std::exp(-x * x) * (1.0 + 0.5 * std::sin(7.0 * t)) + 0.3 * std::sin(5.0 * x); },
+                           2.0, true)}};
+        for (const auto& [name, V] : pots) {
+            const laxol::HamiltonianSpec spec = laxol::make_spec(laxol::mechanical(0.4), V, true, false);
+            for (int q : {1, 3}) {
+                const bool ok = same(dev.step_semidiscrete(u, 0.3, spec, p, q), laxol::step_semidiscrete(u, 0.3, spec, p, q)) &&
+                                same(dev.step_semidiscrete(uw, 0.3, spec, p, q), laxol::step_semidiscrete(uw, 0.3, spec, p, q));
+                report("step_semidiscrete " + name + " q=" + std::to_string(q) + " periodic + windowed", ok);
+            }
         }
     }
     // 6. the reference's argument errors surface as its own exception types
