@@ -88,6 +88,10 @@ def c1(dev):
         sb = torch.empty(steps, dtype=torch.int64, device="cuda")
         ws = torch.empty(dev.fast_workspace_bytes(1, n), dtype=torch.uint8, device="cuda")
         tv = dev_t(api.tau_v(g["v"], tau))
+        # one untimed step first: module loading and one-time kernel setup stay out of the timing
+        w = dev_t(g["u0"][None, :])
+        dev.evolve(w, torch.empty_like(w), dev_t(np.array([0.5])), tau, 1, tv=tv, engine=eng, workspace=ws)
+        torch.cuda.synchronize()
         with Timer() as t:
             done = dev.evolve(u, scratch, dev_t(np.array([0.5])), tau, steps, tv=tv, engine=eng,
                               step_drift=sd, step_blocks=sb, workspace=ws)
