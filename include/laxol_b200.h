@@ -108,7 +108,11 @@ int lob_minplus_window_f64(lob_ctx* ctx, const double* u, double* out, int64_t l
  * The workspace carries per-tile statistics of u between consecutive calls:
  * pass LOB_FAST_STATS_VALID when `u` is the `out` of the previous call with
  * the same workspace, drift, tau and n (the device-resident evolve loop),
- * else 0 and the statistics are recomputed (one extra read of u). */
+ * else 0 and the statistics are recomputed (one extra read of u).  The flag is a promise:
+ * u modified in place under the same pointer between the calls is not detected (the clamps
+ * keep every access in bounds, the minima may be wrong).  Lines of n <= 2048 samples without
+ * block counts run the whole-line kernel (K2L), which carries no statistics and ignores the
+ * flag (lob_ctx_set_fast_line). */
 #define LOB_FAST_STATS_VALID 1
 /* With LOB_FAST_STATS_VALID: nothing else ran on `stream` since the previous
  * lob_minplus_fast_f64 call on this workspace (whose out is this u), so each
@@ -142,8 +146,9 @@ int lob_minplus_fast_window_f64(lob_ctx* ctx, const double* u, double* out, int6
 /* Diagnostic hook: replace the fast engine's slope-inversion tolerance delta (in
  * displacement units) for the line constants computed from now
  * on; NaN restores the computed bound.  A delta below the bound lets the walk miss
- * minimisers: those outputs are recomputed by the exact direct scan and counted
- * (lob_fast_diagnostics [0]), so results stay exact but the walk is shown to fail. */
+ * minimisers: outputs no interval reaches are recomputed by the exact direct scan and
+ * counted (lob_fast_diagnostics [0]), but an output still reached by a non-minimal source
+ * comes out too large -- the hook exists to show that the computed bound is load-bearing. */
 int lob_ctx_set_fast_delta(lob_ctx* ctx, double delta);
 
 /* Fast-engine counters, cumulative since the last call without
@@ -176,12 +181,14 @@ int lob_fast_diagnostics(lob_ctx* ctx, void* workspace, int64_t lines, int64_t n
  * rounding, as the C++ expression a1*a2 + b), i.e. the reference's
  * PotentialNd callback evaluated on the host per axis and per step;
  * a1 == NULL means V == 0.  tmp: device scratch of n*n doubles.
- * engine LOB_ENGINE_DIRECT or LOB_ENGINE_FAST.  With LOB_ENGINE_FAST and a
- * workspace of 2 x lob_fast_workspace_bytes(n, n) the step is fused into four
- * launches: transpose + the fast engine's input statistics, sweep axis 0,
- * transpose + statistics, sweep axis 1 with tau*(a1*a2 + b) in its epilogue (one
- * workspace half per axis; consecutive steps keep each axis' line constants);
- * with a single lob_fast_workspace_bytes(n, n) the unfused sequence runs.
+ * engine LOB_ENGINE_DIRECT or LOB_ENGINE_FAST.  With LOB_ENGINE_FAST and n <= 2048
+ * (the default lob_ctx_set_fast_line setting) the step is four launches without
+ * workspace: 64x64 transpose, whole-line K2L sweep of axis 0, transpose, K2L sweep of
+ * axis 1 with tau*(a1*a2 + b) in its epilogue.  Otherwise, with a workspace of
+ * 2 x lob_fast_workspace_bytes(n, n): transpose + the tiled fast engine's input
+ * statistics, sweep axis 0, transpose + statistics, sweep axis 1 with the potential in its
+ * epilogue (one workspace half per axis); with a single lob_fast_workspace_bytes(n, n) the
+ * unfused sequence runs.
  * Asynchronous on `stream` (the per-axis kernel tables are built once per
  * (n, tau, drift) and cached by the context). */
 int lob_split_step_2d_f64(lob_ctx* ctx, const double* u, double* out, double* tmp, int64_t n,
