@@ -289,28 +289,35 @@ int lob_split_step_2d_f64(lob_ctx* ctx, const double* u, double* out, double* tm
         // K2L twice, tau*V = tau*(a1[i]*a2[k] + b) in the second sweep's epilogue
         const FastSepPot sep{a1, a2, b};
         const FastSepPot* sp = (a1 && a2) ? &sep : nullptr;
-        if (ctx->fast_line == 2) {  // transposes around row sweeps (the default: measured fastest)
+        int mode = ctx->fast_line;
+        if (mode == 5 && (n % 2 != 0 || reinterpret_cast<uintptr_t>(u) % 16 != 0 ||
+                          reinterpret_cast<uintptr_t>(tmp) % 16 != 0))
+            mode = 2;
+        if (mode == 4 && n % 8 != 0) mode = 2;
+        if (mode == 5) {
+            // both sweeps read columns by 2-D TMA and write rows: tmp holds the transposed state
+            // after axis 0, whose columns are the rows of axis 1
+            if ((st = launch_line_f64(ctx, u, tmp, n, n, d1, tau, nullptr, 0, nullptr, kLineTma, kLineRow, nullptr, s)))
+                return st;
+            return launch_line_f64(ctx, tmp, out, n, n, d2, tau, nullptr, 0, sp, kLineTma, kLineRow, nullptr, s);
+        }
+        if (mode == 2) {  // transposes around row sweeps
             if ((st = launch_transpose(ctx, u, tmp, n, s))) return st;
-            if ((st = launch_line_f64(ctx, tmp, out, n, n, d1, tau, nullptr, 0, nullptr, false, false, nullptr, s)))
+            if ((st = launch_line_f64(ctx, tmp, out, n, n, d1, tau, nullptr, 0, nullptr, kLineRow, kLineRow, nullptr, s)))
                 return st;
             if ((st = launch_transpose(ctx, out, tmp, n, s))) return st;
-            return launch_line_f64(ctx, tmp, out, n, n, d2, tau, nullptr, 0, sp, false, false, nullptr, s);
+            return launch_line_f64(ctx, tmp, out, n, n, d2, tau, nullptr, 0, sp, kLineRow, kLineRow, nullptr, s);
         }
-        if (ctx->fast_line == 3) {  // both sweeps read columns and write rows (tmp = the transposed state)
-            if ((st = launch_line_f64(ctx, u, tmp, n, n, d1, tau, nullptr, 0, nullptr, true, false, nullptr, s)))
+        if (mode == 3) {  // both sweeps read columns (strided) and write rows
+            if ((st = launch_line_f64(ctx, u, tmp, n, n, d1, tau, nullptr, 0, nullptr, kLineCol, kLineRow, nullptr, s)))
                 return st;
-            return launch_line_f64(ctx, tmp, out, n, n, d2, tau, nullptr, 0, sp, true, false, nullptr, s);
+            return launch_line_f64(ctx, tmp, out, n, n, d2, tau, nullptr, 0, sp, kLineCol, kLineRow, nullptr, s);
         }
-        if (ctx->fast_line == 4 && n % 8 == 0) {
-            // axis 0 on columns exchanged through distributed shared memory (clusters of 8 CTAs =
-            // 8 adjacent columns, 64-byte row segments), axis 1 on rows
-            if ((st = launch_line_f64(ctx, u, tmp, n, n, d1, tau, nullptr, 0, nullptr, true, true, nullptr, s, true)))
-                return st;
-            return launch_line_f64(ctx, tmp, out, n, n, d2, tau, nullptr, 0, sp, false, false, nullptr, s);
-        }
-        // axis 0 reads and writes the columns of u in place, axis 1 sweeps the rows
-        if ((st = launch_line_f64(ctx, u, tmp, n, n, d1, tau, nullptr, 0, nullptr, true, true, nullptr, s))) return st;
-        return launch_line_f64(ctx, tmp, out, n, n, d2, tau, nullptr, 0, sp, false, false, nullptr, s);
+        // axis 0 on columns in place (1: strided; 4: exchanged through DSMEM in clusters of 8 CTAs
+        // = 8 adjacent columns, 64-byte row segments), axis 1 on rows
+        const int cl = mode == 4 ? kLineClu : kLineCol;
+        if ((st = launch_line_f64(ctx, u, tmp, n, n, d1, tau, nullptr, 0, nullptr, cl, cl, nullptr, s))) return st;
+        return launch_line_f64(ctx, tmp, out, n, n, d2, tau, nullptr, 0, sp, kLineRow, kLineRow, nullptr, s);
     }
     if (engine == LOB_ENGINE_FAST && workspace && workspace_bytes >= 2 * wsz) {
         // fused: transpose + K2 statistics -> sweep axis 0 -> transpose + statistics ->

@@ -45,6 +45,9 @@
 #include <type_traits>
 
 #include <cooperative_groups.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cstddef>
 
 #include "lob_internal.cuh"
 
@@ -1440,12 +1443,17 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
 
 // ---- K2L: one step of short lines, one CTA per whole line ---------------------
 // For n <= kT the whole line is one tile, so the statistics K2 carries between steps
-// (sub-tile slope bounds, line extremes) are computed from the staged line itself: the
-// exact oscillation gate and the line's displacement range [DLg, DRg] come from a block
-// reduction, no workspace statistics are read or written, and the candidate emission,
-// the direct fallbacks and the epilogue are fast_kernel's.  COLIN / COLOUT: line l is
-// column l of an n x n row-major tensor (the 2-D split step's axis-0 sweep reads and
-// writes columns in place: proj/src/splitting.cpp:67-76 gathers and scatters them).
+// (sub-tile slope bounds, line extremes) are computed from the line itself: each thread
+// holds kPer samples in registers, coarse order-preserving keys of u and of its slopes are
+// reduced with REDUX (an enclosure: the oscillation gate and the displacement range
+// [DLg, DRg] are conservative), the unrolled source range is written into the source
+// buffer straight from the registers, and the candidate emission, the direct fallbacks and
+// the epilogue are fast_kernel's.  No workspace statistics are read or written.
+// Load modes: a row of u; column l of an n x n row-major tensor by strided loads, by a
+// cluster exchange through distributed shared memory, or by 2-D TMA tensor-map copies
+// (boxes of 2 columns x 256 rows, cp.async.bulk.tensor, the column picked out of the pair);
+// store modes: a row, a column (strided), a cluster exchange.  The 2-D split step sweeps
+// axis 0 as columns (proj/src/splitting.cpp:67-76 gathers and scatters them).
 // Outputs follow fast_kernel's slot convention (slot i = output i - 1; slots 0 and n + 1
 // are halo outputs nobody reads).
 struct LineShared {  // overlays S.vbuf before the K staging
@@ -1454,28 +1462,51 @@ struct LineShared {  // overlays S.vbuf before the K staging
     long long first;
 };
 static_assert(sizeof(LineShared) <= sizeof(double) * kVCap, "line scratch fits vbuf");
+static_assert(kPer * kNT == kT, "one register sample per thread and kNT outputs");
 
 constexpr int kLC = 8;  // CTAs (= adjacent columns) per cluster of the column-exchange variant
+constexpr int kLdRow = kLineRow, kLdCol = kLineCol, kLdClu = kLineClu, kLdTma = kLineTma;
+constexpr int kStRow = kLineRow, kStCol = kLineCol, kStClu = kLineClu;
+constexpr int kTmaRows = 256;  // rows per TMA box (2 columns x 256 rows = 4 KB)
+static_assert(offsetof(MainShared, queue) >= static_cast<size_t>(kT) * 16, "TMA landing zone below the queue");
 
-template <bool COLIN, bool COLOUT, bool CLU>
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int LD, int ST>
 __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* __restrict__ u, double* __restrict__ out,
                                                                   const double* __restrict__ drift_arr,
                                                                   const double* __restrict__ tv, int64_t tv_stride,
-                                                                  unsigned long long* __restrict__ diag, FastParams p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+                                                                  unsigned long long* __restrict__ diag, FastParams p,
+                                                                  const __grid_constant__ CUtensorMap tmap) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     MainShared& S = *reinterpret_cast<MainShared*>(smem_raw);
     LineShared& L = *reinterpret_cast<LineShared*>(S.vbuf);
     const int n = static_cast<int>(p.n);
     const int64_t line = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t is = COLIN ? p.n : 1, os = COLOUT ? p.n : 1;
-    const double* ul = COLIN ? u + line : u + line * p.n;
-    double* ol = COLOUT ? out + line : out + line * p.n;
+    const int64_t is = LD == kLdRow ? 1 : p.n, os = ST == kStCol ? p.n : 1;
+    const double* ul = LD == kLdRow ? u + line * p.n : u + line;
+    double* ol = ST == kStRow ? out + line * p.n : out + line;
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if constexpr (LD == kLdTma) {
+        if (tid == 0) {
+            unsigned long long* bar = reinterpret_cast<unsigned long long*>(S.queue);
+            mbar_init(bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+        }
+        __syncthreads();
+    }
     asm volatile("griddepcontrol.wait;" ::: "memory");
     // the line into shared memory (the keys area: U[j], j < n <= kT)
     double* U = reinterpret_cast<double*>(S.keys);
-    if constexpr (CLU) {
+    if constexpr (LD == kLdClu) {
         // a cluster of kLC CTAs holds kLC adjacent columns c0 .. c0 + kLC - 1; CTA r reads rows
         // [r n/kLC, (r+1) n/kLC) of all kLC columns (64-byte row segments) and stores each value
         // into its column's CTA through distributed shared memory
@@ -1489,6 +1520,31 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
             *cluster.map_shared_rank(U + row, col) = u[static_cast<int64_t>(row) * p.n + c0 + col];
         }
         cluster.sync();
+    } else if constexpr (LD == kLdTma) {
+        // columns (line & ~1, line | 1) x all rows in boxes of kTmaRows rows into the landing zone
+        // (land[2 j + pick] = U(j), over keys and the start of the source buffer), then compacted
+        // into U through registers
+        unsigned long long* bar = reinterpret_cast<unsigned long long*>(S.queue);
+        const double* land = reinterpret_cast<const double*>(smem_raw);
+        if (tid == 0) {
+            mbar_expect_tx(bar, static_cast<unsigned>((n + kTmaRows - 1) / kTmaRows * kTmaRows) * 16u);
+            for (int r0 = 0; r0 < n; r0 += kTmaRows)
+                tma_load_2d(smem_raw + static_cast<size_t>(r0) * 16, &tmap, static_cast<int>(line & ~1ll), r0, bar);
+        }
+        mbar_wait(bar, 0);
+        const int pick = static_cast<int>(line & 1);
+        double v[kPer];
+#pragma unroll
+        for (int m = 0; m < kPer; ++m) {
+            const int j = tid + kNT * m;
+            v[m] = j < n ? land[2 * j + pick] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < kPer; ++m) {
+            const int j = tid + kNT * m;
+            if (j < n) U[j] = v[m];
+        }
     } else {
         for (int j = tid; j < n; j += kNT) U[j] = ul[j * is];
     }
@@ -1633,7 +1689,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
     const double sa1l = p.sa1 ? __ldg(p.sa1 + line) : 0.0;
     const double* sa2 = p.sa2;
     const double sb = p.sb;
-    double* ostage = S.ubuf;  // CLU && COLOUT: the new line, for the cluster's row-segment stores
+    double* ostage = S.ubuf;  // ST == kStClu: the new line, for the cluster's row-segment stores
 #pragma unroll 4
     for (int j = tid; j < n; j += kNT) {
         const unsigned long long kk = S.keys[j + 1];
@@ -1653,10 +1709,10 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
         if (tvl) t = __ldg(tvl + j);
         else if (sa2) t = __dmul_rn(tau, __dadd_rn(__dmul_rn(sa1l, __ldg(sa2 + j)), sb));
         const double o = __dsub_rn(best, t);
-        if constexpr (CLU && COLOUT) ostage[j] = o;
+        if constexpr (ST == kStClu) ostage[j] = o;
         else ol[j * os] = o;
     }
-    if constexpr (CLU && COLOUT) {
+    if constexpr (ST == kStClu) {
         cg::cluster_group cluster = cg::this_cluster();
         const int r = static_cast<int>(cluster.block_rank());
         const int64_t c0 = line - r;
@@ -1978,13 +2034,31 @@ static FastBuffers make_buffers(void* ws, int64_t lines, int64_t n, int64_t coun
 
 int64_t fast_line_max() { return kT; }
 
+// the driver's cuTensorMapEncodeTiled through the runtime (no -lcuda link)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }
+    return fn;
+}
+
 int launch_line_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n, const double* drift,
-                    double tau, const double* tv, int64_t tv_stride, const FastSepPot* sep, bool colin, bool colout,
-                    unsigned long long* diag, cudaStream_t s, bool cluster) {
+                    double tau, const double* tv, int64_t tv_stride, const FastSepPot* sep, int load, int store,
+                    unsigned long long* diag, cudaStream_t s) {
     if (n < 3 || n > kT) return set_error(ctx, LOB_INVALID_INPUT, "fast line kernel: 3 <= n <= 2048");
-    if (cluster && (!(colin || colout) || n % kLC != 0))
+    if ((load != kLineRow || store != kLineRow) && lines != n)
+        return set_error(ctx, LOB_INVALID_INPUT, "fast line kernel: columns need lines == n");
+    if ((load == kLineClu || store == kLineClu) && n % kLC != 0)
         return set_error(ctx, LOB_INVALID_INPUT, "fast line kernel: cluster columns need n % 8 == 0");
-    if ((colin || colout) && lines != n) return set_error(ctx, LOB_INVALID_INPUT, "fast line kernel: columns need lines == n");
+    if (load == kLineTma && (n % 2 != 0 || reinterpret_cast<uintptr_t>(u) % 16 != 0))
+        return set_error(ctx, LOB_INVALID_INPUT, "fast line kernel: TMA columns need even n and 16-byte rows");
     if (lines < 1 || lines > 0x7fffffffll) return set_error(ctx, LOB_INVALID_INPUT, "fast line kernel: lines");
     FastParams p = make_params(n, tau, 0.0);
     p.delta_override = ctx->fast_delta_override;
@@ -1995,19 +2069,37 @@ int launch_line_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
         p.sa2 = sep->a2;
         p.sb = sep->b;
     }
+    CUtensorMap tmap;
+    std::memset(&tmap, 0, sizeof(tmap));
+    if (load == kLineTma) {
+        auto enc = tensor_map_encoder();
+        if (!enc) return set_error(ctx, LOB_CUDA_ERROR, "fast line kernel: cuTensorMapEncodeTiled unavailable");
+        const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(n)};
+        const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(n) * sizeof(double)};
+        const cuuint32_t box[2] = {2, static_cast<cuuint32_t>(kTmaRows)};
+        const cuuint32_t estride[2] = {1, 1};
+        const CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(u), gdim, gstride, box,
+                               estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return set_error(ctx, LOB_CUDA_ERROR, "fast line kernel: tensor map encoding failed");
+    }
     using KernT = void (*)(const double*, double*, const double*, const double*, int64_t, unsigned long long*,
-                           FastParams);
-    static const KernT kerns[2][2][2] = {{{line_kernel<false, false, false>, line_kernel<false, false, false>},
-                                          {line_kernel<false, true, false>, line_kernel<false, true, true>}},
-                                         {{line_kernel<true, false, false>, line_kernel<true, false, true>},
-                                          {line_kernel<true, true, false>, line_kernel<true, true, true>}}};
-    auto kern = kerns[colin][colout][cluster];
+                           FastParams, const CUtensorMap);
+    KernT kern = nullptr;
+    if (load == kLineRow && store == kLineRow) kern = line_kernel<kLdRow, kStRow>;
+    else if (load == kLineCol && store == kLineCol) kern = line_kernel<kLdCol, kStCol>;
+    else if (load == kLineCol && store == kLineRow) kern = line_kernel<kLdCol, kStRow>;
+    else if (load == kLineClu && store == kLineClu) kern = line_kernel<kLdClu, kStClu>;
+    else if (load == kLineTma && store == kLineRow) kern = line_kernel<kLdTma, kStRow>;
+    else if (load == kLineTma && store == kLineCol) kern = line_kernel<kLdTma, kStCol>;
+    else return set_error(ctx, LOB_INVALID_INPUT, "fast line kernel: unsupported load / store layout");
     if (first_time(ctx, reinterpret_cast<const void*>(kern))) {
         LOB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(sizeof(MainShared))));
         LOB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                                cudaSharedmemCarveoutMaxShared));
     }
+    const bool cluster = load == kLineClu || store == kLineClu;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(lines));
     cfg.blockDim = dim3(kNT);
@@ -2022,7 +2114,7 @@ int launch_line_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = cluster ? 2 : 1;
-    LOB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, u, out, drift, tv, tv_stride, diag, p));
+    LOB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, u, out, drift, tv, tv_stride, diag, p, tmap));
     ctx->launches += 1;
     return cuda_status(ctx, cudaGetLastError(), "fast line kernel");
 }
@@ -2083,7 +2175,7 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
         ctx->ws_chain[workspace] = 0;
         ctx->ws_lc_valid[workspace] = false;
         const FastSepPot* sp = sep;
-        return launch_line_f64(ctx, u, out, lines, n, drift, tau, tv, tv_stride, sp, false, false, dg, s);
+        return launch_line_f64(ctx, u, out, lines, n, drift, tau, tv, tv_stride, sp, kLineRow, kLineRow, dg, s);
     }
     if (ctx->ws_nostats[workspace]) {
         ctx->ws_nostats[workspace] = false;

@@ -161,9 +161,12 @@ int64_t fast_tiles(int64_t n);
 // K2L: one step of short lines (n <= fast_line_max()) with statistics from the staged line itself;
 // colin / colout: line l is column l of an n x n row-major tensor (lines == n)
 int64_t fast_line_max();
+// line layouts: a row; a column by strided accesses; a column exchanged through distributed shared
+// memory in clusters of 8 CTAs; a column loaded by 2-D TMA tensor-map copies (load only)
+enum : int { kLineRow = 0, kLineCol = 1, kLineClu = 2, kLineTma = 3 };
 int launch_line_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n, const double* drift,
-                    double tau, const double* tv, int64_t tv_stride, const FastSepPot* sep, bool colin, bool colout,
-                    unsigned long long* diag, cudaStream_t s, bool cluster = false);
+                    double tau, const double* tv, int64_t tv_stride, const FastSepPot* sep, int load, int store,
+                    unsigned long long* diag, cudaStream_t s);
 int launch_drift_tiles(lob_ctx* ctx, const double* dpart, int64_t lines, int64_t n, double* drift_out, int* halt,
                        int step, cudaStream_t s);
 // K2R: all steps of an evolve of short lines (n <= 8192) in one launch, one CTA per line

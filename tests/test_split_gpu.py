@@ -96,3 +96,24 @@ def test_split_non_tile_multiple_sizes(dev, orc, ref, engine, n):
         tv = api.tau_v(np.add.outer(a, np.zeros(n)) * a[None, :] + b, tau)
         want = orc.split2d(u, k1, f1, k2, f2, tv=tv)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4, 5])
+@pytest.mark.parametrize("n", [64, 250, 512])
+def test_split_fast_layouts_vs_reference(dev, ref, mode, n):
+    """Every 2-D layout of the fast engine's split step (lob_ctx_set_fast_line): 0 tiled kernels
+    with carried statistics, 1 columns in place (strided), 2 transposes around K2L row sweeps (the
+    default), 3 columns read / rows written, 4 columns exchanged through DSMEM in clusters of 8,
+    5 columns read by 2-D TMA tensor maps (odd or non-multiple-of-8 sizes fall back to 2) ==
+    the reference's split_step_nd with the C4 potential."""
+    rng = np.random.default_rng(n + mode)
+    tau, t = (0.05 if n <= 64 else 0.01), 0.35
+    u = api.gen_c4_u0(n) + 0.01 * rng.uniform(-1, 1, (n, n))
+    a = api.gen_cos(n)
+    b = api.c4_time_term(t + tau)
+    dev.set_fast_line(mode)
+    try:
+        got = run_split(dev, u, tau, 0.3, -0.7, a1=a, a2=a, b=b, engine=FUSED)
+    finally:
+        dev.set_fast_line(2)
+    assert np.array_equal(got, ref.split_step_2d(u, tau, 0.3, -0.7, pot_kind=1, t=t))
