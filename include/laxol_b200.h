@@ -119,6 +119,12 @@ int lob_minplus_window_f64(lob_ctx* ctx, const double* u, double* out, int64_t l
  * tile may start as soon as its own line's previous step is done instead of
  * after the whole previous grid (back-to-back stepping loops). */
 #define LOB_FAST_CHAINED 2
+/* With LOB_FAST_STATS_VALID: verify the promise.  Each step stores 32 samples of its output
+ * (positions (k n) >> 5) with the statistics; a checked call compares its input u with them
+ * bitwise, and a line whose samples differ (u modified in place under the same pointer) takes the
+ * exact direct formula in every tile, counted in lob_fast_diagnostics [10].  A sampled check: a
+ * modification that touches none of the 32 positions is not seen. */
+#define LOB_FAST_STATS_CHECK 4
 int lob_fast_workspace_bytes(int64_t lines, int64_t n, size_t* bytes);
 int lob_minplus_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
                          const double* drift, double tau, const double* tv, int64_t tv_stride,
@@ -166,7 +172,7 @@ int lob_ctx_set_fast_delta(lob_ctx* ctx, double delta);
  *      candidate count exceeded a quarter of the window's,
  *  [9] chained-step waits that timed out (a misused LOB_FAST_CHAINED; the
  *      results of that call are not trustworthy),
- *  [10] unused,
+ *  [10] lines whose LOB_FAST_STATS_CHECK samples differed from u (per tile),
  *  [11] tiles whose carried line constants (LOB_FAST_STATS_VALID) no longer
  *       matched the caller's drift / window (another table at a reused address,
  *       a drift changed in place): computed by the direct formula with the

@@ -25,6 +25,7 @@ ENGINE_FAST = 1
 ENGINE_RELAXED = 2
 FAST_STATS_VALID = 1
 FAST_CHAINED = 2
+FAST_STATS_CHECK = 4
 DIRECT_SCREENED = 0
 DIRECT_PLAIN = 1
 POTENTIAL_ZERO, POTENTIAL_CONST, POTENTIAL_COSINE = 0, 1, 2

@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _capi
-from ._capi import (DIRECT_PLAIN, DIRECT_SCREENED, ENGINE_DIRECT, ENGINE_FAST, ENGINE_RELAXED, FAST_CHAINED, FAST_STATS_VALID, EvaluationError,  # noqa: F401
+from ._capi import (DIRECT_PLAIN, DIRECT_SCREENED, ENGINE_DIRECT, ENGINE_FAST, ENGINE_RELAXED, FAST_CHAINED, FAST_STATS_CHECK, FAST_STATS_VALID, EvaluationError,  # noqa: F401
                     InvalidInput, check)
 
 
@@ -221,7 +221,7 @@ class Device:
 
     FAST_COUNTER_KEYS = ["missed_outputs", "sources", "queued_candidates", "queued_intervals", "tiles", "tiles_k_unstaged",
                          "k_range_sum", "direct_tiles_gate", "direct_tiles_heavy", "chain_timeouts",
-                         "unused10", "stale_line_constants"]
+                         "stats_check_mismatches", "stale_line_constants"]
 
     def fast_counters(self, workspace, lines: int, n: int) -> dict:
         """The fast engine's work counters (include/laxol_b200.h, lob_fast_diagnostics)."""

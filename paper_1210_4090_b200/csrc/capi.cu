@@ -197,6 +197,7 @@ int lob_minplus_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lin
     if (!u || !out || !drift)
         return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_fast_f64: null buffer");
     if (u == out) return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_fast_f64: out must not alias u");
+    if (flags & ~kFastUserFlags) return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_fast_f64: unknown flags");
     return launch_fast_f64(ctx, u, out, lines, n, drift, tau, tv, tv_stride, eta, blocks, workspace,
                            workspace_bytes, flags, static_cast<cudaStream_t>(stream));
 }
@@ -214,6 +215,7 @@ int lob_minplus_fast_window_f64(lob_ctx* ctx, const double* u, double* out, int6
     if (!(tau > 0.0)) return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_fast_window_f64: tau must be positive");
     if (ktab_stride != 0 && ktab_stride < 2 * n + 1)
         return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_fast_window_f64: ktab_stride < 2n+1");
+    if (flags & ~kFastUserFlags) return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_fast_window_f64: unknown flags");
     const FastTable tab{ktab, ktab_stride, first};
     return launch_fast_f64(ctx, u, out, lines, n, nullptr, tau, tv, tv_stride, eta, blocks, workspace,
                            workspace_bytes, flags, static_cast<cudaStream_t>(stream), nullptr, &tab);

@@ -127,6 +127,8 @@ struct FastParams {
     const double* vtab;  // v_d for d in [-vofs, vofs]
     int64_t vofs;
     int fsm_on;  // the epilogue produces decompose()'s FSM summaries for the next step's block count
+    int check;   // LOB_FAST_STATS_CHECK: compare u with the samples the statistics were taken with
+    int samples; // the epilogue stores samples of u^{n+1} (a workspace that has seen a checked call)
     double delta_override;  // NaN: the computed rounding bound delta (diagnostic hook, lob_ctx_set_fast_delta)
     // the caller's current per-line inputs (checked against the carried line constants)
     const double* drift_arr;                      // mechanical mode
@@ -148,7 +150,10 @@ struct FastBuffers {
     unsigned long long* fsm_out;
     unsigned long long* line_out;
     unsigned long long* line_reset;
+    const double* samp_in;  // [lines][kSamp] samples of u taken with its statistics
+    double* samp_out;       // ... of u^{n+1}
 };
+constexpr int kSamp = 32;  // sampled positions per line: (k n) >> 5, k < 32
 
 namespace {
 
@@ -378,6 +383,10 @@ __global__ void __launch_bounds__(kNT) stats_kernel(const double* __restrict__ u
         vals[P8(i)] = ul[j];
     }
     __syncthreads();
+    if (threadIdx.x < kSamp) {
+        const int64_t pos = (static_cast<int64_t>(threadIdx.x) * p.n) >> 5;
+        if (pos >= j0 && pos < j0 + Tl) b.samp_out[line * kSamp + threadIdx.x] = vals[P8(static_cast<int>(pos - j0) + 1)];
+    }
     if (Tl == kT && j0 + kT <= p.n - 1)
         tile_stats<true>(vals, Tl, j0, line, tile, p, b, sh, lut);
     else
@@ -900,6 +909,19 @@ __device__ void tile_direct(MainShared& S, const double* ul, int n, int j0, int 
     if (warp < 3 && lane == 0) S.keys[warp == 0 ? 0 : Tl + warp] = dbits(hb);
 }
 
+// LOB_FAST_STATS_CHECK (warp 0, all lanes): u changed since its statistics were taken when a
+// sampled position differs bitwise; the statistics then do not describe u, and every tile of the
+// line sees it and takes the direct formula (exact), counted.  Out of line: the unchecked setup
+// keeps its registers.  Loads through L2 (a chained predecessor may still be finishing).
+__device__ __noinline__ bool samples_differ(const double* ul, const double* samp, int n, unsigned long long* diag) {
+    const int lane = threadIdx.x & 31;
+    const int pos = static_cast<int>((static_cast<int64_t>(lane) * n) >> 5);
+    const bool diff = __double_as_longlong(__ldcg(ul + pos)) != __double_as_longlong(__ldcg(samp + lane));
+    const bool any = __any_sync(0xffffffffu, diff);
+    if (any && lane == 0 && diag) atomicAdd(diag + 10, 1ull);
+    return any;
+}
+
 // Per-line constants of the step (identical IEEE operations to the host's
 // build_kernel for first/center; the tolerance only needs to be a bound).
 __device__ __forceinline__ LineConst line_const(double drift, const FastParams& p) {
@@ -1101,6 +1123,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
         const bool exact_ok = isfinite(osc) && osc * (1.0 + 1e-12) < lc.gap * (1.0 - 1e-12);
         const bool loose_ok = loose * (1.0 + 1e-12) < lc.gap * (1.0 - 1e-12);
         bool okl = !stale && (exact_ok || loose_ok) && isfinite(smin) && isfinite(smax) && n >= 3;
+        if (p.check && samples_differ(ul, b.samp_in + line * kSamp, n, diag)) okl = false;
         // this step's epilogue collects the exact extremes of u^{n+1} unless the cheap bound of
         // u^n passes with a factor 2 to spare (the same decision in every tile of the line)
         if (lane == 0) S.osc_exact = !(loose * 2.0 < lc.gap) || !isfinite(loose);
@@ -1409,6 +1432,11 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
             atomicAdd(diag + 3, static_cast<unsigned long long>(S.c_qent));
         }
         atomicAdd(diag + 4, 1ull);
+    }
+    // the samples the next step's LOB_FAST_STATS_CHECK compares its input with
+    if (p.samples && tid < kSamp) {
+        const int pos = static_cast<int>((static_cast<int64_t>(tid) * n) >> 5);
+        if (pos >= j0 && pos < j0 + Tl) b.samp_out[line * kSamp + tid] = vals[P8(pos - j0 + 1)];
     }
     if (Tl == kT && j0 + kT <= n - 1)
         tile_stats<true>(vals, Tl, j0, line, tile, p, b, S.epi(), g_fsm_lut2, osc_exact);
@@ -1931,7 +1959,7 @@ __global__ void __launch_bounds__(kRT) resident_kernel(double* __restrict__ u, i
 //            line[3][lines][4] u64 | LineConst[lines] | diag u64[16] | done u32[lines]
 constexpr int kDiag = 16;
 struct WsLayout {
-    size_t sub, fsm, line, lc, diag, done, total;
+    size_t sub, fsm, line, lc, diag, done, samp, total;
 };
 static WsLayout ws_layout(int64_t lines, int64_t n) {
     const int64_t tiles = (n + kT - 1) / kT, subs = (n + kG - 1) / kG;
@@ -1942,7 +1970,8 @@ static WsLayout ws_layout(int64_t lines, int64_t n) {
     w.lc = w.line + 3 * static_cast<size_t>(lines) * 4 * sizeof(unsigned long long);
     w.diag = w.lc + static_cast<size_t>(lines) * sizeof(LineConst);
     w.done = w.diag + kDiag * sizeof(unsigned long long);  // [lines] warps finished since the counters reset
-    w.total = w.done + (static_cast<size_t>(lines) * sizeof(unsigned) + 255) / 256 * 256;
+    w.samp = w.done + (static_cast<size_t>(lines) * sizeof(unsigned) + 255) / 256 * 256;
+    w.total = w.samp + 2 * static_cast<size_t>(lines) * kSamp * sizeof(double);
     return w;
 }
 
@@ -2029,6 +2058,9 @@ static FastBuffers make_buffers(void* ws, int64_t lines, int64_t n, int64_t coun
     b.line_in = line + c3 * lines * 4;
     b.line_out = line + ((c3 + 1) % 3) * lines * 4;
     b.line_reset = line + ((c3 + 2) % 3) * lines * 4;
+    double* samp = reinterpret_cast<double*>(base + w.samp);
+    b.samp_in = samp + c2 * lines * kSamp;
+    b.samp_out = samp + (1 - c2) * lines * kSamp;
     return b;
 }
 
@@ -2181,6 +2213,12 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
         ctx->ws_nostats[workspace] = false;
         flags &= ~(LOB_FAST_STATS_VALID | kFastStatsGiven);
     }
+    // a checked call needs the samples its statistics were taken with: the first one on a workspace
+    // (or after a call that stored none) recomputes the statistics and their samples
+    if (flags & LOB_FAST_STATS_CHECK) {
+        ctx->ws_sampling[workspace] = true;
+        if (!ctx->ws_samples_valid[workspace]) flags &= ~LOB_FAST_STATS_VALID;
+    }
     // the per-line done counters restart with the statistics (keeps them in range)
     if (ctx->ws_chain[workspace] * p.tiles * (kNT / 32) > 0xf0000000ll) flags &= ~LOB_FAST_STATS_VALID;
     int64_t& counter = ctx->ws_counter[workspace];
@@ -2221,6 +2259,7 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
         sb.sub_out = const_cast<double2*>(b.sub_in);
         sb.fsm_out = const_cast<unsigned long long*>(b.fsm_in);
         sb.line_out = const_cast<unsigned long long*>(b.line_in);
+        sb.samp_out = const_cast<double*>(b.samp_in);
         const unsigned lb = static_cast<unsigned>((lines + 127) / 128);
         line_init_kernel<<<lb, 128, 0, s>>>(const_cast<unsigned long long*>(b.line_in), lines);
         line_init_kernel<<<lb, 128, 0, s>>>(b.line_out, lines);
@@ -2259,6 +2298,10 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
                                                cudaSharedmemCarveoutMaxShared));
     }
     p.fsm_on = blocks ? 1 : 0;  // the stats kernel above always produced them
+    // the sampled check needs samples taken by this engine (not by a caller's statistics pass)
+    p.check = (flags & LOB_FAST_STATS_CHECK) && (flags & LOB_FAST_STATS_VALID) && !given ? 1 : 0;
+    p.samples = ctx->ws_sampling[workspace] ? 1 : 0;
+    ctx->ws_samples_valid[workspace] = p.samples != 0;
     ctx->ws_fsm_valid[workspace] = blocks != nullptr;
     dim3 grid(static_cast<unsigned>(p.tiles), static_cast<unsigned>(lines));
     cudaLaunchConfig_t cfg = {};
@@ -2348,6 +2391,7 @@ int launch_block_counts(lob_ctx* ctx, const double* u, int64_t lines, int64_t n,
     sb.sub_out = const_cast<double2*>(b.sub_in);
     sb.fsm_out = const_cast<unsigned long long*>(b.fsm_in);
     sb.line_out = const_cast<unsigned long long*>(b.line_in);
+    sb.samp_out = const_cast<double*>(b.samp_in);
     line_init_kernel<<<static_cast<unsigned>((lines + 127) / 128), 128, 0, s>>>(sb.line_out, lines);
     stats_kernel<<<static_cast<unsigned>(nblk), kNT, 0, s>>>(u, p, sb);
     combine_blocks_kernel<<<static_cast<unsigned>((lines + 127) / 128), 128, 0, s>>>(b.fsm_in, lines,

@@ -35,6 +35,8 @@ struct lob_ctx {
     std::map<const void*, const void*> ws_table;     // workspace -> window table of its line constants
     std::map<const void*, bool> ws_lc_valid;         // the workspace holds line constants (mechanical)
     std::map<const void*, bool> ws_nostats;          // its last call (K2L) left no statistics of its out
+    std::map<const void*, bool> ws_sampling;         // a checked call ran on it: steps store samples
+    std::map<const void*, bool> ws_samples_valid;    // its last call stored samples of its out
     int fast_line = 2;  // n <= 2048: one CTA per whole line with in-kernel statistics (K2L); 2-D layout 2
     // K1 mode (LOB_DIRECT_SCREENED / LOB_DIRECT_PLAIN) and the screened kernel's
     // count of outputs swept in full fp64 (device counter, lazily allocated)
@@ -140,6 +142,8 @@ struct FastSepPot {
 // launch_fast_f64 flag: the "in" statistics of u were written by the caller into the buffers
 // fast_given_stats_buffers returned for this workspace (no statistics pass, no pointer check)
 constexpr int kFastStatsGiven = 1 << 8;
+// the flags a C-ABI caller may pass (the rest are internal)
+constexpr int kFastUserFlags = LOB_FAST_STATS_VALID | LOB_FAST_CHAINED | LOB_FAST_STATS_CHECK;
 // dpart (nullable): per-tile sums of u^{n+1} - u^n for evolve's drift ([lines][fast_tiles(n)]);
 // tab (nullable): any convex window per line instead of the mechanical drift;
 // sep (nullable): a separable potential instead of the tv table

@@ -437,3 +437,45 @@ def test_shrunk_delta_bound_makes_the_walk_miss(dev, orc, delta, kernel_mode):
     got, _, c = fast_step_counted(dev, u, 0.4, tau)
     assert np.array_equal(got.cpu().numpy(), want)
     assert_walk(c)
+
+
+def test_stats_check_catches_input_modified_in_place(dev, orc):
+    """LOB_FAST_STATS_CHECK: the carried statistics are promised to describe u; with the check a
+    line whose u was rewritten in place (same pointer) is detected through its 32 samples and
+    every tile of it takes the exact direct formula (counted); unmodified lines keep the walk."""
+    import torch
+    n, tau, lines = 8192, 0.02, 3  # > 2048: the tiled kernel, which carries statistics
+    rng = np.random.default_rng(23)
+    u = rough_walk(rng, lines, n, 2.0)
+    drifts = np.array([0.3, -0.5, 1.1])
+    du = to_dev(u)
+    dd = to_dev(drifts)
+    x = torch.empty_like(du)
+    y = torch.empty_like(du)
+    ws = torch.empty(dev.fast_workspace_bytes(lines, n), dtype=torch.uint8, device="cuda")
+    # a checked workspace stores the samples of every output (the first checked call computes the
+    # statistics of its input itself)
+    dev.fast_f64(du, x, dd, tau, workspace=ws, flags=api.FAST_STATS_CHECK)
+    # line 1 rewritten in place: a large bump over the whole line
+    x[1] += torch.from_numpy(0.5 * np.sin(2 * np.pi * np.arange(n) / n)).cuda()
+    dev.fast_f64(x, y, dd, tau, workspace=ws, flags=api.FAST_STATS_VALID | api.FAST_STATS_CHECK)
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), oracle_step(orc, x.cpu().numpy(), drifts, tau))
+    c = dev.fast_counters(ws, lines, n)
+    tiles_per_line = (n + 2047) // 2048
+    assert c["stats_check_mismatches"] == tiles_per_line, c
+    assert c["direct_tiles_gate"] == tiles_per_line and c["missed_outputs"] == 0, c
+    # unmodified input: the check passes, the walk runs everywhere
+    dev.fast_f64(y, x, dd, tau, workspace=ws, flags=api.FAST_STATS_VALID | api.FAST_STATS_CHECK)
+    torch.cuda.synchronize()
+    assert np.array_equal(x.cpu().numpy(), oracle_step(orc, y.cpu().numpy(), drifts, tau))
+    c2 = dev.fast_counters(ws, lines, n)
+    assert c2["stats_check_mismatches"] == c["stats_check_mismatches"], c2
+
+
+def test_fast_rejects_internal_flags(dev):
+    import torch
+    u = torch.zeros((1, 64), dtype=torch.float64, device="cuda")
+    ws = torch.empty(dev.fast_workspace_bytes(1, 64), dtype=torch.uint8, device="cuda")
+    with pytest.raises(api.InvalidInput):
+        dev.fast_f64(u, torch.empty_like(u), to_dev(np.zeros(1)), 0.05, workspace=ws, flags=1 << 8)
