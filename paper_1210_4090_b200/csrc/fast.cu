@@ -1548,6 +1548,9 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
             *cluster.map_shared_rank(U + row, col) = u[static_cast<int64_t>(row) * p.n + c0 + col];
         }
         cluster.sync();
+    } else if (LD == kLdTma && (smem_u32(smem_raw) & 127u) != 0u) {
+        // (a TMA tensor copy needs a 128-byte aligned destination: strided loads otherwise)
+        for (int j = tid; j < n; j += kNT) U[j] = ul[j * is];
     } else if constexpr (LD == kLdTma) {
         // columns (line & ~1, line | 1) x all rows in boxes of kTmaRows rows into the landing zone
         // (land[2 j + pick] = U(j), over keys and the start of the source buffer), then compacted
