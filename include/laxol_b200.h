@@ -235,6 +235,15 @@ int lob_potential2d_rows_f64(lob_ctx* ctx, double* out, int64_t rows, int64_t n,
  * Device buffers of b*n doubles, asynchronous on `stream`. */
 int lob_slab_pack_f64(lob_ctx* ctx, const double* x, int64_t b, int64_t world, double* send, void* stream);
 int lob_slab_unpack_f64(lob_ctx* ctx, const double* recv, int64_t b, int64_t world, double* y, void* stream);
+/* The same exchange as ONE kernel over NVLink peer memory, replacing pack + all-to-all + unpack:
+ * this rank (`rank` of `world`, row slab x of b x n doubles, n = b*world, b % 64 == 0) writes
+ * X^T's blocks straight into every rank's receive slab: R_q[c][rank*b + i] = x[i][q*b + c]
+ * (R_q = rank q's b x n slab of X^T).  peer_slabs: host array of `world` device addresses of the
+ * receive slabs, valid on this device (CUDA symmetric memory / IPC mappings; this rank's own
+ * entry included), world <= 16.  Asynchronous on `stream`; the ranks synchronise after it (e.g.
+ * a symmetric-memory barrier) before reading their slabs. */
+int lob_slab_push_f64(lob_ctx* ctx, const double* x, int64_t b, int64_t world, int rank, const uint64_t* peer_slabs,
+                      void* stream);
 
 /* Device-resident batched evolve (proj/src/scheme.cpp:208-272): `steps`
  * steps of `lines` periodic lines with a shared, time-independent tv.  u is

@@ -63,6 +63,7 @@ SIGNATURES = {
                                             c_double, _P, _P, c_size_t, c_int, _P]),
     "lob_slab_pack_f64": (c_int, [_P, _P, c_int64, c_int64, _P, _P]),
     "lob_slab_unpack_f64": (c_int, [_P, _P, c_int64, c_int64, _P, _P]),
+    "lob_slab_push_f64": (c_int, [_P, _P, c_int64, c_int64, c_int, _P, _P]),
     "lob_ctx_set_fast_delta": (c_int, [_P, c_double]),
     "lob_fast_diagnostics": (c_int, [_P, _P, c_int64, c_int64, _P]),
     "lob_block_counts": (c_int, [_P, _P, c_int64, c_int64, c_double, _P, _P]),

@@ -365,6 +365,15 @@ int lob_slab_pack_f64(lob_ctx* ctx, const double* x, int64_t b, int64_t world, d
     return launch_transpose_batched(ctx, x, send, 1, b, b * world, static_cast<cudaStream_t>(stream));
 }
 
+int lob_slab_push_f64(lob_ctx* ctx, const double* x, int64_t b, int64_t world, int rank, const uint64_t* peer_slabs,
+                      void* stream) {
+    if (!ctx || !x || !peer_slabs) return set_error(ctx, LOB_INVALID_INPUT, "lob_slab_push_f64: invalid arguments");
+    double* ps[16] = {};
+    if (world < 1 || world > 16) return set_error(ctx, LOB_INVALID_INPUT, "lob_slab_push_f64: 1 <= world <= 16");
+    for (int64_t q = 0; q < world; ++q) ps[q] = reinterpret_cast<double*>(static_cast<uintptr_t>(peer_slabs[q]));
+    return launch_slab_push(ctx, x, b, world, rank, ps, static_cast<cudaStream_t>(stream));
+}
+
 int lob_slab_unpack_f64(lob_ctx* ctx, const double* recv, int64_t b, int64_t world, double* y, void* stream) {
     if (!ctx || !recv || !y || b < 1 || world < 1 || recv == y)
         return set_error(ctx, LOB_INVALID_INPUT, "lob_slab_unpack_f64: invalid arguments");

@@ -203,6 +203,8 @@ int launch_transpose_batched(lob_ctx* ctx, const double* src, double* dst, int64
                              cudaStream_t s);
 int launch_sub_table(lob_ctx* ctx, double* out, const double* tv, int64_t count, cudaStream_t s);
 int launch_slab_unpack(lob_ctx* ctx, const double* recv, double* y, int64_t b, int64_t world, cudaStream_t s);
+int launch_slab_push(lob_ctx* ctx, const double* x, int64_t b, int64_t world, int rank, double* const* peer_slabs,
+                     cudaStream_t s);
 int launch_potential2d(lob_ctx* ctx, double* out, const double* a1, const double* a2, double b,
                        double tau, int64_t n, cudaStream_t s, int64_t rows = -1);
 int launch_drift(lob_ctx* ctx, const double* nxt, const double* cur, int64_t lines, int64_t n,

@@ -68,6 +68,44 @@ __global__ void __launch_bounds__(256) transpose64_kernel(const double* __restri
     }
 }
 
+// The multi-GPU split step's exchange as one kernel over NVLink peer memory (no NCCL, no pack /
+// unpack passes): rank `rank` holds the row slab x = X[rank*b .. rank*b + b) (b x n) and writes
+// X^T's blocks straight into every peer's receive slab, R_q[c][rank*b + i] = X[rank*b + i][q*b + c]
+// (R_q = rank q's b x n slab of X^T).  64 x 64 tiles through shared memory: each tile lands in one
+// peer (b % 64 == 0) as 64 row segments of 512 contiguous bytes.  Peer slabs: device addresses
+// valid on this device (CUDA symmetric memory / IPC); the caller synchronises the ranks after it.
+constexpr int kMaxPeers = 16;
+struct PeerSlabs {
+    double* p[kMaxPeers];
+};
+__global__ void __launch_bounds__(256) slab_push_kernel(const double* __restrict__ x, int64_t b, int64_t n,
+                                                        int rank, PeerSlabs peers) {
+    __shared__ double tile[kTV][kTV + 1];
+    const int64_t bx = static_cast<int64_t>(blockIdx.x) * kTV;  // column block of x (global column)
+    const int64_t by = static_cast<int64_t>(blockIdx.y) * kTV;  // row block of x (local row)
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int64_t k = bx + 2 * lane;
+#pragma unroll
+    for (int r = w; r < kTV; r += 8) {
+        const int64_t i = by + r;
+        const double2 v = *reinterpret_cast<const double2*>(x + i * n + k);
+        tile[r][2 * lane] = v.x;
+        tile[r][2 * lane + 1] = v.y;
+    }
+    __syncthreads();
+    const int q = static_cast<int>(bx / b);  // the peer owning these 64 columns
+    double* dst = peers.p[q];
+    const int64_t col0 = static_cast<int64_t>(rank) * b + by;  // destination column of local row by
+#pragma unroll
+    for (int c = w; c < kTV; c += 8) {
+        const int64_t crow = bx + c - static_cast<int64_t>(q) * b;  // destination row in peer q's slab
+        *reinterpret_cast<double2*>(dst + crow * n + col0 + 2 * lane) =
+            make_double2(tile[2 * lane][c], tile[2 * lane + 1][c]);
+    }
+}
+
 // rows x n block (rows = n for the whole tensor; a row slab of it for the multi-GPU step)
 __global__ void __launch_bounds__(256) potential2d_kernel(double* __restrict__ out,
                                                           const double* __restrict__ a1,
@@ -167,6 +205,32 @@ int launch_slab_unpack(lob_ctx* ctx, const double* recv, double* y, int64_t b, i
     slab_unpack_kernel<<<g, 256, 0, s>>>(recv, y, b, world);
     ctx->launches += 1;
     return cuda_status(ctx, cudaGetLastError(), "slab_unpack_kernel");
+}
+
+int launch_slab_push(lob_ctx* ctx, const double* x, int64_t b, int64_t world, int rank, double* const* peer_slabs,
+                     cudaStream_t s) {
+    if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world || b < 1 || b % kTV != 0)
+        return set_error(ctx, LOB_INVALID_INPUT, "lob_slab_push_f64: 1 <= world <= 16, 0 <= rank < world, b % 64 == 0");
+    if (reinterpret_cast<uintptr_t>(x) % 16 != 0) return set_error(ctx, LOB_INVALID_INPUT, "lob_slab_push_f64: x alignment");
+    PeerSlabs ps{};
+    for (int q = 0; q < world; ++q) {
+        if (!peer_slabs[q] || reinterpret_cast<uintptr_t>(peer_slabs[q]) % 16 != 0)
+            return set_error(ctx, LOB_INVALID_INPUT, "lob_slab_push_f64: peer slab missing or misaligned");
+        ps.p[q] = peer_slabs[q];
+    }
+    const int64_t n = b * world;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(n / kTV), static_cast<unsigned>(b / kTV));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    LOB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, slab_push_kernel, x, b, n, rank, ps));
+    ctx->launches += 1;
+    return cuda_status(ctx, cudaGetLastError(), "slab_push_kernel");
 }
 
 int launch_sub_table(lob_ctx* ctx, double* out, const double* tv, int64_t count, cudaStream_t s) {

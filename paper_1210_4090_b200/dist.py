@@ -9,8 +9,10 @@ subtracts tau*V once.  Per step:
     slab of U  --all-to-all transpose-->  slab of U^T  --K1/K2 row sweep (kernel 1)-->
     --all-to-all transpose back-->  slab  --K1/K2 row sweep (kernel 2)-->  - tau*V (row slab)
 
-i.e. two exchanges of the whole tensor per step (``torch.distributed.all_to_all_single``,
-NCCL over NVLink/NVSwitch on the GPU box), each carrying (world-1)/world of the state;
+i.e. two exchanges of the whole tensor per step, each carrying (world-1)/world of the state:
+``torch.distributed.all_to_all_single`` (NCCL) between library pack / unpack kernels, or — with a
+``P2PExchange`` — one kernel per exchange that writes the transposed blocks straight into the
+peers' symmetric-memory slabs over NVLink, followed by a symmetric-memory barrier;
 the sweeps and the potential are the same device kernels as the single-GPU
 ``lob_split_step_2d_f64``, with the same IEEE operations, so every rank's slab equals the
 corresponding rows of the single-GPU step bit for bit.
@@ -82,9 +84,44 @@ def transpose_slabs(x, group=None, dev: Device | None = None, host_staged: bool 
     return recv.view(world, b, b).permute(1, 0, 2).reshape(b, n).contiguous()
 
 
+class P2PExchange:
+    """The row-slab transpose of the split step over NVLink peer memory: two receive slabs in
+    CUDA symmetric memory (torch.distributed._symmetric_memory; one per exchange of a step, so a
+    fast rank's next push never lands in a slab a slow rank still reads), and per exchange ONE
+    kernel (lob_slab_push_f64) that writes this rank's blocks of X^T straight into every peer's
+    slab, then the symmetric-memory barrier on the stream — no NCCL call, no pack / unpack pass.
+    Requires an initialised process group with CUDA devices and b % 64 == 0."""
+
+    def __init__(self, dev: Device, b: int, n: int, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        if b * max(1, _world(group)[0]) != n or b % 64:
+            raise InvalidInput("P2PExchange: rows per rank must be n / world and a multiple of 64")
+        self.dev, self.b, self.n = dev, b, n
+        self.world, self.rank = _world(group)
+        gname = (group or dist.group.WORLD).group_name
+        self.slabs = [symm_mem.empty((b, n), dtype=torch.float64, device="cuda") for _ in range(2)]
+        self.handles = [symm_mem.rendezvous(t, gname) for t in self.slabs]
+        self.peers = [np.array(h.buffer_ptrs, dtype=np.uint64) for h in self.handles]
+        self.k = 0
+
+    def transpose(self, x):
+        """x: this rank's row slab (b x n, contiguous CUDA) of X; returns this rank's row slab of
+        X^T (a symmetric-memory slab, valid until the next-but-one call)."""
+        k = self.k
+        self.k ^= 1
+        st = self.dev.lib.lob_slab_push_f64(self.dev.ctx, _ptr(x), self.b, self.world, self.rank,
+                                            self.peers[k].ctypes.data, _stream_ptr(None))
+        _capi.check(st, self.dev.ctx, "lob_slab_push_f64")
+        self.handles[k].barrier(channel=k)
+        return self.slabs[k]
+
+
 def split_step_2d_dist(dev: Device, u_slab, tau: float, drift1: float, drift2: float, a1=None, a2=None,
                        b: float = 0.0, engine: int = ENGINE_DIRECT, group=None, workspaces=None,
-                       host_staged: bool = False):
+                       host_staged: bool = False, p2p: "P2PExchange | None" = None):
     """One split step of the row-partitioned periodic n x n tensor (this rank's slab,
     rows [r*b, (r+1)*b) as a torch CUDA tensor).  a1 (length n, the x1 factor of the whole
     grid) and a2 (length n) describe V = a1(x1) a2(x2) + b at the step's sampling time,
@@ -115,9 +152,12 @@ def split_step_2d_dist(dev: Device, u_slab, tau: float, drift1: float, drift2: f
             dev.direct_f64(src, out, kt, fr)
         return out
 
-    t = transpose_slabs(u_slab, group, dev, host_staged)  # slab of U^T: columns of U as rows
-    t = sweep(t, drift1, "axis0")                          # axis 0 (kernel 1)
-    v = transpose_slabs(t, group, dev, host_staged)       # back to rows
+    def exchange(x):
+        return p2p.transpose(x) if p2p is not None else transpose_slabs(x, group, dev, host_staged)
+
+    t = exchange(u_slab)                  # slab of U^T: columns of U as rows
+    t = sweep(t, drift1, "axis0")         # axis 0 (kernel 1)
+    v = exchange(t)                       # back to rows
     w = sweep(v, drift2, "axis1")               # axis 1 (kernel 2)
     if a1 is not None:
         a1d = torch.as_tensor(np.ascontiguousarray(a1[rank * bl:(rank + 1) * bl]), device=w.device)
