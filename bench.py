@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-extras", action="store_true", help="skip the per-kernel extra measurements")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--c4-dist", action="store_true",
+                    help="N>1: also time the row-sharded C4 split step (P2P symmetric-memory exchange)")
     ap.add_argument("--ref-lines", type=int, default=0,
                     help="C2 lines per reference-arm step (default: one per host thread, <= 64)")
     return ap.parse_args()
@@ -341,6 +343,8 @@ def run_b200(args, world, rank, local):
             e2e["cpp_api_pageable"] = {"error": str(exc)[:200]}
     st.clear()
     torch.cuda.empty_cache()
+    # the row-sharded C4 split step across the ranks (every rank takes part)
+    c4d = c4_dist_workload(dev, world, rank) if world > 1 and args.c4_dist else None
 
     if rank != 0:
         return
@@ -375,6 +379,8 @@ def run_b200(args, world, rank, local):
     if world == 1:
         line["c5"] = c5_workload(dev, hbm_peak)
         line["c4"] = c4_workload(dev, hbm_peak)
+    if c4d is not None:
+        line["c4_dist"] = c4d
     if not args.no_extras and world == 1:
         line["kernels"] = extras(dev)
     print(json.dumps(line))
@@ -468,6 +474,62 @@ def c4_workload(dev, hbm_peak):
                         "note": "32 MB state resident in the 126 MB L2"}}
     del u, o, t, ws
     torch.cuda.empty_cache()
+    return out
+
+
+def c4_dist_workload(dev, world, rank):
+    """C4 (2048^2, P=(0.3,-0.7), V=cos cos + 0.2 sin 2 pi t, tau=0.01) sharded by rows over the
+    ranks (paper_1210_4090_b200/dist.py): per step two row-slab exchanges around K2L sweeps.  The
+    exchange runs over NVLink peer memory (CUDA symmetric memory, one push-transpose kernel per
+    exchange) when every rank can set it up, else NCCL all-to-all between pack / unpack kernels.
+    Timed with CUDA events, max over ranks; 16 updates-bytes per point and step as for c4."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1210_4090_b200 import api
+    from paper_1210_4090_b200.dist import P2PExchange, split_step_2d_dist
+
+    n, tau, steps = 2048, 0.01, 50
+    b = n // world
+    out = {"workload": "C4 2048^2 row-sharded over the ranks", "rows_per_rank": b}
+    try:
+        p2p, err = None, ""
+        try:
+            p2p = P2PExchange(dev, b, n)
+        except Exception as exc:  # decided collectively below
+            err = str(exc)[:160]
+        ok = torch.tensor([1 if p2p is not None else 0], dtype=torch.int32, device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if not int(ok.item()):
+            p2p = None
+        out["exchange"] = "p2p symmetric-memory push (lob_slab_push_f64)" if p2p else \
+            ("nccl all_to_all" + (f" (p2p unavailable: {err})" if err else " (p2p unavailable on a peer)"))
+        u0 = api.gen_c4_u0(n)
+        a = api.gen_cos(n)
+        v = torch.from_numpy(np.ascontiguousarray(u0[rank * b:(rank + 1) * b])).cuda()
+        wss = {}
+        k = 0
+
+        def run(m):
+            nonlocal v, k
+            for _ in range(m):
+                v = split_step_2d_dist(dev, v, tau, 0.3, -0.7, a1=a, a2=a, b=api.c4_time_term((k + 1) * tau),
+                                       engine=api.ENGINE_FAST, workspaces=wss, p2p=p2p)
+                k += 1
+
+        run(5)
+        torch.cuda.synchronize()
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        run(steps)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = allreduce_max(e0.elapsed_time(e1) / steps, world, device="cuda")
+        out.update({"ms_per_step": ms, "updates_per_s": n * n / (ms * 1e-3), "steps": steps,
+                    "finite": bool(torch.isfinite(v).all().item())})
+    except Exception as exc:  # reported, not fatal
+        out["error"] = str(exc)[:200]
     return out
 
 
