@@ -135,15 +135,24 @@ def split_step_2d_dist(dev: Device, u_slab, tau: float, drift1: float, drift2: f
     if engine not in (ENGINE_DIRECT, ENGINE_FAST):
         raise InvalidInput("split_step_2d_dist: engine must be ENGINE_DIRECT or ENGINE_FAST")
 
+    cache = workspaces if workspaces is not None else {}
+
+    def cached(key, make):
+        v = cache.get(key)
+        if v is None:
+            v = cache[key] = make()
+        return v
+
     def sweep(src, drift, key):
-        out = torch.empty_like(src)
+        # two output buffers per axis alternate, so the slab returned by the previous call survives
+        flip = cache.get(key + "/flip", 0)
+        cache[key + "/flip"] = flip ^ 1
+        out = cached(f"{key}/out{flip}", lambda: torch.empty_like(src))
         if engine == ENGINE_FAST:
-            ws = None if workspaces is None else workspaces.get(key)
-            if ws is None:
-                ws = torch.empty(dev.fast_workspace_bytes(bl, n), dtype=torch.uint8, device=src.device)
-                if workspaces is not None:
-                    workspaces[key] = ws
-            d = torch.full((bl,), drift, dtype=torch.float64, device=src.device)
+            ws = cached(key, lambda: torch.empty(dev.fast_workspace_bytes(bl, n), dtype=torch.uint8,
+                                                 device=src.device))
+            d = cached(f"{key}/drift{drift!r}", lambda: torch.full((bl,), drift, dtype=torch.float64,
+                                                                     device=src.device))
             dev.fast_f64(src, out, d, tau, workspace=ws)
         else:
             k = dev.build_kernel(n, tau, drift)
@@ -160,8 +169,9 @@ def split_step_2d_dist(dev: Device, u_slab, tau: float, drift1: float, drift2: f
     v = exchange(t)                       # back to rows
     w = sweep(v, drift2, "axis1")               # axis 1 (kernel 2)
     if a1 is not None:
-        a1d = torch.as_tensor(np.ascontiguousarray(a1[rank * bl:(rank + 1) * bl]), device=w.device)
-        a2d = torch.as_tensor(np.ascontiguousarray(a2), device=w.device)
+        a1d = cached("a1/" + str(hash(np.asarray(a1).tobytes())), lambda: torch.as_tensor(np.ascontiguousarray(a1[rank * bl:(rank + 1) * bl]),
+                                                             device=w.device))
+        a2d = cached("a2/" + str(hash(np.asarray(a2).tobytes())), lambda: torch.as_tensor(np.ascontiguousarray(a2), device=w.device))
         st = dev.lib.lob_potential2d_rows_f64(dev.ctx, _ptr(w), bl, n, _ptr(a1d), _ptr(a2d), float(b), float(tau),
                                               _stream_ptr(None))
         _capi.check(st, dev.ctx, "lob_potential2d_rows_f64")
