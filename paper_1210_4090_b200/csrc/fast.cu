@@ -519,7 +519,7 @@ struct MainShared {
     __align__(16) double ubuf[kC + 8];  // sources (unpadded) / then u^{n+1} (padded, stats)
     int3 queue[kQCap];
     __align__(16) double vbuf[kVCap];  // v_d of the tile's displacement range, converted to K(d)
-    int ya, yb, nq, dlo, dhi, DLg, DRg, mode, gate, abort, osc_exact;
+    int ya, yb, nq, nlong, dlo, dhi, DLg, DRg, mode, gate, abort, osc_exact;
     unsigned qwork, budget;            // long queued runs of the tile, and the walk's work budget
     int nruns, rs[kRuns], re[kRuns];  // runs of reaching sub-tiles (unrolled source ranges)
     unsigned int c_src, c_queued, c_qent;
@@ -763,6 +763,7 @@ __device__ __forceinline__ bool process_chunk(MainShared& S, const ChunkArgs& a,
                 if (qhi - qlo >= 32) atomicAdd(&S.qwork, static_cast<unsigned>(qhi - qlo + 1));
                 if (q < kQCap) {
                     S.queue[q] = make_int3(i, qlo, qhi);
+                    if (qhi - qlo >= kQShort) atomicAdd(&S.nlong, 1);  // finished by a whole warp
                 } else if (*reinterpret_cast<volatile unsigned*>(&S.qwork) <= S.budget) {
                     for (int d = qlo; d <= qhi; ++d) smem_fmin(&S.keys[off + d], __dadd_rn(u0, kvalue<TAB, KS>(a, d)));
                 } else {
@@ -786,7 +787,8 @@ __device__ __forceinline__ bool process_chunk(MainShared& S, const ChunkArgs& a,
                 for (int d = qe.y; d <= qe.z; ++d) smem_fmin(&S.keys[off + d], __dadd_rn(uy, kvalue<TAB, KS>(a, d)));
             }
         }
-        for (int e = warp; e < nq; e += kNT / 32) {
+        // (warps scan the queue for long runs only when there are any)
+        for (int e = S.nlong ? warp : nq; e < nq; e += kNT / 32) {
             const int3 qe = S.queue[e];
             if (qe.z - qe.y < kQShort) continue;
             const double uy = a.ub[qe.x + 1];
@@ -799,6 +801,7 @@ __device__ __forceinline__ bool process_chunk(MainShared& S, const ChunkArgs& a,
         if (threadIdx.x == 0) {
             S.c_qent += nq;
             S.nq = 0;
+            S.nlong = 0;
         }
         __syncthreads();
     }
@@ -1234,6 +1237,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
             S.dlo = dlo;
             S.dhi = dhi;
             S.nq = 0;
+            S.nlong = 0;
             S.abort = 0;
             S.qwork = 0;
             // queued candidates beyond this cost more than the direct formula over the window
@@ -1645,6 +1649,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
             S.dlo = DLg;
             S.dhi = DRg;
             S.nq = 0;
+            S.nlong = 0;
             S.abort = 0;
             S.qwork = 0;
             const double bud = LOB_HEAVY * static_cast<double>(jspan + 1) * static_cast<double>(2 * n + 1);
