@@ -1536,9 +1536,17 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
         __syncthreads();
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    // the line into shared memory (the keys area: U[j], j < n <= kT)
-    double* U = reinterpret_cast<double*>(S.keys);
+    // the line in the middle of the source buffer (Ub[j] = U(j), j < n <= kT), so the unrolled source
+    // range needs only its wrapped halos filled; the keys are initialised meanwhile
+    constexpr int kUbLen = kC + 8;
+    const int H0 = (kUbLen - n) / 2;
+    double* Ub = S.ubuf + H0;
+    auto init_keys = [&]() {
+        ulonglong2* k2 = reinterpret_cast<ulonglong2*>(S.keys);
+        for (int i = tid; i < (kT + 4) / 2; i += kNT) k2[i] = make_ulonglong2(kInfBits, kInfBits);
+    };
     if constexpr (LD == kLdClu) {
+        init_keys();
         // a cluster of kLC CTAs holds kLC adjacent columns c0 .. c0 + kLC - 1; CTA r reads rows
         // [r n/kLC, (r+1) n/kLC) of all kLC columns (64-byte row segments) and stores each value
         // into its column's CTA through distributed shared memory
@@ -1549,16 +1557,17 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
         cluster.sync();  // every CTA of the cluster runs: its shared memory may be written
         for (int e = tid; e < rows * kLC; e += kNT) {
             const int row = r * rows + e / kLC, col = e % kLC;
-            *cluster.map_shared_rank(U + row, col) = u[static_cast<int64_t>(row) * p.n + c0 + col];
+            *cluster.map_shared_rank(Ub + row, col) = u[static_cast<int64_t>(row) * p.n + c0 + col];
         }
         cluster.sync();
     } else if (LD == kLdTma && (smem_u32(smem_raw) & 127u) != 0u) {
         // (a TMA tensor copy needs a 128-byte aligned destination: strided loads otherwise)
-        for (int j = tid; j < n; j += kNT) U[j] = ul[j * is];
+        init_keys();
+        for (int j = tid; j < n; j += kNT) Ub[j] = ul[j * is];
     } else if constexpr (LD == kLdTma) {
         // columns (line & ~1, line | 1) x all rows in boxes of kTmaRows rows into the landing zone
-        // (land[2 j + pick] = U(j), over keys and the start of the source buffer), then compacted
-        // into U through registers
+        // (land[2 j + pick] = U(j), over the keys and the start of the source buffer), then
+        // compacted into the source buffer through registers
         unsigned long long* bar = reinterpret_cast<unsigned long long*>(S.queue);
         const double* land = reinterpret_cast<const double*>(smem_raw);
         if (tid == 0) {
@@ -1578,11 +1587,14 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
 #pragma unroll
         for (int m = 0; m < kPer; ++m) {
             const int j = tid + kNT * m;
-            if (j < n) U[j] = v[m];
+            if (j < n) Ub[j] = v[m];
         }
+        init_keys();
     } else {
-        for (int j = tid; j < n; j += kNT) U[j] = ul[j * is];
+        init_keys();
+        for (int j = tid; j < n; j += kNT) Ub[j] = ul[j * is];
     }
+    double* U = Ub;
     if (tid == 0) {
         const LineConst c = line_const(__ldg(drift_arr + line), p);
         L.hl = c.hl;
@@ -1663,25 +1675,24 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
     if (walk) {
         const int ya = S.ya, yb = S.yb, dlo = S.dlo, dhi = S.dhi;
         const unsigned budget = S.budget;
-        // the first source chunk straight from the staged line, before the keys take its place
-        int clen = min(kC, yb - ya + 1);
-        {
+        // the unrolled sources ya - 1 .. yb + 1 around the staged line: its wrapped halos, or (a
+        // range wider than the buffer) chunks read from global memory
+        const int lo = ya - 1, hi = yb + 1;
+        const bool inplace = H0 + lo >= 0 && H0 + hi <= kUbLen - 1;
+        int clen;
+        const double* ub0;
+        if (inplace) {
+            for (int y = lo + tid; y < 0; y += kNT) Ub[y] = Ub[y + n];
+            for (int y = n + tid; y <= hi; y += kNT) Ub[y] = Ub[y - n];
+            clen = yb - ya + 1;
+            ub0 = Ub + lo;
+        } else {
+            __syncthreads();  // the stats read the staged line
+            clen = min(kC, yb - ya + 1);
             int y0 = (ya - 1) % n;
             y0 += y0 < 0 ? n : 0;
-            if (clen + 2 <= 2 * n) {  // at most two wraps
-                for (int i = tid; i < clen + 2; i += kNT) {
-                    int y = y0 + i;
-                    y -= y >= n ? n : 0;
-                    S.ubuf[i] = U[y >= n ? y - n : y];
-                }
-            } else {
-                for (int i = tid; i < clen + 2; i += kNT) S.ubuf[i] = U[(y0 + i) % n];
-            }
-        }
-        __syncthreads();
-        {
-            ulonglong2* k2 = reinterpret_cast<ulonglong2*>(S.keys);
-            for (int i = tid; i < (kT + 4) / 2; i += kNT) k2[i] = make_ulonglong2(kInfBits, kInfBits);
+            for (int i = tid; i < clen + 2; i += kNT) S.ubuf[i] = ul[((y0 + i) % n) * is];
+            ub0 = S.ubuf;
         }
         // K(d) of the line's displacement range in shared memory when it fits (vbuf: the line
         // scratch above is dead once the constants are in registers)
@@ -1705,8 +1716,8 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
                 __syncthreads();
             }
             if (tid == 0) S.c_src += static_cast<unsigned>(clen);
-            const ChunkArgs ca{S.ubuf, clen, yc - jlo, jspan, ia, hl, hr, dlo, dhi, skt, p.vtab + p.vofs, drift, tau,
-                               nullptr};
+            const ChunkArgs ca{yc == ya ? ub0 : S.ubuf, clen, yc - jlo, jspan, ia, hl, hr, dlo, dhi, skt,
+                               p.vtab + p.vofs, drift, tau, nullptr};
             walk = kstage ? process_chunk<false, true>(S, ca, budget) : process_chunk<false, false>(S, ca, budget);
             if (!walk) break;  // the walk would cost more than the window: the direct formula
             yc += clen;
