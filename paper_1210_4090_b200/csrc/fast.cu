@@ -81,6 +81,9 @@ constexpr int kEmitUnroll = LOB_EMIT_UNROLL;  // sources in flight per lane in t
 #ifndef LOB_EMIT_SERIAL
 #define LOB_EMIT_SERIAL 0  // 1: each thread walks a contiguous block of sources (else lane-interleaved)
 #endif
+#ifndef LOB_EMIT_INTERLEAVE
+#define LOB_EMIT_INTERLEAVE 1  // warps take interleaved 32-source blocks (else one contiguous range each)
+#endif
 constexpr int kQCap = LOB_QCAP;  // queued source intervals (long / contended) per chunk
 #ifndef LOB_QSHORT
 #define LOB_QSHORT 8
@@ -719,6 +722,16 @@ __device__ __forceinline__ bool process_chunk(MainShared& S, const ChunkArgs& a,
         const double sl = slc, sr = __dsub_rn(un, u0);
         uc = un;
         slc = sr;
+#elif LOB_EMIT_INTERLEAVE
+    // warps take interleaved 32-source blocks (w, w + 8, ...): the uneven per-source work (long
+    // intervals, folds) spreads over all warps before the chunk's barrier
+    (void)lane;
+    (void)warp;
+    const int iend = a.clen;
+#pragma unroll kEmitUnroll
+    for (int i = threadIdx.x; i < iend; i += kNT) {
+        const double ul0 = a.ub[i], u0 = a.ub[i + 1], ur0 = a.ub[i + 2];
+        const double sl = __dsub_rn(u0, ul0), sr = __dsub_rn(ur0, u0);
 #else
     (void)lane;
     const int per = ((a.clen + kNT - 1) / kNT) * 32;
