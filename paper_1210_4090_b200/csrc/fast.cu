@@ -1161,6 +1161,21 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
         int Q0 = 0, Q1 = -1;
         // sub-tile Q of the unrolled source axis: its sources [ys, ye] and whether
         // their slope-implied displacements reach this tile's outputs
+        // sub-tile Q = k subs + q of the unrolled axis (k periods, q < subs); reach_kq takes the split
+        auto reach_kq = [&](int k, int q, int& ys, int& ye, int& dl, int& dr) {
+            const double2 sb = xload<CHAIN>(b.sub_in + line * p.subs + q);
+            ys = k * n + q * kG;
+            ye = ys + min(kG, n - q * kG) - 1;
+            if constexpr (TAB) {
+                tab_interval(sigg, lc, sb.x, sb.y, DLg, DRg, dl, dr);
+                dl = max(dl, DLg);
+                dr = min(dr, DRg);
+            } else {
+                dl = max(__double2int_ru(__fma_rn(sb.x, ia, hl)), DLg);
+                dr = min(__double2int_rd(__fma_rn(sb.y, ia, hr)), DRg);
+            }
+            return dl <= dr && ys + dl <= jhi && ye + dr >= jlo;
+        };
         auto reach = [&](int Q, int& ys, int& ye, int& dl, int& dr, int& q) {
             const int k = Q >= 0 ? Q / subs : -((subs - 1 - Q) / subs);
             q = Q - k * subs;
@@ -1187,9 +1202,22 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
             int k1 = k0;
             while (y1 - k1 * n >= n) ++k1;
             Q1 = k1 * subs + (y1 - k1 * n) / kG;
+            // lane l takes Q0 + l, Q0 + l + 32, ...: the (period, sub-tile) split advanced without a
+            // division per sub-tile (k0 periods and q0 = Q0 - k0 subs from the loop above)
+            int kq = k0, qq = Q0 - k0 * subs + lane;
+            while (qq >= subs) {
+                qq -= subs;
+                ++kq;
+            }
             for (int Q = Q0 + lane; Q <= Q1; Q += 32) {
-                int ys, ye, dl, dr, q;
-                if (reach(Q, ys, ye, dl, dr, q)) {
+                int ys, ye, dl, dr;
+                const bool hit = reach_kq(kq, qq, ys, ye, dl, dr);
+                qq += 32;
+                while (qq >= subs) {
+                    qq -= subs;
+                    ++kq;
+                }
+                if (hit) {
                     ya = min(ya, ys);
                     yb = max(yb, ye);
                     dlo = min(dlo, max(dl, jlo - ye));
