@@ -709,6 +709,10 @@ __device__ __forceinline__ void tab_interval(SIG sig, const LineConst& lc, doubl
 template <bool TAB, bool KS>
 __device__ __forceinline__ bool process_chunk(MainShared& S, const ChunkArgs& a, unsigned budget) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // the chunk's output base held in a register: opaque to the compiler, which otherwise
+    // re-derives it from the block index (an S2R on the emission loop's critical path)
+    int cbase;
+    asm volatile("mov.b32 %0, %1;" : "=r"(cbase) : "r"(a.base));
 #if LOB_EMIT_SERIAL
     // thread t walks the sources t*k .. t*k+k-1 (k odd: conflict-free strided shared loads), each
     // value and slope read once and carried to the next source
@@ -750,7 +754,7 @@ __device__ __forceinline__ bool process_chunk(MainShared& S, const ChunkArgs& a,
             dl = __double2int_ru(__fma_rn(sl, a.ia, a.hl));
             dr = __double2int_rd(__fma_rn(sr, a.ia, a.hr));
         }
-        const int off = a.base + i;  // output index of this source at d = 0
+        const int off = cbase + i;  // output index of this source at d = 0
         // every candidate lies in [dlo, dhi] when the statistics describe u;
         // the clamp keeps stale statistics memory-safe (wrong, never out of bounds)
         dl = max(max(dl, a.dlo), -off);
