@@ -1727,8 +1727,9 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
         int clen;
         const double* ub0;
         if (inplace) {
-            for (int y = lo + tid; y < 0; y += kNT) Ub[y] = Ub[y + n];
-            for (int y = n + tid; y <= hi; y += kNT) Ub[y] = Ub[y - n];
+            // (a halo may span more than one period when the window's centre lies beyond n)
+            for (int y = lo + tid; y < 0; y += kNT) Ub[y] = Ub[(y % n + n) % n];
+            for (int y = n + tid; y <= hi; y += kNT) Ub[y] = Ub[y % n];
             clen = yb - ya + 1;
             ub0 = Ub + lo;
         } else {

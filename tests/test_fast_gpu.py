@@ -479,3 +479,16 @@ def test_fast_rejects_internal_flags(dev):
     ws = torch.empty(dev.fast_workspace_bytes(1, 64), dtype=torch.uint8, device="cuda")
     with pytest.raises(api.InvalidInput):
         dev.fast_f64(u, torch.empty_like(u), to_dev(np.zeros(1)), 0.05, workspace=ws, flags=1 << 8)
+
+
+@pytest.mark.parametrize("n, drift", [(512, 68.4), (512, -90.0), (300, 80.0), (2048, 30.0)])
+def test_fast_window_centre_beyond_one_period(dev, orc, n, drift, kernel_mode):
+    """|tau P| between 1 and 2 (the window's centre llround(tau P / eps) lies between n and 2n, still
+    inside the cached v_d table): the walk runs with source ranges and halos spanning more than one
+    period; bit-exact against the oracle."""
+    tau = 0.02
+    x = np.arange(n) / n
+    u = np.stack([0.05 * np.sin(2 * np.pi * x), 0.03 * np.cos(4 * np.pi * x + 0.3)])
+    got, _, c = fast_step_counted(dev, u, drift, tau)
+    assert np.array_equal(got.cpu().numpy(), oracle_step(orc, u, drift, tau))
+    assert_walk(c)
