@@ -492,3 +492,17 @@ def test_fast_window_centre_beyond_one_period(dev, orc, n, drift, kernel_mode):
     got, _, c = fast_step_counted(dev, u, drift, tau)
     assert np.array_equal(got.cpu().numpy(), oracle_step(orc, u, drift, tau))
     assert_walk(c)
+
+
+@pytest.mark.parametrize("n, amp", [(2048, 5.0), (1000, 8.0)])
+def test_fast_wide_displacement_range(dev, orc, n, amp, kernel_mode):
+    """A kinked line whose slope range spans more displacements than the staged K buffer holds
+    (K read from the global v_d table in the emission) and more sources than the in-place source
+    layout of the whole-line kernel fits; bit-exact, the walk on every tile."""
+    tau = 0.01
+    x = np.arange(n) / n
+    u = np.stack([amp * np.abs(np.sin(2 * np.pi * x)), -amp * np.abs(np.sin(2 * np.pi * x + 0.4))])
+    got, _, c = fast_step_counted(dev, u, [0.2, -0.6], tau)
+    assert np.array_equal(got.cpu().numpy(), oracle_step(orc, u, np.array([0.2, -0.6]), tau))
+    assert_walk(c)
+    assert c["tiles_k_unstaged"] > 0, c
