@@ -1561,7 +1561,8 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
                                                                   const double* __restrict__ tv, int64_t tv_stride,
                                                                   unsigned long long* __restrict__ diag, FastParams p,
                                                                   const __grid_constant__ CUtensorMap tmap) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_line[];  // 128-byte aligned: TMA tensor copies land here
+    unsigned char* smem_raw = smem_line;
     MainShared& S = *reinterpret_cast<MainShared*>(smem_raw);
     LineShared& L = *reinterpret_cast<LineShared*>(S.vbuf);
     const int n = static_cast<int>(p.n);
@@ -2133,16 +2134,14 @@ int64_t fast_line_max() { return kT; }
 
 // the driver's cuTensorMapEncodeTiled through the runtime (no -lcuda link)
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
         void* f = nullptr;
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-    }
+            return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+        return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+    }();  // thread-safe one-time initialisation (function-local static)
     return fn;
 }
 
