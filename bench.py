@@ -601,7 +601,7 @@ def extras(dev):
     tvd = torch.from_numpy(api.tau_v(api.gen_potential(2, N_SPACE), TAU)).cuda()
     wse = torch.empty(dev.fast_workspace_bytes(LINES, N_SPACE), dtype=torch.uint8, device="cuda")
     dev.evolve(st, scr, dr, TAU, 200, tv=tvd, workspace=wse)
-    ne = 100
+    ne = 500  # one evolve call of 500 steps (C2 runs as one call of 5000)
     sd = torch.empty(ne * LINES, dtype=torch.float64, device="cuda")
     sb = torch.empty(ne * LINES, dtype=torch.int64, device="cuda")
     t = timeit(lambda: dev.evolve(st, scr, dr, TAU, ne, tv=tvd, step_drift=sd, step_blocks=sb, workspace=wse), 1)

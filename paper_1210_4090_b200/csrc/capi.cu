@@ -450,8 +450,16 @@ int lob_evolve_f64(lob_ctx* ctx, double* u, double* scratch, int64_t lines, int6
         return LOB_OK;
     }
     double* dpart = nullptr;
+    unsigned* dcount = nullptr;
+    // the fast engine on lines of more than one tile: each step's drift reduced inside its launch,
+    // so consecutive steps chain (a tile waits only for its own line's previous step)
+    const bool chained = engine == LOB_ENGINE_FAST && n > fast_line_max();
     if (engine == LOB_ENGINE_FAST)
         LOB_CUDA_TRY(ctx, cudaMallocAsync(&dpart, static_cast<size_t>(lines * fast_tiles(n)) * sizeof(double), s));
+    if (chained) {
+        LOB_CUDA_TRY(ctx, cudaMallocAsync(&dcount, static_cast<size_t>(lines) * sizeof(unsigned), s));
+        LOB_CUDA_TRY(ctx, cudaMemsetAsync(dcount, 0, static_cast<size_t>(lines) * sizeof(unsigned), s));
+    }
     double* cur = u;
     double* nxt = scratch;
     int64_t done = 0;
@@ -467,12 +475,20 @@ int lob_evolve_f64(lob_ctx* ctx, double* u, double* scratch, int64_t lines, int6
                                     step_blocks ? step_blocks + i * lines : nullptr, rws, rwsb, s);
         } else {
             // the drift's per-tile partial sums come out of the K2 epilogue (no second pass over u)
-            st = launch_fast_f64(ctx, cur, nxt, lines, n, drift, tau, tv, tv_stride, eta,
-                                 step_blocks ? step_blocks + i * lines : nullptr, workspace,
-                                 workspace_bytes, i == 0 ? 0 : LOB_FAST_STATS_VALID, s, dpart);
-            if (st == LOB_OK)
-                st = launch_drift_tiles(ctx, dpart, lines, n, step_drift ? step_drift + i * lines : nullptr, halt,
-                                        static_cast<int>(i), s);
+            if (chained) {
+                const FastDriftOut dout{step_drift ? step_drift + i * lines : nullptr, halt, dcount, static_cast<int>(i)};
+                st = launch_fast_f64(ctx, cur, nxt, lines, n, drift, tau, tv, tv_stride, eta,
+                                     step_blocks ? step_blocks + i * lines : nullptr, workspace, workspace_bytes,
+                                     LOB_FAST_CHAINED | (i == 0 ? 0 : LOB_FAST_STATS_VALID), s, dpart, nullptr,
+                                     nullptr, &dout);
+            } else {
+                st = launch_fast_f64(ctx, cur, nxt, lines, n, drift, tau, tv, tv_stride, eta,
+                                     step_blocks ? step_blocks + i * lines : nullptr, workspace,
+                                     workspace_bytes, i == 0 ? 0 : LOB_FAST_STATS_VALID, s, dpart);
+                if (st == LOB_OK)
+                    st = launch_drift_tiles(ctx, dpart, lines, n, step_drift ? step_drift + i * lines : nullptr,
+                                            halt, static_cast<int>(i), s);
+            }
         }
         if (st) break;
         if (engine != LOB_ENGINE_FAST)
@@ -500,6 +516,7 @@ int lob_evolve_f64(lob_ctx* ctx, double* u, double* scratch, int64_t lines, int6
     if (firsts) cudaFreeAsync(firsts, s);
     if (rws) cudaFreeAsync(rws, s);
     if (dpart) cudaFreeAsync(dpart, s);
+    if (dcount) cudaFreeAsync(dcount, s);
     cudaFreeAsync(halt, s);
     LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
     if (completed_steps) *completed_steps = done;

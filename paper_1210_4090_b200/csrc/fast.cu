@@ -132,6 +132,12 @@ struct FastParams {
     int fsm_on;  // the epilogue produces decompose()'s FSM summaries for the next step's block count
     int check;   // LOB_FAST_STATS_CHECK: compare u with the samples the statistics were taken with
     int samples; // the epilogue stores samples of u^{n+1} (a workspace that has seen a checked call)
+    // evolve's per-step drift reduced in the kernel (with dpart): the line's last tile to finish sums
+    // the tiles' partials in tile order (dcount: per-line arrival counter, monotonic across steps)
+    double* drift_out;
+    int* halt;
+    unsigned* dcount;
+    int dstep;
     double delta_override;  // NaN: the computed rounding bound delta (diagnostic hook, lob_ctx_set_fast_delta)
     // the caller's current per-line inputs (checked against the carried line constants)
     const double* drift_arr;                      // mechanical mode
@@ -1472,6 +1478,19 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
             double sum = 0.0;
             for (int w = 0; w < kNT / 32; ++w) sum += red[w];
             dpart[line * tiles + tile] = sum;
+            if (p.dcount) {
+                // the last tile of the line to arrive: the line's drift, partials in tile order (the
+                // drift_tiles_kernel's sum, so consecutive steps need no kernel in between)
+                __threadfence();
+                const unsigned old = atomicAdd(p.dcount + line, 1u);
+                if (old % static_cast<unsigned>(tiles) == static_cast<unsigned>(tiles - 1)) {
+                    __threadfence();
+                    double tot = 0.0;
+                    for (int t = 0; t < tiles; ++t) tot += __ldcg(dpart + line * tiles + t);
+                    if (p.drift_out) p.drift_out[line] = tot / static_cast<double>(n);
+                    if (!isfinite(tot) && p.halt) atomicMin(p.halt, p.dstep);
+                }
+            }
         }
     }
     if (tid == 0 && diag) {
@@ -2218,7 +2237,8 @@ int launch_line_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
 int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t n,
                     const double* drift, double tau, const double* tv, int64_t tv_stride,
                     double eta, int64_t* blocks, void* workspace, size_t ws_bytes, int flags,
-                    cudaStream_t s, double* dpart, const FastTable* tab, const FastSepPot* sep) {
+                    cudaStream_t s, double* dpart, const FastTable* tab, const FastSepPot* sep,
+                    const FastDriftOut* dout) {
     if (ws_bytes < fast_workspace_bytes(lines, n) || !workspace)
         return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_fast_f64: workspace too small");
     if (n > (1ll << 29)) return set_error(ctx, LOB_INVALID_INPUT, "fast: n too large");
@@ -2365,6 +2385,12 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     // the sampled check needs samples taken by this engine (not by a caller's statistics pass)
     p.check = (flags & LOB_FAST_STATS_CHECK) && (flags & LOB_FAST_STATS_VALID) && !given ? 1 : 0;
     p.samples = ctx->ws_sampling[workspace] ? 1 : 0;
+    if (dout && dpart) {
+        p.drift_out = dout->drift_out;
+        p.halt = dout->halt;
+        p.dcount = dout->dcount;
+        p.dstep = dout->step;
+    }
     ctx->ws_samples_valid[workspace] = p.samples != 0;
     ctx->ws_fsm_valid[workspace] = blocks != nullptr;
     dim3 grid(static_cast<unsigned>(p.tiles), static_cast<unsigned>(lines));

@@ -133,6 +133,14 @@ struct FastTable {
     int64_t stride;
     const int64_t* first;
 };
+// evolve's per-step drift reduced inside the K2 launch (with dpart): drift_out[line] (nullable),
+// atomicMin(halt, step) on a non-finite line; dcount: per-line arrival counters, zeroed once
+struct FastDriftOut {
+    double* drift_out;
+    int* halt;
+    unsigned* dcount;
+    int step;
+};
 // separable potential tau * (a1[line] * a2[j] + b) applied in K2's epilogue (device a1, a2)
 struct FastSepPot {
     const double* a1;
@@ -151,7 +159,7 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
                     const double* drift, double tau, const double* tv, int64_t tv_stride,
                     double eta, int64_t* blocks, void* workspace, size_t ws_bytes, int flags,
                     cudaStream_t s, double* dpart = nullptr, const FastTable* tab = nullptr,
-                    const FastSepPot* sep = nullptr);
+                    const FastSepPot* sep = nullptr, const struct FastDriftOut* dout = nullptr);
 // the statistics buffers the next launch_fast_f64 call on `workspace` reads (for kFastStatsGiven):
 // per-256-sample sub-tile slope bounds [lines][subs] (double2: min, max) and per-line keys
 // [lines][4] (umin, umax, smin, smax as order-preserving keys; the caller resets them)
