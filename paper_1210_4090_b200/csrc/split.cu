@@ -41,17 +41,24 @@ __global__ void __launch_bounds__(256) transpose_kernel(const double* __restrict
 // tile pitch of 65 doubles keeps the column reads at two wavefronts per half warp.  Launched
 // with programmatic dependent launch: the previous kernel's tail overlaps this prologue.
 constexpr int kTV = 64;
+#ifndef LOB_TRANSPOSE_ROWS
+#define LOB_TRANSPOSE_ROWS 32
+#endif
+// tiles of kTR rows x 64 columns: a 2048^2 transpose is 4096 CTAs (16.6 KB of shared memory
+// each, 8 per SM), so the last wave is nearly full
+constexpr int kTR = LOB_TRANSPOSE_ROWS;
+static_assert(kTR >= 4 && kTR <= 64 && 64 % kTR == 0, "rows per transpose tile");
 __global__ void __launch_bounds__(256) transpose64_kernel(const double* __restrict__ src,
                                                           double* __restrict__ dst, int64_t n) {
-    __shared__ double tile[kTV][kTV + 1];
+    __shared__ double tile[kTR][kTV + 1];
     const int64_t bx = static_cast<int64_t>(blockIdx.x) * kTV;  // column block of src
-    const int64_t by = static_cast<int64_t>(blockIdx.y) * kTV;  // row block of src
+    const int64_t by = static_cast<int64_t>(blockIdx.y) * kTR;  // row block of src
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const int64_t k = bx + 2 * lane;
 #pragma unroll
-    for (int r = w; r < kTV; r += 8) {
+    for (int r = w; r < kTR; r += 8) {
         const int64_t i = by + r;
         double2 v = make_double2(0.0, 0.0);
         if (i < n && k < n) v = *reinterpret_cast<const double2*>(src + i * n + k);
@@ -59,12 +66,17 @@ __global__ void __launch_bounds__(256) transpose64_kernel(const double* __restri
         tile[r][2 * lane + 1] = v.y;
     }
     __syncthreads();
-    const int64_t i = by + 2 * lane;
+    // each destination row (a source column) holds kTR values = kTR / 2 double2: a warp writes
+    // 64 / kTR rows per pass
+    constexpr int kHalf = kTR / 2, kRowsPerWarp = 32 / kHalf;
+    const int sub = lane / kHalf, e = lane % kHalf;
+    const int64_t i = by + 2 * e;
 #pragma unroll
-    for (int c = w; c < kTV; c += 8) {
+    for (int c0 = w * kRowsPerWarp; c0 < kTV; c0 += 8 * kRowsPerWarp) {
+        const int c = c0 + sub;
         const int64_t kk = bx + c;  // dst[kk][i] = src[i][kk]
         if (kk < n && i < n)
-            *reinterpret_cast<double2*>(dst + kk * n + i) = make_double2(tile[2 * lane][c], tile[2 * lane + 1][c]);
+            *reinterpret_cast<double2*>(dst + kk * n + i) = make_double2(tile[2 * e][c], tile[2 * e + 1][c]);
     }
 }
 
@@ -243,7 +255,7 @@ int launch_sub_table(lob_ctx* ctx, double* out, const double* tv, int64_t count,
 int launch_transpose(lob_ctx* ctx, const double* src, double* dst, int64_t n, cudaStream_t s) {
     if (n % 2 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0) {
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(static_cast<unsigned>((n + kTV - 1) / kTV), static_cast<unsigned>((n + kTV - 1) / kTV));
+        cfg.gridDim = dim3(static_cast<unsigned>((n + kTV - 1) / kTV), static_cast<unsigned>((n + kTR - 1) / kTR));
         cfg.blockDim = dim3(256);
         cfg.stream = s;
         cudaLaunchAttribute attr[1];

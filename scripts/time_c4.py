@@ -8,11 +8,17 @@ import sys
 import torch
 
 sys.path.insert(0, ".")
-from paper_1210_4090_b200 import api  # noqa: E402
+import os  # noqa: E402
+
+from paper_1210_4090_b200 import _capi, api  # noqa: E402
+
+if os.environ.get("LOB_LIB"):
+    _capi.LIB_PATH = os.path.abspath(os.environ["LOB_LIB"])
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=50)
 ap.add_argument("--mode", type=int, default=-1, help="time this fast_line mode only (no checks)")
+ap.add_argument("--time", type=int, default=-1, help="time this mode (and check it == K1 after 20 steps)")
 a = ap.parse_args()
 n, tau = 2048, 0.01
 dev = api.Device(0)
@@ -33,6 +39,20 @@ def run(line, engine, k0, k, u):
 
 
 res = {}
+if a.time >= 0:
+    ok = bool(torch.equal(run(a.time, api.ENGINE_FAST, 0, 20, u0), run(a.time, api.ENGINE_DIRECT, 0, 20, u0)))
+    u = run(a.time, api.ENGINE_FAST, 0, 5, u0)
+    torch.cuda.synchronize()
+    best = []
+    for r in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        u = run(a.time, api.ENGINE_FAST, 5, a.steps, u)
+        e1.record()
+        torch.cuda.synchronize()
+        best.append(e0.elapsed_time(e1) / a.steps)
+    print(json.dumps({"mode": a.time, "lib": os.environ.get("LOB_LIB", "default"), "equal_k1": ok, "ms": sorted(best)}))
+    sys.exit(0)
 if a.mode >= 0:
     u = run(a.mode, api.ENGINE_FAST, 0, a.steps, u0)
     torch.cuda.synchronize()
