@@ -15,6 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--pre", type=int, default=300)
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--lines", type=int, default=256)
+ap.add_argument("--blocks", action="store_true", help="request decompose() block counts")
 a = ap.parse_args()
 n, tau, L = 65536, 0.02, a.lines
 dev = api.Device(0)
@@ -29,10 +30,11 @@ for i in range(a.pre + a.steps):
 torch.cuda.synchronize()
 print("done", float(x.mean()))
 ws2 = torch.empty_like(ws)
-dev.fast_f64(x, y, dr, tau, tv=tv, workspace=ws2, flags=0)
+bl = torch.empty(L, dtype=torch.int64, device="cuda") if a.blocks else None
+dev.fast_f64(x, y, dr, tau, tv=tv, blocks=bl, workspace=ws2, flags=0)
 for i in range(5):
     x, y = y, x
-    dev.fast_f64(x, y, dr, tau, tv=tv, workspace=ws2, flags=api.FAST_STATS_VALID)
+    dev.fast_f64(x, y, dr, tau, tv=tv, blocks=bl, workspace=ws2, flags=api.FAST_STATS_VALID)
 c = dev.fast_counters(ws2, L, n)
 upd = 6 * L * n
 print({k: v / upd for k, v in c.items()}, c)
