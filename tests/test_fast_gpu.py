@@ -506,3 +506,36 @@ def test_fast_wide_displacement_range(dev, orc, n, amp, kernel_mode):
     assert np.array_equal(got.cpu().numpy(), oracle_step(orc, u, np.array([0.2, -0.6]), tau))
     assert_walk(c)
     assert c["tiles_k_unstaged"] > 0, c
+
+
+@pytest.mark.parametrize("n", [3, 5, 17, 255, 1023, 2047])
+def test_fast_short_odd_lines(dev, orc, n, kernel_mode):
+    """Short and odd line lengths (the whole-line kernel's range, both kernels), rough and smooth
+    lines with a drift: bit-exact."""
+    tau = max(0.02, 2.0 / n)  # eps / tau < 1
+    rng = np.random.default_rng(n)
+    x = np.arange(n) / n
+    u = np.stack([np.sin(2 * np.pi * x), rough_walk(rng, 1, n, 1.0)[0]])
+    for drift in (0.0, 0.7):
+        got, _, c = fast_step_counted(dev, u, drift, tau)
+        assert np.array_equal(got.cpu().numpy(), oracle_step(orc, u, drift, tau)), (n, drift)
+        assert c["missed_outputs"] == 0, c
+
+
+@pytest.mark.parametrize("n", [512, 4096])
+def test_fast_non_finite_inputs(dev, orc, n, kernel_mode):
+    """Lines holding NaN, +inf or -inf (the reference rejects them before stepping; the engine's
+    contract is the definition-level formula): the gate sends the line to the exact direct formula
+    and the result is the oracle's, NaN for NaN."""
+    tau = 0.02
+    x = np.arange(n) / n
+    u = np.stack([np.sin(2 * np.pi * x)] * 3)
+    u[0, n // 3] = np.nan
+    u[1, n // 2] = np.inf
+    u[2, n // 5] = -np.inf
+    got, _, c = fast_step_counted(dev, u, 0.3, tau)
+    want = oracle_step(orc, u, 0.3, tau)
+    g = got.cpu().numpy()
+    assert np.array_equal(np.isnan(g), np.isnan(want))
+    ok = ~np.isnan(want)
+    assert np.array_equal(g[ok], want[ok])
