@@ -38,6 +38,11 @@
 //    statistics of u^{n+1} for the next step, including decompose()'s block
 //    count (proj/src/minplus.cpp:152-188) as a composable 3-state
 //    transition summary per tile.
+// Lines of n <= 2048 run K2L instead (line_kernel): one CTA per whole line,
+// the statistics reduced from the staged line itself, nothing carried; its
+// load / store layouts (rows, strided columns, DSMEM cluster exchange, 2-D TMA
+// tensor maps) serve the 2-D split step.  K2R (resident_kernel) runs every
+// step of an evolve of short lines in one launch.
 #include <algorithm>
 #include <climits>
 #include <cmath>
