@@ -1808,13 +1808,43 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
     const double* sa2 = p.sa2;
     const double sb = p.sb;
     double* ostage = S.ubuf;  // ST == kStClu: the new line, for the cluster's row-segment stores
-#pragma unroll 4
-    for (int j = tid; j < n; j += kNT) {
-        const unsigned long long kk = S.keys[j + 1];
-        double best = __longlong_as_double(static_cast<long long>(kk));
-        if (kk == kInfBits) {
+    // thread t owns outputs t + kNT m: the potential's samples are loaded for all of them first (one
+    // memory latency, not kPer), the hot loop has no branch, and outputs no interval reached (+inf
+    // keys: never when the gate holds) are rescanned after it.  KIND 0: no potential (best - 0 ==
+    // best bitwise), 1: a tau*V table, 2: the separable tau*(a1 a2 + b).
+    auto epilogue = [&](auto kind_c) {
+        constexpr int KIND = decltype(kind_c)::value;
+        double t[kPer];
+#pragma unroll
+        for (int m = 0; m < kPer; ++m) {
+            const int j = tid + kNT * m;
+            t[m] = 0.0;
+            if constexpr (KIND == 1) t[m] = j < n ? __ldg(tvl + j) : 0.0;
+            if constexpr (KIND == 2) t[m] = j < n ? __ldg(sa2 + j) : 0.0;
+        }
+        auto tvof = [&](double x) -> double {
+            if constexpr (KIND == 2) return __dmul_rn(tau, __dadd_rn(__dmul_rn(sa1l, x), sb));
+            else return x;
+        };
+        unsigned miss = 0;
+#pragma unroll
+        for (int m = 0; m < kPer; ++m) {
+            const int j = tid + kNT * m;
+            if (j < n) {
+                const unsigned long long kk = S.keys[j + 1];
+                const double best = __longlong_as_double(static_cast<long long>(kk));
+                const double o = KIND == 0 ? best : __dsub_rn(best, tvof(t[m]));
+                if constexpr (ST == kStClu) ostage[j] = o;
+                else ol[j * os] = o;
+                miss |= static_cast<unsigned>(kk == kInfBits) << m;
+            }
+        }
+        while (miss) {  // cold: the direct formula over the whole window
+            const int m = __ffs(miss) - 1;
+            miss &= miss - 1;
+            const int j = tid + kNT * m;
             if (diag) atomicAdd(diag, 1ull);
-            best = INFINITY;
+            double best = INFINITY;
             int y = (j - first) % n;
             if (y < 0) y += n;
             for (int w = 0; w <= 2 * n; ++w) {
@@ -1822,14 +1852,17 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
                 best = c2 < best ? c2 : best;
                 y = y == 0 ? n - 1 : y - 1;
             }
+            double x = 0.0;  // (the sample reloaded: t[] stays in registers)
+            if constexpr (KIND == 1) x = __ldg(tvl + j);
+            if constexpr (KIND == 2) x = __ldg(sa2 + j);
+            const double o = KIND == 0 ? best : __dsub_rn(best, tvof(x));
+            if constexpr (ST == kStClu) ostage[j] = o;
+            else ol[j * os] = o;
         }
-        double t = 0.0;
-        if (tvl) t = __ldg(tvl + j);
-        else if (sa2) t = __dmul_rn(tau, __dadd_rn(__dmul_rn(sa1l, __ldg(sa2 + j)), sb));
-        const double o = __dsub_rn(best, t);
-        if constexpr (ST == kStClu) ostage[j] = o;
-        else ol[j * os] = o;
-    }
+    };
+    if (tvl) epilogue(std::integral_constant<int, 1>{});
+    else if (sa2) epilogue(std::integral_constant<int, 2>{});
+    else epilogue(std::integral_constant<int, 0>{});
     if constexpr (ST == kStClu) {
         cg::cluster_group cluster = cg::this_cluster();
         const int r = static_cast<int>(cluster.block_rank());
