@@ -988,6 +988,43 @@ __device__ __forceinline__ LineConst line_const(double drift, const FastParams& 
     return c;
 }
 
+// line_const for one warp (all lanes): the seven window values the gate needs are computed by
+// seven lanes at once, each v_d by build_kernel's two roundings (the cached table's own values,
+// build_vtab_kernel), so K2L's setup has no table round trip on its critical path.
+__device__ __forceinline__ LineConst line_const_warp(double drift, const FastParams& p) {
+    const int lane = threadIdx.x & 31;
+    const int64_t n = p.n;
+    const double tau = p.tau, eps = p.eps, a = p.a;
+    const int64_t center = llround(__ddiv_rn(__dmul_rn(tau, drift), eps));
+    const int64_t first = center - n;
+    const double uu = 1.1102230246251565e-16;
+    const double dm = fmax(fabs(static_cast<double>(first)), fabs(static_cast<double>(first + 2 * n)));
+    const double vmax = dm * eps / tau;
+    const double kmag = tau * (0.5 * vmax * vmax + fabs(drift) * vmax);
+    double delta = 2.0 * (32.0 * uu * kmag / a + 8.0 * uu * (2.0 * n + fabs(drift) * eps / a) + 1e-9);
+    if (p.delta_override == p.delta_override) delta = p.delta_override;
+    const bool intab = first >= -p.vofs && first + 2 * n <= p.vofs;
+    LineConst c{};
+    c.first = first;
+    c.pe = __dmul_rn(drift, eps);
+    const double pz = __dmul_rn(c.pe, p.ia);
+    c.hl = pz - (0.5 + delta);
+    c.hr = pz + (0.5 + delta);
+    c.drift = drift;
+    // lanes 0..4: K(center - 2 .. center + 2) inside the window; lane 5: K(first); lane 6: K(last)
+    const int64_t d = lane < 5 ? center - 2 + lane : (lane == 5 ? first : first + 2 * n);
+    double kv = INFINITY;
+    if (intab && lane < 7 && (lane >= 5 || (d >= first && d <= first + 2 * n)))
+        kv = kval_v(__ddiv_rn(__dmul_rn(static_cast<double>(d), eps), tau), drift, tau);
+    const double kfirst = __shfl_sync(0xffffffffu, kv, 5), klast = __shfl_sync(0xffffffffu, kv, 6);
+    double km = lane < 5 ? kv : INFINITY;
+#pragma unroll
+    for (int o = 4; o; o >>= 1) km = fmin(km, __shfl_xor_sync(0xffffffffu, km, o));
+    km = __shfl_sync(0xffffffffu, km, 0);
+    c.gap = intab ? fmin(kfirst, klast) - km : -INFINITY;
+    return c;
+}
+
 __global__ void line_setup_kernel(const double* __restrict__ drift_arr, int64_t lines, FastParams p,
                                   LineConst* __restrict__ lc) {
     const int64_t line = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1606,6 +1643,8 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
         __syncthreads();
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    // the line's drift, in flight with the line's samples (warp 0 derives the line constants)
+    const double ldrift = warp == 0 ? __ldg(drift_arr + line) : 0.0;
     // the line in the middle of the source buffer (Ub[j] = U(j), j < n <= kT), so the unrolled source
     // range needs only its wrapped halos filled; the keys are initialised meanwhile
     constexpr int kUbLen = kC + 8;
@@ -1665,13 +1704,15 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
         for (int j = tid; j < n; j += kNT) Ub[j] = ul[j * is];
     }
     double* U = Ub;
-    if (tid == 0) {
-        const LineConst c = line_const(__ldg(drift_arr + line), p);
-        L.hl = c.hl;
-        L.hr = c.hr;
-        L.gap = c.gap;
-        L.drift = c.drift;
-        L.first = c.first;
+    if (warp == 0) {
+        const LineConst c = line_const_warp(ldrift, p);
+        if (lane == 0) {
+            L.hl = c.hl;
+            L.hr = c.hr;
+            L.gap = c.gap;
+            L.drift = c.drift;
+            L.first = c.first;
+        }
     }
     __syncthreads();
     // enclosures of u and of its slopes s(j) = U(j+1) - U(j) (periodic): coarse order-preserving
