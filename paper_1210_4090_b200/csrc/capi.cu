@@ -25,6 +25,16 @@ int check_lines(lob_ctx* ctx, int64_t lines, int64_t n, const char* who) {
     return LOB_OK;
 }
 
+// validate(SchemeParams) of the reference (proj/src/scheme.cpp:39-53) with its defaults h0 = 1,
+// AntiCflMode::Fail: the same conditions, the same messages' leading text
+int check_scheme(lob_ctx* ctx, int64_t n, double tau, double eta) {
+    if (!(tau > 0.0)) return set_error(ctx, LOB_INVALID_INPUT, "SchemeParams: tau must be positive");
+    if (eta < 0.0) return set_error(ctx, LOB_INVALID_INPUT, "SchemeParams: eta must be >= 0");
+    if ((1.0 / static_cast<double>(n)) / tau >= 1.0)
+        return set_error(ctx, LOB_INVALID_INPUT, "SchemeParams: epsilon/tau violates epsilon/tau < h0");
+    return LOB_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -189,10 +199,7 @@ int lob_minplus_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lin
                          int flags, void* stream) {
     int st = check_lines(ctx, lines, n, "lob_minplus_fast_f64");
     if (st) return st;
-    if (!(tau > 0.0)) return set_error(ctx, LOB_INVALID_INPUT, "SchemeParams: tau must be positive");
-    if (eta < 0.0) return set_error(ctx, LOB_INVALID_INPUT, "SchemeParams: eta must be >= 0");
-    if ((1.0 / static_cast<double>(n)) / tau >= 1.0)
-        return set_error(ctx, LOB_INVALID_INPUT, "SchemeParams: epsilon/tau violates epsilon/tau < h0");
+    if ((st = check_scheme(ctx, n, tau, eta))) return st;
     if (lines == 0) return LOB_OK;
     if (!u || !out || !drift)
         return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_fast_f64: null buffer");
@@ -389,6 +396,7 @@ int lob_evolve_f64(lob_ctx* ctx, double* u, double* scratch, int64_t lines, int6
     if (st) return st;
     if (steps < 0) return set_error(ctx, LOB_INVALID_INPUT, "evolve: steps must be >= 0");
     if (completed_steps) *completed_steps = 0;
+    if ((st = check_scheme(ctx, n, tau, eta))) return st;  // evolve validates before stepping (scheme.cpp:211)
     if (lines == 0 || steps == 0) return LOB_OK;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     // direct engine needs the per-line kernel tables: built on the host
@@ -538,6 +546,7 @@ int lob_step_host_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines,
                       double eta, int engine, int64_t* blocks) {
     int st = check_lines(ctx, lines, n, "lob_step_host_f64");
     if (st) return st;
+    if ((st = check_scheme(ctx, n, tau, eta))) return st;
     if (lines == 0) return LOB_OK;
     cudaStream_t s = ctx->stream;
     const size_t ub = static_cast<size_t>(lines * n) * sizeof(double);

@@ -1,0 +1,167 @@
+"""Edge cases of the stepping path through the C-ABI, against the reference itself:
+empty batches, zero steps, the smallest grids the reference accepts (n_space = 1, 2, ...,
+proj/src/scheme.cpp:40), grids one sample either side of the K2 tile and K2L limits, and
+the argument checks that map to the reference's InvalidInput (proj/src/scheme.cpp:39-53)."""
+import numpy as np
+import pytest
+
+from paper_1210_4090_b200 import api
+
+pytestmark = pytest.mark.gpu
+
+
+def to_dev(x):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def windows(dev, n, tau, drifts):
+    import torch
+    ks = [dev.build_kernel(n, tau, float(d)) for d in drifts]
+    kt = to_dev(np.concatenate([k.window for k in ks]))
+    fr = torch.tensor([k.first for k in ks], dtype=torch.int64, device="cuda")
+    return kt, fr
+
+
+def all_engines(dev, u, drifts, tau, tv=None):
+    """One step of the same lines through K1 (screened and plain), K2, the window-table K2 and
+    the relaxed engine at eta = 0; returns {name: ndarray}."""
+    import torch
+    lines, n = u.shape
+    du, dd = to_dev(u), to_dev(drifts)
+    dtv = None if tv is None else to_dev(tv)
+    kt, fr = windows(dev, n, tau, drifts)
+    res = {}
+    for name, mode in (("k1_screened", api.DIRECT_SCREENED), ("k1_plain", api.DIRECT_PLAIN)):
+        dev.set_direct_mode(mode)
+        o = torch.empty_like(du)
+        dev.direct_f64(du, o, kt, fr, tv=dtv, ktab_stride=2 * n + 1)
+        res[name] = o
+    dev.set_direct_mode(api.DIRECT_SCREENED)
+    ws = torch.empty(dev.fast_workspace_bytes(lines, n), dtype=torch.uint8, device="cuda")
+    o = torch.empty_like(du)
+    dev.fast_f64(du, o, dd, tau, tv=dtv, workspace=ws)
+    res["k2"] = o
+    o = torch.empty_like(du)
+    ws2 = torch.empty(dev.fast_workspace_bytes(lines, n), dtype=torch.uint8, device="cuda")
+    dev.fast_window_f64(du, o, kt, fr, tau, tv=dtv, workspace=ws2, ktab_stride=2 * n + 1)
+    res["k2_window"] = o
+    o = torch.empty_like(du)
+    dev.relaxed_f64(du, o, kt, fr, 0.0, tv=dtv, ktab_stride=2 * n + 1)
+    res["relaxed_eta0"] = o
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in res.items()}
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 6])
+def test_smallest_grids_equal_the_reference(dev, ref, n):
+    """n_space = 1 is legal in the reference (SchemeParams: n_space >= 1); every engine gives
+    the reference's step on the smallest periodic grids (the window spans two periods of a line
+    shorter than a warp)."""
+    tau, lines = 1.5, 5  # epsilon/tau = 1/(1.5 n) < 1
+    rng = np.random.default_rng(n)
+    u = rng.uniform(-1, 1, (lines, n))
+    drifts = np.array([0.0, 0.4, -0.7, 1.0, -2.5])
+    v = rng.uniform(-1, 1, n)
+    want, _ = ref.step_lines(u, tau, drifts, v=v, engine=1)
+    for name, got in all_engines(dev, u, drifts, tau, tv=tau * v).items():
+        assert np.array_equal(got, want), (name, n)
+
+
+@pytest.mark.parametrize("n", [2047, 2048, 2049, 2050, 4095, 4097])
+def test_grids_around_the_tile_and_line_kernel_limits(dev, ref, n):
+    """One sample either side of K2L's whole-line limit and K2's 2048-output tile (a last tile of
+    1 or 2 outputs), odd and even: == the reference's step (Naive engine) for K1 and K2."""
+    import torch
+    tau, lines = 0.01, 3
+    rng = np.random.default_rng(n)
+    u = np.cumsum(rng.uniform(-1.0 / n, 1.0 / n, (lines, n)), axis=1)
+    u -= np.linspace(0, 1, n, endpoint=False)[None, :] * u[:, -1:]
+    u += 0.2 * np.sin(2 * np.pi * np.arange(n) / n)[None, :]
+    drifts = np.array([0.3, -0.7, 1.9])
+    want, wb = ref.step_lines(u, tau, drifts, engine=1, nthreads=3)
+    du, dd = to_dev(u), to_dev(drifts)
+    kt, fr = windows(dev, n, tau, drifts)
+    o1 = torch.empty_like(du)
+    dev.direct_f64(du, o1, kt, fr, ktab_stride=2 * n + 1)
+    ws = torch.empty(dev.fast_workspace_bytes(lines, n), dtype=torch.uint8, device="cuda")
+    o2 = torch.empty_like(du)
+    bl = torch.empty(lines, dtype=torch.int64, device="cuda")
+    dev.fast_f64(du, o2, dd, tau, blocks=bl, workspace=ws)
+    torch.cuda.synchronize()
+    assert np.array_equal(o1.cpu().numpy(), want)
+    assert np.array_equal(o2.cpu().numpy(), want)
+    assert list(bl.cpu().numpy()) == list(wb)
+    c = dev.fast_counters(ws, lines, n)
+    assert c["missed_outputs"] == 0, c
+
+
+def test_empty_batch_is_a_no_op(dev):
+    """lines = 0: every batched entry returns success without touching anything."""
+    import torch
+    n, tau = 64, 0.05
+    u = torch.empty((0, n), dtype=torch.float64, device="cuda")
+    out = torch.empty_like(u)
+    dd = torch.empty(0, dtype=torch.float64, device="cuda")
+    k = dev.build_kernel(n, tau, 0.5)
+    kt = to_dev(k.window)
+    fr = torch.tensor([k.first], dtype=torch.int64, device="cuda")
+    ws = torch.empty(max(1, dev.fast_workspace_bytes(1, n)), dtype=torch.uint8, device="cuda")
+    dev.direct_f64(u, out, kt, fr)
+    dev.fast_f64(u, out, dd, tau, workspace=ws)
+    dev.fast_window_f64(u, out, kt, fr, tau, workspace=ws)
+    dev.relaxed_f64(u, out, kt, fr, 0.0, workspace=ws)
+    assert dev.evolve(u, out, dd, tau, 3, workspace=ws) in (0, 3)
+    got = dev.step_host(np.empty((0, n)), np.empty(0), tau)
+    assert got.shape == (0, n)
+    torch.cuda.synchronize()
+
+
+def test_zero_steps_leave_the_state_untouched(dev):
+    import torch
+    n, tau, lines = 256, 0.05, 2
+    rng = np.random.default_rng(1)
+    u = rng.uniform(-1, 1, (lines, n))
+    du = to_dev(u)
+    sc = torch.full_like(du, 7.0)
+    ws = torch.empty(dev.fast_workspace_bytes(lines, n), dtype=torch.uint8, device="cuda")
+    for eng in (api.ENGINE_FAST, api.ENGINE_DIRECT):
+        done = dev.evolve(du, sc, to_dev(np.array([0.5, -0.5])), tau, 0, engine=eng, workspace=ws)
+        torch.cuda.synchronize()
+        assert done == 0
+        assert np.array_equal(du.cpu().numpy(), u)
+
+
+def test_invalid_arguments_map_to_invalid_input(dev):
+    """The reference's validate(SchemeParams) (proj/src/scheme.cpp:39-53): n_space < 1, tau <= 0,
+    eta < 0 and the anti-CFL bound epsilon/tau >= h0 = 1 all throw InvalidInput; so do the
+    C-ABI entries, before any launch."""
+    import torch
+    n = 64
+    u = torch.zeros((2, n), dtype=torch.float64, device="cuda")
+    out = torch.empty_like(u)
+    dd = torch.zeros(2, dtype=torch.float64, device="cuda")
+    ws = torch.empty(dev.fast_workspace_bytes(2, n), dtype=torch.uint8, device="cuda")
+    with pytest.raises(api.InvalidInput):
+        dev.fast_f64(u, out, dd, 0.0, workspace=ws)  # tau must be positive
+    with pytest.raises(api.InvalidInput):
+        dev.fast_f64(u, out, dd, -0.1, workspace=ws)
+    with pytest.raises(api.InvalidInput):
+        dev.fast_f64(u, out, dd, 1.0 / n, workspace=ws)  # epsilon/tau == 1: anti-CFL
+    with pytest.raises(api.InvalidInput):
+        dev.fast_f64(u, out, dd, 0.05, eta=-1e-3, workspace=ws)
+    with pytest.raises(api.InvalidInput):
+        dev.evolve(u, out, dd, 1.0 / (2 * n), 1, workspace=ws)  # epsilon/tau = 2
+    with pytest.raises(api.InvalidInput):
+        dev.build_kernel(n, 1.0 / n, 0.0)
+    with pytest.raises(api.InvalidInput):
+        dev.build_kernel(0, 0.05, 0.0)
+    with pytest.raises(api.InvalidInput):
+        dev.step_host(np.zeros((2, n)), np.zeros(2), 0.0)
+    # a workspace too small for the batch is rejected, not overrun
+    with pytest.raises(api.InvalidInput):
+        dev.fast_f64(u, out, dd, 0.05, workspace=ws[:64])
+    # nothing above left an error behind: a valid call still works
+    dev.fast_f64(u, out, dd, 0.05, workspace=ws)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), np.zeros((2, n)))
