@@ -167,7 +167,6 @@ int lob_minplus_window_f64(lob_ctx* ctx, const double* u, double* out, int64_t l
     if (st) return st;
     if (m < 1) return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_window_f64: empty sample vector");
     if (lines == 0) return LOB_OK;
-    if (lines > 65535) return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_window_f64: too many lines");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     int* d_err = nullptr;
     LOB_CUDA_TRY(ctx, cudaMallocAsync(&d_err, sizeof(int), s));
@@ -779,10 +778,6 @@ int lob_split_step_nd_window_f64(lob_ctx* ctx, const double* u, double* out, dou
         int64_t B = 1;
         for (int b = a + 1; b < rank; ++b) B *= dims[b];
         const int64_t A = total / (L * B), lines = A * B;
-        if (lines > 65535) {
-            st = set_error(ctx, LOB_INVALID_INPUT, "split_step_nd (windowed): more than 65535 lines per axis");
-            break;
-        }
         std::fill(hf.begin(), hf.begin() + lines, firsts[a]);
         LOB_CUDA_TRY(ctx, cudaMemcpyAsync(dfirst, hf.data(), lines * sizeof(int64_t), cudaMemcpyHostToDevice, s));
         LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));

@@ -97,10 +97,10 @@ int launch_cfg(lob_ctx* ctx, const T* u, T* out, int64_t lines, int64_t n, const
 __global__ void window_kernel(const double* __restrict__ u, double* __restrict__ out, int64_t m,
                               int64_t n, const double* __restrict__ ktab, int64_t ktab_stride,
                               const int64_t* __restrict__ first_arr, const double* __restrict__ tv,
-                              int64_t tv_stride, int* err) {
-    const int64_t line = blockIdx.y;
+                              int64_t tv_stride, int* err, int64_t lines) {
+    const int64_t line = grid_line();
     const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (j >= m) return;
+    if (j >= m || line >= lines) return;
     const int64_t W = 2 * n + 1;
     const int64_t r = j - first_arr[line];  // conv index j + shift (proj/src/scheme.cpp:137)
     if (r < 0 || r >= W + m - 1) {
@@ -150,9 +150,9 @@ int launch_direct_f32(lob_ctx* ctx, const float* u, float* out, int64_t lines, i
 int launch_window_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, int64_t m,
                       int64_t n, const double* ktab, int64_t ktab_stride, const int64_t* first,
                       const double* tv, int64_t tv_stride, int* d_err, cudaStream_t s) {
-    dim3 grid(static_cast<unsigned>((m + 127) / 128), static_cast<unsigned>(lines));
+    const dim3 grid = line_grid(static_cast<unsigned>((m + 127) / 128), lines);
     window_kernel<<<grid, 128, 0, s>>>(u, out, m, n, ktab, ktab_stride, first, tv, tv_stride,
-                                       d_err);
+                                       d_err, lines);
     ctx->launches += 1;
     return cuda_status(ctx, cudaGetLastError(), "window_kernel launch");
 }

@@ -127,6 +127,7 @@ static_assert(kPer % 2 == 0, "FSM pairs");
 
 struct FastParams {
     int64_t n;
+    int64_t lines;  // lines of the batch (fast_kernel: CTAs of the folded grid past it exit)
     int64_t tiles;  // ceil(n / kT)
     int64_t subs;   // ceil(n / kG)
     double tau;
@@ -1096,7 +1097,8 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) fast_kernel(
     const int n = static_cast<int>(p.n);
     const int tiles = static_cast<int>(p.tiles), subs = static_cast<int>(p.subs);
     const int tile = blockIdx.x;
-    const int64_t line = blockIdx.y;
+    const int64_t line = grid_line();
+    if (line >= p.lines) return;  // (uniform per CTA: before any barrier)
     const int j0 = tile * kT;
     const int Tl = min(kT, n - j0);
     const int jlo = j0 - 1;     // outputs evaluated: jlo .. jlo + jspan (unrolled)
@@ -2321,7 +2323,6 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     if (ws_bytes < fast_workspace_bytes(lines, n) || !workspace)
         return set_error(ctx, LOB_INVALID_INPUT, "lob_minplus_fast_f64: workspace too small");
     if (n > (1ll << 29)) return set_error(ctx, LOB_INVALID_INPUT, "fast: n too large");
-    if (lines > 65535) return set_error(ctx, LOB_INVALID_INPUT, "fast: at most 65535 lines per call");
     int st = ensure_lut(ctx);
     if (st) return st;
     FastParams p = make_params(n, tau, eta);
@@ -2472,7 +2473,8 @@ int launch_fast_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines, i
     }
     ctx->ws_samples_valid[workspace] = p.samples != 0;
     ctx->ws_fsm_valid[workspace] = blocks != nullptr;
-    dim3 grid(static_cast<unsigned>(p.tiles), static_cast<unsigned>(lines));
+    const dim3 grid = line_grid(static_cast<unsigned>(p.tiles), lines);
+    p.lines = lines;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(kNT);

@@ -59,6 +59,20 @@ struct lob_ctx {
 
 namespace lob {
 
+// Batches of more than 65535 lines (gridDim.y's limit): the line index folded over grid.y
+// and grid.z, line = blockIdx.y + kGridY * blockIdx.z, CTAs past the last line exit.
+constexpr unsigned kGridY = 65535u;
+#ifdef __CUDACC__
+inline dim3 line_grid(unsigned gx, int64_t lines) {
+    return dim3(gx, static_cast<unsigned>(lines < kGridY ? lines : kGridY),
+                static_cast<unsigned>((lines + kGridY - 1) / kGridY));
+}
+__device__ __forceinline__ int64_t grid_line() {
+    return static_cast<int64_t>(blockIdx.y) + static_cast<int64_t>(kGridY) * blockIdx.z;
+}
+#endif
+
+
 // true the first time `key` is seen by this context (per-device state is per context)
 inline bool first_time(lob_ctx* ctx, const void* key) { return ctx->done_once.insert(key).second; }
 

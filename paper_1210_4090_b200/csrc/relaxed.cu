@@ -157,10 +157,12 @@ __global__ void __launch_bounds__(kNTs) relaxed_scatter_kernel(const double* __r
                                                                int64_t ktab_stride, const int2* __restrict__ pieces,
                                                                const int* __restrict__ npieces,
                                                                unsigned long long* __restrict__ conv,
-                                                               int periodic = 1, int64_t nf_arg = -1) {
+                                                               int periodic = 1, int64_t nf_arg = -1,
+                                                               int64_t lines = 1) {
     __shared__ double gv[kCap + 1], gs[kCap];
     __shared__ int I[kCap + 1];  // merge: I_j; envelope: i_j (index 0 = P0)
-    const int64_t line = blockIdx.y;
+    const int64_t line = grid_line();
+    if (line >= lines) return;  // (uniform per CTA: before any barrier)
     const double* ul = u + line * (periodic ? n : n + 1);
     const double* K = ktab + line * ktab_stride;
     const int nf = static_cast<int>(nf_arg < 0 ? 2 * n : nf_arg);  // kernel slopes
@@ -225,10 +227,11 @@ __global__ void __launch_bounds__(kNTs) relaxed_scatter_kernel(const double* __r
 // (min_pointwise's gap check, proj/src/minplus.cpp:271-272).
 __global__ void relaxed_finalize_kernel(const unsigned long long* __restrict__ conv, int64_t n,
                                         const int64_t* __restrict__ first_arr, const double* __restrict__ tv,
-                                        int64_t tv_stride, double* __restrict__ out, int* __restrict__ flag) {
-    const int64_t line = blockIdx.y;
+                                        int64_t tv_stride, double* __restrict__ out, int* __restrict__ flag,
+                                        int64_t lines) {
+    const int64_t line = grid_line();
     const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (j >= n) return;
+    if (j >= n || line >= lines) return;
     const unsigned long long* cl = conv + line * (3 * n + 1);
     const int64_t shift = -first_arr[line];  // half - center_index
     int64_t i = (j + shift) % n;
@@ -284,7 +287,6 @@ int launch_relaxed_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines
                        int64_t* blocks, void* workspace, size_t ws_bytes, cudaStream_t s) {
     if (!(eta >= 0.0)) return set_error(ctx, LOB_INVALID_INPUT, "decompose: eta must be >= 0");
     if (n > (1ll << 29)) return set_error(ctx, LOB_INVALID_INPUT, "relaxed: n too large");
-    if (lines > 65535) return set_error(ctx, LOB_INVALID_INPUT, "relaxed: at most 65535 lines per call");
     const RelaxedWs w = relaxed_layout(workspace, lines, n);
     if (!workspace || ws_bytes < w.total) return set_error(ctx, LOB_INVALID_INPUT, "relaxed: workspace too small");
     LOB_CUDA_TRY(ctx, cudaMemsetAsync(w.conv, 0xff, static_cast<size_t>(lines) * (3 * n + 1) * 8, s));
@@ -292,10 +294,10 @@ int launch_relaxed_f64(lob_ctx* ctx, const double* u, double* out, int64_t lines
     relaxed_decompose_kernel<<<static_cast<unsigned>((lines + 63) / 64), 64, 0, s>>>(u, lines, n, eta, w.pieces,
                                                                                     w.npieces, blocks, w.flag);
     const unsigned gx = static_cast<unsigned>(std::min<int64_t>(n, std::max<int64_t>(1, 2 * ctx->sm_count)));
-    relaxed_scatter_kernel<<<dim3(gx, static_cast<unsigned>(lines)), kNTs, 0, s>>>(u, n, ktab, ktab_stride, w.pieces,
-                                                                                  w.npieces, w.conv);
-    relaxed_finalize_kernel<<<dim3(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>(lines)), 256, 0, s>>>(
-        w.conv, n, first, tv, tv_stride, out, w.flag);
+    relaxed_scatter_kernel<<<line_grid(gx, lines), kNTs, 0, s>>>(u, n, ktab, ktab_stride, w.pieces, w.npieces, w.conv, 1,
+                                                                 -1, lines);
+    relaxed_finalize_kernel<<<line_grid(static_cast<unsigned>((n + 255) / 256), lines), 256, 0, s>>>(
+        w.conv, n, first, tv, tv_stride, out, w.flag, lines);
     ctx->launches += 3;
     LOB_CUDA_TRY(ctx, cudaGetLastError());
     int hflag = 0;

@@ -52,9 +52,10 @@ constexpr int kParts = 4;
 __global__ void __launch_bounds__(32 * kParts) semidiscrete_kernel(
     const double* __restrict__ u, double* __restrict__ out, int64_t m, int64_t n, int periodic, double origin,
     double step, const double* __restrict__ ktab, int64_t first, double tau, int q, SemiPot P,
-    int* __restrict__ err) {
+    int* __restrict__ err, int64_t lines) {
     __shared__ double part[kParts][32];
-    const int64_t line = blockIdx.y;
+    const int64_t line = grid_line();
+    if (line >= lines) return;  // (uniform per CTA: before any barrier)
     const int lane = threadIdx.x & 31, pw = threadIdx.x >> 5;
     const int64_t j = static_cast<int64_t>(blockIdx.x) * 32 + lane;
     const double* ul = u + line * m;
@@ -142,15 +143,14 @@ extern "C" int lob_step_semidiscrete_f64(lob_ctx* ctx, const double* u, double* 
             P.am[r] = V->amplitude * mod;
         }
     }
-    if (lines > 65535) return set_error(ctx, LOB_INVALID_INPUT, "step_semidiscrete: at most 65535 lines");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     int* err = nullptr;
     LOB_CUDA_TRY(ctx, cudaMallocAsync(&err, sizeof(int), s));
     LOB_CUDA_TRY(ctx, cudaMemsetAsync(err, 0, sizeof(int), s));
     const double step = 1.0 / static_cast<double>(n_space);
-    const dim3 grid(static_cast<unsigned>((m + 31) / 32), static_cast<unsigned>(lines));
+    const dim3 grid = line_grid(static_cast<unsigned>((m + 31) / 32), lines);
     semidiscrete_kernel<<<grid, 32 * kParts, 0, s>>>(u, out, m, n_space, periodic, origin, step, ktab, first, tau,
-                                             quad_points, P, err);
+                                             quad_points, P, err, lines);
     ctx->launches += 1;
     int herr = 0;
     LOB_CUDA_TRY(ctx, cudaGetLastError());

@@ -165,3 +165,61 @@ def test_invalid_arguments_map_to_invalid_input(dev):
     dev.fast_f64(u, out, dd, 0.05, workspace=ws)
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), np.zeros((2, n)))
+
+
+def test_more_lines_than_one_grid_dimension(dev, orc, ref):
+    """Batches of more than 65535 lines (a 256^3 tensor has 65536 lines per axis sweep): the line
+    index is folded over two grid dimensions; every line of K2 (tiled and whole-line), the
+    relaxed engine, the windowed K1 and the semi-discrete step equals the oracle's / the
+    reference's, the last lines included."""
+    import torch
+    lines, n, tau = 65535 + 70, 8, 0.5
+    rng = np.random.default_rng(65535)
+    u = rng.uniform(-1, 1, (lines, n))
+    drifts = rng.uniform(-1.5, 1.5, lines)
+    k = [orc.kernel(n, tau, float(d)) for d in drifts[-80:]]
+    # the last 80 lines (both sides of the fold) against the oracle, each with its own window
+    K = np.ascontiguousarray(np.stack([x[0] for x in k]))
+    first = np.array([x[1] for x in k], np.int64)
+    want_tail = orc.direct(u[-80:], K, first, ktab_stride=2 * n + 1)
+    du, dd = to_dev(u), to_dev(drifts)
+    ws = torch.empty(dev.fast_workspace_bytes(lines, n), dtype=torch.uint8, device="cuda")
+    outs = {}
+    for mode in (0, 2):  # tiled fast_kernel, whole-line K2L
+        dev.set_fast_line(mode)
+        o = torch.empty_like(du)
+        bl = torch.empty(lines, dtype=torch.int64, device="cuda") if mode == 0 else None
+        dev.fast_f64(du, o, dd, tau, blocks=bl, workspace=ws)
+        torch.cuda.synchronize()
+        outs[mode] = o.cpu().numpy()
+        assert np.array_equal(outs[mode][-80:], want_tail), mode
+    dev.set_fast_line(2)
+    assert np.array_equal(outs[0], outs[2])
+    # one shared window for the table engines
+    kw, kfirst, _, _ = orc.kernel(n, tau, 0.25)
+    kt = to_dev(kw)
+    fr = torch.full((lines,), int(kfirst), dtype=torch.int64, device="cuda")
+    want = orc.direct(u, kw, np.array([kfirst], np.int64))
+    o = torch.empty_like(du)
+    dev.relaxed_f64(du, o, kt, fr, 0.0)
+    torch.cuda.synchronize()
+    assert np.array_equal(o.cpu().numpy(), want)
+    o2 = torch.empty_like(du)
+    dev.fast_window_f64(du, o2, kt, fr[:1], tau, workspace=ws)
+    torch.cuda.synchronize()
+    assert np.array_equal(o2.cpu().numpy(), want)
+    # windowed (wall) lines of m = 12 samples through the windowed K1: the last lines == the reference
+    m = 12
+    uw = rng.uniform(-1, 1, (lines, m))
+    o3 = torch.empty((lines, m), dtype=torch.float64, device="cuda")
+    dev.window_f64(to_dev(uw), o3, n, kt, fr[:1])
+    torch.cuda.synchronize()
+    got = o3.cpu().numpy()
+    for l in (0, 65534, 65535, 65536, lines - 1):
+        w, _, st = ref.kinetic_convolve(uw[l], n, tau, 0.25, periodic=False)
+        assert st == 0 and np.array_equal(got[l], w), l
+    # semi-discrete step with a zero potential == the fully discrete one (q = 1, V = 0)
+    o4 = torch.empty_like(du)
+    dev.step_semidiscrete(du, o4, kt, int(kfirst), 0.0, tau)
+    torch.cuda.synchronize()
+    assert np.array_equal(o4.cpu().numpy(), want)

@@ -77,3 +77,25 @@ def test_split_nd_windowed_equals_reference(dev, ref, dims, n, tau):
     ks = [dev.build_kernel(n, tau, d) for d in drifts]
     dev.split_step_nd_window(du, out, tmp, dims, n, tau, ks, tv=torch.from_numpy((tau * v).ravel()).cuda())
     assert np.array_equal(out.cpu().numpy(), want)
+
+
+def test_split_nd_rank3_with_more_than_65535_lines_per_sweep(dev):
+    """A 256^3 tensor has 65536 lines per axis sweep, one more than a grid dimension holds: the
+    fast engine (lines folded over two grid dimensions; whole-line and tiled kernels) == the direct
+    engine (a flat grid) on every point, with a potential."""
+    rank, n, tau = 3, 256, 0.02
+    rng = np.random.default_rng(256)
+    x = np.arange(n) / n
+    g = np.meshgrid(x, x, x, indexing="ij")
+    u = np.sin(2 * np.pi * g[0]) + np.cos(4 * np.pi * g[1] + 0.5) * np.sin(2 * np.pi * g[2]) + \
+        rng.uniform(-1e-3, 1e-3, (n,) * 3)
+    v = np.cos(2 * np.pi * g[0]) * np.cos(2 * np.pi * g[2]) + 0.3 * np.sin(2 * np.pi * g[1])
+    drifts = [0.3, -0.7, 0.45]
+    want = _run(dev, u, rank, n, tau, drifts, tau * v, 0.0, api.ENGINE_DIRECT)
+    for mode in (2, 0):
+        dev.set_fast_line(mode)
+        try:
+            got = _run(dev, u, rank, n, tau, drifts, tau * v, 0.0, api.ENGINE_FAST)
+        finally:
+            dev.set_fast_line(2)
+        assert np.array_equal(got, want), mode
