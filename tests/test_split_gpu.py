@@ -117,3 +117,28 @@ def test_split_fast_layouts_vs_reference(dev, ref, mode, n):
     finally:
         dev.set_fast_line(2)
     assert np.array_equal(got, ref.split_step_2d(u, tau, 0.3, -0.7, pot_kind=1, t=t))
+
+
+@pytest.mark.parametrize("n", [2051, 2304, 4096])
+def test_split_fast_beyond_the_whole_line_limit(dev, n):
+    """n > 2048: the split step leaves the whole-line kernel for the tiled K2 (statistics-producing
+    transposes, a last tile of 3 or 256 samples, an odd n without bulk copies).  Three steps of
+    the fast engine, both workspace layouts, == the direct engine on every point."""
+    import torch
+    tau = 0.01
+    u0 = torch.from_numpy(api.gen_c4_u0(n)).cuda()
+    am = torch.from_numpy(api.gen_cos(n)).cuda()
+
+    def run(engine, halves):
+        u, o, t = u0.clone(), torch.empty_like(u0), torch.empty_like(u0)
+        ws = torch.empty(halves * dev.fast_workspace_bytes(n, n), dtype=torch.uint8, device="cuda")
+        for i in range(3):
+            dev.split_step_2d(u, o, t, tau, 0.3, -0.7, a1=am, a2=am, b=api.c4_time_term(i * tau + tau),
+                              engine=engine, workspace=ws)
+            u, o = o, u
+        torch.cuda.synchronize()
+        return u.cpu().numpy()
+
+    want = run(api.ENGINE_DIRECT, 1)
+    assert np.array_equal(run(api.ENGINE_FAST, 1), want)
+    assert np.array_equal(run(api.ENGINE_FAST, 2), want)
