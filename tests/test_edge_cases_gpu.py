@@ -223,3 +223,24 @@ def test_more_lines_than_one_grid_dimension(dev, orc, ref):
     dev.step_semidiscrete(du, o4, kt, int(kfirst), 0.0, tau)
     torch.cuda.synchronize()
     assert np.array_equal(o4.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("lines", [1, 3, 7, 9, 17])
+@pytest.mark.parametrize("engine", [api.ENGINE_FAST, api.ENGINE_DIRECT, api.ENGINE_RELAXED])
+def test_host_step_with_fewer_lines_than_pipeline_chunks(dev, orc, lines, engine):
+    """lob_step_host_f64 pipelines the lines in 8 chunks: batches smaller than, equal to one more than,
+    and not divisible by the chunk count give the oracle's step and block counts line by line."""
+    n, tau = 512, 0.05
+    rng = np.random.default_rng(lines)
+    u = np.cumsum(rng.uniform(-2.0 / n, 2.0 / n, (lines, n)), axis=1)
+    u -= np.linspace(0, 1, n, endpoint=False)[None, :] * u[:, -1:]
+    drifts = rng.uniform(-1, 1, lines)
+    v = np.cos(2 * np.pi * np.arange(n) / n)
+    blocks = np.empty(lines, np.int64)
+    got = dev.step_host(u, drifts, tau, tv=tau * v, engine=engine, blocks=blocks)
+    ks = [orc.kernel(n, tau, float(d)) for d in drifts]
+    K = np.ascontiguousarray(np.stack([k[0] for k in ks]))
+    first = np.array([k[1] for k in ks], np.int64)
+    want = orc.direct(u, K, first, tv=tau * v, ktab_stride=2 * n + 1)
+    assert np.array_equal(got, want)
+    assert list(blocks) == [orc.line_blocks(u[l]) for l in range(lines)]
