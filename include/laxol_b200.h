@@ -15,6 +15,9 @@
  *    domain, no duplicated seam (the host GridFn keeps n+1 samples,
  *    proj/include/laxol/grid_fn.hpp:8-12).  Lines are stored row-major,
  *    lines x n doubles, in device memory owned by the caller.
+ *    Any lines >= 0 (0 is a no-op; batches above 65535 lines are folded over two
+ *    grid dimensions inside the kernels) and any n >= 1 (n_space = 1 is legal in the
+ *    reference, proj/src/scheme.cpp:40); the fast and relaxed engines take n <= 2^29.
  *  - The kernel window of line l is ktab[l*ktab_stride + w], w = 0..2n, the
  *    table build_kernel produces (proj/src/scheme.cpp:77-81), with grid
  *    displacement d = first[l] + w (first = center_index - n).
