@@ -420,7 +420,9 @@ int lob_decompose_f64(lob_ctx* ctx, const double* u, int64_t m, double eta, int*
 /* conv_fast (proj/src/minplus.cpp:190-252) of a convex kernel (nk device samples) with a plain
  * sequence (nu device samples): out[nk + nu - 1] (device), *blocks (host) = the block count
  * (capped for eta > 0).  For eta > 0 the reference's relaxed approximation, bit for bit.
- * Synchronous (min_pointwise's gap check -> LOB_INVALID_INPUT). */
+ * nk, nu >= 1 (a one-sample side gives the plain sums, as in the reference).  A kernel whose
+ * slope drops is rejected like require_convex (proj/src/minplus.cpp:24-29): LOB_INVALID_INPUT
+ * naming the first such segment.  Synchronous (min_pointwise's gap check -> LOB_INVALID_INPUT). */
 int lob_conv_fast_f64(lob_ctx* ctx, const double* kern, int64_t nk, const double* u, int64_t nu, double eta,
                       double* out, int64_t* blocks, void* stream);
 

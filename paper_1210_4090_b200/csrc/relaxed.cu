@@ -278,6 +278,16 @@ __global__ void conv_naive_kernel(const double* __restrict__ f, int64_t nf, cons
     }
 }
 
+// is_convex (proj/src/grid_fn.cpp:44-54): the first segment whose slope drops, exact comparison
+// of the two rounded differences; *bad = the smallest such index (LLONG_MAX when convex)
+__global__ void convex_check_kernel(const double* __restrict__ f, int64_t nf, unsigned long long* __restrict__ bad) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i + 2 < nf;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double lo = __dsub_rn(f[i + 1], f[i]), hi = __dsub_rn(f[i + 2], f[i + 1]);
+        if (hi < lo) atomicMin(bad, static_cast<unsigned long long>(i));
+    }
+}
+
 }  // namespace
 
 size_t relaxed_workspace_bytes(int64_t lines, int64_t n) { return relaxed_layout(nullptr, lines, n).total; }
@@ -385,10 +395,55 @@ extern "C" int lob_conv_fast_f64(lob_ctx* ctx, const double* kern, int64_t nk, c
                                  double* out, int64_t* blocks, void* stream) {
     if (!ctx) return LOB_INVALID_INPUT;
     if (!(eta >= 0.0)) return set_error(ctx, LOB_INVALID_INPUT, "decompose: eta must be >= 0");
-    if (nk < 2 || nu < 2 || !kern || !u || !out)
-        return set_error(ctx, LOB_INVALID_INPUT, "conv_fast: need at least two samples on each side");
+    if (nk < 1 || nu < 1 || !kern || !u || !out) return set_error(ctx, LOB_INVALID_INPUT, "conv_fast: empty input");
     if (nk + nu > (1ll << 30)) return set_error(ctx, LOB_INVALID_INPUT, "conv_fast: too long");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (nk >= 3) {
+        // require_convex(kernel) of conv_fast(kernel, u, eta) (proj/src/minplus.cpp:24-29,190-194)
+        unsigned long long* dbad = nullptr;
+        unsigned long long hbad = ~0ull;
+        LOB_CUDA_TRY(ctx, cudaMallocAsync(&dbad, sizeof(hbad), s));
+        LOB_CUDA_TRY(ctx, cudaMemsetAsync(dbad, 0xff, sizeof(hbad), s));
+        convex_check_kernel<<<static_cast<unsigned>(std::min<int64_t>((nk + 255) / 256, 148 * 8)), 256, 0, s>>>(kern, nk,
+                                                                                                             dbad);
+        ctx->launches += 1;
+        LOB_CUDA_TRY(ctx, cudaGetLastError());
+        LOB_CUDA_TRY(ctx, cudaMemcpyAsync(&hbad, dbad, sizeof(hbad), cudaMemcpyDeviceToHost, s));
+        cudaFreeAsync(dbad, s);
+        LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+        if (hbad != ~0ull)
+            return set_error(ctx, LOB_INVALID_INPUT,
+                             "conv_fast: kernel is not convex, slope drops at segment " + std::to_string(hbad + 1));
+    }
+    if (nk == 1 || nu == 1) {
+        // a one-sample side has no slopes: every block's merge / envelope walk degenerates to the
+        // plain sums f[i] + g[j] (proj/src/minplus.cpp:40-57,62-105 with an empty slope list), the
+        // reference's own exhaustive test includes these (proj/tests/unit_minplus.cpp:436-437);
+        // the block count is decompose(u, eta)'s (one Convex block for a single sample, :157-160)
+        int st = lob_minplus_conv_naive_f64(ctx, kern, nk, u, nu, out, stream);
+        if (st) return st;
+        int64_t hb = 1;
+        if (nu >= 2) {
+            const int64_t m = nu - 1;
+            int2* pieces = nullptr;
+            int* np = nullptr;
+            int64_t* db = nullptr;
+            LOB_CUDA_TRY(ctx, cudaMallocAsync(&pieces, static_cast<size_t>(m) * sizeof(int2), s));
+            LOB_CUDA_TRY(ctx, cudaMallocAsync(&np, 2 * sizeof(int), s));
+            LOB_CUDA_TRY(ctx, cudaMallocAsync(&db, sizeof(int64_t), s));
+            LOB_CUDA_TRY(ctx, cudaMemsetAsync(np + 1, 0, sizeof(int), s));
+            relaxed_decompose_kernel<<<1, 1, 0, s>>>(u, 1, m, eta, pieces, np, db, np + 1, 0, kCap);
+            ctx->launches += 1;
+            LOB_CUDA_TRY(ctx, cudaGetLastError());
+            LOB_CUDA_TRY(ctx, cudaMemcpyAsync(&hb, db, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+            cudaFreeAsync(pieces, s);
+            cudaFreeAsync(np, s);
+            cudaFreeAsync(db, s);
+        }
+        LOB_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+        if (blocks) *blocks = hb;
+        return LOB_OK;
+    }
     const int64_t m = nu - 1, nf = nk - 1, len = nf + m + 1;
     unsigned long long* conv = nullptr;
     int2* pieces = nullptr;
@@ -401,7 +456,6 @@ extern "C" int lob_conv_fast_f64(lob_ctx* ctx, const double* kern, int64_t nk, c
     flag = np + 1;
     LOB_CUDA_TRY(ctx, cudaMemsetAsync(conv, 0xff, static_cast<size_t>(len) * 8, s));
     LOB_CUDA_TRY(ctx, cudaMemsetAsync(flag, 0, sizeof(int), s));
-    // kernel convexity is the caller's contract (proj/src/minplus.cpp:190-194 require_convex)
     relaxed_decompose_kernel<<<1, 1, 0, s>>>(u, 1, m, eta, pieces, np, db, flag, 0, kCap);
     const unsigned gx = static_cast<unsigned>(std::min<int64_t>(m, std::max<int64_t>(1, 2 * ctx->sm_count)));
     relaxed_scatter_kernel<<<dim3(gx, 1), kNTs, 0, s>>>(u, m, kern, 0, pieces, np, conv, 0, nf);
