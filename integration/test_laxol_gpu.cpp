@@ -280,6 +280,85 @@ int main() {
             }
         }
     }
+    // 5b. evolve's trace semantics on the reference's own test shapes (proj/tests/unit_scheme.cpp:
+    // 283-296 windowed convex flow, 323-333 blow-up abort, 381-393 snapshot thinning) and a long
+    // thinned run: the whole EvolutionTrace == the reference's
+    {
+        auto same_trace = [&](const laxol::EvolutionTrace& got, const laxol::EvolutionTrace& want) {
+            bool ok = got.completed == want.completed && got.abort_reason == want.abort_reason &&
+                      got.snapshots.size() == want.snapshots.size() && got.per_step.size() == want.per_step.size() &&
+                      got.times == want.times && got.snapshot_steps == want.snapshot_steps;
+            for (std::size_t i = 0; ok && i < want.snapshots.size(); ++i) ok = same(got.snapshots[i], want.snapshots[i]);
+            for (std::size_t i = 0; ok && i < want.per_step.size(); ++i)
+                ok = got.per_step[i].drift == want.per_step[i].drift && got.per_step[i].blocks == want.per_step[i].blocks &&
+                     got.per_step[i].time == want.per_step[i].time;
+            return ok;
+        };
+        laxol::EvolveOptions naive;
+        naive.engine = laxol::ConvEngine::Naive;
+        {  // values blow up: a partial trace, completed == false, the same abort reason and last snapshot
+            const laxol::SchemeParams p = params_of(16, 0.25);
+            const laxol::Potential pot =
+                laxol::potential_custom([](double t, double) { return t < 0.9 ? 0.0 : 1e308; }, 1e308, true);
+            const laxol::HamiltonianSpec spec{laxol::mechanical(0.0), pot, true, false};
+            const laxol::GridFn u = laxol::make_periodic(std::vector<double>(16, 0.0), p.epsilon());
+            const laxol::EvolutionTrace want = laxol::evolve(u, 0.0, 12, spec, p, naive);
+            for (Engine e : {Engine::GpuFast, Engine::GpuDirect}) {
+                const laxol::EvolutionTrace got = dev.evolve(u, 0.0, 12, spec, p, e, {});
+                report(std::string("evolve blow-up abort ") + (e == Engine::GpuFast ? "GpuFast" : "GpuDirect"),
+                       !want.completed && !got.abort_reason.empty() && same_trace(got, want));
+            }
+        }
+        {  // snapshot thinning keeps the endpoints and the requested captures
+            const laxol::SchemeParams p = params_of(8, 0.5);
+            const laxol::HamiltonianSpec spec = laxol::make_spec(laxol::mechanical(0.0), laxol::potential_zero(), true, true);
+            const laxol::GridFn u = laxol::make_periodic(std::vector<double>(8, 0.0), p.epsilon());
+            laxol::EvolveOptions o = naive;
+            o.snapshot_stride = 1000;
+            o.capture_steps = {3};
+            const laxol::EvolutionTrace want = laxol::evolve(u, 0.0, 7, spec, p, o);
+            const laxol::EvolutionTrace got = dev.evolve(u, 0.0, 7, spec, p, Engine::GpuFast, o);
+            report("evolve snapshot thinning (stride 1000, capture {3})",
+                   got.snapshot_steps == std::vector<std::int64_t>{0, 3, 7} && same_trace(got, want));
+        }
+        {  // more than 1024 steps: the automatic stride, a time-dependent potential, an unsorted capture list
+            const int n = 96;
+            const laxol::SchemeParams p = params_of(n, 0.05);
+            const laxol::HamiltonianSpec spec = laxol::make_spec(
+                laxol::mechanical(-0.35),
+                laxol::potential_custom([&](double t, double x) { return std::cos(kTwoPi * x) * (1.0 + 0.25 * std::sin(kTwoPi * t)); },
+                                        1.25, true),
+                true, false);
+            std::vector<double> u0(n);
+            for (int j = 0; j < n; ++j) u0[j] = 0.3 * std::sin(2.0 * kTwoPi * j / n);
+            const laxol::GridFn u = laxol::make_periodic(u0, p.epsilon());
+            laxol::EvolveOptions o = naive;
+            o.capture_steps = {1501, 7, 1024};
+            const laxol::EvolutionTrace want = laxol::evolve(u, 0.5, 2500, spec, p, o);
+            for (Engine e : {Engine::GpuFast, Engine::GpuDirect}) {
+                const laxol::EvolutionTrace got = dev.evolve(u, 0.5, 2500, spec, p, e, o);
+                report(std::string("evolve 2500 thinned steps, time-dependent V ") +
+                           (e == Engine::GpuFast ? "GpuFast" : "GpuDirect"),
+                       want.snapshots.size() < 1100 && same_trace(got, want));
+            }
+        }
+        {  // windowed (wall) domain: the kinetic-only flow of convex data, 20 steps
+            const laxol::SchemeParams p = params_of(32, 0.125);
+            const laxol::HamiltonianSpec spec = laxol::make_spec(laxol::mechanical(0.0), laxol::potential_zero(), true, true);
+            std::vector<double> v(65);
+            for (int i = 0; i < 65; ++i) {
+                const double x = -1.0 + static_cast<double>(i) * p.epsilon();
+                v[i] = x * x + 0.25 * std::fabs(x - 0.3);
+            }
+            const laxol::GridFn u = laxol::make_grid_fn(v, p.epsilon(), -1.0);
+            const laxol::EvolutionTrace want = laxol::evolve(u, 0.0, 20, spec, p, naive);
+            for (Engine e : {Engine::GpuFast, Engine::GpuDirect}) {
+                const laxol::EvolutionTrace got = dev.evolve(u, 0.0, 20, spec, p, e, {});
+                report(std::string("evolve windowed convex flow ") + (e == Engine::GpuFast ? "GpuFast" : "GpuDirect"),
+                       same_trace(got, want));
+            }
+        }
+    }
     // 6. the reference's argument errors surface as its own exception types
     {
         const laxol::SchemeParams p = params_of(64, 0.05);
