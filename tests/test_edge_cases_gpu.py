@@ -244,3 +244,32 @@ def test_host_step_with_fewer_lines_than_pipeline_chunks(dev, orc, lines, engine
     want = orc.direct(u, K, first, tv=tau * v, ktab_stride=2 * n + 1)
     assert np.array_equal(got, want)
     assert list(blocks) == [orc.line_blocks(u[l]) for l in range(lines)]
+
+
+@pytest.mark.parametrize("n,tau", [(64, 1.0 / (64 * 0.999)), (1000, 1.0 / (1000 * 0.97)), (64, 100.0), (512, 1e4),
+                                   (4096, 1.0 / (4096 * 0.999))])
+def test_time_steps_at_both_ends_of_the_anti_cfl_range(dev, ref, n, tau):
+    """epsilon/tau just below the bound h0 = 1 (a window two samples wide in velocity) and a huge
+    tau (a window so flat that its edges can hold minimisers: K2's gate sends those tiles to the
+    direct formula): every engine == the reference's step."""
+    lines = 3
+    rng = np.random.default_rng(n)
+    u = np.cumsum(rng.uniform(-1.0 / n, 1.0 / n, (lines, n)), axis=1) + 0.1 * np.sin(2 * np.pi * np.arange(n) / n)
+    drifts = np.array([0.0, 0.37, -1.2])
+    want, wb = ref.step_lines(u, tau, drifts, engine=1, nthreads=3)
+    for name, got in all_engines(dev, u, drifts, tau).items():
+        assert np.array_equal(got, want), name
+
+
+@pytest.mark.parametrize("scale", [1e300, 1e150, 1e-290, 1e-310])
+def test_extreme_magnitudes_through_every_engine(dev, ref, scale):
+    """Lines scaled to the ends of the double range (overflowing fp32 screens and slope inversions,
+    subnormal samples): every engine == the reference's step, infinities and all."""
+    n, tau, lines = 1024, 0.05, 3
+    rng = np.random.default_rng(7)
+    u = (np.cumsum(rng.uniform(-1.0 / n, 1.0 / n, (lines, n)), axis=1) +
+         np.sin(2 * np.pi * np.arange(n) / n)[None, :]) * scale
+    drifts = np.array([0.5, -0.3, 1.1])
+    want, _ = ref.step_lines(u, tau, drifts, engine=1, nthreads=3)
+    for name, got in all_engines(dev, u, drifts, tau).items():
+        assert np.array_equal(got, want), name
