@@ -273,3 +273,61 @@ def test_extreme_magnitudes_through_every_engine(dev, ref, scale):
     want, _ = ref.step_lines(u, tau, drifts, engine=1, nthreads=3)
     for name, got in all_engines(dev, u, drifts, tau).items():
         assert np.array_equal(got, want), name
+
+
+def test_contexts_on_concurrent_host_threads(dev):
+    """One context per host thread (SURVEY 8b threading): four threads, each with its own context
+    and stream, step different batches at once (K2 tiled with block counts, K2L, K1, the relaxed
+    engine); every result == the same work done alone on the session's context."""
+    import threading
+
+    import torch
+    n_long, n_short, tau, steps = 8192, 512, 0.02, 12
+
+    def work(d, seed, stream):
+        rng = np.random.default_rng(seed)
+        res = {}
+        for name, n in (("long", n_long), ("short", n_short)):
+            lines = 6
+            u = np.cumsum(rng.uniform(-1.0 / n, 1.0 / n, (lines, n)), axis=1) + np.sin(2 * np.pi * np.arange(n) / n)
+            dr = rng.uniform(-1.5, 1.5, lines)
+            with torch.cuda.stream(stream):
+                a, b = to_dev(u), torch.empty((lines, n), dtype=torch.float64, device="cuda")
+                dd = to_dev(dr)
+                ws = torch.empty(d.fast_workspace_bytes(lines, n), dtype=torch.uint8, device="cuda")
+                bl = torch.empty(lines, dtype=torch.int64, device="cuda")
+                for i in range(steps):
+                    d.fast_f64(a, b, dd, tau, blocks=bl, workspace=ws, flags=api.FAST_STATS_VALID if i else 0,
+                               stream=stream)
+                    a, b = b, a
+                kt, fr = windows(d, n, tau, dr)
+                o1, o2 = torch.empty_like(a), torch.empty_like(a)
+                d.direct_f64(a, o1, kt, fr, ktab_stride=2 * n + 1, stream=stream)
+                d.relaxed_f64(a, o2, kt, fr, 1e-6, ktab_stride=2 * n + 1, stream=stream)
+                stream.synchronize()
+                res[name] = (a.cpu().numpy(), bl.cpu().numpy(), o1.cpu().numpy(), o2.cpu().numpy())
+        return res
+
+    alone = [work(dev, 100 + t, torch.cuda.current_stream()) for t in range(4)]
+    got, errs = [None] * 4, []
+
+    def run(t):
+        try:
+            d = api.Device(0)
+            try:
+                got[t] = work(d, 100 + t, torch.cuda.Stream())
+            finally:
+                d.close()
+        except Exception as exc:  # surfaced below
+            errs.append(exc)
+
+    threads = [threading.Thread(target=run, args=(t,)) for t in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errs, errs
+    for t in range(4):
+        for name in ("long", "short"):
+            for x, y in zip(got[t][name], alone[t][name]):
+                assert np.array_equal(x, y), (t, name)
