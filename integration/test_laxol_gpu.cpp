@@ -342,6 +342,22 @@ int main() {
                        want.snapshots.size() < 1100 && same_trace(got, want));
             }
         }
+        {  // eta > 0: the reference's relaxed Fast engine step after step (its approximation errors
+           // compound; the device reproduces every one), block counts capped as the reference reports
+            const int n = 600;
+            laxol::SchemeParams p = params_of(n, 0.04);
+            p.eta = 1e-6;
+            const laxol::HamiltonianSpec spec =
+                laxol::make_spec(laxol::mechanical(1.0), laxol::potential_cosine(1.0, -1.0, 1), true, true);
+            std::vector<double> v(n);
+            for (int i = 0; i < n; ++i) v[i] = std::cos(2.0 * kTwoPi * (static_cast<double>(i) * p.epsilon()));
+            const laxol::GridFn u = laxol::make_periodic(v, p.epsilon());
+            laxol::EvolveOptions fast;
+            fast.engine = laxol::ConvEngine::Fast;
+            const laxol::EvolutionTrace want = laxol::evolve(u, 0.0, 60, spec, p, fast);
+            const laxol::EvolutionTrace got = dev.evolve(u, 0.0, 60, spec, p, Engine::GpuFast, {});
+            report("evolve 60 steps, eta 1e-6 (relaxed Fast engine)", same_trace(got, want));
+        }
         {  // windowed (wall) domain: the kinetic-only flow of convex data, 20 steps
             const laxol::SchemeParams p = params_of(32, 0.125);
             const laxol::HamiltonianSpec spec = laxol::make_spec(laxol::mechanical(0.0), laxol::potential_zero(), true, true);
