@@ -2075,8 +2075,9 @@ __global__ void __launch_bounds__(kRT) resident_kernel(double* __restrict__ u, i
                 const double sr = __dsub_rn(cur[y + 1 == n ? 0 : y + 1], u0);
                 const int dl = max(__double2int_ru(__fma_rn(sl, ia, hl)), dmin_w);
                 const int dr = min(__double2int_rd(__fma_rn(sr, ia, hr)), dmax_w);
-                int j = (y + dl) % n;
-                if (j < 0) j += n;
+                int j = y + dl;  // wrapped by add / subtract (|dl| < 2n + |centre|: a few passes at most)
+                while (j < 0) j += n;
+                while (j >= n) j -= n;
                 for (int d = dl; d <= dr; ++d) {
                     smem_fmin(&keys[j], __dadd_rn(u0, Kd[d]));
                     j = j + 1 == n ? 0 : j + 1;
