@@ -1652,6 +1652,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
     constexpr int kUbLen = kC + 8;
     const int H0 = (kUbLen - n) / 2;
     double* Ub = S.ubuf + H0;
+    bool line_bulk = false;
     auto init_keys = [&]() {
         ulonglong2* k2 = reinterpret_cast<ulonglong2*>(S.keys);
         for (int i = tid; i < (kT + 4) / 2; i += kNT) k2[i] = make_ulonglong2(kInfBits, kInfBits);
@@ -1702,8 +1703,23 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
         }
         init_keys();
     } else {
-        init_keys();
-        for (int j = tid; j < n; j += kNT) Ub[j] = ul[j * is];
+        // a row of even length on a 16-byte boundary: one TMA bulk copy (cp.async.bulk) issued by
+        // thread 0 while every thread initialises the keys; else 8-byte loads through registers
+        if constexpr (LD == kLdRow)
+            line_bulk = n >= 256 && (n & 1) == 0 && (H0 & 1) == 0 && (reinterpret_cast<uintptr_t>(ul) & 15u) == 0;
+        if (line_bulk) {
+            if (tid == 0) {
+                mbar_init(&S.mbar, 1);
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+                fence_proxy_async();
+                mbar_expect_tx(&S.mbar, static_cast<unsigned>(n) * 8u);
+                tma_load_1d(Ub, ul, static_cast<unsigned>(n) * 8u, &S.mbar);
+            }
+            init_keys();
+        } else {
+            init_keys();
+            for (int j = tid; j < n; j += kNT) Ub[j] = ul[j * is];
+        }
     }
     double* U = Ub;
     if (warp == 0) {
@@ -1714,6 +1730,10 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
             L.gap = c.gap;
             L.drift = c.drift;
             L.first = c.first;
+        }
+        if (line_bulk) {
+            __syncwarp();  // thread 0 initialised the barrier
+            mbar_wait(&S.mbar, 0);
         }
     }
     __syncthreads();
