@@ -68,7 +68,11 @@ inline dim3 line_grid(unsigned gx, int64_t lines) {
                 static_cast<unsigned>((lines + kGridY - 1) / kGridY));
 }
 __device__ __forceinline__ int64_t grid_line() {
-    return static_cast<int64_t>(blockIdx.y) + static_cast<int64_t>(kGridY) * blockIdx.z;
+    // 32-bit (line counts stay below 2^31), and opaque: the compiler would otherwise re-derive
+    // the index from the two special registers at every use
+    unsigned l = blockIdx.y + kGridY * blockIdx.z;
+    asm volatile("" : "+r"(l));
+    return static_cast<int64_t>(l);
 }
 #endif
 
