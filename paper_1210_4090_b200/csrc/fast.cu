@@ -1734,8 +1734,10 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
         if (line_bulk) {
             __syncwarp();  // thread 0 initialised the barrier
             mbar_wait(&S.mbar, 0);
+            if (lane == 0) Ub[n] = Ub[0];  // the seam sample, for the slope of the last segment
         }
     }
+    if (!line_bulk && tid == 0) Ub[n] = Ub[0];  // (thread 0 staged U(0) itself, or a cluster barrier ordered it)
     __syncthreads();
     // enclosures of u and of its slopes s(j) = U(j+1) - U(j) (periodic): coarse order-preserving
     // keys (within 2^-20 relative, tile_stats' keys) reduced with REDUX
@@ -1744,7 +1746,7 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
 #pragma unroll 4
         for (int j = tid; j < n; j += kNT) {
             const double uj = U[j];
-            const unsigned ks = hkey(__dsub_rn(U[j + 1 < n ? j + 1 : 0], uj)), ku = hkey(uj);
+            const unsigned ks = hkey(__dsub_rn(U[j + 1], uj)), ku = hkey(uj);
             kmn = min(kmn, ks);
             kmx = max(kmx, ks);
             hmn = min(hmn, ku);
@@ -1909,7 +1911,9 @@ __global__ void __launch_bounds__(kNT, LOB_FAST_MINB) line_kernel(const double* 
                 const double o = KIND == 0 ? best : __dsub_rn(best, tvof(t[m]));
                 if constexpr (ST == kStClu) ostage[j] = o;
                 else ol[j * os] = o;
-                miss |= static_cast<unsigned>(kk == kInfBits) << m;
+                // (high word only: a slot holding a genuine +inf or NaN sum is rescanned to the same value)
+                miss |= static_cast<unsigned>(static_cast<unsigned>(kk >> 32) >= 0x7ff00000u &&
+                                              static_cast<int>(kk >> 32) >= 0) << m;
             }
         }
         while (miss) {  // cold: the direct formula over the whole window
