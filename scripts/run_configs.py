@@ -202,6 +202,8 @@ def c4(dev, steps=500):
         # two workspace halves: the fused four-launch step (transpose + statistics, sweep, x2)
         ws = torch.empty(halves * dev.fast_workspace_bytes(n, n), dtype=torch.uint8, device="cuda")
         bs = [api.c4_time_term(i * tau + tau) for i in range(steps)]
+        # one untimed step on a scratch state: module loading and one-time engine setup stay out of the timing
+        dev.split_step_2d(u.clone(), o, tmp, tau, 0.3, -0.7, a1=a, a2=a, b=bs[0], engine=eng, workspace=ws)
         with Timer() as t:
             for i in range(steps):
                 dev.split_step_2d(u, o, tmp, tau, 0.3, -0.7, a1=a, a2=a, b=bs[i], engine=eng, workspace=ws)
