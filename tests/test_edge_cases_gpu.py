@@ -331,3 +331,32 @@ def test_contexts_on_concurrent_host_threads(dev):
         for name in ("long", "short"):
             for x, y in zip(got[t][name], alone[t][name]):
                 assert np.array_equal(x, y), (t, name)
+
+
+@pytest.mark.parametrize("n", [256, 258, 260, 1000, 1002, 2044, 2046, 2048])
+@pytest.mark.parametrize("offset", [0, 1])
+def test_whole_line_kernel_bulk_and_register_loads(dev, orc, n, offset):
+    """K2L loads a row by one TMA bulk copy when the row is even, 16-byte aligned and lands on an
+    even shared-memory offset (n = 0 mod 4), else through registers: both paths, rows shifted by
+    one sample off the 16-byte grid, lengths around the limits == the oracle."""
+    import torch
+    tau, lines = 0.02, 5
+    rng = np.random.default_rng(n + offset)
+    u = np.cumsum(rng.uniform(-1.0 / n, 1.0 / n, (lines, n)), axis=1) + 0.3 * np.sin(2 * np.pi * np.arange(n) / n)
+    drifts = np.array([-1.1, -0.2, 0.0, 0.6, 1.7])
+    buf = torch.zeros(lines * n + offset, dtype=torch.float64, device="cuda")
+    du = buf[offset:].view(lines, n)
+    du.copy_(to_dev(u))
+    obuf = torch.zeros(lines * n + offset, dtype=torch.float64, device="cuda")
+    out = obuf[offset:].view(lines, n)
+    ws = torch.empty(dev.fast_workspace_bytes(lines, n), dtype=torch.uint8, device="cuda")
+    v = np.cos(2 * np.pi * np.arange(n) / n)
+    dev.fast_f64(du, out, to_dev(drifts), tau, tv=to_dev(tau * v), workspace=ws)
+    torch.cuda.synchronize()
+    ks = [orc.kernel(n, tau, float(d)) for d in drifts]
+    K = np.ascontiguousarray(np.stack([k[0] for k in ks]))
+    first = np.array([k[1] for k in ks], np.int64)
+    want = orc.direct(u, K, first, tv=tau * v, ktab_stride=2 * n + 1)
+    assert np.array_equal(out.cpu().numpy(), want)
+    c = dev.fast_counters(ws, lines, n)
+    assert c["missed_outputs"] == 0, c
