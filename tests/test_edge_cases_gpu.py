@@ -360,3 +360,40 @@ def test_whole_line_kernel_bulk_and_register_loads(dev, orc, n, offset):
     assert np.array_equal(out.cpu().numpy(), want)
     c = dev.fast_counters(ws, lines, n)
     assert c["missed_outputs"] == 0, c
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_seeded_differential_sweep_of_engines(dev, orc, seed):
+    """Seeded random shapes (length 1..3000, time step anywhere in the anti-CFL range, drifts up to
+    |tau P| ~ 2.5, smooth / rough / piecewise-constant / kinked / spiky lines, a random potential):
+    12 seeds x 8 cases, every engine (K1 screened and plain, K2 whole-line or tiled, the window-table
+    K2, the relaxed engine at eta = 0) == the oracle's direct formula."""
+    rng = np.random.default_rng(9000 + seed)
+    for case in range(8):
+        n = int(rng.choice([rng.integers(1, 40), rng.integers(40, 600), rng.integers(600, 3000)]))
+        ratio = float(rng.uniform(0.02, 0.98))  # epsilon / tau
+        tau = 1.0 / (n * ratio)
+        lines = int(rng.integers(1, 6))
+        x = np.arange(n) / n
+        kind = int(rng.integers(0, 5))
+        if kind == 0:
+            u = np.sin(2 * np.pi * rng.integers(1, 5) * x)[None, :] * rng.uniform(0.1, 3.0, (lines, 1))
+        elif kind == 1:
+            u = np.cumsum(rng.uniform(-1, 1, (lines, n)), axis=1) / max(n, 1) ** 0.5
+        elif kind == 2:
+            u = np.floor(rng.uniform(0, 6, (lines, 1)) * x[None, :] * 4) * 0.25  # plateaus and jumps
+        elif kind == 3:
+            u = np.abs(x[None, :] - rng.uniform(0.2, 0.8, (lines, 1))) * rng.uniform(-3, 3, (lines, 1))  # kinks
+        else:
+            u = np.zeros((lines, n))
+            u[np.arange(lines), rng.integers(0, n, lines)] = rng.uniform(-5, 5, lines)  # spikes
+        u = np.ascontiguousarray(u + rng.uniform(-1e-9, 1e-9, (lines, n)) * (rng.random() < 0.5))
+        drifts = rng.uniform(-2.5, 2.5, lines) / max(tau, 1e-300)
+        drifts = np.clip(drifts, -50.0, 50.0)
+        v = rng.uniform(-1, 1, n)
+        ks = [orc.kernel(n, tau, float(d)) for d in drifts]
+        K = np.ascontiguousarray(np.stack([k[0] for k in ks]))
+        first = np.array([k[1] for k in ks], np.int64)
+        want = orc.direct(u, K, first, tv=tau * v, ktab_stride=2 * n + 1)
+        for name, got in all_engines(dev, u, drifts, tau, tv=tau * v).items():
+            assert np.array_equal(got, want), (seed, case, name, n, tau, kind)
