@@ -576,8 +576,13 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 
 constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;  // +inf
 
-// x in (-3n, 3n) -> x mod n in [0, n)
+// x mod n in [0, n): selects for x in (-3n, 3n), the general remainder beyond (a window whose centre
+// lies more than two periods away: |tau P| > 2 in window-table mode; once per chunk, never per source)
 __device__ __forceinline__ int wrap_idx(int x, int n) {
+    if (x <= -3 * n || x >= 3 * n) {
+        x %= n;
+        return x < 0 ? x + n : x;
+    }
     x += x < 0 ? n : 0;
     x += x < 0 ? n : 0;
     x += x < 0 ? n : 0;

@@ -397,3 +397,25 @@ def test_seeded_differential_sweep_of_engines(dev, orc, seed):
         want = orc.direct(u, K, first, tv=tau * v, ktab_stride=2 * n + 1)
         for name, got in all_engines(dev, u, drifts, tau, tv=tau * v).items():
             assert np.array_equal(got, want), (seed, case, name, n, tau, kind)
+
+
+@pytest.mark.parametrize("n", [21, 64, 1024, 4096])
+@pytest.mark.parametrize("tp", [2.5, 3.2, -4.5])
+def test_window_centres_several_periods_away(dev, orc, n, tp):
+    """|tau P| > 2: the window's centre lies more than two periods from the output, so the sources of
+    the window-table K2 wrap three and more periods back (found by scripts/fuzz_engines.py: the
+    wrap helper handled (-3n, 3n) only).  Smooth, spiky and rough lines, every engine == the oracle."""
+    tau, lines = 4.0 / n, 3
+    rng = np.random.default_rng(n)
+    x = np.arange(n) / n
+    u = np.stack([np.sin(2 * np.pi * x) * 0.7,
+                  np.where(np.arange(n) == n // 3, 4.0, 0.0) + 1e-3 * x,
+                  np.cumsum(rng.uniform(-1, 1, n)) / n ** 0.5])
+    drifts = np.full(lines, tp / tau)
+    v = rng.uniform(-1, 1, n)
+    ks = [orc.kernel(n, tau, float(d)) for d in drifts]
+    K = np.ascontiguousarray(np.stack([k[0] for k in ks]))
+    first = np.array([k[1] for k in ks], np.int64)
+    want = orc.direct(u, K, first, tv=tau * v, ktab_stride=2 * n + 1)
+    for name, got in all_engines(dev, u, drifts, tau, tv=tau * v).items():
+        assert np.array_equal(got, want), name
