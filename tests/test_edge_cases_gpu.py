@@ -419,3 +419,17 @@ def test_window_centres_several_periods_away(dev, orc, n, tp):
     want = orc.direct(u, K, first, tv=tau * v, ktab_stride=2 * n + 1)
     for name, got in all_engines(dev, u, drifts, tau, tv=tau * v).items():
         assert np.array_equal(got, want), name
+
+
+def test_seeded_differential_sweep_of_paths():
+    """scripts/fuzz_paths.py, 24 seeds: evolve (resident and launch loop, both engines: states, block
+    counts, drifts), the host step (every engine, eta 0 / 1e-7 / 1e-4) and the 2-D split step (direct
+    and four fast layouts) on random sizes, time steps and drifts up to |tau P| = 4 == the reference."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "fuzz_paths.py"), "24"], cwd=root,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "failures: 0" in r.stdout and "checks: 288" in r.stdout, r.stdout[-2000:]
