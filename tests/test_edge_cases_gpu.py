@@ -433,3 +433,17 @@ def test_seeded_differential_sweep_of_paths():
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "failures: 0" in r.stdout and "checks: 288" in r.stdout, r.stdout[-2000:]
+
+
+def test_seeded_sweep_of_random_convex_windows():
+    """scripts/fuzz_windows.py, 30 seeds: the window-table K2 on random convex tables (sorted random
+    slopes, a few distinct slopes with exact ties, quadratics centred in or outside the window, one
+    kink; any first displacement) over random lines, three carried steps each == the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "fuzz_windows.py"), "30"], cwd=root,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "failures: 0" in r.stdout and "checks: 90" in r.stdout, r.stdout[-2000:]
