@@ -447,3 +447,17 @@ def test_seeded_sweep_of_random_convex_windows():
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "failures: 0" in r.stdout and "checks: 90" in r.stdout, r.stdout[-2000:]
+
+
+def test_seeded_sweep_of_nd_split_and_tropical_gemm():
+    """scripts/fuzz_nd.py, 20 seeds: split_step_nd on periodic tensors of rank 1-3 (every engine, the
+    relaxed one with eta > 0, drifts up to |tau P| = 3) and on windowed tensors of ragged shapes
+    (status and values), and the tropical GEMM with +inf entries == the reference."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "fuzz_nd.py"), "20"], cwd=root,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "failures: 0" in r.stdout and "checks: 120" in r.stdout, r.stdout[-2000:]
