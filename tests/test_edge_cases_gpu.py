@@ -461,3 +461,17 @@ def test_seeded_sweep_of_nd_split_and_tropical_gemm():
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "failures: 0" in r.stdout and "checks: 120" in r.stdout, r.stdout[-2000:]
+
+
+def test_seeded_sweep_of_long_lines_with_carried_statistics():
+    """scripts/fuzz_long.py, 12 seeds: the tiled K2 on lines of 4096 .. 65536 samples (odd sizes too)
+    mixing smooth modes, shocks, plateaus and noise, six consecutive steps on carried statistics
+    (chained on alternate seeds), values and block counts == K1 at every step."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "fuzz_long.py"), "12"], cwd=root,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "failures: 0" in r.stdout and "checks: 72" in r.stdout, r.stdout[-2000:]
